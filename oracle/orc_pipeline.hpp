@@ -1,0 +1,347 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (see orc_core.hpp header).
+//
+// BUILDER-DEFINED (no reference): the lifted tracker
+// and the CSFD frame-derivative driver.  The reference's track_frame
+// (icp.cpp:169-244) is double-only; this lifts its kLinearized solver to the
+// packed scalar S = Lifted<D>:
+//   - preprocessing (bilateral, pyramid) and every gate read real parts only;
+//   - measured vertices/normals, the raycast prediction, J, r, the 6x6 normal
+//     equations and their LDLT solve carry all D channels;
+//   - the normal equations use the canonical slot-tiled reduction order.
+// The driver seeds D directions (first-frame twist components and/or the
+// four intrinsics), fuses frame 0 at exp(xi0*) * T0_gt, then tracks and fuses
+// frames 1..N-1, and differentiates an objective of the lifted trajectory.
+#pragma once
+
+#include "orc_icp.hpp"
+#include "orc_synth.hpp"
+
+namespace orc {
+
+template <typename S>
+struct LiftedTrackResult {
+  PoseT<S> pose;
+  int iterations = 0;
+  bool converged = false;
+  int correspondences = 0;
+};
+
+template <typename S>
+SurfaceMaps<double> real_maps(const SurfaceMaps<S>& m) {
+  SurfaceMaps<double> o;
+  o.vertices = Image<Vec3d>(m.vertices.width, m.vertices.height, Vec3d());
+  o.normals = Image<Vec3d>(m.normals.width, m.normals.height, Vec3d());
+  for (std::size_t i = 0; i < m.vertices.data.size(); ++i)
+    for (int c = 0; c < 3; ++c) {
+      o.vertices.data[i][c] = real_part(m.vertices.data[i][c]);
+      o.normals.data[i][c] = real_part(m.normals.data[i][c]);
+    }
+  return o;
+}
+
+// Canonical slot-tiled normal equations over the strided slot grid.
+template <typename S>
+NormalEq<S> tiled_normal_equations(const std::vector<CorrIndex>& idx, int width, int height, int stride,
+                                   const SurfaceMaps<S>& measured, const SurfaceMaps<S>& predicted,
+                                   const PoseT<S>& base) {
+  const int nxs = (width + stride - 1) / stride;
+  const int nys = (height + stride - 1) / stride;
+  const int n_slots = nxs * nys;
+  const int n_tiles = (n_slots + kTile - 1) / kTile;
+  std::vector<NormalEq<S>> partial(n_tiles);
+  for (const CorrIndex& c : idx) {
+    const int slot = (c.y / stride) * nxs + c.x / stride;
+    S j[6], r;
+    jacobian_row<S>(measured.vertices.at(c.x, c.y), predicted.vertices.at(c.u, c.v), predicted.normals.at(c.u, c.v),
+                    base, j, &r);
+    accumulate_row(partial[slot / kTile], j, r);
+  }
+  NormalEq<S> total;
+  for (int t = 0; t < n_tiles; ++t) add_into(total, partial[t]);
+  return total;
+}
+
+template <typename S, typename V, typename K>
+LiftedTrackResult<S> track_frame_lifted(const V& volume, const Image<double>& depth, const PoseT<S>& init,
+                                        const IntrinsicsT<K>& k, const IcpConfig& cfg, const RaycastConfig& rc = {}) {
+  LiftedTrackResult<S> out;
+  const int levels = std::clamp(cfg.levels, 1, 3);
+  const auto pyramid = build_depth_pyramid(bilateral_filter(depth), levels);
+  PoseT<S> pose = init;
+  int iteration = 0;
+  for (int li = 0; li < levels; ++li) {
+    const int level = levels - 1 - li;
+    const IntrinsicsT<K> kl = k.at_level(level);
+    const Intrinsics klr = real_intrinsics(kl);
+    const SurfaceMaps<S> measured = measure_surface<S>(pyramid[level], kl);
+    const SurfaceMaps<double> measured_re = real_maps(measured);
+    const PoseT<S> prediction_pose = pose;
+    const SurfaceMaps<S> predicted = raycast<S>(volume, prediction_pose, kl, rc);
+    const SurfaceMaps<double> predicted_re = real_maps(predicted);
+    const int stride = std::max(1, cfg.level_pixel_stride[li]);
+    for (int it = 0; it < cfg.level_iterations[li]; ++it) {
+      std::vector<CorrIndex> idx;
+      associate(measured_re, predicted_re, real_pose(pose), real_pose(prediction_pose), klr, cfg, stride, &idx);
+      out.correspondences = static_cast<int>(idx.size());
+      if (idx.size() < 12) break;
+      const NormalEq<S> ne = tiled_normal_equations(idx, klr.width, klr.height, stride, measured, predicted, pose);
+      S nb[6];
+      for (int i = 0; i < 6; ++i) nb[i] = -ne.b[i];
+      const Ldlt6<S> ldlt(ne.a);
+      S d[6];
+      ldlt.solve(nb, d);
+      bool finite = true;
+      for (int i = 0; i < 6; ++i) finite = finite && isfinite_s(d[i]);
+      Vec6<S> delta;
+      for (int i = 0; i < 6; ++i) delta[i] = finite ? d[i] : S(0.0);
+      pose = apply_increment(delta, pose);
+      ++iteration;
+      Vec6<double> dre;
+      for (int i = 0; i < 6; ++i) dre[i] = real_part(delta[i]);
+      if (norm6(dre) < cfg.step_tolerance) {
+        if (level == 0) out.converged = true;
+        break;
+      }
+    }
+  }
+  out.pose = pose;
+  out.iterations = iteration;
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Driver
+// ---------------------------------------------------------------------------
+enum class Objective { kFinalTranslationError = 0, kTrajectoryError = 1 };
+
+struct PipelineConfig {
+  bool hashed = false;
+  VolumeParams dense;
+  HashParams hash;
+  Intrinsics k;
+  IcpConfig icp;
+  RaycastConfig rc;
+  double h = 1e-8;
+  std::vector<int> directions;  // parameter per channel: 0..5 twist (rho, phi), 6..9 fx, fy, cx, cy
+  Objective objective = Objective::kFinalTranslationError;
+};
+
+struct PipelineResult {
+  std::vector<double> gradient;        // [D]
+  double objective = 0.0;
+  std::vector<double> poses;           // [N][12][1+D]  (R row-major, t)
+  std::vector<int> iterations;         // [N]
+  std::vector<int> correspondences;    // [N]
+  std::vector<int> blocks;             // [N] allocated blocks after frame (hashed)
+  std::vector<int> visible;            // [N] visible blocks of frame (hashed)
+};
+
+template <int D>
+void store_pose(const PoseT<Lifted<D>>& p, double* out) {
+  for (int e = 0; e < 12; ++e) {
+    const Lifted<D>& s = e < 9 ? p.rotation(e / 3, e % 3) : p.translation[e - 9];
+    out[e * (1 + D)] = s.re;
+    for (int d = 0; d < D; ++d) out[e * (1 + D) + 1 + d] = s.im[d];
+  }
+}
+
+template <int D, typename V>
+PipelineResult run_pipeline_on(V& vol, const PipelineConfig& cfg, const std::vector<Image<double>>& frames,
+                               const std::vector<Pose>& gt) {
+  using S = Lifted<D>;
+  if (static_cast<int>(cfg.directions.size()) != D) throw std::invalid_argument("direction count != D");
+  const int n = static_cast<int>(frames.size());
+  PipelineResult res;
+  res.poses.assign(static_cast<std::size_t>(n) * 12 * (1 + D), 0.0);
+  res.iterations.assign(n, 0);
+  res.correspondences.assign(n, 0);
+  res.blocks.assign(n, 0);
+  res.visible.assign(n, 0);
+
+  Vec6<S> xi;
+  for (int i = 0; i < 6; ++i) xi[i] = S(0.0);
+  IntrinsicsT<S> ks;
+  ks.fx = S(cfg.k.fx); ks.fy = S(cfg.k.fy); ks.cx = S(cfg.k.cx); ks.cy = S(cfg.k.cy);
+  ks.width = cfg.k.width; ks.height = cfg.k.height; ks.depth_scale = cfg.k.depth_scale;
+  for (int d = 0; d < D; ++d) {
+    const int prm = cfg.directions[d];
+    if (prm >= 0 && prm < 6) xi[prm].im[d] = cfg.h;
+    else if (prm == 6) ks.fx.im[d] = cfg.h;
+    else if (prm == 7) ks.fy.im[d] = cfg.h;
+    else if (prm == 8) ks.cx.im[d] = cfg.h;
+    else if (prm == 9) ks.cy.im[d] = cfg.h;
+    else throw std::invalid_argument("unknown direction parameter");
+  }
+  const Intrinsics kr = cfg.k;
+
+  std::vector<PoseT<S>> poses(n);
+  auto integrate = [&](int f) {
+    if constexpr (V::kHashed) {
+      AllocStats st;
+      const std::vector<int> visible = allocate_band(vol, frames[f], kr, real_pose(poses[f]), &st);
+      surface_update_blocks(vol, visible, frames[f], poses[f], ks);
+      res.blocks[f] = vol.n_blocks();
+      res.visible[f] = st.touched;
+    } else {
+      surface_update(vol, frames[f], poses[f], ks);
+    }
+  };
+
+  poses[0] = exp_map(xi) * pose_cast<S>(gt[0]);
+  integrate(0);
+  for (int f = 1; f < n; ++f) {
+    const LiftedTrackResult<S> tr = track_frame_lifted<S>(vol, frames[f], poses[f - 1], ks, cfg.icp, cfg.rc);
+    poses[f] = tr.pose;
+    res.iterations[f] = tr.iterations;
+    res.correspondences[f] = tr.correspondences;
+    integrate(f);
+  }
+  S obj(0.0);
+  if (cfg.objective == Objective::kFinalTranslationError) {
+    const Vec3<S> diff = poses[n - 1].translation -
+                         Vec3<S>(S(gt[n - 1].translation[0]), S(gt[n - 1].translation[1]), S(gt[n - 1].translation[2]));
+    obj = sqrt(dot(diff, diff));
+  } else {
+    for (int f = 0; f < n; ++f) {
+      const Vec3<S> diff = poses[f].translation -
+                           Vec3<S>(S(gt[f].translation[0]), S(gt[f].translation[1]), S(gt[f].translation[2]));
+      obj = obj + dot(diff, diff);
+    }
+  }
+  res.objective = obj.re;
+  res.gradient.resize(D);
+  for (int d = 0; d < D; ++d) res.gradient[d] = obj.im[d] / cfg.h;
+  for (int f = 0; f < n; ++f) store_pose(poses[f], &res.poses[static_cast<std::size_t>(f) * 12 * (1 + D)]);
+  return res;
+}
+
+template <int D>
+PipelineResult run_pipeline(const PipelineConfig& cfg, const std::vector<Image<double>>& frames,
+                            const std::vector<Pose>& gt) {
+  if (cfg.hashed) {
+    HashedVolumeT<Lifted<D>> vol(cfg.hash);
+    return run_pipeline_on<D>(vol, cfg, frames, gt);
+  }
+  TsdfVolumeT<Lifted<D>> vol(cfg.dense);
+  return run_pipeline_on<D>(vol, cfg, frames, gt);
+}
+
+inline PipelineResult run_pipeline_dyn(const PipelineConfig& cfg, const std::vector<Image<double>>& frames,
+                                       const std::vector<Pose>& gt) {
+  switch (cfg.directions.size()) {
+    case 1: return run_pipeline<1>(cfg, frames, gt);
+    case 2: return run_pipeline<2>(cfg, frames, gt);
+    case 3: return run_pipeline<3>(cfg, frames, gt);
+    case 4: return run_pipeline<4>(cfg, frames, gt);
+    case 5: return run_pipeline<5>(cfg, frames, gt);
+    case 6: return run_pipeline<6>(cfg, frames, gt);
+    case 7: return run_pipeline<7>(cfg, frames, gt);
+    case 8: return run_pipeline<8>(cfg, frames, gt);
+    case 10: return run_pipeline<10>(cfg, frames, gt);
+    default: throw std::invalid_argument("oracle pipeline: unsupported direction count");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// BASELINE configs 1 and 2 inputs (builder-defined geometry)
+// ---------------------------------------------------------------------------
+struct Workload {
+  Scene scene;
+  Intrinsics k;
+  std::vector<Pose> gt;
+  std::vector<Image<double>> frames;
+};
+
+// Config 1: 4x4x3 m room + 3 spheres (seed 0), 10 frames 160x120,
+// fx=fy=120 cx=80 cy=60, orbit radius 1 m, 3 deg step, sigma = 1 mm.
+inline Scene config1_scene(uint64_t seed = 0) {
+  Scene s;
+  add_room(s, -2.0, 2.0, -2.0, 2.0, 0.0, 3.0);
+  Uniform53 u(seed);
+  for (int i = 0; i < 3; ++i) {
+    SdfSphere sp;
+    sp.radius = u.next(0.3, 0.6);
+    sp.center = Vec3d(u.next(-1.6, -0.6), u.next(-1.0, 1.0), u.next(0.3, 1.2));
+    s.spheres.push_back(sp);
+  }
+  return s;
+}
+inline Intrinsics config1_intrinsics() {
+  Intrinsics k;
+  k.fx = 120.0; k.fy = 120.0; k.cx = 80.0; k.cy = 60.0; k.width = 160; k.height = 120;
+  return k;
+}
+inline Pose config1_pose(int f) {
+  return orbit_pose(Vec3d(0.0, 0.0, 1.0), 1.0, 0.4, static_cast<double>(f) * (3.0 * M_PI / 180.0));
+}
+inline VolumeParams config1_volume() {
+  VolumeParams vp = VolumeParams::cube(128, 0.02, Vec3d(-2.1, -1.28, -0.1));
+  vp.mu = 0.06;
+  return vp;
+}
+
+// Config 2: room + 20 random spheres/boxes (seed 1), VGA, K = 525/525/319.5/239.5,
+// sigma = 0.0012 z^2, 5% dropout; hashed 5 mm voxels, mu = 5 voxels.
+inline Scene config2_scene(uint64_t seed = 1) {
+  Scene s;
+  add_room(s, -2.0, 2.0, -2.0, 2.0, 0.0, 3.0);
+  Uniform53 u(seed);
+  int placed = 0;
+  while (placed < 20) {
+    const bool sphere = (placed % 2) == 0;
+    const double r = sphere ? u.next(0.1, 0.35) : u.next(0.08, 0.3);
+    const Vec3d c(u.next(-1.8, 1.8), u.next(-1.8, 1.8), u.next(0.2, 2.5));
+    const double radial = std::sqrt(c[0] * c[0] + c[1] * c[1]);
+    const double bound = sphere ? r : r * 1.7320508075688772;
+    if (std::fabs(radial - 1.2) < bound + 0.35 && std::fabs(c[2] - 1.3) < bound + 0.45) continue;  // keep the orbit free
+    if (sphere) {
+      s.spheres.push_back({c, r});
+    } else {
+      const double hy = u.next(0.08, 0.3), hz = u.next(0.08, 0.3);
+      s.boxes.push_back({c, Vec3d(r, hy, hz)});
+    }
+    ++placed;
+  }
+  return s;
+}
+inline Pose config2_pose(int f) {
+  return orbit_pose(Vec3d(0.0, 0.0, 1.0), 1.2, 0.3, static_cast<double>(f) * (1.5 * M_PI / 180.0));
+}
+inline HashParams config2_hash() {
+  HashParams hp;
+  hp.voxel_size = 0.005;
+  hp.mu = 5.0 * hp.voxel_size;
+  hp.bucket_bits = 20;
+  hp.max_blocks = 1 << 19;
+  return hp;
+}
+
+inline Workload make_workload(int config, int n_frames, int width = 0, int height = 0) {
+  Workload w;
+  if (config == 1) {
+    w.scene = config1_scene(0);
+    w.k = config1_intrinsics();
+  } else {
+    w.scene = config2_scene(1);
+    w.k = Intrinsics();
+  }
+  if (width > 0) {  // reduced-resolution variant of the same geometry (tests)
+    const double s = static_cast<double>(width) / w.k.width;
+    w.k.fx *= s; w.k.fy *= s; w.k.cx *= s; w.k.cy *= s;
+    w.k.width = width;
+    w.k.height = height;
+  }
+  for (int f = 0; f < n_frames; ++f) {
+    const Pose p = config == 1 ? config1_pose(f) : config2_pose(f);
+    w.gt.push_back(p);
+    Image<double> d = render_depth(w.scene, p, w.k);
+    if (config == 1)
+      d = add_depth_noise(d, 0.001, 1000 + f);
+    else
+      d = add_depth_noise_quadratic(d, 0.0012, 0.05, 2000 + f);
+    w.frames.push_back(to_float32(d));
+  }
+  return w;
+}
+
+}  // namespace orc
