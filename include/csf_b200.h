@@ -1,0 +1,206 @@
+/*
+ * csf_b200.h — C-ABI of the B200-native CSFD dense-SLAM hot path.
+ *
+ * This is the drop-in boundary under the reference's C++ API
+ * (proj/include/csf/ *.hpp).  Everything is plain C: pointers, sizes and POD
+ * structs; no torch, Eigen or STL types cross it.  Each entry point cites the
+ * reference function it replaces.  The C++ mirror of the reference API
+ * (include/csf/b200.hpp) is a thin layer over these calls.
+ *
+ * Conventions:
+ *   - Poses are camera->world, 12 scalars (rotation row-major, translation).
+ *     A lifted scalar with D perturbation channels is stored as (1+D)
+ *     doubles [re, im_0 .. im_{D-1}]; a lifted array is element-major,
+ *     channel-minor: value e occupies [e*(1+D), e*(1+D)+D].
+ *   - Lifted intrinsics are 4 scalars (fx, fy, cx, cy), same layout.
+ *   - Depth is camera z in metres, 0 = invalid.  Images are row-major.
+ *   - Status codes map to the reference's exception types:
+ *       CSF_EINVAL  -> std::invalid_argument
+ *       CSF_EDOMAIN -> std::domain_error (zero real-part divisor on device)
+ *       CSF_ERUNTIME/CSF_ECUDA/CSF_ENOMEM -> std::runtime_error
+ *     csf_last_error() returns the message of the last failure on a context.
+ *   - Host buffers are borrowed for the duration of a call; device memory is
+ *     owned by handles.  Calls on one context are serialised by the caller;
+ *     different contexts (one per GPU / host thread) may run concurrently.
+ */
+#ifndef CSF_B200_H
+#define CSF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSF_OK 0
+#define CSF_EINVAL 1
+#define CSF_EDOMAIN 2
+#define CSF_ERUNTIME 3
+#define CSF_ECUDA 4
+#define CSF_ENOMEM 5
+
+#define CSF_MAX_DIRECTIONS 36
+
+typedef struct csf_ctx_s* csf_ctx;
+typedef struct csf_volume_s* csf_volume;
+typedef struct csf_pipeline_s* csf_pipeline;
+
+/* frames.hpp:15-36 (Intrinsics) */
+typedef struct {
+  double fx, fy, cx, cy;
+  int width, height;
+  double depth_scale;
+} csf_intrinsics;
+
+/* tsdf.hpp:21-36 (VolumeParams) */
+typedef struct {
+  int dims[3];
+  double voxel_size;
+  double origin[3];
+  double mu;
+  double weight_cap;
+} csf_volume_params;
+
+/* Hashed 8^3-block volume (builder-defined) */
+typedef struct {
+  double voxel_size;
+  double origin[3];
+  double mu;
+  double weight_cap;
+  int bucket_bits; /* 2^bucket_bits hash buckets (20 in BASELINE config 2) */
+  int max_blocks;  /* block-pool capacity */
+} csf_hash_params;
+
+/* tsdf.hpp:198-204 (RaycastConfig) */
+typedef struct {
+  double near_clip, far_clip, step_fraction;
+} csf_raycast_cfg;
+
+/* icp.hpp:33-53 (IcpSolver, IcpConfig).  The device tracker implements
+ * CSF_SOLVER_LINEARIZED; the lifted tracker is the linearized solver lifted
+ * to the packed scalar. */
+#define CSF_SOLVER_LINEARIZED 0
+#define CSF_SOLVER_NEWTON 1
+#define CSF_SOLVER_GRADIENT_DESCENT 2
+#define CSF_SOLVER_CONJUGATE_GRADIENT 3
+typedef struct {
+  int solver;
+  double d_max;
+  double theta_max_deg;
+  int levels;
+  int level_iterations[3];
+  int level_pixel_stride[3];
+  double step_tolerance;
+  double levenberg_lambda0;
+  int ncg_restart;
+  double h; /* StepSize (csfd.hpp:20-28) */
+} csf_icp_cfg;
+
+/* icp.hpp:119-125 (TrackResult) */
+typedef struct {
+  int iterations;
+  int converged;
+  int correspondences;
+  int pad;
+  double final_loss;
+} csf_track_result;
+
+#define CSF_OBJECTIVE_FINAL_TRANSLATION_ERROR 0
+#define CSF_OBJECTIVE_TRAJECTORY_ERROR 1
+
+/* The CSFD frame-derivative run: seed D directions (first-frame
+ * twist components 0..5 in (rho, phi) order and/or intrinsics 6..9 =
+ * fx, fy, cx, cy), fuse frame 0 at exp(xi0*) T0, track + fuse frames
+ * 1..N-1 with the lifted tracker, differentiate the objective. */
+typedef struct {
+  int hashed;
+  csf_volume_params dense;
+  csf_hash_params hash;
+  csf_intrinsics k;
+  csf_icp_cfg icp;
+  csf_raycast_cfg rc;
+  double h;
+  int n_dirs;
+  int dirs[CSF_MAX_DIRECTIONS];
+  int objective;
+  int max_frames;
+} csf_pipeline_cfg;
+
+/* ---- defaults (the reference's struct defaults) ------------------------- */
+void csf_default_intrinsics(csf_intrinsics* k);      /* frames.hpp:16-22 */
+void csf_default_volume_params(csf_volume_params* p); /* tsdf.hpp:22-26 */
+void csf_default_raycast_cfg(csf_raycast_cfg* c);     /* tsdf.hpp:199-203 */
+void csf_default_icp_cfg(csf_icp_cfg* c);             /* icp.hpp:41-52 */
+
+/* ---- context -------------------------------------------------------------- */
+int csf_ctx_create(int device, csf_ctx* out);
+int csf_ctx_destroy(csf_ctx ctx);
+const char* csf_last_error(csf_ctx ctx);
+int csf_ctx_synchronize(csf_ctx ctx);
+/* Number of kernels this context has launched so far (for launch accounting). */
+int csf_ctx_launch_count(csf_ctx ctx, unsigned long long* out);
+/* CUDA stream of the context (cudaStream_t as void*), for event timing. */
+void* csf_ctx_stream(csf_ctx ctx);
+
+/* ---- frames: frames.cpp:7-75, frames.hpp:86-114 --------------------------- */
+int csf_bilateral_filter(csf_ctx ctx, const double* depth, int w, int h, double sigma_s, double sigma_r, int radius,
+                         double* out);
+int csf_downsample_depth(csf_ctx ctx, const double* depth, int w, int h, double sigma_r, double* out);
+/* depth [w*h][1+D] lifted (depth seeds), intr [4][1+D]; outputs [w*h][3][1+D] */
+int csf_measure_surface(csf_ctx ctx, const double* depth, int w, int h, const double* intr, int n_channels,
+                        double* vertices, double* normals);
+
+/* ---- volumes: tsdf.hpp:38-78 ----------------------------------------------- */
+int csf_volume_create_dense(csf_ctx ctx, const csf_volume_params* p, int n_channels, csf_volume* out);
+int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, csf_volume* out);
+int csf_volume_destroy(csf_volume vol);
+/* Dense: n = dims product.  Hashed: n = block_count * 512 (block-major,
+ * voxel (lz*8+ly)*8+lx).  field [n][1+D], weight [n]. */
+int csf_volume_upload(csf_volume vol, const double* field, const double* weight);
+int csf_volume_download(csf_volume vol, double* field, double* weight);
+int csf_volume_block_count(csf_volume vol, int* n_blocks);
+/* heads [2^bits], keys [n_blocks], next [n_blocks], coords [n_blocks][3] */
+int csf_volume_download_hash(csf_volume vol, int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords);
+
+/* tsdf.cpp:11-40 — fuse one unperturbed depth frame at a lifted camera pose
+ * with lifted intrinsics.  Hashed volumes first allocate the frame's
+ * truncation-band blocks; *n_visible (optional) receives the visible count. */
+int csf_surface_update(csf_volume vol, const double* depth, int w, int h, const double* pose, const double* intr,
+                       int* n_visible);
+/* tsdf.hpp:209-284 — lifted raycast; outputs [w*h][3][1+D] world-frame maps */
+int csf_raycast(csf_volume vol, const double* pose, const double* intr, int w, int h, const csf_raycast_cfg* cfg,
+                double* vertices, double* normals);
+
+/* ---- icp: icp.cpp:169-244 ----------------------------------------------------
+ * Coarse-to-fine tracking of one frame against a volume's real channel
+ * (solver CSF_SOLVER_LINEARIZED; canonical slot-tiled reduction order). */
+int csf_track_frame(csf_volume vol, const double* depth, int w, int h, const double* init_pose,
+                    const csf_intrinsics* k, const csf_icp_cfg* cfg, double* out_pose, csf_track_result* result);
+
+/* ---- pipeline ------------------------------------------------------------ */
+int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf_pipeline* out);
+int csf_pipeline_destroy(csf_pipeline p);
+/* depth [n][h][w] float32 metres (host), gt [n][12] camera->world (host). */
+int csf_pipeline_upload(csf_pipeline p, const float* depth, const double* gt, int n_frames);
+/* Runs the uploaded frames on the device; asynchronous on the context stream. */
+int csf_pipeline_run(csf_pipeline p, int n_frames);
+/* Synchronises; gradient [D], poses [n][12][1+D] (optional), stats [n][8]
+ * (optional: iterations, correspondences, converged, blocks, visible, new). */
+int csf_pipeline_result(csf_pipeline p, double* gradient, double* objective, double* poses, int32_t* stats);
+/* One end-to-end call from host buffers: upload, run, read back. */
+int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames, double* gradient,
+                          double* objective);
+
+/* ---- synthetic inputs (harness; not on the timed path) ----------------------
+ * BASELINE configs 1 and 2 rendered on the device with the reference's
+ * sphere tracer (synth.cpp:55-90) and the builder-defined sensor model;
+ * depth [n][h][w] float32, gt [n][12].  width/height 0 = config default. */
+int csf_synth_workload(csf_ctx ctx, int config, int n_frames, int width, int height, float* depth, double* gt,
+                       csf_intrinsics* k);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSF_B200_H */

@@ -1,0 +1,192 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes wrapper of oracle/_build/liborc.so (the CPU restatement of the
+reference hot path).  Imported only by tests/, __graft_entry__.smoke() and
+bench.py's CPU-baseline / --impl reference legs — never by the product.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from paper_2405_02187_b200 import capi as _capi  # struct layouts only (no product calls)
+
+LIB_PATH = Path(__file__).resolve().parent / "_build" / "liborc.so"
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"oracle library {LIB_PATH} missing: run make -C oracle")
+        L = C.CDLL(str(LIB_PATH))
+        dp, ip, vp = C.POINTER(C.c_double), C.c_int, C.c_void_p
+        i32p, u64p, fp = C.POINTER(C.c_int32), C.POINTER(C.c_uint64), C.POINTER(C.c_float)
+        sig = {
+            "orc_last_error": (C.c_char_p, []),
+            "orc_bilateral": (ip, [dp, ip, ip, C.c_double, C.c_double, ip, dp]),
+            "orc_downsample": (ip, [dp, ip, ip, C.c_double, dp]),
+            "orc_measure": (ip, [dp, ip, ip, dp, ip, dp, dp]),
+            "orc_volume_create_dense": (ip, [C.POINTER(_capi.VolumeParams), ip, C.POINTER(vp)]),
+            "orc_volume_create_hashed": (ip, [C.POINTER(_capi.HashParams), ip, C.POINTER(vp)]),
+            "orc_volume_destroy": (None, [vp]),
+            "orc_surface_update": (ip, [vp, dp, ip, ip, dp, dp, C.POINTER(C.c_int)]),
+            "orc_raycast": (ip, [vp, dp, dp, ip, ip, C.POINTER(_capi.RaycastCfg), dp, dp]),
+            "orc_volume_voxels": (C.c_longlong, [vp]),
+            "orc_volume_download": (ip, [vp, dp, dp]),
+            "orc_volume_upload": (ip, [vp, dp, dp]),
+            "orc_volume_block_count": (ip, [vp]),
+            "orc_volume_hash": (ip, [vp, i32p, u64p, i32p, i32p]),
+            "orc_track_frame": (ip, [vp, dp, ip, ip, dp, C.POINTER(_capi.Intrinsics), C.POINTER(_capi.IcpCfg), ip,
+                                     dp, C.POINTER(_capi.TrackResult)]),
+            "orc_workload": (ip, [ip, ip, ip, ip, fp, dp, C.POINTER(_capi.Intrinsics)]),
+            "orc_pipeline_run": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, i32p, dp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().orc_last_error()
+        raise RuntimeError(f"oracle error {rc}: {msg.decode() if msg else ''}")
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def bilateral_filter(depth, sigma_s=4.5, sigma_r=0.03, radius=3):
+    d = np.ascontiguousarray(depth, dtype=np.float64)
+    h, w = d.shape
+    out = np.empty_like(d)
+    _check(lib().orc_bilateral(_dp(d), w, h, sigma_s, sigma_r, radius, _dp(out)))
+    return out
+
+
+def downsample_depth(depth, sigma_r=0.03):
+    d = np.ascontiguousarray(depth, dtype=np.float64)
+    h, w = d.shape
+    out = np.empty((h // 2, w // 2))
+    _check(lib().orc_downsample(_dp(d), w, h, sigma_r, _dp(out)))
+    return out
+
+
+def measure_surface(depth_lifted, intr_lifted):
+    d = np.ascontiguousarray(depth_lifted, dtype=np.float64)
+    h, w, cc = d.shape
+    k = np.ascontiguousarray(intr_lifted, dtype=np.float64)
+    V = np.empty((h, w, 3, cc))
+    N = np.empty_like(V)
+    _check(lib().orc_measure(_dp(d), w, h, _dp(k), cc - 1, _dp(V), _dp(N)))
+    return V, N
+
+
+class Volume:
+    def __init__(self, params, channels: int, hashed: bool):
+        self.h = C.c_void_p()
+        self.channels = channels
+        self.hashed = hashed
+        self.params = params
+        if hashed:
+            _check(lib().orc_volume_create_hashed(C.byref(params), channels, C.byref(self.h)))
+        else:
+            _check(lib().orc_volume_create_dense(C.byref(params), channels, C.byref(self.h)))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().orc_volume_destroy(self.h)
+        except Exception:
+            pass
+
+    def surface_update(self, depth, pose, intr) -> int:
+        d = np.ascontiguousarray(depth, dtype=np.float64)
+        h, w = d.shape
+        p = np.ascontiguousarray(pose, dtype=np.float64)
+        k = np.ascontiguousarray(intr, dtype=np.float64)
+        nv = C.c_int()
+        _check(lib().orc_surface_update(self.h, _dp(d), w, h, _dp(p), _dp(k), C.byref(nv)))
+        return nv.value
+
+    def raycast(self, pose, intr, w, h, cfg=None):
+        p = np.ascontiguousarray(pose, dtype=np.float64)
+        k = np.ascontiguousarray(intr, dtype=np.float64)
+        V = np.empty((h, w, 3, 1 + self.channels))
+        N = np.empty_like(V)
+        _check(lib().orc_raycast(self.h, _dp(p), _dp(k), w, h, C.byref(cfg) if cfg is not None else None, _dp(V),
+                                 _dp(N)))
+        return V, N
+
+    def download(self):
+        n = lib().orc_volume_voxels(self.h)
+        f = np.empty((n, 1 + self.channels))
+        wt = np.empty(n)
+        _check(lib().orc_volume_download(self.h, _dp(f), _dp(wt)))
+        return f, wt
+
+    def upload(self, field, weight):
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        w = np.ascontiguousarray(weight, dtype=np.float64)
+        _check(lib().orc_volume_upload(self.h, _dp(f), _dp(w)))
+
+    def block_count(self) -> int:
+        return lib().orc_volume_block_count(self.h)
+
+    def hash_tables(self):
+        nb = self.block_count()
+        heads = np.empty(1 << self.params.bucket_bits, dtype=np.int32)
+        keys = np.empty(nb, dtype=np.uint64)
+        nxt = np.empty(nb, dtype=np.int32)
+        coords = np.empty((nb, 3), dtype=np.int32)
+        _check(lib().orc_volume_hash(self.h, heads.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     keys.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                     nxt.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     coords.ctypes.data_as(C.POINTER(C.c_int32))))
+        return heads, keys, nxt, coords
+
+    def track_frame(self, depth, init_pose12, k, cfg, canonical=True):
+        d = np.ascontiguousarray(depth, dtype=np.float64)
+        h, w = d.shape
+        init = np.ascontiguousarray(init_pose12, dtype=np.float64)
+        out = np.empty(12)
+        res = _capi.TrackResult()
+        _check(lib().orc_track_frame(self.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg), int(canonical),
+                                     _dp(out), C.byref(res)))
+        return out, res
+
+
+def workload(config: int, n_frames: int, width: int = 0, height: int = 0):
+    if width == 0:
+        w, h = (160, 120) if config == 1 else (640, 480)
+    else:
+        w, h = width, height
+    depth = np.empty((n_frames, h, w), dtype=np.float32)
+    gt = np.empty((n_frames, 12))
+    k = _capi.Intrinsics()
+    _check(lib().orc_workload(config, n_frames, width, height, depth.ctypes.data_as(C.POINTER(C.c_float)), _dp(gt),
+                              C.byref(k)))
+    return depth, gt, k
+
+
+def pipeline_run(cfg, depth, gt):
+    d = np.ascontiguousarray(depth, dtype=np.float32)
+    g = np.ascontiguousarray(gt, dtype=np.float64).reshape(-1, 12)
+    n = d.shape[0]
+    D = cfg.n_dirs
+    grad = np.empty(D)
+    obj = C.c_double()
+    poses = np.empty((n, 12, 1 + D))
+    stats = np.empty((n, 8), dtype=np.int32)
+    secs = C.c_double()
+    _check(lib().orc_pipeline_run(C.byref(cfg), d.ctypes.data_as(C.POINTER(C.c_float)), _dp(g), n, _dp(grad),
+                                  C.byref(obj), _dp(poses), stats.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  C.byref(secs)))
+    return grad, obj.value, poses, stats, secs.value

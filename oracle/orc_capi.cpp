@@ -1,0 +1,380 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" entry points of the CPU oracle for tests/ (ctypes), the smoke
+// check and bench.py's CPU-baseline leg.  The POD structs are the product's
+// (include/csf_b200.h) so both sides are driven with the same descriptors;
+// nothing here links the product library.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../include/csf_b200.h"
+#include "orc_pipeline.hpp"
+
+using namespace orc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int guard(const std::function<void()>& fn) {
+  try {
+    fn();
+    return CSF_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return CSF_EINVAL;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return CSF_EDOMAIN;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CSF_ERUNTIME;
+  }
+}
+
+Intrinsics to_intr(const csf_intrinsics& k) {
+  Intrinsics o;
+  o.fx = k.fx; o.fy = k.fy; o.cx = k.cx; o.cy = k.cy;
+  o.width = k.width; o.height = k.height; o.depth_scale = k.depth_scale;
+  return o;
+}
+IcpConfig to_icp(const csf_icp_cfg& c) {
+  IcpConfig o;
+  o.solver = static_cast<IcpSolver>(c.solver);
+  o.d_max = c.d_max;
+  o.theta_max_deg = c.theta_max_deg;
+  o.levels = c.levels;
+  for (int i = 0; i < 3; ++i) {
+    o.level_iterations[i] = c.level_iterations[i];
+    o.level_pixel_stride[i] = c.level_pixel_stride[i];
+  }
+  o.step_tolerance = c.step_tolerance;
+  o.levenberg_lambda0 = c.levenberg_lambda0;
+  o.ncg_restart = c.ncg_restart;
+  o.step = StepSize(c.h);
+  return o;
+}
+VolumeParams to_vp(const csf_volume_params& p) {
+  VolumeParams o;
+  for (int i = 0; i < 3; ++i) o.dims[i] = p.dims[i];
+  o.voxel_size = p.voxel_size;
+  o.origin = Vec3d(p.origin[0], p.origin[1], p.origin[2]);
+  o.mu = p.mu;
+  o.weight_cap = p.weight_cap;
+  return o;
+}
+HashParams to_hp(const csf_hash_params& p) {
+  HashParams o;
+  o.voxel_size = p.voxel_size;
+  o.origin = Vec3d(p.origin[0], p.origin[1], p.origin[2]);
+  o.mu = p.mu;
+  o.weight_cap = p.weight_cap;
+  o.bucket_bits = p.bucket_bits;
+  o.max_blocks = p.max_blocks;
+  return o;
+}
+RaycastConfig to_rc(const csf_raycast_cfg* c) {
+  RaycastConfig o;
+  if (c) {
+    o.near_clip = c->near_clip;
+    o.far_clip = c->far_clip;
+    o.step_fraction = c->step_fraction;
+  }
+  return o;
+}
+
+template <int D> using FT = std::conditional_t<D == 0, double, Lifted<D>>;
+
+template <int D> FT<D> load_s(const double* p) {
+  if constexpr (D == 0) {
+    return p[0];
+  } else {
+    Lifted<D> o(p[0]);
+    for (int d = 0; d < D; ++d) o.im[d] = p[1 + d];
+    return o;
+  }
+}
+template <int D> void store_s(double* p, const FT<D>& v) {
+  if constexpr (D == 0) {
+    p[0] = v;
+  } else {
+    p[0] = v.re;
+    for (int d = 0; d < D; ++d) p[1 + d] = v.im[d];
+  }
+}
+template <int D> PoseT<FT<D>> load_pose(const double* p) {
+  PoseT<FT<D>> o;
+  for (int e = 0; e < 9; ++e) o.rotation(e / 3, e % 3) = load_s<D>(p + e * (1 + D));
+  for (int e = 0; e < 3; ++e) o.translation[e] = load_s<D>(p + (9 + e) * (1 + D));
+  return o;
+}
+template <int D> IntrinsicsT<FT<D>> load_intr(const double* p, int w, int h) {
+  IntrinsicsT<FT<D>> k;
+  k.fx = load_s<D>(p);
+  k.fy = load_s<D>(p + (1 + D));
+  k.cx = load_s<D>(p + 2 * (1 + D));
+  k.cy = load_s<D>(p + 3 * (1 + D));
+  k.width = w;
+  k.height = h;
+  return k;
+}
+
+struct VolBase {
+  virtual ~VolBase() = default;
+  virtual int channels() const = 0;
+  virtual void fuse(const Image<double>& depth, const double* pose, const double* intr, int* n_visible) = 0;
+  virtual void raycast(const double* pose, const double* intr, int w, int h, const RaycastConfig& rc, double* vert,
+                       double* norm) = 0;
+  virtual long long voxels() const = 0;
+  virtual void download(double* field, double* weight) const = 0;
+  virtual void upload(const double* field, const double* weight) = 0;
+  virtual int blocks() const = 0;
+  virtual void hash_tables(int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords) const = 0;
+  virtual TrackResult track(const Image<double>& depth, const Pose& init, const Intrinsics& k, const IcpConfig& cfg,
+                            bool canonical) const = 0;
+};
+
+template <int D, bool H>
+struct Vol : VolBase {
+  using F = FT<D>;
+  using V = std::conditional_t<H, HashedVolumeT<F>, TsdfVolumeT<F>>;
+  V vol;
+  template <typename P> explicit Vol(const P& p) : vol(p) {}
+  int channels() const override { return D; }
+  void fuse(const Image<double>& depth, const double* pose, const double* intr, int* n_visible) override {
+    const PoseT<F> c2w = load_pose<D>(pose);
+    const IntrinsicsT<F> k = load_intr<D>(intr, depth.width, depth.height);
+    if constexpr (H) {
+      Intrinsics kr = real_intrinsics(k);
+      AllocStats st;
+      const auto vis = allocate_band(vol, depth, kr, real_pose(c2w), &st);
+      surface_update_blocks(vol, vis, depth, c2w, k);
+      if (n_visible) *n_visible = st.touched;
+    } else {
+      surface_update(vol, depth, c2w, k);
+      if (n_visible) *n_visible = 0;
+    }
+  }
+  void raycast(const double* pose, const double* intr, int w, int h, const RaycastConfig& rc, double* vert,
+               double* norm) override {
+    const PoseT<F> c2w = load_pose<D>(pose);
+    const IntrinsicsT<F> k = load_intr<D>(intr, w, h);
+    const SurfaceMaps<F> m = orc::raycast<F>(vol, c2w, k, rc);
+    for (std::size_t i = 0; i < m.vertices.data.size(); ++i)
+      for (int c = 0; c < 3; ++c) {
+        store_s<D>(vert + (i * 3 + c) * (1 + D), m.vertices.data[i][c]);
+        store_s<D>(norm + (i * 3 + c) * (1 + D), m.normals.data[i][c]);
+      }
+  }
+  long long voxels() const override { return static_cast<long long>(vol.tsdf.size()); }
+  void download(double* field, double* weight) const override {
+    for (std::size_t i = 0; i < vol.tsdf.size(); ++i) {
+      store_s<D>(field + i * (1 + D), vol.tsdf[i]);
+      weight[i] = vol.weight[i];
+    }
+  }
+  void upload(const double* field, const double* weight) override {
+    for (std::size_t i = 0; i < vol.tsdf.size(); ++i) {
+      vol.tsdf[i] = load_s<D>(field + i * (1 + D));
+      vol.weight[i] = weight[i];
+    }
+  }
+  int blocks() const override {
+    if constexpr (H) return vol.n_blocks();
+    return 0;
+  }
+  void hash_tables(int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords) const override {
+    if constexpr (H) {
+      if (heads) std::memcpy(heads, vol.heads.data(), sizeof(int32_t) * vol.heads.size());
+      if (keys) std::memcpy(keys, vol.keys.data(), sizeof(uint64_t) * vol.keys.size());
+      if (next) std::memcpy(next, vol.next.data(), sizeof(int32_t) * vol.next.size());
+      if (coords) std::memcpy(coords, vol.coords.data(), sizeof(int32_t) * vol.coords.size());
+    }
+  }
+  TrackResult track(const Image<double>& depth, const Pose& init, const Intrinsics& k, const IcpConfig& cfg,
+                    bool canonical) const override {
+    return track_frame(vol, depth, init, k, cfg, nullptr, canonical);
+  }
+};
+
+template <bool H, typename P> VolBase* make_vol(int D, const P& p) {
+  switch (D) {
+    case 0: return new Vol<0, H>(p);
+    case 1: return new Vol<1, H>(p);
+    case 2: return new Vol<2, H>(p);
+    case 3: return new Vol<3, H>(p);
+    case 4: return new Vol<4, H>(p);
+    case 5: return new Vol<5, H>(p);
+    case 6: return new Vol<6, H>(p);
+    case 8: return new Vol<8, H>(p);
+    case 10: return new Vol<10, H>(p);
+    default: throw std::invalid_argument("oracle: unsupported channel count");
+  }
+}
+
+Image<double> image_of(const double* d, int w, int h) {
+  Image<double> im(w, h, 0.0);
+  std::memcpy(im.data.data(), d, sizeof(double) * w * h);
+  return im;
+}
+
+template <int D>
+void measure_impl(const double* depth, int w, int h, const double* intr, double* vert, double* norm) {
+  using S = FT<D>;
+  Image<S> dimg(w, h, S(0.0));
+  for (int i = 0; i < w * h; ++i) dimg.data[i] = load_s<D>(depth + i * (1 + D));
+  const IntrinsicsT<S> k = load_intr<D>(intr, w, h);
+  const auto m = measure_surface<S>(dimg, k);
+  for (int i = 0; i < w * h; ++i)
+    for (int c = 0; c < 3; ++c) {
+      store_s<D>(vert + (i * 3 + c) * (1 + D), m.vertices.data[i][c]);
+      store_s<D>(norm + (i * 3 + c) * (1 + D), m.normals.data[i][c]);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* orc_last_error() { return g_err.c_str(); }
+
+int orc_bilateral(const double* depth, int w, int h, double ss, double sr, int r, double* out) {
+  return guard([&] {
+    const auto o = bilateral_filter(image_of(depth, w, h), ss, sr, r);
+    std::memcpy(out, o.data.data(), sizeof(double) * w * h);
+  });
+}
+
+int orc_downsample(const double* depth, int w, int h, double sr, double* out) {
+  return guard([&] {
+    const auto o = downsample_depth(image_of(depth, w, h), sr);
+    std::memcpy(out, o.data.data(), sizeof(double) * o.data.size());
+  });
+}
+
+int orc_measure(const double* depth, int w, int h, const double* intr, int D, double* vert, double* norm) {
+  return guard([&] {
+    switch (D) {
+      case 0: measure_impl<0>(depth, w, h, intr, vert, norm); break;
+      case 1: measure_impl<1>(depth, w, h, intr, vert, norm); break;
+      case 2: measure_impl<2>(depth, w, h, intr, vert, norm); break;
+      case 3: measure_impl<3>(depth, w, h, intr, vert, norm); break;
+      case 4: measure_impl<4>(depth, w, h, intr, vert, norm); break;
+      default: throw std::invalid_argument("orc_measure: unsupported channel count");
+    }
+  });
+}
+
+int orc_volume_create_dense(const csf_volume_params* p, int D, void** out) {
+  return guard([&] { *out = make_vol<false>(D, to_vp(*p)); });
+}
+int orc_volume_create_hashed(const csf_hash_params* p, int D, void** out) {
+  return guard([&] { *out = make_vol<true>(D, to_hp(*p)); });
+}
+void orc_volume_destroy(void* v) { delete static_cast<VolBase*>(v); }
+int orc_surface_update(void* v, const double* depth, int w, int h, const double* pose, const double* intr,
+                       int* n_visible) {
+  return guard([&] { static_cast<VolBase*>(v)->fuse(image_of(depth, w, h), pose, intr, n_visible); });
+}
+int orc_raycast(void* v, const double* pose, const double* intr, int w, int h, const csf_raycast_cfg* rc, double* vert,
+                double* norm) {
+  return guard([&] { static_cast<VolBase*>(v)->raycast(pose, intr, w, h, to_rc(rc), vert, norm); });
+}
+long long orc_volume_voxels(void* v) { return static_cast<VolBase*>(v)->voxels(); }
+int orc_volume_download(void* v, double* field, double* weight) {
+  return guard([&] { static_cast<VolBase*>(v)->download(field, weight); });
+}
+int orc_volume_upload(void* v, const double* field, const double* weight) {
+  return guard([&] { static_cast<VolBase*>(v)->upload(field, weight); });
+}
+int orc_volume_block_count(void* v) { return static_cast<VolBase*>(v)->blocks(); }
+int orc_volume_hash(void* v, int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords) {
+  return guard([&] { static_cast<VolBase*>(v)->hash_tables(heads, keys, next, coords); });
+}
+int orc_track_frame(void* v, const double* depth, int w, int h, const double* init_pose, const csf_intrinsics* k,
+                    const csf_icp_cfg* cfg, int canonical, double* out_pose, csf_track_result* res) {
+  return guard([&] {
+    Pose init;
+    for (int e = 0; e < 9; ++e) init.rotation(e / 3, e % 3) = init_pose[e];
+    for (int e = 0; e < 3; ++e) init.translation[e] = init_pose[9 + e];
+    const TrackResult r =
+        static_cast<VolBase*>(v)->track(image_of(depth, w, h), init, to_intr(*k), to_icp(*cfg), canonical != 0);
+    for (int e = 0; e < 9; ++e) out_pose[e] = r.pose.rotation(e / 3, e % 3);
+    for (int e = 0; e < 3; ++e) out_pose[9 + e] = r.pose.translation[e];
+    if (res) {
+      res->iterations = r.iterations;
+      res->converged = r.converged;
+      res->correspondences = r.correspondences;
+      res->final_loss = r.final_loss;
+    }
+  });
+}
+
+// Oracle synthetic workload (configs 1/2): depth [n][h][w] float32, gt [n][12].
+int orc_workload(int config, int n_frames, int width, int height, float* depth, double* gt, csf_intrinsics* k) {
+  return guard([&] {
+    const Workload w = make_workload(config, n_frames, width, height);
+    const std::size_t P = static_cast<std::size_t>(w.k.width) * w.k.height;
+    for (int f = 0; f < n_frames; ++f) {
+      for (std::size_t i = 0; i < P; ++i) depth[f * P + i] = static_cast<float>(w.frames[f].data[i]);
+      for (int e = 0; e < 9; ++e) gt[12 * f + e] = w.gt[f].rotation(e / 3, e % 3);
+      for (int e = 0; e < 3; ++e) gt[12 * f + 9 + e] = w.gt[f].translation[e];
+    }
+    if (k) {
+      k->fx = w.k.fx; k->fy = w.k.fy; k->cx = w.k.cx; k->cy = w.k.cy;
+      k->width = w.k.width; k->height = w.k.height; k->depth_scale = w.k.depth_scale;
+    }
+  });
+}
+
+// The CSFD frame-derivative run.  poses [n][12][1+D], stats [n][8]
+// (iterations, correspondences, 0, blocks, visible, ...).  Returns wall
+// seconds through *seconds (the CPU baseline's timed region).
+int orc_pipeline_run(const csf_pipeline_cfg* c, const float* depth, const double* gt_in, int n_frames,
+                     double* gradient, double* objective, double* poses, int32_t* stats, double* seconds) {
+  return guard([&] {
+    PipelineConfig cfg;
+    cfg.hashed = c->hashed != 0;
+    cfg.dense = to_vp(c->dense);
+    cfg.hash = to_hp(c->hash);
+    cfg.k = to_intr(c->k);
+    cfg.icp = to_icp(c->icp);
+    cfg.rc = to_rc(&c->rc);
+    cfg.h = StepSize(c->h).h;
+    cfg.directions.assign(c->dirs, c->dirs + c->n_dirs);
+    cfg.objective = static_cast<Objective>(c->objective);
+    const std::size_t P = static_cast<std::size_t>(cfg.k.width) * cfg.k.height;
+    std::vector<Image<double>> frames;
+    std::vector<Pose> gt;
+    for (int f = 0; f < n_frames; ++f) {
+      Image<double> im(cfg.k.width, cfg.k.height, 0.0);
+      for (std::size_t i = 0; i < P; ++i) im.data[i] = static_cast<double>(depth[f * P + i]);
+      frames.push_back(std::move(im));
+      Pose p;
+      for (int e = 0; e < 9; ++e) p.rotation(e / 3, e % 3) = gt_in[12 * f + e];
+      for (int e = 0; e < 3; ++e) p.translation[e] = gt_in[12 * f + 9 + e];
+      gt.push_back(p);
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const PipelineResult r = run_pipeline_dyn(cfg, frames, gt);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (objective) *objective = r.objective;
+    if (gradient)
+      for (int d = 0; d < c->n_dirs; ++d) gradient[d] = r.gradient[d];
+    if (poses) std::memcpy(poses, r.poses.data(), sizeof(double) * r.poses.size());
+    if (stats)
+      for (int f = 0; f < n_frames; ++f) {
+        stats[8 * f] = r.iterations[f];
+        stats[8 * f + 1] = r.correspondences[f];
+        stats[8 * f + 2] = 0;
+        stats[8 * f + 3] = r.blocks[f];
+        stats[8 * f + 4] = r.visible[f];
+        for (int j = 5; j < 8; ++j) stats[8 * f + j] = 0;
+      }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,472 @@
+"""B200-native CSFD dense-SLAM hot path (X-SLAM, arXiv 2405.02187).
+
+Python host mirror of the reference's C++ API (proj/include/csf/*.hpp) over
+the C-ABI in include/csf_b200.h.  Names, argument meaning and error types
+follow the reference:
+
+    bilateral_filter, downsample_depth, build_depth_pyramid  (frames.hpp:56-65)
+    measure_surface                                            (frames.hpp:86-114)
+    TsdfVolume / HashedVolume, surface_update, raycast         (tsdf.hpp:38-284)
+    track_frame                                                (icp.hpp:130-133)
+    Pipeline (the CSFD frame-derivative run)
+
+Errors: CSF_EINVAL -> InvalidArgument (ValueError, std::invalid_argument),
+CSF_EDOMAIN -> DomainError (ArithmeticError, std::domain_error), everything
+else -> RuntimeError (std::runtime_error).
+
+Lifted values carry D perturbation channels as a trailing axis of size 1+D
+(index 0 = real part).  Poses are camera->world (12, 1+D): rotation
+row-major then translation.  Every compute call runs on the sm_100a kernels;
+importing works without a GPU but creating a Context requires one.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import capi as _capi
+
+__all__ = [
+    "InvalidArgument", "DomainError", "Context", "bilateral_filter", "downsample_depth", "build_depth_pyramid",
+    "measure_surface", "TsdfVolume", "HashedVolume", "surface_update", "raycast", "track_frame", "TrackResult",
+    "Pipeline", "PipelineResult", "synth_workload", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
+    "lift_pose", "lift_intrinsics", "library",
+]
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument"""
+
+
+class DomainError(ArithmeticError):
+    """std::domain_error"""
+
+
+_LIB: Optional[C.CDLL] = None
+
+
+def library() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        _LIB = _capi.load_library()
+    return _LIB
+
+
+def _raise(rc: int, msg: str) -> None:
+    if rc == _capi.CSF_OK:
+        return
+    if rc == _capi.CSF_EINVAL:
+        raise InvalidArgument(msg)
+    if rc == _capi.CSF_EDOMAIN:
+        raise DomainError(msg)
+    raise RuntimeError(f"csf_b200 error {rc}: {msg}")
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _fp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Context:
+    """One device context: a CUDA stream and an error flag (csf_ctx_create)."""
+
+    _default: Optional["Context"] = None
+
+    def __init__(self, device: int = 0):
+        self.lib = library()
+        h = C.c_void_p()
+        rc = self.lib.csf_ctx_create(device, C.byref(h))
+        if rc != _capi.CSF_OK:
+            raise RuntimeError(f"csf_ctx_create(device={device}) failed with {rc}: no usable CUDA device "
+                               "(the sm_100a path has no CPU fallback)")
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def default(cls) -> "Context":
+        if cls._default is None:
+            cls._default = Context(0)
+        return cls._default
+
+    def check(self, rc: int) -> None:
+        if rc != _capi.CSF_OK:
+            msg = self.lib.csf_last_error(self.h)
+            _raise(rc, msg.decode() if msg else "")
+
+    def synchronize(self) -> None:
+        self.check(self.lib.csf_ctx_synchronize(self.h))
+
+    @property
+    def launch_count(self) -> int:
+        n = C.c_ulonglong()
+        self.check(self.lib.csf_ctx_launch_count(self.h, C.byref(n)))
+        return int(n.value)
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.csf_ctx_stream(self.h) or 0)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.csf_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _ctx(ctx: Optional[Context]) -> Context:
+    return ctx if ctx is not None else Context.default()
+
+
+# ----------------------------------------------------------------------------- config helpers
+def intrinsics(fx=525.0, fy=525.0, cx=319.5, cy=239.5, width=640, height=480, depth_scale=5000.0):
+    """frames.hpp:15-22 defaults."""
+    return _capi.Intrinsics(fx, fy, cx, cy, width, height, depth_scale)
+
+
+def default_icp_cfg(**kw) -> _capi.IcpCfg:
+    c = _capi.IcpCfg()
+    library().csf_default_icp_cfg(C.byref(c))
+    for k, v in kw.items():
+        if k in ("level_iterations", "level_pixel_stride"):
+            getattr(c, k)[:] = list(v)
+        else:
+            setattr(c, k, v)
+    return c
+
+
+def default_raycast_cfg(**kw) -> _capi.RaycastCfg:
+    c = _capi.RaycastCfg(0.0, 10.0, 0.5)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def lift_pose(pose, channels: int = 0) -> np.ndarray:
+    """(12,) / (3,4) / (4,4) real pose -> (12, 1+D) with zero channels."""
+    p = np.asarray(pose, dtype=np.float64)
+    if p.shape == (4, 4):
+        p = np.concatenate([p[:3, :3].reshape(9), p[:3, 3]])
+    elif p.shape == (3, 4):
+        p = np.concatenate([p[:, :3].reshape(9), p[:, 3]])
+    if p.shape == (12,):
+        out = np.zeros((12, 1 + channels))
+        out[:, 0] = p
+        return out
+    if p.shape == (12, 1 + channels):
+        return _f64(p)
+    raise InvalidArgument(f"pose must be (12,), (3,4), (4,4) or (12,{1 + channels}); got {p.shape}")
+
+
+def lift_intrinsics(k, channels: int = 0) -> np.ndarray:
+    if isinstance(k, _capi.Intrinsics):
+        out = np.zeros((4, 1 + channels))
+        out[:, 0] = [k.fx, k.fy, k.cx, k.cy]
+        return out
+    a = np.asarray(k, dtype=np.float64)
+    if a.shape == (4,):
+        out = np.zeros((4, 1 + channels))
+        out[:, 0] = a
+        return out
+    if a.shape == (4, 1 + channels):
+        return _f64(a)
+    raise InvalidArgument(f"intrinsics must be csf Intrinsics, (4,) or (4,{1 + channels}); got {a.shape}")
+
+
+# ----------------------------------------------------------------------------- frames
+def bilateral_filter(depth, sigma_s: float = 4.5, sigma_r: float = 0.03, radius: int = 3,
+                     ctx: Optional[Context] = None) -> np.ndarray:
+    """frames.cpp:7-38 on the device."""
+    c = _ctx(ctx)
+    d = _f64(depth)
+    h, w = d.shape
+    out = np.empty_like(d)
+    c.check(c.lib.csf_bilateral_filter(c.h, _dp(d), w, h, sigma_s, sigma_r, radius, _dp(out)))
+    return out
+
+
+def downsample_depth(depth, sigma_r: float = 0.03, ctx: Optional[Context] = None) -> np.ndarray:
+    """frames.cpp:40-66 on the device."""
+    c = _ctx(ctx)
+    d = _f64(depth)
+    h, w = d.shape
+    out = np.empty((h // 2, w // 2))
+    c.check(c.lib.csf_downsample_depth(c.h, _dp(d), w, h, sigma_r, _dp(out)))
+    return out
+
+
+def build_depth_pyramid(depth, levels: int = 3, sigma_r: float = 0.03, ctx: Optional[Context] = None):
+    """frames.cpp:68-75."""
+    pyr = [_f64(depth)]
+    for _ in range(1, levels):
+        pyr.append(downsample_depth(pyr[-1], sigma_r, ctx))
+    return pyr
+
+
+def measure_surface(depth, k, channels: int = 0, ctx: Optional[Context] = None):
+    """frames.hpp:86-114.  depth (h, w) or (h, w, 1+D); returns (V, N) of shape (h, w, 3, 1+D)."""
+    c = _ctx(ctx)
+    d = _f64(depth)
+    if d.ndim == 2:
+        d = np.ascontiguousarray(np.stack([d] + [np.zeros_like(d)] * channels, axis=-1))
+    h, w, cc = d.shape
+    D = cc - 1
+    kk = lift_intrinsics(k, D)
+    V = np.empty((h, w, 3, 1 + D))
+    N = np.empty((h, w, 3, 1 + D))
+    c.check(c.lib.csf_measure_surface(c.h, _dp(d), w, h, _dp(kk), D, _dp(V), _dp(N)))
+    return V, N
+
+
+# ----------------------------------------------------------------------------- volumes
+class _Volume:
+    hashed = False
+
+    def __init__(self, ctx: Optional[Context], channels: int):
+        self.ctx = _ctx(ctx)
+        self.channels = channels
+        self.h = C.c_void_p()
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.ctx.lib.csf_volume_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def surface_update(self, depth, pose, k) -> int:
+        """tsdf.cpp:11-40; returns the visible block count (hashed) or 0."""
+        d = _f64(depth)
+        h, w = d.shape
+        p = lift_pose(pose, self.channels)
+        kk = lift_intrinsics(k, self.channels)
+        nv = C.c_int(0)
+        self.ctx.check(self.ctx.lib.csf_surface_update(self.h, _dp(d), w, h, _dp(p), _dp(kk), C.byref(nv)))
+        return nv.value
+
+    def raycast(self, pose, k, width: int, height: int, cfg: Optional[_capi.RaycastCfg] = None):
+        """tsdf.hpp:209-284; returns (V, N) of shape (h, w, 3, 1+D)."""
+        p = lift_pose(pose, self.channels)
+        kk = lift_intrinsics(k, self.channels)
+        V = np.empty((height, width, 3, 1 + self.channels))
+        N = np.empty_like(V)
+        cfgp = C.byref(cfg) if cfg is not None else None
+        self.ctx.check(self.ctx.lib.csf_raycast(self.h, _dp(p), _dp(kk), width, height, cfgp, _dp(V), _dp(N)))
+        return V, N
+
+    def voxel_count(self) -> int:
+        raise NotImplementedError
+
+    def download(self):
+        n = self.voxel_count()
+        field = np.empty((n, 1 + self.channels))
+        weight = np.empty(n)
+        self.ctx.check(self.ctx.lib.csf_volume_download(self.h, _dp(field), _dp(weight)))
+        return field, weight
+
+    def upload(self, field, weight):
+        f = _f64(field)
+        wt = _f64(weight)
+        self.ctx.check(self.ctx.lib.csf_volume_upload(self.h, _dp(f), _dp(wt)))
+
+
+class TsdfVolume(_Volume):
+    """Dense lattice volume (tsdf.hpp:38-78), F carries `channels` perturbation channels."""
+
+    def __init__(self, dims=(128, 128, 128), voxel_size=0.02, origin=(0.0, 0.0, 0.0), mu=0.1, weight_cap=128.0,
+                 channels: int = 0, ctx: Optional[Context] = None):
+        super().__init__(ctx, channels)
+        self.params = _capi.VolumeParams((C.c_int * 3)(*dims), voxel_size, (C.c_double * 3)(*origin), mu, weight_cap)
+        self.ctx.check(self.ctx.lib.csf_volume_create_dense(self.ctx.h, C.byref(self.params), channels,
+                                                            C.byref(self.h)))
+
+    @classmethod
+    def cube(cls, n: int, voxel: float, origin, channels: int = 0, ctx: Optional[Context] = None):
+        """VolumeParams::cube (tsdf.hpp:28-35): mu = 5 voxels."""
+        return cls((n, n, n), voxel, origin, 5.0 * voxel, 128.0, channels, ctx)
+
+    def voxel_count(self) -> int:
+        d = self.params.dims
+        return d[0] * d[1] * d[2]
+
+
+class HashedVolume(_Volume):
+    """Hashed 8^3-block volume (builder-defined)."""
+    hashed = True
+
+    def __init__(self, voxel_size=0.005, origin=(0.0, 0.0, 0.0), mu=0.025, weight_cap=128.0, bucket_bits=20,
+                 max_blocks=1 << 18, channels: int = 0, ctx: Optional[Context] = None):
+        super().__init__(ctx, channels)
+        self.params = _capi.HashParams(voxel_size, (C.c_double * 3)(*origin), mu, weight_cap, bucket_bits, max_blocks)
+        self.ctx.check(self.ctx.lib.csf_volume_create_hashed(self.ctx.h, C.byref(self.params), channels,
+                                                             C.byref(self.h)))
+
+    def block_count(self) -> int:
+        n = C.c_int()
+        self.ctx.check(self.ctx.lib.csf_volume_block_count(self.h, C.byref(n)))
+        return n.value
+
+    def voxel_count(self) -> int:
+        return self.block_count() * 512
+
+    def hash_tables(self):
+        nb = self.block_count()
+        heads = np.empty(1 << self.params.bucket_bits, dtype=np.int32)
+        keys = np.empty(nb, dtype=np.uint64)
+        nxt = np.empty(nb, dtype=np.int32)
+        coords = np.empty((nb, 3), dtype=np.int32)
+        self.ctx.check(self.ctx.lib.csf_volume_download_hash(
+            self.h, heads.ctypes.data_as(C.POINTER(C.c_int32)), keys.ctypes.data_as(C.POINTER(C.c_uint64)),
+            nxt.ctypes.data_as(C.POINTER(C.c_int32)), coords.ctypes.data_as(C.POINTER(C.c_int32))))
+        return heads, keys, nxt, coords
+
+
+def surface_update(volume: _Volume, depth, camera_to_world, k) -> int:
+    return volume.surface_update(depth, camera_to_world, k)
+
+
+def raycast(volume: _Volume, camera_to_world, k, width=None, height=None, cfg=None):
+    if width is None:
+        width, height = k.width, k.height
+    return volume.raycast(camera_to_world, k, width, height, cfg)
+
+
+@dataclass
+class TrackResult:
+    """icp.hpp:119-125"""
+    pose: np.ndarray
+    iterations: int
+    converged: bool
+    final_loss: float
+    correspondences: int
+
+
+def track_frame(volume: _Volume, depth, init_camera_to_world, k, cfg: Optional[_capi.IcpCfg] = None) -> TrackResult:
+    """icp.cpp:169-244 on the device (linearized solver)."""
+    ctx = volume.ctx
+    d = _f64(depth)
+    h, w = d.shape
+    init = lift_pose(init_camera_to_world, 0)[:, 0].copy()
+    out = np.empty(12)
+    res = _capi.TrackResult()
+    cfg = cfg if cfg is not None else default_icp_cfg()
+    ctx.check(ctx.lib.csf_track_frame(volume.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg), _dp(out),
+                                      C.byref(res)))
+    return TrackResult(out, res.iterations, bool(res.converged), res.final_loss, res.correspondences)
+
+
+# ----------------------------------------------------------------------------- pipeline
+@dataclass
+class PipelineResult:
+    gradient: np.ndarray
+    objective: float
+    poses: Optional[np.ndarray] = None
+    stats: Optional[np.ndarray] = None
+
+
+class Pipeline:
+    """The CSFD frame-derivative run on the device (csf_pipeline_*)."""
+
+    def __init__(self, cfg: _capi.PipelineCfg, ctx: Optional[Context] = None):
+        self.ctx = _ctx(ctx)
+        self.cfg = cfg
+        self.D = cfg.n_dirs
+        self.h = C.c_void_p()
+        self.ctx.check(self.ctx.lib.csf_pipeline_create(self.ctx.h, C.byref(cfg), C.byref(self.h)))
+        self.n_frames = 0
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.ctx.lib.csf_pipeline_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, depth: np.ndarray, gt: np.ndarray) -> None:
+        d = np.ascontiguousarray(depth, dtype=np.float32)
+        g = _f64(gt).reshape(-1, 12)
+        self.n_frames = d.shape[0]
+        self.ctx.check(self.ctx.lib.csf_pipeline_upload(self.h, _fp(d), _dp(g), self.n_frames))
+
+    def run(self, n_frames: Optional[int] = None) -> None:
+        self.ctx.check(self.ctx.lib.csf_pipeline_run(self.h, n_frames or self.n_frames))
+
+    def result(self, poses: bool = True, stats: bool = True) -> PipelineResult:
+        n = self.n_frames
+        g = np.zeros(max(self.D, 1))
+        obj = C.c_double()
+        P = np.empty((n, 12, 1 + self.D)) if poses else None
+        S = np.empty((n, 8), dtype=np.int32) if stats else None
+        self.ctx.check(self.ctx.lib.csf_pipeline_result(
+            self.h, _dp(g), C.byref(obj), _dp(P) if P is not None else None,
+            S.ctypes.data_as(C.POINTER(C.c_int32)) if S is not None else None))
+        return PipelineResult(g[: self.D].copy(), obj.value, P, S)
+
+    def run_host(self, depth: np.ndarray, gt: np.ndarray) -> PipelineResult:
+        """End-to-end call from host buffers (upload + run + read back)."""
+        d = np.ascontiguousarray(depth, dtype=np.float32)
+        g = _f64(gt).reshape(-1, 12)
+        self.n_frames = d.shape[0]
+        grad = np.zeros(max(self.D, 1))
+        obj = C.c_double()
+        self.ctx.check(self.ctx.lib.csf_pipeline_run_host(self.h, _fp(d), _dp(g), self.n_frames, _dp(grad),
+                                                          C.byref(obj)))
+        return PipelineResult(grad[: self.D].copy(), obj.value)
+
+
+def make_pipeline_cfg(*, hashed: bool, k: _capi.Intrinsics, dirs: Sequence[int], h: float, objective: int,
+                      max_frames: int, dense: Optional[_capi.VolumeParams] = None,
+                      hash_params: Optional[_capi.HashParams] = None, icp: Optional[_capi.IcpCfg] = None,
+                      rc: Optional[_capi.RaycastCfg] = None) -> _capi.PipelineCfg:
+    cfg = _capi.PipelineCfg()
+    cfg.hashed = int(hashed)
+    if dense is not None:
+        cfg.dense = dense
+    if hash_params is not None:
+        cfg.hash = hash_params
+    cfg.k = k
+    cfg.icp = icp if icp is not None else default_icp_cfg(solver=_capi.SOLVER_LINEARIZED)
+    cfg.rc = rc if rc is not None else default_raycast_cfg()
+    cfg.h = h
+    cfg.n_dirs = len(dirs)
+    for i, d in enumerate(dirs):
+        cfg.dirs[i] = d
+    cfg.objective = objective
+    cfg.max_frames = max_frames
+    return cfg
+
+
+def synth_workload(config: int, n_frames: int, width: int = 0, height: int = 0, ctx: Optional[Context] = None):
+    """BASELINE config 1/2 inputs rendered on the device: (depth float32 (n,h,w), gt (n,12), Intrinsics)."""
+    c = _ctx(ctx)
+    k = _capi.Intrinsics()
+    if width == 0:
+        w, h = (160, 120) if config == 1 else (640, 480)
+    else:
+        w, h = width, height
+    depth = np.empty((n_frames, h, w), dtype=np.float32)
+    gt = np.empty((n_frames, 12))
+    c.check(c.lib.csf_synth_workload(c.h, config, n_frames, width, height, _fp(depth), _dp(gt), C.byref(k)))
+    return depth, gt, k

@@ -1,0 +1,115 @@
+"""ctypes mirror of include/csf_b200.h (the C-ABI boundary).
+
+The structs below follow the header field for field; the loader fails loudly
+when the sm_100a library has not been built — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "_build" / "libcsf_b200.so"
+
+CSF_OK, CSF_EINVAL, CSF_EDOMAIN, CSF_ERUNTIME, CSF_ECUDA, CSF_ENOMEM = 0, 1, 2, 3, 4, 5
+CSF_MAX_DIRECTIONS = 36
+SOLVER_LINEARIZED, SOLVER_NEWTON, SOLVER_GRADIENT_DESCENT, SOLVER_CONJUGATE_GRADIENT = 0, 1, 2, 3
+OBJECTIVE_FINAL_TRANSLATION_ERROR, OBJECTIVE_TRAJECTORY_ERROR = 0, 1
+
+# Every symbol include/csf_b200.h declares (checked by tests/test_capi_exports.py).
+EXPORTS = (
+    "csf_default_intrinsics", "csf_default_volume_params", "csf_default_raycast_cfg", "csf_default_icp_cfg",
+    "csf_ctx_create", "csf_ctx_destroy", "csf_last_error", "csf_ctx_synchronize", "csf_ctx_launch_count",
+    "csf_ctx_stream", "csf_bilateral_filter", "csf_downsample_depth", "csf_measure_surface",
+    "csf_volume_create_dense", "csf_volume_create_hashed", "csf_volume_destroy", "csf_volume_upload",
+    "csf_volume_download", "csf_volume_block_count", "csf_volume_download_hash", "csf_surface_update",
+    "csf_raycast", "csf_track_frame", "csf_pipeline_create", "csf_pipeline_destroy", "csf_pipeline_upload",
+    "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_run_host", "csf_synth_workload",
+)
+
+
+class Intrinsics(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_int), ("height", C.c_int), ("depth_scale", C.c_double)]
+
+
+class VolumeParams(C.Structure):
+    _fields_ = [("dims", C.c_int * 3), ("voxel_size", C.c_double), ("origin", C.c_double * 3),
+                ("mu", C.c_double), ("weight_cap", C.c_double)]
+
+
+class HashParams(C.Structure):
+    _fields_ = [("voxel_size", C.c_double), ("origin", C.c_double * 3), ("mu", C.c_double),
+                ("weight_cap", C.c_double), ("bucket_bits", C.c_int), ("max_blocks", C.c_int)]
+
+
+class RaycastCfg(C.Structure):
+    _fields_ = [("near_clip", C.c_double), ("far_clip", C.c_double), ("step_fraction", C.c_double)]
+
+
+class IcpCfg(C.Structure):
+    _fields_ = [("solver", C.c_int), ("d_max", C.c_double), ("theta_max_deg", C.c_double), ("levels", C.c_int),
+                ("level_iterations", C.c_int * 3), ("level_pixel_stride", C.c_int * 3),
+                ("step_tolerance", C.c_double), ("levenberg_lambda0", C.c_double), ("ncg_restart", C.c_int),
+                ("h", C.c_double)]
+
+
+class TrackResult(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("correspondences", C.c_int), ("pad", C.c_int),
+                ("final_loss", C.c_double)]
+
+
+class PipelineCfg(C.Structure):
+    _fields_ = [("hashed", C.c_int), ("dense", VolumeParams), ("hash", HashParams), ("k", Intrinsics),
+                ("icp", IcpCfg), ("rc", RaycastCfg), ("h", C.c_double), ("n_dirs", C.c_int),
+                ("dirs", C.c_int * CSF_MAX_DIRECTIONS), ("objective", C.c_int), ("max_frames", C.c_int)]
+
+
+def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"csf_b200: CUDA library {p} is missing — run __graft_entry__.build() "
+            "(make -C paper_2405_02187_b200); there is no CPU fallback")
+    lib = C.CDLL(str(p))
+    vp, ip, dp, fp = C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_float)
+    i32p, u64p = C.POINTER(C.c_int32), C.POINTER(C.c_uint64)
+    sig = {
+        "csf_ctx_create": (ip, [ip, C.POINTER(vp)]),
+        "csf_ctx_destroy": (ip, [vp]),
+        "csf_last_error": (C.c_char_p, [vp]),
+        "csf_ctx_synchronize": (ip, [vp]),
+        "csf_ctx_launch_count": (ip, [vp, C.POINTER(C.c_ulonglong)]),
+        "csf_ctx_stream": (vp, [vp]),
+        "csf_bilateral_filter": (ip, [vp, dp, ip, ip, C.c_double, C.c_double, ip, dp]),
+        "csf_downsample_depth": (ip, [vp, dp, ip, ip, C.c_double, dp]),
+        "csf_measure_surface": (ip, [vp, dp, ip, ip, dp, ip, dp, dp]),
+        "csf_volume_create_dense": (ip, [vp, C.POINTER(VolumeParams), ip, C.POINTER(vp)]),
+        "csf_volume_create_hashed": (ip, [vp, C.POINTER(HashParams), ip, C.POINTER(vp)]),
+        "csf_volume_destroy": (ip, [vp]),
+        "csf_volume_upload": (ip, [vp, dp, dp]),
+        "csf_volume_download": (ip, [vp, dp, dp]),
+        "csf_volume_block_count": (ip, [vp, C.POINTER(C.c_int)]),
+        "csf_volume_download_hash": (ip, [vp, i32p, u64p, i32p, i32p]),
+        "csf_surface_update": (ip, [vp, dp, ip, ip, dp, dp, C.POINTER(C.c_int)]),
+        "csf_raycast": (ip, [vp, dp, dp, ip, ip, C.POINTER(RaycastCfg), dp, dp]),
+        "csf_track_frame": (ip, [vp, dp, ip, ip, dp, C.POINTER(Intrinsics), C.POINTER(IcpCfg), dp,
+                                 C.POINTER(TrackResult)]),
+        "csf_pipeline_create": (ip, [vp, C.POINTER(PipelineCfg), C.POINTER(vp)]),
+        "csf_pipeline_destroy": (ip, [vp]),
+        "csf_pipeline_upload": (ip, [vp, fp, dp, ip]),
+        "csf_pipeline_run": (ip, [vp, ip]),
+        "csf_pipeline_result": (ip, [vp, dp, dp, dp, i32p]),
+        "csf_pipeline_run_host": (ip, [vp, fp, dp, ip, dp, dp]),
+        "csf_synth_workload": (ip, [vp, ip, ip, ip, ip, fp, dp, C.POINTER(Intrinsics)]),
+        "csf_default_intrinsics": (None, [C.POINTER(Intrinsics)]),
+        "csf_default_volume_params": (None, [C.POINTER(VolumeParams)]),
+        "csf_default_raycast_cfg": (None, [C.POINTER(RaycastCfg)]),
+        "csf_default_icp_cfg": (None, [C.POINTER(IcpCfg)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib

@@ -1,0 +1,915 @@
+// C-ABI implementation (include/csf_b200.h): contexts, volumes, stage calls
+// and the device-resident CSFD frame-derivative pipeline.
+//
+// The host code only orders launches and moves buffers; every numeric stage
+// runs in the kernels of frames.cu / volume.cu / icp.cu.  A missing or
+// failing CUDA device is reported as an error — there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/csf_b200.h"
+#include "../../include/csf_detmath.h"
+#include "csf_internal.h"
+
+namespace csfi {
+int synth_workload(cudaStream_t stream, int config, int n_frames, int width, int height, float* depth_out,
+                   double* gt_out, csf_intrinsics* k_out, std::string* err);
+int band_samples(double mu, double vs);
+size_t alloc_scan_bytes(int n);
+}  // namespace csfi
+
+using namespace csfi;
+
+struct csf_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int* d_err = nullptr;
+  unsigned long long launches = 0;
+  std::string last_error;
+};
+
+namespace {
+
+int fail(csf_ctx ctx, int code, const std::string& msg) {
+  if (ctx) ctx->last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                     \
+  do {                                                                                          \
+    const cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                      \
+      return fail(ctx, _e == cudaErrorMemoryAllocation ? CSF_ENOMEM : CSF_ECUDA,                \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                          \
+  } while (0)
+
+Launch launch_of(csf_ctx ctx) { return Launch{ctx->stream, ctx->d_err, &ctx->launches}; }
+
+// Synchronise and translate the device error flag into a status code.
+int sync_check(csf_ctx ctx, const char* what) {
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(ctx, cudaGetLastError());
+  int err = 0;
+  CUDA_TRY(ctx, cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err != 0) {
+    cudaMemset(ctx->d_err, 0, sizeof(int));
+    if (err == 2) return fail(ctx, CSF_EDOMAIN, std::string(what) + ": division by a zero real part");
+    if (err == 5) return fail(ctx, CSF_ENOMEM, std::string(what) + ": hashed volume capacity exhausted");
+    return fail(ctx, CSF_ERUNTIME, std::string(what) + ": device error");
+  }
+  return CSF_OK;
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t alloc(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    const cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// volume
+// ---------------------------------------------------------------------------
+struct csf_volume_s {
+  csf_ctx ctx = nullptr;
+  bool hashed = false;
+  int D = 0, G = 0, Dp = 0;
+  DenseDev dense{};
+  HashDev hash{};
+  long long n_vox = 0;  // dense voxel count / pool voxel capacity
+  DevBuf<double2> rw;
+  DevBuf<double> fim;
+  DevBuf<int> heads, next, coords, nblocks;
+  DevBuf<unsigned long long> keys;
+  // allocation scratch (hashed)
+  AllocScratch alloc{};
+  DevBuf<unsigned long long> a_cand, a_set_keys;
+  DevBuf<int> a_cand_block, a_first_flag, a_new_flag, a_first_rank, a_new_rank, a_set_first, a_set_slot, a_visible,
+      a_counters;
+  DevBuf<unsigned char> a_cub;
+  // stage buffers for the single-call APIs
+  DevBuf<double> s_depth, s_pose, s_intr, s_vre, s_nre, s_vim, s_nim;
+
+  ~csf_volume_s() {
+    rw.release(); fim.release(); heads.release(); next.release(); coords.release(); nblocks.release(); keys.release();
+    a_cand.release(); a_set_keys.release(); a_cand_block.release(); a_first_flag.release(); a_new_flag.release();
+    a_first_rank.release(); a_new_rank.release(); a_set_first.release(); a_set_slot.release(); a_visible.release();
+    a_counters.release(); a_cub.release();
+    s_depth.release(); s_pose.release(); s_intr.release(); s_vre.release(); s_nre.release(); s_vim.release();
+    s_nim.release();
+  }
+};
+
+namespace {
+
+int ensure_alloc_scratch(csf_volume v, int w, int h) {
+  csf_ctx ctx = v->ctx;
+  const int K = band_samples(v->hash.mu, v->hash.vs);
+  const size_t n = static_cast<size_t>(w) * h * K;
+  if (v->alloc.max_cand >= static_cast<int>(n) && v->alloc.cand) return CSF_OK;
+  if (n > 0x7fffffffULL) return fail(ctx, CSF_EINVAL, "frame too large for hashed allocation");
+  CUDA_TRY(ctx, v->a_cand.alloc(n));
+  CUDA_TRY(ctx, v->a_cand_block.alloc(n));
+  CUDA_TRY(ctx, v->a_first_flag.alloc(n));
+  CUDA_TRY(ctx, v->a_new_flag.alloc(n));
+  CUDA_TRY(ctx, v->a_first_rank.alloc(n));
+  CUDA_TRY(ctx, v->a_new_rank.alloc(n));
+  CUDA_TRY(ctx, v->a_set_slot.alloc(n));
+  const int set_bits = 20;
+  CUDA_TRY(ctx, v->a_set_keys.alloc(size_t(1) << set_bits));
+  CUDA_TRY(ctx, v->a_set_first.alloc(size_t(1) << set_bits));
+  CUDA_TRY(ctx, v->a_visible.alloc(n));
+  CUDA_TRY(ctx, v->a_counters.alloc(4));
+  const size_t cub_bytes = alloc_scan_bytes(static_cast<int>(n));
+  CUDA_TRY(ctx, v->a_cub.alloc(cub_bytes));
+  CUDA_TRY(ctx, cudaMemsetAsync(v->a_counters.p, 0, sizeof(int) * 4, ctx->stream));
+  AllocScratch& a = v->alloc;
+  a.cand = v->a_cand.p;
+  a.cand_block = v->a_cand_block.p;
+  a.first_flag = v->a_first_flag.p;
+  a.new_flag = v->a_new_flag.p;
+  a.first_rank = v->a_first_rank.p;
+  a.new_rank = v->a_new_rank.p;
+  a.set_keys = v->a_set_keys.p;
+  a.set_first = v->a_set_first.p;
+  a.set_slot = v->a_set_slot.p;
+  a.set_bits = set_bits;
+  a.visible = v->a_visible.p;
+  a.counters = v->a_counters.p;
+  a.cub_tmp = v->a_cub.p;
+  a.cub_tmp_bytes = cub_bytes;
+  a.max_cand = static_cast<int>(n);
+  return CSF_OK;
+}
+
+int volume_init_common(csf_volume v, int n_channels) {
+  if (n_channels < 0 || n_channels > CSF_MAX_DIRECTIONS)
+    return fail(v->ctx, CSF_EINVAL, "channel count must be in [0, " + std::to_string(CSF_MAX_DIRECTIONS) + "]");
+  v->D = n_channels;
+  v->G = pick_group(n_channels);
+  v->Dp = padded_channels(n_channels, v->G);
+  return CSF_OK;
+}
+
+// Fuse one double depth frame already on the device.
+int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double* d_pose, const double* d_intr) {
+  const Launch L = launch_of(v->ctx);
+  if (v->hashed) {
+    const int rc = ensure_alloc_scratch(v, w, h);
+    if (rc) return rc;
+    launch_allocate(L, v->hash, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr);
+    launch_integrate_hashed(L, v->hash, v->G, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr);
+  } else {
+    launch_integrate_dense(L, v->dense, v->G, v->Dp, d_depth, w, h, d_pose, d_intr);
+  }
+  return CSF_OK;
+}
+
+void raycast_dev(csf_volume v, const double* d_pose, const double* d_intr, int w, int h, const csf_raycast_cfg& rc,
+                 double* vre, double* nre, double* vim, double* nim) {
+  const Launch L = launch_of(v->ctx);
+  const double mu = v->hashed ? v->hash.mu : v->dense.mu;
+  const double step = rc.step_fraction * mu;
+  if (v->hashed)
+    launch_raycast_hashed(L, v->hash, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, vre, nre,
+                          vim, nim);
+  else
+    launch_raycast_dense(L, v->dense, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, vre, nre,
+                         vim, nim);
+}
+
+// Host lifted array [n][1+D] -> padded [n][1+Dp]
+std::vector<double> pad_channels(const double* src, int n, int D, int Dp) {
+  std::vector<double> out(static_cast<size_t>(n) * (1 + Dp), 0.0);
+  for (int e = 0; e < n; ++e)
+    for (int c = 0; c <= std::min(D, Dp); ++c) out[static_cast<size_t>(e) * (1 + Dp) + c] = src[e * (1 + D) + c];
+  return out;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// defaults
+// ---------------------------------------------------------------------------
+extern "C" void csf_default_intrinsics(csf_intrinsics* k) {
+  k->fx = 525.0; k->fy = 525.0; k->cx = 319.5; k->cy = 239.5;
+  k->width = 640; k->height = 480; k->depth_scale = 5000.0;
+}
+extern "C" void csf_default_volume_params(csf_volume_params* p) {
+  p->dims[0] = p->dims[1] = p->dims[2] = 128;
+  p->voxel_size = 0.02;
+  p->origin[0] = p->origin[1] = p->origin[2] = 0.0;
+  p->mu = 0.1;
+  p->weight_cap = 128.0;
+}
+extern "C" void csf_default_raycast_cfg(csf_raycast_cfg* c) {
+  c->near_clip = 0.0; c->far_clip = 10.0; c->step_fraction = 0.5;
+}
+extern "C" void csf_default_icp_cfg(csf_icp_cfg* c) {
+  c->solver = CSF_SOLVER_LINEARIZED;
+  c->d_max = 0.1;
+  c->theta_max_deg = 30.0;
+  c->levels = 3;
+  c->level_iterations[0] = 10; c->level_iterations[1] = 5; c->level_iterations[2] = 4;
+  c->level_pixel_stride[0] = 1; c->level_pixel_stride[1] = 1; c->level_pixel_stride[2] = 2;
+  c->step_tolerance = 1e-6;
+  c->levenberg_lambda0 = 1e-6;
+  c->ncg_restart = 6;
+  c->h = 1e-8;
+}
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+extern "C" int csf_ctx_create(int device, csf_ctx* out) {
+  if (!out) return CSF_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return CSF_ECUDA;
+  if (device < 0 || device >= n) return CSF_EINVAL;
+  csf_ctx ctx = new csf_ctx_s();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_err, 0, sizeof(int)) != cudaSuccess) {
+    delete ctx;
+    return CSF_ECUDA;
+  }
+  *out = ctx;
+  return CSF_OK;
+}
+
+extern "C" int csf_ctx_destroy(csf_ctx ctx) {
+  if (!ctx) return CSF_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return CSF_OK;
+}
+
+extern "C" const char* csf_last_error(csf_ctx ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+extern "C" int csf_ctx_synchronize(csf_ctx ctx) {
+  if (!ctx) return CSF_EINVAL;
+  cudaSetDevice(ctx->device);
+  return sync_check(ctx, "synchronize");
+}
+
+extern "C" int csf_ctx_launch_count(csf_ctx ctx, unsigned long long* out) {
+  if (!ctx || !out) return CSF_EINVAL;
+  *out = ctx->launches;
+  return CSF_OK;
+}
+
+extern "C" void* csf_ctx_stream(csf_ctx ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+// ---------------------------------------------------------------------------
+// frames
+// ---------------------------------------------------------------------------
+extern "C" int csf_bilateral_filter(csf_ctx ctx, const double* depth, int w, int h, double sigma_s, double sigma_r,
+                                    int radius, double* out) {
+  if (!ctx || !depth || !out || w <= 0 || h <= 0 || radius < 0 || radius > 7)
+    return fail(ctx, CSF_EINVAL, "csf_bilateral_filter: bad arguments (radius must be 0..7)");
+  cudaSetDevice(ctx->device);
+  const size_t P = static_cast<size_t>(w) * h;
+  DevBuf<double> din, dout;
+  CUDA_TRY(ctx, din.alloc(P));
+  CUDA_TRY(ctx, dout.alloc(P));
+  CUDA_TRY(ctx, cudaMemcpyAsync(din.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  launch_bilateral(launch_of(ctx), nullptr, din.p, nullptr, dout.p, w, h, sigma_s, sigma_r, radius);
+  CUDA_TRY(ctx, cudaMemcpyAsync(out, dout.p, sizeof(double) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  const int rc = sync_check(ctx, "csf_bilateral_filter");
+  din.release();
+  dout.release();
+  return rc;
+}
+
+extern "C" int csf_downsample_depth(csf_ctx ctx, const double* depth, int w, int h, double sigma_r, double* out) {
+  if (!ctx || !depth || !out || w <= 1 || h <= 1) return fail(ctx, CSF_EINVAL, "csf_downsample_depth: bad arguments");
+  cudaSetDevice(ctx->device);
+  const size_t P = static_cast<size_t>(w) * h, Po = static_cast<size_t>(w / 2) * (h / 2);
+  DevBuf<double> din, dout;
+  CUDA_TRY(ctx, din.alloc(P));
+  CUDA_TRY(ctx, dout.alloc(Po));
+  CUDA_TRY(ctx, cudaMemcpyAsync(din.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  launch_downsample(launch_of(ctx), din.p, dout.p, w, h, sigma_r);
+  CUDA_TRY(ctx, cudaMemcpyAsync(out, dout.p, sizeof(double) * Po, cudaMemcpyDeviceToHost, ctx->stream));
+  const int rc = sync_check(ctx, "csf_downsample_depth");
+  din.release();
+  dout.release();
+  return rc;
+}
+
+extern "C" int csf_measure_surface(csf_ctx ctx, const double* depth, int w, int h, const double* intr, int n_channels,
+                                   double* vertices, double* normals) {
+  if (!ctx || !depth || !intr || !vertices || !normals || w <= 0 || h <= 0 || n_channels < 0 ||
+      n_channels > CSF_MAX_DIRECTIONS)
+    return fail(ctx, CSF_EINVAL, "csf_measure_surface: bad arguments");
+  cudaSetDevice(ctx->device);
+  const size_t P = static_cast<size_t>(w) * h, C = 1 + n_channels;
+  DevBuf<double> dd, dk, dv, dn;
+  CUDA_TRY(ctx, dd.alloc(P * C));
+  CUDA_TRY(ctx, dk.alloc(4 * C));
+  CUDA_TRY(ctx, dv.alloc(P * 3 * C));
+  CUDA_TRY(ctx, dn.alloc(P * 3 * C));
+  CUDA_TRY(ctx, cudaMemcpyAsync(dd.p, depth, sizeof(double) * P * C, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(dk.p, intr, sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
+  launch_measure(launch_of(ctx), dd.p, w, h, dk.p, n_channels, dv.p, dn.p);
+  CUDA_TRY(ctx, cudaMemcpyAsync(vertices, dv.p, sizeof(double) * P * 3 * C, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(normals, dn.p, sizeof(double) * P * 3 * C, cudaMemcpyDeviceToHost, ctx->stream));
+  const int rc = sync_check(ctx, "csf_measure_surface");
+  dd.release(); dk.release(); dv.release(); dn.release();
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// volumes
+// ---------------------------------------------------------------------------
+extern "C" int csf_volume_create_dense(csf_ctx ctx, const csf_volume_params* p, int n_channels, csf_volume* out) {
+  if (!ctx || !p || !out) return CSF_EINVAL;
+  *out = nullptr;
+  if (p->dims[0] <= 0 || p->dims[1] <= 0 || p->dims[2] <= 0 || !(p->voxel_size > 0.0))
+    return fail(ctx, CSF_EINVAL, "csf_volume_create_dense: dims and voxel_size must be positive");
+  cudaSetDevice(ctx->device);
+  csf_volume v = new csf_volume_s();
+  v->ctx = ctx;
+  int rc = volume_init_common(v, n_channels);
+  if (rc) {
+    delete v;
+    return rc;
+  }
+  v->n_vox = static_cast<long long>(p->dims[0]) * p->dims[1] * p->dims[2];
+  if (v->rw.alloc(v->n_vox) != cudaSuccess || v->fim.alloc(static_cast<size_t>(v->n_vox) * std::max(v->Dp, 1)) != cudaSuccess) {
+    delete v;
+    return fail(ctx, CSF_ENOMEM, "csf_volume_create_dense: out of device memory");
+  }
+  DenseDev& d = v->dense;
+  d.rw = v->rw.p;
+  d.fim = v->fim.p;
+  d.nx = p->dims[0]; d.ny = p->dims[1]; d.nz = p->dims[2];
+  d.vs = p->voxel_size;
+  d.ox = p->origin[0]; d.oy = p->origin[1]; d.oz = p->origin[2];
+  d.mu = p->mu;
+  d.cap = p->weight_cap;
+  launch_init_volume(launch_of(ctx), d.rw, d.fim, v->n_vox, v->Dp);
+  rc = sync_check(ctx, "csf_volume_create_dense");
+  if (rc) {
+    delete v;
+    return rc;
+  }
+  *out = v;
+  return CSF_OK;
+}
+
+extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, csf_volume* out) {
+  if (!ctx || !p || !out) return CSF_EINVAL;
+  *out = nullptr;
+  if (!(p->voxel_size > 0.0) || p->bucket_bits < 4 || p->bucket_bits > 28 || p->max_blocks <= 0)
+    return fail(ctx, CSF_EINVAL, "csf_volume_create_hashed: bad parameters");
+  cudaSetDevice(ctx->device);
+  csf_volume v = new csf_volume_s();
+  v->ctx = ctx;
+  v->hashed = true;
+  int rc = volume_init_common(v, n_channels);
+  if (rc) {
+    delete v;
+    return rc;
+  }
+  v->n_vox = static_cast<long long>(p->max_blocks) * 512;
+  const size_t nb = size_t(1) << p->bucket_bits;
+  if (v->rw.alloc(v->n_vox) != cudaSuccess ||
+      v->fim.alloc(static_cast<size_t>(v->n_vox) * std::max(v->Dp, 1)) != cudaSuccess ||
+      v->heads.alloc(nb) != cudaSuccess || v->next.alloc(p->max_blocks) != cudaSuccess ||
+      v->coords.alloc(3 * static_cast<size_t>(p->max_blocks)) != cudaSuccess ||
+      v->keys.alloc(p->max_blocks) != cudaSuccess || v->nblocks.alloc(1) != cudaSuccess) {
+    delete v;
+    return fail(ctx, CSF_ENOMEM, "csf_volume_create_hashed: out of device memory");
+  }
+  HashDev& d = v->hash;
+  d.rw = v->rw.p;
+  d.fim = v->fim.p;
+  d.heads = v->heads.p;
+  d.keys = v->keys.p;
+  d.next = v->next.p;
+  d.coords = v->coords.p;
+  d.n_blocks = v->nblocks.p;
+  d.bits = p->bucket_bits;
+  d.max_blocks = p->max_blocks;
+  d.vs = p->voxel_size;
+  d.ox = p->origin[0]; d.oy = p->origin[1]; d.oz = p->origin[2];
+  d.mu = p->mu;
+  d.cap = p->weight_cap;
+  cudaMemsetAsync(d.heads, 0xFF, sizeof(int) * nb, ctx->stream);
+  cudaMemsetAsync(d.next, 0xFF, sizeof(int) * p->max_blocks, ctx->stream);
+  cudaMemsetAsync(d.n_blocks, 0, sizeof(int), ctx->stream);
+  launch_init_volume(launch_of(ctx), d.rw, d.fim, v->n_vox, v->Dp);
+  rc = sync_check(ctx, "csf_volume_create_hashed");
+  if (rc) {
+    delete v;
+    return rc;
+  }
+  *out = v;
+  return CSF_OK;
+}
+
+extern "C" int csf_volume_destroy(csf_volume vol) {
+  if (!vol) return CSF_OK;
+  cudaSetDevice(vol->ctx->device);
+  cudaStreamSynchronize(vol->ctx->stream);
+  delete vol;
+  return CSF_OK;
+}
+
+extern "C" int csf_volume_block_count(csf_volume v, int* n) {
+  if (!v || !n) return CSF_EINVAL;
+  if (!v->hashed) {
+    *n = 0;
+    return CSF_OK;
+  }
+  cudaSetDevice(v->ctx->device);
+  CUDA_TRY(v->ctx, cudaStreamSynchronize(v->ctx->stream));
+  CUDA_TRY(v->ctx, cudaMemcpy(n, v->hash.n_blocks, sizeof(int), cudaMemcpyDeviceToHost));
+  return CSF_OK;
+}
+
+static long long volume_voxels_now(csf_volume v) {
+  if (!v->hashed) return v->n_vox;
+  int nb = 0;
+  csf_volume_block_count(v, &nb);
+  return static_cast<long long>(nb) * 512;
+}
+
+extern "C" int csf_volume_upload(csf_volume v, const double* field, const double* weight) {
+  if (!v || !field || !weight) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  cudaSetDevice(ctx->device);
+  const long long n = volume_voxels_now(v);
+  std::vector<double2> rw(n);
+  std::vector<double> fim(static_cast<size_t>(n) * std::max(v->Dp, 1), 0.0);
+  const int C = 1 + v->D;
+  for (long long i = 0; i < n; ++i) {
+    rw[i] = make_double2(field[i * C], weight[i]);
+    for (int d = 0; d < v->D; ++d) fim[i * v->Dp + d] = field[i * C + 1 + d];
+  }
+  CUDA_TRY(ctx, cudaMemcpy(v->rw.p, rw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+  if (v->Dp > 0) CUDA_TRY(ctx, cudaMemcpy(v->fim.p, fim.data(), sizeof(double) * n * v->Dp, cudaMemcpyHostToDevice));
+  return CSF_OK;
+}
+
+extern "C" int csf_volume_download(csf_volume v, double* field, double* weight) {
+  if (!v || !field || !weight) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  const long long n = volume_voxels_now(v);
+  std::vector<double2> rw(n);
+  std::vector<double> fim(static_cast<size_t>(n) * std::max(v->Dp, 1));
+  CUDA_TRY(ctx, cudaMemcpy(rw.data(), v->rw.p, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+  if (v->Dp > 0) CUDA_TRY(ctx, cudaMemcpy(fim.data(), v->fim.p, sizeof(double) * n * v->Dp, cudaMemcpyDeviceToHost));
+  const int C = 1 + v->D;
+  for (long long i = 0; i < n; ++i) {
+    field[i * C] = rw[i].x;
+    weight[i] = rw[i].y;
+    for (int d = 0; d < v->D; ++d) field[i * C + 1 + d] = fim[i * v->Dp + d];
+  }
+  return CSF_OK;
+}
+
+extern "C" int csf_volume_download_hash(csf_volume v, int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords) {
+  if (!v || !v->hashed) return v ? fail(v->ctx, CSF_EINVAL, "csf_volume_download_hash: not a hashed volume") : CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  int nb = 0;
+  const int rc = csf_volume_block_count(v, &nb);
+  if (rc) return rc;
+  if (heads) CUDA_TRY(ctx, cudaMemcpy(heads, v->hash.heads, sizeof(int) << v->hash.bits, cudaMemcpyDeviceToHost));
+  if (keys) CUDA_TRY(ctx, cudaMemcpy(keys, v->hash.keys, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost));
+  if (next) CUDA_TRY(ctx, cudaMemcpy(next, v->hash.next, sizeof(int) * nb, cudaMemcpyDeviceToHost));
+  if (coords) CUDA_TRY(ctx, cudaMemcpy(coords, v->hash.coords, sizeof(int) * 3 * nb, cudaMemcpyDeviceToHost));
+  return CSF_OK;
+}
+
+extern "C" int csf_surface_update(csf_volume v, const double* depth, int w, int h, const double* pose,
+                                  const double* intr, int* n_visible) {
+  if (!v || !depth || !pose || !intr || w <= 1 || h <= 1) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  cudaSetDevice(ctx->device);
+  const size_t P = static_cast<size_t>(w) * h;
+  const int C = 1 + v->Dp;
+  const std::vector<double> pp = pad_channels(pose, 12, v->D, v->Dp);
+  const std::vector<double> kp = pad_channels(intr, 4, v->D, v->Dp);
+  CUDA_TRY(ctx, v->s_depth.alloc(P));
+  CUDA_TRY(ctx, v->s_pose.alloc(12 * C));
+  CUDA_TRY(ctx, v->s_intr.alloc(4 * C));
+  CUDA_TRY(ctx, cudaMemcpyAsync(v->s_depth.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(v->s_pose.p, pp.data(), sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(v->s_intr.p, kp.data(), sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = volume_fuse(v, v->s_depth.p, w, h, v->s_pose.p, v->s_intr.p);
+  if (rc) return rc;
+  rc = sync_check(ctx, "csf_surface_update");
+  if (rc) return rc;
+  if (n_visible) {
+    *n_visible = 0;
+    if (v->hashed) CUDA_TRY(ctx, cudaMemcpy(n_visible, v->alloc.counters, sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  return CSF_OK;
+}
+
+extern "C" int csf_raycast(csf_volume v, const double* pose, const double* intr, int w, int h,
+                           const csf_raycast_cfg* cfg, double* vertices, double* normals) {
+  if (!v || !pose || !intr || !vertices || !normals || w <= 0 || h <= 0) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  cudaSetDevice(ctx->device);
+  csf_raycast_cfg rc;
+  if (cfg)
+    rc = *cfg;
+  else
+    csf_default_raycast_cfg(&rc);
+  const size_t P = static_cast<size_t>(w) * h;
+  const int C = 1 + v->Dp;
+  const std::vector<double> pp = pad_channels(pose, 12, v->D, v->Dp);
+  const std::vector<double> kp = pad_channels(intr, 4, v->D, v->Dp);
+  CUDA_TRY(ctx, v->s_pose.alloc(12 * C));
+  CUDA_TRY(ctx, v->s_intr.alloc(4 * C));
+  CUDA_TRY(ctx, v->s_vre.alloc(P * 3));
+  CUDA_TRY(ctx, v->s_nre.alloc(P * 3));
+  CUDA_TRY(ctx, v->s_vim.alloc(P * 3 * std::max(v->Dp, 1)));
+  CUDA_TRY(ctx, v->s_nim.alloc(P * 3 * std::max(v->Dp, 1)));
+  CUDA_TRY(ctx, cudaMemcpyAsync(v->s_pose.p, pp.data(), sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(v->s_intr.p, kp.data(), sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
+  raycast_dev(v, v->s_pose.p, v->s_intr.p, w, h, rc, v->s_vre.p, v->s_nre.p, v->s_vim.p, v->s_nim.p);
+  std::vector<double> vre(P * 3), nre(P * 3), vim(P * 3 * std::max(v->Dp, 1)), nim(P * 3 * std::max(v->Dp, 1));
+  CUDA_TRY(ctx, cudaMemcpyAsync(vre.data(), v->s_vre.p, sizeof(double) * P * 3, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(nre.data(), v->s_nre.p, sizeof(double) * P * 3, cudaMemcpyDeviceToHost, ctx->stream));
+  if (v->Dp > 0) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(vim.data(), v->s_vim.p, sizeof(double) * P * 3 * v->Dp, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(nim.data(), v->s_nim.p, sizeof(double) * P * 3 * v->Dp, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  const int r = sync_check(ctx, "csf_raycast");
+  if (r) return r;
+  const int Cu = 1 + v->D;
+  for (size_t e = 0; e < P * 3; ++e) {
+    vertices[e * Cu] = vre[e];
+    normals[e * Cu] = nre[e];
+    for (int d = 0; d < v->D; ++d) {
+      vertices[e * Cu + 1 + d] = vim[e * v->Dp + d];
+      normals[e * Cu + 1 + d] = nim[e * v->Dp + d];
+    }
+  }
+  return CSF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// pipeline
+// ---------------------------------------------------------------------------
+struct csf_pipeline_s {
+  csf_ctx ctx = nullptr;
+  csf_pipeline_cfg cfg{};
+  csf_volume vol = nullptr;
+  int D = 0, G = 0, Dp = 0, C = 1;
+  int W = 0, H = 0, levels = 3;
+  int n_uploaded = 0, n_run = 0;
+  DevBuf<float> frames;
+  DevBuf<double> gt, raw, pyr0, pyr1, pyr2, vre, nre, vim, nim, partials, pose, pred_pose, intr_levels, traj, kbase,
+      out;
+  DevBuf<int> counts, stats, dirs;
+  DevBuf<TrackState> st;
+  ~csf_pipeline_s() {
+    frames.release(); gt.release(); raw.release(); pyr0.release(); pyr1.release(); pyr2.release(); vre.release();
+    nre.release(); vim.release(); nim.release(); partials.release(); pose.release(); pred_pose.release();
+    intr_levels.release(); traj.release(); kbase.release(); out.release(); counts.release(); stats.release();
+    dirs.release(); st.release();
+    if (vol) csf_volume_destroy(vol);
+  }
+};
+
+extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf_pipeline* out) {
+  if (!ctx || !cfg || !out) return CSF_EINVAL;
+  *out = nullptr;
+  if (cfg->n_dirs < 0 || cfg->n_dirs > CSF_MAX_DIRECTIONS)
+    return fail(ctx, CSF_EINVAL, "csf_pipeline_create: n_dirs out of range");
+  if (!(cfg->h > 0.0) || cfg->h > 1e-6)
+    return fail(ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
+  for (int d = 0; d < cfg->n_dirs; ++d)
+    if (cfg->dirs[d] < 0 || cfg->dirs[d] > 9) return fail(ctx, CSF_EINVAL, "csf_pipeline_create: unknown direction");
+  if (cfg->icp.solver != CSF_SOLVER_LINEARIZED)
+    return fail(ctx, CSF_EINVAL, "csf_pipeline_create: the lifted tracker implements the linearized solver");
+  if (cfg->icp.levels < 1 || cfg->icp.levels > 3 || cfg->max_frames <= 0 || cfg->k.width <= 0 || cfg->k.height <= 0)
+    return fail(ctx, CSF_EINVAL, "csf_pipeline_create: bad levels/frames/size");
+  cudaSetDevice(ctx->device);
+  csf_pipeline p = new csf_pipeline_s();
+  p->ctx = ctx;
+  p->cfg = *cfg;
+  int rc = cfg->hashed ? csf_volume_create_hashed(ctx, &cfg->hash, cfg->n_dirs, &p->vol)
+                       : csf_volume_create_dense(ctx, &cfg->dense, cfg->n_dirs, &p->vol);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  p->D = cfg->n_dirs;
+  p->G = p->vol->G;
+  p->Dp = p->vol->Dp;
+  p->C = 1 + p->Dp;
+  p->W = cfg->k.width;
+  p->H = cfg->k.height;
+  p->levels = cfg->icp.levels;
+  const size_t P = static_cast<size_t>(p->W) * p->H;
+  const int C = p->C;
+  const int max_tiles = icp_tiles(p->W, p->H, 1);
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) {
+    if (r != cudaSuccess && e == cudaSuccess) e = r;
+  };
+  A(p->frames.alloc(P * cfg->max_frames));
+  A(p->gt.alloc(12 * static_cast<size_t>(cfg->max_frames)));
+  A(p->raw.alloc(P));
+  A(p->pyr0.alloc(P));
+  A(p->pyr1.alloc(P / 4 + 1));
+  A(p->pyr2.alloc(P / 16 + 1));
+  A(p->vre.alloc(P * 3));
+  A(p->nre.alloc(P * 3));
+  A(p->vim.alloc(P * 3 * std::max(p->Dp, 1)));
+  A(p->nim.alloc(P * 3 * std::max(p->Dp, 1)));
+  A(p->partials.alloc(static_cast<size_t>(max_tiles) * 27 * C));
+  A(p->counts.alloc(max_tiles));
+  A(p->pose.alloc(12 * C));
+  A(p->pred_pose.alloc(12 * C));
+  A(p->intr_levels.alloc(3 * 4 * C));
+  A(p->traj.alloc(static_cast<size_t>(cfg->max_frames) * 12 * C));
+  A(p->stats.alloc(8 * static_cast<size_t>(cfg->max_frames)));
+  A(p->dirs.alloc(CSF_MAX_DIRECTIONS));
+  A(p->kbase.alloc(4));
+  A(p->out.alloc(2 + CSF_MAX_DIRECTIONS));
+  A(p->st.alloc(1));
+  if (e != cudaSuccess) {
+    delete p;
+    return fail(ctx, CSF_ENOMEM, std::string("csf_pipeline_create: ") + cudaGetErrorString(e));
+  }
+  if (cfg->hashed) {
+    rc = ensure_alloc_scratch(p->vol, p->W, p->H);
+    if (rc) {
+      delete p;
+      return rc;
+    }
+  }
+  const double kb[4] = {cfg->k.fx, cfg->k.fy, cfg->k.cx, cfg->k.cy};
+  cudaMemcpy(p->kbase.p, kb, sizeof(kb), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->dirs.p, cfg->dirs, sizeof(int) * CSF_MAX_DIRECTIONS, cudaMemcpyHostToDevice);
+  cudaMemset(p->st.p, 0, sizeof(TrackState));
+  *out = p;
+  return CSF_OK;
+}
+
+extern "C" int csf_pipeline_destroy(csf_pipeline p) {
+  if (!p) return CSF_OK;
+  cudaSetDevice(p->ctx->device);
+  cudaStreamSynchronize(p->ctx->stream);
+  delete p;
+  return CSF_OK;
+}
+
+extern "C" int csf_pipeline_upload(csf_pipeline p, const float* depth, const double* gt, int n_frames) {
+  if (!p || !depth || !gt || n_frames <= 0) return CSF_EINVAL;
+  csf_ctx ctx = p->ctx;
+  if (n_frames > p->cfg.max_frames) return fail(ctx, CSF_EINVAL, "csf_pipeline_upload: more frames than max_frames");
+  cudaSetDevice(ctx->device);
+  const size_t P = static_cast<size_t>(p->W) * p->H;
+  CUDA_TRY(ctx, cudaMemcpyAsync(p->frames.p, depth, sizeof(float) * P * n_frames, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(p->gt.p, gt, sizeof(double) * 12 * n_frames, cudaMemcpyHostToDevice, ctx->stream));
+  p->n_uploaded = n_frames;
+  return CSF_OK;
+}
+
+static int pipeline_reset_volume(csf_pipeline p) {
+  csf_volume v = p->vol;
+  csf_ctx ctx = p->ctx;
+  const Launch L = launch_of(ctx);
+  if (v->hashed) {
+    int nb = 0;
+    CUDA_TRY(ctx, cudaMemcpyAsync(&nb, v->hash.n_blocks, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (nb > 0) {
+      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.heads, 0xFF, sizeof(int) << v->hash.bits, ctx->stream));
+      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.next, 0xFF, sizeof(int) * v->hash.max_blocks, ctx->stream));
+      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.n_blocks, 0, sizeof(int), ctx->stream));
+      launch_init_volume(L, v->hash.rw, v->hash.fim, static_cast<long long>(nb) * 512, v->Dp);
+    }
+  } else {
+    launch_init_volume(L, v->dense.rw, v->dense.fim, v->n_vox, v->Dp);
+  }
+  return CSF_OK;
+}
+
+extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
+  if (!p) return CSF_EINVAL;
+  csf_ctx ctx = p->ctx;
+  if (n_frames <= 0 || n_frames > p->n_uploaded) return fail(ctx, CSF_EINVAL, "csf_pipeline_run: frames not uploaded");
+  cudaSetDevice(ctx->device);
+  int rc = pipeline_reset_volume(p);
+  if (rc) return rc;
+  const Launch L = launch_of(ctx);
+  const csf_pipeline_cfg& cfg = p->cfg;
+  const int W = p->W, H = p->H, C = p->C;
+  const size_t P = static_cast<size_t>(W) * H;
+  csf_volume v = p->vol;
+  const double cos_max = csf_det::cos(cfg.icp.theta_max_deg * M_PI / 180.0);
+  double* pyr[3] = {p->pyr0.p, p->pyr1.p, p->pyr2.p};
+  TrackState* st = p->st.p;
+  const int* nblk = v->hashed ? v->hash.n_blocks : nullptr;
+  const int* counters = v->hashed ? v->alloc.counters : nullptr;
+
+  launch_seed(L, p->G, p->Dp, p->dirs.p, p->D, cfg.h, p->gt.p, p->kbase.p, p->pose.p, p->intr_levels.p, p->levels);
+  launch_frame_begin(L, st, 0);
+  launch_bilateral(L, p->frames.p, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
+  rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p);
+  if (rc) return rc;
+  launch_frame_end(L, st, p->pose.p, p->traj.p, p->Dp, p->stats.p, nblk, counters);
+
+  for (int f = 1; f < n_frames; ++f) {
+    launch_frame_begin(L, st, f);
+    launch_bilateral(L, p->frames.p + P * f, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
+    if (p->levels > 1) launch_downsample(L, p->pyr0.p, p->pyr1.p, W, H, 0.03);
+    if (p->levels > 2) launch_downsample(L, p->pyr1.p, p->pyr2.p, W / 2, H / 2, 0.03);
+    for (int li = 0; li < p->levels; ++li) {
+      const int level = p->levels - 1 - li;
+      const int wl = W >> level, hl = H >> level;
+      const double* kl = p->intr_levels.p + level * 4 * C;
+      launch_level_begin(L, st, p->pose.p, p->pred_pose.p, p->Dp);
+      raycast_dev(v, p->pred_pose.p, kl, wl, hl, cfg.rc, p->vre.p, p->nre.p, p->vim.p, p->nim.p);
+      const int stride = std::max(1, cfg.icp.level_pixel_stride[li]);
+      const int tiles = icp_tiles(wl, hl, stride);
+      for (int it = 0; it < cfg.icp.level_iterations[li]; ++it) {
+        launch_icp_reduce(L, p->G, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p, p->vim.p,
+                          p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p);
+        launch_icp_solve(L, p->G, p->Dp, st, p->partials.p, p->counts.p, tiles, p->pose.p, level,
+                         cfg.icp.step_tolerance);
+      }
+    }
+    rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p);
+    if (rc) return rc;
+    launch_frame_end(L, st, p->pose.p, p->traj.p, p->Dp, p->stats.p, nblk, counters);
+  }
+  launch_objective(L, p->G, p->Dp, p->D, p->traj.p, p->gt.p, n_frames, cfg.objective, cfg.h, p->out.p);
+  p->n_run = n_frames;
+  CUDA_TRY(ctx, cudaGetLastError());
+  return CSF_OK;
+}
+
+extern "C" int csf_pipeline_result(csf_pipeline p, double* gradient, double* objective, double* poses,
+                                   int32_t* stats) {
+  if (!p) return CSF_EINVAL;
+  csf_ctx ctx = p->ctx;
+  cudaSetDevice(ctx->device);
+  int rc = sync_check(ctx, "csf_pipeline_run");
+  if (rc) return rc;
+  std::vector<double> out(2 + CSF_MAX_DIRECTIONS);
+  CUDA_TRY(ctx, cudaMemcpy(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
+  if (objective) *objective = out[0];
+  if (gradient)
+    for (int d = 0; d < p->D; ++d) gradient[d] = out[2 + d];
+  const int n = p->n_run;
+  if (poses) {
+    std::vector<double> t(static_cast<size_t>(n) * 12 * p->C);
+    CUDA_TRY(ctx, cudaMemcpy(t.data(), p->traj.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost));
+    const int Cu = 1 + p->D;
+    for (int f = 0; f < n; ++f)
+      for (int e = 0; e < 12; ++e)
+        for (int c = 0; c < Cu; ++c)
+          poses[(static_cast<size_t>(f) * 12 + e) * Cu + c] = t[(static_cast<size_t>(f) * 12 + e) * p->C + c];
+  }
+  if (stats) CUDA_TRY(ctx, cudaMemcpy(stats, p->stats.p, sizeof(int) * 8 * n, cudaMemcpyDeviceToHost));
+  return CSF_OK;
+}
+
+extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames,
+                                     double* gradient, double* objective) {
+  int rc = csf_pipeline_upload(p, depth, gt, n_frames);
+  if (rc) return rc;
+  rc = csf_pipeline_run(p, n_frames);
+  if (rc) return rc;
+  return csf_pipeline_result(p, gradient, objective, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// track_frame (real tracker on the device)
+// ---------------------------------------------------------------------------
+extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, const double* init_pose,
+                               const csf_intrinsics* k, const csf_icp_cfg* cfg_in, double* out_pose,
+                               csf_track_result* result) {
+  if (!v || !depth || !init_pose || !k || !out_pose) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  csf_icp_cfg cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    csf_default_icp_cfg(&cfg);
+  if (cfg.solver != CSF_SOLVER_LINEARIZED)
+    return fail(ctx, CSF_EINVAL, "csf_track_frame: the device tracker implements the linearized solver");
+  cudaSetDevice(ctx->device);
+  const int levels = std::clamp(cfg.levels, 1, 3);
+  const size_t P = static_cast<size_t>(w) * h;
+  DevBuf<double> dd, raw, pyr0, pyr1, pyr2, vre, nre, pose, pred, intr, partials;
+  DevBuf<int> counts;
+  DevBuf<TrackState> st;
+  const int tiles_max = icp_tiles(w, h, 1);
+  CUDA_TRY(ctx, dd.alloc(P));
+  CUDA_TRY(ctx, raw.alloc(P));
+  CUDA_TRY(ctx, pyr0.alloc(P));
+  CUDA_TRY(ctx, pyr1.alloc(P / 4 + 1));
+  CUDA_TRY(ctx, pyr2.alloc(P / 16 + 1));
+  CUDA_TRY(ctx, vre.alloc(P * 3));
+  CUDA_TRY(ctx, nre.alloc(P * 3));
+  CUDA_TRY(ctx, pose.alloc(12));
+  CUDA_TRY(ctx, pred.alloc(12));
+  CUDA_TRY(ctx, intr.alloc(12));
+  CUDA_TRY(ctx, partials.alloc(static_cast<size_t>(tiles_max) * 27));
+  CUDA_TRY(ctx, counts.alloc(tiles_max));
+  CUDA_TRY(ctx, st.alloc(1));
+  double kl[12];
+  for (int l = 0; l < 3; ++l) {
+    const double s = static_cast<double>(1 << l);
+    kl[4 * l] = k->fx / s;
+    kl[4 * l + 1] = k->fy / s;
+    kl[4 * l + 2] = k->cx / s;
+    kl[4 * l + 3] = k->cy / s;
+  }
+  const Launch L = launch_of(ctx);
+  CUDA_TRY(ctx, cudaMemcpyAsync(dd.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(pose.p, init_pose, sizeof(double) * 12, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(intr.p, kl, sizeof(kl), cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemsetAsync(st.p, 0, sizeof(TrackState), ctx->stream));
+  const double cos_max = csf_det::cos(cfg.theta_max_deg * M_PI / 180.0);
+  launch_bilateral(L, nullptr, dd.p, raw.p, pyr0.p, w, h, 4.5, 0.03, 3);
+  if (levels > 1) launch_downsample(L, pyr0.p, pyr1.p, w, h, 0.03);
+  if (levels > 2) launch_downsample(L, pyr1.p, pyr2.p, w / 2, h / 2, 0.03);
+  double* pyr[3] = {pyr0.p, pyr1.p, pyr2.p};
+  // The volume's real channel only: a G = 0 view over its voxel store.
+  csf_volume_s real_view;
+  real_view.ctx = ctx;
+  real_view.hashed = v->hashed;
+  real_view.D = 0;
+  real_view.G = 0;
+  real_view.Dp = 0;  // pose/intrinsics buffers carry the real channel only
+  real_view.dense = v->dense;
+  real_view.hash = v->hash;
+  csf_raycast_cfg rcfg;
+  csf_default_raycast_cfg(&rcfg);
+  int tiles_last = 0;
+  for (int li = 0; li < levels; ++li) {
+    const int level = levels - 1 - li;
+    const int wl = w >> level, hl = h >> level;
+    launch_level_begin(L, st.p, pose.p, pred.p, 0);
+    raycast_dev(&real_view, pred.p, intr.p + 4 * level, wl, hl, rcfg, vre.p, nre.p, nullptr, nullptr);
+    const int stride = std::max(1, cfg.level_pixel_stride[li]);
+    tiles_last = icp_tiles(wl, hl, stride);
+    for (int it = 0; it < cfg.level_iterations[li]; ++it) {
+      launch_icp_reduce(L, 0, 0, st.p, pyr[level], wl, hl, stride, intr.p + 4 * level, pose.p, vre.p, nre.p, nullptr,
+                        nullptr, cfg.d_max, cos_max, partials.p, counts.p);
+      launch_icp_solve(L, 0, 0, st.p, partials.p, counts.p, tiles_last, pose.p, level, cfg.step_tolerance);
+    }
+  }
+  TrackState hs;
+  CUDA_TRY(ctx, cudaMemcpyAsync(out_pose, pose.p, sizeof(double) * 12, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(&hs, st.p, sizeof(TrackState), cudaMemcpyDeviceToHost, ctx->stream));
+  const int rc = sync_check(ctx, "csf_track_frame");
+  if (rc) return rc;
+  if (result) {
+    result->iterations = hs.iterations;
+    result->converged = hs.converged;
+    result->correspondences = hs.n_corr;
+    result->final_loss = std::nan("");  // loss_after is not evaluated by the device tracker
+  }
+  return CSF_OK;
+}
+
+extern "C" int csf_synth_workload(csf_ctx ctx, int config, int n_frames, int width, int height, float* depth,
+                                  double* gt, csf_intrinsics* k) {
+  if (!ctx || !depth || !gt || n_frames <= 0) return CSF_EINVAL;
+  cudaSetDevice(ctx->device);
+  std::string err;
+  const int rc = synth_workload(ctx->stream, config, n_frames, width, height, depth, gt, k, &err);
+  ctx->launches += 1;
+  if (rc) return fail(ctx, rc, err);
+  return CSF_OK;
+}

@@ -1,0 +1,115 @@
+// Internal interface between the C-ABI layer (capi.cu) and the kernel
+// translation units.  Plain structs of device pointers; no torch types.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace csfi {
+
+// Channel-group widths with instantiated kernels.  A run with D directions
+// uses the group width G chosen by pick_group(D) and stores Dp = ceil(D/G)*G
+// channels (padding channels stay zero).
+int pick_group(int D);
+inline int padded_channels(int D, int G) { return G == 0 ? 0 : ((D + G - 1) / G) * G; }
+
+struct DenseDev {
+  double2* rw;   // [n] (F.re, W)
+  double* fim;   // [n][Dp]
+  int nx, ny, nz;
+  double vs, ox, oy, oz, mu, cap;
+};
+
+struct HashDev {
+  double2* rw;                  // [max_blocks*512]
+  double* fim;                  // [max_blocks*512][Dp]
+  int* heads;                   // [2^bits]
+  unsigned long long* keys;     // [max_blocks]
+  int* next;                    // [max_blocks]
+  int* coords;                  // [max_blocks][3]
+  int* n_blocks;                // device counter
+  int bits, max_blocks;
+  double vs, ox, oy, oz, mu, cap;
+};
+
+// Per-frame allocation scratch (hashed volumes).
+struct AllocScratch {
+  unsigned long long* cand;     // [P*K] candidate keys (kEmptyKey = none)
+  int* cand_block;              // [P*K] existing block id or -1
+  int* first_flag;              // [P*K]
+  int* new_flag;                // [P*K]
+  int* first_rank;              // [P*K]
+  int* new_rank;                // [P*K]
+  unsigned long long* set_keys; // [set_cap]
+  int* set_first;               // [set_cap]
+  int* set_slot;                // [P*K] set index of the candidate
+  int set_bits;
+  int* visible;                 // [max visible] block ids
+  int* counters;                // [4]: n_visible, n_new, overflow, spare
+  void* cub_tmp;
+  size_t cub_tmp_bytes;
+  int max_cand;                 // P*K
+};
+
+// Tracker state (device)
+struct TrackState {
+  int level_done;
+  int converged;
+  int iterations;
+  int n_corr;
+  int frame;
+  int err;
+  int pad[2];
+  double pred_w2c[12];  // real inverse of the prediction pose (association)
+  double cur_c2w[12];   // real current pose snapshot (unused by kernels)
+};
+
+struct Launch {
+  cudaStream_t stream;
+  int* err;                // device error flag
+  unsigned long long* launches;  // host counter of kernels launched
+};
+
+// ---- frames.cu
+void launch_bilateral(const Launch& L, const float* in_f32, const double* in_f64, double* raw_out, double* out, int w,
+                      int h, double sigma_s, double sigma_r, int radius);
+void launch_downsample(const Launch& L, const double* in, double* out, int w, int h, double sigma_r);
+void launch_measure(const Launch& L, const double* depth, int w, int h, const double* intr, int D, double* vert,
+                    double* norm);
+
+// ---- volume.cu
+void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* depth, int w, int h,
+                            const double* pose, const double* intr);
+void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, const AllocScratch& a,
+                             const double* depth, int w, int h, const double* pose, const double* intr);
+void launch_allocate(const Launch& L, const HashDev& v, int Dp, AllocScratch& a, const double* depth, int w, int h,
+                     const double* pose, const double* intr);
+void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* pose, const double* intr,
+                          int w, int h, double near_clip, double far_clip, double step, double* vre, double* nre,
+                          double* vim, double* nim);
+void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, const double* pose, const double* intr,
+                           int w, int h, double near_clip, double far_clip, double step, double* vre, double* nre,
+                           double* vim, double* nim);
+void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp);
+
+// ---- icp.cu
+void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp);
+int icp_tiles(int w, int h, int stride);
+void launch_icp_reduce(const Launch& L, int G, int Dp, const TrackState* st, const double* depth, int w, int h,
+                       int stride, const double* intr, const double* pose, const double* vre, const double* nre,
+                       const double* vim, const double* nim, double d_max, double cos_max, double* partials,
+                       int* counts);
+void launch_icp_solve(const Launch& L, int G, int Dp, TrackState* st, const double* partials, const int* counts,
+                      int n_tiles, double* pose, int level, double tol);
+void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,
+                 const double* intr_base, double* pose, double* intr_levels, int levels);
+void launch_frame_begin(const Launch& L, TrackState* st, int frame);
+void launch_frame_end(const Launch& L, TrackState* st, const double* pose, double* traj, int Dp, int* stats,
+                      const int* n_blocks, const int* counters);
+void launch_objective(const Launch& L, int G, int Dp, int D, const double* traj, const double* gt, int n_frames,
+                      int kind, double h, double* out /*[2 + D]: objective re, pad, grad*/);
+void launch_linearized_corrs(const Launch& L, const double* corrs, int n, const double* base, double* partials,
+                             int* counts);
+
+}  // namespace csfi

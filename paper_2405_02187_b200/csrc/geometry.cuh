@@ -1,0 +1,270 @@
+// Device TSDF geometry: volume views (dense / hashed voxel blocks), projective
+// measurement, trilinear sampling, and the 6x6 LDLT — generic over the scalar
+// S (double or a channel group L<G>).  Each function names the reference
+// function it re-implements; the evaluation order is the oracle's
+// (oracle/orc_tsdf.hpp, oracle/orc_icp.hpp).
+#pragma once
+
+#include "lifted.cuh"
+
+namespace csfd {
+
+constexpr int kBlockVoxels = 512;
+constexpr int kCoordBias = 1 << 20;
+constexpr unsigned long long kEmptyKey = ~0ULL;
+
+CSF_DEV unsigned long long block_key(int bx, int by, int bz) {
+  return (static_cast<unsigned long long>(static_cast<unsigned>(bx + kCoordBias)) << 42) |
+         (static_cast<unsigned long long>(static_cast<unsigned>(by + kCoordBias)) << 21) |
+         static_cast<unsigned long long>(static_cast<unsigned>(bz + kCoordBias));
+}
+CSF_DEV unsigned block_hash(int bx, int by, int bz, unsigned mask) {
+  return ((static_cast<unsigned>(bx) * 73856093u) ^ (static_cast<unsigned>(by) * 19349669u) ^
+          (static_cast<unsigned>(bz) * 83492791u)) & mask;
+}
+
+// Voxel storage shared by both volume kinds: rw[v] = (F.re, W) and the
+// perturbation channels fim[v*Dp + d] (voxel-major, channel-minor).
+struct VoxelStore {
+  double2* rw;
+  double* fim;
+  int Dp;
+};
+
+// Dense lattice (tsdf.hpp:38-78): index (k*ny + j)*nx + i.
+struct DenseView {
+  VoxelStore vox;
+  int nx, ny, nz;
+  double vs, ox, oy, oz, mu, cap;
+  static constexpr bool kHashed = false;
+  CSF_DEV bool cell_in_grid(int i0, int j0, int k0) const {
+    return !(i0 < 0 || j0 < 0 || k0 < 0 || i0 + 1 >= nx || j0 + 1 >= ny || k0 + 1 >= nz);
+  }
+  // returns the voxel index or -1
+  CSF_DEV long long voxel(int i, int j, int k) const {
+    return (static_cast<long long>(k) * ny + j) * nx + i;
+  }
+};
+
+// Hashed 8^3 blocks: chained buckets, chains sorted by key (builder-defined;
+// oracle/orc_tsdf.hpp HashedVolumeT).
+struct HashView {
+  VoxelStore vox;
+  const int* heads;
+  const unsigned long long* keys;
+  const int* next;
+  unsigned mask;
+  double vs, ox, oy, oz, mu, cap;
+  static constexpr bool kHashed = true;
+  CSF_DEV bool cell_in_grid(int, int, int) const { return true; }
+  CSF_DEV int find(int bx, int by, int bz) const {
+    const unsigned long long key = block_key(bx, by, bz);
+    int e = __ldg(heads + block_hash(bx, by, bz, mask));
+    while (e >= 0) {
+      const unsigned long long k = __ldg(keys + e);
+      if (k == key) return e;
+      if (k > key) return -1;
+      e = __ldg(next + e);
+    }
+    return -1;
+  }
+  CSF_DEV long long voxel(int i, int j, int k) const {
+    const int b = find(i >> 3, j >> 3, k >> 3);
+    if (b < 0) return -1;
+    return static_cast<long long>(b) * kBlockVoxels + (((k & 7) * 8 + (j & 7)) * 8 + (i & 7));
+  }
+};
+
+// Stored field value of voxel v as S (channel group g0).
+template <typename S> CSF_DEV S field_at(const VoxelStore& vs, long long v, double fre, int g0);
+template <> CSF_DEV double field_at<double>(const VoxelStore&, long long, double fre, int) { return fre; }
+template <typename S> CSF_DEV S field_at(const VoxelStore& vs, long long v, double fre, int g0) {
+  S o;
+  o.re = fre;
+  const double* p = vs.fim + v * vs.Dp + g0;
+#pragma unroll
+  for (int g = 0; g < Traits<S>::G; ++g) o.im[g] = p[g];
+  return o;
+}
+
+// sample_tsdf (tsdf.hpp:148-177): all 8 corners must exist with W > 0.
+template <typename S, typename V>
+CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out) {
+  const S gx = (p.v[0] - vol.ox) / vol.vs;
+  const S gy = (p.v[1] - vol.oy) / vol.vs;
+  const S gz = (p.v[2] - vol.oz) / vol.vs;
+  const int i0 = ifloor(re(gx)), j0 = ifloor(re(gy)), k0 = ifloor(re(gz));
+  if (!vol.cell_in_grid(i0, j0, k0)) return false;
+  const S fx = gx - static_cast<double>(i0);
+  const S fy = gy - static_cast<double>(j0);
+  const S fz = gz - static_cast<double>(k0);
+  S accum = lit<S>(0.0);
+#pragma unroll
+  for (int dk = 0; dk < 2; ++dk)
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+      for (int di = 0; di < 2; ++di) {
+        const long long v = vol.voxel(i0 + di, j0 + dj, k0 + dk);
+        if (v < 0) return false;
+        const double2 rw = vol.vox.rw[v];
+        if (!(rw.y > 0.0)) return false;
+        const S wx = di ? fx : 1.0 - fx;
+        const S wy = dj ? fy : 1.0 - fy;
+        const S wz = dk ? fz : 1.0 - fz;
+        accum = accum + ((wx * wy) * wz) * field_at<S>(vol.vox, v, rw.x, g0);
+      }
+  *out = accum;
+  return true;
+}
+
+// sample_gradient (tsdf.hpp:181-196)
+template <typename S, typename V>
+CSF_DEV bool sample_gradient(const V& vol, const V3<S>& p, int g0, V3<S>* g) {
+  const double h = vol.vs;
+#pragma unroll
+  for (int axis = 0; axis < 3; ++axis) {
+    V3<S> lo = p, hi = p;
+    lo.v[axis] = lo.v[axis] - h;
+    hi.v[axis] = hi.v[axis] + h;
+    S flo, fhi;
+    if (!sample_tsdf<S>(vol, lo, g0, &flo)) return false;
+    if (!sample_tsdf<S>(vol, hi, g0, &fhi)) return false;
+    g->v[axis] = (fhi - flo) / (2.0 * h);
+  }
+  return true;
+}
+
+// Lifted intrinsics of one pyramid level.
+template <typename S> struct Intr {
+  S fx, fy, cx, cy;
+  int w, h;
+};
+
+// measured_tsdf (tsdf.hpp:97-140) against an unperturbed depth image.
+template <typename S>
+CSF_DEV bool measured_tsdf(const double* depth, int w, int h, const Pose<S>& w2c, const Intr<S>& k, double mu,
+                           double px, double py, double pz, const V3<S>& center, S* psi) {
+  V3<S> pc;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    pc.v[r] = sum3(w2c.R.m[3 * r] * px, w2c.R.m[3 * r + 1] * py, w2c.R.m[3 * r + 2] * pz) + w2c.t.v[r];
+  if (!(re(pc.v[2]) > 0.0)) return false;
+  const S lx = (k.fx * pc.v[0]) / pc.v[2] + k.cx;
+  const S ly = (k.fy * pc.v[1]) / pc.v[2] + k.cy;
+  const int x0 = ifloor(re(lx)), y0 = ifloor(re(ly));
+  if (x0 < 0 || y0 < 0 || x0 + 1 >= w || y0 + 1 >= h) return false;
+  const double d00 = depth[y0 * w + x0];
+  const double d10 = depth[y0 * w + x0 + 1];
+  const double d01 = depth[(y0 + 1) * w + x0];
+  const double d11 = depth[(y0 + 1) * w + x0 + 1];
+  if (!(d00 > 0.0) || !(d10 > 0.0) || !(d01 > 0.0) || !(d11 > 0.0)) return false;
+  const double nearv = fmin(fmin(d00, d10), fmin(d01, d11));
+  const double farv = fmax(fmax(d00, d10), fmax(d01, d11));
+  if (farv - nearv > 0.1) return false;
+  const S fx = lx - static_cast<double>(x0);
+  const S fy = ly - static_cast<double>(y0);
+  const S top = d00 + fx * (d10 - d00);
+  const S bot = d01 + fx * (d11 - d01);
+  const S sampled = top + fy * (bot - top);
+  const S rx = (lx - k.cx) / k.fx;
+  const S ry = (ly - k.cy) / k.fy;
+  const S one = lit<S>(1.0);
+  const S lambda = sqrt_s(sum3(rx * rx, ry * ry, one * one));
+  const S dx = center.v[0] - px, dy = center.v[1] - py, dz = center.v[2] - pz;
+  const S eta = sampled - sqrt_s(sum3(dx * dx, dy * dy, dz * dz)) / lambda;
+  if (re(eta) < -mu) return false;
+  *psi = clamp_s(eta / mu, -1.0, 1.0);
+  return true;
+}
+
+// ----------------------------------------------------------------------------
+// Ldlt6 — the oracle's restatement of Eigen::LDLT<Mat6d> (oracle/orc_icp.hpp)
+// ----------------------------------------------------------------------------
+CSF_DEV int tri(int r, int c) { return r * (r + 1) / 2 + c; }
+
+template <typename S> CSF_DEV void swap_s(S& a, S& b) {
+  const S t = a;
+  a = b;
+  b = t;
+}
+template <typename S> CSF_DEV double absre(const S& x) { return fabs(re(x)); }
+
+// Factor the symmetric matrix given by its lower triangle and solve A x = rhs.
+// Returns false when Eigen would report info() != Success.
+template <typename S>
+CSF_DEV bool ldlt6_solve(const S* a_lower, const S* rhs, S* dst) {
+  S m[6][6];
+  int transp[6];
+  bool ok = true;
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) m[r][c] = r >= c ? a_lower[tri(r, c)] : a_lower[tri(c, r)];
+  S temp[6];
+  for (int k = 0; k < 6; ++k) {
+    int piv = k;
+    double best = absre(m[k][k]);
+    for (int i = k + 1; i < 6; ++i)
+      if (absre(m[i][i]) > best) {
+        best = absre(m[i][i]);
+        piv = i;
+      }
+    transp[k] = piv;
+    if (piv != k) {
+      for (int j = 0; j < k; ++j) swap_s(m[k][j], m[piv][j]);
+      for (int i = piv + 1; i < 6; ++i) swap_s(m[i][k], m[i][piv]);
+      swap_s(m[k][k], m[piv][piv]);
+      for (int i = k + 1; i < piv; ++i) {
+        const S tmp = m[i][k];
+        m[i][k] = m[piv][i];
+        m[piv][i] = tmp;
+      }
+    }
+    if (k > 0) {
+      for (int j = 0; j < k; ++j) temp[j] = m[j][j] * m[k][j];
+      S s = m[k][0] * temp[0];
+      for (int j = 1; j < k; ++j) s = s + m[k][j] * temp[j];
+      m[k][k] = m[k][k] - s;
+      for (int i = k + 1; i < 6; ++i) {
+        S si = m[i][0] * temp[0];
+        for (int j = 1; j < k; ++j) si = si + m[i][j] * temp[j];
+        m[i][k] = m[i][k] - si;
+      }
+    }
+    const S akk = m[k][k];
+    const bool pivot_valid = absre(akk) > 0.0;
+    if (k == 0 && !pivot_valid) {
+      ok = false;
+      for (int j = 0; j < 6; ++j) transp[j] = j;
+      break;
+    }
+    if (k < 5) {
+      if (pivot_valid) {
+        for (int i = k + 1; i < 6; ++i) m[i][k] = m[i][k] / akk;
+      } else {
+        for (int i = k + 1; i < 6; ++i) ok = ok && re(m[i][k]) == 0.0;
+      }
+    }
+  }
+  for (int i = 0; i < 6; ++i) dst[i] = rhs[i];
+  for (int k = 0; k < 6; ++k) swap_s(dst[k], dst[transp[k]]);
+  for (int i = 0; i < 6; ++i)
+    for (int j = i + 1; j < 6; ++j) dst[j] = dst[j] - dst[i] * m[j][i];
+  const double tol = 2.2250738585072014e-308;  // numeric_limits<double>::min()
+  for (int i = 0; i < 6; ++i) {
+    if (absre(m[i][i]) > tol)
+      dst[i] = dst[i] / m[i][i];
+    else
+      dst[i] = lit<S>(0.0);
+  }
+  for (int i = 4; i >= 0; --i) {
+    S s = m[i + 1][i] * dst[i + 1];
+    for (int j = i + 2; j < 6; ++j) s = s + m[j][i] * dst[j];
+    dst[i] = dst[i] - s;
+  }
+  for (int k = 5; k >= 0; --k) swap_s(dst[k], dst[transp[k]]);
+  return ok;
+}
+
+}  // namespace csfd

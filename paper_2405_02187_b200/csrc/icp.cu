@@ -1,0 +1,485 @@
+// Lifted point-to-plane ICP for sm_100a.
+//
+//   associate          — proj/src/icp.cpp:89-126 (real-part gates, scan order)
+//   normal_equations   — proj/src/icp.cpp:15-28 (J = [n; p x n], r), lifted
+//   LDLT solve         — Eigen::LDLT<Mat6d>(a).solve(-b), icp.cpp:43,151
+//   apply_increment    — proj/include/csf/se3.hpp:116-119
+//   track_frame loop   — proj/src/icp.cpp:185-240 (break rules)
+//
+// One ICP iteration is two launches:
+//   k_icp_reduce: one CTA per tile of 256 slots (the strided pixel grid in
+//     row-major order).  Measured vertex/normal are recomputed from the
+//     pyramid depth, gated on real parts, compacted in slot order into shared
+//     memory as lifted (J, r) rows, and summed sequentially per accumulator —
+//     the canonical "slot-tiled" order the oracle restates.
+//   k_icp_solve: one CTA sums the tile partials in tile order, then one
+//     thread per channel group runs the 6x6 LDLT, the exp map and the pose
+//     update in L<G> arithmetic.  Break decisions are written to TrackState so
+//     the whole level stays on the device (no host round trip).
+#include <cstdio>
+
+#include "csf_internal.h"
+#include "geometry.cuh"
+
+namespace csfd {
+
+using csfi::TrackState;
+constexpr int kTile = 256;
+__constant__ int c_tri_r[21] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5, 5, 5, 5};
+__constant__ int c_tri_c[21] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2, 3, 4, 5};
+
+CSF_DEV void load_pose_real(const double* p, int C, Pose<double>* out) {
+#pragma unroll
+  for (int e = 0; e < 9; ++e) out->R.m[e] = p[e * C];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) out->t.v[e] = p[(9 + e) * C];
+}
+
+// Real measured vertex at (x, y) (frames.hpp:38-41 via measure_surface).
+CSF_DEV bool vertex_at(const double* depth, int w, int x, int y, double fx, double fy, double cx, double cy,
+                       V3<double>* v) {
+  const double d = depth[y * w + x];
+  if (!(d > 0.0)) return false;
+  *v = mk3<double>(d * (static_cast<double>(x) - cx) / fx, d * (static_cast<double>(y) - cy) / fy, d);
+  return true;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* __restrict__ st, const double* __restrict__ depth,
+                                                    int w, int h, int stride, const double* __restrict__ intr,
+                                                    const double* __restrict__ pose, const double* __restrict__ vre,
+                                                    const double* __restrict__ nre, const double* __restrict__ vim,
+                                                    const double* __restrict__ nim, double d_max, double cos_max,
+                                                    int Dp, int chunk, double* __restrict__ partials,
+                                                    int* __restrict__ counts) {
+  if (st->level_done) return;
+  using S = Scal<G>;
+  extern __shared__ double sm[];
+  const int C = 1 + Dp;
+  double* s_pose = sm;
+  double* s_intr = s_pose + 12 * C;
+  double* s_jr = s_intr + 4 * C;
+  __shared__ int s_wsum[8];
+  __shared__ int s_total;
+  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) s_pose[i] = pose[i];
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_intr[i] = intr[i];
+  __syncthreads();
+
+  Pose<double> c2w, w2p;
+  load_pose_real(s_pose, C, &c2w);
+#pragma unroll
+  for (int e = 0; e < 9; ++e) w2p.R.m[e] = st->pred_w2c[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) w2p.t.v[e] = st->pred_w2c[9 + e];
+  const double fx = s_intr[0], fy = s_intr[C], cx = s_intr[2 * C], cy = s_intr[3 * C];
+  const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
+  const int n_slots = nxs * nys;
+  const int n_acc = 27 * C;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int tile_count = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (int cbase = 0; cbase < kTile; cbase += chunk) {
+    const int slot = blockIdx.x * kTile + cbase + threadIdx.x;
+    bool corr = false;
+    int x = 0, y = 0, u = 0, v = 0;
+    if (threadIdx.x < chunk && slot < n_slots) {
+      x = (slot % nxs) * stride;
+      y = (slot / nxs) * stride;
+      V3<double> vert, vx, vy;
+      if (vertex_at(depth, w, x, y, fx, fy, cx, cy, &vert) && x + 1 < w && y + 1 < h &&
+          vertex_at(depth, w, x + 1, y, fx, fy, cx, cy, &vx) && vertex_at(depth, w, x, y + 1, fx, fy, cx, cy, &vy)) {
+        V3<double> n = cross3(sub3(vx, vert), sub3(vy, vert));
+        const double len2 = dot3(n, n);
+        if (len2 > 0.0) {
+          const double l = sqrt(len2);
+          n = mk3<double>(n.v[0] / l, n.v[1] / l, n.v[2] / l);
+          if (dot3(n, vert) > 0.0) n = mk3<double>(-n.v[0], -n.v[1], -n.v[2]);
+          if (dot3(n, n) > 0.5) {
+            const V3<double> world = apply(c2w, vert);
+            const V3<double> inp = apply(w2p, world);
+            if (inp.v[2] > 0.0) {
+              const double uvx = (fx * inp.v[0]) / inp.v[2] + cx;
+              const double uvy = (fy * inp.v[1]) / inp.v[2] + cy;
+              u = static_cast<int>(lround(uvx));
+              v = static_cast<int>(lround(uvy));
+              if (u >= 0 && u < w && v >= 0 && v < h) {
+                const long long m = static_cast<long long>(v) * w + u;
+                const V3<double> mn = mk3<double>(nre[3 * m], nre[3 * m + 1], nre[3 * m + 2]);
+                if (dot3(mn, mn) > 0.5) {
+                  const V3<double> mv = mk3<double>(vre[3 * m], vre[3 * m + 1], vre[3 * m + 2]);
+                  const V3<double> dd = sub3(world, mv);
+                  if (!(sqrt(dot3(dd, dd)) > d_max)) {
+                    const V3<double> wn = matvec(c2w.R, n);
+                    corr = !(dot3(wn, mn) < cos_max);
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    // order-preserving compaction within the chunk
+    const unsigned ballot = __ballot_sync(0xffffffffu, corr);
+    if (lane == 0) s_wsum[warp] = __popc(ballot);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int k = 0; k < 8; ++k) {
+      if (k < warp) before += s_wsum[k];
+      total += s_wsum[k];
+    }
+    const int pos = before + __popc(ballot & ((1u << lane) - 1u));
+    if (corr) {
+      const long long m = static_cast<long long>(v) * w + u;
+      double* row = s_jr + static_cast<long long>(pos) * 7 * C;
+      const int passes = G == 0 ? 1 : Dp / G;
+      for (int gi = 0; gi < passes; ++gi) {
+        const int g0 = gi * G;
+        Pose<S> base;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) base.R.m[e] = load_ch<S>(s_pose + e * C, g0, G);
+#pragma unroll
+        for (int e = 0; e < 3; ++e) base.t.v[e] = load_ch<S>(s_pose + (9 + e) * C, g0, G);
+        const S kfx = load_ch<S>(s_intr, g0, G), kfy = load_ch<S>(s_intr + C, g0, G);
+        const S kcx = load_ch<S>(s_intr + 2 * C, g0, G), kcy = load_ch<S>(s_intr + 3 * C, g0, G);
+        const double d = depth[y * w + x];
+        const V3<S> vert = mk3<S>((d * (static_cast<double>(x) - kcx)) / kfx, (d * (static_cast<double>(y) - kcy)) / kfy,
+                                  lit<S>(d));
+        V3<S> mv, mn;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if constexpr (G == 0) {
+            mv.v[c] = vre[3 * m + c];
+            mn.v[c] = nre[3 * m + c];
+          } else {
+            mv.v[c].re = vre[3 * m + c];
+            mn.v[c].re = nre[3 * m + c];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              mv.v[c].im[g] = vim[(3 * m + c) * Dp + g0 + g];
+              mn.v[c].im[g] = nim[(3 * m + c) * Dp + g0 + g];
+            }
+          }
+        }
+        const V3<S> p = apply(base, vert);
+        const S r = dot3(sub3(p, mv), mn);
+        const V3<S> pn = cross3(p, mn);
+        const S jr[7] = {mn.v[0], mn.v[1], mn.v[2], pn.v[0], pn.v[1], pn.v[2], r};
+#pragma unroll
+        for (int q = 0; q < 7; ++q) store_ch<S>(row + q * C, jr[q], g0, G, gi == 0);
+      }
+    }
+    __syncthreads();
+    // per-accumulator sequential sums in slot order
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int a = threadIdx.x + 256 * j;
+      if (a >= n_acc) break;
+      const int q = a / C, c = a % C;
+      int ja, jb;
+      if (q < 21) {
+        ja = c_tri_r[q];
+        jb = c_tri_c[q];
+      } else {
+        ja = q - 21;
+        jb = 6;
+      }
+      double s = acc[j];
+      for (int e = 0; e < total; ++e) {
+        const double* row = s_jr + static_cast<long long>(e) * 7 * C;
+        const double are = row[ja * C], bre = row[jb * C];
+        const double term = c == 0 ? are * bre : are * row[jb * C + c] + row[ja * C + c] * bre;
+        s = s + term;
+      }
+      acc[j] = s;
+    }
+    tile_count += total;
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int a = threadIdx.x + 256 * j;
+    if (a < n_acc) partials[static_cast<long long>(blockIdx.x) * n_acc + a] = acc[j];
+  }
+  if (threadIdx.x == 0) counts[blockIdx.x] = tile_count;
+}
+
+template <int G>
+__global__ void __launch_bounds__(512) k_icp_solve(TrackState* st, const double* __restrict__ partials,
+                                                   const int* __restrict__ counts, int n_tiles, double* pose, int Dp,
+                                                   int level, double tol) {
+  if (st->level_done) return;
+  using S = Scal<G>;
+  extern __shared__ double sm[];
+  __shared__ int s_n, s_finite;
+  const int C = 1 + Dp;
+  const int n_acc = 27 * C;
+  for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
+    double total = 0.0;
+    for (int t = 0; t < n_tiles; ++t) total = total + partials[static_cast<long long>(t) * n_acc + a];
+    sm[a] = total;
+  }
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int t = 0; t < n_tiles; ++t) n += counts[t];
+    s_n = n;
+    s_finite = 1;
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (n < 12) {
+    if (threadIdx.x == 0) {
+      st->n_corr = n;
+      st->level_done = 1;
+    }
+    return;
+  }
+  const int ngroups = G == 0 ? 1 : Dp / G;
+  const bool mine = static_cast<int>(threadIdx.x) < ngroups;
+  const int g0 = threadIdx.x * G;
+  S d[6];
+  if (mine) {
+    S a[21], nb[6];
+#pragma unroll
+    for (int q = 0; q < 21; ++q) a[q] = load_ch<S>(sm + q * C, g0, G);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) nb[i] = -load_ch<S>(sm + (21 + i) * C, g0, G);
+    ldlt6_solve<S>(a, nb, d);
+    bool fin = true;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) fin = fin && finite_s(d[i]);
+    if (!fin) atomicAnd(&s_finite, 0);
+  }
+  __syncthreads();
+  Pose<S> np;
+  if (mine) {
+    if (!s_finite)
+#pragma unroll
+      for (int i = 0; i < 6; ++i) d[i] = lit<S>(0.0);
+    Pose<S> cur;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
+    np = compose(exp_map<S>(d), cur);
+  }
+  __syncthreads();
+  if (mine) {
+#pragma unroll
+    for (int e = 0; e < 9; ++e) store_ch<S>(pose + e * C, np.R.m[e], g0, G, threadIdx.x == 0);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) store_ch<S>(pose + (9 + e) * C, np.t.v[e], g0, G, threadIdx.x == 0);
+  }
+  if (threadIdx.x == 0) {
+    double sq[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) sq[i] = re(d[i]) * re(d[i]);
+    const double nrm = sqrt((sq[0] + (sq[1] + sq[2])) + (sq[3] + (sq[4] + sq[5])));
+    st->iterations += 1;
+    st->n_corr = n;
+    if (nrm < tol) {
+      st->level_done = 1;
+      if (level == 0) st->converged = 1;
+    }
+  }
+}
+
+// Level entry: the prediction pose is the current estimate (icp.cpp:191).
+__global__ void k_level_begin(TrackState* st, const double* pose, double* pred_pose, int Dp) {
+  const int C = 1 + Dp;
+  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) pred_pose[i] = pose[i];
+  if (threadIdx.x == 0) {
+    Pose<double> p;
+    load_pose_real(pose, C, &p);
+    const Pose<double> inv = inverse(p);
+    for (int e = 0; e < 9; ++e) st->pred_w2c[e] = inv.R.m[e];
+    for (int e = 0; e < 3; ++e) st->pred_w2c[9 + e] = inv.t.v[e];
+    st->level_done = 0;
+  }
+}
+
+// Seeds: first-frame twist xi0* and intrinsics channels; T0* = exp(xi0*) T0.
+template <int G>
+__global__ void k_seed(const int* __restrict__ dirs, int D, double hstep, const double* __restrict__ gt0,
+                       const double* __restrict__ kbase, double* pose, double* intr_levels, int levels, int Dp) {
+  using S = Scal<G>;
+  const int C = 1 + Dp;
+  const int ngroups = G == 0 ? 1 : Dp / G;
+  const int gi = threadIdx.x;
+  if (gi >= ngroups) return;
+  const int g0 = gi * G;
+  S xi[6], kk[4];
+  for (int i = 0; i < 6; ++i) xi[i] = lit<S>(0.0);
+  for (int i = 0; i < 4; ++i) kk[i] = lit<S>(kbase[i]);
+  if constexpr (G > 0) {
+    for (int g = 0; g < G; ++g) {
+      const int dd = g0 + g;
+      if (dd >= D) continue;
+      const int prm = dirs[dd];
+      if (prm >= 0 && prm < 6) xi[prm].im[g] = hstep;
+      else if (prm >= 6 && prm < 10) kk[prm - 6].im[g] = hstep;
+    }
+  }
+  Pose<S> base;
+  for (int e = 0; e < 9; ++e) base.R.m[e] = lit<S>(gt0[e]);
+  for (int e = 0; e < 3; ++e) base.t.v[e] = lit<S>(gt0[9 + e]);
+  const Pose<S> p = compose(exp_map<S>(xi), base);
+  for (int e = 0; e < 9; ++e) store_ch<S>(pose + e * C, p.R.m[e], g0, G, gi == 0);
+  for (int e = 0; e < 3; ++e) store_ch<S>(pose + (9 + e) * C, p.t.v[e], g0, G, gi == 0);
+  for (int l = 0; l < levels; ++l) {
+    const double s = static_cast<double>(1 << l);
+    for (int i = 0; i < 4; ++i) store_ch<S>(intr_levels + (l * 4 + i) * C, kk[i] / s, g0, G, gi == 0);
+  }
+}
+
+__global__ void k_frame_begin(TrackState* st, int frame) {
+  st->frame = frame;
+  st->iterations = 0;
+  st->converged = 0;
+  st->n_corr = 0;
+  st->level_done = 0;
+}
+
+__global__ void k_frame_end(const TrackState* st, const double* pose, double* traj, int Dp, int* stats,
+                            const int* n_blocks, const int* counters) {
+  const int C = 1 + Dp;
+  const int f = st->frame;
+  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) traj[static_cast<long long>(f) * 12 * C + i] = pose[i];
+  if (threadIdx.x == 0) {
+    int* s = stats + 8 * f;
+    s[0] = st->iterations;
+    s[1] = st->n_corr;
+    s[2] = st->converged;
+    s[3] = n_blocks ? *n_blocks : 0;
+    s[4] = counters ? counters[0] : 0;
+    s[5] = counters ? counters[1] : 0;
+  }
+}
+
+// Objective of the lifted trajectory and Im(f)/h.
+template <int G>
+__global__ void k_objective(const double* __restrict__ traj, const double* __restrict__ gt, int n_frames, int kind,
+                            double hstep, int Dp, int D, double* out) {
+  using S = Scal<G>;
+  const int C = 1 + Dp;
+  const int ngroups = G == 0 ? 1 : Dp / G;
+  const int gi = threadIdx.x;
+  if (gi >= ngroups) return;
+  const int g0 = gi * G;
+  auto diff_at = [&](int f) {
+    V3<S> t;
+    for (int e = 0; e < 3; ++e)
+      t.v[e] = load_ch<S>(traj + (static_cast<long long>(f) * 12 + 9 + e) * C, g0, G) - gt[f * 12 + 9 + e];
+    return t;
+  };
+  S obj = lit<S>(0.0);
+  if (kind == 0) {
+    const V3<S> d = diff_at(n_frames - 1);
+    obj = sqrt_s(dot3(d, d));
+  } else {
+    for (int f = 0; f < n_frames; ++f) {
+      const V3<S> d = diff_at(f);
+      obj = obj + dot3(d, d);
+    }
+  }
+  if (gi == 0) out[0] = re(obj);
+  if constexpr (G > 0) {
+    for (int g = 0; g < G; ++g)
+      if (g0 + g < D) out[2 + g0 + g] = obj.im[g] / hstep;
+  }
+}
+
+}  // namespace csfd
+
+// ============================================================================
+namespace csfi {
+
+using namespace csfd;
+
+static void chk(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
+}
+
+#define CSF_DISPATCH_G(G, BODY)                       \
+  switch (G) {                                        \
+    case 0: { constexpr int kG = 0; BODY; } break;    \
+    case 1: { constexpr int kG = 1; BODY; } break;    \
+    case 2: { constexpr int kG = 2; BODY; } break;    \
+    case 3: { constexpr int kG = 3; BODY; } break;    \
+    case 4: { constexpr int kG = 4; BODY; } break;    \
+    case 5: { constexpr int kG = 5; BODY; } break;    \
+    case 6: { constexpr int kG = 6; BODY; } break;    \
+    default: std::fprintf(stderr, "csf_b200: no kernel for group width %d\n", G); \
+  }
+
+int icp_tiles(int w, int h, int stride) {
+  const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
+  return (nxs * nys + kTile - 1) / kTile;
+}
+
+static int reduce_chunk(int C) {
+  if (7 * C * 256 * 8 <= 200 * 1024) return 256;
+  if (7 * C * 128 * 8 <= 200 * 1024) return 128;
+  return 64;
+}
+
+void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp) {
+  k_level_begin<<<1, 128, 0, L.stream>>>(st, pose, pred_pose, Dp);
+  ++*L.launches;
+  chk("level_begin");
+}
+
+void launch_icp_reduce(const Launch& L, int G, int Dp, const TrackState* st, const double* depth, int w, int h,
+                       int stride, const double* intr, const double* pose, const double* vre, const double* nre,
+                       const double* vim, const double* nim, double d_max, double cos_max, double* partials,
+                       int* counts) {
+  const int C = 1 + Dp;
+  const int chunk = reduce_chunk(C);
+  const size_t smem = sizeof(double) * (16 * C + static_cast<size_t>(chunk) * 7 * C);
+  const int tiles = icp_tiles(w, h, stride);
+  CSF_DISPATCH_G(G, (cudaFuncSetAttribute(k_icp_reduce<kG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+                     k_icp_reduce<kG><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre,
+                                                                      vim, nim, d_max, cos_max, Dp, chunk, partials,
+                                                                      counts)));
+  ++*L.launches;
+  chk("icp_reduce");
+}
+
+void launch_icp_solve(const Launch& L, int G, int Dp, TrackState* st, const double* partials, const int* counts,
+                      int n_tiles, double* pose, int level, double tol) {
+  const size_t smem = sizeof(double) * 27 * (1 + Dp);
+  CSF_DISPATCH_G(G, (k_icp_solve<kG><<<1, 512, smem, L.stream>>>(st, partials, counts, n_tiles, pose, Dp, level, tol)));
+  ++*L.launches;
+  chk("icp_solve");
+}
+
+void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,
+                 const double* intr_base, double* pose, double* intr_levels, int levels) {
+  CSF_DISPATCH_G(G, (k_seed<kG><<<1, 64, 0, L.stream>>>(dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp)));
+  ++*L.launches;
+  chk("seed");
+}
+
+void launch_frame_begin(const Launch& L, TrackState* st, int frame) {
+  k_frame_begin<<<1, 1, 0, L.stream>>>(st, frame);
+  ++*L.launches;
+  chk("frame_begin");
+}
+
+void launch_frame_end(const Launch& L, TrackState* st, const double* pose, double* traj, int Dp, int* stats,
+                      const int* n_blocks, const int* counters) {
+  k_frame_end<<<1, 128, 0, L.stream>>>(st, pose, traj, Dp, stats, n_blocks, counters);
+  ++*L.launches;
+  chk("frame_end");
+}
+
+void launch_objective(const Launch& L, int G, int Dp, int D, const double* traj, const double* gt, int n_frames,
+                      int kind, double h, double* out) {
+  CSF_DISPATCH_G(G, (k_objective<kG><<<1, 64, 0, L.stream>>>(traj, gt, n_frames, kind, h, Dp, D, out)));
+  ++*L.launches;
+  chk("objective");
+}
+
+}  // namespace csfi

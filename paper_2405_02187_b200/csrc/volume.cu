@@ -1,0 +1,607 @@
+// TSDF kernels for sm_100a: fusion (dense lattice and hashed 8^3 blocks),
+// hashed-block allocation, and raycast surface prediction.
+//
+//   surface_update / measured_tsdf — proj/src/tsdf.cpp:11-40, tsdf.hpp:97-140
+//   sample_tsdf / sample_gradient  — proj/include/csf/tsdf.hpp:148-196
+//   raycast                        — proj/include/csf/tsdf.hpp:209-284
+//   hashed allocation              — builder-defined (oracle/orc_tsdf.hpp)
+//
+// Layout: rw[v] = (F.re, W) as one 16 B load, perturbation channels
+// fim[v*Dp + d] voxel-major / channel-minor so a fused voxel's channel group
+// is one contiguous run.  The raycast march reads only rw (the real channel
+// decides every branch); channels are gathered once per hit pixel.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "csf_internal.h"
+#include "geometry.cuh"
+
+namespace csfd {
+
+// ----------------------------------------------------------------------------
+// block prologue: the frame's pose (c2w) -> w2c per channel group in smem
+// layout in smem: w2c[12][1+Dp], center[3][1+Dp], intr[4][1+Dp]
+// ----------------------------------------------------------------------------
+template <int G>
+__device__ void stage_pose_w2c(const double* __restrict__ pose, const double* __restrict__ intr, int Dp, double* sm) {
+  using S = Scal<G>;
+  const int C = 1 + Dp;
+  const int ngroups = G == 0 ? 1 : Dp / G;
+  double* w2c = sm;
+  double* center = sm + 12 * C;
+  double* kk = sm + 15 * C;
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) kk[i] = intr[i];
+  for (int i = threadIdx.x; i < 3 * C; i += blockDim.x) center[i] = pose[9 * C + i];
+  for (int gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
+    const int g0 = gi * G;
+    Pose<S> c2w;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) c2w.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) c2w.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
+    const Pose<S> inv = inverse(c2w);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) store_ch<S>(w2c + e * C, inv.R.m[e], g0, G, gi == 0);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) store_ch<S>(w2c + (9 + e) * C, inv.t.v[e], g0, G, gi == 0);
+  }
+  __syncthreads();
+}
+
+template <typename S>
+__device__ void load_pose_intr(const double* sm, int Dp, int g0, Pose<S>* w2c, V3<S>* center, Intr<S>* k) {
+  const int C = 1 + Dp;
+  constexpr int G = Traits<S>::G;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) w2c->R.m[e] = load_ch<S>(sm + e * C, g0, G);
+#pragma unroll
+  for (int e = 0; e < 3; ++e) w2c->t.v[e] = load_ch<S>(sm + (9 + e) * C, g0, G);
+#pragma unroll
+  for (int e = 0; e < 3; ++e) center->v[e] = load_ch<S>(sm + (12 + e) * C, g0, G);
+  k->fx = load_ch<S>(sm + 15 * C, g0, G);
+  k->fy = load_ch<S>(sm + 16 * C, g0, G);
+  k->cx = load_ch<S>(sm + 17 * C, g0, G);
+  k->cy = load_ch<S>(sm + 18 * C, g0, G);
+}
+
+// Fuse one voxel: the real pass decides validity, then every channel group
+// re-evaluates psi (bit-identical real part) and updates its channels.
+template <int G>
+__device__ void fuse_voxel(const VoxelStore& vox, long long v, double px, double py, double pz,
+                           const double* __restrict__ depth, int w, int h, double mu, double cap, int Dp,
+                           const double* sm) {
+  Pose<double> w2c_re;
+  V3<double> c_re;
+  Intr<double> k_re;
+  load_pose_intr<double>(sm, Dp, 0, &w2c_re, &c_re, &k_re);
+  double psi_re;
+  if (!measured_tsdf<double>(depth, w, h, w2c_re, k_re, mu, px, py, pz, c_re, &psi_re)) return;
+  const double2 rw = vox.rw[v];
+  const double wt = rw.y;
+  const double fre = (wt * rw.x + psi_re) / (wt + 1.0);
+  if constexpr (G > 0) {
+    using S = L<G>;
+    for (int g0 = 0; g0 < Dp; g0 += G) {
+      Pose<S> w2c;
+      V3<S> c;
+      Intr<S> k;
+      load_pose_intr<S>(sm, Dp, g0, &w2c, &c, &k);
+      S psi;
+      measured_tsdf<S>(depth, w, h, w2c, k, mu, px, py, pz, c, &psi);
+      const S f = field_at<S>(vox, v, rw.x, g0);
+      const S fn = (wt * f + psi) / (wt + 1.0);
+      double* dst = vox.fim + v * vox.Dp + g0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) dst[g] = fn.im[g];
+    }
+  }
+  const double wn = wt + 1.0;
+  vox.rw[v] = make_double2(fre, cap < wn ? cap : wn);
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_integrate_dense(DenseView vol, const double* __restrict__ depth, int w,
+                                                         int h, const double* __restrict__ pose,
+                                                         const double* __restrict__ intr, int Dp) {
+  extern __shared__ double sm[];
+  stage_pose_w2c<G>(pose, intr, Dp, sm);
+  const long long n = static_cast<long long>(vol.nx) * vol.ny * vol.nz;
+  for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(v % vol.nx);
+    const int j = static_cast<int>((v / vol.nx) % vol.ny);
+    const int k = static_cast<int>(v / (static_cast<long long>(vol.nx) * vol.ny));
+    const double px = vol.ox + vol.vs * static_cast<double>(i);
+    const double py = vol.oy + vol.vs * static_cast<double>(j);
+    const double pz = vol.oz + vol.vs * static_cast<double>(k);
+    fuse_voxel<G>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_integrate_hashed(HashView vol, const int* __restrict__ coords,
+                                                          const int* __restrict__ visible,
+                                                          const int* __restrict__ counters,
+                                                          const double* __restrict__ depth, int w, int h,
+                                                          const double* __restrict__ pose,
+                                                          const double* __restrict__ intr, int Dp) {
+  extern __shared__ double sm[];
+  stage_pose_w2c<G>(pose, intr, Dp, sm);
+  const int n_vis = counters[0];
+  for (int vb = blockIdx.x; vb < n_vis; vb += gridDim.x) {
+    const int b = visible[vb];
+    if (b < 0) continue;
+    const int bx = coords[3 * b], by = coords[3 * b + 1], bz = coords[3 * b + 2];
+    for (int l = threadIdx.x; l < kBlockVoxels; l += blockDim.x) {
+      const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
+      const double px = vol.ox + vol.vs * static_cast<double>(8 * bx + lx);
+      const double py = vol.oy + vol.vs * static_cast<double>(8 * by + ly);
+      const double pz = vol.oz + vol.vs * static_cast<double>(8 * bz + lz);
+      fuse_voxel<G>(vol.vox, static_cast<long long>(b) * kBlockVoxels + l, px, py, pz, depth, w, h, vol.mu, vol.cap,
+                    Dp, sm);
+    }
+  }
+}
+
+__global__ void k_init_volume(double2* rw, double* fim, long long n, int Dp) {
+  for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<long long>(gridDim.x) * blockDim.x) {
+    rw[v] = make_double2(1.0, 0.0);
+    for (int d = 0; d < Dp; ++d) fim[v * Dp + d] = 0.0;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Hashed allocation (builder-defined; oracle/orc_tsdf.hpp allocate_band)
+// ----------------------------------------------------------------------------
+__global__ void k_band(const double* __restrict__ depth, int w, int h, const double* __restrict__ pose,
+                       const double* __restrict__ intr, int C, double mu, double vs, double ox, double oy, double oz,
+                       int K, unsigned long long* __restrict__ cand) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= w || y >= h) return;
+  const long long pix = static_cast<long long>(y) * w + x;
+  unsigned long long* out = cand + pix * K;
+  const double d = depth[pix];
+  if (!(d > 0.0)) {
+    for (int s = 0; s < K; ++s) out[s] = kEmptyKey;
+    return;
+  }
+  Pose<double> c2w;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) c2w.R.m[e] = pose[e * C];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) c2w.t.v[e] = pose[(9 + e) * C];
+  const double fx = intr[0], fy = intr[C], cx = intr[2 * C], cy = intr[3 * C];
+  const double lo = d - mu;
+  const double step = (2.0 * mu) / static_cast<double>(K - 1);
+  const double rx = (static_cast<double>(x) - cx) / fx;
+  const double ry = (static_cast<double>(y) - cy) / fy;
+  int pbx = 0, pby = 0, pbz = 0;
+  bool have = false;
+  for (int s = 0; s < K; ++s) {
+    out[s] = kEmptyKey;
+    const double z = lo + static_cast<double>(s) * step;
+    if (!(z > 0.0)) continue;
+    const V3<double> wp = apply(c2w, mk3<double>(z * rx, z * ry, z));
+    const int bx = ifloor((wp.v[0] - ox) / vs) >> 3;
+    const int by = ifloor((wp.v[1] - oy) / vs) >> 3;
+    const int bz = ifloor((wp.v[2] - oz) / vs) >> 3;
+    if (have && bx == pbx && by == pby && bz == pbz) continue;
+    out[s] = block_key(bx, by, bz);
+    pbx = bx; pby = by; pbz = bz;
+    have = true;
+  }
+}
+
+CSF_DEV unsigned set_hash(unsigned long long key, int bits) {
+  return static_cast<unsigned>((key * 0x9E3779B97F4A7C15ULL) >> (64 - bits));
+}
+
+__global__ void k_touch(const unsigned long long* __restrict__ cand, int n, unsigned long long* set_keys,
+                        int* set_first, int* set_slot, int bits, int* err, int* counters) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const unsigned long long key = cand[s];
+  if (key == kEmptyKey) {
+    set_slot[s] = -1;
+    return;
+  }
+  const unsigned mask = (1u << bits) - 1u;
+  unsigned hsh = set_hash(key, bits);
+  for (unsigned probe = 0; probe <= mask; ++probe) {
+    const unsigned long long prev = atomicCAS(set_keys + hsh, kEmptyKey, key);
+    if (prev == kEmptyKey || prev == key) {
+      atomicMin(set_first + hsh, s);
+      set_slot[s] = static_cast<int>(hsh);
+      return;
+    }
+    hsh = (hsh + 1u) & mask;
+  }
+  set_slot[s] = -1;
+  atomicExch(counters + 2, 1);
+  raise(err, kErrNoMem);
+}
+
+__global__ void k_flags(HashView vol, const unsigned long long* __restrict__ cand, int n,
+                        const int* __restrict__ set_first, const int* __restrict__ set_slot, int* first_flag,
+                        int* new_flag, int* cand_block) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int hs = set_slot[s];
+  const bool first = hs >= 0 && set_first[hs] == s;
+  int nf = 0;
+  if (first) {
+    const unsigned long long key = cand[s];
+    const int bx = static_cast<int>((key >> 42) & 0x1FFFFF) - kCoordBias;
+    const int by = static_cast<int>((key >> 21) & 0x1FFFFF) - kCoordBias;
+    const int bz = static_cast<int>(key & 0x1FFFFF) - kCoordBias;
+    const int id = vol.find(bx, by, bz);
+    cand_block[s] = id;
+    nf = id < 0;
+  }
+  first_flag[s] = first;
+  new_flag[s] = nf;
+}
+
+// Lock-free insertion into a chain kept sorted by key: the resulting chains
+// depend only on the key set, never on thread order.
+__device__ void chain_insert(int* heads, const unsigned long long* keys, int* next, unsigned bucket, int id,
+                             unsigned long long key) {
+  while (true) {
+    int* link = heads + bucket;
+    int cur = *reinterpret_cast<volatile int*>(link);
+    while (cur >= 0 && *reinterpret_cast<const volatile unsigned long long*>(keys + cur) < key) {
+      link = next + cur;
+      cur = *reinterpret_cast<volatile int*>(link);
+    }
+    *reinterpret_cast<volatile int*>(next + id) = cur;
+    __threadfence();
+    if (atomicCAS(link, cur, id) == cur) return;
+  }
+}
+
+__global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int* next, int* coords, const int* n_blocks,
+                         int max_blocks, const unsigned long long* __restrict__ cand, int n,
+                         const int* __restrict__ first_flag, const int* __restrict__ new_flag,
+                         const int* __restrict__ first_rank, const int* __restrict__ new_rank,
+                         const int* __restrict__ cand_block, int* visible, int* err) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n || !first_flag[s]) return;
+  int id = cand_block[s];
+  if (new_flag[s]) {
+    id = *n_blocks + new_rank[s];
+    if (id >= max_blocks) {
+      raise(err, kErrNoMem);
+      visible[first_rank[s]] = -1;
+      return;
+    }
+    const unsigned long long key = cand[s];
+    const int bx = static_cast<int>((key >> 42) & 0x1FFFFF) - kCoordBias;
+    const int by = static_cast<int>((key >> 21) & 0x1FFFFF) - kCoordBias;
+    const int bz = static_cast<int>(key & 0x1FFFFF) - kCoordBias;
+    keys[id] = key;
+    coords[3 * id] = bx;
+    coords[3 * id + 1] = by;
+    coords[3 * id + 2] = bz;
+    __threadfence();
+    chain_insert(heads, keys, next, block_hash(bx, by, bz, vol.mask), id, key);
+  }
+  visible[first_rank[s]] = id;
+}
+
+__global__ void k_alloc_finalize(int* n_blocks, int max_blocks, const int* first_flag, const int* new_flag,
+                                 const int* first_rank, const int* new_rank, int n, int* counters) {
+  const int n_vis = n > 0 ? first_rank[n - 1] + first_flag[n - 1] : 0;
+  const int n_new = n > 0 ? new_rank[n - 1] + new_flag[n - 1] : 0;
+  const int old = *n_blocks;
+  const int nb = old + n_new > max_blocks ? max_blocks : old + n_new;
+  *n_blocks = nb;
+  counters[0] = n_vis;
+  counters[1] = n_new;
+  counters[3] = old;
+}
+
+// ----------------------------------------------------------------------------
+// Raycast (tsdf.hpp:209-284)
+// ----------------------------------------------------------------------------
+struct Box {
+  bool use;
+  double lo[3], hi[3];
+};
+
+template <int G, typename V>
+__global__ void __launch_bounds__(128) k_raycast(V vol, const double* __restrict__ pose, const double* __restrict__ intr,
+                                                 int w, int h, int Dp, double near_clip, double far_clip, double step,
+                                                 Box box, double* __restrict__ vre, double* __restrict__ nre,
+                                                 double* __restrict__ vim, double* __restrict__ nim) {
+  extern __shared__ double sm[];
+  const int C = 1 + Dp;
+  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
+  __syncthreads();
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= w * h) return;
+  const int x = pix % w, y = pix / w;
+  const double* kk = sm + 12 * C;
+
+  // real ray (identical to the real part of the lifted ray below)
+  Pose<double> c2w;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) c2w.R.m[e] = sm[e * C];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) c2w.t.v[e] = sm[(9 + e) * C];
+  const V3<double> dc = mk3<double>((static_cast<double>(x) - kk[2 * C]) / kk[0],
+                                    (static_cast<double>(y) - kk[3 * C]) / kk[C], 1.0 * 1.0);
+  const double rn = sqrt(dot3(dc, dc));
+  const V3<double> dir = matvec(c2w.R, mk3<double>(dc.v[0] / rn, dc.v[1] / rn, dc.v[2] / rn));
+  const V3<double> o = c2w.t;
+
+  double* vr = vre + static_cast<long long>(pix) * 3;
+  double* nr = nre + static_cast<long long>(pix) * 3;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) vr[c] = nr[c] = 0.0;
+  if (G > 0) {
+    double* vi = vim + static_cast<long long>(pix) * 3 * Dp;
+    double* ni = nim + static_cast<long long>(pix) * 3 * Dp;
+    for (int c = 0; c < 3 * Dp; ++c) vi[c] = ni[c] = 0.0;
+  }
+
+  double t0 = near_clip, t1 = far_clip;
+  if (box.use) {
+    bool hit_box = true;
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+      const double od = o.v[axis], dd = dir.v[axis];
+      if (fabs(dd) < 1e-12) {
+        if (od < box.lo[axis] || od > box.hi[axis]) hit_box = false;
+        continue;
+      }
+      double ta = (box.lo[axis] - od) / dd;
+      double tb = (box.hi[axis] - od) / dd;
+      if (ta > tb) {
+        const double t = ta;
+        ta = tb;
+        tb = t;
+      }
+      t0 = t0 < ta ? ta : t0;  // std::max(t0, ta)
+      t1 = tb < t1 ? tb : t1;  // std::min(t1, tb)
+    }
+    if (!hit_box) return;
+  }
+  if (t0 >= t1) return;
+
+  bool have_prev = false, crossed = false;
+  double alpha_prev = 0.0, f_prev = 0.0, alpha_hit = 0.0;
+  for (double alpha = t0; alpha <= t1; alpha += step) {
+    const V3<double> p = mk3<double>(o.v[0] + alpha * dir.v[0], o.v[1] + alpha * dir.v[1], o.v[2] + alpha * dir.v[2]);
+    double f;
+    if (!sample_tsdf<double>(vol, p, 0, &f)) {
+      have_prev = false;
+      continue;
+    }
+    if (have_prev && f_prev > 0.0 && f < 0.0) {
+      crossed = true;
+      alpha_hit = alpha;
+      break;
+    }
+    have_prev = true;
+    alpha_prev = alpha;
+    f_prev = f;
+  }
+  if (!crossed) return;
+
+  const int passes = G == 0 ? 1 : Dp / G;
+  for (int gi = 0; gi < passes; ++gi) {
+    using S = Scal<G>;
+    const int g0 = gi * G;
+    Pose<S> P;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) P.R.m[e] = load_ch<S>(sm + e * C, g0, G);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) P.t.v[e] = load_ch<S>(sm + (9 + e) * C, g0, G);
+    const S fx = load_ch<S>(kk, g0, G), fy = load_ch<S>(kk + C, g0, G);
+    const S cx = load_ch<S>(kk + 2 * C, g0, G), cy = load_ch<S>(kk + 3 * C, g0, G);
+    const S one = lit<S>(1.0);
+    const V3<S> dcs = mk3<S>((static_cast<double>(x) - cx) / fx, (static_cast<double>(y) - cy) / fy, one);
+    const S rns = sqrt_s(dot3(dcs, dcs));
+    const V3<S> dirs = matvec(P.R, mk3<S>(dcs.v[0] / rns, dcs.v[1] / rns, dcs.v[2] / rns));
+    const V3<S>& os = P.t;
+    auto at = [&](double a) {
+      return mk3<S>(os.v[0] + a * dirs.v[0], os.v[1] + a * dirs.v[1], os.v[2] + a * dirs.v[2]);
+    };
+    S fl_prev, fl;
+    sample_tsdf<S>(vol, at(alpha_prev), g0, &fl_prev);
+    sample_tsdf<S>(vol, at(alpha_hit), g0, &fl);
+    const double span = alpha_hit - alpha_prev;
+    const S astar = alpha_prev - (span * fl_prev) / (fl - fl_prev);
+    const V3<S> v = mk3<S>(os.v[0] + astar * dirs.v[0], os.v[1] + astar * dirs.v[1], os.v[2] + astar * dirs.v[2]);
+    V3<S> grad;
+    if (!sample_gradient<S>(vol, v, g0, &grad)) return;
+    const S len2 = dot3(grad, grad);
+    if (!(re(len2) > 0.0)) return;
+    const S ln = sqrt_s(len2);
+    const V3<S> n = mk3<S>(grad.v[0] / ln, grad.v[1] / ln, grad.v[2] / ln);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (gi == 0) {
+        vr[c] = re(v.v[c]);
+        nr[c] = re(n.v[c]);
+      }
+      if constexpr (G > 0) {
+        double* vi = vim + (static_cast<long long>(pix) * 3 + c) * Dp + g0;
+        double* ni = nim + (static_cast<long long>(pix) * 3 + c) * Dp + g0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          vi[g] = v.v[c].im[g];
+          ni[g] = n.v[c].im[g];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace csfd
+
+// ============================================================================
+namespace csfi {
+
+using namespace csfd;
+
+static void chk(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
+}
+
+int pick_group(int D) {
+  if (D <= 0) return 0;
+  if (D <= 6) return D;
+  int best = 4, best_dp = padded_channels(D, 4);
+  for (int g : {5, 6}) {
+    const int dp = padded_channels(D, g);
+    if (dp <= best_dp) {
+      best = g;
+      best_dp = dp;
+    }
+  }
+  return best;
+}
+
+#define CSF_DISPATCH_G(G, BODY)                       \
+  switch (G) {                                        \
+    case 0: { constexpr int kG = 0; BODY; } break;    \
+    case 1: { constexpr int kG = 1; BODY; } break;    \
+    case 2: { constexpr int kG = 2; BODY; } break;    \
+    case 3: { constexpr int kG = 3; BODY; } break;    \
+    case 4: { constexpr int kG = 4; BODY; } break;    \
+    case 5: { constexpr int kG = 5; BODY; } break;    \
+    case 6: { constexpr int kG = 6; BODY; } break;    \
+    default: std::fprintf(stderr, "csf_b200: no kernel for group width %d\n", G); \
+  }
+
+static DenseView dense_view(const DenseDev& v, int Dp) {
+  DenseView d;
+  d.vox = {v.rw, v.fim, Dp};
+  d.nx = v.nx; d.ny = v.ny; d.nz = v.nz;
+  d.vs = v.vs; d.ox = v.ox; d.oy = v.oy; d.oz = v.oz; d.mu = v.mu; d.cap = v.cap;
+  return d;
+}
+static HashView hash_view(const HashDev& v, int Dp) {
+  HashView d;
+  d.vox = {v.rw, v.fim, Dp};
+  d.heads = v.heads; d.keys = v.keys; d.next = v.next;
+  d.mask = (1u << v.bits) - 1u;
+  d.vs = v.vs; d.ox = v.ox; d.oy = v.oy; d.oz = v.oz; d.mu = v.mu; d.cap = v.cap;
+  return d;
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp) {
+  k_init_volume<<<sm_count() * 8, 256, 0, L.stream>>>(rw, fim, n, Dp);
+  ++*L.launches;
+  chk("init_volume");
+}
+
+void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* depth, int w, int h,
+                            const double* pose, const double* intr) {
+  const DenseView view = dense_view(v, Dp);
+  const size_t smem = sizeof(double) * 19 * (1 + Dp);
+  const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
+  const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, sm_count() * 16LL));
+  CSF_DISPATCH_G(G, (k_integrate_dense<kG><<<grid, 256, smem, L.stream>>>(view, depth, w, h, pose, intr, Dp)));
+  ++*L.launches;
+  chk("integrate_dense");
+}
+
+void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, const AllocScratch& a,
+                             const double* depth, int w, int h, const double* pose, const double* intr) {
+  const HashView view = hash_view(v, Dp);
+  const size_t smem = sizeof(double) * 19 * (1 + Dp);
+  const int grid = sm_count() * 8;
+  CSF_DISPATCH_G(G, (k_integrate_hashed<kG><<<grid, 256, smem, L.stream>>>(view, v.coords, a.visible, a.counters,
+                                                                           depth, w, h, pose, intr, Dp)));
+  ++*L.launches;
+  chk("integrate_hashed");
+}
+
+int band_samples(double mu, double vs) {
+  const int k = static_cast<int>(std::ceil((2.0 * mu) / vs)) + 1;
+  return k < 2 ? 2 : k;
+}
+
+void launch_allocate(const Launch& L, const HashDev& v, int Dp, AllocScratch& a, const double* depth, int w, int h,
+                     const double* pose, const double* intr) {
+  const HashView view = hash_view(v, Dp);
+  const int K = band_samples(v.mu, v.vs);
+  const int n = w * h * K;
+  const int C = 1 + Dp;
+  cudaMemsetAsync(a.set_keys, 0xFF, sizeof(unsigned long long) << a.set_bits, L.stream);
+  cudaMemsetAsync(a.set_first, 0x7F, sizeof(int) << a.set_bits, L.stream);
+  const dim3 b2(32, 8), g2((w + 31) / 32, (h + 7) / 8);
+  k_band<<<g2, b2, 0, L.stream>>>(depth, w, h, pose, intr, C, v.mu, v.vs, v.ox, v.oy, v.oz, K, a.cand);
+  const int tb = 256, gb = (n + tb - 1) / tb;
+  k_touch<<<gb, tb, 0, L.stream>>>(a.cand, n, a.set_keys, a.set_first, a.set_slot, a.set_bits, L.err, a.counters);
+  k_flags<<<gb, tb, 0, L.stream>>>(view, a.cand, n, a.set_first, a.set_slot, a.first_flag, a.new_flag, a.cand_block);
+  size_t bytes = a.cub_tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(a.cub_tmp, bytes, a.first_flag, a.first_rank, n, L.stream);
+  bytes = a.cub_tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(a.cub_tmp, bytes, a.new_flag, a.new_rank, n, L.stream);
+  k_insert<<<gb, tb, 0, L.stream>>>(view, v.heads, v.keys, v.next, v.coords, v.n_blocks, v.max_blocks, a.cand, n,
+                                    a.first_flag, a.new_flag, a.first_rank, a.new_rank, a.cand_block, a.visible, L.err);
+  k_alloc_finalize<<<1, 1, 0, L.stream>>>(v.n_blocks, v.max_blocks, a.first_flag, a.new_flag, a.first_rank,
+                                          a.new_rank, n, a.counters);
+  *L.launches += 7;
+  chk("allocate");
+}
+
+size_t alloc_scan_bytes(int n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<int*>(nullptr), static_cast<int*>(nullptr), n);
+  return bytes;
+}
+
+void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* pose, const double* intr,
+                          int w, int h, double near_clip, double far_clip, double step, double* vre, double* nre,
+                          double* vim, double* nim) {
+  const DenseView view = dense_view(v, Dp);
+  Box box;
+  box.use = true;
+  box.lo[0] = v.ox; box.lo[1] = v.oy; box.lo[2] = v.oz;
+  box.hi[0] = v.ox + v.vs * (static_cast<double>(v.nx) - 1.0);
+  box.hi[1] = v.oy + v.vs * (static_cast<double>(v.ny) - 1.0);
+  box.hi[2] = v.oz + v.vs * (static_cast<double>(v.nz) - 1.0);
+  const size_t smem = sizeof(double) * 16 * (1 + Dp);
+  const int grid = (w * h + 127) / 128;
+  CSF_DISPATCH_G(G, (k_raycast<kG, DenseView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
+                                                                             far_clip, step, box, vre, nre, vim, nim)));
+  ++*L.launches;
+  chk("raycast_dense");
+}
+
+void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, const double* pose, const double* intr,
+                           int w, int h, double near_clip, double far_clip, double step, double* vre, double* nre,
+                           double* vim, double* nim) {
+  const HashView view = hash_view(v, Dp);
+  Box box;
+  box.use = false;
+  const size_t smem = sizeof(double) * 16 * (1 + Dp);
+  const int grid = (w * h + 127) / 128;
+  CSF_DISPATCH_G(G, (k_raycast<kG, HashView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
+                                                                            far_clip, step, box, vre, nre, vim, nim)));
+  ++*L.launches;
+  chk("raycast_hashed");
+}
+
+}  // namespace csfi
