@@ -142,6 +142,12 @@ int csf_ctx_synchronize(csf_ctx ctx);
 int csf_ctx_launch_count(csf_ctx ctx, unsigned long long* out);
 /* CUDA stream of the context (cudaStream_t as void*), for event timing. */
 void* csf_ctx_stream(csf_ctx ctx);
+/* Per-kernel-category CUDA-event timing on the context stream (off by default).
+ * read: names [n][32] (NUL-terminated), total ms and launch counts per
+ * category since the last read; resets the records. */
+int csf_ctx_profile(csf_ctx ctx, int enable);
+int csf_ctx_profile_read(csf_ctx ctx, int max_categories, char* names, double* ms, long long* counts,
+                         int* n_categories);
 
 /* ---- frames: frames.cpp:7-75, frames.hpp:86-114 --------------------------- */
 int csf_bilateral_filter(csf_ctx ctx, const double* depth, int w, int h, double sigma_s, double sigma_r, int radius,

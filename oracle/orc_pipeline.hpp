@@ -261,7 +261,11 @@ inline Scene config1_scene(uint64_t seed = 0) {
   for (int i = 0; i < 3; ++i) {
     SdfSphere sp;
     sp.radius = u.next(0.3, 0.6);
-    sp.center = Vec3d(u.next(-1.6, -0.6), u.next(-1.0, 1.0), u.next(0.3, 1.2));
+    // draws in statement order (constructor-argument order is unspecified)
+    const double cx = u.next(-1.6, -0.6);
+    const double cy = u.next(-1.0, 1.0);
+    const double cz = u.next(0.3, 1.2);
+    sp.center = Vec3d(cx, cy, cz);
     s.spheres.push_back(sp);
   }
   return s;
@@ -290,7 +294,10 @@ inline Scene config2_scene(uint64_t seed = 1) {
   while (placed < 20) {
     const bool sphere = (placed % 2) == 0;
     const double r = sphere ? u.next(0.1, 0.35) : u.next(0.08, 0.3);
-    const Vec3d c(u.next(-1.8, 1.8), u.next(-1.8, 1.8), u.next(0.2, 2.5));
+    const double c0 = u.next(-1.8, 1.8);
+    const double c1 = u.next(-1.8, 1.8);
+    const double c2 = u.next(0.2, 2.5);
+    const Vec3d c(c0, c1, c2);
     const double radial = std::sqrt(c[0] * c[0] + c[1] * c[1]);
     const double bound = sphere ? r : r * 1.7320508075688772;
     if (std::fabs(radial - 1.2) < bound + 0.35 && std::fabs(c[2] - 1.3) < bound + 0.45) continue;  // keep the orbit free

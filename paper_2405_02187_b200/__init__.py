@@ -112,6 +112,24 @@ class Context:
         self.check(self.lib.csf_ctx_launch_count(self.h, C.byref(n)))
         return int(n.value)
 
+    def profile(self, enable: bool = True) -> None:
+        """Per-kernel-category CUDA-event timing on this context's stream."""
+        self.check(self.lib.csf_ctx_profile(self.h, int(enable)))
+
+    def profile_read(self) -> dict:
+        """{category: (total_ms, launches)} since the last read."""
+        names = C.create_string_buffer(32 * 16)
+        ms = np.zeros(16)
+        cnt = np.zeros(16, dtype=np.int64)
+        n = C.c_int()
+        self.check(self.lib.csf_ctx_profile_read(self.h, 16, names, _dp(ms),
+                                                 cnt.ctypes.data_as(C.POINTER(C.c_longlong)), C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            nm = names.raw[32 * i: 32 * i + 32].split(b"\0", 1)[0].decode()
+            out[nm] = (float(ms[i]), int(cnt[i]))
+        return out
+
     @property
     def stream(self) -> int:
         return int(self.lib.csf_ctx_stream(self.h) or 0)

@@ -21,7 +21,7 @@ OBJECTIVE_FINAL_TRANSLATION_ERROR, OBJECTIVE_TRAJECTORY_ERROR = 0, 1
 EXPORTS = (
     "csf_default_intrinsics", "csf_default_volume_params", "csf_default_raycast_cfg", "csf_default_icp_cfg",
     "csf_ctx_create", "csf_ctx_destroy", "csf_last_error", "csf_ctx_synchronize", "csf_ctx_launch_count",
-    "csf_ctx_stream", "csf_bilateral_filter", "csf_downsample_depth", "csf_measure_surface",
+    "csf_ctx_stream", "csf_ctx_profile", "csf_ctx_profile_read", "csf_bilateral_filter", "csf_downsample_depth", "csf_measure_surface",
     "csf_volume_create_dense", "csf_volume_create_hashed", "csf_volume_destroy", "csf_volume_upload",
     "csf_volume_download", "csf_volume_block_count", "csf_volume_download_hash", "csf_surface_update",
     "csf_raycast", "csf_track_frame", "csf_pipeline_create", "csf_pipeline_destroy", "csf_pipeline_upload",
@@ -82,6 +82,8 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_ctx_synchronize": (ip, [vp]),
         "csf_ctx_launch_count": (ip, [vp, C.POINTER(C.c_ulonglong)]),
         "csf_ctx_stream": (vp, [vp]),
+        "csf_ctx_profile": (ip, [vp, ip]),
+        "csf_ctx_profile_read": (ip, [vp, ip, C.c_char_p, dp, C.POINTER(C.c_longlong), C.POINTER(C.c_int)]),
         "csf_bilateral_filter": (ip, [vp, dp, ip, ip, C.c_double, C.c_double, ip, dp]),
         "csf_downsample_depth": (ip, [vp, dp, ip, ip, C.c_double, dp]),
         "csf_measure_surface": (ip, [vp, dp, ip, ip, dp, ip, dp, dp]),

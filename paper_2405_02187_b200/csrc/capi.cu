@@ -26,13 +26,55 @@ size_t alloc_scan_bytes(int n);
 
 using namespace csfi;
 
+// Per-category kernel timing with CUDA events on the context stream
+// (bench.py's roofline numbers).  Off unless csf_ctx_profile(ctx, 1).
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<int, size_t>> recs;  // (category, first event index)
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+
+enum ProfCat { kPBilateral = 0, kPDownsample, kPRaycast, kPIcpReduce, kPIcpSolve, kPAlloc, kPIntegrate, kPMisc, kPN };
+static const char* kProfNames[kPN] = {"bilateral", "downsample", "raycast", "icp_reduce", "icp_solve",
+                                      "allocate", "integrate", "misc"};
+
 struct csf_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int* d_err = nullptr;
   unsigned long long launches = 0;
   std::string last_error;
+  Profiler prof;
 };
+
+// Brackets a launch with events when profiling is on.
+struct ProfScope {
+  csf_ctx ctx;
+  int cat;
+  size_t first = 0;
+  ProfScope(csf_ctx c, int k) : ctx(c), cat(k) {
+    if (ctx->prof.on) {
+      first = ctx->prof.used;
+      cudaEventRecord(ctx->prof.ev(), ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (ctx->prof.on) {
+      cudaEventRecord(ctx->prof.ev(), ctx->stream);
+      ctx->prof.recs.emplace_back(cat, first);
+    }
+  }
+};
+#define PROF(ctx, cat) ProfScope _prof_scope_##__LINE__((ctx), (cat))
 
 namespace {
 
@@ -178,9 +220,14 @@ int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double*
   if (v->hashed) {
     const int rc = ensure_alloc_scratch(v, w, h);
     if (rc) return rc;
-    launch_allocate(L, v->hash, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr);
+    {
+      PROF(v->ctx, kPAlloc);
+      launch_allocate(L, v->hash, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr);
+    }
+    PROF(v->ctx, kPIntegrate);
     launch_integrate_hashed(L, v->hash, v->G, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr);
   } else {
+    PROF(v->ctx, kPIntegrate);
     launch_integrate_dense(L, v->dense, v->G, v->Dp, d_depth, w, h, d_pose, d_intr);
   }
   return CSF_OK;
@@ -191,6 +238,7 @@ void raycast_dev(csf_volume v, const double* d_pose, const double* d_intr, int w
   const Launch L = launch_of(v->ctx);
   const double mu = v->hashed ? v->hash.mu : v->dense.mu;
   const double step = rc.step_fraction * mu;
+  PROF(v->ctx, kPRaycast);
   if (v->hashed)
     launch_raycast_hashed(L, v->hash, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, vre, nre,
                           vim, nim);
@@ -284,6 +332,39 @@ extern "C" int csf_ctx_launch_count(csf_ctx ctx, unsigned long long* out) {
 }
 
 extern "C" void* csf_ctx_stream(csf_ctx ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+extern "C" int csf_ctx_profile(csf_ctx ctx, int enable) {
+  if (!ctx) return CSF_EINVAL;
+  ctx->prof.on = enable != 0;
+  ctx->prof.used = 0;
+  ctx->prof.recs.clear();
+  return CSF_OK;
+}
+
+extern "C" int csf_ctx_profile_read(csf_ctx ctx, int max_categories, char* names, double* ms, long long* counts,
+                                    int* n_categories) {
+  if (!ctx || !n_categories) return CSF_EINVAL;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  double tot[kPN] = {0};
+  long long cnt[kPN] = {0};
+  for (const auto& r : ctx->prof.recs) {
+    float t = 0.0f;
+    cudaEventElapsedTime(&t, ctx->prof.pool[r.second], ctx->prof.pool[r.second + 1]);
+    tot[r.first] += t;
+    cnt[r.first] += 1;
+  }
+  const int n = std::min<int>(kPN, max_categories);
+  for (int i = 0; i < n; ++i) {
+    if (names) std::snprintf(names + 32 * i, 32, "%s", kProfNames[i]);
+    if (ms) ms[i] = tot[i];
+    if (counts) counts[i] = cnt[i];
+  }
+  *n_categories = n;
+  ctx->prof.used = 0;
+  ctx->prof.recs.clear();
+  return CSF_OK;
+}
 
 // ---------------------------------------------------------------------------
 // frames
@@ -748,9 +829,15 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
 
   for (int f = 1; f < n_frames; ++f) {
     launch_frame_begin(L, st, f);
-    launch_bilateral(L, p->frames.p + P * f, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
-    if (p->levels > 1) launch_downsample(L, p->pyr0.p, p->pyr1.p, W, H, 0.03);
-    if (p->levels > 2) launch_downsample(L, p->pyr1.p, p->pyr2.p, W / 2, H / 2, 0.03);
+    {
+      PROF(ctx, kPBilateral);
+      launch_bilateral(L, p->frames.p + P * f, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
+    }
+    {
+      PROF(ctx, kPDownsample);
+      if (p->levels > 1) launch_downsample(L, p->pyr0.p, p->pyr1.p, W, H, 0.03);
+      if (p->levels > 2) launch_downsample(L, p->pyr1.p, p->pyr2.p, W / 2, H / 2, 0.03);
+    }
     for (int li = 0; li < p->levels; ++li) {
       const int level = p->levels - 1 - li;
       const int wl = W >> level, hl = H >> level;
@@ -760,8 +847,12 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
       const int stride = std::max(1, cfg.icp.level_pixel_stride[li]);
       const int tiles = icp_tiles(wl, hl, stride);
       for (int it = 0; it < cfg.icp.level_iterations[li]; ++it) {
-        launch_icp_reduce(L, p->G, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p, p->vim.p,
-                          p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p);
+        {
+          PROF(ctx, kPIcpReduce);
+          launch_icp_reduce(L, p->G, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p,
+                            p->vim.p, p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p);
+        }
+        PROF(ctx, kPIcpSolve);
         launch_icp_solve(L, p->G, p->Dp, st, p->partials.p, p->counts.p, tiles, p->pose.p, level,
                          cfg.icp.step_tolerance);
       }
