@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""CSFD SLAM frame-derivatives/s at 640x480 (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 2 — 100 VGA depth frames of the seeded
+procedural room (synthetic stand-in for TUM-style sequences, rendered on the
+device by the harness; not timed), hashed 8^3-block TSDF at 5 mm voxels with
+2^20 buckets, 10 CSFD directions (6 first-frame twist + 4 intrinsics),
+objective = accumulated trajectory error.  One step = one full CSFD run over
+all frames (volume reset, frame 0 fused at exp(xi0*)T0, frames 1..99 tracked
+with the lifted 3-level ICP and fused).  Units = frames x directions.
+
+  value       device-resident inputs, CUDA events on the library stream
+  e2e         the public API call Pipeline.run_host() from pinned host
+              frames: H2D of the step's frames + D2H of the gradient inside
+              the timed region
+  roofline    dominant kernel category, algorithmic bytes per launch /
+              average launch time (CUDA events on the launching stream)
+  cpu_baseline the CPU oracle (oracle/, a restatement of the reference,
+              which cannot be built here) on a bounded sample, rank 0 only
+
+Multi-GPU (torchrun): the 10 directions are sharded in contiguous blocks
+(paper_2405_02187_b200/shard.py); each rank recomputes the shared real
+pipeline; the derivative columns are all-gathered over NCCL.  Total work is
+fixed, so scaling is "strong".  --impl reference times the CPU oracle port
+(the reference's own CPU path restated) on a bounded sample of the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "CSFD SLAM frame-derivatives/sec at 640×480 (frames×directions/s), 1/2/4/8 GPU"
+UNIT = "frame-derivatives/s"
+DIRS = list(range(10))  # 6 first-frame twist components (rho, phi) + fx, fy, cx, cy
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--frames", type=int, default=100)
+    ap.add_argument("--cpu-frames", type=int, default=5, help="CPU-baseline sample: frames")
+    ap.add_argument("--cpu-dirs", type=int, default=2, help="CPU-baseline sample: directions (one pass each)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-json", default="")
+    return ap.parse_args()
+
+
+def pipeline_cfg(csf, capi, k, dirs, n_frames):
+    import ctypes as C
+    hp = capi.HashParams(0.005, (C.c_double * 3)(0.0, 0.0, 0.0), 5 * 0.005, 128.0, 20, 1 << 18)
+    return csf.make_pipeline_cfg(hashed=True, k=k, dirs=dirs, h=1e-8, objective=capi.OBJECTIVE_TRAJECTORY_ERROR,
+                                 max_frames=n_frames, hash_params=hp)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait(timeout=10)
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1].split()[0]))
+                mx = float(r[2].split()[0])
+                for n, v in zip(names, r[5:9]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(n)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(depth, gt, k, frames, ndirs):
+    """Oracle port, one Complex-style pass per direction (the reference's
+    pattern, diff.hpp:46-56), all host threads (OpenMP)."""
+    from oracle import orc
+    import paper_2405_02187_b200 as csf
+    from paper_2405_02187_b200 import capi
+    secs = 0.0
+    for d in range(ndirs):
+        cfg = pipeline_cfg(csf, capi, k, [DIRS[d]], frames)
+        _, _, _, _, s = orc.pipeline_run(cfg, depth[:frames], gt[:frames])
+        secs += s
+    units = frames * ndirs
+    cores = os.cpu_count() or 1
+    omp = os.environ.get("OMP_NUM_THREADS")
+    if omp:
+        cores = int(omp)
+    return {"value": units / secs, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"config 2 first {frames} VGA frames x {ndirs} directions, one pass per direction "
+                      f"({units} units in {secs:.2f} s)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle port on the box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2405_02187_b200 as csf  # noqa: F401 (struct layouts)
+    from oracle import orc
+    frames = 3
+    depth, gt, k = orc.workload(2, frames)
+    from paper_2405_02187_b200 import capi
+    cfg = pipeline_cfg(__import__("paper_2405_02187_b200"), capi, k, [0], frames)
+    for _ in range(args.warmup):
+        orc.pipeline_run(cfg, depth, gt)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        orc.pipeline_run(cfg, depth, gt)
+    secs = time.perf_counter() - t0
+    units = frames * 1 * args.steps
+    value = units / secs
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded procedural room, BASELINE config 2 shapes)",
+        "config": {"workload": "config2 VGA hashed 5mm, bounded CPU sample: 3 frames x 1 direction per step",
+                   "frames": frames, "directions": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": "3 VGA frames x 1 direction per step (oracle/ restatement; the reference needs "
+                                   "Eigen/libpng/doctest, absent)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def algorithmic_bytes_per_step(cat, stats, D, W, H, n_frames):
+    """Algorithmic HBM bytes of one kernel category over one step."""
+    P = W * H
+    if cat == "integrate":
+        vis = float(stats[:n_frames, 4].sum())  # visible blocks summed over the step's frames
+        return vis * 512 * 2 * (16 + 8 * D) + n_frames * 8 * P, \
+            "sum over frames of visible voxels x 2 x (16 + 8D) B (read+write F.re,W and D channels) + depth"
+    if cat == "bilateral":
+        return (n_frames - 1) * (4 + 8 + 8) * P, "float32 depth in, raw + filtered float64 out"
+    if cat == "raycast":
+        per = (P + P / 4 + P / 16) * (2 * 3 * 8 * (1 + D))
+        return (n_frames - 1) * per, "vertex+normal maps written (real + D channels), 3 levels"
+    return None, None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import paper_2405_02187_b200 as csf
+    from paper_2405_02187_b200 import capi
+    from paper_2405_02187_b200.shard import gather_columns, shard_directions
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    ctx = csf.Context(local)
+    n = args.frames
+    depth, gt, k = csf.synth_workload(2, n, ctx=ctx)
+    off, mine = shard_directions(DIRS, world, rank)
+    cfg = pipeline_cfg(csf, capi, k, mine, n)
+    pipe = csf.Pipeline(cfg, ctx=ctx)
+    pipe.upload(depth, gt)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+
+    for _ in range(max(args.warmup, 0)):
+        pipe.run()
+    ctx.synchronize()
+
+    # ---------------- timed region: device-resident inputs
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    clocks = Clocks(local)
+    barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    ctx.profile(True)
+    l0 = ctx.launch_count
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        pipe.run()
+    e1.record(stream)
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count - l0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    clk = clocks.stop()
+    res = pipe.result()
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        grad = gather_columns(torch.from_numpy(res.gradient).cuda(), len(DIRS), world, rank).cpu().numpy()
+    else:
+        grad = res.gradient
+
+    units_per_step = n * len(DIRS)
+    value = units_per_step * args.steps / (ms / 1000.0)
+
+    # ---------------- e2e through the public API from pinned host memory
+    pinned = torch.empty(depth.shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = depth
+    host_frames = pinned.numpy()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = pipe.run_host(host_frames, gt)
+    t_e2e = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e_value = units_per_step * args.steps / t_e2e
+    h2d = int(depth.nbytes + gt.nbytes)
+    d2h = int(8 * (len(mine) + 1))
+
+    # ---------------- roofline of the dominant kernel
+    peak, peak_src = measured_peak()
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    cat, (cat_ms, cat_n) = dom
+    bytes_step, bytes_def = algorithmic_bytes_per_step(cat, res.stats, len(mine), k.width, k.height, n)
+    roofline = None
+    if bytes_step is not None and cat_n > 0:
+        bytes_per_launch = bytes_step * args.steps / cat_n
+        avg_ms = cat_ms / cat_n
+        achieved = bytes_per_launch / (avg_ms / 1000.0) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": cat, "avg_launch_ms": avg_ms, "launches": cat_n,
+                    "algorithmic_bytes_per_launch": bytes_per_launch, "bytes_model": bytes_def,
+                    "peak_source": peak_src}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded procedural room rendered on device; BASELINE config 2 shapes)",
+        "config": {"workload": "config2: 100 VGA frames, hashed 8^3 blocks 5 mm, 2^20 buckets, 10 CSFD directions",
+                   "frames": n, "directions": len(DIRS), "directions_per_rank": len(mine),
+                   "parallelism": f"directions sharded x{world}", "l2": "working set (hashed volume, ~GBs) >> L2"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "clocks": clk,
+        "kernel_ms_per_step": {c: v[0] / args.steps for c, v in prof.items()},
+        "gradient": [float(x) for x in grad],
+        "blocks_allocated": int(res.stats[-1, 3]),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(depth, gt, k, args.cpu_frames, args.cpu_dirs)
+        except Exception as e:  # the oracle must have been built by build()
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if args.profile_json:
+        Path(args.profile_json).write_text(json.dumps(prof, indent=1))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -269,6 +269,28 @@ struct Ldlt6 {
   }
 };
 
+// Canonical slot-tiled normal equations over the strided slot grid.
+template <typename S>
+NormalEq<S> tiled_normal_equations(const std::vector<CorrIndex>& idx, int width, int height, int stride,
+                                   const SurfaceMaps<S>& measured, const SurfaceMaps<S>& predicted,
+                                   const PoseT<S>& base) {
+  const int nxs = (width + stride - 1) / stride;
+  const int nys = (height + stride - 1) / stride;
+  const int n_slots = nxs * nys;
+  const int n_tiles = (n_slots + kTile - 1) / kTile;
+  std::vector<NormalEq<S>> partial(n_tiles);
+  for (const CorrIndex& c : idx) {
+    const int slot = (c.y / stride) * nxs + c.x / stride;
+    S j[6], r;
+    jacobian_row<S>(measured.vertices.at(c.x, c.y), predicted.vertices.at(c.u, c.v), predicted.normals.at(c.u, c.v),
+                    base, j, &r);
+    accumulate_row(partial[slot / kTile], j, r);
+  }
+  NormalEq<S> total;
+  for (int t = 0; t < n_tiles; ++t) add_into(total, partial[t]);
+  return total;
+}
+
 // icp.cpp:146-153 (with the reduction order selectable)
 inline Vec6<double> linearized_step(const std::vector<Correspondence>& corrs, const Pose& base,
                                     bool sequential = false) {
@@ -450,14 +472,27 @@ TrackResult track_frame(const V& volume, const Image<double>& depth, const Pose&
     const SurfaceMaps<double> predicted = raycast<double>(volume, prediction_pose, kl);
     stepper.reset();
     for (int it = 0; it < cfg.level_iterations[li]; ++it) {
-      const auto corrs = associate(measured, predicted, pose, prediction_pose, kl, cfg, cfg.level_pixel_stride[li]);
+      std::vector<CorrIndex> idx;
+      const int stride = std::max(1, cfg.level_pixel_stride[li]);
+      const auto corrs = associate(measured, predicted, pose, prediction_pose, kl, cfg, stride, &idx);
       out.correspondences = static_cast<int>(corrs.size());
       if (corrs.size() < 12) break;
       StepOutcome s;
       if (cfg.solver == IcpSolver::kLinearized) {
-        const NormalEq<double> ne = normal_equations(corrs, pose, !canonical_order);
+        // canonical: slot-tiled over the strided pixel grid (the device order);
+        // otherwise the reference's literal sequential sum (icp.cpp:19-27)
+        const NormalEq<double> ne = canonical_order
+                                        ? tiled_normal_equations<double>(idx, kl.width, kl.height, stride, measured,
+                                                                         predicted, pose)
+                                        : normal_equations(corrs, pose, true);
         for (int i = 0; i < 6; ++i) s.gradient[i] = 2.0 * ne.b[i];
-        s.delta = linearized_step(corrs, pose, !canonical_order);
+        double nb[6], d[6];
+        for (int i = 0; i < 6; ++i) nb[i] = -ne.b[i];
+        const Ldlt6<double> ldlt(ne.a);
+        ldlt.solve(nb, d);
+        bool finite = true;
+        for (int i = 0; i < 6; ++i) finite = finite && std::isfinite(d[i]);
+        for (int i = 0; i < 6; ++i) s.delta[i] = finite ? d[i] : 0.0;
         s.loss_after = icp_energy(corrs, s.delta, pose);
       } else if (cfg.solver == IcpSolver::kNewton) {
         const double loss0 = icp_loss(corrs, pose);

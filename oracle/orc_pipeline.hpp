@@ -39,28 +39,6 @@ SurfaceMaps<double> real_maps(const SurfaceMaps<S>& m) {
   return o;
 }
 
-// Canonical slot-tiled normal equations over the strided slot grid.
-template <typename S>
-NormalEq<S> tiled_normal_equations(const std::vector<CorrIndex>& idx, int width, int height, int stride,
-                                   const SurfaceMaps<S>& measured, const SurfaceMaps<S>& predicted,
-                                   const PoseT<S>& base) {
-  const int nxs = (width + stride - 1) / stride;
-  const int nys = (height + stride - 1) / stride;
-  const int n_slots = nxs * nys;
-  const int n_tiles = (n_slots + kTile - 1) / kTile;
-  std::vector<NormalEq<S>> partial(n_tiles);
-  for (const CorrIndex& c : idx) {
-    const int slot = (c.y / stride) * nxs + c.x / stride;
-    S j[6], r;
-    jacobian_row<S>(measured.vertices.at(c.x, c.y), predicted.vertices.at(c.u, c.v), predicted.normals.at(c.u, c.v),
-                    base, j, &r);
-    accumulate_row(partial[slot / kTile], j, r);
-  }
-  NormalEq<S> total;
-  for (int t = 0; t < n_tiles; ++t) add_into(total, partial[t]);
-  return total;
-}
-
 template <typename S, typename V, typename K>
 LiftedTrackResult<S> track_frame_lifted(const V& volume, const Image<double>& depth, const PoseT<S>& init,
                                         const IntrinsicsT<K>& k, const IcpConfig& cfg, const RaycastConfig& rc = {}) {

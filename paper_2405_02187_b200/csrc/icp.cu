@@ -420,8 +420,8 @@ int icp_tiles(int w, int h, int stride) {
 }
 
 static int reduce_chunk(int C) {
-  if (7 * C * 256 * 8 <= 200 * 1024) return 256;
-  if (7 * C * 128 * 8 <= 200 * 1024) return 128;
+  if (8 * C * (16 + 256 * 7) <= 200 * 1024) return 256;
+  if (8 * C * (16 + 128 * 7) <= 200 * 1024) return 128;
   return 64;
 }
 
@@ -439,7 +439,10 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, const TrackState* st, con
   const int chunk = reduce_chunk(C);
   const size_t smem = sizeof(double) * (16 * C + static_cast<size_t>(chunk) * 7 * C);
   const int tiles = icp_tiles(w, h, stride);
-  CSF_DISPATCH_G(G, (cudaFuncSetAttribute(k_icp_reduce<kG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+  CSF_DISPATCH_G(G, ((smem > 48 * 1024 ? (void)cudaFuncSetAttribute(k_icp_reduce<kG>,
+                                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                                  static_cast<int>(smem))
+                                         : (void)0),
                      k_icp_reduce<kG><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre,
                                                                       vim, nim, d_max, cos_max, Dp, chunk, partials,
                                                                       counts)));
