@@ -31,8 +31,23 @@ struct VoxelStore {
   int Dp;
 };
 
+// Per-thread lookup cache.  Dense volumes need none; hashed volumes keep the
+// last block id per (bx, by, bz) parity class, which holds a whole 2x2x2
+// block neighbourhood — every corner of a trilinear cell — without conflicts.
+struct NoCache {
+  CSF_DEV void reset() {}
+};
+struct BlockCache {
+  int bx[8], by[8], bz[8], id[8];
+  CSF_DEV void reset() {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bx[i] = 0x7fffffff;
+  }
+};
+
 // Dense lattice (tsdf.hpp:38-78): index (k*ny + j)*nx + i.
 struct DenseView {
+  using Cache = NoCache;
   VoxelStore vox;
   int nx, ny, nz;
   double vs, ox, oy, oz, mu, cap;
@@ -44,11 +59,13 @@ struct DenseView {
   CSF_DEV long long voxel(int i, int j, int k) const {
     return (static_cast<long long>(k) * ny + j) * nx + i;
   }
+  CSF_DEV long long voxel(int i, int j, int k, NoCache&) const { return voxel(i, j, k); }
 };
 
 // Hashed 8^3 blocks: chained buckets, chains sorted by key (builder-defined;
 // oracle/orc_tsdf.hpp HashedVolumeT).
 struct HashView {
+  using Cache = BlockCache;
   VoxelStore vox;
   const int* heads;
   const unsigned long long* keys;
@@ -73,6 +90,22 @@ struct HashView {
     if (b < 0) return -1;
     return static_cast<long long>(b) * kBlockVoxels + (((k & 7) * 8 + (j & 7)) * 8 + (i & 7));
   }
+  CSF_DEV long long voxel(int i, int j, int k, BlockCache& c) const {
+    const int bx = i >> 3, by = j >> 3, bz = k >> 3;
+    const int s = (bx & 1) | ((by & 1) << 1) | ((bz & 1) << 2);
+    int b;
+    if (c.bx[s] == bx && c.by[s] == by && c.bz[s] == bz) {
+      b = c.id[s];
+    } else {
+      b = find(bx, by, bz);
+      c.bx[s] = bx;
+      c.by[s] = by;
+      c.bz[s] = bz;
+      c.id[s] = b;
+    }
+    if (b < 0) return -1;
+    return static_cast<long long>(b) * kBlockVoxels + (((k & 7) * 8 + (j & 7)) * 8 + (i & 7));
+  }
 };
 
 // Stored field value of voxel v as S (channel group g0).
@@ -89,7 +122,7 @@ template <typename S> CSF_DEV S field_at(const VoxelStore& vs, long long v, doub
 
 // sample_tsdf (tsdf.hpp:148-177): all 8 corners must exist with W > 0.
 template <typename S, typename V>
-CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out) {
+CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out, typename V::Cache& cache) {
   const S gx = (p.v[0] - vol.ox) / vol.vs;
   const S gy = (p.v[1] - vol.oy) / vol.vs;
   const S gz = (p.v[2] - vol.oz) / vol.vs;
@@ -105,7 +138,7 @@ CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out) {
     for (int dj = 0; dj < 2; ++dj)
 #pragma unroll
       for (int di = 0; di < 2; ++di) {
-        const long long v = vol.voxel(i0 + di, j0 + dj, k0 + dk);
+        const long long v = vol.voxel(i0 + di, j0 + dj, k0 + dk, cache);
         if (v < 0) return false;
         const double2 rw = vol.vox.rw[v];
         if (!(rw.y > 0.0)) return false;
@@ -117,10 +150,16 @@ CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out) {
   *out = accum;
   return true;
 }
+template <typename S, typename V>
+CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out) {
+  typename V::Cache c;
+  c.reset();
+  return sample_tsdf<S>(vol, p, g0, out, c);
+}
 
 // sample_gradient (tsdf.hpp:181-196)
 template <typename S, typename V>
-CSF_DEV bool sample_gradient(const V& vol, const V3<S>& p, int g0, V3<S>* g) {
+CSF_DEV bool sample_gradient(const V& vol, const V3<S>& p, int g0, V3<S>* g, typename V::Cache& cache) {
   const double h = vol.vs;
 #pragma unroll
   for (int axis = 0; axis < 3; ++axis) {
@@ -128,8 +167,8 @@ CSF_DEV bool sample_gradient(const V& vol, const V3<S>& p, int g0, V3<S>* g) {
     lo.v[axis] = lo.v[axis] - h;
     hi.v[axis] = hi.v[axis] + h;
     S flo, fhi;
-    if (!sample_tsdf<S>(vol, lo, g0, &flo)) return false;
-    if (!sample_tsdf<S>(vol, hi, g0, &fhi)) return false;
+    if (!sample_tsdf<S>(vol, lo, g0, &flo, cache)) return false;
+    if (!sample_tsdf<S>(vol, hi, g0, &fhi, cache)) return false;
     g->v[axis] = (fhi - flo) / (2.0 * h);
   }
   return true;
@@ -191,48 +230,51 @@ template <typename S> CSF_DEV void swap_s(S& a, S& b) {
 template <typename S> CSF_DEV double absre(const S& x) { return fabs(re(x)); }
 
 // Factor the symmetric matrix given by its lower triangle and solve A x = rhs.
-// Returns false when Eigen would report info() != Success.
+// Returns false when Eigen would report info() != Success.  The pivoted
+// (data-dependent) indexing runs on `ws`, a 48-scalar workspace the caller
+// places in shared memory: m[36] (row-major), temp[6], x[6].
 template <typename S>
-CSF_DEV bool ldlt6_solve(const S* a_lower, const S* rhs, S* dst) {
-  S m[6][6];
+CSF_DEV bool ldlt6_solve(const S* a_lower, const S* rhs, S* dst, S* ws) {
+  S* m = ws;
+  S* temp = ws + 36;
+  S* x = ws + 42;
   int transp[6];
   bool ok = true;
 #pragma unroll
   for (int r = 0; r < 6; ++r)
 #pragma unroll
-    for (int c = 0; c < 6; ++c) m[r][c] = r >= c ? a_lower[tri(r, c)] : a_lower[tri(c, r)];
-  S temp[6];
+    for (int c = 0; c < 6; ++c) m[6 * r + c] = r >= c ? a_lower[tri(r, c)] : a_lower[tri(c, r)];
   for (int k = 0; k < 6; ++k) {
     int piv = k;
-    double best = absre(m[k][k]);
+    double best = absre(m[7 * k]);
     for (int i = k + 1; i < 6; ++i)
-      if (absre(m[i][i]) > best) {
-        best = absre(m[i][i]);
+      if (absre(m[7 * i]) > best) {
+        best = absre(m[7 * i]);
         piv = i;
       }
     transp[k] = piv;
     if (piv != k) {
-      for (int j = 0; j < k; ++j) swap_s(m[k][j], m[piv][j]);
-      for (int i = piv + 1; i < 6; ++i) swap_s(m[i][k], m[i][piv]);
-      swap_s(m[k][k], m[piv][piv]);
+      for (int j = 0; j < k; ++j) swap_s(m[6 * k + j], m[6 * piv + j]);
+      for (int i = piv + 1; i < 6; ++i) swap_s(m[6 * i + k], m[6 * i + piv]);
+      swap_s(m[7 * k], m[7 * piv]);
       for (int i = k + 1; i < piv; ++i) {
-        const S tmp = m[i][k];
-        m[i][k] = m[piv][i];
-        m[piv][i] = tmp;
+        const S tmp = m[6 * i + k];
+        m[6 * i + k] = m[6 * piv + i];
+        m[6 * piv + i] = tmp;
       }
     }
     if (k > 0) {
-      for (int j = 0; j < k; ++j) temp[j] = m[j][j] * m[k][j];
-      S s = m[k][0] * temp[0];
-      for (int j = 1; j < k; ++j) s = s + m[k][j] * temp[j];
-      m[k][k] = m[k][k] - s;
+      for (int j = 0; j < k; ++j) temp[j] = m[7 * j] * m[6 * k + j];
+      S s = m[6 * k] * temp[0];
+      for (int j = 1; j < k; ++j) s = s + m[6 * k + j] * temp[j];
+      m[7 * k] = m[7 * k] - s;
       for (int i = k + 1; i < 6; ++i) {
-        S si = m[i][0] * temp[0];
-        for (int j = 1; j < k; ++j) si = si + m[i][j] * temp[j];
-        m[i][k] = m[i][k] - si;
+        S si = m[6 * i] * temp[0];
+        for (int j = 1; j < k; ++j) si = si + m[6 * i + j] * temp[j];
+        m[6 * i + k] = m[6 * i + k] - si;
       }
     }
-    const S akk = m[k][k];
+    const S akk = m[7 * k];
     const bool pivot_valid = absre(akk) > 0.0;
     if (k == 0 && !pivot_valid) {
       ok = false;
@@ -241,29 +283,32 @@ CSF_DEV bool ldlt6_solve(const S* a_lower, const S* rhs, S* dst) {
     }
     if (k < 5) {
       if (pivot_valid) {
-        for (int i = k + 1; i < 6; ++i) m[i][k] = m[i][k] / akk;
+        for (int i = k + 1; i < 6; ++i) m[6 * i + k] = m[6 * i + k] / akk;
       } else {
-        for (int i = k + 1; i < 6; ++i) ok = ok && re(m[i][k]) == 0.0;
+        for (int i = k + 1; i < 6; ++i) ok = ok && re(m[6 * i + k]) == 0.0;
       }
     }
   }
-  for (int i = 0; i < 6; ++i) dst[i] = rhs[i];
-  for (int k = 0; k < 6; ++k) swap_s(dst[k], dst[transp[k]]);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) x[i] = rhs[i];
+  for (int k = 0; k < 6; ++k) swap_s(x[k], x[transp[k]]);
   for (int i = 0; i < 6; ++i)
-    for (int j = i + 1; j < 6; ++j) dst[j] = dst[j] - dst[i] * m[j][i];
+    for (int j = i + 1; j < 6; ++j) x[j] = x[j] - x[i] * m[6 * j + i];
   const double tol = 2.2250738585072014e-308;  // numeric_limits<double>::min()
   for (int i = 0; i < 6; ++i) {
-    if (absre(m[i][i]) > tol)
-      dst[i] = dst[i] / m[i][i];
+    if (absre(m[7 * i]) > tol)
+      x[i] = x[i] / m[7 * i];
     else
-      dst[i] = lit<S>(0.0);
+      x[i] = lit<S>(0.0);
   }
   for (int i = 4; i >= 0; --i) {
-    S s = m[i + 1][i] * dst[i + 1];
-    for (int j = i + 2; j < 6; ++j) s = s + m[j][i] * dst[j];
-    dst[i] = dst[i] - s;
+    S s = m[6 * (i + 1) + i] * x[i + 1];
+    for (int j = i + 2; j < 6; ++j) s = s + m[6 * j + i] * x[j];
+    x[i] = x[i] - s;
   }
-  for (int k = 5; k >= 0; --k) swap_s(dst[k], dst[transp[k]]);
+  for (int k = 5; k >= 0; --k) swap_s(x[k], x[transp[k]]);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) dst[i] = x[i];
   return ok;
 }
 

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* __restrict
 }
 
 template <int G>
-__global__ void __launch_bounds__(512) k_icp_solve(TrackState* st, const double* __restrict__ partials,
+__global__ void __launch_bounds__(256) k_icp_solve(TrackState* st, const double* __restrict__ partials,
                                                    const int* __restrict__ counts, int n_tiles, double* pose, int Dp,
                                                    int level, double tol) {
   if (st->level_done) return;
@@ -215,6 +215,8 @@ __global__ void __launch_bounds__(512) k_icp_solve(TrackState* st, const double*
   __shared__ int s_n, s_finite;
   const int C = 1 + Dp;
   const int n_acc = 27 * C;
+  // per-group LDLT workspace after the accumulators (48 scalars each)
+  S* ws = reinterpret_cast<S*>(sm + n_acc) + 48 * threadIdx.x;
   for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
     double total = 0.0;
     for (int t = 0; t < n_tiles; ++t) total = total + partials[static_cast<long long>(t) * n_acc + a];
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(512) k_icp_solve(TrackState* st, const double*
     for (int q = 0; q < 21; ++q) a[q] = load_ch<S>(sm + q * C, g0, G);
 #pragma unroll
     for (int i = 0; i < 6; ++i) nb[i] = -load_ch<S>(sm + (21 + i) * C, g0, G);
-    ldlt6_solve<S>(a, nb, d);
+    ldlt6_solve<S>(a, nb, d, ws);
     bool fin = true;
 #pragma unroll
     for (int i = 0; i < 6; ++i) fin = fin && finite_s(d[i]);
@@ -439,28 +441,53 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, const TrackState* st, con
   const int chunk = reduce_chunk(C);
   const size_t smem = sizeof(double) * (16 * C + static_cast<size_t>(chunk) * 7 * C);
   const int tiles = icp_tiles(w, h, stride);
-  CSF_DISPATCH_G(G, ((smem > 48 * 1024 ? (void)cudaFuncSetAttribute(k_icp_reduce<kG>,
-                                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                                  static_cast<int>(smem))
-                                         : (void)0),
-                     k_icp_reduce<kG><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre,
-                                                                      vim, nim, d_max, cos_max, Dp, chunk, partials,
-                                                                      counts)));
+  // J/r rows are evaluated in channel groups of 2 (or 1): register-light,
+  // any width that divides Dp addresses the same channel layout.
+  const int RG = G == 0 ? 0 : (Dp % 2 == 0 ? 2 : 1);
+  switch (RG) {
+    case 0:
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_icp_reduce<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_icp_reduce<0><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
+                                                      cos_max, Dp, chunk, partials, counts);
+      break;
+    case 1:
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_icp_reduce<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_icp_reduce<1><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
+                                                      cos_max, Dp, chunk, partials, counts);
+      break;
+    default:
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_icp_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_icp_reduce<2><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
+                                                      cos_max, Dp, chunk, partials, counts);
+  }
   ++*L.launches;
   chk("icp_reduce");
 }
 
 void launch_icp_solve(const Launch& L, int G, int Dp, TrackState* st, const double* partials, const int* counts,
                       int n_tiles, double* pose, int level, double tol) {
-  const size_t smem = sizeof(double) * 27 * (1 + Dp);
-  CSF_DISPATCH_G(G, (k_icp_solve<kG><<<1, 512, smem, L.stream>>>(st, partials, counts, n_tiles, pose, Dp, level, tol)));
+  // The solve is latency-bound and register-heavy (6x6 LDLT, exp map, pose
+  // compose): one thread per channel in L<1> arithmetic keeps it in registers.
+  const int GS = G == 0 ? 0 : 1;
+  const int ngroups = GS == 0 ? 1 : Dp;
+  const size_t smem = sizeof(double) * 27 * (1 + Dp) + sizeof(double) * (1 + GS) * 48 * ngroups;
+  if (GS == 0)
+    k_icp_solve<0><<<1, 256, smem, L.stream>>>(st, partials, counts, n_tiles, pose, Dp, level, tol);
+  else
+    k_icp_solve<1><<<1, 256, smem, L.stream>>>(st, partials, counts, n_tiles, pose, Dp, level, tol);
   ++*L.launches;
   chk("icp_solve");
 }
 
 void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,
                  const double* intr_base, double* pose, double* intr_levels, int levels) {
-  CSF_DISPATCH_G(G, (k_seed<kG><<<1, 64, 0, L.stream>>>(dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp)));
+  if (G == 0)
+    k_seed<0><<<1, 64, 0, L.stream>>>(dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp);
+  else
+    k_seed<1><<<1, 64, 0, L.stream>>>(dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp);
   ++*L.launches;
   chk("seed");
 }
@@ -480,7 +507,10 @@ void launch_frame_end(const Launch& L, TrackState* st, const double* pose, doubl
 
 void launch_objective(const Launch& L, int G, int Dp, int D, const double* traj, const double* gt, int n_frames,
                       int kind, double h, double* out) {
-  CSF_DISPATCH_G(G, (k_objective<kG><<<1, 64, 0, L.stream>>>(traj, gt, n_frames, kind, h, Dp, D, out)));
+  if (G == 0)
+    k_objective<0><<<1, 64, 0, L.stream>>>(traj, gt, n_frames, kind, h, Dp, D, out);
+  else
+    k_objective<1><<<1, 64, 0, L.stream>>>(traj, gt, n_frames, kind, h, Dp, D, out);
   ++*L.launches;
   chk("objective");
 }

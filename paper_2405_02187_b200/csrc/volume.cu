@@ -373,12 +373,14 @@ __global__ void __launch_bounds__(128) k_raycast(V vol, const double* __restrict
   }
   if (t0 >= t1) return;
 
+  typename V::Cache cache;
+  cache.reset();
   bool have_prev = false, crossed = false;
   double alpha_prev = 0.0, f_prev = 0.0, alpha_hit = 0.0;
   for (double alpha = t0; alpha <= t1; alpha += step) {
     const V3<double> p = mk3<double>(o.v[0] + alpha * dir.v[0], o.v[1] + alpha * dir.v[1], o.v[2] + alpha * dir.v[2]);
     double f;
-    if (!sample_tsdf<double>(vol, p, 0, &f)) {
+    if (!sample_tsdf<double>(vol, p, 0, &f, cache)) {
       have_prev = false;
       continue;
     }
@@ -413,13 +415,13 @@ __global__ void __launch_bounds__(128) k_raycast(V vol, const double* __restrict
       return mk3<S>(os.v[0] + a * dirs.v[0], os.v[1] + a * dirs.v[1], os.v[2] + a * dirs.v[2]);
     };
     S fl_prev, fl;
-    sample_tsdf<S>(vol, at(alpha_prev), g0, &fl_prev);
-    sample_tsdf<S>(vol, at(alpha_hit), g0, &fl);
+    sample_tsdf<S>(vol, at(alpha_prev), g0, &fl_prev, cache);
+    sample_tsdf<S>(vol, at(alpha_hit), g0, &fl, cache);
     const double span = alpha_hit - alpha_prev;
     const S astar = alpha_prev - (span * fl_prev) / (fl - fl_prev);
     const V3<S> v = mk3<S>(os.v[0] + astar * dirs.v[0], os.v[1] + astar * dirs.v[1], os.v[2] + astar * dirs.v[2]);
     V3<S> grad;
-    if (!sample_gradient<S>(vol, v, g0, &grad)) return;
+    if (!sample_gradient<S>(vol, v, g0, &grad, cache)) return;
     const S len2 = dot3(grad, grad);
     if (!(re(len2) > 0.0)) return;
     const S ln = sqrt_s(len2);
@@ -479,6 +481,20 @@ int pick_group(int D) {
     case 5: { constexpr int kG = 5; BODY; } break;    \
     case 6: { constexpr int kG = 6; BODY; } break;    \
     default: std::fprintf(stderr, "csf_b200: no kernel for group width %d\n", G); \
+  }
+
+// The raycast's lifted epilogue is register-heavy: it evaluates channel
+// groups of width 2 (or 1) regardless of the volume's group width.
+static int raycast_group(int G, int Dp) {
+  if (G == 0) return 0;
+  return (Dp % 2 == 0) ? 2 : 1;
+}
+#define CSF_DISPATCH_RG(G, BODY)                      \
+  switch (G) {                                        \
+    case 0: { constexpr int kG = 0; BODY; } break;    \
+    case 1: { constexpr int kG = 1; BODY; } break;    \
+    case 2: { constexpr int kG = 2; BODY; } break;    \
+    default: std::fprintf(stderr, "csf_b200: no raycast kernel for group width %d\n", G); \
   }
 
 static DenseView dense_view(const DenseDev& v, int Dp) {
@@ -584,8 +600,10 @@ void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, con
   box.hi[2] = v.oz + v.vs * (static_cast<double>(v.nz) - 1.0);
   const size_t smem = sizeof(double) * 16 * (1 + Dp);
   const int grid = (w * h + 127) / 128;
-  CSF_DISPATCH_G(G, (k_raycast<kG, DenseView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
-                                                                             far_clip, step, box, vre, nre, vim, nim)));
+  const int RG = raycast_group(G, Dp);
+  CSF_DISPATCH_RG(RG, (k_raycast<kG, DenseView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
+                                                                               far_clip, step, box, vre, nre, vim,
+                                                                               nim)));
   ++*L.launches;
   chk("raycast_dense");
 }
@@ -598,8 +616,10 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
   box.use = false;
   const size_t smem = sizeof(double) * 16 * (1 + Dp);
   const int grid = (w * h + 127) / 128;
-  CSF_DISPATCH_G(G, (k_raycast<kG, HashView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
-                                                                            far_clip, step, box, vre, nre, vim, nim)));
+  const int RG = raycast_group(G, Dp);
+  CSF_DISPATCH_RG(RG, (k_raycast<kG, HashView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
+                                                                              far_clip, step, box, vre, nre, vim,
+                                                                              nim)));
   ++*L.launches;
   chk("raycast_hashed");
 }
