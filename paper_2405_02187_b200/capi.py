@@ -10,7 +10,7 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_build" / "libcsf_b200.so"
+LIB_PATH = Path(os.environ["CSF_B200_LIB"]) if os.environ.get("CSF_B200_LIB") else _HERE / "_build" / "libcsf_b200.so"
 
 CSF_OK, CSF_EINVAL, CSF_EDOMAIN, CSF_ERUNTIME, CSF_ECUDA, CSF_ENOMEM = 0, 1, 2, 3, 4, 5
 CSF_MAX_DIRECTIONS = 36

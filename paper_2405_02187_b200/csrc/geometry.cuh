@@ -37,11 +37,13 @@ struct VoxelStore {
 struct NoCache {
   CSF_DEV void reset() {}
 };
+// The 8 entries live in shared memory (a per-thread slice supplied by the
+// kernel): data-dependent indexing stays out of local memory.
 struct BlockCache {
-  int bx[8], by[8], bz[8], id[8];
+  int4* e;  // (bx, by, bz, id) per parity class
   CSF_DEV void reset() {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) bx[i] = 0x7fffffff;
+    for (int i = 0; i < 8; ++i) e[i].x = 0x7fffffff;
   }
 };
 
@@ -94,14 +96,12 @@ struct HashView {
     const int bx = i >> 3, by = j >> 3, bz = k >> 3;
     const int s = (bx & 1) | ((by & 1) << 1) | ((bz & 1) << 2);
     int b;
-    if (c.bx[s] == bx && c.by[s] == by && c.bz[s] == bz) {
-      b = c.id[s];
+    const int4 ce = c.e[s];
+    if (ce.x == bx && ce.y == by && ce.z == bz) {
+      b = ce.w;
     } else {
       b = find(bx, by, bz);
-      c.bx[s] = bx;
-      c.by[s] = by;
-      c.bz[s] = bz;
-      c.id[s] = b;
+      c.e[s] = make_int4(bx, by, bz, b);
     }
     if (b < 0) return -1;
     return static_cast<long long>(b) * kBlockVoxels + (((k & 7) * 8 + (j & 7)) * 8 + (i & 7));
@@ -150,10 +150,9 @@ CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out, typename 
   *out = accum;
   return true;
 }
-template <typename S, typename V>
-CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out) {
-  typename V::Cache c;
-  c.reset();
+template <typename S>
+CSF_DEV bool sample_tsdf(const DenseView& vol, const V3<S>& p, int g0, S* out) {
+  NoCache c;
   return sample_tsdf<S>(vol, p, g0, out, c);
 }
 

@@ -321,6 +321,8 @@ __global__ void __launch_bounds__(128) k_raycast(V vol, const double* __restrict
   const int C = 1 + Dp;
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
   for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
+  // per-thread block-lookup cache slice (hashed volumes): 8 x int4 after the pose
+  int4* cache_mem = reinterpret_cast<int4*>(sm + 16 * C) + 8 * threadIdx.x;
   __syncthreads();
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= w * h) return;
@@ -374,6 +376,8 @@ __global__ void __launch_bounds__(128) k_raycast(V vol, const double* __restrict
   if (t0 >= t1) return;
 
   typename V::Cache cache;
+  if constexpr (V::kHashed) cache.e = cache_mem;
+  (void)cache_mem;
   cache.reset();
   bool have_prev = false, crossed = false;
   double alpha_prev = 0.0, f_prev = 0.0, alpha_hit = 0.0;
@@ -487,7 +491,11 @@ int pick_group(int D) {
 // groups of width 2 (or 1) regardless of the volume's group width.
 static int raycast_group(int G, int Dp) {
   if (G == 0) return 0;
+#ifdef CSF_RAYCAST_RG1
+  return 1;
+#else
   return (Dp % 2 == 0) ? 2 : 1;
+#endif
 }
 #define CSF_DISPATCH_RG(G, BODY)                      \
   switch (G) {                                        \
@@ -614,7 +622,7 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
   const HashView view = hash_view(v, Dp);
   Box box;
   box.use = false;
-  const size_t smem = sizeof(double) * 16 * (1 + Dp);
+  const size_t smem = sizeof(double) * 16 * (1 + Dp) + sizeof(int4) * 8 * 128;
   const int grid = (w * h + 127) / 128;
   const int RG = raycast_group(G, Dp);
   CSF_DISPATCH_RG(RG, (k_raycast<kG, HashView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
