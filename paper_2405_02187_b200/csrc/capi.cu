@@ -152,6 +152,7 @@ struct csf_volume_s {
   DevBuf<unsigned char> a_cub;
   // stage buffers for the single-call APIs
   DevBuf<double> s_depth, s_pose, s_intr, s_vre, s_nre, s_vim, s_nim;
+  DevBuf<double2> s_hits;
 
   ~csf_volume_s() {
     rw.release(); fim.release(); heads.release(); next.release(); coords.release(); nblocks.release(); keys.release();
@@ -160,6 +161,7 @@ struct csf_volume_s {
     a_counters.release(); a_cub.release();
     s_depth.release(); s_pose.release(); s_intr.release(); s_vre.release(); s_nre.release(); s_vim.release();
     s_nim.release();
+    s_hits.release();
   }
 };
 
@@ -234,17 +236,17 @@ int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double*
 }
 
 void raycast_dev(csf_volume v, const double* d_pose, const double* d_intr, int w, int h, const csf_raycast_cfg& rc,
-                 double* vre, double* nre, double* vim, double* nim) {
+                 double2* hits, double* vre, double* nre, double* vim, double* nim) {
   const Launch L = launch_of(v->ctx);
   const double mu = v->hashed ? v->hash.mu : v->dense.mu;
   const double step = rc.step_fraction * mu;
   PROF(v->ctx, kPRaycast);
   if (v->hashed)
-    launch_raycast_hashed(L, v->hash, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, vre, nre,
-                          vim, nim);
+    launch_raycast_hashed(L, v->hash, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, hits, vre,
+                          nre, vim, nim);
   else
-    launch_raycast_dense(L, v->dense, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, vre, nre,
-                         vim, nim);
+    launch_raycast_dense(L, v->dense, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, hits, vre,
+                         nre, vim, nim);
 }
 
 // Host lifted array [n][1+D] -> padded [n][1+Dp]
@@ -637,9 +639,10 @@ extern "C" int csf_raycast(csf_volume v, const double* pose, const double* intr,
   CUDA_TRY(ctx, v->s_nre.alloc(P * 3));
   CUDA_TRY(ctx, v->s_vim.alloc(P * 3 * std::max(v->Dp, 1)));
   CUDA_TRY(ctx, v->s_nim.alloc(P * 3 * std::max(v->Dp, 1)));
+  CUDA_TRY(ctx, v->s_hits.alloc(P));
   CUDA_TRY(ctx, cudaMemcpyAsync(v->s_pose.p, pp.data(), sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(v->s_intr.p, kp.data(), sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
-  raycast_dev(v, v->s_pose.p, v->s_intr.p, w, h, rc, v->s_vre.p, v->s_nre.p, v->s_vim.p, v->s_nim.p);
+  raycast_dev(v, v->s_pose.p, v->s_intr.p, w, h, rc, v->s_hits.p, v->s_vre.p, v->s_nre.p, v->s_vim.p, v->s_nim.p);
   std::vector<double> vre(P * 3), nre(P * 3), vim(P * 3 * std::max(v->Dp, 1)), nim(P * 3 * std::max(v->Dp, 1));
   CUDA_TRY(ctx, cudaMemcpyAsync(vre.data(), v->s_vre.p, sizeof(double) * P * 3, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(nre.data(), v->s_nre.p, sizeof(double) * P * 3, cudaMemcpyDeviceToHost, ctx->stream));
@@ -676,7 +679,9 @@ struct csf_pipeline_s {
       out;
   DevBuf<int> counts, stats, dirs;
   DevBuf<TrackState> st;
+  DevBuf<double2> hits;
   ~csf_pipeline_s() {
+    hits.release();
     frames.release(); gt.release(); raw.release(); pyr0.release(); pyr1.release(); pyr2.release(); vre.release();
     nre.release(); vim.release(); nim.release(); partials.release(); pose.release(); pred_pose.release();
     intr_levels.release(); traj.release(); kbase.release(); out.release(); counts.release(); stats.release();
@@ -743,6 +748,7 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   A(p->kbase.alloc(4));
   A(p->out.alloc(2 + CSF_MAX_DIRECTIONS));
   A(p->st.alloc(1));
+  A(p->hits.alloc(P));
   if (e != cudaSuccess) {
     delete p;
     return fail(ctx, CSF_ENOMEM, std::string("csf_pipeline_create: ") + cudaGetErrorString(e));
@@ -843,7 +849,7 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
       const int wl = W >> level, hl = H >> level;
       const double* kl = p->intr_levels.p + level * 4 * C;
       launch_level_begin(L, st, p->pose.p, p->pred_pose.p, p->Dp);
-      raycast_dev(v, p->pred_pose.p, kl, wl, hl, cfg.rc, p->vre.p, p->nre.p, p->vim.p, p->nim.p);
+      raycast_dev(v, p->pred_pose.p, kl, wl, hl, cfg.rc, p->hits.p, p->vre.p, p->nre.p, p->vim.p, p->nim.p);
       const int stride = std::max(1, cfg.icp.level_pixel_stride[li]);
       const int tiles = icp_tiles(wl, hl, stride);
       for (int it = 0; it < cfg.icp.level_iterations[li]; ++it) {
@@ -923,7 +929,9 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
   DevBuf<double> dd, raw, pyr0, pyr1, pyr2, vre, nre, pose, pred, intr, partials;
   DevBuf<int> counts;
   DevBuf<TrackState> st;
+  DevBuf<double2> hits;
   const int tiles_max = icp_tiles(w, h, 1);
+  CUDA_TRY(ctx, hits.alloc(P));
   CUDA_TRY(ctx, dd.alloc(P));
   CUDA_TRY(ctx, raw.alloc(P));
   CUDA_TRY(ctx, pyr0.alloc(P));
@@ -971,7 +979,7 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
     const int level = levels - 1 - li;
     const int wl = w >> level, hl = h >> level;
     launch_level_begin(L, st.p, pose.p, pred.p, 0);
-    raycast_dev(&real_view, pred.p, intr.p + 4 * level, wl, hl, rcfg, vre.p, nre.p, nullptr, nullptr);
+    raycast_dev(&real_view, pred.p, intr.p + 4 * level, wl, hl, rcfg, hits.p, vre.p, nre.p, nullptr, nullptr);
     const int stride = std::max(1, cfg.level_pixel_stride[li]);
     tiles_last = icp_tiles(wl, hl, stride);
     for (int it = 0; it < cfg.level_iterations[li]; ++it) {

@@ -85,12 +85,13 @@ void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, c
                              const double* depth, int w, int h, const double* pose, const double* intr);
 void launch_allocate(const Launch& L, const HashDev& v, int Dp, AllocScratch& a, const double* depth, int w, int h,
                      const double* pose, const double* intr);
+// hits: [w*h] scratch (alpha_prev, alpha) of the zero crossing per pixel
 void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* pose, const double* intr,
-                          int w, int h, double near_clip, double far_clip, double step, double* vre, double* nre,
-                          double* vim, double* nim);
+                          int w, int h, double near_clip, double far_clip, double step, double2* hits, double* vre,
+                          double* nre, double* vim, double* nim);
 void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, const double* pose, const double* intr,
-                           int w, int h, double near_clip, double far_clip, double step, double* vre, double* nre,
-                           double* vim, double* nim);
+                           int w, int h, double near_clip, double far_clip, double step, double2* hits, double* vre,
+                           double* nre, double* vim, double* nim);
 void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp);
 
 // ---- icp.cu

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "csf_internal.h"
 #include "geometry.cuh"
@@ -305,51 +306,108 @@ __global__ void k_alloc_finalize(int* n_blocks, int max_blocks, const int* first
 }
 
 // ----------------------------------------------------------------------------
-// Raycast (tsdf.hpp:209-284)
+// Raycast (tsdf.hpp:209-284) as two kernels:
+//   k_raycast_march — one thread per pixel, real channel only: the slab clip,
+//     the fixed-step march and the zero-crossing test (every branch of the
+//     reference reads real parts).  Hashed volumes skip the samples whose
+//     base corner lies in an unallocated block: those samples are invalid by
+//     definition, alpha still advances by the same repeated addition, and the
+//     skip stops 1e-6 m before the block's analytic exit so the exact
+//     per-sample test decides every boundary case.  Output: the crossing's
+//     (alpha_prev, alpha) or a miss.
+//   k_raycast_lift — one thread per (hit pixel, channel group): re-evaluates
+//     the two samples at the recorded alphas (bit-identical real parts), the
+//     interpolated vertex and the gradient normal in L<G>.
 // ----------------------------------------------------------------------------
 struct Box {
   bool use;
   double lo[3], hi[3];
 };
 
-template <int G, typename V>
-__global__ void __launch_bounds__(128) k_raycast(V vol, const double* __restrict__ pose, const double* __restrict__ intr,
-                                                 int w, int h, int Dp, double near_clip, double far_clip, double step,
-                                                 Box box, double* __restrict__ vre, double* __restrict__ nre,
-                                                 double* __restrict__ vim, double* __restrict__ nim) {
-  extern __shared__ double sm[];
+// Real trilinear sample with all eight corner loads issued before any test.
+template <typename V>
+CSF_DEV bool sample_real(const V& vol, double px, double py, double pz, typename V::Cache& cache, double* out) {
+  const double gx = (px - vol.ox) / vol.vs;
+  const double gy = (py - vol.oy) / vol.vs;
+  const double gz = (pz - vol.oz) / vol.vs;
+  const int i0 = ifloor(gx), j0 = ifloor(gy), k0 = ifloor(gz);
+  if (!vol.cell_in_grid(i0, j0, k0)) return false;
+  long long v[8];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    v[c] = vol.voxel(i0 + (c & 1), j0 + ((c >> 1) & 1), k0 + (c >> 2), cache);
+    ok = ok && v[c] >= 0;
+  }
+  if (!ok) return false;
+  double2 rw[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) rw[c] = vol.vox.rw[v[c]];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) ok = ok && rw[c].y > 0.0;
+  if (!ok) return false;
+  const double fx = gx - static_cast<double>(i0);
+  const double fy = gy - static_cast<double>(j0);
+  const double fz = gz - static_cast<double>(k0);
+  double accum = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double wx = (c & 1) ? fx : 1.0 - fx;
+    const double wy = ((c >> 1) & 1) ? fy : 1.0 - fy;
+    const double wz = (c >> 2) ? fz : 1.0 - fz;
+    accum = accum + ((wx * wy) * wz) * rw[c].x;
+  }
+  *out = accum;
+  return true;
+}
+
+// Analytic exit distance of the ray from block (bx, by, bz).
+CSF_DEV double block_exit(const HashView& vol, int bx, int by, int bz, const V3<double>& o, const V3<double>& dir) {
+  const int b[3] = {bx, by, bz};
+  const double org[3] = {vol.ox, vol.oy, vol.oz};
+  double t = 1e300;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double d = dir.v[a];
+    if (d > 0.0) {
+      const double hi = org[a] + vol.vs * static_cast<double>(8 * b[a] + 8);
+      t = fmin(t, (hi - o.v[a]) / d);
+    } else if (d < 0.0) {
+      const double lo = org[a] + vol.vs * static_cast<double>(8 * b[a]);
+      t = fmin(t, (lo - o.v[a]) / d);
+    }
+  }
+  return t;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __restrict__ pose,
+                                                       const double* __restrict__ intr, int w, int h, int Dp,
+                                                       double near_clip, double far_clip, double step, Box box,
+                                                       double2* __restrict__ hits, double* __restrict__ vre,
+                                                       double* __restrict__ nre) {
+  __shared__ double s_pose[16];
+  __shared__ int4 s_cache[V::kHashed ? 8 * 128 : 1];
   const int C = 1 + Dp;
-  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
-  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
-  // per-thread block-lookup cache slice (hashed volumes): 8 x int4 after the pose
-  int4* cache_mem = reinterpret_cast<int4*>(sm + 16 * C) + 8 * threadIdx.x;
+  if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
+  else if (threadIdx.x < 16) s_pose[threadIdx.x] = intr[(threadIdx.x - 12) * C];
   __syncthreads();
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= w * h) return;
   const int x = pix % w, y = pix / w;
-  const double* kk = sm + 12 * C;
-
-  // real ray (identical to the real part of the lifted ray below)
   Pose<double> c2w;
 #pragma unroll
-  for (int e = 0; e < 9; ++e) c2w.R.m[e] = sm[e * C];
+  for (int e = 0; e < 9; ++e) c2w.R.m[e] = s_pose[e];
 #pragma unroll
-  for (int e = 0; e < 3; ++e) c2w.t.v[e] = sm[(9 + e) * C];
-  const V3<double> dc = mk3<double>((static_cast<double>(x) - kk[2 * C]) / kk[0],
-                                    (static_cast<double>(y) - kk[3 * C]) / kk[C], 1.0 * 1.0);
+  for (int e = 0; e < 3; ++e) c2w.t.v[e] = s_pose[9 + e];
+  const double fxk = s_pose[12], fyk = s_pose[13], cxk = s_pose[14], cyk = s_pose[15];
+  const V3<double> dc = mk3<double>((static_cast<double>(x) - cxk) / fxk, (static_cast<double>(y) - cyk) / fyk, 1.0);
   const double rn = sqrt(dot3(dc, dc));
   const V3<double> dir = matvec(c2w.R, mk3<double>(dc.v[0] / rn, dc.v[1] / rn, dc.v[2] / rn));
   const V3<double> o = c2w.t;
-
-  double* vr = vre + static_cast<long long>(pix) * 3;
-  double* nr = nre + static_cast<long long>(pix) * 3;
 #pragma unroll
-  for (int c = 0; c < 3; ++c) vr[c] = nr[c] = 0.0;
-  if (G > 0) {
-    double* vi = vim + static_cast<long long>(pix) * 3 * Dp;
-    double* ni = nim + static_cast<long long>(pix) * 3 * Dp;
-    for (int c = 0; c < 3 * Dp; ++c) vi[c] = ni[c] = 0.0;
-  }
+  for (int c = 0; c < 3; ++c) vre[3LL * pix + c] = nre[3LL * pix + c] = 0.0;
+  hits[pix] = make_double2(0.0, -1.0);  // y < 0: no crossing
 
   double t0 = near_clip, t1 = far_clip;
   if (box.use) {
@@ -376,74 +434,110 @@ __global__ void __launch_bounds__(128) k_raycast(V vol, const double* __restrict
   if (t0 >= t1) return;
 
   typename V::Cache cache;
-  if constexpr (V::kHashed) cache.e = cache_mem;
-  (void)cache_mem;
+  if constexpr (V::kHashed) cache.e = s_cache + 8 * threadIdx.x;
   cache.reset();
-  bool have_prev = false, crossed = false;
-  double alpha_prev = 0.0, f_prev = 0.0, alpha_hit = 0.0;
-  for (double alpha = t0; alpha <= t1; alpha += step) {
-    const V3<double> p = mk3<double>(o.v[0] + alpha * dir.v[0], o.v[1] + alpha * dir.v[1], o.v[2] + alpha * dir.v[2]);
+  bool have_prev = false;
+  double alpha_prev = 0.0, f_prev = 0.0;
+  double alpha = t0;
+  while (alpha <= t1) {
+    const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1], pz = o.v[2] + alpha * dir.v[2];
+    if constexpr (V::kHashed) {
+      // unallocated base block: every sample until the block exit is invalid
+      const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
+                k0 = ifloor((pz - vol.oz) / vol.vs);
+      if (vol.voxel(i0, j0, k0, cache) < 0) {
+        have_prev = false;
+        const double lim = block_exit(vol, i0 >> 3, j0 >> 3, k0 >> 3, o, dir) - 1e-6;
+        alpha += step;
+        while (alpha < lim && alpha <= t1) alpha += step;
+        continue;
+      }
+    }
     double f;
-    if (!sample_tsdf<double>(vol, p, 0, &f, cache)) {
+    if (!sample_real(vol, px, py, pz, cache, &f)) {
       have_prev = false;
+      alpha += step;
       continue;
     }
     if (have_prev && f_prev > 0.0 && f < 0.0) {
-      crossed = true;
-      alpha_hit = alpha;
-      break;
+      hits[pix] = make_double2(alpha_prev, alpha);
+      return;
     }
     have_prev = true;
     alpha_prev = alpha;
     f_prev = f;
+    alpha += step;
   }
-  if (!crossed) return;
+}
 
+template <int G, typename V>
+__global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __restrict__ pose,
+                                                      const double* __restrict__ intr, int w, int h, int Dp,
+                                                      const double2* __restrict__ hits, double* __restrict__ vre,
+                                                      double* __restrict__ nre, double* __restrict__ vim,
+                                                      double* __restrict__ nim) {
+  extern __shared__ double sm[];
+  const int C = 1 + Dp;
+  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
+  int4* cache_mem = reinterpret_cast<int4*>(sm + 16 * C) + 8 * threadIdx.x;
+  __syncthreads();
   const int passes = G == 0 ? 1 : Dp / G;
-  for (int gi = 0; gi < passes; ++gi) {
-    using S = Scal<G>;
-    const int g0 = gi * G;
-    Pose<S> P;
+  const long long item = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (item >= static_cast<long long>(w) * h * passes) return;
+  const int pix = static_cast<int>(item / passes);
+  const int gi = static_cast<int>(item % passes);
+  const double2 hit = hits[pix];
+  if (hit.y < 0.0) return;
+  const double alpha_prev = hit.x, alpha_hit = hit.y;
+  const int x = pix % w, y = pix / w;
+  const double* kk = sm + 12 * C;
+  using S = Scal<G>;
+  const int g0 = gi * G;
+  typename V::Cache cache;
+  if constexpr (V::kHashed) cache.e = cache_mem;
+  (void)cache_mem;
+  cache.reset();
+  Pose<S> P;
 #pragma unroll
-    for (int e = 0; e < 9; ++e) P.R.m[e] = load_ch<S>(sm + e * C, g0, G);
+  for (int e = 0; e < 9; ++e) P.R.m[e] = load_ch<S>(sm + e * C, g0, G);
 #pragma unroll
-    for (int e = 0; e < 3; ++e) P.t.v[e] = load_ch<S>(sm + (9 + e) * C, g0, G);
-    const S fx = load_ch<S>(kk, g0, G), fy = load_ch<S>(kk + C, g0, G);
-    const S cx = load_ch<S>(kk + 2 * C, g0, G), cy = load_ch<S>(kk + 3 * C, g0, G);
-    const S one = lit<S>(1.0);
-    const V3<S> dcs = mk3<S>((static_cast<double>(x) - cx) / fx, (static_cast<double>(y) - cy) / fy, one);
-    const S rns = sqrt_s(dot3(dcs, dcs));
-    const V3<S> dirs = matvec(P.R, mk3<S>(dcs.v[0] / rns, dcs.v[1] / rns, dcs.v[2] / rns));
-    const V3<S>& os = P.t;
-    auto at = [&](double a) {
-      return mk3<S>(os.v[0] + a * dirs.v[0], os.v[1] + a * dirs.v[1], os.v[2] + a * dirs.v[2]);
-    };
-    S fl_prev, fl;
-    sample_tsdf<S>(vol, at(alpha_prev), g0, &fl_prev, cache);
-    sample_tsdf<S>(vol, at(alpha_hit), g0, &fl, cache);
-    const double span = alpha_hit - alpha_prev;
-    const S astar = alpha_prev - (span * fl_prev) / (fl - fl_prev);
-    const V3<S> v = mk3<S>(os.v[0] + astar * dirs.v[0], os.v[1] + astar * dirs.v[1], os.v[2] + astar * dirs.v[2]);
-    V3<S> grad;
-    if (!sample_gradient<S>(vol, v, g0, &grad, cache)) return;
-    const S len2 = dot3(grad, grad);
-    if (!(re(len2) > 0.0)) return;
-    const S ln = sqrt_s(len2);
-    const V3<S> n = mk3<S>(grad.v[0] / ln, grad.v[1] / ln, grad.v[2] / ln);
+  for (int e = 0; e < 3; ++e) P.t.v[e] = load_ch<S>(sm + (9 + e) * C, g0, G);
+  const S fx = load_ch<S>(kk, g0, G), fy = load_ch<S>(kk + C, g0, G);
+  const S cx = load_ch<S>(kk + 2 * C, g0, G), cy = load_ch<S>(kk + 3 * C, g0, G);
+  const S one = lit<S>(1.0);
+  const V3<S> dcs = mk3<S>((static_cast<double>(x) - cx) / fx, (static_cast<double>(y) - cy) / fy, one);
+  const S rns = sqrt_s(dot3(dcs, dcs));
+  const V3<S> dirs = matvec(P.R, mk3<S>(dcs.v[0] / rns, dcs.v[1] / rns, dcs.v[2] / rns));
+  const V3<S>& os = P.t;
+  auto at = [&](double a) {
+    return mk3<S>(os.v[0] + a * dirs.v[0], os.v[1] + a * dirs.v[1], os.v[2] + a * dirs.v[2]);
+  };
+  S fl_prev, fl;
+  sample_tsdf<S>(vol, at(alpha_prev), g0, &fl_prev, cache);
+  sample_tsdf<S>(vol, at(alpha_hit), g0, &fl, cache);
+  const double span = alpha_hit - alpha_prev;
+  const S astar = alpha_prev - (span * fl_prev) / (fl - fl_prev);
+  const V3<S> v = mk3<S>(os.v[0] + astar * dirs.v[0], os.v[1] + astar * dirs.v[1], os.v[2] + astar * dirs.v[2]);
+  V3<S> grad;
+  if (!sample_gradient<S>(vol, v, g0, &grad, cache)) return;
+  const S len2 = dot3(grad, grad);
+  if (!(re(len2) > 0.0)) return;
+  const S ln = sqrt_s(len2);
+  const V3<S> n = mk3<S>(grad.v[0] / ln, grad.v[1] / ln, grad.v[2] / ln);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      if (gi == 0) {
-        vr[c] = re(v.v[c]);
-        nr[c] = re(n.v[c]);
-      }
-      if constexpr (G > 0) {
-        double* vi = vim + (static_cast<long long>(pix) * 3 + c) * Dp + g0;
-        double* ni = nim + (static_cast<long long>(pix) * 3 + c) * Dp + g0;
+  for (int c = 0; c < 3; ++c) {
+    if (gi == 0) {
+      vre[3LL * pix + c] = re(v.v[c]);
+      nre[3LL * pix + c] = re(n.v[c]);
+    }
+    if constexpr (G > 0) {
+      double* vi = vim + (3LL * pix + c) * Dp + g0;
+      double* ni = nim + (3LL * pix + c) * Dp + g0;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          vi[g] = v.v[c].im[g];
-          ni[g] = n.v[c].im[g];
-        }
+      for (int g = 0; g < G; ++g) {
+        vi[g] = v.v[c].im[g];
+        ni[g] = n.v[c].im[g];
       }
     }
   }
@@ -538,8 +632,23 @@ void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, 
   chk("init_volume");
 }
 
+// Channel-group width of the fusion kernels.  Any width dividing Dp
+// addresses the same channel layout; narrower groups trade a recomputed real
+// channel for registers (occupancy).  CSF_INTEGRATE_G overrides (tuning).
+static int integrate_group(int G, int Dp) {
+  if (G == 0) return 0;
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = std::getenv("CSF_INTEGRATE_G");
+    forced = e ? std::atoi(e) : -1;
+  }
+  if (forced > 0 && forced <= 6 && Dp % forced == 0) return forced;
+  return G;
+}
+
 void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* depth, int w, int h,
                             const double* pose, const double* intr) {
+  G = integrate_group(G, Dp);
   const DenseView view = dense_view(v, Dp);
   const size_t smem = sizeof(double) * 19 * (1 + Dp);
   const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
@@ -551,6 +660,7 @@ void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, c
 
 void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, const AllocScratch& a,
                              const double* depth, int w, int h, const double* pose, const double* intr) {
+  G = integrate_group(G, Dp);
   const HashView view = hash_view(v, Dp);
   const size_t smem = sizeof(double) * 19 * (1 + Dp);
   const int grid = sm_count() * 8;
@@ -596,9 +706,30 @@ size_t alloc_scan_bytes(int n) {
   return bytes;
 }
 
+template <typename V>
+static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp, const double* pose,
+                         const double* intr, int w, int h, double near_clip, double far_clip, double step,
+                         double2* hits, double* vre, double* nre, double* vim, double* nim) {
+  const int P = w * h;
+  k_raycast_march<V><<<(P + 127) / 128, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip, step,
+                                                            box, hits, vre, nre);
+  if (Dp > 0 && vim) {
+    cudaMemsetAsync(vim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
+    cudaMemsetAsync(nim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
+  }
+  const int RG = raycast_group(G, Dp);
+  const int passes = RG == 0 ? 1 : Dp / RG;
+  const long long items = static_cast<long long>(P) * passes;
+  const int grid = static_cast<int>((items + 127) / 128);
+  const size_t smem = sizeof(double) * 16 * (1 + Dp) + sizeof(int4) * 8 * 128;
+  CSF_DISPATCH_RG(RG, (k_raycast_lift<kG, V><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre,
+                                                                            nre, vim, nim)));
+  *L.launches += 2;
+}
+
 void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* pose, const double* intr,
-                          int w, int h, double near_clip, double far_clip, double step, double* vre, double* nre,
-                          double* vim, double* nim) {
+                          int w, int h, double near_clip, double far_clip, double step, double2* hits, double* vre,
+                          double* nre, double* vim, double* nim) {
   const DenseView view = dense_view(v, Dp);
   Box box;
   box.use = true;
@@ -606,29 +737,17 @@ void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, con
   box.hi[0] = v.ox + v.vs * (static_cast<double>(v.nx) - 1.0);
   box.hi[1] = v.oy + v.vs * (static_cast<double>(v.ny) - 1.0);
   box.hi[2] = v.oz + v.vs * (static_cast<double>(v.nz) - 1.0);
-  const size_t smem = sizeof(double) * 16 * (1 + Dp);
-  const int grid = (w * h + 127) / 128;
-  const int RG = raycast_group(G, Dp);
-  CSF_DISPATCH_RG(RG, (k_raycast<kG, DenseView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
-                                                                               far_clip, step, box, vre, nre, vim,
-                                                                               nim)));
-  ++*L.launches;
+  raycast_impl(L, view, box, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
   chk("raycast_dense");
 }
 
 void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, const double* pose, const double* intr,
-                           int w, int h, double near_clip, double far_clip, double step, double* vre, double* nre,
-                           double* vim, double* nim) {
+                           int w, int h, double near_clip, double far_clip, double step, double2* hits, double* vre,
+                           double* nre, double* vim, double* nim) {
   const HashView view = hash_view(v, Dp);
   Box box;
   box.use = false;
-  const size_t smem = sizeof(double) * 16 * (1 + Dp) + sizeof(int4) * 8 * 128;
-  const int grid = (w * h + 127) / 128;
-  const int RG = raycast_group(G, Dp);
-  CSF_DISPATCH_RG(RG, (k_raycast<kG, HashView><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, near_clip,
-                                                                              far_clip, step, box, vre, nre, vim,
-                                                                              nim)));
-  ++*L.launches;
+  raycast_impl(L, view, box, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
   chk("raycast_hashed");
 }
 
