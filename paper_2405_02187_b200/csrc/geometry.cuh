@@ -131,22 +131,30 @@ CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out, typename 
   const S fx = gx - static_cast<double>(i0);
   const S fy = gy - static_cast<double>(j0);
   const S fz = gz - static_cast<double>(k0);
+  // all eight corner lookups and loads are issued before any test; the
+  // accumulation keeps the reference's dk, dj, di order (tsdf.hpp:163-176)
+  long long v[8];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    v[c] = vol.voxel(i0 + (c & 1), j0 + ((c >> 1) & 1), k0 + (c >> 2), cache);
+    ok = ok && v[c] >= 0;
+  }
+  if (!ok) return false;
+  double2 rw[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) rw[c] = vol.vox.rw[v[c]];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) ok = ok && rw[c].y > 0.0;
+  if (!ok) return false;
   S accum = lit<S>(0.0);
 #pragma unroll
-  for (int dk = 0; dk < 2; ++dk)
-#pragma unroll
-    for (int dj = 0; dj < 2; ++dj)
-#pragma unroll
-      for (int di = 0; di < 2; ++di) {
-        const long long v = vol.voxel(i0 + di, j0 + dj, k0 + dk, cache);
-        if (v < 0) return false;
-        const double2 rw = vol.vox.rw[v];
-        if (!(rw.y > 0.0)) return false;
-        const S wx = di ? fx : 1.0 - fx;
-        const S wy = dj ? fy : 1.0 - fy;
-        const S wz = dk ? fz : 1.0 - fz;
-        accum = accum + ((wx * wy) * wz) * field_at<S>(vol.vox, v, rw.x, g0);
-      }
+  for (int c = 0; c < 8; ++c) {
+    const S wx = (c & 1) ? fx : 1.0 - fx;
+    const S wy = ((c >> 1) & 1) ? fy : 1.0 - fy;
+    const S wz = (c >> 2) ? fz : 1.0 - fz;
+    accum = accum + ((wx * wy) * wz) * field_at<S>(vol.vox, v[c], rw[c].x, g0);
+  }
   *out = accum;
   return true;
 }
