@@ -853,14 +853,11 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
       const int stride = std::max(1, cfg.icp.level_pixel_stride[li]);
       const int tiles = icp_tiles(wl, hl, stride);
       for (int it = 0; it < cfg.icp.level_iterations[li]; ++it) {
-        {
-          PROF(ctx, kPIcpReduce);
-          launch_icp_reduce(L, p->G, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p,
-                            p->vim.p, p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p);
-        }
-        PROF(ctx, kPIcpSolve);
-        launch_icp_solve(L, p->G, p->Dp, st, p->partials.p, p->counts.p, tiles, p->pose.p, level,
-                         cfg.icp.step_tolerance);
+        PROF(ctx, kPIcpReduce);
+        launch_icp_reduce(L, p->G, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p,
+                          p->vim.p, p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p, level,
+                          cfg.icp.step_tolerance);
+        (void)tiles;
       }
     }
     rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p);
@@ -984,8 +981,7 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
     tiles_last = icp_tiles(wl, hl, stride);
     for (int it = 0; it < cfg.level_iterations[li]; ++it) {
       launch_icp_reduce(L, 0, 0, st.p, pyr[level], wl, hl, stride, intr.p + 4 * level, pose.p, vre.p, nre.p, nullptr,
-                        nullptr, cfg.d_max, cos_max, partials.p, counts.p);
-      launch_icp_solve(L, 0, 0, st.p, partials.p, counts.p, tiles_last, pose.p, level, cfg.step_tolerance);
+                        nullptr, cfg.d_max, cos_max, partials.p, counts.p, level, cfg.step_tolerance);
     }
   }
   TrackState hs;

@@ -97,10 +97,12 @@ void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, 
 // ---- icp.cu
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp);
 int icp_tiles(int w, int h, int stride);
-void launch_icp_reduce(const Launch& L, int G, int Dp, const TrackState* st, const double* depth, int w, int h,
-                       int stride, const double* intr, const double* pose, const double* vre, const double* nre,
+// One ICP iteration: association + lifted normal equations per tile, and the
+// last CTA solves and updates the pose (TrackState::pad[0] is its counter).
+void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const double* depth, int w, int h,
+                       int stride, const double* intr, double* pose, const double* vre, const double* nre,
                        const double* vim, const double* nim, double d_max, double cos_max, double* partials,
-                       int* counts);
+                       int* counts, int level, double tol);
 void launch_icp_solve(const Launch& L, int G, int Dp, TrackState* st, const double* partials, const int* counts,
                       int n_tiles, double* pose, int level, double tol);
 void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,

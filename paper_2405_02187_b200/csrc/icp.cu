@@ -16,6 +16,7 @@
 //     thread per channel group runs the 6x6 LDLT, the exp map and the pose
 //     update in L<G> arithmetic.  Break decisions are written to TrackState so
 //     the whole level stays on the device (no host round trip).
+#include <algorithm>
 #include <cstdio>
 
 #include "csf_internal.h"
@@ -44,14 +45,106 @@ CSF_DEV bool vertex_at(const double* depth, int w, int x, int y, double fx, doub
   return true;
 }
 
+// The solve of one ICP iteration, run by one CTA of >= 64 threads: sum the
+// tile partials in tile order, then one thread per channel group factors the
+// lifted 6x6 system, applies exp(delta) * T and writes the break decisions.
+// `sm` holds >= 27*(1+Dp) + 48*(1+G)*ngroups doubles.
 template <int G>
-__global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* __restrict__ st, const double* __restrict__ depth,
+__device__ void icp_solve_block(TrackState* st, const double* partials, const int* counts, int n_tiles,
+                                double* pose, int Dp, int level, double tol, double* sm) {
+  using S = Scal<G>;
+  __shared__ int s_n, s_finite;
+  const int C = 1 + Dp;
+  const int n_acc = 27 * C;
+  S* ws = reinterpret_cast<S*>(sm + n_acc) + 48 * threadIdx.x;
+  for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
+    double total = 0.0;
+    for (int t = 0; t < n_tiles; ++t) total = total + __ldcg(partials + static_cast<long long>(t) * n_acc + a);
+    sm[a] = total;
+  }
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int t = 0; t < n_tiles; ++t) n += __ldcg(counts + t);
+    s_n = n;
+    s_finite = 1;
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (n < 12) {
+    if (threadIdx.x == 0) {
+      st->n_corr = n;
+      st->level_done = 1;
+    }
+    return;
+  }
+  const int ngroups = G == 0 ? 1 : Dp / G;
+  const bool mine = static_cast<int>(threadIdx.x) < ngroups;
+  const int g0 = threadIdx.x * G;
+  S d[6];
+  if (mine) {
+    S a[21], nb[6];
+#pragma unroll
+    for (int q = 0; q < 21; ++q) a[q] = load_ch<S>(sm + q * C, g0, G);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) nb[i] = -load_ch<S>(sm + (21 + i) * C, g0, G);
+    ldlt6_solve<S>(a, nb, d, ws);
+    bool fin = true;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) fin = fin && finite_s(d[i]);
+    if (!fin) atomicAnd(&s_finite, 0);
+  }
+  __syncthreads();
+  Pose<S> np;
+  if (mine) {
+    if (!s_finite)
+#pragma unroll
+      for (int i = 0; i < 6; ++i) d[i] = lit<S>(0.0);
+    Pose<S> cur;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
+    np = compose(exp_map<S>(d), cur);
+  }
+  __syncthreads();
+  if (mine) {
+#pragma unroll
+    for (int e = 0; e < 9; ++e) store_ch<S>(pose + e * C, np.R.m[e], g0, G, threadIdx.x == 0);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) store_ch<S>(pose + (9 + e) * C, np.t.v[e], g0, G, threadIdx.x == 0);
+  }
+  if (threadIdx.x == 0) {
+    double sq[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) sq[i] = re(d[i]) * re(d[i]);
+    const double nrm = sqrt((sq[0] + (sq[1] + sq[2])) + (sq[3] + (sq[4] + sq[5])));
+    st->iterations += 1;
+    st->n_corr = n;
+    if (nrm < tol) {
+      st->level_done = 1;
+      if (level == 0) st->converged = 1;
+    }
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_icp_solve(TrackState* st, const double* __restrict__ partials,
+                                                   const int* __restrict__ counts, int n_tiles, double* pose, int Dp,
+                                                   int level, double tol) {
+  if (st->level_done) return;
+  extern __shared__ double sm[];
+  icp_solve_block<G>(st, partials, counts, n_tiles, pose, Dp, level, tol, sm);
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
                                                     int w, int h, int stride, const double* __restrict__ intr,
-                                                    const double* __restrict__ pose, const double* __restrict__ vre,
+                                                    const double* pose, const double* __restrict__ vre,
                                                     const double* __restrict__ nre, const double* __restrict__ vim,
                                                     const double* __restrict__ nim, double d_max, double cos_max,
                                                     int Dp, int chunk, double* __restrict__ partials,
-                                                    int* __restrict__ counts) {
+                                                    int* __restrict__ counts, TrackState* st_rw, double* pose_rw,
+                                                    int level, double tol) {
   if (st->level_done) return;
   using S = Scal<G>;
   extern __shared__ double sm[];
@@ -203,88 +296,22 @@ __global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* __restrict
     if (a < n_acc) partials[static_cast<long long>(blockIdx.x) * n_acc + a] = acc[j];
   }
   if (threadIdx.x == 0) counts[blockIdx.x] = tile_count;
-}
-
-template <int G>
-__global__ void __launch_bounds__(256) k_icp_solve(TrackState* st, const double* __restrict__ partials,
-                                                   const int* __restrict__ counts, int n_tiles, double* pose, int Dp,
-                                                   int level, double tol) {
-  if (st->level_done) return;
-  using S = Scal<G>;
-  extern __shared__ double sm[];
-  __shared__ int s_n, s_finite;
-  const int C = 1 + Dp;
-  const int n_acc = 27 * C;
-  // per-group LDLT workspace after the accumulators (48 scalars each)
-  S* ws = reinterpret_cast<S*>(sm + n_acc) + 48 * threadIdx.x;
-  for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
-    double total = 0.0;
-    for (int t = 0; t < n_tiles; ++t) total = total + partials[static_cast<long long>(t) * n_acc + a];
-    sm[a] = total;
-  }
+  // The last CTA to finish runs the solve (no second launch per iteration).
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
   if (threadIdx.x == 0) {
-    int n = 0;
-    for (int t = 0; t < n_tiles; ++t) n += counts[t];
-    s_n = n;
-    s_finite = 1;
+    const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(&st_rw->pad[0]), 1u);
+    s_last = prev == gridDim.x - 1;
   }
   __syncthreads();
-  const int n = s_n;
-  if (n < 12) {
-    if (threadIdx.x == 0) {
-      st->n_corr = n;
-      st->level_done = 1;
-    }
-    return;
-  }
-  const int ngroups = G == 0 ? 1 : Dp / G;
-  const bool mine = static_cast<int>(threadIdx.x) < ngroups;
-  const int g0 = threadIdx.x * G;
-  S d[6];
-  if (mine) {
-    S a[21], nb[6];
-#pragma unroll
-    for (int q = 0; q < 21; ++q) a[q] = load_ch<S>(sm + q * C, g0, G);
-#pragma unroll
-    for (int i = 0; i < 6; ++i) nb[i] = -load_ch<S>(sm + (21 + i) * C, g0, G);
-    ldlt6_solve<S>(a, nb, d, ws);
-    bool fin = true;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) fin = fin && finite_s(d[i]);
-    if (!fin) atomicAnd(&s_finite, 0);
-  }
-  __syncthreads();
-  Pose<S> np;
-  if (mine) {
-    if (!s_finite)
-#pragma unroll
-      for (int i = 0; i < 6; ++i) d[i] = lit<S>(0.0);
-    Pose<S> cur;
-#pragma unroll
-    for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<S>(pose + e * C, g0, G);
-#pragma unroll
-    for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
-    np = compose(exp_map<S>(d), cur);
-  }
-  __syncthreads();
-  if (mine) {
-#pragma unroll
-    for (int e = 0; e < 9; ++e) store_ch<S>(pose + e * C, np.R.m[e], g0, G, threadIdx.x == 0);
-#pragma unroll
-    for (int e = 0; e < 3; ++e) store_ch<S>(pose + (9 + e) * C, np.t.v[e], g0, G, threadIdx.x == 0);
-  }
-  if (threadIdx.x == 0) {
-    double sq[6];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) sq[i] = re(d[i]) * re(d[i]);
-    const double nrm = sqrt((sq[0] + (sq[1] + sq[2])) + (sq[3] + (sq[4] + sq[5])));
-    st->iterations += 1;
-    st->n_corr = n;
-    if (nrm < tol) {
-      st->level_done = 1;
-      if (level == 0) st->converged = 1;
-    }
-  }
+  if (!s_last) return;
+  if (threadIdx.x == 0) st_rw->pad[0] = 0;
+  __threadfence();
+  if (Dp == 0)
+    icp_solve_block<0>(st_rw, partials, counts, gridDim.x, pose_rw, Dp, level, tol, sm);
+  else
+    icp_solve_block<1>(st_rw, partials, counts, gridDim.x, pose_rw, Dp, level, tol, sm);
 }
 
 // Level entry: the prediction pose is the current estimate (icp.cpp:191).
@@ -433,13 +460,14 @@ void launch_level_begin(const Launch& L, TrackState* st, const double* pose, dou
   chk("level_begin");
 }
 
-void launch_icp_reduce(const Launch& L, int G, int Dp, const TrackState* st, const double* depth, int w, int h,
-                       int stride, const double* intr, const double* pose, const double* vre, const double* nre,
+void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const double* depth, int w, int h,
+                       int stride, const double* intr, double* pose, const double* vre, const double* nre,
                        const double* vim, const double* nim, double d_max, double cos_max, double* partials,
-                       int* counts) {
+                       int* counts, int level, double tol) {
   const int C = 1 + Dp;
   const int chunk = reduce_chunk(C);
-  const size_t smem = sizeof(double) * (16 * C + static_cast<size_t>(chunk) * 7 * C);
+  const size_t solve_smem = 27 * C + 48 * 2 * static_cast<size_t>(Dp > 0 ? Dp : 1);
+  const size_t smem = sizeof(double) * std::max<size_t>(16 * C + static_cast<size_t>(chunk) * 7 * C, solve_smem);
   const int tiles = icp_tiles(w, h, stride);
   // J/r rows are evaluated in channel groups of 2 (or 1): register-light,
   // any width that divides Dp addresses the same channel layout.
@@ -449,19 +477,19 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, const TrackState* st, con
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       k_icp_reduce<0><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
-                                                      cos_max, Dp, chunk, partials, counts);
+                                                      cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
       break;
     case 1:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       k_icp_reduce<1><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
-                                                      cos_max, Dp, chunk, partials, counts);
+                                                      cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
       break;
     default:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       k_icp_reduce<2><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
-                                                      cos_max, Dp, chunk, partials, counts);
+                                                      cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
   }
   ++*L.launches;
   chk("icp_reduce");

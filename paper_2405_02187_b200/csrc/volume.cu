@@ -74,32 +74,30 @@ template <int G>
 __device__ void fuse_voxel(const VoxelStore& vox, long long v, double px, double py, double pz,
                            const double* __restrict__ depth, int w, int h, double mu, double cap, int Dp,
                            const double* sm) {
-  Pose<double> w2c_re;
-  V3<double> c_re;
-  Intr<double> k_re;
-  load_pose_intr<double>(sm, Dp, 0, &w2c_re, &c_re, &k_re);
-  double psi_re;
-  if (!measured_tsdf<double>(depth, w, h, w2c_re, k_re, mu, px, py, pz, c_re, &psi_re)) return;
-  const double2 rw = vox.rw[v];
-  const double wt = rw.y;
-  const double fre = (wt * rw.x + psi_re) / (wt + 1.0);
-  if constexpr (G > 0) {
-    using S = L<G>;
-    for (int g0 = 0; g0 < Dp; g0 += G) {
-      Pose<S> w2c;
-      V3<S> c;
-      Intr<S> k;
-      load_pose_intr<S>(sm, Dp, g0, &w2c, &c, &k);
-      S psi;
-      measured_tsdf<S>(depth, w, h, w2c, k, mu, px, py, pz, c, &psi);
-      const S f = field_at<S>(vox, v, rw.x, g0);
-      const S fn = (wt * f + psi) / (wt + 1.0);
+  using S = Scal<G>;
+  const int passes = G == 0 ? 1 : Dp / G;
+  double2 rw = make_double2(0.0, 0.0);
+  double fre = 0.0;
+  for (int gi = 0; gi < passes; ++gi) {
+    const int g0 = gi * G;
+    Pose<S> w2c;
+    V3<S> c;
+    Intr<S> k;
+    load_pose_intr<S>(sm, Dp, g0, &w2c, &c, &k);
+    S psi;
+    // validity depends on real parts only: the first pass decides for all
+    if (!measured_tsdf<S>(depth, w, h, w2c, k, mu, px, py, pz, c, &psi)) return;
+    if (gi == 0) rw = vox.rw[v];
+    const S f = field_at<S>(vox, v, rw.x, g0);
+    const S fn = (rw.y * f + psi) / (rw.y + 1.0);
+    fre = re(fn);
+    if constexpr (G > 0) {
       double* dst = vox.fim + v * vox.Dp + g0;
 #pragma unroll
       for (int g = 0; g < G; ++g) dst[g] = fn.im[g];
     }
   }
-  const double wn = wt + 1.0;
+  const double wn = rw.y + 1.0;
   vox.rw[v] = make_double2(fre, cap < wn ? cap : wn);
 }
 

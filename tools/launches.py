@@ -1,0 +1,26 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum launch list (CSV)."""
+import collections
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+h = rows[hi]
+ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+gi = h.index("Grid Size") if "Grid Size" in h else None
+agg = collections.defaultdict(lambda: [0, 0.0])
+for r in rows[hi + 1:]:
+    if len(r) <= vi:
+        continue
+    name = r[ki].split("(")[0]
+    name = name.replace("void ", "")
+    v = float(r[vi].replace(",", ""))
+    u = r[ui]
+    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u, 1.0)
+    agg[name][0] += 1
+    agg[name][1] += v
+tot = sum(v[1] for v in agg.values())
+print(f"{'kernel':50s} {'launches':>8s} {'total ms':>10s} {'share':>6s} {'avg us':>9s}")
+for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"{k[:50]:50s} {n:8d} {t / 1e3:10.3f} {100 * t / tot:5.1f}% {t / n:9.1f}")
+print(f"total {tot / 1e3:.3f} ms")
