@@ -142,7 +142,7 @@ struct csf_volume_s {
   long long n_vox = 0;  // dense voxel count / pool voxel capacity
   DevBuf<double2> rw;
   DevBuf<double> fim;
-  DevBuf<int> heads, next, coords, nblocks;
+  DevBuf<int> heads, next, coords, nblocks, grid;
   DevBuf<unsigned long long> keys;
   // allocation scratch (hashed)
   AllocScratch alloc{};
@@ -156,6 +156,7 @@ struct csf_volume_s {
 
   ~csf_volume_s() {
     rw.release(); fim.release(); heads.release(); next.release(); coords.release(); nblocks.release(); keys.release();
+    grid.release();
     a_cand.release(); a_set_keys.release(); a_cand_block.release(); a_first_flag.release(); a_new_flag.release();
     a_first_rank.release(); a_new_rank.release(); a_set_first.release(); a_set_slot.release(); a_visible.release();
     a_counters.release(); a_cub.release();
@@ -482,6 +483,12 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   }
   v->n_vox = static_cast<long long>(p->max_blocks) * 512;
   const size_t nb = size_t(1) << p->bucket_bits;
+  const int gbits = 9;  // 512^3 block-id window (512 MiB of int32)
+  const size_t ng = size_t(1) << (3 * gbits);
+  if (v->grid.alloc(ng) != cudaSuccess) {
+    delete v;
+    return fail(ctx, CSF_ENOMEM, "csf_volume_create_hashed: out of device memory (block grid)");
+  }
   if (v->rw.alloc(v->n_vox) != cudaSuccess ||
       v->fim.alloc(static_cast<size_t>(v->n_vox) * std::max(v->Dp, 1)) != cudaSuccess ||
       v->heads.alloc(nb) != cudaSuccess || v->next.alloc(p->max_blocks) != cudaSuccess ||
@@ -498,6 +505,8 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   d.next = v->next.p;
   d.coords = v->coords.p;
   d.n_blocks = v->nblocks.p;
+  d.grid = v->grid.p;
+  d.gbits = gbits;
   d.bits = p->bucket_bits;
   d.max_blocks = p->max_blocks;
   d.vs = p->voxel_size;
@@ -507,6 +516,7 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   cudaMemsetAsync(d.heads, 0xFF, sizeof(int) * nb, ctx->stream);
   cudaMemsetAsync(d.next, 0xFF, sizeof(int) * p->max_blocks, ctx->stream);
   cudaMemsetAsync(d.n_blocks, 0, sizeof(int), ctx->stream);
+  cudaMemsetAsync(d.grid, 0xFF, sizeof(int) * ng, ctx->stream);
   launch_init_volume(launch_of(ctx), d.rw, d.fim, v->n_vox, v->Dp);
   rc = sync_check(ctx, "csf_volume_create_hashed");
   if (rc) {
@@ -800,6 +810,7 @@ static int pipeline_reset_volume(csf_pipeline p) {
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.heads, 0xFF, sizeof(int) << v->hash.bits, ctx->stream));
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.next, 0xFF, sizeof(int) * v->hash.max_blocks, ctx->stream));
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.n_blocks, 0, sizeof(int), ctx->stream));
+      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.grid, 0xFF, sizeof(int) << (3 * v->hash.gbits), ctx->stream));
       launch_init_volume(L, v->hash.rw, v->hash.fim, static_cast<long long>(nb) * 512, v->Dp);
     }
   } else {

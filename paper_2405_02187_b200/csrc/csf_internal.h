@@ -29,7 +29,8 @@ struct HashDev {
   int* next;                    // [max_blocks]
   int* coords;                  // [max_blocks][3]
   int* n_blocks;                // device counter
-  int bits, max_blocks;
+  int* grid;                    // [2^(3*gbits)] dense block-id window (derived index)
+  int bits, max_blocks, gbits;
   double vs, ox, oy, oz, mu, cap;
 };
 

@@ -31,20 +31,10 @@ struct VoxelStore {
   int Dp;
 };
 
-// Per-thread lookup cache.  Dense volumes need none; hashed volumes keep the
-// last block id per (bx, by, bz) parity class, which holds a whole 2x2x2
-// block neighbourhood — every corner of a trilinear cell — without conflicts.
+// Lookup-cache hook of the sampling functions (no state is needed: hashed
+// volumes resolve in-window blocks through a dense block-id grid).
 struct NoCache {
   CSF_DEV void reset() {}
-};
-// The 8 entries live in shared memory (a per-thread slice supplied by the
-// kernel): data-dependent indexing stays out of local memory.
-struct BlockCache {
-  int4* e;  // (bx, by, bz, id) per parity class
-  CSF_DEV void reset() {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) e[i].x = 0x7fffffff;
-  }
 };
 
 // Dense lattice (tsdf.hpp:38-78): index (k*ny + j)*nx + i.
@@ -66,13 +56,20 @@ struct DenseView {
 
 // Hashed 8^3 blocks: chained buckets, chains sorted by key (builder-defined;
 // oracle/orc_tsdf.hpp HashedVolumeT).
+// Hashed 8^3 blocks: chained buckets, chains sorted by key (builder-defined;
+// oracle/orc_tsdf.hpp HashedVolumeT).  The hash table is the canonical
+// structure; `grid` is a derived dense block-id index over a window of
+// 2^gbits blocks per axis (centred on block 0) so in-window lookups are one
+// load instead of a chain walk.  Blocks outside the window use the chains.
 struct HashView {
-  using Cache = BlockCache;
+  using Cache = NoCache;
   VoxelStore vox;
   const int* heads;
   const unsigned long long* keys;
   const int* next;
+  const int* grid;
   unsigned mask;
+  int gbits;
   double vs, ox, oy, oz, mu, cap;
   static constexpr bool kHashed = true;
   CSF_DEV bool cell_in_grid(int, int, int) const { return true; }
@@ -87,25 +84,21 @@ struct HashView {
     }
     return -1;
   }
+  CSF_DEV int block(int bx, int by, int bz) const {
+    const int half = 1 << (gbits - 1);
+    const unsigned ux = static_cast<unsigned>(bx + half), uy = static_cast<unsigned>(by + half),
+                   uz = static_cast<unsigned>(bz + half);
+    const unsigned side = 1u << gbits;
+    if (ux < side && uy < side && uz < side)
+      return __ldg(grid + ((static_cast<size_t>(uz) << gbits | uy) << gbits | ux));
+    return find(bx, by, bz);
+  }
   CSF_DEV long long voxel(int i, int j, int k) const {
-    const int b = find(i >> 3, j >> 3, k >> 3);
+    const int b = block(i >> 3, j >> 3, k >> 3);
     if (b < 0) return -1;
     return static_cast<long long>(b) * kBlockVoxels + (((k & 7) * 8 + (j & 7)) * 8 + (i & 7));
   }
-  CSF_DEV long long voxel(int i, int j, int k, BlockCache& c) const {
-    const int bx = i >> 3, by = j >> 3, bz = k >> 3;
-    const int s = (bx & 1) | ((by & 1) << 1) | ((bz & 1) << 2);
-    int b;
-    const int4 ce = c.e[s];
-    if (ce.x == bx && ce.y == by && ce.z == bz) {
-      b = ce.w;
-    } else {
-      b = find(bx, by, bz);
-      c.e[s] = make_int4(bx, by, bz, b);
-    }
-    if (b < 0) return -1;
-    return static_cast<long long>(b) * kBlockVoxels + (((k & 7) * 8 + (j & 7)) * 8 + (i & 7));
-  }
+  CSF_DEV long long voxel(int i, int j, int k, NoCache&) const { return voxel(i, j, k); }
 };
 
 // Stored field value of voxel v as S (channel group g0).
@@ -158,8 +151,8 @@ CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out, typename 
   *out = accum;
   return true;
 }
-template <typename S>
-CSF_DEV bool sample_tsdf(const DenseView& vol, const V3<S>& p, int g0, S* out) {
+template <typename S, typename V>
+CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out) {
   NoCache c;
   return sample_tsdf<S>(vol, p, g0, out, c);
 }

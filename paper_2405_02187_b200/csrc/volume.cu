@@ -287,6 +287,12 @@ __global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int
     coords[3 * id + 2] = bz;
     __threadfence();
     chain_insert(heads, keys, next, block_hash(bx, by, bz, vol.mask), id, key);
+    const int half = 1 << (vol.gbits - 1);
+    const unsigned ux = static_cast<unsigned>(bx + half), uy = static_cast<unsigned>(by + half),
+                   uz = static_cast<unsigned>(bz + half);
+    const unsigned side = 1u << vol.gbits;
+    if (ux < side && uy < side && uz < side)
+      const_cast<int*>(vol.grid)[(static_cast<size_t>(uz) << vol.gbits | uy) << vol.gbits | ux] = id;
   }
   visible[first_rank[s]] = id;
 }
@@ -385,7 +391,6 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
                                                        double2* __restrict__ hits, double* __restrict__ vre,
                                                        double* __restrict__ nre) {
   __shared__ double s_pose[16];
-  __shared__ int4 s_cache[V::kHashed ? 8 * 128 : 1];
   const int C = 1 + Dp;
   if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
   else if (threadIdx.x < 16) s_pose[threadIdx.x] = intr[(threadIdx.x - 12) * C];
@@ -432,7 +437,6 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
   if (t0 >= t1) return;
 
   typename V::Cache cache;
-  if constexpr (V::kHashed) cache.e = s_cache + 8 * threadIdx.x;
   cache.reset();
   bool have_prev = false;
   double alpha_prev = 0.0, f_prev = 0.0;
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
       // unallocated base block: every sample until the block exit is invalid
       const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
                 k0 = ifloor((pz - vol.oz) / vol.vs);
-      if (vol.voxel(i0, j0, k0, cache) < 0) {
+      if (vol.block(i0 >> 3, j0 >> 3, k0 >> 3) < 0) {
         have_prev = false;
         const double lim = block_exit(vol, i0 >> 3, j0 >> 3, k0 >> 3, o, dir) - 1e-6;
         alpha += step;
@@ -478,7 +482,6 @@ __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __res
   const int C = 1 + Dp;
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
   for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
-  int4* cache_mem = reinterpret_cast<int4*>(sm + 16 * C) + 8 * threadIdx.x;
   __syncthreads();
   const int passes = G == 0 ? 1 : Dp / G;
   const long long item = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -493,8 +496,6 @@ __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __res
   using S = Scal<G>;
   const int g0 = gi * G;
   typename V::Cache cache;
-  if constexpr (V::kHashed) cache.e = cache_mem;
-  (void)cache_mem;
   cache.reset();
   Pose<S> P;
 #pragma unroll
@@ -608,6 +609,8 @@ static HashView hash_view(const HashDev& v, int Dp) {
   HashView d;
   d.vox = {v.rw, v.fim, Dp};
   d.heads = v.heads; d.keys = v.keys; d.next = v.next;
+  d.grid = v.grid;
+  d.gbits = v.gbits;
   d.mask = (1u << v.bits) - 1u;
   d.vs = v.vs; d.ox = v.ox; d.oy = v.oy; d.oz = v.oz; d.mu = v.mu; d.cap = v.cap;
   return d;
@@ -719,7 +722,7 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
   const int passes = RG == 0 ? 1 : Dp / RG;
   const long long items = static_cast<long long>(P) * passes;
   const int grid = static_cast<int>((items + 127) / 128);
-  const size_t smem = sizeof(double) * 16 * (1 + Dp) + sizeof(int4) * 8 * 128;
+  const size_t smem = sizeof(double) * 16 * (1 + Dp);
   CSF_DISPATCH_RG(RG, (k_raycast_lift<kG, V><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre,
                                                                             nre, vim, nim)));
   *L.launches += 2;
