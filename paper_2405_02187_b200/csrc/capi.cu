@@ -43,8 +43,10 @@ struct Profiler {
   }
 };
 
-enum ProfCat { kPBilateral = 0, kPDownsample, kPRaycast, kPIcpReduce, kPIcpSolve, kPAlloc, kPIntegrate, kPMisc, kPN };
-static const char* kProfNames[kPN] = {"bilateral", "downsample", "raycast", "icp_reduce", "icp_solve",
+enum ProfCat {
+  kPBilateral = 0, kPDownsample, kPRaycast, kPRaycastLift, kPIcpReduce, kPIcpSolve, kPAlloc, kPIntegrate, kPMisc, kPN
+};
+static const char* kProfNames[kPN] = {"bilateral", "downsample", "raycast", "raycast_lift", "icp", "icp_solve",
                                       "allocate", "integrate", "misc"};
 
 struct csf_ctx_s {
@@ -238,16 +240,19 @@ int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double*
 
 void raycast_dev(csf_volume v, const double* d_pose, const double* d_intr, int w, int h, const csf_raycast_cfg& rc,
                  double2* hits, double* vre, double* nre, double* vim, double* nim) {
-  const Launch L = launch_of(v->ctx);
+  Launch L = launch_of(v->ctx);
   const double mu = v->hashed ? v->hash.mu : v->dense.mu;
   const double step = rc.step_fraction * mu;
-  PROF(v->ctx, kPRaycast);
-  if (v->hashed)
-    launch_raycast_hashed(L, v->hash, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, hits, vre,
-                          nre, vim, nim);
-  else
-    launch_raycast_dense(L, v->dense, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, hits, vre,
-                         nre, vim, nim);
+  for (int phase = 1; phase <= 2; ++phase) {
+    PROF(v->ctx, phase == 1 ? kPRaycast : kPRaycastLift);
+    L.phase = phase;
+    if (v->hashed)
+      launch_raycast_hashed(L, v->hash, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, hits, vre,
+                            nre, vim, nim);
+    else
+      launch_raycast_dense(L, v->dense, v->G, v->Dp, d_pose, d_intr, w, h, rc.near_clip, rc.far_clip, step, hits,
+                           vre, nre, vim, nim);
+  }
 }
 
 // Host lifted array [n][1+D] -> padded [n][1+Dp]

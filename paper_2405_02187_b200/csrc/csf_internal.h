@@ -70,6 +70,7 @@ struct Launch {
   cudaStream_t stream;
   int* err;                // device error flag
   unsigned long long* launches;  // host counter of kernels launched
+  int phase = 0;           // multi-kernel stages: 0 = all, 1/2 = first/second half only
 };
 
 // ---- frames.cu

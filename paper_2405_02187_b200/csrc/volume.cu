@@ -712,12 +712,16 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
                          const double* intr, int w, int h, double near_clip, double far_clip, double step,
                          double2* hits, double* vre, double* nre, double* vim, double* nim) {
   const int P = w * h;
-  k_raycast_march<V><<<(P + 127) / 128, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip, step,
-                                                            box, hits, vre, nre);
-  if (Dp > 0 && vim) {
-    cudaMemsetAsync(vim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
-    cudaMemsetAsync(nim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
+  if (L.phase != 2) {
+    k_raycast_march<V><<<(P + 127) / 128, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip, step,
+                                                              box, hits, vre, nre);
+    if (Dp > 0 && vim) {
+      cudaMemsetAsync(vim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
+      cudaMemsetAsync(nim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
+    }
+    *L.launches += 1;
   }
+  if (L.phase == 1) return;
   const int RG = raycast_group(G, Dp);
   const int passes = RG == 0 ? 1 : Dp / RG;
   const long long items = static_cast<long long>(P) * passes;
@@ -725,7 +729,7 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
   const size_t smem = sizeof(double) * 16 * (1 + Dp);
   CSF_DISPATCH_RG(RG, (k_raycast_lift<kG, V><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre,
                                                                             nre, vim, nim)));
-  *L.launches += 2;
+  *L.launches += 1;
 }
 
 void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* pose, const double* intr,
