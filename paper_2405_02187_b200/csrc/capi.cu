@@ -145,6 +145,7 @@ struct csf_volume_s {
   DevBuf<double2> rw;
   DevBuf<double> fim;
   DevBuf<int> heads, next, coords, nblocks, grid;
+  DevBuf<unsigned> occ;
   DevBuf<unsigned long long> keys;
   // allocation scratch (hashed)
   AllocScratch alloc{};
@@ -159,6 +160,7 @@ struct csf_volume_s {
   ~csf_volume_s() {
     rw.release(); fim.release(); heads.release(); next.release(); coords.release(); nblocks.release(); keys.release();
     grid.release();
+    occ.release();
     a_cand.release(); a_set_keys.release(); a_cand_block.release(); a_first_flag.release(); a_new_flag.release();
     a_first_rank.release(); a_new_rank.release(); a_set_first.release(); a_set_slot.release(); a_visible.release();
     a_counters.release(); a_cub.release();
@@ -490,7 +492,8 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   const size_t nb = size_t(1) << p->bucket_bits;
   const int gbits = 9;  // 512^3 block-id window (512 MiB of int32)
   const size_t ng = size_t(1) << (3 * gbits);
-  if (v->grid.alloc(ng) != cudaSuccess) {
+  const size_t nocc = (size_t(1) << (3 * (gbits - 3))) / 32;
+  if (v->grid.alloc(ng) != cudaSuccess || v->occ.alloc(nocc) != cudaSuccess) {
     delete v;
     return fail(ctx, CSF_ENOMEM, "csf_volume_create_hashed: out of device memory (block grid)");
   }
@@ -511,6 +514,7 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   d.coords = v->coords.p;
   d.n_blocks = v->nblocks.p;
   d.grid = v->grid.p;
+  d.occ = v->occ.p;
   d.gbits = gbits;
   d.bits = p->bucket_bits;
   d.max_blocks = p->max_blocks;
@@ -522,6 +526,7 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   cudaMemsetAsync(d.next, 0xFF, sizeof(int) * p->max_blocks, ctx->stream);
   cudaMemsetAsync(d.n_blocks, 0, sizeof(int), ctx->stream);
   cudaMemsetAsync(d.grid, 0xFF, sizeof(int) * ng, ctx->stream);
+  cudaMemsetAsync(d.occ, 0, sizeof(unsigned) * nocc, ctx->stream);
   launch_init_volume(launch_of(ctx), d.rw, d.fim, v->n_vox, v->Dp);
   rc = sync_check(ctx, "csf_volume_create_hashed");
   if (rc) {
@@ -816,6 +821,8 @@ static int pipeline_reset_volume(csf_pipeline p) {
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.next, 0xFF, sizeof(int) * v->hash.max_blocks, ctx->stream));
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.n_blocks, 0, sizeof(int), ctx->stream));
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.grid, 0xFF, sizeof(int) << (3 * v->hash.gbits), ctx->stream));
+      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.occ, 0, sizeof(unsigned) * ((size_t(1) << (3 * (v->hash.gbits - 3))) / 32),
+                                    ctx->stream));
       launch_init_volume(L, v->hash.rw, v->hash.fim, static_cast<long long>(nb) * 512, v->Dp);
     }
   } else {

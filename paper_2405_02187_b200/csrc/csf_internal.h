@@ -30,6 +30,7 @@ struct HashDev {
   int* coords;                  // [max_blocks][3]
   int* n_blocks;                // device counter
   int* grid;                    // [2^(3*gbits)] dense block-id window (derived index)
+  unsigned* occ;                // [2^(3*(gbits-3))/32] super-block occupancy bits
   int bits, max_blocks, gbits;
   double vs, ox, oy, oz, mu, cap;
 };

@@ -68,6 +68,7 @@ struct HashView {
   const unsigned long long* keys;
   const int* next;
   const int* grid;
+  const unsigned* occ;  // one bit per 8^3-block super-block of the window
   unsigned mask;
   int gbits;
   double vs, ox, oy, oz, mu, cap;
@@ -92,6 +93,18 @@ struct HashView {
     if (ux < side && uy < side && uz < side)
       return __ldg(grid + ((static_cast<size_t>(uz) << gbits | uy) << gbits | ux));
     return find(bx, by, bz);
+  }
+  // -1: super-block outside the window (unknown), 0: no allocated block in
+  // it, 1: at least one.
+  CSF_DEV int super_occupied(int bx, int by, int bz) const {
+    const int half = 1 << (gbits - 1);
+    const unsigned ux = static_cast<unsigned>(bx + half), uy = static_cast<unsigned>(by + half),
+                   uz = static_cast<unsigned>(bz + half);
+    const unsigned side = 1u << gbits;
+    if (!(ux < side && uy < side && uz < side)) return -1;
+    const int sb = gbits - 3;
+    const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
+    return (__ldg(occ + (bit >> 5)) >> (bit & 31)) & 1u;
   }
   CSF_DEV long long voxel(int i, int j, int k) const {
     const int b = block(i >> 3, j >> 3, k >> 3);

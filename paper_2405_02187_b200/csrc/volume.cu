@@ -291,8 +291,12 @@ __global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int
     const unsigned ux = static_cast<unsigned>(bx + half), uy = static_cast<unsigned>(by + half),
                    uz = static_cast<unsigned>(bz + half);
     const unsigned side = 1u << vol.gbits;
-    if (ux < side && uy < side && uz < side)
+    if (ux < side && uy < side && uz < side) {
       const_cast<int*>(vol.grid)[(static_cast<size_t>(uz) << vol.gbits | uy) << vol.gbits | ux] = id;
+      const int sb = vol.gbits - 3;
+      const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
+      atomicOr(const_cast<unsigned*>(vol.occ) + (bit >> 5), 1u << (bit & 31));
+    }
   }
   visible[first_rank[s]] = id;
 }
@@ -365,21 +369,20 @@ CSF_DEV bool sample_real(const V& vol, double px, double py, double pz, typename
   return true;
 }
 
-// Analytic exit distance of the ray from block (bx, by, bz).
-CSF_DEV double block_exit(const HashView& vol, int bx, int by, int bz, const V3<double>& o, const V3<double>& dir) {
+// Exit distance of the ray from the axis-aligned box of `span` blocks whose
+// lowest block is (bx, by, bz) (inverse direction precomputed; used only to
+// bound skipped alphas, with a margin, so ~1 ulp error is immaterial).
+CSF_DEV double box_exit(const HashView& vol, int bx, int by, int bz, int span, const V3<double>& o,
+                        const V3<double>& invd) {
   const int b[3] = {bx, by, bz};
   const double org[3] = {vol.ox, vol.oy, vol.oz};
+  const double side = vol.vs * static_cast<double>(8 * span);
   double t = 1e300;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double d = dir.v[a];
-    if (d > 0.0) {
-      const double hi = org[a] + vol.vs * static_cast<double>(8 * b[a] + 8);
-      t = fmin(t, (hi - o.v[a]) / d);
-    } else if (d < 0.0) {
-      const double lo = org[a] + vol.vs * static_cast<double>(8 * b[a]);
-      t = fmin(t, (lo - o.v[a]) / d);
-    }
+    const double lo = org[a] + vol.vs * static_cast<double>(8 * b[a]);
+    if (invd.v[a] > 0.0) t = fmin(t, ((lo + side) - o.v[a]) * invd.v[a]);
+    else if (invd.v[a] < 0.0) t = fmin(t, (lo - o.v[a]) * invd.v[a]);
   }
   return t;
 }
@@ -438,6 +441,9 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
 
   typename V::Cache cache;
   cache.reset();
+  V3<double> invd;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) invd.v[a] = dir.v[a] != 0.0 ? 1.0 / dir.v[a] : 0.0;
   bool have_prev = false;
   double alpha_prev = 0.0, f_prev = 0.0;
   double alpha = t0;
@@ -447,9 +453,15 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
       // unallocated base block: every sample until the block exit is invalid
       const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
                 k0 = ifloor((pz - vol.oz) / vol.vs);
-      if (vol.block(i0 >> 3, j0 >> 3, k0 >> 3) < 0) {
+      const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
+      const int occ = vol.super_occupied(bx, by, bz);
+      int span = 0;
+      if (occ == 0) span = 8;                      // empty 8^3-block super-block
+      else if (vol.block(bx, by, bz) < 0) span = 1;  // unallocated block
+      if (span > 0) {
         have_prev = false;
-        const double lim = block_exit(vol, i0 >> 3, j0 >> 3, k0 >> 3, o, dir) - 1e-6;
+        const int m = span == 8 ? ~7 : ~0;
+        const double lim = box_exit(vol, bx & m, by & m, bz & m, span, o, invd) - 1e-6;
         alpha += step;
         while (alpha < lim && alpha <= t1) alpha += step;
         continue;
@@ -610,6 +622,7 @@ static HashView hash_view(const HashDev& v, int Dp) {
   d.vox = {v.rw, v.fim, Dp};
   d.heads = v.heads; d.keys = v.keys; d.next = v.next;
   d.grid = v.grid;
+  d.occ = v.occ;
   d.gbits = v.gbits;
   d.mask = (1u << v.bits) - 1u;
   d.vs = v.vs; d.ox = v.ox; d.oy = v.oy; d.oz = v.oz; d.mu = v.mu; d.cap = v.cap;
