@@ -102,7 +102,7 @@ __device__ void fuse_voxel(const VoxelStore& vox, long long v, double px, double
 }
 
 template <int G>
-__global__ void __launch_bounds__(256) k_integrate_dense(DenseView vol, const double* __restrict__ depth, int w,
+__global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const double* __restrict__ depth, int w,
                                                          int h, const double* __restrict__ pose,
                                                          const double* __restrict__ intr, int Dp) {
   extern __shared__ double sm[];
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) k_integrate_dense(DenseView vol, const do
 }
 
 template <int G>
-__global__ void __launch_bounds__(256) k_integrate_hashed(HashView vol, const int* __restrict__ coords,
+__global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const int* __restrict__ coords,
                                                           const int* __restrict__ visible,
                                                           const int* __restrict__ counters,
                                                           const double* __restrict__ depth, int w, int h,
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
 }
 
 template <int G, typename V>
-__global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __restrict__ pose,
+__global__ void __launch_bounds__(128, 4) k_raycast_lift(V vol, const double* __restrict__ pose,
                                                       const double* __restrict__ intr, int w, int h, int Dp,
                                                       const double2* __restrict__ hits, double* __restrict__ vre,
                                                       double* __restrict__ nre, double* __restrict__ vim,
