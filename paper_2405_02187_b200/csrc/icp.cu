@@ -18,6 +18,7 @@
 //     the whole level stays on the device (no host round trip).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "csf_internal.h"
 #include "geometry.cuh"
@@ -472,7 +473,7 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
   const int tiles = icp_tiles(w, h, stride);
   // J/r rows are evaluated in channel groups of 2 (or 1): register-light,
   // any width that divides Dp addresses the same channel layout.
-  const int RG = G == 0 ? 0 : (Dp % 2 == 0 ? 2 : 1);
+  const int RG = G == 0 ? 0 : (std::getenv("CSF_ICP_RG2") ? (Dp % 2 == 0 ? 2 : 1) : 1);
   switch (RG) {
     case 0:
       if (smem > 48 * 1024)

@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
 }
 
 template <int G, typename V>
-__global__ void __launch_bounds__(128, 4) k_raycast_lift(V vol, const double* __restrict__ pose,
+__global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __restrict__ pose,
                                                       const double* __restrict__ intr, int w, int h, int Dp,
                                                       const double2* __restrict__ hits, double* __restrict__ vre,
                                                       double* __restrict__ nre, double* __restrict__ vim,
