@@ -58,9 +58,19 @@ __device__ void icp_solve_block(TrackState* st, const double* partials, const in
   const int C = 1 + Dp;
   const int n_acc = 27 * C;
   S* ws = reinterpret_cast<S*>(sm + n_acc) + 48 * threadIdx.x;
+  // tile partials in tile order; loads are issued 8 at a time so the
+  // sequential add chain does not wait on one L2 round trip per tile
   for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
     double total = 0.0;
-    for (int t = 0; t < n_tiles; ++t) total = total + __ldcg(partials + static_cast<long long>(t) * n_acc + a);
+    for (int t = 0; t < n_tiles; t += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = t + u < n_tiles ? __ldcg(partials + static_cast<long long>(t + u) * n_acc + a) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (t + u < n_tiles) total = total + v[u];
+    }
     sm[a] = total;
   }
   if (threadIdx.x == 0) {
@@ -138,7 +148,7 @@ __global__ void __launch_bounds__(256) k_icp_solve(TrackState* st, const double*
 }
 
 template <int G>
-__global__ void __launch_bounds__(256, 2) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
+__global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
                                                     int w, int h, int stride, const double* __restrict__ intr,
                                                     const double* pose, const double* __restrict__ vre,
                                                     const double* __restrict__ nre, const double* __restrict__ vim,
@@ -449,11 +459,11 @@ int icp_tiles(int w, int h, int stride) {
   return (nxs * nys + kTile - 1) / kTile;
 }
 
-// Slots per shared-memory chunk: small enough for two CTAs per SM.
+// Slots per shared-memory chunk of the (J, r) rows.
 static int reduce_chunk(int C) {
-  if (8 * C * (16 + 128 * 7) <= 100 * 1024) return 128;
-  if (8 * C * (16 + 64 * 7) <= 100 * 1024) return 64;
-  return 32;
+  if (8 * C * (16 + 256 * 7) <= 200 * 1024) return 256;
+  if (8 * C * (16 + 128 * 7) <= 200 * 1024) return 128;
+  return 64;
 }
 
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp) {
