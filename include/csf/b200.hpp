@@ -1,0 +1,206 @@
+// csf/b200.hpp — C++ mirror of the reference API (proj/include/csf/*.hpp)
+// over the C-ABI in include/csf_b200.h.  Header-only; link libcsf_b200.so.
+//
+// Names, argument meaning and error behaviour follow the reference:
+//   bilateral_filter / build_depth_pyramid   frames.hpp:56-65, frames.cpp:7-75
+//   measure_surface                          frames.hpp:86-114
+//   TsdfVolume (+ HashedVolume), surface_update, raycast   tsdf.hpp:38-284
+//   track_frame                              icp.hpp:130-133
+// Errors are thrown as std::invalid_argument / std::domain_error /
+// std::runtime_error exactly where the reference throws them.  Scalars are
+// plain structs (no Eigen): Complex{re, im}, lifted values as (1+D) doubles.
+#pragma once
+
+#include <array>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../csf_b200.h"
+
+namespace csf {
+namespace b200 {
+
+inline void check(csf_ctx ctx, int rc) {
+  if (rc == CSF_OK) return;
+  const std::string msg = ctx ? csf_last_error(ctx) : "csf_b200 error";
+  if (rc == CSF_EINVAL) throw std::invalid_argument(msg);
+  if (rc == CSF_EDOMAIN) throw std::domain_error(msg);
+  throw std::runtime_error(msg);
+}
+
+// image.hpp:12-35
+template <typename T>
+struct Image {
+  int width = 0, height = 0;
+  std::vector<T> data;
+  Image() = default;
+  Image(int w, int h, T fill = T{}) : width(w), height(h), data(static_cast<size_t>(w) * h, fill) {}
+  bool in_bounds(int x, int y) const { return x >= 0 && x < width && y >= 0 && y < height; }
+  T& at(int x, int y) { return data[static_cast<size_t>(y) * width + x]; }
+  const T& at(int x, int y) const { return data[static_cast<size_t>(y) * width + x]; }
+};
+
+// A pose with D perturbation channels: 12 scalars x (1+D), rotation
+// row-major then translation (se3.hpp:21-45 with the channels unpacked).
+struct LiftedPose {
+  int channels = 0;
+  std::vector<double> v;  // [12][1+D]
+  explicit LiftedPose(int D = 0) : channels(D), v(12 * (1 + D), 0.0) {
+    for (int i = 0; i < 3; ++i) at(4 * i, 0) = 1.0;
+  }
+  double& at(int e, int c) { return v[e * (1 + channels) + c]; }
+  double at(int e, int c) const { return v[e * (1 + channels) + c]; }
+  static LiftedPose real(const std::array<double, 12>& p, int D = 0) {
+    LiftedPose o(D);
+    for (int e = 0; e < 12; ++e) o.at(e, 0) = p[e];
+    return o;
+  }
+};
+
+struct LiftedIntrinsics {
+  int channels = 0;
+  std::vector<double> v;  // [4][1+D]: fx, fy, cx, cy
+  LiftedIntrinsics(const csf_intrinsics& k, int D = 0) : channels(D), v(4 * (1 + D), 0.0) {
+    v[0] = k.fx;
+    v[1 + D] = k.fy;
+    v[2 * (1 + D)] = k.cx;
+    v[3 * (1 + D)] = k.cy;
+  }
+};
+
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    if (csf_ctx_create(device, &ctx_) != CSF_OK)
+      throw std::runtime_error("csf_b200: no usable CUDA device (no CPU fallback)");
+  }
+  ~Context() { csf_ctx_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  csf_ctx get() const { return ctx_; }
+
+ private:
+  csf_ctx ctx_ = nullptr;
+};
+
+// frames.cpp:7-38
+inline Image<double> bilateral_filter(Context& c, const Image<double>& depth, double sigma_s = 4.5,
+                                      double sigma_r = 0.03, int radius = 3) {
+  Image<double> out(depth.width, depth.height);
+  check(c.get(), csf_bilateral_filter(c.get(), depth.data.data(), depth.width, depth.height, sigma_s, sigma_r, radius,
+                                      out.data.data()));
+  return out;
+}
+
+// frames.cpp:40-75
+inline Image<double> downsample_depth(Context& c, const Image<double>& depth, double sigma_r = 0.03) {
+  Image<double> out(depth.width / 2, depth.height / 2);
+  check(c.get(), csf_downsample_depth(c.get(), depth.data.data(), depth.width, depth.height, sigma_r, out.data.data()));
+  return out;
+}
+inline std::vector<Image<double>> build_depth_pyramid(Context& c, const Image<double>& depth, int levels = 3,
+                                                      double sigma_r = 0.03) {
+  std::vector<Image<double>> pyr{depth};
+  for (int l = 1; l < levels; ++l) pyr.push_back(downsample_depth(c, pyr.back(), sigma_r));
+  return pyr;
+}
+
+// tsdf.hpp:38-78 — a device-resident volume whose field carries D channels.
+class Volume {
+ public:
+  Volume(Context& c, const csf_volume_params& p, int channels) : ctx_(c.get()), channels_(channels), n_(1) {
+    check(ctx_, csf_volume_create_dense(ctx_, &p, channels, &vol_));
+    n_ = static_cast<size_t>(p.dims[0]) * p.dims[1] * p.dims[2];
+  }
+  Volume(Context& c, const csf_hash_params& p, int channels) : ctx_(c.get()), channels_(channels), hashed_(true) {
+    check(ctx_, csf_volume_create_hashed(ctx_, &p, channels, &vol_));
+  }
+  ~Volume() { csf_volume_destroy(vol_); }
+  Volume(const Volume&) = delete;
+  Volume& operator=(const Volume&) = delete;
+  csf_volume get() const { return vol_; }
+  int channels() const { return channels_; }
+  size_t voxel_count() const {
+    if (!hashed_) return n_;
+    int nb = 0;
+    check(ctx_, csf_volume_block_count(vol_, &nb));
+    return static_cast<size_t>(nb) * 512;
+  }
+  // host copies: field [n][1+D], weight [n]
+  void download(std::vector<double>& field, std::vector<double>& weight) const {
+    const size_t n = voxel_count();
+    field.resize(n * (1 + channels_));
+    weight.resize(n);
+    check(ctx_, csf_volume_download(vol_, field.data(), weight.data()));
+  }
+  void upload(const std::vector<double>& field, const std::vector<double>& weight) {
+    check(ctx_, csf_volume_upload(vol_, field.data(), weight.data()));
+  }
+
+ private:
+  csf_ctx ctx_;
+  csf_volume vol_ = nullptr;
+  int channels_ = 0;
+  bool hashed_ = false;
+  size_t n_ = 0;
+};
+
+// tsdf.cpp:11-40 — surface_update(volume, depth, camera_to_world, k)
+inline int surface_update(Context& c, Volume& vol, const Image<double>& depth, const LiftedPose& camera_to_world,
+                          const LiftedIntrinsics& k) {
+  if (camera_to_world.channels != vol.channels() || k.channels != vol.channels())
+    throw std::invalid_argument("surface_update: channel count mismatch");
+  int n_visible = 0;
+  check(c.get(), csf_surface_update(vol.get(), depth.data.data(), depth.width, depth.height, camera_to_world.v.data(),
+                                    k.v.data(), &n_visible));
+  return n_visible;
+}
+
+// frames.hpp:67-71 SurfaceMaps with channels unpacked: [h][w][3][1+D]
+struct SurfaceMaps {
+  int width = 0, height = 0, channels = 0;
+  std::vector<double> vertices, normals;
+};
+
+// tsdf.hpp:209-284
+inline SurfaceMaps raycast(Context& c, const Volume& vol, const LiftedPose& camera_to_world,
+                           const LiftedIntrinsics& k, int width, int height, const csf_raycast_cfg* cfg = nullptr) {
+  SurfaceMaps m;
+  m.width = width;
+  m.height = height;
+  m.channels = vol.channels();
+  m.vertices.resize(static_cast<size_t>(width) * height * 3 * (1 + m.channels));
+  m.normals.resize(m.vertices.size());
+  check(c.get(), csf_raycast(vol.get(), camera_to_world.v.data(), k.v.data(), width, height, cfg, m.vertices.data(),
+                             m.normals.data()));
+  return m;
+}
+
+// icp.hpp:119-133
+struct TrackResult {
+  std::array<double, 12> pose{};
+  int iterations = 0;
+  bool converged = false;
+  double final_loss = 0.0;
+  int correspondences = 0;
+};
+inline TrackResult track_frame(Context& c, const Volume& vol, const Image<double>& depth,
+                               const std::array<double, 12>& init_camera_to_world, const csf_intrinsics& k,
+                               const csf_icp_cfg* cfg = nullptr) {
+  csf_icp_cfg def;
+  csf_default_icp_cfg(&def);
+  TrackResult r;
+  csf_track_result tr{};
+  check(c.get(), csf_track_frame(vol.get(), depth.data.data(), depth.width, depth.height, init_camera_to_world.data(),
+                                 &k, cfg ? cfg : &def, r.pose.data(), &tr));
+  r.iterations = tr.iterations;
+  r.converged = tr.converged != 0;
+  r.final_loss = tr.final_loss;
+  r.correspondences = tr.correspondences;
+  return r;
+}
+
+}  // namespace b200
+}  // namespace csf

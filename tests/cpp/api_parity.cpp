@@ -1,0 +1,217 @@
+// The reference's own TSDF / ICP test cases (proj/tests/test_tsdf.cpp,
+// test_icp.cpp) run through the C++ mirror (include/csf/b200.hpp) on the
+// device, with the CPU oracle (oracle/, header-only) as the checker.
+// Built and run by tests/test_cpp_api.py (GPU).
+#include <cmath>
+#include <cstdio>
+
+#include "csf/b200.hpp"
+#include "orc_pipeline.hpp"
+
+namespace B = csf::b200;
+
+static int g_fail = 0;
+#define CHECK(c)                                                       \
+  do {                                                                 \
+    if (!(c)) {                                                        \
+      ++g_fail;                                                        \
+      std::printf("  FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);       \
+    }                                                                  \
+  } while (0)
+
+static csf_intrinsics small_camera() {
+  csf_intrinsics k;
+  k.fx = 120; k.fy = 120; k.cx = 79.5; k.cy = 59.5; k.width = 160; k.height = 120; k.depth_scale = 5000;
+  return k;
+}
+static orc::Intrinsics to_orc(const csf_intrinsics& k) {
+  orc::Intrinsics o;
+  o.fx = k.fx; o.fy = k.fy; o.cx = k.cx; o.cy = k.cy; o.width = k.width; o.height = k.height;
+  return o;
+}
+static std::array<double, 12> arr(const orc::Pose& p) {
+  std::array<double, 12> a{};
+  for (int e = 0; e < 9; ++e) a[e] = p.rotation(e / 3, e % 3);
+  for (int e = 0; e < 3; ++e) a[9 + e] = p.translation[e];
+  return a;
+}
+static B::Image<double> img(const orc::Image<double>& d) {
+  B::Image<double> o(d.width, d.height);
+  o.data = d.data;
+  return o;
+}
+
+int main() {
+  B::Context ctx(0);
+  const csf_intrinsics k = small_camera();
+  const orc::Intrinsics ko = to_orc(k);
+  orc::Scene sphere;
+  sphere.spheres.push_back({orc::Vec3d(), 0.5});
+  std::vector<orc::Pose> poses;
+  for (int i = 0; i < 8; ++i) poses.push_back(orc::orbit_pose(orc::Vec3d(), 1.6, 0.8, 2.0 * M_PI * i / 8));
+
+  {  // test_tsdf.cpp:248-276 — fusing one frame stores the raw measurement bit for bit
+    csf_volume_params p;
+    p.dims[0] = p.dims[1] = p.dims[2] = 24;
+    p.voxel_size = 0.02;
+    p.origin[0] = -0.24; p.origin[1] = -0.24; p.origin[2] = 0.1;
+    p.mu = 0.1;
+    p.weight_cap = 128;
+    B::Volume vol(ctx, p, 1);
+    const orc::Image<double> depth = orc::render_depth(sphere, poses[0], ko);
+    B::surface_update(ctx, vol, img(depth), B::LiftedPose::real(arr(poses[0]), 1), B::LiftedIntrinsics(k, 1));
+    std::vector<double> f, w;
+    vol.download(f, w);
+    const orc::Pose w2c = poses[0].inverse();
+    int observed = 0;
+    bool ok = true;
+    for (int kk = 0; kk < 24; ++kk)
+      for (int j = 0; j < 24; ++j)
+        for (int i = 0; i < 24; ++i) {
+          const size_t idx = (static_cast<size_t>(kk) * 24 + j) * 24 + i;
+          const orc::Vec3d pos(-0.24 + 0.02 * double(i), -0.24 + 0.02 * double(j), 0.1 + 0.02 * double(kk));
+          const auto m = orc::measured_tsdf<double>(orc::complex_depth(depth), w2c, ko, 0.1, pos,
+                                                    poses[0].translation);
+          if (m) {
+            ++observed;
+            ok = ok && w[idx] == 1.0 && f[2 * idx] == *m && f[2 * idx + 1] == 0.0;
+          } else {
+            ok = ok && w[idx] == 0.0 && f[2 * idx] == 1.0;
+          }
+        }
+    CHECK(ok);
+    CHECK(observed > 500);
+    std::printf("ok   fusion stores psi bit for bit (observed %d)\n", observed);
+  }
+
+  {  // test_tsdf.cpp:278-309 — capped running average
+    csf_volume_params p;
+    p.dims[0] = p.dims[1] = p.dims[2] = 4;
+    p.voxel_size = 0.02;
+    p.origin[0] = -0.03; p.origin[1] = -0.03; p.origin[2] = 1.9;
+    p.mu = 0.1;
+    p.weight_cap = 4.0;
+    B::Volume vol(ctx, p, 0);
+    const B::LiftedPose id = B::LiftedPose::real({1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0}, 0);
+    const B::LiftedIntrinsics kk(k, 0);
+    auto flat = [&](double d) { return B::Image<double>(k.width, k.height, d); };
+    B::surface_update(ctx, vol, flat(2.00), id, kk);
+    B::surface_update(ctx, vol, flat(2.01), id, kk);
+    std::vector<double> f, w;
+    vol.download(f, w);
+    const size_t idx = (1 * 4 + 1) * 4 + 1;
+    const orc::Vec3d pos(-0.03 + 0.02, -0.03 + 0.02, 1.9 + 0.02);
+    const auto m1 = orc::measured_tsdf<double>(orc::Image<double>(k.width, k.height, 2.00), orc::Pose(), ko, 0.1, pos,
+                                               orc::Vec3d());
+    const auto m2 = orc::measured_tsdf<double>(orc::Image<double>(k.width, k.height, 2.01), orc::Pose(), ko, 0.1, pos,
+                                               orc::Vec3d());
+    CHECK(w[idx] == 2.0);
+    CHECK(std::fabs(f[idx] - 0.5 * (*m1 + *m2)) <= 1e-15 * (1 + std::fabs(f[idx])));
+    for (int i = 0; i < 10; ++i) B::surface_update(ctx, vol, flat(2.00), id, kk);
+    vol.download(f, w);
+    CHECK(w[idx] == 4.0);
+    const double late = f[idx];
+    B::surface_update(ctx, vol, flat(2.00), id, kk);
+    vol.download(f, w);
+    CHECK(w[idx] == 4.0 && std::fabs(f[idx] - *m1) < std::fabs(late - *m1));
+    std::printf("ok   capped running average\n");
+  }
+
+  // shared fused sphere (test_tsdf.cpp:37-64)
+  csf_volume_params sp;
+  sp.dims[0] = sp.dims[1] = sp.dims[2] = 64;
+  sp.voxel_size = 0.02;
+  sp.origin[0] = sp.origin[1] = sp.origin[2] = -0.63;
+  sp.mu = 0.1;
+  sp.weight_cap = 128;
+  B::Volume fused(ctx, sp, 0);
+  for (const orc::Pose& p : poses)
+    B::surface_update(ctx, fused, img(orc::render_depth(sphere, p, ko)), B::LiftedPose::real(arr(p)),
+                      B::LiftedIntrinsics(k, 0));
+
+  {  // test_tsdf.cpp:392-441 — raycast recovers the fused sphere
+    const orc::Pose view = orc::orbit_pose(orc::Vec3d(), 1.5, 0.7, 0.39);
+    const B::SurfaceMaps m = B::raycast(ctx, fused, B::LiftedPose::real(arr(view)), B::LiftedIntrinsics(k, 0), 160, 120);
+    int hits = 0, misses_ok = 0;
+    double max_e = 0, sum_e = 0, worst_n = 1.0;
+    bool required = true;
+    for (int y = 0; y < 120; ++y)
+      for (int x = 0; x < 160; ++x) {
+        const orc::Vec3d dir =
+            orc::normalized(view.rotation * orc::Vec3d((x - k.cx) / k.fx, (y - k.cy) / k.fy, 1.0));
+        const orc::Vec3d o = view.translation;
+        const double tca = -orc::dot(o, dir);
+        const double b2 = orc::squared_norm(o + tca * dir);
+        const size_t base = (static_cast<size_t>(y) * 160 + x) * 3;
+        const orc::Vec3d v(m.vertices[base], m.vertices[base + 1], m.vertices[base + 2]);
+        const orc::Vec3d n(m.normals[base], m.normals[base + 1], m.normals[base + 2]);
+        const bool valid = orc::dot(n, n) > 0.5;
+        const double tic = b2 < 0.25 ? tca - std::sqrt(0.25 - b2) : 0.0;
+        if (b2 < 0.46 * 0.46 && tca > 0 && (o + tic * dir).z() > -0.1) {
+          required = required && valid;
+          if (!valid) continue;
+          const double e = std::fabs(orc::norm(v) - 0.5);
+          max_e = std::max(max_e, e);
+          sum_e += e;
+          worst_n = std::min(worst_n, orc::dot(n, orc::normalized(v)));
+          ++hits;
+        } else if (b2 > 0.54 * 0.54 && !valid) {
+          ++misses_ok;
+        }
+      }
+    CHECK(required && hits > 1000 && misses_ok > 1000 && sum_e / hits < 0.005 && max_e < 0.03 && worst_n > 0.95);
+    std::printf("ok   raycast recovers the fused sphere (hits %d, mean err %.2e m)\n", hits, sum_e / hits);
+  }
+
+  {  // test_icp.cpp:323-370 — tracking refines a perturbed pose (linearized solver), bit-identical rerun
+    orc::Scene scene;
+    scene.planes.push_back({orc::Vec3d(0, 0, 1), 0.0});
+    scene.spheres.push_back({orc::Vec3d(0.0, 0.1, 0.55), 0.5});
+    scene.spheres.push_back({orc::Vec3d(0.85, 0.55, 0.3), 0.3});
+    const orc::Vec3d target(0.25, 0.15, 0.35);
+    csf_volume_params tp;
+    tp.dims[0] = tp.dims[1] = tp.dims[2] = 72;
+    tp.voxel_size = 0.026;
+    tp.origin[0] = -0.7; tp.origin[1] = -0.8; tp.origin[2] = -0.33;
+    tp.mu = 5 * 0.026;
+    tp.weight_cap = 128;
+    B::Volume vol(ctx, tp, 0);
+    for (int i = 0; i < 8; ++i) {
+      const orc::Pose p = orc::orbit_pose(target, 1.9, 1.4, 2.0 * M_PI * i / 8);
+      B::surface_update(ctx, vol, img(orc::render_depth(scene, p, ko)), B::LiftedPose::real(arr(p)),
+                        B::LiftedIntrinsics(k, 0));
+    }
+    const orc::Pose truth = orc::orbit_pose(target, 1.9, 1.4, 0.39);
+    const orc::Pose init = orc::apply_increment(orc::Vec6<double>{0.03, -0.02, 0.02, 0.02, -0.015, 0.015}, truth);
+    const B::Image<double> frame = img(orc::render_depth(scene, truth, ko));
+    csf_icp_cfg cfg;
+    csf_default_icp_cfg(&cfg);
+    const B::TrackResult r = B::track_frame(ctx, vol, frame, arr(init), k, &cfg);
+    orc::Pose got;
+    for (int e = 0; e < 9; ++e) got.rotation(e / 3, e % 3) = r.pose[e];
+    for (int e = 0; e < 3; ++e) got.translation[e] = r.pose[9 + e];
+    const double terr = orc::norm(got.translation - truth.translation);
+    orc::Pose rel;
+    rel.rotation = orc::transpose(truth.rotation) * got.rotation;
+    const double rerr = orc::log_angle(rel) * 180.0 / M_PI;
+    CHECK(r.iterations > 0 && r.converged && r.correspondences > 500);
+    CHECK(terr < 0.008 && rerr < 0.15);
+    const B::TrackResult again = B::track_frame(ctx, vol, frame, arr(init), k, &cfg);
+    CHECK(again.pose == r.pose);
+    std::printf("ok   track_frame: %d iterations, %d correspondences, %.2e m, %.3f deg\n", r.iterations,
+                r.correspondences, terr, rerr);
+  }
+
+  {  // error behaviour: invalid arguments throw std::invalid_argument
+    bool threw = false;
+    try {
+      B::bilateral_filter(ctx, B::Image<double>(16, 16, 1.0), 4.5, 0.03, 9);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    std::printf("ok   invalid arguments raise std::invalid_argument\n");
+  }
+  std::printf("C++ API summary: failures=%d\n", g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
