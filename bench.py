@@ -179,8 +179,9 @@ def algorithmic_bytes_per_step(cat, stats, D, W, H, n_frames):
     vis_vox = float(stats[:n_frames, 4].sum()) * 512
     tracked = max(n_frames - 1, 0)
     if cat == "integrate":
-        return vis_vox * 2 * (16 + 8 * D) + n_frames * 8 * P, \
-            "sum over frames of visible voxels x 2 x (16 + 8D) B (read+write F.re,W and D channels) + depth"
+        fused = float(stats[:n_frames, 6].sum())
+        return fused * 2 * (16 + 8 * D) + n_frames * 8 * P, \
+            "sum over frames of fused voxels x 2 x (16 + 8D) B (read+write F.re,W and D channels) + depth"
     if cat == "raycast":
         # each visible voxel's (F.re, W) read once per level + real maps/hits written
         return 3 * vis_vox * 16 * tracked / max(n_frames, 1) + tracked * P_tot * (6 * 8 + 16), \

@@ -192,7 +192,8 @@ int csf_pipeline_upload(csf_pipeline p, const float* depth, const double* gt, in
 /* Runs the uploaded frames on the device; asynchronous on the context stream. */
 int csf_pipeline_run(csf_pipeline p, int n_frames);
 /* Synchronises; gradient [D], poses [n][12][1+D] (optional), stats [n][8]
- * (optional: iterations, correspondences, converged, blocks, visible, new). */
+ * (optional: iterations, correspondences, converged, allocated blocks,
+ * visible blocks, new blocks, fused voxels, 0). */
 int csf_pipeline_result(csf_pipeline p, double* gradient, double* objective, double* poses, int32_t* stats);
 /* One end-to-end call from host buffers: upload, run, read back. */
 int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames, double* gradient,

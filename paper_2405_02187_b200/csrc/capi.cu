@@ -221,8 +221,10 @@ int volume_init_common(csf_volume v, int n_channels) {
   return CSF_OK;
 }
 
-// Fuse one double depth frame already on the device.
-int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double* d_pose, const double* d_intr) {
+// Fuse one double depth frame already on the device.  upd (nullable) counts
+// the fused voxels.
+int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double* d_pose, const double* d_intr,
+                int* upd = nullptr) {
   const Launch L = launch_of(v->ctx);
   if (v->hashed) {
     const int rc = ensure_alloc_scratch(v, w, h);
@@ -232,10 +234,10 @@ int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double*
       launch_allocate(L, v->hash, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr);
     }
     PROF(v->ctx, kPIntegrate);
-    launch_integrate_hashed(L, v->hash, v->G, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr);
+    launch_integrate_hashed(L, v->hash, v->G, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr, upd);
   } else {
     PROF(v->ctx, kPIntegrate);
-    launch_integrate_dense(L, v->dense, v->G, v->Dp, d_depth, w, h, d_pose, d_intr);
+    launch_integrate_dense(L, v->dense, v->G, v->Dp, d_depth, w, h, d_pose, d_intr, upd);
   }
   return CSF_OK;
 }
@@ -852,7 +854,8 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
   launch_seed(L, p->G, p->Dp, p->dirs.p, p->D, cfg.h, p->gt.p, p->kbase.p, p->pose.p, p->intr_levels.p, p->levels);
   launch_frame_begin(L, st, 0);
   launch_bilateral(L, p->frames.p, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
-  rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p);
+  int* upd = &st->pad[1];
+  rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p, upd);
   if (rc) return rc;
   launch_frame_end(L, st, p->pose.p, p->traj.p, p->Dp, p->stats.p, nblk, counters);
 
@@ -883,7 +886,7 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
         (void)tiles;
       }
     }
-    rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p);
+    rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p, upd);
     if (rc) return rc;
     launch_frame_end(L, st, p->pose.p, p->traj.p, p->Dp, p->stats.p, nblk, counters);
   }

@@ -82,10 +82,11 @@ void launch_measure(const Launch& L, const double* depth, int w, int h, const do
                     double* norm);
 
 // ---- volume.cu
+// upd (nullable): incremented by the number of voxels fused
 void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* depth, int w, int h,
-                            const double* pose, const double* intr);
+                            const double* pose, const double* intr, int* upd);
 void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, const AllocScratch& a,
-                             const double* depth, int w, int h, const double* pose, const double* intr);
+                             const double* depth, int w, int h, const double* pose, const double* intr, int* upd);
 void launch_allocate(const Launch& L, const HashDev& v, int Dp, AllocScratch& a, const double* depth, int w, int h,
                      const double* pose, const double* intr);
 // hits: [w*h] scratch (alpha_prev, alpha) of the zero crossing per pixel

@@ -375,6 +375,7 @@ __global__ void k_seed(const int* __restrict__ dirs, int D, double hstep, const 
 
 __global__ void k_frame_begin(TrackState* st, int frame) {
   st->frame = frame;
+  st->pad[1] = 0;  // voxels fused this frame
   st->iterations = 0;
   st->converged = 0;
   st->n_corr = 0;
@@ -394,6 +395,7 @@ __global__ void k_frame_end(const TrackState* st, const double* pose, double* tr
     s[3] = n_blocks ? *n_blocks : 0;
     s[4] = counters ? counters[0] : 0;
     s[5] = counters ? counters[1] : 0;
+    s[6] = st->pad[1];
   }
 }
 

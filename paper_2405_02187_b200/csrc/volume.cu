@@ -71,7 +71,7 @@ __device__ void load_pose_intr(const double* sm, int Dp, int g0, Pose<S>* w2c, V
 // Fuse one voxel: the real pass decides validity, then every channel group
 // re-evaluates psi (bit-identical real part) and updates its channels.
 template <int G>
-__device__ void fuse_voxel(const VoxelStore& vox, long long v, double px, double py, double pz,
+__device__ bool fuse_voxel(const VoxelStore& vox, long long v, double px, double py, double pz,
                            const double* __restrict__ depth, int w, int h, double mu, double cap, int Dp,
                            const double* sm) {
   using S = Scal<G>;
@@ -86,7 +86,7 @@ __device__ void fuse_voxel(const VoxelStore& vox, long long v, double px, double
     load_pose_intr<S>(sm, Dp, g0, &w2c, &c, &k);
     S psi;
     // validity depends on real parts only: the first pass decides for all
-    if (!measured_tsdf<S>(depth, w, h, w2c, k, mu, px, py, pz, c, &psi)) return;
+    if (!measured_tsdf<S>(depth, w, h, w2c, k, mu, px, py, pz, c, &psi)) return false;
     if (gi == 0) rw = vox.rw[v];
     const S f = field_at<S>(vox, v, rw.x, g0);
     const S fn = (rw.y * f + psi) / (rw.y + 1.0);
@@ -99,12 +99,21 @@ __device__ void fuse_voxel(const VoxelStore& vox, long long v, double px, double
   }
   const double wn = rw.y + 1.0;
   vox.rw[v] = make_double2(fre, cap < wn ? cap : wn);
+  return true;
+}
+
+// Warp-aggregated count of fused voxels (bench's algorithmic-byte model).
+CSF_DEV void count_updates(int* upd, bool fused) {
+  if (!upd) return;
+  const unsigned m = __activemask();
+  const unsigned b = __ballot_sync(m, fused);
+  if ((threadIdx.x & 31) == __ffs(m) - 1 && b) atomicAdd(upd, __popc(b));
 }
 
 template <int G>
 __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const double* __restrict__ depth, int w,
                                                          int h, const double* __restrict__ pose,
-                                                         const double* __restrict__ intr, int Dp) {
+                                                         const double* __restrict__ intr, int Dp, int* upd) {
   extern __shared__ double sm[];
   stage_pose_w2c<G>(pose, intr, Dp, sm);
   const long long n = static_cast<long long>(vol.nx) * vol.ny * vol.nz;
@@ -116,7 +125,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     const double px = vol.ox + vol.vs * static_cast<double>(i);
     const double py = vol.oy + vol.vs * static_cast<double>(j);
     const double pz = vol.oz + vol.vs * static_cast<double>(k);
-    fuse_voxel<G>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
+    count_updates(upd, fuse_voxel<G>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
   }
 }
 
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const
                                                           const int* __restrict__ counters,
                                                           const double* __restrict__ depth, int w, int h,
                                                           const double* __restrict__ pose,
-                                                          const double* __restrict__ intr, int Dp) {
+                                                          const double* __restrict__ intr, int Dp, int* upd) {
   extern __shared__ double sm[];
   stage_pose_w2c<G>(pose, intr, Dp, sm);
   const int n_vis = counters[0];
@@ -139,8 +148,8 @@ __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const
       const double px = vol.ox + vol.vs * static_cast<double>(8 * bx + lx);
       const double py = vol.oy + vol.vs * static_cast<double>(8 * by + ly);
       const double pz = vol.oz + vol.vs * static_cast<double>(8 * bz + lz);
-      fuse_voxel<G>(vol.vox, static_cast<long long>(b) * kBlockVoxels + l, px, py, pz, depth, w, h, vol.mu, vol.cap,
-                    Dp, sm);
+      count_updates(upd, fuse_voxel<G>(vol.vox, static_cast<long long>(b) * kBlockVoxels + l, px, py, pz, depth, w,
+                                       h, vol.mu, vol.cap, Dp, sm));
     }
   }
 }
@@ -661,25 +670,25 @@ static int integrate_group(int G, int Dp) {
 }
 
 void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* depth, int w, int h,
-                            const double* pose, const double* intr) {
+                            const double* pose, const double* intr, int* upd) {
   G = integrate_group(G, Dp);
   const DenseView view = dense_view(v, Dp);
   const size_t smem = sizeof(double) * 19 * (1 + Dp);
   const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
   const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, sm_count() * 16LL));
-  CSF_DISPATCH_G(G, (k_integrate_dense<kG><<<grid, 256, smem, L.stream>>>(view, depth, w, h, pose, intr, Dp)));
+  CSF_DISPATCH_G(G, (k_integrate_dense<kG><<<grid, 256, smem, L.stream>>>(view, depth, w, h, pose, intr, Dp, upd)));
   ++*L.launches;
   chk("integrate_dense");
 }
 
 void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, const AllocScratch& a,
-                             const double* depth, int w, int h, const double* pose, const double* intr) {
+                             const double* depth, int w, int h, const double* pose, const double* intr, int* upd) {
   G = integrate_group(G, Dp);
   const HashView view = hash_view(v, Dp);
   const size_t smem = sizeof(double) * 19 * (1 + Dp);
   const int grid = sm_count() * 8;
   CSF_DISPATCH_G(G, (k_integrate_hashed<kG><<<grid, 256, smem, L.stream>>>(view, v.coords, a.visible, a.counters,
-                                                                           depth, w, h, pose, intr, Dp)));
+                                                                           depth, w, h, pose, intr, Dp, upd)));
   ++*L.launches;
   chk("integrate_hashed");
 }
