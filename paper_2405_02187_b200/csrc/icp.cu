@@ -235,43 +235,79 @@ __global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const 
     }
     const int pos = before + __popc(ballot & ((1u << lane) - 1u));
     if (corr) {
+      // One lifted (J, r) row in tangent form: the real chain once, then each
+      // channel's im by the truncated-Complex rule of every operation
+      // (csfd.hpp:44-58) applied to the saved real intermediates.
       const long long m = static_cast<long long>(v) * w + u;
       double* row = s_jr + static_cast<long long>(pos) * 7 * C;
-      const int passes = G == 0 ? 1 : Dp / G;
-      for (int gi = 0; gi < passes; ++gi) {
-        const int g0 = gi * G;
-        Pose<S> base;
+      const double d = depth[y * w + x];
+      // vertex: ((d*(x - cx))/fx, (d*(y - cy))/fy, d)
+      const double tx = static_cast<double>(x) - s_intr[2 * C], ty = static_cast<double>(y) - s_intr[3 * C];
+      const double nx = d * tx, ny = d * ty;
+      const double kfx = s_intr[0], kfy = s_intr[C];
+      const double vre3[3] = {nx / kfx, ny / kfy, d};
+      const double ifx = 1.0 / (kfx * kfx), ify = 1.0 / (kfy * kfy);
+      (void)ifx;
+      (void)ify;
+      double R[9], T[3], MV[3], MN[3], P[3], PR[9];
 #pragma unroll
-        for (int e = 0; e < 9; ++e) base.R.m[e] = load_ch<S>(s_pose + e * C, g0, G);
+      for (int e = 0; e < 9; ++e) R[e] = s_pose[e * C];
 #pragma unroll
-        for (int e = 0; e < 3; ++e) base.t.v[e] = load_ch<S>(s_pose + (9 + e) * C, g0, G);
-        const S kfx = load_ch<S>(s_intr, g0, G), kfy = load_ch<S>(s_intr + C, g0, G);
-        const S kcx = load_ch<S>(s_intr + 2 * C, g0, G), kcy = load_ch<S>(s_intr + 3 * C, g0, G);
-        const double d = depth[y * w + x];
-        const V3<S> vert = mk3<S>((d * (static_cast<double>(x) - kcx)) / kfx, (d * (static_cast<double>(y) - kcy)) / kfy,
-                                  lit<S>(d));
-        V3<S> mv, mn;
+      for (int e = 0; e < 3; ++e) T[e] = s_pose[(9 + e) * C];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if constexpr (G == 0) {
-            mv.v[c] = vre[3 * m + c];
-            mn.v[c] = nre[3 * m + c];
-          } else {
-            mv.v[c].re = vre[3 * m + c];
-            mn.v[c].re = nre[3 * m + c];
+      for (int c3 = 0; c3 < 3; ++c3) {
+        MV[c3] = vre[3 * m + c3];
+        MN[c3] = nre[3 * m + c3];
+      }
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-              mv.v[c].im[g] = vim[(3 * m + c) * Dp + g0 + g];
-              mn.v[c].im[g] = nim[(3 * m + c) * Dp + g0 + g];
-            }
-          }
+      for (int r3 = 0; r3 < 3; ++r3) {
+#pragma unroll
+        for (int c3 = 0; c3 < 3; ++c3) PR[3 * r3 + c3] = R[3 * r3 + c3] * vre3[c3];
+        P[r3] = (PR[3 * r3] + (PR[3 * r3 + 1] + PR[3 * r3 + 2])) + T[r3];
+      }
+      const double DF[3] = {P[0] - MV[0], P[1] - MV[1], P[2] - MV[2]};
+      const double rr = DF[0] * MN[0] + (DF[1] * MN[1] + DF[2] * MN[2]);
+      const double PN[3] = {P[1] * MN[2] - P[2] * MN[1], P[2] * MN[0] - P[0] * MN[2], P[0] * MN[1] - P[1] * MN[0]};
+      row[0] = MN[0];
+      row[C] = MN[1];
+      row[2 * C] = MN[2];
+      row[3 * C] = PN[0];
+      row[4 * C] = PN[1];
+      row[5 * C] = PN[2];
+      row[6 * C] = rr;
+      for (int ch = 1; ch <= Dp; ++ch) {
+        // vertex channels (intrinsics seeds): d*(x - cx) has im d*(-cx.im)
+        const double tnx = d * -s_intr[2 * C + ch], tny = d * -s_intr[3 * C + ch];
+        const double vim3[3] = {CSF_CH_DIV(tnx * kfx - nx * s_intr[ch], kfx * kfx, ifx),
+                                CSF_CH_DIV(tny * kfy - ny * s_intr[C + ch], kfy * kfy, ify), 0.0};
+        double Pi[3], MVi[3], MNi[3];
+#pragma unroll
+        for (int c3 = 0; c3 < 3; ++c3) {
+          MVi[c3] = vim[(3 * m + c3) * Dp + ch - 1];
+          MNi[c3] = nim[(3 * m + c3) * Dp + ch - 1];
         }
-        const V3<S> p = apply(base, vert);
-        const S r = dot3(sub3(p, mv), mn);
-        const V3<S> pn = cross3(p, mn);
-        const S jr[7] = {mn.v[0], mn.v[1], mn.v[2], pn.v[0], pn.v[1], pn.v[2], r};
 #pragma unroll
-        for (int q = 0; q < 7; ++q) store_ch<S>(row + q * C, jr[q], g0, G, gi == 0);
+        for (int r3 = 0; r3 < 3; ++r3) {
+          double qi[3];
+#pragma unroll
+          for (int c3 = 0; c3 < 3; ++c3) qi[c3] = R[3 * r3 + c3] * vim3[c3] + s_pose[(3 * r3 + c3) * C + ch] * vre3[c3];
+          Pi[r3] = (qi[0] + (qi[1] + qi[2])) + s_pose[(9 + r3) * C + ch];
+        }
+        const double DFi[3] = {Pi[0] - MVi[0], Pi[1] - MVi[1], Pi[2] - MVi[2]};
+        double ti[3];
+#pragma unroll
+        for (int c3 = 0; c3 < 3; ++c3) ti[c3] = DF[c3] * MNi[c3] + DFi[c3] * MN[c3];
+        const double ri = ti[0] + (ti[1] + ti[2]);
+        const double PNi[3] = {(P[1] * MNi[2] + Pi[1] * MN[2]) - (P[2] * MNi[1] + Pi[2] * MN[1]),
+                               (P[2] * MNi[0] + Pi[2] * MN[0]) - (P[0] * MNi[2] + Pi[0] * MN[2]),
+                               (P[0] * MNi[1] + Pi[0] * MN[1]) - (P[1] * MNi[0] + Pi[1] * MN[0])};
+        row[ch] = MNi[0];
+        row[C + ch] = MNi[1];
+        row[2 * C + ch] = MNi[2];
+        row[3 * C + ch] = PNi[0];
+        row[4 * C + ch] = PNi[1];
+        row[5 * C + ch] = PNi[2];
+        row[6 * C + ch] = ri;
       }
     }
     __syncthreads();
