@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) k_icp_solve(TrackState* st, const double*
 }
 
 template <int G>
-__global__ void __launch_bounds__(256, 2) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
+__global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
                                                     int w, int h, int stride, const double* __restrict__ intr,
                                                     const double* pose, const double* __restrict__ vre,
                                                     const double* __restrict__ nre, const double* __restrict__ vim,
@@ -499,9 +499,9 @@ int icp_tiles(int w, int h, int stride) {
 
 // Slots per shared-memory chunk of the (J, r) rows.
 static int reduce_chunk(int C) {
-  if (8 * C * (16 + 128 * 7) <= 100 * 1024) return 128;
-  if (8 * C * (16 + 64 * 7) <= 100 * 1024) return 64;
-  return 32;
+  if (8 * C * (16 + 256 * 7) <= 200 * 1024) return 256;
+  if (8 * C * (16 + 128 * 7) <= 200 * 1024) return 128;
+  return 64;
 }
 
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp) {
