@@ -153,15 +153,48 @@ CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out, typename 
 #pragma unroll
   for (int c = 0; c < 8; ++c) ok = ok && rw[c].y > 0.0;
   if (!ok) return false;
-  S accum = lit<S>(0.0);
+  if constexpr (Traits<S>::G == 0) {
+    S accum = 0.0;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const S wx = (c & 1) ? fx : 1.0 - fx;
-    const S wy = ((c >> 1) & 1) ? fy : 1.0 - fy;
-    const S wz = (c >> 2) ? fz : 1.0 - fz;
-    accum = accum + ((wx * wy) * wz) * field_at<S>(vol.vox, v[c], rw[c].x, g0);
+    for (int c = 0; c < 8; ++c) {
+      const double wx = (c & 1) ? fx : 1.0 - fx;
+      const double wy = ((c >> 1) & 1) ? fy : 1.0 - fy;
+      const double wz = (c >> 2) ? fz : 1.0 - fz;
+      accum = accum + ((wx * wy) * wz) * rw[c].x;
+    }
+    *out = accum;
+  } else {
+    // Real channel: the reference's accumulation (bit-identical).  Channels:
+    // the interpolant is linear in the corner values and trilinear in the
+    // cell fractions, so  im = sum_c w_c * F_c.im + (ds/dfx, ds/dfy, ds/dfz) . (fx, fy, fz).im
+    // — the same first-order quantity with 11 instead of ~64 operations per
+    // channel (rounding differs from the per-operation rule by ~1 ulp).
+    const double fxr = fx.re, fyr = fy.re, fzr = fz.re;
+    double acc = 0.0, dsx = 0.0, dsy = 0.0, dsz = 0.0;
+    double wgt[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double wx = (c & 1) ? fxr : 1.0 - fxr;
+      const double wy = ((c >> 1) & 1) ? fyr : 1.0 - fyr;
+      const double wz = (c >> 2) ? fzr : 1.0 - fzr;
+      wgt[c] = (wx * wy) * wz;
+      acc = acc + wgt[c] * rw[c].x;
+      const double F = rw[c].x;
+      dsx += ((c & 1) ? 1.0 : -1.0) * (wy * wz) * F;
+      dsy += (((c >> 1) & 1) ? 1.0 : -1.0) * (wx * wz) * F;
+      dsz += ((c >> 2) ? 1.0 : -1.0) * (wx * wy) * F;
+    }
+    S accum;
+    accum.re = acc;
+#pragma unroll
+    for (int g = 0; g < Traits<S>::G; ++g) {
+      double t = dsx * fx.im[g] + dsy * fy.im[g] + dsz * fz.im[g];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) t += wgt[c] * vol.vox.fim[v[c] * vol.vox.Dp + g0 + g];
+      accum.im[g] = t;
+    }
+    *out = accum;
   }
-  *out = accum;
   return true;
 }
 template <typename S, typename V>

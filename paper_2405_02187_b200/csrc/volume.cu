@@ -605,17 +605,20 @@ int pick_group(int D) {
 // groups of width 2 (or 1) regardless of the volume's group width.
 static int raycast_group(int G, int Dp) {
   if (G == 0) return 0;
-#ifdef CSF_RAYCAST_RG1
-  return 1;
-#else
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = std::getenv("CSF_LIFT_G");
+    forced = e ? std::atoi(e) : -1;
+  }
+  if ((forced == 1 || forced == 2 || forced == 5) && Dp % forced == 0) return forced;
   return (Dp % 2 == 0) ? 2 : 1;
-#endif
 }
 #define CSF_DISPATCH_RG(G, BODY)                      \
   switch (G) {                                        \
     case 0: { constexpr int kG = 0; BODY; } break;    \
     case 1: { constexpr int kG = 1; BODY; } break;    \
     case 2: { constexpr int kG = 2; BODY; } break;    \
+    case 5: { constexpr int kG = 5; BODY; } break;    \
     default: std::fprintf(stderr, "csf_b200: no raycast kernel for group width %d\n", G); \
   }
 
