@@ -493,6 +493,191 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
   }
 }
 
+// Real trilinear sample that also returns what the channel pass needs: the
+// corner voxel ids, the corner weights and the derivative of the sample with
+// respect to the cell fractions (real parts of sample_tsdf<S>, bit-identical).
+template <typename V>
+CSF_DEV bool sample_real_ex(const V& vol, double px, double py, double pz, double* out, int* vid, double* wgt,
+                            double* ds) {
+  const double gx = (px - vol.ox) / vol.vs;
+  const double gy = (py - vol.oy) / vol.vs;
+  const double gz = (pz - vol.oz) / vol.vs;
+  const int i0 = ifloor(gx), j0 = ifloor(gy), k0 = ifloor(gz);
+  if (!vol.cell_in_grid(i0, j0, k0)) return false;
+  long long v[8];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    v[c] = vol.voxel(i0 + (c & 1), j0 + ((c >> 1) & 1), k0 + (c >> 2));
+    ok = ok && v[c] >= 0;
+  }
+  if (!ok) return false;
+  double2 rw[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) rw[c] = vol.vox.rw[v[c]];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) ok = ok && rw[c].y > 0.0;
+  if (!ok) return false;
+  const double fx = gx - static_cast<double>(i0);
+  const double fy = gy - static_cast<double>(j0);
+  const double fz = gz - static_cast<double>(k0);
+  double acc = 0.0, dsx = 0.0, dsy = 0.0, dsz = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double wx = (c & 1) ? fx : 1.0 - fx;
+    const double wy = ((c >> 1) & 1) ? fy : 1.0 - fy;
+    const double wz = (c >> 2) ? fz : 1.0 - fz;
+    wgt[c] = (wx * wy) * wz;
+    acc = acc + wgt[c] * rw[c].x;
+    const double F = rw[c].x;
+    dsx += ((c & 1) ? 1.0 : -1.0) * (wy * wz) * F;
+    dsy += (((c >> 1) & 1) ? 1.0 : -1.0) * (wx * wz) * F;
+    dsz += ((c >> 2) ? 1.0 : -1.0) * (wx * wy) * F;
+    vid[c] = static_cast<int>(v[c]);
+  }
+  ds[0] = dsx;
+  ds[1] = dsy;
+  ds[2] = dsz;
+  *out = acc;
+  return true;
+}
+
+// Channel d of a sample at a position with channel `pim` (3 values).
+CSF_DEV double sample_channel(const VoxelStore& vox, const int* vid, const double* wgt, const double* ds,
+                              const double* pim, double vs, double inv_vs2, int d) {
+  double t = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) t += ds[a] * CSF_CH_DIV(pim[a] * vs, vs * vs, inv_vs2);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) t += wgt[c] * vox.fim[static_cast<long long>(vid[c]) * vox.Dp + d];
+  return t;
+}
+
+// Lifted epilogue, one thread per hit pixel: the real chain once (bit-identical
+// to the L<G> evaluation), then every channel in tangent form from the saved
+// real intermediates (per-operation truncated-Complex rules; the trilinear
+// samples use the weight/gradient form of sample_tsdf<S>).
+template <typename V>
+__global__ void __launch_bounds__(128) k_raycast_lift_all(V vol, const double* __restrict__ pose,
+                                                          const double* __restrict__ intr, int w, int h, int Dp,
+                                                          const double2* __restrict__ hits, double* __restrict__ vre,
+                                                          double* __restrict__ nre, double* __restrict__ vim,
+                                                          double* __restrict__ nim) {
+  extern __shared__ double sm[];
+  const int C = 1 + Dp;
+  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
+  __syncthreads();
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= w * h) return;
+  const double2 hit = hits[pix];
+  if (hit.y < 0.0) return;
+  const double a0 = hit.x, a1 = hit.y;
+  const int x = pix % w, y = pix / w;
+  const double* kk = sm + 12 * C;
+  // ---- real chain (as the L<G> code's real parts)
+  double R[9], T[3];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) R[e] = sm[e * C];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) T[e] = sm[(9 + e) * C];
+  const double fxk = kk[0], fyk = kk[C], cxk = kk[2 * C], cyk = kk[3 * C];
+  const double tx = static_cast<double>(x) - cxk, ty = static_cast<double>(y) - cyk;
+  const double dc[3] = {tx / fxk, ty / fyk, 1.0};
+  const double dot_dc = dc[0] * dc[0] + (dc[1] * dc[1] + 1.0 * 1.0);
+  const double rn = sqrt(dot_dc);
+  const double dn[3] = {dc[0] / rn, dc[1] / rn, dc[2] / rn};
+  double dir[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) dir[r] = R[3 * r] * dn[0] + (R[3 * r + 1] * dn[1] + R[3 * r + 2] * dn[2]);
+  int vid[8][8];
+  double wgt[8][8], dsv[8][3], f[8];
+  const double q0[3] = {T[0] + a0 * dir[0], T[1] + a0 * dir[1], T[2] + a0 * dir[2]};
+  const double q1[3] = {T[0] + a1 * dir[0], T[1] + a1 * dir[1], T[2] + a1 * dir[2]};
+  sample_real_ex(vol, q0[0], q0[1], q0[2], &f[0], vid[0], wgt[0], dsv[0]);
+  sample_real_ex(vol, q1[0], q1[1], q1[2], &f[1], vid[1], wgt[1], dsv[1]);
+  const double span = a1 - a0;
+  const double num = span * f[0], den = f[1] - f[0];
+  const double qq = num / den;
+  const double astar = a0 - qq;
+  const double vv[3] = {T[0] + astar * dir[0], T[1] + astar * dir[1], T[2] + astar * dir[2]};
+  const double hv = vol.vs;
+  double grad[3];
+#pragma unroll
+  for (int axis = 0; axis < 3; ++axis) {
+    double lo[3] = {vv[0], vv[1], vv[2]}, hi[3] = {vv[0], vv[1], vv[2]};
+    lo[axis] = lo[axis] - hv;
+    hi[axis] = hi[axis] + hv;
+    if (!sample_real_ex(vol, lo[0], lo[1], lo[2], &f[2 + 2 * axis], vid[2 + 2 * axis], wgt[2 + 2 * axis],
+                        dsv[2 + 2 * axis]))
+      return;
+    if (!sample_real_ex(vol, hi[0], hi[1], hi[2], &f[3 + 2 * axis], vid[3 + 2 * axis], wgt[3 + 2 * axis],
+                        dsv[3 + 2 * axis]))
+      return;
+    grad[axis] = (f[3 + 2 * axis] - f[2 + 2 * axis]) / (2.0 * hv);
+  }
+  const double len2 = grad[0] * grad[0] + (grad[1] * grad[1] + grad[2] * grad[2]);
+  if (!(len2 > 0.0)) return;
+  const double ln = sqrt(len2);
+  const double nn[3] = {grad[0] / ln, grad[1] / ln, grad[2] / ln};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    vre[3LL * pix + c] = vv[c];
+    nre[3LL * pix + c] = nn[c];
+  }
+  // ---- channels
+  const double inv_fx2 = 1.0 / (fxk * fxk), inv_fy2 = 1.0 / (fyk * fyk), inv_rn2 = 1.0 / (rn * rn);
+  const double inv_vs2 = 1.0 / (hv * hv), inv_den2 = 1.0 / (den * den), inv_2h2 = 1.0 / ((2.0 * hv) * (2.0 * hv));
+  const double inv_ln2 = 1.0 / (ln * ln), half_rn = 0.5 / rn, half_ln = 0.5 / ln;
+  (void)inv_fx2; (void)inv_fy2; (void)inv_rn2; (void)inv_vs2; (void)inv_den2; (void)inv_2h2; (void)inv_ln2;
+  for (int d = 0; d < Dp; ++d) {
+    const int ch = 1 + d;
+    // dir_cam = ((x - cx)/fx, (y - cy)/fy, 1)
+    const double dci[3] = {CSF_CH_DIV(-kk[2 * C + ch] * fxk - tx * kk[ch], fxk * fxk, inv_fx2),
+                           CSF_CH_DIV(-kk[3 * C + ch] * fyk - ty * kk[C + ch], fyk * fyk, inv_fy2), 0.0};
+    const double doti = (dc[0] * dci[0] + dci[0] * dc[0]) + ((dc[1] * dci[1] + dci[1] * dc[1]) + 0.0);
+    const double rni = half_rn * doti;
+    double dni[3], diri[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dni[a] = CSF_CH_DIV(dci[a] * rn - dc[a] * rni, rn * rn, inv_rn2);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const double t0 = R[3 * r] * dni[0] + sm[(3 * r) * C + ch] * dn[0];
+      const double t1 = R[3 * r + 1] * dni[1] + sm[(3 * r + 1) * C + ch] * dn[1];
+      const double t2 = R[3 * r + 2] * dni[2] + sm[(3 * r + 2) * C + ch] * dn[2];
+      diri[r] = t0 + (t1 + t2);
+    }
+    const double Ti[3] = {sm[9 * C + ch], sm[10 * C + ch], sm[11 * C + ch]};
+    const double q0i[3] = {Ti[0] + a0 * diri[0], Ti[1] + a0 * diri[1], Ti[2] + a0 * diri[2]};
+    const double q1i[3] = {Ti[0] + a1 * diri[0], Ti[1] + a1 * diri[1], Ti[2] + a1 * diri[2]};
+    const double f0i = sample_channel(vol.vox, vid[0], wgt[0], dsv[0], q0i, hv, inv_vs2, d);
+    const double f1i = sample_channel(vol.vox, vid[1], wgt[1], dsv[1], q1i, hv, inv_vs2, d);
+    const double numi = span * f0i, deni = f1i - f0i;
+    const double qqi = CSF_CH_DIV(numi * den - num * deni, den * den, inv_den2);
+    const double asti = -qqi;
+    double vvi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) vvi[a] = Ti[a] + (astar * diri[a] + asti * dir[a]);
+    double gi[3];
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+      const double lo = sample_channel(vol.vox, vid[2 + 2 * axis], wgt[2 + 2 * axis], dsv[2 + 2 * axis], vvi, hv,
+                                       inv_vs2, d);
+      const double hi = sample_channel(vol.vox, vid[3 + 2 * axis], wgt[3 + 2 * axis], dsv[3 + 2 * axis], vvi, hv,
+                                       inv_vs2, d);
+      gi[axis] = CSF_CH_DIV((hi - lo) * (2.0 * hv), (2.0 * hv) * (2.0 * hv), inv_2h2);
+    }
+    const double l2i = (grad[0] * gi[0] + gi[0] * grad[0]) + ((grad[1] * gi[1] + gi[1] * grad[1]) +
+                                                             (grad[2] * gi[2] + gi[2] * grad[2]));
+    const double lni = half_ln * l2i;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      vim[(3LL * pix + c) * Dp + d] = vvi[c];
+      nim[(3LL * pix + c) * Dp + d] = CSF_CH_DIV(gi[c] * ln - grad[c] * lni, ln * ln, inv_ln2);
+    }
+  }
+}
+
 template <int G, typename V>
 __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __restrict__ pose,
                                                       const double* __restrict__ intr, int w, int h, int Dp,
@@ -747,11 +932,18 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
     *L.launches += 1;
   }
   if (L.phase == 1) return;
+  const size_t smem = sizeof(double) * 16 * (1 + Dp);
+  static const bool grouped = std::getenv("CSF_LIFT_G") != nullptr;
+  if (G > 0 && !grouped) {
+    k_raycast_lift_all<V><<<(P + 127) / 128, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre, nre, vim,
+                                                                    nim);
+    *L.launches += 1;
+    return;
+  }
   const int RG = raycast_group(G, Dp);
   const int passes = RG == 0 ? 1 : Dp / RG;
   const long long items = static_cast<long long>(P) * passes;
   const int grid = static_cast<int>((items + 127) / 128);
-  const size_t smem = sizeof(double) * 16 * (1 + Dp);
   CSF_DISPATCH_RG(RG, (k_raycast_lift<kG, V><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre,
                                                                             nre, vim, nim)));
   *L.launches += 1;
