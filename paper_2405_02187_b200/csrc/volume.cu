@@ -796,6 +796,7 @@ static int raycast_group(int G, int Dp) {
     forced = e ? std::atoi(e) : -1;
   }
   if ((forced == 1 || forced == 2 || forced == 5) && Dp % forced == 0) return forced;
+  if (Dp % 5 == 0) return 5;
   return (Dp % 2 == 0) ? 2 : 1;
 }
 #define CSF_DISPATCH_RG(G, BODY)                      \
@@ -933,8 +934,11 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
   }
   if (L.phase == 1) return;
   const size_t smem = sizeof(double) * 16 * (1 + Dp);
-  static const bool grouped = std::getenv("CSF_LIFT_G") != nullptr;
-  if (G > 0 && !grouped) {
+  // one thread per hit pixel with tangent-form channels (CSF_LIFT_ALL=1) or
+  // one thread per (hit pixel, channel group) — the default: more memory
+  // parallelism wins over the recomputed real chain on B200.
+  static const bool per_pixel = std::getenv("CSF_LIFT_ALL") != nullptr;
+  if (G > 0 && per_pixel) {
     k_raycast_lift_all<V><<<(P + 127) / 128, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre, nre, vim,
                                                                     nim);
     *L.launches += 1;
