@@ -27,6 +27,9 @@ namespace csfd {
 
 using csfi::TrackState;
 constexpr int kTile = 256;
+// 256 threads evaluate the tile's slots; all 320 sum accumulators (27*(1+Dp)
+// of them, one per thread up to Dp = 10), so no thread carries two.
+constexpr int kRedThreads = 320;
 __constant__ int c_tri_r[21] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5, 5, 5, 5};
 __constant__ int c_tri_c[21] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2, 3, 4, 5};
 
@@ -51,7 +54,7 @@ CSF_DEV bool vertex_at(const double* depth, int w, int x, int y, double fx, doub
 // lifted 6x6 system, applies exp(delta) * T and writes the break decisions.
 // `sm` holds >= 27*(1+Dp) + 48*(1+G)*ngroups doubles.
 template <int G>
-__device__ void icp_solve_block(TrackState* st, const double* partials, const int* counts, int n_tiles,
+__device__ __noinline__ void icp_solve_block(TrackState* st, const double* partials, const int* counts, int n_tiles,
                                 double* pose, int Dp, int level, double tol, double* sm) {
   using S = Scal<G>;
   __shared__ int s_n, s_finite;
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(256) k_icp_solve(TrackState* st, const double*
 }
 
 template <int G>
-__global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
+__global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
                                                     int w, int h, int stride, const double* __restrict__ intr,
                                                     const double* pose, const double* __restrict__ vre,
                                                     const double* __restrict__ nre, const double* __restrict__ vim,
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const 
   double* s_pose = sm;
   double* s_intr = s_pose + 12 * C;
   double* s_jr = s_intr + 4 * C;
-  __shared__ int s_wsum[8];
+  __shared__ int s_wsum[kRedThreads / 32];
   __shared__ int s_total;
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) s_pose[i] = pose[i];
   for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_intr[i] = intr[i];
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const 
     if (lane == 0) s_wsum[warp] = __popc(ballot);
     __syncthreads();
     int before = 0, total = 0;
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kRedThreads / 32; ++k) {
       if (k < warp) before += s_wsum[k];
       total += s_wsum[k];
     }
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const 
     // per-accumulator sequential sums in slot order
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int a = threadIdx.x + 256 * j;
+      const int a = threadIdx.x + kRedThreads * j;
       if (a >= n_acc) break;
       const int q = a / C, c = a % C;
       int ja, jb;
@@ -325,12 +328,17 @@ __global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const 
         ja = q - 21;
         jb = 6;
       }
+      const int stride = 7 * C;
+      const double* pa = s_jr + ja * C;
+      const double* pb = s_jr + jb * C;
       double s = acc[j];
-      for (int e = 0; e < total; ++e) {
-        const double* row = s_jr + static_cast<long long>(e) * 7 * C;
-        const double are = row[ja * C], bre = row[jb * C];
-        const double term = c == 0 ? are * bre : are * row[jb * C + c] + row[ja * C + c] * bre;
-        s = s + term;
+      if (c == 0) {
+        for (int e = 0; e < total; ++e) s = s + pa[e * stride] * pb[e * stride];
+      } else {
+        for (int e = 0; e < total; ++e) {
+          const int o = e * stride;
+          s = s + (pa[o] * pb[o + c] + pa[o + c] * pb[o]);
+        }
       }
       acc[j] = s;
     }
@@ -339,7 +347,7 @@ __global__ void __launch_bounds__(256) k_icp_reduce(const TrackState* st, const 
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int a = threadIdx.x + 256 * j;
+    const int a = threadIdx.x + kRedThreads * j;
     if (a < n_acc) partials[static_cast<long long>(blockIdx.x) * n_acc + a] = acc[j];
   }
   if (threadIdx.x == 0) counts[blockIdx.x] = tile_count;
@@ -526,19 +534,19 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
     case 0:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_icp_reduce<0><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
+      k_icp_reduce<0><<<tiles, kRedThreads, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
                                                       cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
       break;
     case 1:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_icp_reduce<1><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
+      k_icp_reduce<1><<<tiles, kRedThreads, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
                                                       cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
       break;
     default:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_icp_reduce<2><<<tiles, 256, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
+      k_icp_reduce<2><<<tiles, kRedThreads, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
                                                       cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
   }
   ++*L.launches;
