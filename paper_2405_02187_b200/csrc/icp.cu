@@ -332,9 +332,13 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
       const double* pa = s_jr + ja * C;
       const double* pb = s_jr + jb * C;
       double s = acc[j];
+      // the add chain is sequential (canonical order); the shared-memory
+      // loads of the next entries are independent and are issued ahead
       if (c == 0) {
+#pragma unroll 8
         for (int e = 0; e < total; ++e) s = s + pa[e * stride] * pb[e * stride];
       } else {
+#pragma unroll 8
         for (int e = 0; e < total; ++e) {
           const int o = e * stride;
           s = s + (pa[o] * pb[o + c] + pa[o + c] * pb[o]);
