@@ -76,11 +76,18 @@ __device__ __noinline__ void icp_solve_block(TrackState* st, const double* parti
     }
     sm[a] = total;
   }
+  // correspondence count: integer sum, any order is exact
   if (threadIdx.x == 0) {
-    int n = 0;
-    for (int t = 0; t < n_tiles; ++t) n += __ldcg(counts + t);
-    s_n = n;
+    s_n = 0;
     s_finite = 1;
+  }
+  __syncthreads();
+  {
+    int part = 0;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) part += __ldcg(counts + t);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_down_sync(0xffffffffu, part, off);
+    if ((threadIdx.x & 31) == 0 && part) atomicAdd(&s_n, part);
   }
   __syncthreads();
   const int n = s_n;
