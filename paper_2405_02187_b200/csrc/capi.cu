@@ -18,6 +18,7 @@
 #include "csf_internal.h"
 
 namespace csfi {
+void icp_clock_enable(unsigned long long* buf);
 int synth_workload(cudaStream_t stream, int config, int n_frames, int width, int height, float* depth_out,
                    double* gt_out, csf_intrinsics* k_out, std::string* err);
 int band_samples(double mu, double vs);
@@ -1021,6 +1022,21 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
     result->correspondences = hs.n_corr;
     result->final_loss = std::nan("");  // loss_after is not evaluated by the device tracker
   }
+  return CSF_OK;
+}
+
+// Debug hook (not part of the public header): per-CTA ICP phase timestamps.
+extern "C" int csf_debug_icp_clock(unsigned long long* host_out, int enable) {
+  static unsigned long long* dbuf = nullptr;
+  const size_t n = size_t(4096) * 512 * 5;
+  if (enable) {
+    if (!dbuf && cudaMalloc(&dbuf, n * sizeof(unsigned long long)) != cudaSuccess) return CSF_ENOMEM;
+    cudaMemset(dbuf, 0, n * sizeof(unsigned long long));
+    icp_clock_enable(dbuf);
+    return CSF_OK;
+  }
+  icp_clock_enable(nullptr);
+  if (dbuf && host_out) cudaMemcpy(host_out, dbuf, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return CSF_OK;
 }
 

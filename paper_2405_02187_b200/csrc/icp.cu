@@ -27,6 +27,20 @@ namespace csfd {
 
 using csfi::TrackState;
 constexpr int kTile = 256;
+
+// Optional phase timing (tools/icp_timing.py): per launch, per CTA
+// [start, after association/J, after sums, solve start, solve end] in ns.
+__device__ unsigned long long* g_icp_clock = nullptr;
+__device__ unsigned g_icp_clock_launch = 0;
+CSF_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+CSF_DEV void clock_mark(int slot) {
+  if (g_icp_clock && threadIdx.x == 0 && g_icp_clock_launch < 4096)
+    g_icp_clock[(static_cast<unsigned long long>(g_icp_clock_launch) * 512 + blockIdx.x) * 5 + slot] = gtimer();
+}
 // 256 threads evaluate the tile's slots; all 320 sum accumulators (27*(1+Dp)
 // of them, one per thread up to Dp = 10), so no thread carries two.
 constexpr int kRedThreads = 320;
@@ -167,6 +181,7 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
                                                     int* __restrict__ counts, TrackState* st_rw, double* pose_rw,
                                                     int level, double tol) {
   if (st->level_done) return;
+  clock_mark(0);
   using S = Scal<G>;
   extern __shared__ double sm[];
   const int C = 1 + Dp;
@@ -321,6 +336,7 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
       }
     }
     __syncthreads();
+    if (cbase == 0) clock_mark(1);
     // per-accumulator sequential sums in slot order
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -362,6 +378,7 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
     if (a < n_acc) partials[static_cast<long long>(blockIdx.x) * n_acc + a] = acc[j];
   }
   if (threadIdx.x == 0) counts[blockIdx.x] = tile_count;
+  clock_mark(2);
   // The last CTA to finish runs the solve (no second launch per iteration).
   __shared__ bool s_last;
   __threadfence();
@@ -374,10 +391,13 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
   if (!s_last) return;
   if (threadIdx.x == 0) st_rw->pad[0] = 0;
   __threadfence();
+  clock_mark(3);
   if (Dp == 0)
     icp_solve_block<0>(st_rw, partials, counts, gridDim.x, pose_rw, Dp, level, tol, sm);
   else
     icp_solve_block<1>(st_rw, partials, counts, gridDim.x, pose_rw, Dp, level, tol, sm);
+  clock_mark(4);
+  if (threadIdx.x == 0 && g_icp_clock) atomicAdd(&g_icp_clock_launch, 1u);
 }
 
 // Level entry: the prediction pose is the current estimate (icp.cpp:191).
@@ -510,6 +530,14 @@ static void chk(const char* what) {
     case 6: { constexpr int kG = 6; BODY; } break;    \
     default: std::fprintf(stderr, "csf_b200: no kernel for group width %d\n", G); \
   }
+
+// Debug: enable per-CTA phase timestamps into a device buffer of
+// 4096 launches x 512 CTAs x 5 slots (nullptr disables).
+void icp_clock_enable(unsigned long long* buf) {
+  cudaMemcpyToSymbol(g_icp_clock, &buf, sizeof(buf));
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(g_icp_clock_launch, &z, sizeof(z));
+}
 
 int icp_tiles(int w, int h, int stride) {
   const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
