@@ -44,6 +44,8 @@ CSF_DEV void clock_mark(int slot) {
 // 256 threads evaluate the tile's slots; all 320 sum accumulators (27*(1+Dp)
 // of them, one per thread up to Dp = 10), so no thread carries two.
 constexpr int kRedThreads = 320;
+// Tiles per shared-memory stage of the solve's cross-tile sums.
+constexpr int kSolveChunk = 16;
 __constant__ int c_tri_r[21] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5, 5, 5, 5};
 __constant__ int c_tri_c[21] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2, 3, 4, 5};
 
@@ -75,20 +77,30 @@ __device__ __noinline__ void icp_solve_block(TrackState* st, const double* parti
   const int C = 1 + Dp;
   const int n_acc = 27 * C;
   S* ws = reinterpret_cast<S*>(sm + n_acc) + 48 * threadIdx.x;
-  // tile partials in tile order; loads are issued 8 at a time so the
-  // sequential add chain does not wait on one L2 round trip per tile
-  for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
+  // Tile partials in tile order.  Chunks of tiles are staged through shared
+  // memory by the whole CTA (coalesced, all loads in flight at once), then
+  // each accumulator adds its chunk sequentially — one L2 round trip per
+  // chunk instead of one per tile.
+  {
+    double* stage = sm + n_acc + 48 * (1 + G) * ((G == 0 ? 1 : Dp / G));
+    const int chunk_t = kSolveChunk;
     double total = 0.0;
-    for (int t = 0; t < n_tiles; t += 8) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        v[u] = t + u < n_tiles ? __ldcg(partials + static_cast<long long>(t + u) * n_acc + a) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (t + u < n_tiles) total = total + v[u];
+    const int a = threadIdx.x;
+    for (int t0 = 0; t0 < n_tiles; t0 += chunk_t) {
+      const int nt = min(chunk_t, n_tiles - t0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < nt * n_acc; i += blockDim.x)
+        stage[i] = __ldcg(partials + static_cast<long long>(t0) * n_acc + i);
+      __syncthreads();
+      if (a < n_acc)
+        for (int t = 0; t < nt; ++t) total = total + stage[t * n_acc + a];
     }
-    sm[a] = total;
+    if (a < n_acc) sm[a] = total;
+    for (int extra = a + blockDim.x; extra < n_acc; extra += blockDim.x) {
+      double tot = 0.0;
+      for (int t = 0; t < n_tiles; ++t) tot = tot + __ldcg(partials + static_cast<long long>(t) * n_acc + extra);
+      sm[extra] = tot;
+    }
   }
   // correspondence count: integer sum, any order is exact
   if (threadIdx.x == 0) {
@@ -563,7 +575,7 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
                        int* counts, int level, double tol) {
   const int C = 1 + Dp;
   const int chunk = reduce_chunk(C);
-  const size_t solve_smem = 27 * C + 48 * 2 * static_cast<size_t>(Dp > 0 ? Dp : 1);
+  const size_t solve_smem = 27 * C + 48 * 2 * static_cast<size_t>(Dp > 0 ? Dp : 1) + 27 * C * kSolveChunk;
   const size_t smem = sizeof(double) * std::max<size_t>(16 * C + static_cast<size_t>(chunk) * 7 * C, solve_smem);
   const int tiles = icp_tiles(w, h, stride);
   // J/r rows are evaluated in channel groups of 2 (or 1): register-light,
