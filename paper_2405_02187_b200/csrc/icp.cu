@@ -77,30 +77,20 @@ __device__ __noinline__ void icp_solve_block(TrackState* st, const double* parti
   const int C = 1 + Dp;
   const int n_acc = 27 * C;
   S* ws = reinterpret_cast<S*>(sm + n_acc) + 48 * threadIdx.x;
-  // Tile partials in tile order.  Chunks of tiles are staged through shared
-  // memory by the whole CTA (coalesced, all loads in flight at once), then
-  // each accumulator adds its chunk sequentially — one L2 round trip per
-  // chunk instead of one per tile.
-  {
-    double* stage = sm + n_acc + 48 * (1 + G) * ((G == 0 ? 1 : Dp / G));
-    const int chunk_t = kSolveChunk;
+  // Tile partials in tile order: each accumulator thread keeps 32 loads in
+  // flight, then adds them in sequence (one L2 round trip per 32 tiles).
+  for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
     double total = 0.0;
-    const int a = threadIdx.x;
-    for (int t0 = 0; t0 < n_tiles; t0 += chunk_t) {
-      const int nt = min(chunk_t, n_tiles - t0);
-      __syncthreads();
-      for (int i = threadIdx.x; i < nt * n_acc; i += blockDim.x)
-        stage[i] = __ldcg(partials + static_cast<long long>(t0) * n_acc + i);
-      __syncthreads();
-      if (a < n_acc)
-        for (int t = 0; t < nt; ++t) total = total + stage[t * n_acc + a];
+    for (int t = 0; t < n_tiles; t += 32) {
+      double v[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        v[u] = t + u < n_tiles ? __ldcg(partials + static_cast<long long>(t + u) * n_acc + a) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (t + u < n_tiles) total = total + v[u];
     }
-    if (a < n_acc) sm[a] = total;
-    for (int extra = a + blockDim.x; extra < n_acc; extra += blockDim.x) {
-      double tot = 0.0;
-      for (int t = 0; t < n_tiles; ++t) tot = tot + __ldcg(partials + static_cast<long long>(t) * n_acc + extra);
-      sm[extra] = tot;
-    }
+    sm[a] = total;
   }
   // correspondence count: integer sum, any order is exact
   if (threadIdx.x == 0) {
@@ -575,7 +565,7 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
                        int* counts, int level, double tol) {
   const int C = 1 + Dp;
   const int chunk = reduce_chunk(C);
-  const size_t solve_smem = 27 * C + 48 * 2 * static_cast<size_t>(Dp > 0 ? Dp : 1) + 27 * C * kSolveChunk;
+  const size_t solve_smem = 27 * C + 48 * 2 * static_cast<size_t>(Dp > 0 ? Dp : 1);
   const size_t smem = sizeof(double) * std::max<size_t>(16 * C + static_cast<size_t>(chunk) * 7 * C, solve_smem);
   const int tiles = icp_tiles(w, h, stride);
   // J/r rows are evaluated in channel groups of 2 (or 1): register-light,
