@@ -1028,7 +1028,7 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
 // Debug hook (not part of the public header): per-CTA ICP phase timestamps.
 extern "C" int csf_debug_icp_clock(unsigned long long* host_out, int enable) {
   static unsigned long long* dbuf = nullptr;
-  const size_t n = size_t(4096) * 512 * 5;
+  const size_t n = size_t(4096) * 512 * 8;
   if (enable) {
     if (!dbuf && cudaMalloc(&dbuf, n * sizeof(unsigned long long)) != cudaSuccess) return CSF_ENOMEM;
     cudaMemset(dbuf, 0, n * sizeof(unsigned long long));

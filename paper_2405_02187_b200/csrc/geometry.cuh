@@ -358,4 +358,117 @@ CSF_DEV bool ldlt6_solve(const S* a_lower, const S* rhs, S* dst, S* ws) {
   return ok;
 }
 
+// Register-resident variant of ldlt6_solve: the same operations in the same
+// order, with every loop fully unrolled and the pivot swaps expressed as
+// predicated swaps over compile-time indices (no dynamic indexing, so the
+// matrix never leaves registers).  Used by the latency-critical ICP solve.
+template <typename S>
+CSF_DEV bool ldlt6_solve_reg(const S* a_lower, const S* rhs, S* dst) {
+  S m[6][6];
+  int transp[6];
+  bool ok = true, stop = false;
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) m[r][c] = r >= c ? a_lower[tri(r, c)] : a_lower[tri(c, r)];
+  S temp[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    if (stop) continue;
+    int piv = k;
+    double best = absre(m[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (absre(m[i][i]) > best) {
+        best = absre(m[i][i]);
+        piv = i;
+      }
+    transp[k] = piv;
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) {
+      if (piv == i) {
+#pragma unroll
+        for (int j = 0; j < k; ++j) swap_s(m[k][j], m[i][j]);
+#pragma unroll
+        for (int r = i + 1; r < 6; ++r) swap_s(m[r][k], m[r][i]);
+        swap_s(m[k][k], m[i][i]);
+#pragma unroll
+        for (int r = k + 1; r < i; ++r) {
+          const S tmp = m[r][k];
+          m[r][k] = m[i][r];
+          m[i][r] = tmp;
+        }
+      }
+    }
+    if (k > 0) {
+#pragma unroll
+      for (int j = 0; j < k; ++j) temp[j] = m[j][j] * m[k][j];
+      S sacc = m[k][0] * temp[0];
+#pragma unroll
+      for (int j = 1; j < k; ++j) sacc = sacc + m[k][j] * temp[j];
+      m[k][k] = m[k][k] - sacc;
+#pragma unroll
+      for (int i = k + 1; i < 6; ++i) {
+        S si = m[i][0] * temp[0];
+#pragma unroll
+        for (int j = 1; j < k; ++j) si = si + m[i][j] * temp[j];
+        m[i][k] = m[i][k] - si;
+      }
+    }
+    const S akk = m[k][k];
+    const bool pivot_valid = absre(akk) > 0.0;
+    if (k == 0 && !pivot_valid) {
+      ok = false;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) transp[j] = j;
+      stop = true;
+      continue;
+    }
+    if (k < 5) {
+      if (pivot_valid) {
+#pragma unroll
+        for (int i = k + 1; i < 6; ++i) m[i][k] = m[i][k] / akk;
+      } else {
+#pragma unroll
+        for (int i = k + 1; i < 6; ++i) ok = ok && re(m[i][k]) == 0.0;
+      }
+    }
+  }
+  S x[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) x[i] = rhs[i];
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (transp[k] == i) swap_s(x[k], x[i]);
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = i + 1; j < 6; ++j) x[j] = x[j] - x[i] * m[j][i];
+  const double tol = 2.2250738585072014e-308;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    if (absre(m[i][i]) > tol)
+      x[i] = x[i] / m[i][i];
+    else
+      x[i] = lit<S>(0.0);
+  }
+#pragma unroll
+  for (int i = 4; i >= 0; --i) {
+    S sacc = m[i + 1][i] * x[i + 1];
+#pragma unroll
+    for (int j = i + 2; j < 6; ++j) sacc = sacc + m[j][i] * x[j];
+    x[i] = x[i] - sacc;
+  }
+#pragma unroll
+  for (int k = 5; k >= 0; --k)
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (transp[k] == i) swap_s(x[k], x[i]);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) dst[i] = x[i];
+  return ok;
+}
+
 }  // namespace csfd

@@ -39,7 +39,7 @@ CSF_DEV unsigned long long gtimer() {
 }
 CSF_DEV void clock_mark(int slot) {
   if (g_icp_clock && threadIdx.x == 0 && g_icp_clock_launch < 4096)
-    g_icp_clock[(static_cast<unsigned long long>(g_icp_clock_launch) * 512 + blockIdx.x) * 5 + slot] = gtimer();
+    g_icp_clock[(static_cast<unsigned long long>(g_icp_clock_launch) * 512 + blockIdx.x) * 8 + slot] = gtimer();
 }
 // 256 threads evaluate the tile's slots; all 320 sum accumulators (27*(1+Dp)
 // of them, one per thread up to Dp = 10), so no thread carries two.
@@ -92,6 +92,7 @@ __device__ __noinline__ void icp_solve_block(TrackState* st, const double* parti
     }
     sm[a] = total;
   }
+  clock_mark(5);
   // correspondence count: integer sum, any order is exact
   if (threadIdx.x == 0) {
     s_n = 0;
@@ -124,7 +125,9 @@ __device__ __noinline__ void icp_solve_block(TrackState* st, const double* parti
     for (int q = 0; q < 21; ++q) a[q] = load_ch<S>(sm + q * C, g0, G);
 #pragma unroll
     for (int i = 0; i < 6; ++i) nb[i] = -load_ch<S>(sm + (21 + i) * C, g0, G);
-    ldlt6_solve<S>(a, nb, d, ws);
+    ldlt6_solve_reg<S>(a, nb, d);
+    (void)ws;
+    clock_mark(6);
     bool fin = true;
 #pragma unroll
     for (int i = 0; i < 6; ++i) fin = fin && finite_s(d[i]);
@@ -142,6 +145,7 @@ __device__ __noinline__ void icp_solve_block(TrackState* st, const double* parti
 #pragma unroll
     for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
     np = compose(exp_map<S>(d), cur);
+    clock_mark(7);
   }
   __syncthreads();
   if (mine) {
