@@ -678,6 +678,127 @@ __global__ void __launch_bounds__(128) k_raycast_lift_all(V vol, const double* _
   }
 }
 
+// Warp-cooperative march for the small pyramid levels, where a few long
+// (grazing) rays set the kernel time: one warp per ray evaluates 32
+// consecutive alpha steps at once.  Each lane forms its alpha by the same
+// repeated additions as the sequential loop (bit-identical), samples it, and
+// the reference's sequential rule (have_prev reset on an invalid sample,
+// crossing on f_prev > 0 > f) is resolved across the window with one shuffle
+// and one ballot.  Empty-space skipping is the per-thread kernel's, applied
+// uniformly at window starts.
+template <typename V>
+__global__ void __launch_bounds__(128) k_raycast_march_warp(V vol, const double* __restrict__ pose,
+                                                            const double* __restrict__ intr, int w, int h, int Dp,
+                                                            double near_clip, double far_clip, double step, Box box,
+                                                            double2* __restrict__ hits, double* __restrict__ vre,
+                                                            double* __restrict__ nre) {
+  __shared__ double s_pose[16];
+  const int C = 1 + Dp;
+  if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
+  else if (threadIdx.x < 16) s_pose[threadIdx.x] = intr[(threadIdx.x - 12) * C];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int pix = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (pix >= w * h) return;
+  const int x = pix % w, y = pix / w;
+  Pose<double> c2w;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) c2w.R.m[e] = s_pose[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) c2w.t.v[e] = s_pose[9 + e];
+  const double fxk = s_pose[12], fyk = s_pose[13], cxk = s_pose[14], cyk = s_pose[15];
+  const V3<double> dc = mk3<double>((static_cast<double>(x) - cxk) / fxk, (static_cast<double>(y) - cyk) / fyk, 1.0);
+  const double rn = sqrt(dot3(dc, dc));
+  const V3<double> dir = matvec(c2w.R, mk3<double>(dc.v[0] / rn, dc.v[1] / rn, dc.v[2] / rn));
+  const V3<double> o = c2w.t;
+  if (lane < 3) {
+    vre[3LL * pix + lane] = 0.0;
+    nre[3LL * pix + lane] = 0.0;
+  }
+  if (lane == 0) hits[pix] = make_double2(0.0, -1.0);
+  double t0 = near_clip, t1 = far_clip;
+  if (box.use) {
+    bool hit_box = true;
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+      const double od = o.v[axis], dd = dir.v[axis];
+      if (fabs(dd) < 1e-12) {
+        if (od < box.lo[axis] || od > box.hi[axis]) hit_box = false;
+        continue;
+      }
+      double ta = (box.lo[axis] - od) / dd;
+      double tb = (box.hi[axis] - od) / dd;
+      if (ta > tb) {
+        const double t = ta;
+        ta = tb;
+        tb = t;
+      }
+      t0 = t0 < ta ? ta : t0;
+      t1 = tb < t1 ? tb : t1;
+    }
+    if (!hit_box) return;
+  }
+  if (t0 >= t1) return;
+  typename V::Cache cache;
+  cache.reset();
+  V3<double> invd;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) invd.v[a] = dir.v[a] != 0.0 ? 1.0 / dir.v[a] : 0.0;
+  bool have_prev = false;
+  double alpha_prev = 0.0, f_prev = 0.0;
+  double alpha = t0;  // alpha of the window's first step
+  while (alpha <= t1) {
+    if constexpr (V::kHashed) {
+      const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1], pz = o.v[2] + alpha * dir.v[2];
+      const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
+                k0 = ifloor((pz - vol.oz) / vol.vs);
+      const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
+      const int occ = vol.super_occupied(bx, by, bz);
+      int span = 0;
+      if (occ == 0) span = 8;
+      else if (vol.block(bx, by, bz) < 0) span = 1;
+      if (span > 0) {
+        have_prev = false;
+        const int m = span == 8 ? ~7 : ~0;
+        const double lim = box_exit(vol, bx & m, by & m, bz & m, span, o, invd) - 1e-6;
+        alpha += step;
+        while (alpha < lim && alpha <= t1) alpha += step;
+        continue;
+      }
+    }
+    // this lane's alpha: the window start plus `lane` sequential additions
+    double a = alpha;
+    for (int i = 0; i < lane; ++i) a += step;
+    const bool in_range = a <= t1;
+    double f = 0.0;
+    bool ok = false;
+    if (in_range)
+      ok = sample_real(vol, o.v[0] + a * dir.v[0], o.v[1] + a * dir.v[1], o.v[2] + a * dir.v[2], cache, &f);
+    // predecessor of this lane in the sequential order
+    const double pf = __shfl_up_sync(0xffffffffu, f, 1);
+    const bool pok = __shfl_up_sync(0xffffffffu, ok, 1);
+    const double pa = __shfl_up_sync(0xffffffffu, a, 1);
+    const bool prev_ok = lane == 0 ? have_prev : pok;
+    const double prev_f = lane == 0 ? f_prev : pf;
+    const double prev_a = lane == 0 ? alpha_prev : pa;
+    const bool cross = in_range && ok && prev_ok && prev_f > 0.0 && f < 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, cross);
+    if (bal) {
+      const int c = __ffs(bal) - 1;
+      if (lane == c) hits[pix] = make_double2(prev_a, a);
+      return;
+    }
+    // carry the state of the window's last in-range step
+    const unsigned inr = __ballot_sync(0xffffffffu, in_range);
+    const int last = 31 - __clz(inr);
+    have_prev = __shfl_sync(0xffffffffu, ok, last);
+    f_prev = __shfl_sync(0xffffffffu, f, last);
+    alpha_prev = __shfl_sync(0xffffffffu, a, last);
+    const double a31 = __shfl_sync(0xffffffffu, a, 31);
+    alpha = a31 + step;
+  }
+}
+
 template <int G, typename V>
 __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __restrict__ pose,
                                                       const double* __restrict__ intr, int w, int h, int Dp,
@@ -924,8 +1045,15 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
                          double2* hits, double* vre, double* nre, double* vim, double* nim) {
   const int P = w * h;
   if (L.phase != 2) {
-    k_raycast_march<V><<<(P + 127) / 128, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip, step,
-                                                              box, hits, vre, nre);
+    static const long long warp_threshold = std::getenv("CSF_MARCH_WARP_MAX")
+                                                ? std::atoll(std::getenv("CSF_MARCH_WARP_MAX"))
+                                                : 100000;
+    if (P <= warp_threshold)
+      k_raycast_march_warp<V><<<(P + 3) / 4, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip,
+                                                                 step, box, hits, vre, nre);
+    else
+      k_raycast_march<V><<<(P + 127) / 128, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip,
+                                                                step, box, hits, vre, nre);
     if (Dp > 0 && vim) {
       cudaMemsetAsync(vim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
       cudaMemsetAsync(nim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
