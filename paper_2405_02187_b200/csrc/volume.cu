@@ -102,12 +102,128 @@ __device__ bool fuse_voxel(const VoxelStore& vox, long long v, double px, double
   return true;
 }
 
+#ifdef CSF_EXACT_CHANNELS
+constexpr bool kAdjointFusion = false;
+#else
+constexpr bool kAdjointFusion = true;
+#endif
+
 // Warp-aggregated count of fused voxels (bench's algorithmic-byte model).
 CSF_DEV void count_updates(int* upd, bool fused) {
   if (!upd) return;
   const unsigned m = __activemask();
   const unsigned b = __ballot_sync(m, fused);
   if ((threadIdx.x & 31) == __ffs(m) - 1 && b) atomicAdd(upd, __popc(b));
+}
+
+// Fusion with adjoint-form channels.  The real channel is the reference's
+// chain (bit-identical to measured_tsdf<double> and the running average).
+// Every perturbation channel of psi is a linear function of the channels of
+// the frame's 19 lifted inputs (world->camera R, t; camera centre; fx, fy,
+// cx, cy), so one reverse sweep through the real chain gives the 19 partials
+// and each channel costs one 19-term contraction instead of a full lifted
+// re-evaluation (rounding differs from the per-operation rule by a few ulp).
+// Shared-memory layout as stage_pose_w2c: w2c[12][C], centre[3][C], intr[4][C].
+CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, double py, double pz,
+                                const double* __restrict__ depth, int w, int h, double mu, double cap, int Dp,
+                                const double* sm) {
+  const int C = 1 + Dp;
+  double R[9], t[3], c[3];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) R[e] = sm[e * C];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    t[e] = sm[(9 + e) * C];
+    c[e] = sm[(12 + e) * C];
+  }
+  const double kfx = sm[15 * C], kfy = sm[16 * C], kcx = sm[17 * C], kcy = sm[18 * C];
+  double pc[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) pc[r] = (R[3 * r] * px + (R[3 * r + 1] * py + R[3 * r + 2] * pz)) + t[r];
+  if (!(pc[2] > 0.0)) return false;
+  const double lx = (kfx * pc[0]) / pc[2] + kcx;
+  const double ly = (kfy * pc[1]) / pc[2] + kcy;
+  const int x0 = ifloor(lx), y0 = ifloor(ly);
+  if (x0 < 0 || y0 < 0 || x0 + 1 >= w || y0 + 1 >= h) return false;
+  const double d00 = depth[y0 * w + x0];
+  const double d10 = depth[y0 * w + x0 + 1];
+  const double d01 = depth[(y0 + 1) * w + x0];
+  const double d11 = depth[(y0 + 1) * w + x0 + 1];
+  if (!(d00 > 0.0) || !(d10 > 0.0) || !(d01 > 0.0) || !(d11 > 0.0)) return false;
+  const double nearv = fmin(fmin(d00, d10), fmin(d01, d11));
+  const double farv = fmax(fmax(d00, d10), fmax(d01, d11));
+  if (farv - nearv > 0.1) return false;
+  const double fxf = lx - static_cast<double>(x0);
+  const double fyf = ly - static_cast<double>(y0);
+  const double top = d00 + fxf * (d10 - d00);
+  const double bot = d01 + fxf * (d11 - d01);
+  const double sampled = top + fyf * (bot - top);
+  const double rx = (lx - kcx) / kfx;
+  const double ry = (ly - kcy) / kfy;
+  const double lam = sqrt(rx * rx + (ry * ry + 1.0 * 1.0));
+  const double dx = c[0] - px, dy = c[1] - py, dz = c[2] - pz;
+  const double dist = sqrt(dx * dx + (dy * dy + dz * dz));
+  const double eta = sampled - dist / lam;
+  if (eta < -mu) return false;
+  const double q = eta / mu;
+  double psi = 1.0 < q ? 1.0 : q;
+  psi = -1.0 > psi ? -1.0 : psi;
+  const bool sat = 1.0 < q || -1.0 > q;
+  const double2 rw = vox.rw[v];
+  const double wt = rw.y;
+  const double fre = (wt * rw.x + psi) / (wt + 1.0);
+  if (Dp > 0) {
+    // reverse sweep: partials of psi with respect to the 19 lifted inputs
+    double g[19];
+#pragma unroll
+    for (int k = 0; k < 19; ++k) g[k] = 0.0;
+    if (!sat) {
+      const double eb = 1.0 / mu;
+      const double sb = eb, distb = -eb / lam, lamb = eb * dist / (lam * lam);
+      const double Sb = lamb * (0.5 / lam);
+      const double rxb = 2.0 * rx * Sb, ryb = 2.0 * ry * Sb;
+      double lxb = rxb / kfx, lyb = ryb / kfy;
+      double cxb = -rxb / kfx, cyb = -ryb / kfy;
+      double fxb = -rxb * rx / kfx, fyb = -ryb * ry / kfy;
+      const double topb = sb * (1.0 - fyf), botb = sb * fyf, fyfb = sb * (bot - top);
+      const double fxfb = topb * (d10 - d00) + botb * (d11 - d01);
+      lxb += fxfb;
+      lyb += fyfb;
+      const double iz = 1.0 / pc[2];
+      fxb += lxb * pc[0] * iz;
+      fyb += lyb * pc[1] * iz;
+      cxb += lxb;
+      cyb += lyb;
+      const double pcb[3] = {lxb * kfx * iz, lyb * kfy * iz,
+                             -(lxb * kfx * pc[0] + lyb * kfy * pc[1]) * iz * iz};
+      const double pp[3] = {px, py, pz};
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) g[3 * r + j] = pcb[r] * pp[j];
+        g[9 + r] = pcb[r];
+      }
+      const double cd = distb / dist;
+      g[12] = cd * dx;
+      g[13] = cd * dy;
+      g[14] = cd * dz;
+      g[15] = fxb;
+      g[16] = fyb;
+      g[17] = cxb;
+      g[18] = cyb;
+    }
+    const double inv_w1 = 1.0 / (wt + 1.0);
+    double* fim = vox.fim + v * vox.Dp;
+    for (int d = 0; d < Dp; ++d) {
+      double pim = 0.0;
+#pragma unroll
+      for (int k = 0; k < 19; ++k) pim = fma(g[k], sm[k * C + 1 + d], pim);
+      fim[d] = (wt * fim[d] + pim) * inv_w1;
+    }
+  }
+  const double wn = wt + 1.0;
+  vox.rw[v] = make_double2(fre, cap < wn ? cap : wn);
+  return true;
 }
 
 template <int G>
@@ -125,7 +241,10 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     const double px = vol.ox + vol.vs * static_cast<double>(i);
     const double py = vol.oy + vol.vs * static_cast<double>(j);
     const double pz = vol.oz + vol.vs * static_cast<double>(k);
-    count_updates(upd, fuse_voxel<G>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+    if constexpr (kAdjointFusion && G > 0)
+      count_updates(upd, fuse_voxel_adjoint(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+    else
+      count_updates(upd, fuse_voxel<G>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
   }
 }
 
@@ -148,8 +267,11 @@ __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const
       const double px = vol.ox + vol.vs * static_cast<double>(8 * bx + lx);
       const double py = vol.oy + vol.vs * static_cast<double>(8 * by + ly);
       const double pz = vol.oz + vol.vs * static_cast<double>(8 * bz + lz);
-      count_updates(upd, fuse_voxel<G>(vol.vox, static_cast<long long>(b) * kBlockVoxels + l, px, py, pz, depth, w,
-                                       h, vol.mu, vol.cap, Dp, sm));
+      const long long vv = static_cast<long long>(b) * kBlockVoxels + l;
+      if constexpr (kAdjointFusion && G > 0)
+        count_updates(upd, fuse_voxel_adjoint(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+      else
+        count_updates(upd, fuse_voxel<G>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
     }
   }
 }
@@ -1045,9 +1167,11 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
                          double2* hits, double* vre, double* nre, double* vim, double* nim) {
   const int P = w * h;
   if (L.phase != 2) {
+    // The warp-cooperative march measured slower than one thread per ray at
+    // every level on B200 (bench r01), so it is opt-in.
     static const long long warp_threshold = std::getenv("CSF_MARCH_WARP_MAX")
                                                 ? std::atoll(std::getenv("CSF_MARCH_WARP_MAX"))
-                                                : 100000;
+                                                : 0;
     if (P <= warp_threshold)
       k_raycast_march_warp<V><<<(P + 3) / 4, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip,
                                                                  step, box, hits, vre, nre);
