@@ -800,6 +800,184 @@ __global__ void __launch_bounds__(128) k_raycast_lift_all(V vol, const double* _
   }
 }
 
+// Cooperative lift: the per-pixel real chain (2 crossing samples, 6
+// gradient samples) is split over 8 lanes per pixel and its intermediates go
+// to shared memory; then one thread per (pixel, channel) evaluates the
+// tangent-form channel from them.  Real parts are bit-identical to the L<G>
+// evaluation (same sample_real_ex arithmetic); channels follow
+// k_raycast_lift_all.  Many light threads keep far more voxel-channel gathers
+// in flight than one heavy thread per (pixel, group).
+struct LiftRec {
+  double wgt[8][8];
+  double ds[8][3];
+  double f[8];
+  double dc[3], dn[3], dir[3], grad[3];
+  double rn, a0, a1, astar, num, den, ln;
+  int vid[8][8];
+  int ok;
+  int pad_;
+};
+constexpr int kLiftPix = 32;  // pixels per block (8 lanes each in the real pass)
+
+template <typename V>
+__global__ void __launch_bounds__(256) k_raycast_lift_coop(V vol, const double* __restrict__ pose,
+                                                           const double* __restrict__ intr, int w, int h, int Dp,
+                                                           const double2* __restrict__ hits, double* __restrict__ vre,
+                                                           double* __restrict__ nre, double* __restrict__ vim,
+                                                           double* __restrict__ nim) {
+  extern __shared__ double sm[];
+  const int C = 1 + Dp;
+  LiftRec* recs = reinterpret_cast<LiftRec*>(sm + 16 * C);
+  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
+  __syncthreads();
+  const double* kk = sm + 12 * C;
+  const int P = w * h;
+  const double hv = vol.vs;
+  // ---- real pass: lane s of pixel p
+  {
+    const int p = threadIdx.x >> 3, s = threadIdx.x & 7;
+    const int pix = blockIdx.x * kLiftPix + p;
+    LiftRec& r = recs[p];
+    double2 hit = make_double2(0.0, -1.0);
+    if (pix < P) hit = hits[pix];
+    const bool active = hit.y >= 0.0;
+    const int x = pix % w, y = pix / w;
+    double R[9], T[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) R[e] = sm[e * C];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) T[e] = sm[(9 + e) * C];
+    const double fxk = kk[0], fyk = kk[C], cxk = kk[2 * C], cyk = kk[3 * C];
+    const double tx = static_cast<double>(x) - cxk, ty = static_cast<double>(y) - cyk;
+    const double dc[3] = {tx / fxk, ty / fyk, 1.0};
+    const double rn = sqrt(dc[0] * dc[0] + (dc[1] * dc[1] + 1.0 * 1.0));
+    const double dn[3] = {dc[0] / rn, dc[1] / rn, dc[2] / rn};
+    double dir[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) dir[q] = R[3 * q] * dn[0] + (R[3 * q + 1] * dn[1] + R[3 * q + 2] * dn[2]);
+    const double a0 = hit.x, a1 = hit.y;
+    double f = 0.0;
+    if (active && s < 2) {
+      const double a = s == 0 ? a0 : a1;
+      sample_real_ex(vol, T[0] + a * dir[0], T[1] + a * dir[1], T[2] + a * dir[2], &f, r.vid[s], r.wgt[s], r.ds[s]);
+    }
+    const unsigned lane0 = (threadIdx.x & 31) & ~7u;
+    const double f0 = __shfl_sync(0xffffffffu, f, lane0);
+    const double f1 = __shfl_sync(0xffffffffu, f, lane0 + 1);
+    const double span = a1 - a0;
+    const double num = span * f0, den = f1 - f0;
+    const double astar = a0 - num / den;
+    const double vv[3] = {T[0] + astar * dir[0], T[1] + astar * dir[1], T[2] + astar * dir[2]};
+    bool ok = true;
+    double g = 0.0;
+    if (active && s < 6) {
+      const int axis = s >> 1;
+      double q[3] = {vv[0], vv[1], vv[2]};
+      q[axis] = (s & 1) ? q[axis] + hv : q[axis] - hv;
+      ok = sample_real_ex(vol, q[0], q[1], q[2], &g, r.vid[2 + s], r.wgt[2 + s], r.ds[2 + s]);
+    }
+    const unsigned all_ok = __ballot_sync(0xffffffffu, ok);
+    const bool group_ok = ((all_ok >> lane0) & 0xffu) == 0xffu;
+    double fs[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) fs[k] = __shfl_sync(0xffffffffu, g, lane0 + k);
+    if (s == 0) {
+      bool good = active && group_ok;
+      double grad[3], ln = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) grad[a] = (fs[2 * a + 1] - fs[2 * a]) / (2.0 * hv);
+      const double len2 = grad[0] * grad[0] + (grad[1] * grad[1] + grad[2] * grad[2]);
+      good = good && len2 > 0.0;
+      if (good) {
+        ln = sqrt(len2);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          vre[3LL * pix + c] = vv[c];
+          nre[3LL * pix + c] = grad[c] / ln;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          r.dc[c] = dc[c];
+          r.dn[c] = dn[c];
+          r.dir[c] = dir[c];
+          r.grad[c] = grad[c];
+        }
+        r.f[0] = f0;
+        r.f[1] = f1;
+        r.rn = rn;
+        r.a0 = a0;
+        r.a1 = a1;
+        r.astar = astar;
+        r.num = num;
+        r.den = den;
+        r.ln = ln;
+      }
+      r.ok = good ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (Dp == 0) return;
+  // ---- channel pass: one thread per (pixel, channel)
+  const double fxk = kk[0], fyk = kk[C];
+  const double inv_fx2 = 1.0 / (fxk * fxk), inv_fy2 = 1.0 / (fyk * fyk), inv_vs2 = 1.0 / (hv * hv);
+  const double inv_2h2 = 1.0 / ((2.0 * hv) * (2.0 * hv));
+  (void)inv_fx2; (void)inv_fy2; (void)inv_vs2; (void)inv_2h2;
+  for (int it = threadIdx.x; it < kLiftPix * Dp; it += blockDim.x) {
+    const int p = it / Dp, d = it - p * Dp;
+    const LiftRec& r = recs[p];
+    if (!r.ok) continue;
+    const int pix = blockIdx.x * kLiftPix + p;
+    const int x = pix % w, y = pix / w;
+    const int ch = 1 + d;
+    const double tx = static_cast<double>(x) - kk[2 * C], ty = static_cast<double>(y) - kk[3 * C];
+    const double rn = r.rn, den = r.den, num = r.num, ln = r.ln;
+    const double inv_rn2 = 1.0 / (rn * rn), inv_den2 = 1.0 / (den * den), inv_ln2 = 1.0 / (ln * ln);
+    (void)inv_rn2; (void)inv_den2; (void)inv_ln2;
+    const double dci[3] = {CSF_CH_DIV(-kk[2 * C + ch] * fxk - tx * kk[ch], fxk * fxk, inv_fx2),
+                           CSF_CH_DIV(-kk[3 * C + ch] * fyk - ty * kk[C + ch], fyk * fyk, inv_fy2), 0.0};
+    const double doti = (r.dc[0] * dci[0] + dci[0] * r.dc[0]) + ((r.dc[1] * dci[1] + dci[1] * r.dc[1]) + 0.0);
+    const double rni = (0.5 / rn) * doti;
+    double dni[3], diri[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dni[a] = CSF_CH_DIV(dci[a] * rn - r.dc[a] * rni, rn * rn, inv_rn2);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double t0 = sm[(3 * q) * C] * dni[0] + sm[(3 * q) * C + ch] * r.dn[0];
+      const double t1 = sm[(3 * q + 1) * C] * dni[1] + sm[(3 * q + 1) * C + ch] * r.dn[1];
+      const double t2 = sm[(3 * q + 2) * C] * dni[2] + sm[(3 * q + 2) * C + ch] * r.dn[2];
+      diri[q] = t0 + (t1 + t2);
+    }
+    const double Ti[3] = {sm[9 * C + ch], sm[10 * C + ch], sm[11 * C + ch]};
+    const double q0i[3] = {Ti[0] + r.a0 * diri[0], Ti[1] + r.a0 * diri[1], Ti[2] + r.a0 * diri[2]};
+    const double q1i[3] = {Ti[0] + r.a1 * diri[0], Ti[1] + r.a1 * diri[1], Ti[2] + r.a1 * diri[2]};
+    const double f0i = sample_channel(vol.vox, r.vid[0], r.wgt[0], r.ds[0], q0i, hv, inv_vs2, d);
+    const double f1i = sample_channel(vol.vox, r.vid[1], r.wgt[1], r.ds[1], q1i, hv, inv_vs2, d);
+    const double numi = (r.a1 - r.a0) * f0i, deni = f1i - f0i;
+    const double asti = -CSF_CH_DIV(numi * den - num * deni, den * den, inv_den2);
+    double vvi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) vvi[a] = Ti[a] + (r.astar * diri[a] + asti * r.dir[a]);
+    double gi[3];
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+      const double lo = sample_channel(vol.vox, r.vid[2 + 2 * axis], r.wgt[2 + 2 * axis], r.ds[2 + 2 * axis], vvi,
+                                       hv, inv_vs2, d);
+      const double hi = sample_channel(vol.vox, r.vid[3 + 2 * axis], r.wgt[3 + 2 * axis], r.ds[3 + 2 * axis], vvi,
+                                       hv, inv_vs2, d);
+      gi[axis] = CSF_CH_DIV((hi - lo) * (2.0 * hv), (2.0 * hv) * (2.0 * hv), inv_2h2);
+    }
+    const double l2i = (r.grad[0] * gi[0] + gi[0] * r.grad[0]) +
+                       ((r.grad[1] * gi[1] + gi[1] * r.grad[1]) + (r.grad[2] * gi[2] + gi[2] * r.grad[2]));
+    const double lni = (0.5 / ln) * l2i;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      vim[(3LL * pix + c) * Dp + d] = vvi[c];
+      nim[(3LL * pix + c) * Dp + d] = CSF_CH_DIV(gi[c] * ln - r.grad[c] * lni, ln * ln, inv_ln2);
+    }
+  }
+}
+
 // Warp-cooperative march for the small pyramid levels, where a few long
 // (grazing) rays set the kernel time: one warp per ray evaluates 32
 // consecutive alpha steps at once.  Each lane forms its alpha by the same
@@ -1189,8 +1367,21 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
   // one thread per hit pixel with tangent-form channels (CSF_LIFT_ALL=1) or
   // one thread per (hit pixel, channel group) — the default: more memory
   // parallelism wins over the recomputed real chain on B200.
-  static const bool per_pixel = std::getenv("CSF_LIFT_ALL") != nullptr;
-  if (G > 0 && per_pixel) {
+  static const char* mode_env = std::getenv("CSF_LIFT_MODE");
+  static const int mode = mode_env ? std::atoi(mode_env) : 0;  // 0 coop, 1 per pixel, 2 per group
+  if (mode == 0) {
+    const size_t smem_c = smem + sizeof(LiftRec) * kLiftPix;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_raycast_lift_coop<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      attr = true;
+    }
+    k_raycast_lift_coop<V><<<(P + kLiftPix - 1) / kLiftPix, 8 * kLiftPix, smem_c, L.stream>>>(
+        view, pose, intr, w, h, Dp, hits, vre, nre, vim, nim);
+    *L.launches += 1;
+    return;
+  }
+  if (G > 0 && mode == 1) {
     k_raycast_lift_all<V><<<(P + 127) / 128, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre, nre, vim,
                                                                     nim);
     *L.launches += 1;
