@@ -662,7 +662,7 @@ extern "C" int csf_raycast(csf_volume v, const double* pose, const double* intr,
   CUDA_TRY(ctx, v->s_nre.alloc(P * 3));
   CUDA_TRY(ctx, v->s_vim.alloc(P * 3 * std::max(v->Dp, 1)));
   CUDA_TRY(ctx, v->s_nim.alloc(P * 3 * std::max(v->Dp, 1)));
-  CUDA_TRY(ctx, v->s_hits.alloc(P));
+  CUDA_TRY(ctx, v->s_hits.alloc(2 * P));  // (alpha_prev, alpha), then (f_prev, f)
   CUDA_TRY(ctx, cudaMemcpyAsync(v->s_pose.p, pp.data(), sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(v->s_intr.p, kp.data(), sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
   raycast_dev(v, v->s_pose.p, v->s_intr.p, w, h, rc, v->s_hits.p, v->s_vre.p, v->s_nre.p, v->s_vim.p, v->s_nim.p);
@@ -771,7 +771,7 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   A(p->kbase.alloc(4));
   A(p->out.alloc(2 + CSF_MAX_DIRECTIONS));
   A(p->st.alloc(1));
-  A(p->hits.alloc(P));
+  A(p->hits.alloc(2 * P));
   if (e != cudaSuccess) {
     delete p;
     return fail(ctx, CSF_ENOMEM, std::string("csf_pipeline_create: ") + cudaGetErrorString(e));
@@ -955,7 +955,7 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
   DevBuf<TrackState> st;
   DevBuf<double2> hits;
   const int tiles_max = icp_tiles(w, h, 1);
-  CUDA_TRY(ctx, hits.alloc(P));
+  CUDA_TRY(ctx, hits.alloc(2 * P));
   CUDA_TRY(ctx, dd.alloc(P));
   CUDA_TRY(ctx, raw.alloc(P));
   CUDA_TRY(ctx, pyr0.alloc(P));

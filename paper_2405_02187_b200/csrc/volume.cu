@@ -606,6 +606,7 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
     }
     if (have_prev && f_prev > 0.0 && f < 0.0) {
       hits[pix] = make_double2(alpha_prev, alpha);
+      hits[w * h + pix] = make_double2(f_prev, f);
       return;
     }
     have_prev = true;
@@ -857,31 +858,39 @@ __global__ void __launch_bounds__(256) k_raycast_lift_coop(V vol, const double* 
 #pragma unroll
     for (int q = 0; q < 3; ++q) dir[q] = R[3 * q] * dn[0] + (R[3 * q + 1] * dn[1] + R[3 * q + 2] * dn[2]);
     const double a0 = hit.x, a1 = hit.y;
-    double f = 0.0;
-    if (active && s < 2) {
-      const double a = s == 0 ? a0 : a1;
-      sample_real_ex(vol, T[0] + a * dir[0], T[1] + a * dir[1], T[2] + a * dir[2], &f, r.vid[s], r.wgt[s], r.ds[s]);
-    }
-    const unsigned lane0 = (threadIdx.x & 31) & ~7u;
-    const double f0 = __shfl_sync(0xffffffffu, f, lane0);
-    const double f1 = __shfl_sync(0xffffffffu, f, lane0 + 1);
+    // f0, f1: the march's samples at a0, a1 (same arithmetic as sample_real_ex)
+    const double2 fpair = active ? hits[P + pix] : make_double2(0.0, 0.0);
+    const double f0 = fpair.x, f1 = fpair.y;
     const double span = a1 - a0;
     const double num = span * f0, den = f1 - f0;
     const double astar = a0 - num / den;
     const double vv[3] = {T[0] + astar * dir[0], T[1] + astar * dir[1], T[2] + astar * dir[2]};
+    // all eight samples at once: lanes 0, 1 the crossing pair (corner data
+    // for the channels), lanes 2..7 the central differences
     bool ok = true;
     double g = 0.0;
-    if (active && s < 6) {
-      const int axis = s >> 1;
-      double q[3] = {vv[0], vv[1], vv[2]};
-      q[axis] = (s & 1) ? q[axis] + hv : q[axis] - hv;
-      ok = sample_real_ex(vol, q[0], q[1], q[2], &g, r.vid[2 + s], r.wgt[2 + s], r.ds[2 + s]);
+    if (active) {
+      double q[3];
+      if (s < 2) {
+        const double a = s == 0 ? a0 : a1;
+        q[0] = T[0] + a * dir[0];
+        q[1] = T[1] + a * dir[1];
+        q[2] = T[2] + a * dir[2];
+      } else {
+        const int axis = (s - 2) >> 1;
+        q[0] = vv[0];
+        q[1] = vv[1];
+        q[2] = vv[2];
+        q[axis] = (s & 1) ? q[axis] + hv : q[axis] - hv;
+      }
+      ok = sample_real_ex(vol, q[0], q[1], q[2], &g, r.vid[s], r.wgt[s], r.ds[s]) || s < 2;
     }
+    const unsigned lane0 = (threadIdx.x & 31) & ~7u;
     const unsigned all_ok = __ballot_sync(0xffffffffu, ok);
     const bool group_ok = ((all_ok >> lane0) & 0xffu) == 0xffu;
     double fs[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) fs[k] = __shfl_sync(0xffffffffu, g, lane0 + k);
+    for (int k = 0; k < 6; ++k) fs[k] = __shfl_sync(0xffffffffu, g, lane0 + 2 + k);
     if (s == 0) {
       bool good = active && group_ok;
       double grad[3], ln = 0.0;
@@ -1085,7 +1094,10 @@ __global__ void __launch_bounds__(128) k_raycast_march_warp(V vol, const double*
     const unsigned bal = __ballot_sync(0xffffffffu, cross);
     if (bal) {
       const int c = __ffs(bal) - 1;
-      if (lane == c) hits[pix] = make_double2(prev_a, a);
+      if (lane == c) {
+        hits[pix] = make_double2(prev_a, a);
+        hits[w * h + pix] = make_double2(prev_f, f);
+      }
       return;
     }
     // carry the state of the window's last in-range step
