@@ -41,6 +41,7 @@ extern "C" {
 #define CSF_ENOMEM 5
 
 #define CSF_MAX_DIRECTIONS 36
+#define CSF_MAX_PAIRS 64
 
 typedef struct csf_ctx_s* csf_ctx;
 typedef struct csf_volume_s* csf_volume;
@@ -112,7 +113,14 @@ typedef struct {
 /* The CSFD frame-derivative run: seed D directions (first-frame
  * twist components 0..5 in (rho, phi) order and/or intrinsics 6..9 =
  * fx, fy, cx, cy), fuse frame 0 at exp(xi0*) T0, track + fuse frames
- * 1..N-1 with the lifted tracker, differentiate the objective. */
+ * 1..N-1 with the lifted tracker, differentiate the objective.
+ *
+ * order = 2 (BASELINE config 3): instead of dirs, n_pairs parameter pairs
+ * (pair_i[p], pair_j[p]) each carried as one reference Bicomplex
+ * (csfd.hpp:83-140; im1 seeded on pair_i, im2 on pair_j) packed as three
+ * channel slots (im1, im2, im12) of one evaluation; the result is the
+ * Hessian entry im12/h^2 per pair (csf_pipeline_hessian), the csfd_hessian
+ * pattern of diff.hpp:58-72 applied to the whole frame loop. */
 typedef struct {
   int hashed;
   csf_volume_params dense;
@@ -125,6 +133,10 @@ typedef struct {
   int dirs[CSF_MAX_DIRECTIONS];
   int objective;
   int max_frames;
+  int order;                    /* 1 (default, 0 also means 1) or 2 */
+  int n_pairs;                  /* order 2 */
+  int pair_i[CSF_MAX_PAIRS];
+  int pair_j[CSF_MAX_PAIRS];
 } csf_pipeline_cfg;
 
 /* ---- defaults (the reference's struct defaults) ------------------------- */
@@ -195,6 +207,11 @@ int csf_pipeline_run(csf_pipeline p, int n_frames);
  * (optional: iterations, correspondences, converged, allocated blocks,
  * visible blocks, new blocks, fused voxels, 0). */
 int csf_pipeline_result(csf_pipeline p, double* gradient, double* objective, double* poses, int32_t* stats);
+/* Order-2 runs: hessian [n_pairs] = H_{pair_i, pair_j}; grad1/grad2 [n_pairs]
+ * (optional) = d obj / d param pair_i / pair_j from the same pass; poses
+ * (optional) [n][12][1 + 3 n_pairs] (re, then im1, im2, im12 per pair). */
+int csf_pipeline_hessian(csf_pipeline p, double* hessian, double* grad1, double* grad2, double* objective,
+                         double* poses, int32_t* stats);
 /* One end-to-end call from host buffers: upload, run, read back. */
 int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames, double* gradient,
                           double* objective);

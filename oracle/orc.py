@@ -44,6 +44,7 @@ def lib() -> C.CDLL:
                                      dp, C.POINTER(_capi.TrackResult)]),
             "orc_workload": (ip, [ip, ip, ip, ip, fp, dp, C.POINTER(_capi.Intrinsics)]),
             "orc_pipeline_run": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, i32p, dp]),
+            "orc_pipeline_hessian": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, dp, dp, i32p, dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -190,3 +191,22 @@ def pipeline_run(cfg, depth, gt):
                                   C.byref(obj), _dp(poses), stats.ctypes.data_as(C.POINTER(C.c_int32)),
                                   C.byref(secs)))
     return grad, obj.value, poses, stats, secs.value
+
+
+def pipeline_hessian(cfg, depth, gt):
+    """Second-order run, one Bicomplex pass per pair (the reference's
+    csfd_hessian pattern).  Returns (hessian[P], grad1[P], grad2[P], objective,
+    poses[n][12][1+3P], stats, seconds)."""
+    d = np.ascontiguousarray(depth, dtype=np.float32)
+    g = np.ascontiguousarray(gt, dtype=np.float64).reshape(-1, 12)
+    n = d.shape[0]
+    P = cfg.n_pairs
+    hess, g1, g2 = np.empty(P), np.empty(P), np.empty(P)
+    obj = C.c_double()
+    poses = np.empty((n, 12, 1 + 3 * P))
+    stats = np.empty((n, 8), dtype=np.int32)
+    secs = C.c_double()
+    _check(lib().orc_pipeline_hessian(C.byref(cfg), d.ctypes.data_as(C.POINTER(C.c_float)), _dp(g), n, _dp(hess),
+                                      _dp(g1), _dp(g2), C.byref(obj), _dp(poses),
+                                      stats.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(secs)))
+    return hess, g1, g2, obj.value, poses, stats, secs.value

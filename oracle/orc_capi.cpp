@@ -332,31 +332,84 @@ int orc_workload(int config, int n_frames, int width, int height, float* depth, 
 // The CSFD frame-derivative run.  poses [n][12][1+D], stats [n][8]
 // (iterations, correspondences, 0, blocks, visible, ...).  Returns wall
 // seconds through *seconds (the CPU baseline's timed region).
+}  // extern "C"
+
+namespace {
+PipelineConfig to_pipeline(const csf_pipeline_cfg* c) {
+  PipelineConfig cfg;
+  cfg.hashed = c->hashed != 0;
+  cfg.dense = to_vp(c->dense);
+  cfg.hash = to_hp(c->hash);
+  cfg.k = to_intr(c->k);
+  cfg.icp = to_icp(c->icp);
+  cfg.rc = to_rc(&c->rc);
+  cfg.h = StepSize(c->h).h;
+  cfg.directions.assign(c->dirs, c->dirs + c->n_dirs);
+  cfg.objective = static_cast<Objective>(c->objective);
+  return cfg;
+}
+void to_frames(const PipelineConfig& cfg, const float* depth, const double* gt_in, int n_frames,
+               std::vector<Image<double>>* frames, std::vector<Pose>* gt) {
+  const std::size_t P = static_cast<std::size_t>(cfg.k.width) * cfg.k.height;
+  for (int f = 0; f < n_frames; ++f) {
+    Image<double> im(cfg.k.width, cfg.k.height, 0.0);
+    for (std::size_t i = 0; i < P; ++i) im.data[i] = static_cast<double>(depth[f * P + i]);
+    frames->push_back(std::move(im));
+    Pose p;
+    for (int e = 0; e < 9; ++e) p.rotation(e / 3, e % 3) = gt_in[12 * f + e];
+    for (int e = 0; e < 3; ++e) p.translation[e] = gt_in[12 * f + 9 + e];
+    gt->push_back(p);
+  }
+}
+void write_stats(int n_frames, const std::vector<int>& it, const std::vector<int>& corr, const std::vector<int>& blocks,
+                 const std::vector<int>& vis, int32_t* stats) {
+  for (int f = 0; f < n_frames; ++f) {
+    stats[8 * f] = it[f];
+    stats[8 * f + 1] = corr[f];
+    stats[8 * f + 2] = 0;
+    stats[8 * f + 3] = blocks[f];
+    stats[8 * f + 4] = vis[f];
+    for (int j = 5; j < 8; ++j) stats[8 * f + j] = 0;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+// Second-order run: one Bicomplex pass per pair (csfd_hessian pattern).
+int orc_pipeline_hessian(const csf_pipeline_cfg* c, const float* depth, const double* gt_in, int n_frames,
+                         double* hessian, double* grad1, double* grad2, double* objective, double* poses,
+                         int32_t* stats, double* seconds) {
+  return guard([&] {
+    const PipelineConfig cfg = to_pipeline(c);
+    if (c->n_pairs <= 0 || c->n_pairs > CSF_MAX_PAIRS) throw std::invalid_argument("orc_pipeline_hessian: n_pairs");
+    std::vector<std::pair<int, int>> pairs;
+    for (int p = 0; p < c->n_pairs; ++p) pairs.emplace_back(c->pair_i[p], c->pair_j[p]);
+    std::vector<Image<double>> frames;
+    std::vector<Pose> gt;
+    to_frames(cfg, depth, gt_in, n_frames, &frames, &gt);
+    const auto t0 = std::chrono::steady_clock::now();
+    const HessianResult r = run_pipeline_hessian(cfg, pairs, frames, gt);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (objective) *objective = r.objective;
+    for (int p = 0; p < c->n_pairs; ++p) {
+      if (hessian) hessian[p] = r.hessian[p];
+      if (grad1) grad1[p] = r.grad1[p];
+      if (grad2) grad2[p] = r.grad2[p];
+    }
+    if (poses) std::memcpy(poses, r.poses.data(), sizeof(double) * r.poses.size());
+    if (stats) write_stats(n_frames, r.iterations, r.correspondences, r.blocks, r.visible, stats);
+  });
+}
+
 int orc_pipeline_run(const csf_pipeline_cfg* c, const float* depth, const double* gt_in, int n_frames,
                      double* gradient, double* objective, double* poses, int32_t* stats, double* seconds) {
   return guard([&] {
-    PipelineConfig cfg;
-    cfg.hashed = c->hashed != 0;
-    cfg.dense = to_vp(c->dense);
-    cfg.hash = to_hp(c->hash);
-    cfg.k = to_intr(c->k);
-    cfg.icp = to_icp(c->icp);
-    cfg.rc = to_rc(&c->rc);
-    cfg.h = StepSize(c->h).h;
-    cfg.directions.assign(c->dirs, c->dirs + c->n_dirs);
-    cfg.objective = static_cast<Objective>(c->objective);
-    const std::size_t P = static_cast<std::size_t>(cfg.k.width) * cfg.k.height;
+    const PipelineConfig cfg = to_pipeline(c);
     std::vector<Image<double>> frames;
     std::vector<Pose> gt;
-    for (int f = 0; f < n_frames; ++f) {
-      Image<double> im(cfg.k.width, cfg.k.height, 0.0);
-      for (std::size_t i = 0; i < P; ++i) im.data[i] = static_cast<double>(depth[f * P + i]);
-      frames.push_back(std::move(im));
-      Pose p;
-      for (int e = 0; e < 9; ++e) p.rotation(e / 3, e % 3) = gt_in[12 * f + e];
-      for (int e = 0; e < 3; ++e) p.translation[e] = gt_in[12 * f + 9 + e];
-      gt.push_back(p);
-    }
+    to_frames(cfg, depth, gt_in, n_frames, &frames, &gt);
     const auto t0 = std::chrono::steady_clock::now();
     const PipelineResult r = run_pipeline_dyn(cfg, frames, gt);
     const auto t1 = std::chrono::steady_clock::now();
@@ -365,15 +418,7 @@ int orc_pipeline_run(const csf_pipeline_cfg* c, const float* depth, const double
     if (gradient)
       for (int d = 0; d < c->n_dirs; ++d) gradient[d] = r.gradient[d];
     if (poses) std::memcpy(poses, r.poses.data(), sizeof(double) * r.poses.size());
-    if (stats)
-      for (int f = 0; f < n_frames; ++f) {
-        stats[8 * f] = r.iterations[f];
-        stats[8 * f + 1] = r.correspondences[f];
-        stats[8 * f + 2] = 0;
-        stats[8 * f + 3] = r.blocks[f];
-        stats[8 * f + 4] = r.visible[f];
-        for (int j = 5; j < 8; ++j) stats[8 * f + j] = 0;
-      }
+    if (stats) write_stats(n_frames, r.iterations, r.correspondences, r.blocks, r.visible, stats);
   });
 }
 

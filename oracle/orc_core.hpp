@@ -323,6 +323,10 @@ template <> struct Measure<Complex> {
 };
 template <> struct Measure<Bicomplex> {
   template <typename M> static Bicomplex in(const M& m) { return Bicomplex(real_part(m)); }
+  // BUILDER-DEFINED extension: a Bicomplex-stored volume (second-order CSFD
+  // of the whole pipeline, BASELINE config 3) keeps its own channels; the
+  // reference only ever stores Complex fields and drops them (csfd.hpp:331).
+  static Bicomplex in(const Bicomplex& m) { return m; }
 };
 template <int D> struct Measure<Lifted<D>> {
   static Lifted<D> in(const Lifted<D>& m) { return m; }

@@ -123,73 +123,176 @@ void store_pose(const PoseT<Lifted<D>>& p, double* out) {
   }
 }
 
-template <int D, typename V>
-PipelineResult run_pipeline_on(V& vol, const PipelineConfig& cfg, const std::vector<Image<double>>& frames,
-                               const std::vector<Pose>& gt) {
-  using S = Lifted<D>;
-  if (static_cast<int>(cfg.directions.size()) != D) throw std::invalid_argument("direction count != D");
+// One lifted run of the frame loop for any CSFD scalar S (Lifted<D> packs D
+// first-order directions; Bicomplex carries one second-order pair): seed
+// pose exp(xi) * T0_gt with lifted intrinsics ks, fuse frame 0, then track and
+// fuse frames 1..N-1; the objective is evaluated in S.
+template <typename S>
+struct LiftedRun {
+  std::vector<PoseT<S>> poses;
+  S objective = S(0.0);
+  std::vector<int> iterations, correspondences, blocks, visible;
+};
+
+template <typename S, typename V>
+LiftedRun<S> run_lifted(V& vol, const PipelineConfig& cfg, const std::vector<Image<double>>& frames,
+                        const std::vector<Pose>& gt, const Vec6<S>& xi, const IntrinsicsT<S>& ks) {
   const int n = static_cast<int>(frames.size());
-  PipelineResult res;
-  res.poses.assign(static_cast<std::size_t>(n) * 12 * (1 + D), 0.0);
+  LiftedRun<S> res;
+  res.poses.resize(n);
   res.iterations.assign(n, 0);
   res.correspondences.assign(n, 0);
   res.blocks.assign(n, 0);
   res.visible.assign(n, 0);
-
-  Vec6<S> xi;
-  for (int i = 0; i < 6; ++i) xi[i] = S(0.0);
-  IntrinsicsT<S> ks;
-  ks.fx = S(cfg.k.fx); ks.fy = S(cfg.k.fy); ks.cx = S(cfg.k.cx); ks.cy = S(cfg.k.cy);
-  ks.width = cfg.k.width; ks.height = cfg.k.height; ks.depth_scale = cfg.k.depth_scale;
-  for (int d = 0; d < D; ++d) {
-    const int prm = cfg.directions[d];
-    if (prm >= 0 && prm < 6) xi[prm].im[d] = cfg.h;
-    else if (prm == 6) ks.fx.im[d] = cfg.h;
-    else if (prm == 7) ks.fy.im[d] = cfg.h;
-    else if (prm == 8) ks.cx.im[d] = cfg.h;
-    else if (prm == 9) ks.cy.im[d] = cfg.h;
-    else throw std::invalid_argument("unknown direction parameter");
-  }
   const Intrinsics kr = cfg.k;
-
-  std::vector<PoseT<S>> poses(n);
   auto integrate = [&](int f) {
     if constexpr (V::kHashed) {
       AllocStats st;
-      const std::vector<int> visible = allocate_band(vol, frames[f], kr, real_pose(poses[f]), &st);
-      surface_update_blocks(vol, visible, frames[f], poses[f], ks);
+      const std::vector<int> visible = allocate_band(vol, frames[f], kr, real_pose(res.poses[f]), &st);
+      surface_update_blocks(vol, visible, frames[f], res.poses[f], ks);
       res.blocks[f] = vol.n_blocks();
       res.visible[f] = st.touched;
     } else {
-      surface_update(vol, frames[f], poses[f], ks);
+      surface_update(vol, frames[f], res.poses[f], ks);
     }
   };
-
-  poses[0] = exp_map(xi) * pose_cast<S>(gt[0]);
+  res.poses[0] = exp_map(xi) * pose_cast<S>(gt[0]);
   integrate(0);
   for (int f = 1; f < n; ++f) {
-    const LiftedTrackResult<S> tr = track_frame_lifted<S>(vol, frames[f], poses[f - 1], ks, cfg.icp, cfg.rc);
-    poses[f] = tr.pose;
+    const LiftedTrackResult<S> tr = track_frame_lifted<S>(vol, frames[f], res.poses[f - 1], ks, cfg.icp, cfg.rc);
+    res.poses[f] = tr.pose;
     res.iterations[f] = tr.iterations;
     res.correspondences[f] = tr.correspondences;
     integrate(f);
   }
   S obj(0.0);
   if (cfg.objective == Objective::kFinalTranslationError) {
-    const Vec3<S> diff = poses[n - 1].translation -
+    const Vec3<S> diff = res.poses[n - 1].translation -
                          Vec3<S>(S(gt[n - 1].translation[0]), S(gt[n - 1].translation[1]), S(gt[n - 1].translation[2]));
     obj = sqrt(dot(diff, diff));
   } else {
     for (int f = 0; f < n; ++f) {
-      const Vec3<S> diff = poses[f].translation -
+      const Vec3<S> diff = res.poses[f].translation -
                            Vec3<S>(S(gt[f].translation[0]), S(gt[f].translation[1]), S(gt[f].translation[2]));
       obj = obj + dot(diff, diff);
     }
   }
-  res.objective = obj.re;
+  res.objective = obj;
+  return res;
+}
+
+// Seed parameter `prm` of a lifted scalar set: 0..5 twist (rho, phi), 6..9
+// fx, fy, cx, cy.  `set` writes the perturbation into the scalar.
+template <typename S, typename Fn>
+void seed_parameter(int prm, Vec6<S>& xi, IntrinsicsT<S>& ks, Fn&& set) {
+  if (prm >= 0 && prm < 6) set(xi[prm]);
+  else if (prm == 6) set(ks.fx);
+  else if (prm == 7) set(ks.fy);
+  else if (prm == 8) set(ks.cx);
+  else if (prm == 9) set(ks.cy);
+  else throw std::invalid_argument("unknown direction parameter");
+}
+
+template <typename S>
+IntrinsicsT<S> lift_intrinsics(const Intrinsics& k) {
+  IntrinsicsT<S> ks;
+  ks.fx = S(k.fx); ks.fy = S(k.fy); ks.cx = S(k.cx); ks.cy = S(k.cy);
+  ks.width = k.width; ks.height = k.height; ks.depth_scale = k.depth_scale;
+  return ks;
+}
+
+template <int D, typename V>
+PipelineResult run_pipeline_on(V& vol, const PipelineConfig& cfg, const std::vector<Image<double>>& frames,
+                               const std::vector<Pose>& gt) {
+  using S = Lifted<D>;
+  if (static_cast<int>(cfg.directions.size()) != D) throw std::invalid_argument("direction count != D");
+  const int n = static_cast<int>(frames.size());
+  Vec6<S> xi;
+  for (int i = 0; i < 6; ++i) xi[i] = S(0.0);
+  IntrinsicsT<S> ks = lift_intrinsics<S>(cfg.k);
+  for (int d = 0; d < D; ++d) seed_parameter(cfg.directions[d], xi, ks, [&](S& s) { s.im[d] = cfg.h; });
+  const LiftedRun<S> run = run_lifted<S>(vol, cfg, frames, gt, xi, ks);
+  PipelineResult res;
+  res.poses.assign(static_cast<std::size_t>(n) * 12 * (1 + D), 0.0);
+  res.iterations = run.iterations;
+  res.correspondences = run.correspondences;
+  res.blocks = run.blocks;
+  res.visible = run.visible;
+  res.objective = run.objective.re;
   res.gradient.resize(D);
-  for (int d = 0; d < D; ++d) res.gradient[d] = obj.im[d] / cfg.h;
-  for (int f = 0; f < n; ++f) store_pose(poses[f], &res.poses[static_cast<std::size_t>(f) * 12 * (1 + D)]);
+  for (int d = 0; d < D; ++d) res.gradient[d] = run.objective.im[d] / cfg.h;
+  for (int f = 0; f < n; ++f) store_pose(run.poses[f], &res.poses[static_cast<std::size_t>(f) * 12 * (1 + D)]);
+  return res;
+}
+
+// ---------------------------------------------------------------------------
+// Second order (BASELINE config 3): one Bicomplex pass per parameter pair
+// (i, j) — the reference's csfd_hessian pattern (diff.hpp:58-72), applied to
+// the whole frame loop.  im1 is seeded on parameter i, im2 on parameter j;
+// H_ij = im12 / h^2 (csfd.hpp:319), g_i = im1 / h, g_j = im2 / h.  The volume
+// stores Bicomplex fields (builder-defined; see Measure<Bicomplex>).
+// ---------------------------------------------------------------------------
+struct HessianResult {
+  std::vector<double> hessian;   // [P]  H_{i_p j_p}
+  std::vector<double> grad1;     // [P]  d obj / d param i_p
+  std::vector<double> grad2;     // [P]  d obj / d param j_p
+  double objective = 0.0;
+  std::vector<double> poses;     // [N][12][1 + 3P]: re, then (im1, im2, im12) per pair
+  std::vector<int> iterations, correspondences, blocks, visible;
+};
+
+template <typename V>
+LiftedRun<Bicomplex> run_pair(V& vol, const PipelineConfig& cfg, const std::vector<Image<double>>& frames,
+                              const std::vector<Pose>& gt, int pi, int pj) {
+  using S = Bicomplex;
+  Vec6<S> xi;
+  for (int i = 0; i < 6; ++i) xi[i] = S(0.0);
+  IntrinsicsT<S> ks = lift_intrinsics<S>(cfg.k);
+  seed_parameter(pi, xi, ks, [&](S& s) { s.im1 = cfg.h; });
+  seed_parameter(pj, xi, ks, [&](S& s) { s.im2 = cfg.h; });
+  return run_lifted<S>(vol, cfg, frames, gt, xi, ks);
+}
+
+inline HessianResult run_pipeline_hessian(const PipelineConfig& cfg, const std::vector<std::pair<int, int>>& pairs,
+                                          const std::vector<Image<double>>& frames, const std::vector<Pose>& gt) {
+  const int n = static_cast<int>(frames.size());
+  const int P = static_cast<int>(pairs.size());
+  const int C = 1 + 3 * P;
+  HessianResult res;
+  res.hessian.resize(P);
+  res.grad1.resize(P);
+  res.grad2.resize(P);
+  res.poses.assign(static_cast<std::size_t>(n) * 12 * C, 0.0);
+  for (int p = 0; p < P; ++p) {
+    LiftedRun<Bicomplex> run;
+    if (cfg.hashed) {
+      HashedVolumeT<Bicomplex> vol(cfg.hash);
+      run = run_pair(vol, cfg, frames, gt, pairs[p].first, pairs[p].second);
+    } else {
+      TsdfVolumeT<Bicomplex> vol(cfg.dense);
+      run = run_pair(vol, cfg, frames, gt, pairs[p].first, pairs[p].second);
+    }
+    const Bicomplex& o = run.objective;
+    res.hessian[p] = o.im12 / (cfg.h * cfg.h);
+    res.grad1[p] = o.im1 / cfg.h;
+    res.grad2[p] = o.im2 / cfg.h;
+    if (p == 0) {
+      res.objective = o.re;
+      res.iterations = run.iterations;
+      res.correspondences = run.correspondences;
+      res.blocks = run.blocks;
+      res.visible = run.visible;
+    }
+    for (int f = 0; f < n; ++f)
+      for (int e = 0; e < 12; ++e) {
+        const Bicomplex& s = e < 9 ? run.poses[f].rotation(e / 3, e % 3) : run.poses[f].translation[e - 9];
+        double* dst = &res.poses[(static_cast<std::size_t>(f) * 12 + e) * C];
+        dst[0] = s.re;
+        dst[1 + 3 * p] = s.im1;
+        dst[2 + 3 * p] = s.im2;
+        dst[3 + 3 * p] = s.im12;
+      }
+  }
   return res;
 }
 

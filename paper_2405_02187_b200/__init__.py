@@ -23,7 +23,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import Optional, Sequence
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -32,7 +32,7 @@ from . import capi as _capi
 __all__ = [
     "InvalidArgument", "DomainError", "Context", "bilateral_filter", "downsample_depth", "build_depth_pyramid",
     "measure_surface", "TsdfVolume", "HashedVolume", "surface_update", "raycast", "track_frame", "TrackResult",
-    "Pipeline", "PipelineResult", "synth_workload", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
+    "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
     "lift_pose", "lift_intrinsics", "library",
 ]
 
@@ -406,7 +406,11 @@ class Pipeline:
     def __init__(self, cfg: _capi.PipelineCfg, ctx: Optional[Context] = None):
         self.ctx = _ctx(ctx)
         self.cfg = cfg
-        self.D = cfg.n_dirs
+        self.order = 2 if cfg.order == 2 else 1
+        self.n_pairs = cfg.n_pairs if self.order == 2 else 0
+        # outputs per run: D first-order derivatives, or one Hessian entry per pair
+        self.D = self.n_pairs if self.order == 2 else cfg.n_dirs
+        self.slots = 3 * self.n_pairs if self.order == 2 else cfg.n_dirs
         self.h = C.c_void_p()
         self.ctx.check(self.ctx.lib.csf_pipeline_create(self.ctx.h, C.byref(cfg), C.byref(self.h)))
         self.n_frames = 0
@@ -435,7 +439,7 @@ class Pipeline:
         n = self.n_frames
         g = np.zeros(max(self.D, 1))
         obj = C.c_double()
-        P = np.empty((n, 12, 1 + self.D)) if poses else None
+        P = np.empty((n, 12, 1 + self.slots)) if poses else None
         S = np.empty((n, 8), dtype=np.int32) if stats else None
         self.ctx.check(self.ctx.lib.csf_pipeline_result(
             self.h, _dp(g), C.byref(obj), _dp(P) if P is not None else None,
@@ -453,11 +457,39 @@ class Pipeline:
                                                           C.byref(obj)))
         return PipelineResult(grad[: self.D].copy(), obj.value)
 
+    def hessian(self, poses: bool = False, stats: bool = False) -> "HessianResult":
+        """Order-2 result: H_{i_p j_p} per pair and the pair's first-order
+        derivatives d obj / d param i_p, j_p (csf_pipeline_hessian)."""
+        P_ = self.n_pairs
+        H, g1, g2 = np.empty(P_), np.empty(P_), np.empty(P_)
+        obj = C.c_double()
+        n = self.n_frames
+        P = np.empty((n, 12, 1 + self.slots)) if poses else None
+        S = np.empty((n, 8), dtype=np.int32) if stats else None
+        self.ctx.check(self.ctx.lib.csf_pipeline_hessian(
+            self.h, _dp(H), _dp(g1), _dp(g2), C.byref(obj), _dp(P) if P is not None else None,
+            S.ctypes.data_as(C.POINTER(C.c_int32)) if S is not None else None))
+        return HessianResult(H, g1, g2, obj.value, P, S)
+
+
+@dataclass
+class HessianResult:
+    hessian: np.ndarray
+    grad1: np.ndarray
+    grad2: np.ndarray
+    objective: float
+    poses: Optional[np.ndarray] = None
+    stats: Optional[np.ndarray] = None
+
 
 def make_pipeline_cfg(*, hashed: bool, k: _capi.Intrinsics, dirs: Sequence[int], h: float, objective: int,
                       max_frames: int, dense: Optional[_capi.VolumeParams] = None,
                       hash_params: Optional[_capi.HashParams] = None, icp: Optional[_capi.IcpCfg] = None,
-                      rc: Optional[_capi.RaycastCfg] = None) -> _capi.PipelineCfg:
+                      rc: Optional[_capi.RaycastCfg] = None,
+                      pairs: Optional[Sequence[Tuple[int, int]]] = None) -> _capi.PipelineCfg:
+    """Pipeline descriptor.  `dirs` = first-order parameters (0..5 twist, 6..9
+    fx, fy, cx, cy); `pairs` (instead of dirs) = second-order parameter pairs
+    (i, j), order 2 (BASELINE config 3)."""
     cfg = _capi.PipelineCfg()
     cfg.hashed = int(hashed)
     if dense is not None:
@@ -473,6 +505,17 @@ def make_pipeline_cfg(*, hashed: bool, k: _capi.Intrinsics, dirs: Sequence[int],
         cfg.dirs[i] = d
     cfg.objective = objective
     cfg.max_frames = max_frames
+    cfg.order = 1
+    if pairs is not None:
+        if len(dirs):
+            raise ValueError("make_pipeline_cfg: give dirs (order 1) or pairs (order 2), not both")
+        if not 0 < len(pairs) <= _capi.CSF_MAX_PAIRS:
+            raise ValueError("make_pipeline_cfg: 1..CSF_MAX_PAIRS pairs")
+        cfg.order = 2
+        cfg.n_pairs = len(pairs)
+        for p, (i, j) in enumerate(pairs):
+            cfg.pair_i[p] = i
+            cfg.pair_j[p] = j
     return cfg
 
 

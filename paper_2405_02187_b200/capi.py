@@ -14,6 +14,7 @@ LIB_PATH = Path(os.environ["CSF_B200_LIB"]) if os.environ.get("CSF_B200_LIB") el
 
 CSF_OK, CSF_EINVAL, CSF_EDOMAIN, CSF_ERUNTIME, CSF_ECUDA, CSF_ENOMEM = 0, 1, 2, 3, 4, 5
 CSF_MAX_DIRECTIONS = 36
+CSF_MAX_PAIRS = 64
 SOLVER_LINEARIZED, SOLVER_NEWTON, SOLVER_GRADIENT_DESCENT, SOLVER_CONJUGATE_GRADIENT = 0, 1, 2, 3
 OBJECTIVE_FINAL_TRANSLATION_ERROR, OBJECTIVE_TRAJECTORY_ERROR = 0, 1
 
@@ -25,7 +26,8 @@ EXPORTS = (
     "csf_volume_create_dense", "csf_volume_create_hashed", "csf_volume_destroy", "csf_volume_upload",
     "csf_volume_download", "csf_volume_block_count", "csf_volume_download_hash", "csf_surface_update",
     "csf_raycast", "csf_track_frame", "csf_pipeline_create", "csf_pipeline_destroy", "csf_pipeline_upload",
-    "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_run_host", "csf_synth_workload",
+    "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_hessian", "csf_pipeline_run_host",
+    "csf_synth_workload",
 )
 
 
@@ -63,7 +65,9 @@ class TrackResult(C.Structure):
 class PipelineCfg(C.Structure):
     _fields_ = [("hashed", C.c_int), ("dense", VolumeParams), ("hash", HashParams), ("k", Intrinsics),
                 ("icp", IcpCfg), ("rc", RaycastCfg), ("h", C.c_double), ("n_dirs", C.c_int),
-                ("dirs", C.c_int * CSF_MAX_DIRECTIONS), ("objective", C.c_int), ("max_frames", C.c_int)]
+                ("dirs", C.c_int * CSF_MAX_DIRECTIONS), ("objective", C.c_int), ("max_frames", C.c_int),
+                ("order", C.c_int), ("n_pairs", C.c_int), ("pair_i", C.c_int * CSF_MAX_PAIRS),
+                ("pair_j", C.c_int * CSF_MAX_PAIRS)]
 
 
 def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
@@ -103,6 +107,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_pipeline_upload": (ip, [vp, fp, dp, ip]),
         "csf_pipeline_run": (ip, [vp, ip]),
         "csf_pipeline_result": (ip, [vp, dp, dp, dp, i32p]),
+        "csf_pipeline_hessian": (ip, [vp, dp, dp, dp, dp, dp, i32p]),
         "csf_pipeline_run_host": (ip, [vp, fp, dp, ip, dp, dp]),
         "csf_synth_workload": (ip, [vp, ip, ip, ip, ip, fp, dp, C.POINTER(Intrinsics)]),
         "csf_default_intrinsics": (None, [C.POINTER(Intrinsics)]),

@@ -139,7 +139,7 @@ struct DevBuf {
 struct csf_volume_s {
   csf_ctx ctx = nullptr;
   bool hashed = false;
-  int D = 0, G = 0, Dp = 0;
+  int D = 0, G = 0, Dp = 0, order = 1;
   DenseDev dense{};
   HashDev hash{};
   long long n_vox = 0;  // dense voxel count / pool voxel capacity
@@ -213,12 +213,24 @@ int ensure_alloc_scratch(csf_volume v, int w, int h) {
   return CSF_OK;
 }
 
-int volume_init_common(csf_volume v, int n_channels) {
+// order 1: n_channels first-order directions, grouped by pick_group.
+// order 2: n_channels = 3 * pairs bicomplex slots, one pair per group.
+int volume_init_common(csf_volume v, int n_channels, int order) {
+  if (order == 2) {
+    if (n_channels <= 0 || n_channels % 3 != 0 || n_channels > 3 * CSF_MAX_PAIRS)
+      return fail(v->ctx, CSF_EINVAL, "second-order volumes carry 3 slots per pair, 1..CSF_MAX_PAIRS pairs");
+    v->D = n_channels;
+    v->G = 3;
+    v->Dp = n_channels;
+    v->order = 2;
+    return CSF_OK;
+  }
   if (n_channels < 0 || n_channels > CSF_MAX_DIRECTIONS)
     return fail(v->ctx, CSF_EINVAL, "channel count must be in [0, " + std::to_string(CSF_MAX_DIRECTIONS) + "]");
   v->D = n_channels;
   v->G = pick_group(n_channels);
   v->Dp = padded_channels(n_channels, v->G);
+  v->order = 1;
   return CSF_OK;
 }
 
@@ -441,7 +453,7 @@ extern "C" int csf_measure_surface(csf_ctx ctx, const double* depth, int w, int 
 // ---------------------------------------------------------------------------
 // volumes
 // ---------------------------------------------------------------------------
-extern "C" int csf_volume_create_dense(csf_ctx ctx, const csf_volume_params* p, int n_channels, csf_volume* out) {
+static int create_dense(csf_ctx ctx, const csf_volume_params* p, int n_channels, int order, csf_volume* out) {
   if (!ctx || !p || !out) return CSF_EINVAL;
   *out = nullptr;
   if (p->dims[0] <= 0 || p->dims[1] <= 0 || p->dims[2] <= 0 || !(p->voxel_size > 0.0))
@@ -449,7 +461,7 @@ extern "C" int csf_volume_create_dense(csf_ctx ctx, const csf_volume_params* p, 
   cudaSetDevice(ctx->device);
   csf_volume v = new csf_volume_s();
   v->ctx = ctx;
-  int rc = volume_init_common(v, n_channels);
+  int rc = volume_init_common(v, n_channels, order);
   if (rc) {
     delete v;
     return rc;
@@ -467,6 +479,7 @@ extern "C" int csf_volume_create_dense(csf_ctx ctx, const csf_volume_params* p, 
   d.ox = p->origin[0]; d.oy = p->origin[1]; d.oz = p->origin[2];
   d.mu = p->mu;
   d.cap = p->weight_cap;
+  d.order = v->order;
   launch_init_volume(launch_of(ctx), d.rw, d.fim, v->n_vox, v->Dp);
   rc = sync_check(ctx, "csf_volume_create_dense");
   if (rc) {
@@ -477,7 +490,7 @@ extern "C" int csf_volume_create_dense(csf_ctx ctx, const csf_volume_params* p, 
   return CSF_OK;
 }
 
-extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, csf_volume* out) {
+static int create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, int order, csf_volume* out) {
   if (!ctx || !p || !out) return CSF_EINVAL;
   *out = nullptr;
   if (!(p->voxel_size > 0.0) || p->bucket_bits < 4 || p->bucket_bits > 28 || p->max_blocks <= 0)
@@ -486,7 +499,7 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   csf_volume v = new csf_volume_s();
   v->ctx = ctx;
   v->hashed = true;
-  int rc = volume_init_common(v, n_channels);
+  int rc = volume_init_common(v, n_channels, order);
   if (rc) {
     delete v;
     return rc;
@@ -525,6 +538,7 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   d.ox = p->origin[0]; d.oy = p->origin[1]; d.oz = p->origin[2];
   d.mu = p->mu;
   d.cap = p->weight_cap;
+  d.order = v->order;
   cudaMemsetAsync(d.heads, 0xFF, sizeof(int) * nb, ctx->stream);
   cudaMemsetAsync(d.next, 0xFF, sizeof(int) * p->max_blocks, ctx->stream);
   cudaMemsetAsync(d.n_blocks, 0, sizeof(int), ctx->stream);
@@ -538,6 +552,13 @@ extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, i
   }
   *out = v;
   return CSF_OK;
+}
+
+extern "C" int csf_volume_create_dense(csf_ctx ctx, const csf_volume_params* p, int n_channels, csf_volume* out) {
+  return create_dense(ctx, p, n_channels, 1, out);
+}
+extern "C" int csf_volume_create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, csf_volume* out) {
+  return create_hashed(ctx, p, n_channels, 1, out);
 }
 
 extern "C" int csf_volume_destroy(csf_volume vol) {
@@ -695,12 +716,13 @@ struct csf_pipeline_s {
   csf_pipeline_cfg cfg{};
   csf_volume vol = nullptr;
   int D = 0, G = 0, Dp = 0, C = 1;
+  int order = 1, n_pairs = 0;
   int W = 0, H = 0, levels = 3;
   int n_uploaded = 0, n_run = 0;
   DevBuf<float> frames;
   DevBuf<double> gt, raw, pyr0, pyr1, pyr2, vre, nre, vim, nim, partials, pose, pred_pose, intr_levels, traj, kbase,
-      out;
-  DevBuf<int> counts, stats, dirs;
+      out, stage;
+  DevBuf<int> counts, stats, dirs, pair_i, pair_j;
   DevBuf<TrackState> st;
   DevBuf<double2> hits;
   ~csf_pipeline_s() {
@@ -708,7 +730,7 @@ struct csf_pipeline_s {
     frames.release(); gt.release(); raw.release(); pyr0.release(); pyr1.release(); pyr2.release(); vre.release();
     nre.release(); vim.release(); nim.release(); partials.release(); pose.release(); pred_pose.release();
     intr_levels.release(); traj.release(); kbase.release(); out.release(); counts.release(); stats.release();
-    dirs.release(); st.release();
+    dirs.release(); st.release(); stage.release(); pair_i.release(); pair_j.release();
     if (vol) csf_volume_destroy(vol);
   }
 };
@@ -716,12 +738,21 @@ struct csf_pipeline_s {
 extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf_pipeline* out) {
   if (!ctx || !cfg || !out) return CSF_EINVAL;
   *out = nullptr;
+  const int order = cfg->order == 0 ? 1 : cfg->order;
+  if (order != 1 && order != 2) return fail(ctx, CSF_EINVAL, "csf_pipeline_create: order must be 1 or 2");
   if (cfg->n_dirs < 0 || cfg->n_dirs > CSF_MAX_DIRECTIONS)
     return fail(ctx, CSF_EINVAL, "csf_pipeline_create: n_dirs out of range");
   if (!(cfg->h > 0.0) || cfg->h > 1e-6)
     return fail(ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
   for (int d = 0; d < cfg->n_dirs; ++d)
     if (cfg->dirs[d] < 0 || cfg->dirs[d] > 9) return fail(ctx, CSF_EINVAL, "csf_pipeline_create: unknown direction");
+  if (order == 2) {
+    if (cfg->n_pairs <= 0 || cfg->n_pairs > CSF_MAX_PAIRS || cfg->n_dirs != 0)
+      return fail(ctx, CSF_EINVAL, "csf_pipeline_create: order 2 needs 1..CSF_MAX_PAIRS pairs and no dirs");
+    for (int q = 0; q < cfg->n_pairs; ++q)
+      if (cfg->pair_i[q] < 0 || cfg->pair_i[q] > 9 || cfg->pair_j[q] < 0 || cfg->pair_j[q] > 9)
+        return fail(ctx, CSF_EINVAL, "csf_pipeline_create: unknown pair parameter");
+  }
   if (cfg->icp.solver != CSF_SOLVER_LINEARIZED)
     return fail(ctx, CSF_EINVAL, "csf_pipeline_create: the lifted tracker implements the linearized solver");
   if (cfg->icp.levels < 1 || cfg->icp.levels > 3 || cfg->max_frames <= 0 || cfg->k.width <= 0 || cfg->k.height <= 0)
@@ -730,13 +761,16 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   csf_pipeline p = new csf_pipeline_s();
   p->ctx = ctx;
   p->cfg = *cfg;
-  int rc = cfg->hashed ? csf_volume_create_hashed(ctx, &cfg->hash, cfg->n_dirs, &p->vol)
-                       : csf_volume_create_dense(ctx, &cfg->dense, cfg->n_dirs, &p->vol);
+  const int slots = order == 2 ? 3 * cfg->n_pairs : cfg->n_dirs;
+  int rc = cfg->hashed ? create_hashed(ctx, &cfg->hash, slots, order, &p->vol)
+                       : create_dense(ctx, &cfg->dense, slots, order, &p->vol);
   if (rc) {
     delete p;
     return rc;
   }
-  p->D = cfg->n_dirs;
+  p->order = order;
+  p->n_pairs = order == 2 ? cfg->n_pairs : 0;
+  p->D = slots;
   p->G = p->vol->G;
   p->Dp = p->vol->Dp;
   p->C = 1 + p->Dp;
@@ -769,7 +803,10 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   A(p->stats.alloc(8 * static_cast<size_t>(cfg->max_frames)));
   A(p->dirs.alloc(CSF_MAX_DIRECTIONS));
   A(p->kbase.alloc(4));
-  A(p->out.alloc(2 + CSF_MAX_DIRECTIONS));
+  A(p->out.alloc(2 + std::max(CSF_MAX_DIRECTIONS, 3 * CSF_MAX_PAIRS)));
+  A(p->stage.alloc(16));
+  A(p->pair_i.alloc(CSF_MAX_PAIRS));
+  A(p->pair_j.alloc(CSF_MAX_PAIRS));
   A(p->st.alloc(1));
   A(p->hits.alloc(2 * P));
   if (e != cudaSuccess) {
@@ -786,6 +823,8 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   const double kb[4] = {cfg->k.fx, cfg->k.fy, cfg->k.cx, cfg->k.cy};
   cudaMemcpy(p->kbase.p, kb, sizeof(kb), cudaMemcpyHostToDevice);
   cudaMemcpy(p->dirs.p, cfg->dirs, sizeof(int) * CSF_MAX_DIRECTIONS, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->pair_i.p, cfg->pair_i, sizeof(int) * CSF_MAX_PAIRS, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->pair_j.p, cfg->pair_j, sizeof(int) * CSF_MAX_PAIRS, cudaMemcpyHostToDevice);
   cudaMemset(p->st.p, 0, sizeof(TrackState));
   *out = p;
   return CSF_OK;
@@ -852,7 +891,11 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
   const int* nblk = v->hashed ? v->hash.n_blocks : nullptr;
   const int* counters = v->hashed ? v->alloc.counters : nullptr;
 
-  launch_seed(L, p->G, p->Dp, p->dirs.p, p->D, cfg.h, p->gt.p, p->kbase.p, p->pose.p, p->intr_levels.p, p->levels);
+  if (p->order == 2)
+    launch_seed2(L, p->Dp, p->pair_i.p, p->pair_j.p, p->n_pairs, cfg.h, p->gt.p, p->kbase.p, p->pose.p,
+                 p->intr_levels.p, p->levels);
+  else
+    launch_seed(L, p->G, p->Dp, p->dirs.p, p->D, cfg.h, p->gt.p, p->kbase.p, p->pose.p, p->intr_levels.p, p->levels);
   launch_frame_begin(L, st, 0);
   launch_bilateral(L, p->frames.p, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
   int* upd = &st->pad[1];
@@ -881,9 +924,14 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
       const int tiles = icp_tiles(wl, hl, stride);
       for (int it = 0; it < cfg.icp.level_iterations[li]; ++it) {
         PROF(ctx, kPIcpReduce);
-        launch_icp_reduce(L, p->G, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p,
-                          p->vim.p, p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p, level,
-                          cfg.icp.step_tolerance);
+        if (p->order == 2)
+          launch_icp_iteration2(L, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p,
+                                p->vim.p, p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p, p->stage.p,
+                                level, cfg.icp.step_tolerance);
+        else
+          launch_icp_reduce(L, p->G, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p,
+                            p->vim.p, p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p, level,
+                            cfg.icp.step_tolerance);
         (void)tiles;
       }
     }
@@ -891,7 +939,10 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
     if (rc) return rc;
     launch_frame_end(L, st, p->pose.p, p->traj.p, p->Dp, p->stats.p, nblk, counters);
   }
-  launch_objective(L, p->G, p->Dp, p->D, p->traj.p, p->gt.p, n_frames, cfg.objective, cfg.h, p->out.p);
+  if (p->order == 2)
+    launch_objective2(L, p->Dp, p->n_pairs, p->traj.p, p->gt.p, n_frames, cfg.objective, p->out.p);
+  else
+    launch_objective(L, p->G, p->Dp, p->D, p->traj.p, p->gt.p, n_frames, cfg.objective, cfg.h, p->out.p);
   p->n_run = n_frames;
   CUDA_TRY(ctx, cudaGetLastError());
   return CSF_OK;
@@ -904,11 +955,16 @@ extern "C" int csf_pipeline_result(csf_pipeline p, double* gradient, double* obj
   cudaSetDevice(ctx->device);
   int rc = sync_check(ctx, "csf_pipeline_run");
   if (rc) return rc;
-  std::vector<double> out(2 + CSF_MAX_DIRECTIONS);
+  std::vector<double> out(2 + std::max(CSF_MAX_DIRECTIONS, 3 * CSF_MAX_PAIRS));
   CUDA_TRY(ctx, cudaMemcpy(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
   if (objective) *objective = out[0];
-  if (gradient)
-    for (int d = 0; d < p->D; ++d) gradient[d] = out[2 + d];
+  const double hh = p->cfg.h;
+  if (gradient) {
+    if (p->order == 2)  // the run's derivative: one Hessian entry per pair
+      for (int q = 0; q < p->n_pairs; ++q) gradient[q] = out[2 + 3 * q + 2] / (hh * hh);
+    else
+      for (int d = 0; d < p->D; ++d) gradient[d] = out[2 + d];
+  }
   const int n = p->n_run;
   if (poses) {
     std::vector<double> t(static_cast<size_t>(n) * 12 * p->C);
@@ -920,6 +976,25 @@ extern "C" int csf_pipeline_result(csf_pipeline p, double* gradient, double* obj
           poses[(static_cast<size_t>(f) * 12 + e) * Cu + c] = t[(static_cast<size_t>(f) * 12 + e) * p->C + c];
   }
   if (stats) CUDA_TRY(ctx, cudaMemcpy(stats, p->stats.p, sizeof(int) * 8 * n, cudaMemcpyDeviceToHost));
+  return CSF_OK;
+}
+
+extern "C" int csf_pipeline_hessian(csf_pipeline p, double* hessian, double* grad1, double* grad2, double* objective,
+                                    double* poses, int32_t* stats) {
+  if (!p) return CSF_EINVAL;
+  if (p->order != 2) return fail(p->ctx, CSF_EINVAL, "csf_pipeline_hessian: pipeline was created with order 1");
+  csf_ctx ctx = p->ctx;
+  cudaSetDevice(ctx->device);
+  const int rc = csf_pipeline_result(p, nullptr, objective, poses, stats);
+  if (rc) return rc;
+  std::vector<double> out(2 + 3 * p->n_pairs);
+  CUDA_TRY(ctx, cudaMemcpy(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
+  const double h = p->cfg.h;
+  for (int q = 0; q < p->n_pairs; ++q) {
+    if (hessian) hessian[q] = out[2 + 3 * q + 2] / (h * h);  // extract_hessian, csfd.hpp:319
+    if (grad1) grad1[q] = out[2 + 3 * q] / h;
+    if (grad2) grad2[q] = out[2 + 3 * q + 1] / h;
+  }
   return CSF_OK;
 }
 
@@ -996,6 +1071,7 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
   real_view.Dp = 0;  // pose/intrinsics buffers carry the real channel only
   real_view.dense = v->dense;
   real_view.hash = v->hash;
+  real_view.dense.order = real_view.hash.order = 1;
   csf_raycast_cfg rcfg;
   csf_default_raycast_cfg(&rcfg);
   int tiles_last = 0;

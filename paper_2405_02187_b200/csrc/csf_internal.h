@@ -19,6 +19,7 @@ struct DenseDev {
   double* fim;   // [n][Dp]
   int nx, ny, nz;
   double vs, ox, oy, oz, mu, cap;
+  int order = 1;  // CSFD order of the channel slots (2: bicomplex pairs, 3 slots each)
 };
 
 struct HashDev {
@@ -33,6 +34,7 @@ struct HashDev {
   unsigned* occ;                // [2^(3*(gbits-3))/32] super-block occupancy bits
   int bits, max_blocks, gbits;
   double vs, ox, oy, oz, mu, cap;
+  int order = 1;  // CSFD order of the channel slots (2: bicomplex pairs, 3 slots each)
 };
 
 // Per-frame allocation scratch (hashed volumes).
@@ -116,6 +118,17 @@ void launch_frame_end(const Launch& L, TrackState* st, const double* pose, doubl
                       const int* n_blocks, const int* counters);
 void launch_objective(const Launch& L, int G, int Dp, int D, const double* traj, const double* gt, int n_frames,
                       int kind, double h, double* out /*[2 + D]: objective re, pad, grad*/);
+// Second order (channel groups = bicomplex pairs, 3 slots each): one ICP
+// iteration = reduce (tiles x pairs) + per-pair solve + commit; stage [16].
+void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double* depth, int w, int h, int stride,
+                           const double* intr, double* pose, const double* vre, const double* nre, const double* vim,
+                           const double* nim, double d_max, double cos_max, double* partials, int* counts,
+                           double* stage, int level, double tol);
+void launch_seed2(const Launch& L, int Dp, const int* pair_i, const int* pair_j, int n_pairs, double h,
+                  const double* gt0, const double* intr_base, double* pose, double* intr_levels, int levels);
+// out [2 + Dp]: objective re, pad, then the raw slots (im1, im2, im12) per pair
+void launch_objective2(const Launch& L, int Dp, int n_pairs, const double* traj, const double* gt, int n_frames,
+                       int kind, double* out);
 void launch_linearized_corrs(const Launch& L, const double* corrs, int n, const double* base, double* partials,
                              int* counts);
 

@@ -163,6 +163,18 @@ CSF_DEV bool sample_tsdf(const V& vol, const V3<S>& p, int g0, S* out, typename 
       accum = accum + ((wx * wy) * wz) * rw[c].x;
     }
     *out = accum;
+  } else if constexpr (Traits<S>::kOrder == 2) {
+    // Second order: the reference's lifted accumulation, operation for
+    // operation in Bicomplex arithmetic (no tangent shortcut at order 2).
+    S accum = lit<S>(0.0);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const S wx = (c & 1) ? fx : 1.0 - fx;
+      const S wy = ((c >> 1) & 1) ? fy : 1.0 - fy;
+      const S wz = (c >> 2) ? fz : 1.0 - fz;
+      accum = accum + ((wx * wy) * wz) * field_at<S>(vol.vox, v[c], rw[c].x, g0);
+    }
+    *out = accum;
   } else {
     // Real channel: the reference's accumulation (bit-identical).  Channels:
     // the interpolant is linear in the corner values and trilinear in the

@@ -65,6 +65,47 @@ CSF_DEV bool vertex_at(const double* depth, int w, int x, int y, double fx, doub
   return true;
 }
 
+// associate (icp.cpp:89-126) for one strided slot (x, y): the measured
+// vertex/normal recomputed from the pyramid depth (measure_surface), the
+// real-part gates in the reference's order (z > 0, bounds, model normal
+// valid, distance, angle) and the lround pixel pick.  Returns true for a
+// correspondence with model pixel (u, v).
+CSF_DEV bool associate_slot(const double* __restrict__ depth, int w, int h, int x, int y, double fx, double fy,
+                            double cx, double cy, const Pose<double>& c2w, const Pose<double>& w2p,
+                            const double* __restrict__ vre, const double* __restrict__ nre, double d_max,
+                            double cos_max, int* u_out, int* v_out) {
+  V3<double> vert, vx, vy;
+  if (!(vertex_at(depth, w, x, y, fx, fy, cx, cy, &vert) && x + 1 < w && y + 1 < h &&
+        vertex_at(depth, w, x + 1, y, fx, fy, cx, cy, &vx) && vertex_at(depth, w, x, y + 1, fx, fy, cx, cy, &vy)))
+    return false;
+  V3<double> n = cross3(sub3(vx, vert), sub3(vy, vert));
+  const double len2 = dot3(n, n);
+  if (!(len2 > 0.0)) return false;
+  const double l = sqrt(len2);
+  n = mk3<double>(n.v[0] / l, n.v[1] / l, n.v[2] / l);
+  if (dot3(n, vert) > 0.0) n = mk3<double>(-n.v[0], -n.v[1], -n.v[2]);
+  if (!(dot3(n, n) > 0.5)) return false;
+  const V3<double> world = apply(c2w, vert);
+  const V3<double> inp = apply(w2p, world);
+  if (!(inp.v[2] > 0.0)) return false;
+  const double uvx = (fx * inp.v[0]) / inp.v[2] + cx;
+  const double uvy = (fy * inp.v[1]) / inp.v[2] + cy;
+  const int u = static_cast<int>(lround(uvx));
+  const int v = static_cast<int>(lround(uvy));
+  if (!(u >= 0 && u < w && v >= 0 && v < h)) return false;
+  const long long m = static_cast<long long>(v) * w + u;
+  const V3<double> mn = mk3<double>(nre[3 * m], nre[3 * m + 1], nre[3 * m + 2]);
+  if (!(dot3(mn, mn) > 0.5)) return false;
+  const V3<double> mv = mk3<double>(vre[3 * m], vre[3 * m + 1], vre[3 * m + 2]);
+  const V3<double> dd = sub3(world, mv);
+  if (sqrt(dot3(dd, dd)) > d_max) return false;
+  const V3<double> wn = matvec(c2w.R, n);
+  if (dot3(wn, mn) < cos_max) return false;
+  *u_out = u;
+  *v_out = v;
+  return true;
+}
+
 // The solve of one ICP iteration, run by one CTA of >= 64 threads: sum the
 // tile partials in tile order, then one thread per channel group factors the
 // lifted 6x6 system, applies exp(delta) * T and writes the break decisions.
@@ -221,39 +262,7 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
     if (threadIdx.x < chunk && slot < n_slots) {
       x = (slot % nxs) * stride;
       y = (slot / nxs) * stride;
-      V3<double> vert, vx, vy;
-      if (vertex_at(depth, w, x, y, fx, fy, cx, cy, &vert) && x + 1 < w && y + 1 < h &&
-          vertex_at(depth, w, x + 1, y, fx, fy, cx, cy, &vx) && vertex_at(depth, w, x, y + 1, fx, fy, cx, cy, &vy)) {
-        V3<double> n = cross3(sub3(vx, vert), sub3(vy, vert));
-        const double len2 = dot3(n, n);
-        if (len2 > 0.0) {
-          const double l = sqrt(len2);
-          n = mk3<double>(n.v[0] / l, n.v[1] / l, n.v[2] / l);
-          if (dot3(n, vert) > 0.0) n = mk3<double>(-n.v[0], -n.v[1], -n.v[2]);
-          if (dot3(n, n) > 0.5) {
-            const V3<double> world = apply(c2w, vert);
-            const V3<double> inp = apply(w2p, world);
-            if (inp.v[2] > 0.0) {
-              const double uvx = (fx * inp.v[0]) / inp.v[2] + cx;
-              const double uvy = (fy * inp.v[1]) / inp.v[2] + cy;
-              u = static_cast<int>(lround(uvx));
-              v = static_cast<int>(lround(uvy));
-              if (u >= 0 && u < w && v >= 0 && v < h) {
-                const long long m = static_cast<long long>(v) * w + u;
-                const V3<double> mn = mk3<double>(nre[3 * m], nre[3 * m + 1], nre[3 * m + 2]);
-                if (dot3(mn, mn) > 0.5) {
-                  const V3<double> mv = mk3<double>(vre[3 * m], vre[3 * m + 1], vre[3 * m + 2]);
-                  const V3<double> dd = sub3(world, mv);
-                  if (!(sqrt(dot3(dd, dd)) > d_max)) {
-                    const V3<double> wn = matvec(c2w.R, n);
-                    corr = !(dot3(wn, mn) < cos_max);
-                  }
-                }
-              }
-            }
-          }
-        }
-      }
+      corr = associate_slot(depth, w, h, x, y, fx, fy, cx, cy, c2w, w2p, vre, nre, d_max, cos_max, &u, &v);
     }
     // order-preserving compaction within the chunk
     const unsigned ballot = __ballot_sync(0xffffffffu, corr);
@@ -513,6 +522,286 @@ __global__ void k_objective(const double* __restrict__ traj, const double* __res
   }
 }
 
+// ============================================================================
+// Second order (pipeline order 2): channel groups are bicomplex pairs, S =
+// B<1> (re + im1, im2, im12).  Association is the first-order kernel's
+// (associate_slot, real parts); the J/r rows and the normal-equation sums are
+// evaluated generically in S, i.e. with the reference's Bicomplex product
+// (the oracle's jacobian_row/accumulate_row, orc_icp.hpp) — no tangent
+// shortcut exists at order 2.  One ICP iteration is three launches:
+//   k_icp_reduce2  grid (tiles, pairs): per-tile partial sums of one pair's
+//                  slots (pair 0 also writes the real channel and counts)
+//   k_icp_solve2   one CTA per pair: tile partials in tile order, the 6x6
+//                  LDLT/exp map in S; writes its pair's pose slots and (pair 0)
+//                  the real step to `stage`
+//   k_icp_commit   real pose + break decisions (TrackState)
+// ============================================================================
+constexpr int kTile2 = 256;
+
+template <typename S>
+__global__ void __launch_bounds__(256) k_icp_reduce2(const TrackState* st, const double* __restrict__ depth, int w,
+                                                     int h, int stride, const double* __restrict__ intr,
+                                                     const double* __restrict__ pose, const double* __restrict__ vre,
+                                                     const double* __restrict__ nre, const double* __restrict__ vim,
+                                                     const double* __restrict__ nim, double d_max, double cos_max,
+                                                     int Dp, double* __restrict__ partials, int* __restrict__ counts) {
+  if (st->level_done) return;
+  constexpr int G = Traits<S>::G;
+  constexpr int CG = 1 + G;
+  const int C = 1 + Dp;
+  const int g0 = blockIdx.y * G;
+  extern __shared__ double sm[];
+  S* rows = reinterpret_cast<S*>(sm);  // [kTile2][7]
+  __shared__ int s_wsum[8];
+  Pose<double> c2w, w2p;
+  load_pose_real(pose, C, &c2w);
+#pragma unroll
+  for (int e = 0; e < 9; ++e) w2p.R.m[e] = st->pred_w2c[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) w2p.t.v[e] = st->pred_w2c[9 + e];
+  const double fx = intr[0], fy = intr[C], cx = intr[2 * C], cy = intr[3 * C];
+  const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
+  const int n_slots = nxs * nys;
+  const int slot = blockIdx.x * kTile2 + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = 0, y = 0, u = 0, v = 0;
+  bool corr = false;
+  if (slot < n_slots) {
+    x = (slot % nxs) * stride;
+    y = (slot / nxs) * stride;
+    corr = associate_slot(depth, w, h, x, y, fx, fy, cx, cy, c2w, w2p, vre, nre, d_max, cos_max, &u, &v);
+  }
+  const unsigned ballot = __ballot_sync(0xffffffffu, corr);
+  if (lane == 0) s_wsum[warp] = __popc(ballot);
+  __syncthreads();
+  int before = 0, total = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (k < warp) before += s_wsum[k];
+    total += s_wsum[k];
+  }
+  if (corr) {
+    const int pos = before + __popc(ballot & ((1u << lane) - 1u));
+    // jacobian_row (icp.cpp:20-24): vertex = backproject(K, x, y, d) in S
+    // (frames.hpp:38-41), p = base * vertex, r = (p - mv) . mn, J = [mn; p x mn]
+    const double d = depth[y * w + x];
+    const S kfx = load_ch<S>(intr, g0, G), kfy = load_ch<S>(intr + C, g0, G);
+    const S kcx = load_ch<S>(intr + 2 * C, g0, G), kcy = load_ch<S>(intr + 3 * C, g0, G);
+    const V3<S> vert = mk3<S>((d * (static_cast<double>(x) - kcx)) / kfx, (d * (static_cast<double>(y) - kcy)) / kfy,
+                              lit<S>(d));
+    Pose<S> base;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) base.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) base.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
+    const long long m = static_cast<long long>(v) * w + u;
+    V3<S> mv, mn;
+#pragma unroll
+    for (int c3 = 0; c3 < 3; ++c3) {
+      mv.v[c3].re = vre[3 * m + c3];
+      mn.v[c3].re = nre[3 * m + c3];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        mv.v[c3].im[g] = vim[(3 * m + c3) * Dp + g0 + g];
+        mn.v[c3].im[g] = nim[(3 * m + c3) * Dp + g0 + g];
+      }
+    }
+    const V3<S> pw = apply(base, vert);
+    const S r = dot3(sub3(pw, mv), mn);
+    const V3<S> pn = cross3(pw, mn);
+    S* row = rows + 7 * pos;
+    row[0] = mn.v[0]; row[1] = mn.v[1]; row[2] = mn.v[2];
+    row[3] = pn.v[0]; row[4] = pn.v[1]; row[5] = pn.v[2];
+    row[6] = r;
+  }
+  __syncthreads();
+  // accumulate_row (orc_icp.hpp): one thread per (accumulator, slot), the
+  // S product of the two row entries, summed in slot order within the tile
+  const int a = threadIdx.x;
+  if (a < 27 * CG) {
+    const int q = a / CG, c = a % CG;
+    int ja, jb;
+    if (q < 21) {
+      ja = c_tri_r[q];
+      jb = c_tri_c[q];
+    } else {
+      ja = q - 21;
+      jb = 6;
+    }
+    double acc = 0.0;
+    for (int e = 0; e < total; ++e) {
+      const S prod = rows[7 * e + ja] * rows[7 * e + jb];
+      acc = acc + (c == 0 ? prod.re : prod.im[c - 1]);
+    }
+    if (c == 0) {
+      if (blockIdx.y == 0) partials[static_cast<long long>(blockIdx.x) * 27 * C + q * C] = acc;
+    } else {
+      partials[static_cast<long long>(blockIdx.x) * 27 * C + q * C + g0 + c] = acc;
+    }
+  }
+  if (threadIdx.x == 0 && blockIdx.y == 0) counts[blockIdx.x] = total;
+}
+
+// stage: [0..11] new real pose, [12] |delta.re|, [13] correspondence count,
+// [14] 1 if the step was applied
+template <typename S>
+__global__ void __launch_bounds__(128) k_icp_solve2(const TrackState* st, const double* __restrict__ partials,
+                                                    const int* __restrict__ counts, int n_tiles, double* pose, int Dp,
+                                                    double* stage) {
+  if (st->level_done) return;
+  constexpr int G = Traits<S>::G;
+  constexpr int CG = 1 + G;
+  const int C = 1 + Dp;
+  const int g0 = blockIdx.x * G;
+  __shared__ double s_acc[27 * CG];
+  __shared__ int s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  for (int a = threadIdx.x; a < 27 * CG; a += blockDim.x) {
+    const int q = a / CG, c = a % CG;
+    const long long off = static_cast<long long>(q) * C + (c == 0 ? 0 : g0 + c);
+    double total = 0.0;
+    for (int t = 0; t < n_tiles; t += 32) {
+      double vals[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        vals[k] = t + k < n_tiles ? __ldcg(partials + static_cast<long long>(t + k) * 27 * C + off) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (t + k < n_tiles) total = total + vals[k];
+    }
+    s_acc[a] = total;
+  }
+  __syncthreads();
+  {
+    int part = 0;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) part += __ldcg(counts + t);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0 && part) atomicAdd(&s_n, part);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int n = s_n;
+  if (blockIdx.x == 0) {
+    stage[13] = static_cast<double>(n);
+    stage[14] = 0.0;
+  }
+  if (n < 12) return;
+  S a[21], nb[6], d[6];
+#pragma unroll
+  for (int q = 0; q < 21; ++q) a[q] = load_ch<S>(s_acc + q * CG, 0, G);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) nb[i] = -load_ch<S>(s_acc + (21 + i) * CG, 0, G);
+  ldlt6_solve_reg<S>(a, nb, d);
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) fin = fin && finite_s(d[i]);
+  if (!fin)
+#pragma unroll
+    for (int i = 0; i < 6; ++i) d[i] = lit<S>(0.0);
+  Pose<S> cur;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+#pragma unroll
+  for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
+  const Pose<S> np = compose(exp_map<S>(d), cur);
+  // this pair's slots now; the real channel is committed by k_icp_commit
+#pragma unroll
+  for (int e = 0; e < 9; ++e) store_ch<S>(pose + e * C, np.R.m[e], g0, G, false);
+#pragma unroll
+  for (int e = 0; e < 3; ++e) store_ch<S>(pose + (9 + e) * C, np.t.v[e], g0, G, false);
+  if (blockIdx.x == 0) {
+#pragma unroll
+    for (int e = 0; e < 9; ++e) stage[e] = re(np.R.m[e]);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) stage[9 + e] = re(np.t.v[e]);
+    double sq[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) sq[i] = re(d[i]) * re(d[i]);
+    stage[12] = sqrt((sq[0] + (sq[1] + sq[2])) + (sq[3] + (sq[4] + sq[5])));
+    stage[14] = 1.0;
+  }
+}
+
+__global__ void k_icp_commit(TrackState* st, double* pose, int Dp, const double* __restrict__ stage, int level,
+                             double tol) {
+  if (st->level_done) return;
+  const int C = 1 + Dp;
+  const int n = static_cast<int>(stage[13]);
+  if (stage[14] == 0.0) {  // fewer than 12 correspondences: break before the step (icp.cpp:199)
+    st->n_corr = n;
+    st->level_done = 1;
+    return;
+  }
+  for (int e = 0; e < 12; ++e) pose[e * C] = stage[e];
+  st->iterations += 1;
+  st->n_corr = n;
+  if (stage[12] < tol) {
+    st->level_done = 1;
+    if (level == 0) st->converged = 1;
+  }
+}
+
+// Seeds of a second-order run: pair p carries im1 on parameter pair_i[p] and
+// im2 on pair_j[p] (promote2, csfd.hpp:303-307).
+template <typename S>
+__global__ void k_seed2(const int* __restrict__ pair_i, const int* __restrict__ pair_j, int n_pairs, double hstep,
+                        const double* __restrict__ gt0, const double* __restrict__ kbase, double* pose,
+                        double* intr_levels, int levels, int Dp) {
+  constexpr int G = Traits<S>::G;
+  const int C = 1 + Dp;
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= Dp / G) return;
+  const int g0 = gi * G;
+  S xi[6], kk[4];
+  for (int i = 0; i < 6; ++i) xi[i] = lit<S>(0.0);
+  for (int i = 0; i < 4; ++i) kk[i] = lit<S>(kbase[i]);
+  if (gi < n_pairs) {
+    const int pi = pair_i[gi], pj = pair_j[gi];
+    if (pi < 6) xi[pi].im[0] = hstep; else kk[pi - 6].im[0] = hstep;
+    if (pj < 6) xi[pj].im[1] = hstep; else kk[pj - 6].im[1] = hstep;
+  }
+  Pose<S> base;
+  for (int e = 0; e < 9; ++e) base.R.m[e] = lit<S>(gt0[e]);
+  for (int e = 0; e < 3; ++e) base.t.v[e] = lit<S>(gt0[9 + e]);
+  const Pose<S> p = compose(exp_map<S>(xi), base);
+  for (int e = 0; e < 9; ++e) store_ch<S>(pose + e * C, p.R.m[e], g0, G, gi == 0);
+  for (int e = 0; e < 3; ++e) store_ch<S>(pose + (9 + e) * C, p.t.v[e], g0, G, gi == 0);
+  for (int l = 0; l < levels; ++l) {
+    const double sc = static_cast<double>(1 << l);
+    for (int i = 0; i < 4; ++i) store_ch<S>(intr_levels + (l * 4 + i) * C, kk[i] / sc, g0, G, gi == 0);
+  }
+}
+
+// Objective in S per pair; out[0] = re, out[2 + 3p + t] = slot t of pair p.
+template <typename S>
+__global__ void k_objective2(const double* __restrict__ traj, const double* __restrict__ gt, int n_frames, int kind,
+                             int Dp, int n_pairs, double* out) {
+  constexpr int G = Traits<S>::G;
+  const int C = 1 + Dp;
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= n_pairs) return;
+  const int g0 = gi * G;
+  auto diff_at = [&](int f) {
+    V3<S> t;
+    for (int e = 0; e < 3; ++e)
+      t.v[e] = load_ch<S>(traj + (static_cast<long long>(f) * 12 + 9 + e) * C, g0, G) - gt[f * 12 + 9 + e];
+    return t;
+  };
+  S obj = lit<S>(0.0);
+  if (kind == 0) {
+    const V3<S> d = diff_at(n_frames - 1);
+    obj = sqrt_s(dot3(d, d));
+  } else {
+    for (int f = 0; f < n_frames; ++f) {
+      const V3<S> d = diff_at(f);
+      obj = obj + dot3(d, d);
+    }
+  }
+  if (gi == 0) out[0] = re(obj);
+  for (int g = 0; g < G; ++g) out[2 + g0 + g] = obj.im[g];
+}
+
 }  // namespace csfd
 
 // ============================================================================
@@ -644,6 +933,44 @@ void launch_objective(const Launch& L, int G, int Dp, int D, const double* traj,
     k_objective<1><<<1, 64, 0, L.stream>>>(traj, gt, n_frames, kind, h, Dp, D, out);
   ++*L.launches;
   chk("objective");
+}
+
+// ---- second order ----------------------------------------------------------
+void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double* depth, int w, int h, int stride,
+                           const double* intr, double* pose, const double* vre, const double* nre, const double* vim,
+                           const double* nim, double d_max, double cos_max, double* partials, int* counts,
+                           double* stage, int level, double tol) {
+  using S = B<1>;
+  const int tiles = icp_tiles(w, h, stride);
+  const int pairs = Dp / 3;
+  const size_t smem = sizeof(S) * kTile2 * 7;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_icp_reduce2<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  k_icp_reduce2<S><<<dim3(tiles, pairs), kTile2, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim,
+                                                                   nim, d_max, cos_max, Dp, partials, counts);
+  k_icp_solve2<S><<<pairs, 128, 0, L.stream>>>(st, partials, counts, tiles, pose, Dp, stage);
+  k_icp_commit<<<1, 1, 0, L.stream>>>(st, pose, Dp, stage, level, tol);
+  *L.launches += 3;
+  chk("icp_iteration2");
+}
+
+void launch_seed2(const Launch& L, int Dp, const int* pair_i, const int* pair_j, int n_pairs, double h,
+                  const double* gt0, const double* intr_base, double* pose, double* intr_levels, int levels) {
+  const int groups = Dp / 3;
+  k_seed2<B<1>><<<(groups + 63) / 64, 64, 0, L.stream>>>(pair_i, pair_j, n_pairs, h, gt0, intr_base, pose,
+                                                         intr_levels, levels, Dp);
+  ++*L.launches;
+  chk("seed2");
+}
+
+void launch_objective2(const Launch& L, int Dp, int n_pairs, const double* traj, const double* gt, int n_frames,
+                       int kind, double* out) {
+  k_objective2<B<1>><<<(n_pairs + 63) / 64, 64, 0, L.stream>>>(traj, gt, n_frames, kind, Dp, n_pairs, out);
+  ++*L.launches;
+  chk("objective2");
 }
 
 }  // namespace csfi

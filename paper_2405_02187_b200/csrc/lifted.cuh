@@ -42,12 +42,33 @@ template <int G> struct ScalarOf { using type = L<G>; };
 template <> struct ScalarOf<0> { using type = double; };
 template <int G> using Scal = typename ScalarOf<G>::type;
 
+// ----------------------------------------------------------------------------
+// B<NP>: NP second-order direction pairs sharing one real channel.  Pair p
+// occupies three channel slots (im1, im2, im12) — exactly one reference
+// Bicomplex per pair (csfd.hpp:83-140), so slot 3p+2 of a packed run equals
+// the im12 of a standalone Bicomplex pass seeded on that pair.  Storage
+// follows the first-order layout (element-major, slot-minor), so the voxel
+// store, poses and maps address second-order runs unchanged.
+// ----------------------------------------------------------------------------
+template <int NP>
+struct B {
+  double re;
+  double im[3 * NP];
+};
+
+// G = channel slots per value; kOrder = CSFD order (0 = plain real path).
 template <typename S> struct Traits;
 template <> struct Traits<double> {
   static constexpr int G = 0;
+  static constexpr int kOrder = 0;
 };
 template <int G_> struct Traits<L<G_>> {
   static constexpr int G = G_;
+  static constexpr int kOrder = 1;
+};
+template <int NP> struct Traits<B<NP>> {
+  static constexpr int G = 3 * NP;
+  static constexpr int kOrder = 2;
 };
 
 template <typename S> CSF_DEV S lit(double x);
@@ -179,6 +200,153 @@ template <int G> CSF_DEV L<G> operator/(double c, const L<G>& b) {
   return o;
 }
 
+// -- B<NP> arithmetic: the reference Bicomplex rules (csfd.hpp:103-121) per
+// pair, in the oracle's evaluation order (oracle/orc_core.hpp Bicomplex).
+// Constants enter as Bicomplex(c) with zero slots; the exact-zero terms of the
+// general formulas are dropped.
+template <int NP> CSF_DEV double re(const B<NP>& x) { return x.re; }
+template <int NP> CSF_DEV B<NP> operator+(const B<NP>& a, const B<NP>& b) {
+  B<NP> o;
+  o.re = a.re + b.re;
+#pragma unroll
+  for (int g = 0; g < 3 * NP; ++g) o.im[g] = a.im[g] + b.im[g];
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator-(const B<NP>& a, const B<NP>& b) {
+  B<NP> o;
+  o.re = a.re - b.re;
+#pragma unroll
+  for (int g = 0; g < 3 * NP; ++g) o.im[g] = a.im[g] - b.im[g];
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator-(const B<NP>& a) {
+  B<NP> o;
+  o.re = -a.re;
+#pragma unroll
+  for (int g = 0; g < 3 * NP; ++g) o.im[g] = -a.im[g];
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator*(const B<NP>& a, const B<NP>& b) {
+  B<NP> o;
+  o.re = a.re * b.re;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double a1 = a.im[3 * p], a2 = a.im[3 * p + 1], a12 = a.im[3 * p + 2];
+    const double b1 = b.im[3 * p], b2 = b.im[3 * p + 1], b12 = b.im[3 * p + 2];
+    o.im[3 * p] = a.re * b1 + a1 * b.re;
+    o.im[3 * p + 1] = a.re * b2 + a2 * b.re;
+    o.im[3 * p + 2] = ((a.re * b12 + a12 * b.re) + a1 * b2) + a2 * b1;
+  }
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator/(const B<NP>& a, const B<NP>& b) {
+  B<NP> o;
+  o.re = a.re / b.re;
+  const double den = b.re * b.re;
+  const double inv_den = 1.0 / den;
+  (void)inv_den;
+  const double inv = 1.0 / b.re;
+  const double inv2 = inv * inv;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double a1 = a.im[3 * p], a2 = a.im[3 * p + 1], a12 = a.im[3 * p + 2];
+    const double b1 = b.im[3 * p], b2 = b.im[3 * p + 1], b12 = b.im[3 * p + 2];
+    o.im[3 * p] = CSF_CH_DIV(a1 * b.re - a.re * b1, den, inv_den);
+    o.im[3 * p + 1] = CSF_CH_DIV(a2 * b.re - a.re * b2, den, inv_den);
+    o.im[3 * p + 2] = ((a12 * inv - (a1 * b2 + a2 * b1) * inv2) - (a.re * b12) * inv2) +
+                      ((((2.0 * a.re) * b1) * b2) * inv2) * inv;
+  }
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator+(const B<NP>& a, double c) {
+  B<NP> o = a;
+  o.re = a.re + c;
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator+(double c, const B<NP>& a) {
+  B<NP> o = a;
+  o.re = c + a.re;
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator-(const B<NP>& a, double c) {
+  B<NP> o = a;
+  o.re = a.re - c;
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator-(double c, const B<NP>& a) {
+  B<NP> o;
+  o.re = c - a.re;
+#pragma unroll
+  for (int g = 0; g < 3 * NP; ++g) o.im[g] = -a.im[g];
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator*(const B<NP>& a, double c) {
+  B<NP> o;
+  o.re = a.re * c;
+#pragma unroll
+  for (int g = 0; g < 3 * NP; ++g) o.im[g] = a.im[g] * c;
+  return o;
+}
+template <int NP> CSF_DEV B<NP> operator*(double c, const B<NP>& a) {
+  B<NP> o;
+  o.re = c * a.re;
+#pragma unroll
+  for (int g = 0; g < 3 * NP; ++g) o.im[g] = c * a.im[g];
+  return o;
+}
+// a / Bicomplex(c): im1,2 = (a.im*c)/(c*c), im12 = a.im12 * (1/c)
+template <int NP> CSF_DEV B<NP> operator/(const B<NP>& a, double c) {
+  B<NP> o;
+  o.re = a.re / c;
+  const double den = c * c;
+  const double inv_den = 1.0 / den;
+  (void)inv_den;
+  const double inv = 1.0 / c;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    o.im[3 * p] = CSF_CH_DIV(a.im[3 * p] * c, den, inv_den);
+    o.im[3 * p + 1] = CSF_CH_DIV(a.im[3 * p + 1] * c, den, inv_den);
+    o.im[3 * p + 2] = a.im[3 * p + 2] * inv;
+  }
+  return o;
+}
+// Bicomplex(c) / b
+template <int NP> CSF_DEV B<NP> operator/(double c, const B<NP>& b) {
+  B<NP> o;
+  o.re = c / b.re;
+  const double den = b.re * b.re;
+  const double inv_den = 1.0 / den;
+  (void)inv_den;
+  const double inv = 1.0 / b.re;
+  const double inv2 = inv * inv;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double b1 = b.im[3 * p], b2 = b.im[3 * p + 1], b12 = b.im[3 * p + 2];
+    o.im[3 * p] = CSF_CH_DIV(-(c * b1), den, inv_den);
+    o.im[3 * p + 1] = CSF_CH_DIV(-(c * b2), den, inv_den);
+    o.im[3 * p + 2] = -((c * b12) * inv2) + ((((2.0 * c) * b1) * b2) * inv2) * inv;
+  }
+  return o;
+}
+// lift2 (csfd.hpp:212-263): (f, d1*im1, d1*im2, d1*im12 + d2*im1*im2)
+template <int NP> CSF_DEV B<NP> lift2(const B<NP>& z, double f, double d1, double d2) {
+  B<NP> o;
+  o.re = f;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    o.im[3 * p] = d1 * z.im[3 * p];
+    o.im[3 * p + 1] = d1 * z.im[3 * p + 1];
+    o.im[3 * p + 2] = d1 * z.im[3 * p + 2] + (d2 * z.im[3 * p]) * z.im[3 * p + 1];
+  }
+  return o;
+}
+template <int NP> CSF_DEV bool finite_s(const B<NP>& x) {
+  bool ok = isfinite(x.re);
+#pragma unroll
+  for (int g = 0; g < 3 * NP; ++g) ok = ok && isfinite(x.im[g]);
+  return ok;
+}
+
 template <typename S> CSF_DEV S div_checked(const S& a, const S& b, int* err) {
   if (re(b) == 0.0) raise(err, kErrDomain);
   return a / b;
@@ -202,6 +370,20 @@ CSF_DEV double sin_s(double x) { return csf_det::sin(x); }
 template <int G> CSF_DEV L<G> sin_s(const L<G>& z) { return lift(z, csf_det::sin(z.re), csf_det::cos(z.re)); }
 CSF_DEV double cos_s(double x) { return csf_det::cos(x); }
 template <int G> CSF_DEV L<G> cos_s(const L<G>& z) { return lift(z, csf_det::cos(z.re), -csf_det::sin(z.re)); }
+// Bicomplex lifts (csfd.hpp:230-245)
+template <int NP> CSF_DEV B<NP> sqrt_s(const B<NP>& z) {
+  const double f = ::sqrt(z.re);
+  const double d1 = 0.5 / f;
+  return lift2(z, f, d1, (-0.5 * d1) / z.re);
+}
+template <int NP> CSF_DEV B<NP> sin_s(const B<NP>& z) {
+  const double s = csf_det::sin(z.re), c = csf_det::cos(z.re);
+  return lift2(z, s, c, -s);
+}
+template <int NP> CSF_DEV B<NP> cos_s(const B<NP>& z) {
+  const double s = csf_det::sin(z.re), c = csf_det::cos(z.re);
+  return lift2(z, c, -s, -c);
+}
 
 // min/max/clamp keep the winning operand whole; ties keep the first
 // (csfd.hpp:281-288)

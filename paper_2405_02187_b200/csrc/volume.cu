@@ -26,9 +26,9 @@ namespace csfd {
 // block prologue: the frame's pose (c2w) -> w2c per channel group in smem
 // layout in smem: w2c[12][1+Dp], center[3][1+Dp], intr[4][1+Dp]
 // ----------------------------------------------------------------------------
-template <int G>
+template <typename S>
 __device__ void stage_pose_w2c(const double* __restrict__ pose, const double* __restrict__ intr, int Dp, double* sm) {
-  using S = Scal<G>;
+  constexpr int G = Traits<S>::G;
   const int C = 1 + Dp;
   const int ngroups = G == 0 ? 1 : Dp / G;
   double* w2c = sm;
@@ -70,11 +70,11 @@ __device__ void load_pose_intr(const double* sm, int Dp, int g0, Pose<S>* w2c, V
 
 // Fuse one voxel: the real pass decides validity, then every channel group
 // re-evaluates psi (bit-identical real part) and updates its channels.
-template <int G>
+template <typename S>
 __device__ bool fuse_voxel(const VoxelStore& vox, long long v, double px, double py, double pz,
                            const double* __restrict__ depth, int w, int h, double mu, double cap, int Dp,
                            const double* sm) {
-  using S = Scal<G>;
+  constexpr int G = Traits<S>::G;
   const int passes = G == 0 ? 1 : Dp / G;
   double2 rw = make_double2(0.0, 0.0);
   double fre = 0.0;
@@ -226,12 +226,12 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
   return true;
 }
 
-template <int G>
+template <typename S>
 __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const double* __restrict__ depth, int w,
                                                          int h, const double* __restrict__ pose,
                                                          const double* __restrict__ intr, int Dp, int* upd) {
   extern __shared__ double sm[];
-  stage_pose_w2c<G>(pose, intr, Dp, sm);
+  stage_pose_w2c<S>(pose, intr, Dp, sm);
   const long long n = static_cast<long long>(vol.nx) * vol.ny * vol.nz;
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < n;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -241,14 +241,14 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     const double px = vol.ox + vol.vs * static_cast<double>(i);
     const double py = vol.oy + vol.vs * static_cast<double>(j);
     const double pz = vol.oz + vol.vs * static_cast<double>(k);
-    if constexpr (kAdjointFusion && G > 0)
+    if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
       count_updates(upd, fuse_voxel_adjoint(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
     else
-      count_updates(upd, fuse_voxel<G>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+      count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
   }
 }
 
-template <int G>
+template <typename S>
 __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const int* __restrict__ coords,
                                                           const int* __restrict__ visible,
                                                           const int* __restrict__ counters,
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const
                                                           const double* __restrict__ pose,
                                                           const double* __restrict__ intr, int Dp, int* upd) {
   extern __shared__ double sm[];
-  stage_pose_w2c<G>(pose, intr, Dp, sm);
+  stage_pose_w2c<S>(pose, intr, Dp, sm);
   const int n_vis = counters[0];
   for (int vb = blockIdx.x; vb < n_vis; vb += gridDim.x) {
     const int b = visible[vb];
@@ -268,10 +268,10 @@ __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const
       const double py = vol.oy + vol.vs * static_cast<double>(8 * by + ly);
       const double pz = vol.oz + vol.vs * static_cast<double>(8 * bz + lz);
       const long long vv = static_cast<long long>(b) * kBlockVoxels + l;
-      if constexpr (kAdjointFusion && G > 0)
+      if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
         count_updates(upd, fuse_voxel_adjoint(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
       else
-        count_updates(upd, fuse_voxel<G>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+        count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
     }
   }
 }
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(128) k_raycast_march_warp(V vol, const double*
   }
 }
 
-template <int G, typename V>
+template <typename S, typename V>
 __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __restrict__ pose,
                                                       const double* __restrict__ intr, int w, int h, int Dp,
                                                       const double2* __restrict__ hits, double* __restrict__ vre,
@@ -1122,6 +1122,7 @@ __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __res
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
   for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
   __syncthreads();
+  constexpr int G = Traits<S>::G;
   const int passes = G == 0 ? 1 : Dp / G;
   const long long item = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (item >= static_cast<long long>(w) * h * passes) return;
@@ -1132,7 +1133,6 @@ __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __res
   const double alpha_prev = hit.x, alpha_hit = hit.y;
   const int x = pix % w, y = pix / w;
   const double* kk = sm + 12 * C;
-  using S = Scal<G>;
   const int g0 = gi * G;
   typename V::Cache cache;
   cache.reset();
@@ -1298,7 +1298,11 @@ void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, c
   const size_t smem = sizeof(double) * 19 * (1 + Dp);
   const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
   const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, sm_count() * 16LL));
-  CSF_DISPATCH_G(G, (k_integrate_dense<kG><<<grid, 256, smem, L.stream>>>(view, depth, w, h, pose, intr, Dp, upd)));
+  if (v.order == 2)
+    k_integrate_dense<B<1>><<<grid, 256, smem, L.stream>>>(view, depth, w, h, pose, intr, Dp, upd);
+  else
+    CSF_DISPATCH_G(G, (k_integrate_dense<Scal<kG>><<<grid, 256, smem, L.stream>>>(view, depth, w, h, pose, intr, Dp,
+                                                                                  upd)));
   ++*L.launches;
   chk("integrate_dense");
 }
@@ -1309,8 +1313,12 @@ void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, c
   const HashView view = hash_view(v, Dp);
   const size_t smem = sizeof(double) * 19 * (1 + Dp);
   const int grid = sm_count() * 8;
-  CSF_DISPATCH_G(G, (k_integrate_hashed<kG><<<grid, 256, smem, L.stream>>>(view, v.coords, a.visible, a.counters,
-                                                                           depth, w, h, pose, intr, Dp, upd)));
+  if (v.order == 2)
+    k_integrate_hashed<B<1>><<<grid, 256, smem, L.stream>>>(view, v.coords, a.visible, a.counters, depth, w, h, pose,
+                                                            intr, Dp, upd);
+  else
+    CSF_DISPATCH_G(G, (k_integrate_hashed<Scal<kG>><<<grid, 256, smem, L.stream>>>(
+                          view, v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd)));
   ++*L.launches;
   chk("integrate_hashed");
 }
@@ -1352,7 +1360,7 @@ size_t alloc_scan_bytes(int n) {
 }
 
 template <typename V>
-static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp, const double* pose,
+static void raycast_impl(const Launch& L, const V& view, Box box, int order, int G, int Dp, const double* pose,
                          const double* intr, int w, int h, double near_clip, double far_clip, double step,
                          double2* hits, double* vre, double* nre, double* vim, double* nim) {
   const int P = w * h;
@@ -1376,6 +1384,14 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
   }
   if (L.phase == 1) return;
   const size_t smem = sizeof(double) * 16 * (1 + Dp);
+  if (order == 2) {
+    // second order: one thread per (hit pixel, pair) in Bicomplex arithmetic
+    const long long items = static_cast<long long>(P) * (Dp / 3);
+    k_raycast_lift<B<1>, V><<<static_cast<int>((items + 127) / 128), 128, smem, L.stream>>>(view, pose, intr, w, h,
+                                                                                          Dp, hits, vre, nre, vim, nim);
+    *L.launches += 1;
+    return;
+  }
   // one thread per hit pixel with tangent-form channels (CSF_LIFT_ALL=1) or
   // one thread per (hit pixel, channel group) — the default: more memory
   // parallelism wins over the recomputed real chain on B200.
@@ -1403,8 +1419,8 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int G, int Dp,
   const int passes = RG == 0 ? 1 : Dp / RG;
   const long long items = static_cast<long long>(P) * passes;
   const int grid = static_cast<int>((items + 127) / 128);
-  CSF_DISPATCH_RG(RG, (k_raycast_lift<kG, V><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre,
-                                                                            nre, vim, nim)));
+  CSF_DISPATCH_RG(RG, (k_raycast_lift<Scal<kG>, V><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits,
+                                                                                  vre, nre, vim, nim)));
   *L.launches += 1;
 }
 
@@ -1418,7 +1434,7 @@ void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, con
   box.hi[0] = v.ox + v.vs * (static_cast<double>(v.nx) - 1.0);
   box.hi[1] = v.oy + v.vs * (static_cast<double>(v.ny) - 1.0);
   box.hi[2] = v.oz + v.vs * (static_cast<double>(v.nz) - 1.0);
-  raycast_impl(L, view, box, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
+  raycast_impl(L, view, box, v.order, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
   chk("raycast_dense");
 }
 
@@ -1428,7 +1444,7 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
   const HashView view = hash_view(v, Dp);
   Box box;
   box.use = false;
-  raycast_impl(L, view, box, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
+  raycast_impl(L, view, box, v.order, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
   chk("raycast_hashed");
 }
 
