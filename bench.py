@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """CSFD SLAM frame-derivatives/s at 640x480 (BASELINE.json metric).
 
-Workload (N=1): BASELINE config 2 — 100 VGA depth frames of the seeded
+Workload (N=1, default --workload config2): BASELINE config 2 — 100 VGA depth frames of the seeded
 procedural room (synthetic stand-in for TUM-style sequences, rendered on the
 device by the harness; not timed), hashed 8^3-block TSDF at 5 mm voxels with
 2^20 buckets, 10 CSFD directions (6 first-frame twist + 4 intrinsics),
@@ -24,6 +24,15 @@ pipeline; the derivative columns are all-gathered over NCCL.  Total work is
 fixed, so scaling is "strong".  --impl reference times the CPU oracle port
 (the reference's own CPU path restated) on a bounded sample of the same
 workload.
+
+--workload config3: BASELINE config 3 — the same VGA scene, 30 frames, the
+full 10x10 Hessian as 55 second-order parameter pairs (one reference
+Bicomplex per pair, packed as channel slots of one evaluation).  Units =
+frames x pairs; the pairs are sharded across ranks like directions.
+
+`value` is timed without per-kernel events; a second, profiled pass of the
+same steps (CUDA events around every kernel category on the library stream)
+gives the per-kernel split and the rooflines.
 """
 from __future__ import annotations
 
@@ -45,6 +54,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "CSFD SLAM frame-derivatives/sec at 640×480 (frames×directions/s), 1/2/4/8 GPU"
 UNIT = "frame-derivatives/s"
 DIRS = list(range(10))  # 6 first-frame twist components (rho, phi) + fx, fy, cx, cy
+PAIRS = [(i, j) for i in range(10) for j in range(i, 10)]  # 55 Hessian pairs (config 3)
 
 
 def parse():
@@ -53,7 +63,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--frames", type=int, default=100)
+    ap.add_argument("--workload", choices=["config2", "config3"], default="config2")
+    ap.add_argument("--frames", type=int, default=0, help="0 = the workload's frame count (100 / 30)")
     ap.add_argument("--cpu-frames", type=int, default=5, help="CPU-baseline sample: frames")
     ap.add_argument("--cpu-dirs", type=int, default=2, help="CPU-baseline sample: directions (one pass each)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -61,11 +72,15 @@ def parse():
     return ap.parse_args()
 
 
-def pipeline_cfg(csf, capi, k, dirs, n_frames):
+def pipeline_cfg(csf, capi, k, dirs, n_frames, pairs=None):
     import ctypes as C
-    hp = capi.HashParams(0.005, (C.c_double * 3)(0.0, 0.0, 0.0), 5 * 0.005, 128.0, 20, 1 << 18)
-    return csf.make_pipeline_cfg(hashed=True, k=k, dirs=dirs, h=1e-8, objective=capi.OBJECTIVE_TRAJECTORY_ERROR,
-                                 max_frames=n_frames, hash_params=hp)
+    # block pool: config 2 allocates ~68k blocks over 100 frames; second-order
+    # voxels carry 3 slots per pair, so the pool is sized to the 30-frame run
+    max_blocks = (1 << 18) if pairs is None else (1 << 16)
+    hp = capi.HashParams(0.005, (C.c_double * 3)(0.0, 0.0, 0.0), 5 * 0.005, 128.0, 20, max_blocks)
+    return csf.make_pipeline_cfg(hashed=True, k=k, dirs=[] if pairs is not None else dirs, h=1e-8,
+                                 objective=capi.OBJECTIVE_TRAJECTORY_ERROR, max_frames=n_frames, hash_params=hp,
+                                 pairs=pairs)
 
 
 class Clocks:
@@ -114,24 +129,42 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def cpu_baseline(depth, gt, k, frames, ndirs):
+def traffic_for(cat, workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
+    category's kernel from the committed ncu --set full capture
+    (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(workload, {}).get(cat)
+    except Exception:
+        return None
+
+
+def cpu_baseline(depth, gt, k, frames, ndirs, workload="config2"):
     """Oracle port, one Complex-style pass per direction (the reference's
-    pattern, diff.hpp:46-56), all host threads (OpenMP)."""
+    pattern, diff.hpp:46-56) or one Bicomplex pass per pair (diff.hpp:58-72),
+    all host threads (OpenMP)."""
     from oracle import orc
     import paper_2405_02187_b200 as csf
     from paper_2405_02187_b200 import capi
     secs = 0.0
     for d in range(ndirs):
-        cfg = pipeline_cfg(csf, capi, k, [DIRS[d]], frames)
-        _, _, _, _, s = orc.pipeline_run(cfg, depth[:frames], gt[:frames])
-        secs += s
+        if workload == "config3":
+            cfg = pipeline_cfg(csf, capi, k, [], frames, pairs=[PAIRS[d]])
+            secs += orc.pipeline_hessian(cfg, depth[:frames], gt[:frames])[-1]
+        else:
+            cfg = pipeline_cfg(csf, capi, k, [DIRS[d]], frames)
+            secs += orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
     units = frames * ndirs
     cores = os.cpu_count() or 1
     omp = os.environ.get("OMP_NUM_THREADS")
     if omp:
         cores = int(omp)
+    what = "pair" if workload == "config3" else "direction"
     return {"value": units / secs, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"config 2 first {frames} VGA frames x {ndirs} directions, one pass per direction "
+            "sample": f"{workload} first {frames} VGA frames x {ndirs} {what}s, one pass per {what} "
                       f"({units} units in {secs:.2f} s)"}
 
 
@@ -140,30 +173,33 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2405_02187_b200 as csf  # noqa: F401 (struct layouts)
+    import paper_2405_02187_b200 as csf
     from oracle import orc
+    from paper_2405_02187_b200 import capi
     frames = 3
     depth, gt, k = orc.workload(2, frames)
-    from paper_2405_02187_b200 import capi
-    cfg = pipeline_cfg(__import__("paper_2405_02187_b200"), capi, k, [0], frames)
+    second = args.workload == "config3"
+    cfg = pipeline_cfg(csf, capi, k, [0], frames, pairs=[PAIRS[1]] if second else None)
+    run = (lambda: orc.pipeline_hessian(cfg, depth, gt)) if second else (lambda: orc.pipeline_run(cfg, depth, gt))
     for _ in range(args.warmup):
-        orc.pipeline_run(cfg, depth, gt)
+        run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        orc.pipeline_run(cfg, depth, gt)
+        run()
     secs = time.perf_counter() - t0
     units = frames * 1 * args.steps
     value = units / secs
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    what = "pair (Bicomplex pass)" if second else "direction"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded procedural room, BASELINE config 2 shapes)",
-        "config": {"workload": "config2 VGA hashed 5mm, bounded CPU sample: 3 frames x 1 direction per step",
+        "data": f"synthetic (seeded procedural room, BASELINE {args.workload} shapes)",
+        "config": {"workload": f"{args.workload} VGA hashed 5mm, bounded CPU sample: 3 frames x 1 {what} per step",
                    "frames": frames, "directions": 1},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": "3 VGA frames x 1 direction per step (oracle/ restatement; the reference needs "
+                         "sample": f"3 VGA frames x 1 {what} per step (oracle/ restatement; the reference needs "
                                    "Eigen/libpng/doctest, absent)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -201,12 +237,14 @@ def algorithmic_bytes_per_step(cat, stats, D, W, H, n_frames):
 
 def main():
     args = parse()
+    second = args.workload == "config3"
+    if args.frames <= 0:
+        args.frames = 30 if second else 100
     if args.impl == "reference":
         run_reference(args)
         return
     import torch
     import paper_2405_02187_b200 as csf
-    from paper_2405_02187_b200 import capi
     from paper_2405_02187_b200.shard import gather_columns, shard_directions
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -218,11 +256,13 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
+    from paper_2405_02187_b200 import capi
     ctx = csf.Context(local)
     n = args.frames
     depth, gt, k = csf.synth_workload(2, n, ctx=ctx)
-    off, mine = shard_directions(DIRS, world, rank)
-    cfg = pipeline_cfg(csf, capi, k, mine, n)
+    units_all = PAIRS if second else DIRS          # the sharded work items
+    off, mine = shard_directions(units_all, world, rank)
+    cfg = pipeline_cfg(csf, capi, k, mine, n, pairs=mine if second else None)
     pipe = csf.Pipeline(cfg, ctx=ctx)
     pipe.upload(depth, gt)
     stream = torch.cuda.ExternalStream(ctx.stream)
@@ -231,16 +271,15 @@ def main():
         pipe.run()
     ctx.synchronize()
 
-    # ---------------- timed region: device-resident inputs
     def barrier():
         if dist is not None:
             dist.barrier()
 
+    # ---------------- timed region: device-resident inputs, no per-kernel events
     clocks = Clocks(local)
     barrier()
     torch.cuda.synchronize()
     ctx.synchronize()
-    ctx.profile(True)
     l0 = ctx.launch_count
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -253,20 +292,38 @@ def main():
     barrier()
     ms = e0.elapsed_time(e1)
     launches = ctx.launch_count - l0
-    prof = ctx.profile_read()
-    ctx.profile(False)
     clk = clocks.stop()
-    res = pipe.result()
+    if second:
+        hr = pipe.hessian(stats=True)
+        local_cols, stats = hr.hessian, hr.stats
+    else:
+        res = pipe.result()
+        local_cols, stats = res.gradient, res.stats
     if dist is not None:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        grad = gather_columns(torch.from_numpy(res.gradient).cuda(), len(DIRS), world, rank).cpu().numpy()
+        cols = gather_columns(torch.from_numpy(np.asarray(local_cols)).cuda(), len(units_all), world,
+                              rank).cpu().numpy()
     else:
-        grad = res.gradient
+        cols = local_cols
 
-    units_per_step = n * len(DIRS)
+    units_per_step = n * len(units_all)
     value = units_per_step * args.steps / (ms / 1000.0)
+
+    # ---------------- profiled pass (same steps): per-kernel-category CUDA events
+    ctx.synchronize()
+    ctx.profile(True)
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        pipe.run()
+    p1.record(stream)
+    ctx.synchronize()
+    prof_ms = p0.elapsed_time(p1)
+    prof = ctx.profile_read()
+    ctx.profile(False)
 
     # ---------------- e2e through the public API from pinned host memory
     pinned = torch.empty(depth.shape, dtype=torch.float32, pin_memory=True)
@@ -288,39 +345,48 @@ def main():
 
     # ---------------- roofline: every category with a bytes model; the dominant one is `roofline`
     peak, peak_src = measured_peak()
+    slots = 3 * len(mine) if second else len(mine)
     rooflines = {}
     for cat, (cat_ms, cat_n) in prof.items():
-        bytes_step, bytes_def = algorithmic_bytes_per_step(cat, res.stats, len(mine), k.width, k.height, n)
+        bytes_step, bytes_def = algorithmic_bytes_per_step(cat, stats, slots, k.width, k.height, n)
         if bytes_step is None or cat_n == 0 or cat_ms <= 0:
             continue
         bytes_per_launch = bytes_step * args.steps / cat_n
         avg_ms = cat_ms / cat_n
         achieved = bytes_per_launch / (avg_ms / 1000.0) / 1e9
         rooflines[cat] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                          "frac": achieved / peak, "traffic": None, "kernel": cat, "avg_launch_ms": avg_ms,
-                          "launches": cat_n, "share_of_step": cat_ms / ms, "algorithmic_bytes_per_launch":
-                          bytes_per_launch, "bytes_model": bytes_def, "peak_source": peak_src}
+                          "frac": achieved / peak, "traffic": traffic_for(cat, args.workload), "kernel": cat,
+                          "avg_launch_ms": avg_ms, "launches": cat_n, "share_of_step": cat_ms / prof_ms,
+                          "algorithmic_bytes_per_launch": bytes_per_launch, "bytes_model": bytes_def,
+                          "peak_source": peak_src}
     roofline = max(rooflines.values(), key=lambda r: r["share_of_step"]) if rooflines else None
 
+    if second:
+        workload = (f"config3: {n} VGA frames, hashed 8^3 blocks 5 mm, 2^20 buckets, 10x10 Hessian = "
+                    f"{len(PAIRS)} bicomplex pairs")
+    else:
+        workload = f"config2: {n} VGA frames, hashed 8^3 blocks 5 mm, 2^20 buckets, {len(DIRS)} CSFD directions"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded procedural room rendered on device; BASELINE config 2 shapes)",
-        "config": {"workload": "config2: 100 VGA frames, hashed 8^3 blocks 5 mm, 2^20 buckets, 10 CSFD directions",
-                   "frames": n, "directions": len(DIRS), "directions_per_rank": len(mine),
-                   "parallelism": f"directions sharded x{world}", "l2": "working set (hashed volume, ~GBs) >> L2"},
+        "config": {"workload": workload, "frames": n, "directions": len(units_all),
+                   "directions_per_rank": len(mine), "order": 2 if second else 1,
+                   "parallelism": f"{'pairs' if second else 'directions'} sharded x{world}",
+                   "l2": "working set (hashed volume, ~GBs) >> L2"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "roofline_by_kernel": rooflines,
         "clocks": clk,
         "kernel_ms_per_step": {c: v[0] / args.steps for c, v in prof.items()},
-        "gradient": [float(x) for x in grad],
-        "blocks_allocated": int(res.stats[-1, 3]),
+        "profiled_ms_per_step": prof_ms / args.steps,
+        ("hessian_pairs" if second else "gradient"): [float(x) for x in cols],
+        "blocks_allocated": int(stats[-1, 3]),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            line["cpu_baseline"] = cpu_baseline(depth, gt, k, args.cpu_frames, args.cpu_dirs)
+            line["cpu_baseline"] = cpu_baseline(depth, gt, k, args.cpu_frames, args.cpu_dirs, args.workload)
         except Exception as e:  # the oracle must have been built by build()
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if args.profile_json:
