@@ -9,9 +9,12 @@
 // Reduction order of the normal equations: the reference sums sequentially
 // (icp.cpp:19-27).  The canonical order used by the tracker (and by the GPU)
 // is "slot-tiled": slots are cut into tiles of kTile consecutive slots, each
-// tile is summed sequentially in slot order, and tile partials are summed
-// sequentially in tile order.  normal_equations(..., sequential=true) keeps
-// the reference's literal order for the KAT pins.
+// tile is summed sequentially in slot order, tile partials are summed
+// sequentially within groups of kGroup consecutive tiles, and group totals
+// are summed sequentially in group order (the device sums a group as soon as
+// its last tile is done, so the cross-tile sum is a short chain).
+// normal_equations(..., sequential=true) keeps the reference's literal order
+// for the KAT pins.
 #pragma once
 
 #include <functional>
@@ -21,6 +24,7 @@
 namespace orc {
 
 constexpr int kTile = 256;
+constexpr int kGroup = 16;
 
 // icp.hpp:27-31
 struct Correspondence {
@@ -166,15 +170,21 @@ void add_into(NormalEq<S>& dst, const NormalEq<S>& src) {
 inline NormalEq<double> normal_equations(const std::vector<Correspondence>& corrs, const Pose& base,
                                          bool sequential) {
   NormalEq<double> total;
-  NormalEq<double> tile;
+  NormalEq<double> tile, group;
+  const std::size_t n_tiles = (corrs.size() + kTile - 1) / kTile;
   for (std::size_t i = 0; i < corrs.size(); ++i) {
     double j[6], r;
     const Correspondence& c = corrs[i];
     jacobian_row<double>(c.vertex, c.model_vertex, c.model_normal, base, j, &r);
     accumulate_row(sequential ? total : tile, j, r);
     if (!sequential && ((i + 1) % kTile == 0 || i + 1 == corrs.size())) {
-      add_into(total, tile);
+      const std::size_t t = i / kTile;
+      add_into(group, tile);
       tile = NormalEq<double>();
+      if ((t + 1) % kGroup == 0 || t + 1 == n_tiles) {
+        add_into(total, group);
+        group = NormalEq<double>();
+      }
     }
   }
   return total;
@@ -286,8 +296,14 @@ NormalEq<S> tiled_normal_equations(const std::vector<CorrIndex>& idx, int width,
                     base, j, &r);
     accumulate_row(partial[slot / kTile], j, r);
   }
-  NormalEq<S> total;
-  for (int t = 0; t < n_tiles; ++t) add_into(total, partial[t]);
+  NormalEq<S> total, group;
+  for (int t = 0; t < n_tiles; ++t) {
+    add_into(group, partial[t]);
+    if ((t + 1) % kGroup == 0 || t + 1 == n_tiles) {
+      add_into(total, group);
+      group = NormalEq<S>();
+    }
+  }
   return total;
 }
 

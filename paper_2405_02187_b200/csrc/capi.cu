@@ -157,6 +157,9 @@ struct csf_volume_s {
   // stage buffers for the single-call APIs
   DevBuf<double> s_depth, s_pose, s_intr, s_vre, s_nre, s_vim, s_nim;
   DevBuf<double2> s_hits;
+  // raycast alpha table (hashed volumes) for (tab_near, tab_far, tab_step)
+  DevBuf<double> alpha_tab;
+  double tab_near = 0.0, tab_far = -1.0, tab_step = 0.0;
 
   ~csf_volume_s() {
     rw.release(); fim.release(); heads.release(); next.release(); coords.release(); nblocks.release(); keys.release();
@@ -168,6 +171,7 @@ struct csf_volume_s {
     s_depth.release(); s_pose.release(); s_intr.release(); s_vre.release(); s_nre.release(); s_vim.release();
     s_nim.release();
     s_hits.release();
+    alpha_tab.release();
   }
 };
 
@@ -255,11 +259,40 @@ int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double*
   return CSF_OK;
 }
 
+// The alpha sequence of a hashed raycast (a_0 = near, a_{n+1} = a_n + step,
+// IEEE double addition as on the device), tabulated on the host once per
+// (near, far, step) and kept on the device with the volume.
+int ensure_alpha_table(csf_volume v, double near_clip, double far_clip, double step) {
+  if (v->alpha_tab.p && v->tab_near == near_clip && v->tab_far == far_clip && v->tab_step == step) return CSF_OK;
+  if (!(step > 0.0)) return fail(v->ctx, CSF_EINVAL, "raycast: step must be positive");
+  std::vector<double> a;
+  double alpha = near_clip;
+  while (alpha <= far_clip) {
+    a.push_back(alpha);
+    alpha += step;
+    if (a.size() > (1u << 24)) return fail(v->ctx, CSF_EINVAL, "raycast: too many steps");
+  }
+  a.push_back(alpha);  // sentinel > far
+  CUDA_TRY(v->ctx, cudaStreamSynchronize(v->ctx->stream));
+  CUDA_TRY(v->ctx, v->alpha_tab.alloc(a.size()));
+  CUDA_TRY(v->ctx, cudaMemcpy(v->alpha_tab.p, a.data(), sizeof(double) * a.size(), cudaMemcpyHostToDevice));
+  v->tab_near = near_clip;
+  v->tab_far = far_clip;
+  v->tab_step = step;
+  v->hash.alpha_tab = v->alpha_tab.p;
+  v->hash.alpha_n = static_cast<int>(a.size());
+  return CSF_OK;
+}
+
 void raycast_dev(csf_volume v, const double* d_pose, const double* d_intr, int w, int h, const csf_raycast_cfg& rc,
                  double2* hits, double* vre, double* nre, double* vim, double* nim) {
   Launch L = launch_of(v->ctx);
   const double mu = v->hashed ? v->hash.mu : v->dense.mu;
   const double step = rc.step_fraction * mu;
+  if (v->hashed && ensure_alpha_table(v, rc.near_clip, rc.far_clip, step) != CSF_OK) {
+    v->hash.alpha_tab = nullptr;  // fall back to the in-kernel repeated addition
+    v->hash.alpha_n = 0;
+  }
   for (int phase = 1; phase <= 2; ++phase) {
     PROF(v->ctx, phase == 1 ? kPRaycast : kPRaycastLift);
     L.phase = phase;
@@ -794,8 +827,8 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   A(p->nre.alloc(P * 3));
   A(p->vim.alloc(P * 3 * std::max(p->Dp, 1)));
   A(p->nim.alloc(P * 3 * std::max(p->Dp, 1)));
-  A(p->partials.alloc(static_cast<size_t>(max_tiles) * 27 * C));
-  A(p->counts.alloc(max_tiles));
+  A(p->partials.alloc(icp_partials_doubles(C, max_tiles)));
+  A(p->counts.alloc(icp_counts_ints(max_tiles)));
   A(p->pose.alloc(12 * C));
   A(p->pred_pose.alloc(12 * C));
   A(p->intr_levels.alloc(3 * 4 * C));
@@ -826,6 +859,7 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   cudaMemcpy(p->pair_i.p, cfg->pair_i, sizeof(int) * CSF_MAX_PAIRS, cudaMemcpyHostToDevice);
   cudaMemcpy(p->pair_j.p, cfg->pair_j, sizeof(int) * CSF_MAX_PAIRS, cudaMemcpyHostToDevice);
   cudaMemset(p->st.p, 0, sizeof(TrackState));
+  cudaMemset(p->counts.p, 0, sizeof(int) * p->counts.n);
   *out = p;
   return CSF_OK;
 }
@@ -1041,8 +1075,9 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
   CUDA_TRY(ctx, pose.alloc(12));
   CUDA_TRY(ctx, pred.alloc(12));
   CUDA_TRY(ctx, intr.alloc(12));
-  CUDA_TRY(ctx, partials.alloc(static_cast<size_t>(tiles_max) * 27));
-  CUDA_TRY(ctx, counts.alloc(tiles_max));
+  CUDA_TRY(ctx, partials.alloc(icp_partials_doubles(1, tiles_max)));
+  CUDA_TRY(ctx, counts.alloc(icp_counts_ints(tiles_max)));
+  CUDA_TRY(ctx, cudaMemsetAsync(counts.p, 0, sizeof(int) * counts.n, ctx->stream));
   CUDA_TRY(ctx, st.alloc(1));
   double kl[12];
   for (int l = 0; l < 3; ++l) {

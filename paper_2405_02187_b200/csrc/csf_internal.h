@@ -35,6 +35,11 @@ struct HashDev {
   int bits, max_blocks, gbits;
   double vs, ox, oy, oz, mu, cap;
   int order = 1;  // CSFD order of the channel slots (2: bicomplex pairs, 3 slots each)
+  // Raycast alpha sequence a_0 = near, a_{n+1} = a_n + step (the reference's
+  // repeated addition, tsdf.hpp:254): shared by every ray of a hashed volume
+  // (no slab clip), so it is tabulated once; a_{n_tab-1} > far is a sentinel.
+  const double* alpha_tab = nullptr;
+  int alpha_n = 0;
 };
 
 // Per-frame allocation scratch (hashed volumes).
@@ -103,14 +108,16 @@ void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, 
 // ---- icp.cu
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp);
 int icp_tiles(int w, int h, int stride);
+// ICP scratch sizes for frames of up to max_tiles tiles (icp_tiles at stride 1);
+// the counts buffer must be zeroed once at allocation.
+size_t icp_partials_doubles(int C, int max_tiles);
+size_t icp_counts_ints(int max_tiles);
 // One ICP iteration: association + lifted normal equations per tile, and the
 // last CTA solves and updates the pose (TrackState::pad[0] is its counter).
 void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const double* depth, int w, int h,
                        int stride, const double* intr, double* pose, const double* vre, const double* nre,
                        const double* vim, const double* nim, double d_max, double cos_max, double* partials,
                        int* counts, int level, double tol);
-void launch_icp_solve(const Launch& L, int G, int Dp, TrackState* st, const double* partials, const int* counts,
-                      int n_tiles, double* pose, int level, double tol);
 void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,
                  const double* intr_base, double* pose, double* intr_levels, int levels);
 void launch_frame_begin(const Launch& L, TrackState* st, int frame);

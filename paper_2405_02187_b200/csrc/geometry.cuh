@@ -373,12 +373,14 @@ CSF_DEV bool ldlt6_solve(const S* a_lower, const S* rhs, S* dst, S* ws) {
 // Register-resident variant of ldlt6_solve: the same operations in the same
 // order, with every loop fully unrolled and the pivot swaps expressed as
 // predicated swaps over compile-time indices (no dynamic indexing, so the
-// matrix never leaves registers).  Used by the latency-critical ICP solve.
+// matrix never leaves registers).  Split into the factorization and the
+// solve phase so the ICP solve can factor the real matrix once and apply
+// the real factors to every channel's tangent right-hand side.
+// `degenerate` (optional) reports a zero pivot or a pivot below the solve's
+// tolerance — the cases where the solve is not the linear operator A^-1.
 template <typename S>
-CSF_DEV bool ldlt6_solve_reg(const S* a_lower, const S* rhs, S* dst) {
-  S m[6][6];
-  int transp[6];
-  bool ok = true, stop = false;
+CSF_DEV bool ldlt6_factor_reg(const S* a_lower, S (&m)[6][6], int (&transp)[6], bool* degenerate = nullptr) {
+  bool ok = true, stop = false, degen = false;
 #pragma unroll
   for (int r = 0; r < 6; ++r)
 #pragma unroll
@@ -429,6 +431,7 @@ CSF_DEV bool ldlt6_solve_reg(const S* a_lower, const S* rhs, S* dst) {
     }
     const S akk = m[k][k];
     const bool pivot_valid = absre(akk) > 0.0;
+    if (!pivot_valid) degen = true;
     if (k == 0 && !pivot_valid) {
       ok = false;
 #pragma unroll
@@ -446,6 +449,20 @@ CSF_DEV bool ldlt6_solve_reg(const S* a_lower, const S* rhs, S* dst) {
       }
     }
   }
+  const double tol = 2.2250738585072014e-308;  // numeric_limits<double>::min()
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+    if (!(absre(m[i][i]) > tol)) degen = true;
+  if (degenerate) *degenerate = degen || stop;
+  return ok;
+}
+
+// The solve phase of ldlt6_solve (transpositions, unit-lower forward
+// substitution, diagonal, backward substitution, inverse transpositions).
+// M may be the factor of the same scalar type or, for the tangent solve,
+// plain double factors applied to a double right-hand side.
+template <typename S, typename M>
+CSF_DEV void ldlt6_apply_reg(const M (&m)[6][6], const int (&transp)[6], const S* rhs, S* dst) {
   S x[6];
 #pragma unroll
   for (int i = 0; i < 6; ++i) x[i] = rhs[i];
@@ -480,6 +497,14 @@ CSF_DEV bool ldlt6_solve_reg(const S* a_lower, const S* rhs, S* dst) {
       if (transp[k] == i) swap_s(x[k], x[i]);
 #pragma unroll
   for (int i = 0; i < 6; ++i) dst[i] = x[i];
+}
+
+template <typename S>
+CSF_DEV bool ldlt6_solve_reg(const S* a_lower, const S* rhs, S* dst) {
+  S m[6][6];
+  int transp[6];
+  const bool ok = ldlt6_factor_reg<S>(a_lower, m, transp);
+  ldlt6_apply_reg<S>(m, transp, rhs, dst);
   return ok;
 }
 

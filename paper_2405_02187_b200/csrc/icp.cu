@@ -37,15 +37,23 @@ CSF_DEV unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-CSF_DEV void clock_mark(int slot) {
+CSF_DEV void clock_mark(int slot, int cta = -1) {
   if (g_icp_clock && threadIdx.x == 0 && g_icp_clock_launch < 4096)
-    g_icp_clock[(static_cast<unsigned long long>(g_icp_clock_launch) * 512 + blockIdx.x) * 8 + slot] = gtimer();
+    g_icp_clock[(static_cast<unsigned long long>(g_icp_clock_launch) * 512 + (cta < 0 ? blockIdx.x : cta)) * 8 + slot] =
+        gtimer();
 }
+// the solve kernel records into CTA slot 511 of the iteration's record
+constexpr int kSolveClockCta = 511;
+
+// Programmatic dependent launch (sm_90+): the ICP iteration's kernels are
+// launched with programmatic stream serialization, so the next kernel is
+// scheduled while this one runs and waits here for its predecessor's
+// completion and memory instead of paying the full launch gap.
+CSF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+CSF_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 // 256 threads evaluate the tile's slots; all 320 sum accumulators (27*(1+Dp)
 // of them, one per thread up to Dp = 10), so no thread carries two.
 constexpr int kRedThreads = 320;
-// Tiles per shared-memory stage of the solve's cross-tile sums.
-constexpr int kSolveChunk = 16;
 __constant__ int c_tri_r[21] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5, 5, 5, 5};
 __constant__ int c_tri_c[21] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2, 3, 4, 5};
 
@@ -106,94 +114,195 @@ CSF_DEV bool associate_slot(const double* __restrict__ depth, int w, int h, int 
   return true;
 }
 
-// The solve of one ICP iteration, run by one CTA of >= 64 threads: sum the
-// tile partials in tile order, then one thread per channel group factors the
-// lifted 6x6 system, applies exp(delta) * T and writes the break decisions.
-// `sm` holds >= 27*(1+Dp) + 48*(1+G)*ngroups doubles.
-template <int G>
-__device__ __noinline__ void icp_solve_block(TrackState* st, const double* partials, const int* counts, int n_tiles,
-                                double* pose, int Dp, int level, double tol, double* sm) {
-  using S = Scal<G>;
-  __shared__ int s_n, s_finite;
+// Canonical two-level cross-tile order (oracle/orc_icp.hpp, kGroup): the
+// last CTA to finish within a group of kGroup consecutive tiles sums the
+// group's tile partials in tile order into gpartials[group]; the solve then
+// sums the (few) group totals in group order.  Called by every CTA after it
+// wrote its own tile partials.
+constexpr int kGroup = 16;
+constexpr int kMaxGroupCtr = 256;  // tiles per launch <= kGroup * kMaxGroupCtr
+CSF_DEV void group_sum(const double* __restrict__ partials, const int* __restrict__ counts, int n_acc,
+                       double* __restrict__ gpartials, int* __restrict__ gcounts, unsigned* __restrict__ group_ctr) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  const int grp = blockIdx.x / kGroup;
+  const int first = grp * kGroup;
+  const int gn = min(kGroup, static_cast<int>(gridDim.x) - first);
+  if (threadIdx.x == 0) s_last = atomicAdd(group_ctr + grp, 1u) == static_cast<unsigned>(gn - 1);
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x == 0) group_ctr[grp] = 0u;  // ready for the next launch
+  __threadfence();
+  for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
+    double v[kGroup];
+#pragma unroll
+    for (int u = 0; u < kGroup; ++u)
+      v[u] = u < gn ? __ldcg(partials + static_cast<long long>(first + u) * n_acc + a) : 0.0;
+    double total = 0.0;
+#pragma unroll
+    for (int u = 0; u < kGroup; ++u)
+      if (u < gn) total = total + v[u];
+    gpartials[static_cast<long long>(grp) * n_acc + a] = total;
+  }
+  if (threadIdx.x < 32) {
+    int c = static_cast<int>(threadIdx.x) < gn ? __ldcg(counts + first + threadIdx.x) : 0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
+    if (threadIdx.x == 0) gcounts[grp] = c;
+  }
+}
+
+// The solve of one ICP iteration (one CTA): group totals in group order, then
+// the real 6x6 LDLT once (thread 0, the oracle's Ldlt6 order, bit-identical
+// real step) and every perturbation channel in tangent form against the real
+// factors, d.im = A^-1 (nb.im - A.im d.re) — the first-order quantity the
+// truncated-Complex LDLT computes, ~1 ulp per operation apart.  Degenerate
+// systems (zero or sub-normal pivots) take the per-channel lifted LDLT
+// instead.  Then exp(delta) * T per channel thread (L<1>) and the break
+// decisions (icp.cpp:199,235) into TrackState.
+constexpr int kMaxC = 1 + 36;
+__global__ void __launch_bounds__(kRedThreads) k_icp_solve_t(TrackState* st, const double* __restrict__ gpartials,
+                                                          const int* __restrict__ gcounts, int n_groups,
+                                                          double* pose, int Dp, int level, double tol) {
+  pdl_wait();
+  pdl_trigger();
+  if (st->level_done) return;
+  __shared__ double s_acc[27 * kMaxC];
+  __shared__ double s_m[36], s_x[6];
+  __shared__ int s_tr[6];
+  __shared__ int s_n, s_degen, s_finite;
   const int C = 1 + Dp;
   const int n_acc = 27 * C;
-  S* ws = reinterpret_cast<S*>(sm + n_acc) + 48 * threadIdx.x;
-  // Tile partials in tile order: each accumulator thread keeps 32 loads in
-  // flight, then adds them in sequence (one L2 round trip per 32 tiles).
+  clock_mark(3, kSolveClockCta);
   for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
+    double v[32];
     double total = 0.0;
-    for (int t = 0; t < n_tiles; t += 32) {
-      double v[32];
+    for (int g0 = 0; g0 < n_groups; g0 += 32) {
 #pragma unroll
       for (int u = 0; u < 32; ++u)
-        v[u] = t + u < n_tiles ? __ldcg(partials + static_cast<long long>(t + u) * n_acc + a) : 0.0;
+        v[u] = g0 + u < n_groups ? __ldcg(gpartials + static_cast<long long>(g0 + u) * n_acc + a) : 0.0;
 #pragma unroll
       for (int u = 0; u < 32; ++u)
-        if (t + u < n_tiles) total = total + v[u];
+        if (g0 + u < n_groups) total = total + v[u];
     }
-    sm[a] = total;
+    s_acc[a] = total;
   }
-  clock_mark(5);
-  // correspondence count: integer sum, any order is exact
-  if (threadIdx.x == 0) {
-    s_n = 0;
-    s_finite = 1;
-  }
-  __syncthreads();
-  {
-    int part = 0;
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) part += __ldcg(counts + t);
+  if (threadIdx.x < 32) {
+    int c = 0;
+    for (int g = threadIdx.x; g < n_groups; g += 32) c += __ldcg(gcounts + g);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) part += __shfl_down_sync(0xffffffffu, part, off);
-    if ((threadIdx.x & 31) == 0 && part) atomicAdd(&s_n, part);
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
+    if (threadIdx.x == 0) {
+      s_n = c;
+      s_finite = 1;
+    }
   }
   __syncthreads();
+  clock_mark(5, kSolveClockCta);
   const int n = s_n;
   if (n < 12) {
     if (threadIdx.x == 0) {
       st->n_corr = n;
       st->level_done = 1;
+      if (g_icp_clock) atomicAdd(&g_icp_clock_launch, 1u);
     }
     return;
   }
-  const int ngroups = G == 0 ? 1 : Dp / G;
-  const bool mine = static_cast<int>(threadIdx.x) < ngroups;
-  const int g0 = threadIdx.x * G;
-  S d[6];
+  if (threadIdx.x == 0) {
+    double a[21], nb[6], m[6][6], x[6];
+    int tr[6];
+#pragma unroll
+    for (int q = 0; q < 21; ++q) a[q] = s_acc[q * C];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) nb[i] = -s_acc[(21 + i) * C];
+    bool degen = false;
+    ldlt6_factor_reg<double>(a, m, tr, &degen);
+    ldlt6_apply_reg<double>(m, tr, nb, x);
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) s_m[6 * r + c] = m[r][c];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      s_tr[i] = tr[i];
+      s_x[i] = x[i];
+    }
+    s_degen = degen;
+  }
+  __syncthreads();
+  clock_mark(6, kSolveClockCta);
+  // channel threads: thread t < max(Dp, 1) owns channel t (thread 0 also the real part)
+  const bool mine = static_cast<int>(threadIdx.x) < (Dp > 0 ? Dp : 1);
+  L<1> d[6];
   if (mine) {
-    S a[21], nb[6];
+    const int ch = 1 + threadIdx.x;
+    if (Dp == 0) {
 #pragma unroll
-    for (int q = 0; q < 21; ++q) a[q] = load_ch<S>(sm + q * C, g0, G);
+      for (int i = 0; i < 6; ++i) {
+        d[i].re = s_x[i];
+        d[i].im[0] = 0.0;
+      }
+    } else if (!s_degen) {
+      double m[6][6];
+      int tr[6];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) nb[i] = -load_ch<S>(sm + (21 + i) * C, g0, G);
-    ldlt6_solve_reg<S>(a, nb, d);
-    (void)ws;
-    clock_mark(6);
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) m[r][c] = s_m[6 * r + c];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) tr[i] = s_tr[i];
+      double rhs[6], dx[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        double ax = 0.0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) ax = ax + s_acc[(i >= j ? tri(i, j) : tri(j, i)) * C + ch] * s_x[j];
+        rhs[i] = -s_acc[(21 + i) * C + ch] - ax;
+      }
+      ldlt6_apply_reg<double>(m, tr, rhs, dx);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        d[i].re = s_x[i];
+        d[i].im[0] = dx[i];
+      }
+    } else {
+      L<1> a[21], nb[6];
+#pragma unroll
+      for (int q = 0; q < 21; ++q) a[q] = load_ch<L<1>>(s_acc + q * C, threadIdx.x, 1);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) nb[i] = -load_ch<L<1>>(s_acc + (21 + i) * C, threadIdx.x, 1);
+      ldlt6_solve_reg<L<1>>(a, nb, d);
+    }
     bool fin = true;
 #pragma unroll
     for (int i = 0; i < 6; ++i) fin = fin && finite_s(d[i]);
     if (!fin) atomicAnd(&s_finite, 0);
   }
   __syncthreads();
-  Pose<S> np;
+  clock_mark(7, kSolveClockCta);
+  Pose<L<1>> np;
   if (mine) {
     if (!s_finite)
 #pragma unroll
-      for (int i = 0; i < 6; ++i) d[i] = lit<S>(0.0);
-    Pose<S> cur;
+      for (int i = 0; i < 6; ++i) d[i] = lit<L<1>>(0.0);
+    const int g0 = Dp > 0 ? static_cast<int>(threadIdx.x) : 0;
+    const int nv = Dp > 0 ? 1 : 0;
+    Pose<L<1>> cur;
 #pragma unroll
-    for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+    for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<L<1>>(pose + e * C, g0, nv);
 #pragma unroll
-    for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
-    np = compose(exp_map<S>(d), cur);
-    clock_mark(7);
+    for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<L<1>>(pose + (9 + e) * C, g0, nv);
+    np = compose(exp_map<L<1>>(d), cur);
   }
   __syncthreads();
   if (mine) {
+    const int g0 = Dp > 0 ? static_cast<int>(threadIdx.x) : 0;
+    const int nv = Dp > 0 ? 1 : 0;
 #pragma unroll
-    for (int e = 0; e < 9; ++e) store_ch<S>(pose + e * C, np.R.m[e], g0, G, threadIdx.x == 0);
+    for (int e = 0; e < 9; ++e) store_ch<L<1>>(pose + e * C, np.R.m[e], g0, nv, threadIdx.x == 0);
 #pragma unroll
-    for (int e = 0; e < 3; ++e) store_ch<S>(pose + (9 + e) * C, np.t.v[e], g0, G, threadIdx.x == 0);
+    for (int e = 0; e < 3; ++e) store_ch<L<1>>(pose + (9 + e) * C, np.t.v[e], g0, nv, threadIdx.x == 0);
   }
   if (threadIdx.x == 0) {
     double sq[6];
@@ -207,15 +316,8 @@ __device__ __noinline__ void icp_solve_block(TrackState* st, const double* parti
       if (level == 0) st->converged = 1;
     }
   }
-}
-
-template <int G>
-__global__ void __launch_bounds__(256) k_icp_solve(TrackState* st, const double* __restrict__ partials,
-                                                   const int* __restrict__ counts, int n_tiles, double* pose, int Dp,
-                                                   int level, double tol) {
-  if (st->level_done) return;
-  extern __shared__ double sm[];
-  icp_solve_block<G>(st, partials, counts, n_tiles, pose, Dp, level, tol, sm);
+  clock_mark(4, kSolveClockCta);
+  if (threadIdx.x == 0 && g_icp_clock) atomicAdd(&g_icp_clock_launch, 1u);
 }
 
 template <int G>
@@ -225,8 +327,10 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
                                                     const double* __restrict__ nre, const double* __restrict__ vim,
                                                     const double* __restrict__ nim, double d_max, double cos_max,
                                                     int Dp, int chunk, double* __restrict__ partials,
-                                                    int* __restrict__ counts, TrackState* st_rw, double* pose_rw,
-                                                    int level, double tol) {
+                                                    int* __restrict__ counts, double* __restrict__ gpartials,
+                                                    int* __restrict__ gcounts, unsigned* __restrict__ group_ctr) {
+  pdl_wait();
+  pdl_trigger();
   if (st->level_done) return;
   clock_mark(0);
   using S = Scal<G>;
@@ -236,7 +340,6 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
   double* s_intr = s_pose + 12 * C;
   double* s_jr = s_intr + 4 * C;
   __shared__ int s_wsum[kRedThreads / 32];
-  __shared__ int s_total;
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) s_pose[i] = pose[i];
   for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_intr[i] = intr[i];
   __syncthreads();
@@ -394,25 +497,7 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
   }
   if (threadIdx.x == 0) counts[blockIdx.x] = tile_count;
   clock_mark(2);
-  // The last CTA to finish runs the solve (no second launch per iteration).
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(&st_rw->pad[0]), 1u);
-    s_last = prev == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  if (threadIdx.x == 0) st_rw->pad[0] = 0;
-  __threadfence();
-  clock_mark(3);
-  if (Dp == 0)
-    icp_solve_block<0>(st_rw, partials, counts, gridDim.x, pose_rw, Dp, level, tol, sm);
-  else
-    icp_solve_block<1>(st_rw, partials, counts, gridDim.x, pose_rw, Dp, level, tol, sm);
-  clock_mark(4);
-  if (threadIdx.x == 0 && g_icp_clock) atomicAdd(&g_icp_clock_launch, 1u);
+  group_sum(partials, counts, n_acc, gpartials, gcounts, group_ctr);
 }
 
 // Level entry: the prediction pose is the current estimate (icp.cpp:191).
@@ -659,15 +744,19 @@ __global__ void __launch_bounds__(128) k_icp_solve2(const TrackState* st, const 
   for (int a = threadIdx.x; a < 27 * CG; a += blockDim.x) {
     const int q = a / CG, c = a % CG;
     const long long off = static_cast<long long>(q) * C + (c == 0 ? 0 : g0 + c);
+    // canonical two-level order: tiles in order within groups of kGroup,
+    // group totals in order (oracle tiled_normal_equations)
     double total = 0.0;
-    for (int t = 0; t < n_tiles; t += 32) {
-      double vals[32];
+    for (int t = 0; t < n_tiles; t += kGroup) {
+      double vals[kGroup];
 #pragma unroll
-      for (int k = 0; k < 32; ++k)
+      for (int k = 0; k < kGroup; ++k)
         vals[k] = t + k < n_tiles ? __ldcg(partials + static_cast<long long>(t + k) * 27 * C + off) : 0.0;
+      double gsum = 0.0;
 #pragma unroll
-      for (int k = 0; k < 32; ++k)
-        if (t + k < n_tiles) total = total + vals[k];
+      for (int k = 0; k < kGroup; ++k)
+        if (t + k < n_tiles) gsum = gsum + vals[k];
+      total = total + gsum;
     }
     s_acc[a] = total;
   }
@@ -840,10 +929,13 @@ int icp_tiles(int w, int h, int stride) {
 }
 
 // Slots per shared-memory chunk of the (J, r) rows.
+// (one pass over the tile's 256 slots whenever the rows fit: measured faster
+// than two half-tile passes at two CTAs per SM, bench r01)
 static int reduce_chunk(int C) {
   if (8 * C * (16 + 256 * 7) <= 200 * 1024) return 256;
   if (8 * C * (16 + 128 * 7) <= 200 * 1024) return 128;
-  return 64;
+  if (8 * C * (16 + 64 * 7) <= 200 * 1024) return 64;
+  return 32;
 }
 
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp) {
@@ -852,54 +944,78 @@ void launch_level_begin(const Launch& L, TrackState* st, const double* pose, dou
   chk("level_begin");
 }
 
+// Launch with programmatic stream serialization (see pdl_wait).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+size_t icp_partials_doubles(int C, int max_tiles) {
+  return static_cast<size_t>(max_tiles + (max_tiles + kGroup - 1) / kGroup) * 27 * C;
+}
+size_t icp_counts_ints(int max_tiles) {
+  return static_cast<size_t>(kMaxGroupCtr + max_tiles + (max_tiles + kGroup - 1) / kGroup);
+}
+
+// One ICP iteration: k_icp_reduce (association, lifted rows, tile sums, group
+// sums) then k_icp_solve_t.  Scratch layout: partials = [tiles][27C] then
+// [groups][27C]; counts = [kMaxGroupCtr] self-resetting group counters (zero
+// at allocation), [tiles], [groups].
 void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const double* depth, int w, int h,
                        int stride, const double* intr, double* pose, const double* vre, const double* nre,
                        const double* vim, const double* nim, double d_max, double cos_max, double* partials,
                        int* counts, int level, double tol) {
   const int C = 1 + Dp;
+  const int n_acc = 27 * C;
   const int chunk = reduce_chunk(C);
-  const size_t solve_smem = 27 * C + 48 * 2 * static_cast<size_t>(Dp > 0 ? Dp : 1);
-  const size_t smem = sizeof(double) * std::max<size_t>(16 * C + static_cast<size_t>(chunk) * 7 * C, solve_smem);
+  const size_t smem = sizeof(double) * (16 * C + static_cast<size_t>(chunk) * 7 * C);
   const int tiles = icp_tiles(w, h, stride);
-  // J/r rows are evaluated in channel groups of 2 (or 1): register-light,
+  const int groups = (tiles + kGroup - 1) / kGroup;
+  if (groups > kMaxGroupCtr || Dp > kMaxC - 1) {
+    std::fprintf(stderr, "csf_b200: ICP frame too large (%d tiles) or too many channels (%d)\n", tiles, Dp);
+    return;
+  }
+  unsigned* ctr = reinterpret_cast<unsigned*>(counts);
+  int* tcounts = counts + kMaxGroupCtr;
+  int* gcounts = tcounts + tiles;
+  double* gpartials = partials + static_cast<size_t>(tiles) * n_acc;
+  // J/r rows are evaluated in channel groups of 1 (or 2): register-light,
   // any width that divides Dp addresses the same channel layout.
   const int RG = G == 0 ? 0 : (std::getenv("CSF_ICP_RG2") ? (Dp % 2 == 0 ? 2 : 1) : 1);
   switch (RG) {
     case 0:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_icp_reduce<0><<<tiles, kRedThreads, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
-                                                      cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
+      launch_pdl(k_icp_reduce<0>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
+                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
       break;
     case 1:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_icp_reduce<1><<<tiles, kRedThreads, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
-                                                      cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
+      launch_pdl(k_icp_reduce<1>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
+                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
       break;
     default:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_icp_reduce<2><<<tiles, kRedThreads, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim, nim, d_max,
-                                                      cos_max, Dp, chunk, partials, counts, st, pose, level, tol);
+      launch_pdl(k_icp_reduce<2>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
+                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
   }
-  ++*L.launches;
+  launch_pdl(k_icp_solve_t, dim3(1), dim3(kRedThreads), 0, L.stream, st, static_cast<const double*>(gpartials),
+             static_cast<const int*>(gcounts), groups, pose, Dp, level, tol);
+  *L.launches += 2;
   chk("icp_reduce");
-}
-
-void launch_icp_solve(const Launch& L, int G, int Dp, TrackState* st, const double* partials, const int* counts,
-                      int n_tiles, double* pose, int level, double tol) {
-  // The solve is latency-bound and register-heavy (6x6 LDLT, exp map, pose
-  // compose): one thread per channel in L<1> arithmetic keeps it in registers.
-  const int GS = G == 0 ? 0 : 1;
-  const int ngroups = GS == 0 ? 1 : Dp;
-  const size_t smem = sizeof(double) * 27 * (1 + Dp) + sizeof(double) * (1 + GS) * 48 * ngroups;
-  if (GS == 0)
-    k_icp_solve<0><<<1, 256, smem, L.stream>>>(st, partials, counts, n_tiles, pose, Dp, level, tol);
-  else
-    k_icp_solve<1><<<1, 256, smem, L.stream>>>(st, partials, counts, n_tiles, pose, Dp, level, tol);
-  ++*L.launches;
-  chk("icp_solve");
 }
 
 void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,

@@ -523,7 +523,8 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
                                                        const double* __restrict__ intr, int w, int h, int Dp,
                                                        double near_clip, double far_clip, double step, Box box,
                                                        double2* __restrict__ hits, double* __restrict__ vre,
-                                                       double* __restrict__ nre) {
+                                                       double* __restrict__ nre, const double* __restrict__ atab,
+                                                       int n_tab) {
   __shared__ double s_pose[16];
   const int C = 1 + Dp;
   if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
@@ -577,6 +578,56 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
   for (int a = 0; a < 3; ++a) invd.v[a] = dir.v[a] != 0.0 ? 1.0 / dir.v[a] : 0.0;
   bool have_prev = false;
   double alpha_prev = 0.0, f_prev = 0.0;
+  if constexpr (V::kHashed) {
+    if (atab) {
+      // Every ray of a hashed volume marches the same alpha sequence (t0 =
+      // near, no slab clip): index it from the table instead of re-adding.
+      // Semantics are the loop below, sample for sample.
+      const int nmax = n_tab - 1;  // atab[nmax] > t1 (sentinel)
+      const double inv_step = 1.0 / step;
+      int n = 0;
+      while (n < nmax) {
+        const double alpha = atab[n];
+        const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1],
+                     pz = o.v[2] + alpha * dir.v[2];
+        const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
+                  k0 = ifloor((pz - vol.oz) / vol.vs);
+        const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
+        const int occ = vol.super_occupied(bx, by, bz);
+        int span = 0;
+        if (occ == 0) span = 8;
+        else if (vol.block(bx, by, bz) < 0) span = 1;
+        if (span > 0) {
+          have_prev = false;
+          const int m = span == 8 ? ~7 : ~0;
+          const double lim = box_exit(vol, bx & m, by & m, bz & m, span, o, invd) - 1e-6;
+          // first index > n whose alpha reaches lim (or the sentinel)
+          int g = static_cast<int>(fmin(fmax((lim - atab[0]) * inv_step, 0.0), static_cast<double>(nmax)));
+          g = g < n + 1 ? n + 1 : g;
+          while (g > n + 1 && __ldg(atab + g - 1) >= lim) --g;
+          while (g < nmax && __ldg(atab + g) < lim) ++g;
+          n = g;
+          continue;
+        }
+        double f;
+        if (!sample_real(vol, px, py, pz, cache, &f)) {
+          have_prev = false;
+          ++n;
+          continue;
+        }
+        if (have_prev && f_prev > 0.0 && f < 0.0) {
+          hits[pix] = make_double2(alpha_prev, alpha);
+          hits[w * h + pix] = make_double2(f_prev, f);
+          return;
+        }
+        have_prev = true;
+        alpha_prev = alpha;
+        f_prev = f;
+        ++n;
+      }
+      return;
+    }
+  }
   double alpha = t0;
   while (alpha <= t1) {
     const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1], pz = o.v[2] + alpha * dir.v[2];
@@ -1362,7 +1413,8 @@ size_t alloc_scan_bytes(int n) {
 template <typename V>
 static void raycast_impl(const Launch& L, const V& view, Box box, int order, int G, int Dp, const double* pose,
                          const double* intr, int w, int h, double near_clip, double far_clip, double step,
-                         double2* hits, double* vre, double* nre, double* vim, double* nim) {
+                         double2* hits, double* vre, double* nre, double* vim, double* nim,
+                         const double* atab = nullptr, int n_tab = 0) {
   const int P = w * h;
   if (L.phase != 2) {
     // The warp-cooperative march measured slower than one thread per ray at
@@ -1375,7 +1427,7 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
                                                                  step, box, hits, vre, nre);
     else
       k_raycast_march<V><<<(P + 127) / 128, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip,
-                                                                step, box, hits, vre, nre);
+                                                                step, box, hits, vre, nre, atab, n_tab);
     if (Dp > 0 && vim) {
       cudaMemsetAsync(vim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
       cudaMemsetAsync(nim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
@@ -1444,7 +1496,8 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
   const HashView view = hash_view(v, Dp);
   Box box;
   box.use = false;
-  raycast_impl(L, view, box, v.order, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
+  raycast_impl(L, view, box, v.order, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim,
+               v.alpha_tab, v.alpha_n);
   chk("raycast_hashed");
 }
 

@@ -1,0 +1,55 @@
+"""Summarise ncu --set full captures (gpurun_out/prof_<kernel>.ncu-rep) into
+profiles/traffic.json (DRAM bytes per launch per bench kernel category, read
+by bench.py's roofline `traffic`) and profiles/<round>_ncu_<kernel>.csv."""
+import csv
+import io
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+CATS = {"k_icp_reduce": "icp", "k_raycast_march": "raycast", "k_raycast_lift_coop": "raycast_lift",
+        "k_integrate_hashed": "integrate"}
+KEEP = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "dram__throughput",
+        "sm__throughput", "launch__registers_per_thread", "sm__warps_active", "launch__occupancy_limit",
+        "smsp__inst_executed", "sm__inst_executed_pipe_fp64", "l1tex__t_bytes", "lts__t_bytes", "launch__grid_size",
+        "launch__block_size", "sm__pipe_fp64_cycles_active", "smsp__average_warp", "achieved_occupancy")
+
+
+def to_bytes(v, unit):
+    f = float(str(v).replace(",", ""))
+    return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
+
+
+def main(workload="config2", rnd="r01"):
+    out = {}
+    for kern, cat in CATS.items():
+        rep = ROOT / "gpurun_out" / f"prof_{kern}.ncu-rep"
+        if not rep.exists():
+            continue
+        raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        if len(rows) < 3:
+            continue
+        head, units, vals = rows[0], rows[1], rows[2]
+        rec = {h: (v, u) for h, u, v in zip(head, units, vals)}
+        rd = to_bytes(*rec["dram__bytes_read.sum"])
+        wr = to_bytes(*rec["dram__bytes_write.sum"])
+        out[cat] = rd + wr
+        keep = [(h, u, v) for h, u, v in zip(head, units, vals) if h.startswith(KEEP) or h in ("Kernel Name",)]
+        with open(ROOT / "profiles" / f"{rnd}_ncu_{kern}.csv", "w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(["metric", "unit", "value"])
+            w.writerows(keep)
+        print(f"{cat:14s} {kern:24s} dram {out[cat] / 1e6:10.2f} MB  time {rec['gpu__time_duration.sum']}")
+    p = ROOT / "profiles" / "traffic.json"
+    d = json.loads(p.read_text()) if p.exists() else {}
+    d.setdefault("_note", "DRAM bytes (read+write) of ONE launch (frame 5, level 0 for per-level kernels) from "
+                          "ncu --set full --clock-control none; tools/ncu_capture.sh + tools/ncu_traffic.py")
+    d[workload] = out
+    p.write_text(json.dumps(d, indent=1))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
