@@ -27,6 +27,8 @@ __global__ void __launch_bounds__(kBX* kBY) k_bilateral(const float* __restrict_
                                                          const double* __restrict__ in_f64,
                                                          double* __restrict__ raw_out, double* __restrict__ out,
                                                          int w, int h, int radius, double inv2sr) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double tile[];
   const int tw = kBX + 2 * radius, th = kBY + 2 * radius;
   const int x0 = blockIdx.x * kBX - radius, y0 = blockIdx.y * kBY - radius;
@@ -71,6 +73,8 @@ __global__ void __launch_bounds__(kBX* kBY) k_bilateral(const float* __restrict_
 // frames.cpp:40-66 — output pixel (x, y) centred on input (2x, 2y).
 __global__ void k_downsample(const double* __restrict__ in, double* __restrict__ out, int w, int h, int wo, int ho,
                              double reject) {
+  pdl_wait();
+  pdl_trigger();
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= wo || y >= ho) return;
   const double tap[5] = {1.0 / 16, 4.0 / 16, 6.0 / 16, 4.0 / 16, 1.0 / 16};
@@ -107,6 +111,8 @@ __device__ V3<S> backproject_px(const S& d, int x, int y, const S& fx, const S& 
 
 __global__ void k_measure(const double* __restrict__ depth, int w, int h, const double* __restrict__ intr, int D,
                           double* __restrict__ vert, double* __restrict__ norm) {
+  pdl_wait();
+  pdl_trigger();
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= w || y >= h) return;
   using S = L<1>;
@@ -184,7 +190,7 @@ void launch_bilateral(const Launch& L, const float* in_f32, const double* in_f64
   const dim3 block(csfd::kBX, csfd::kBY);
   const dim3 grid((w + csfd::kBX - 1) / csfd::kBX, (h + csfd::kBY - 1) / csfd::kBY);
   const size_t smem = sizeof(double) * (csfd::kBX + 2 * radius) * (csfd::kBY + 2 * radius);
-  csfd::k_bilateral<<<grid, block, smem, L.stream>>>(in_f32, in_f64, raw_out, out, w, h, radius, inv2sr);
+  csfd::launch_pdl(csfd::k_bilateral, dim3(grid), dim3(block), smem, L.stream, in_f32, in_f64, raw_out, out, w, h, radius, inv2sr);
   ++*L.launches;
   check_launch("bilateral");
 }
@@ -192,7 +198,7 @@ void launch_bilateral(const Launch& L, const float* in_f32, const double* in_f64
 void launch_downsample(const Launch& L, const double* in, double* out, int w, int h, double sigma_r) {
   const int wo = w / 2, ho = h / 2;
   const dim3 block(32, 8), grid((wo + 31) / 32, (ho + 7) / 8);
-  csfd::k_downsample<<<grid, block, 0, L.stream>>>(in, out, w, h, wo, ho, 3.0 * sigma_r);
+  csfd::launch_pdl(csfd::k_downsample, dim3(grid), dim3(block), 0, L.stream, in, out, w, h, wo, ho, 3.0 * sigma_r);
   ++*L.launches;
   check_launch("downsample");
 }
@@ -200,7 +206,7 @@ void launch_downsample(const Launch& L, const double* in, double* out, int w, in
 void launch_measure(const Launch& L, const double* depth, int w, int h, const double* intr, int D, double* vert,
                     double* norm) {
   const dim3 block(32, 8), grid((w + 31) / 32, (h + 7) / 8);
-  csfd::k_measure<<<grid, block, 0, L.stream>>>(depth, w, h, intr, D, vert, norm);
+  csfd::launch_pdl(csfd::k_measure, dim3(grid), dim3(block), 0, L.stream, depth, w, h, intr, D, vert, norm);
   ++*L.launches;
   check_launch("measure");
 }

@@ -45,12 +45,6 @@ CSF_DEV void clock_mark(int slot, int cta = -1) {
 // the solve kernel records into CTA slot 511 of the iteration's record
 constexpr int kSolveClockCta = 511;
 
-// Programmatic dependent launch (sm_90+): the ICP iteration's kernels are
-// launched with programmatic stream serialization, so the next kernel is
-// scheduled while this one runs and waits here for its predecessor's
-// completion and memory instead of paying the full launch gap.
-CSF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-CSF_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 // 256 threads evaluate the tile's slots; all 320 sum accumulators (27*(1+Dp)
 // of them, one per thread up to Dp = 10), so no thread carries two.
 constexpr int kRedThreads = 320;
@@ -502,6 +496,8 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
 
 // Level entry: the prediction pose is the current estimate (icp.cpp:191).
 __global__ void k_level_begin(TrackState* st, const double* pose, double* pred_pose, int Dp) {
+  pdl_wait();
+  pdl_trigger();
   const int C = 1 + Dp;
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) pred_pose[i] = pose[i];
   if (threadIdx.x == 0) {
@@ -518,6 +514,8 @@ __global__ void k_level_begin(TrackState* st, const double* pose, double* pred_p
 template <int G>
 __global__ void k_seed(const int* __restrict__ dirs, int D, double hstep, const double* __restrict__ gt0,
                        const double* __restrict__ kbase, double* pose, double* intr_levels, int levels, int Dp) {
+  pdl_wait();
+  pdl_trigger();
   using S = Scal<G>;
   const int C = 1 + Dp;
   const int ngroups = G == 0 ? 1 : Dp / G;
@@ -549,6 +547,8 @@ __global__ void k_seed(const int* __restrict__ dirs, int D, double hstep, const 
 }
 
 __global__ void k_frame_begin(TrackState* st, int frame) {
+  pdl_wait();
+  pdl_trigger();
   st->frame = frame;
   st->pad[1] = 0;  // voxels fused this frame
   st->iterations = 0;
@@ -559,6 +559,8 @@ __global__ void k_frame_begin(TrackState* st, int frame) {
 
 __global__ void k_frame_end(const TrackState* st, const double* pose, double* traj, int Dp, int* stats,
                             const int* n_blocks, const int* counters) {
+  pdl_wait();
+  pdl_trigger();
   const int C = 1 + Dp;
   const int f = st->frame;
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) traj[static_cast<long long>(f) * 12 * C + i] = pose[i];
@@ -578,6 +580,8 @@ __global__ void k_frame_end(const TrackState* st, const double* pose, double* tr
 template <int G>
 __global__ void k_objective(const double* __restrict__ traj, const double* __restrict__ gt, int n_frames, int kind,
                             double hstep, int Dp, int D, double* out) {
+  pdl_wait();
+  pdl_trigger();
   using S = Scal<G>;
   const int C = 1 + Dp;
   const int ngroups = G == 0 ? 1 : Dp / G;
@@ -630,6 +634,8 @@ __global__ void __launch_bounds__(256) k_icp_reduce2(const TrackState* st, const
                                                      const double* __restrict__ nre, const double* __restrict__ vim,
                                                      const double* __restrict__ nim, double d_max, double cos_max,
                                                      int Dp, double* __restrict__ partials, int* __restrict__ counts) {
+  pdl_wait();
+  pdl_trigger();
   if (st->level_done) return;
   constexpr int G = Traits<S>::G;
   constexpr int CG = 1 + G;
@@ -733,6 +739,8 @@ template <typename S>
 __global__ void __launch_bounds__(128) k_icp_solve2(const TrackState* st, const double* __restrict__ partials,
                                                     const int* __restrict__ counts, int n_tiles, double* pose, int Dp,
                                                     double* stage) {
+  pdl_wait();
+  pdl_trigger();
   if (st->level_done) return;
   constexpr int G = Traits<S>::G;
   constexpr int CG = 1 + G;
@@ -814,6 +822,8 @@ __global__ void __launch_bounds__(128) k_icp_solve2(const TrackState* st, const 
 
 __global__ void k_icp_commit(TrackState* st, double* pose, int Dp, const double* __restrict__ stage, int level,
                              double tol) {
+  pdl_wait();
+  pdl_trigger();
   if (st->level_done) return;
   const int C = 1 + Dp;
   const int n = static_cast<int>(stage[13]);
@@ -837,6 +847,8 @@ template <typename S>
 __global__ void k_seed2(const int* __restrict__ pair_i, const int* __restrict__ pair_j, int n_pairs, double hstep,
                         const double* __restrict__ gt0, const double* __restrict__ kbase, double* pose,
                         double* intr_levels, int levels, int Dp) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int G = Traits<S>::G;
   const int C = 1 + Dp;
   const int gi = blockIdx.x * blockDim.x + threadIdx.x;
@@ -866,6 +878,8 @@ __global__ void k_seed2(const int* __restrict__ pair_i, const int* __restrict__ 
 template <typename S>
 __global__ void k_objective2(const double* __restrict__ traj, const double* __restrict__ gt, int n_frames, int kind,
                              int Dp, int n_pairs, double* out) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int G = Traits<S>::G;
   const int C = 1 + Dp;
   const int gi = blockIdx.x * blockDim.x + threadIdx.x;
@@ -939,26 +953,9 @@ static int reduce_chunk(int C) {
 }
 
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp) {
-  k_level_begin<<<1, 128, 0, L.stream>>>(st, pose, pred_pose, Dp);
+  launch_pdl(k_level_begin, dim3(1), dim3(128), 0, L.stream, st, pose, pred_pose, Dp);
   ++*L.launches;
   chk("level_begin");
-}
-
-// Launch with programmatic stream serialization (see pdl_wait).
-template <typename... KArgs, typename... Args>
-static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
-                       Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 size_t icp_partials_doubles(int C, int max_tiles) {
@@ -1021,22 +1018,22 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
 void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,
                  const double* intr_base, double* pose, double* intr_levels, int levels) {
   if (G == 0)
-    k_seed<0><<<1, 64, 0, L.stream>>>(dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp);
+    launch_pdl(k_seed<0>, dim3(1), dim3(64), 0, L.stream, dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp);
   else
-    k_seed<1><<<1, 64, 0, L.stream>>>(dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp);
+    launch_pdl(k_seed<1>, dim3(1), dim3(64), 0, L.stream, dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp);
   ++*L.launches;
   chk("seed");
 }
 
 void launch_frame_begin(const Launch& L, TrackState* st, int frame) {
-  k_frame_begin<<<1, 1, 0, L.stream>>>(st, frame);
+  launch_pdl(k_frame_begin, dim3(1), dim3(1), 0, L.stream, st, frame);
   ++*L.launches;
   chk("frame_begin");
 }
 
 void launch_frame_end(const Launch& L, TrackState* st, const double* pose, double* traj, int Dp, int* stats,
                       const int* n_blocks, const int* counters) {
-  k_frame_end<<<1, 128, 0, L.stream>>>(st, pose, traj, Dp, stats, n_blocks, counters);
+  launch_pdl(k_frame_end, dim3(1), dim3(128), 0, L.stream, st, pose, traj, Dp, stats, n_blocks, counters);
   ++*L.launches;
   chk("frame_end");
 }
@@ -1044,9 +1041,9 @@ void launch_frame_end(const Launch& L, TrackState* st, const double* pose, doubl
 void launch_objective(const Launch& L, int G, int Dp, int D, const double* traj, const double* gt, int n_frames,
                       int kind, double h, double* out) {
   if (G == 0)
-    k_objective<0><<<1, 64, 0, L.stream>>>(traj, gt, n_frames, kind, h, Dp, D, out);
+    launch_pdl(k_objective<0>, dim3(1), dim3(64), 0, L.stream, traj, gt, n_frames, kind, h, Dp, D, out);
   else
-    k_objective<1><<<1, 64, 0, L.stream>>>(traj, gt, n_frames, kind, h, Dp, D, out);
+    launch_pdl(k_objective<1>, dim3(1), dim3(64), 0, L.stream, traj, gt, n_frames, kind, h, Dp, D, out);
   ++*L.launches;
   chk("objective");
 }
@@ -1065,10 +1062,10 @@ void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double
     cudaFuncSetAttribute(k_icp_reduce2<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  k_icp_reduce2<S><<<dim3(tiles, pairs), kTile2, smem, L.stream>>>(st, depth, w, h, stride, intr, pose, vre, nre, vim,
+  launch_pdl(k_icp_reduce2<S>, dim3(dim3(tiles, pairs)), dim3(kTile2), smem, L.stream, st, depth, w, h, stride, intr, pose, vre, nre, vim,
                                                                    nim, d_max, cos_max, Dp, partials, counts);
-  k_icp_solve2<S><<<pairs, 128, 0, L.stream>>>(st, partials, counts, tiles, pose, Dp, stage);
-  k_icp_commit<<<1, 1, 0, L.stream>>>(st, pose, Dp, stage, level, tol);
+  launch_pdl(k_icp_solve2<S>, dim3(pairs), dim3(128), 0, L.stream, st, partials, counts, tiles, pose, Dp, stage);
+  launch_pdl(k_icp_commit, dim3(1), dim3(1), 0, L.stream, st, pose, Dp, stage, level, tol);
   *L.launches += 3;
   chk("icp_iteration2");
 }
@@ -1076,7 +1073,7 @@ void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double
 void launch_seed2(const Launch& L, int Dp, const int* pair_i, const int* pair_j, int n_pairs, double h,
                   const double* gt0, const double* intr_base, double* pose, double* intr_levels, int levels) {
   const int groups = Dp / 3;
-  k_seed2<B<1>><<<(groups + 63) / 64, 64, 0, L.stream>>>(pair_i, pair_j, n_pairs, h, gt0, intr_base, pose,
+  launch_pdl(k_seed2<B<1>>, dim3((groups + 63) / 64), dim3(64), 0, L.stream, pair_i, pair_j, n_pairs, h, gt0, intr_base, pose,
                                                          intr_levels, levels, Dp);
   ++*L.launches;
   chk("seed2");
@@ -1084,7 +1081,7 @@ void launch_seed2(const Launch& L, int Dp, const int* pair_i, const int* pair_j,
 
 void launch_objective2(const Launch& L, int Dp, int n_pairs, const double* traj, const double* gt, int n_frames,
                        int kind, double* out) {
-  k_objective2<B<1>><<<(n_pairs + 63) / 64, 64, 0, L.stream>>>(traj, gt, n_frames, kind, Dp, n_pairs, out);
+  launch_pdl(k_objective2<B<1>>, dim3((n_pairs + 63) / 64), dim3(64), 0, L.stream, traj, gt, n_frames, kind, Dp, n_pairs, out);
   ++*L.launches;
   chk("objective2");
 }

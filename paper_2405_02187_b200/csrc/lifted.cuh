@@ -13,6 +13,8 @@
 // reference's double pipeline).
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 #include "../../include/csf_detmath.h"
@@ -20,6 +22,34 @@
 #define CSF_DEV __device__ __forceinline__
 
 namespace csfd {
+
+// ----------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+).  Every kernel of the library is
+// launched with programmatic stream serialization (launch_pdl) and begins
+// with pdl_wait() — it waits for the previous kernel on the stream to
+// complete and its memory to be visible before touching anything — then
+// pdl_trigger() lets the next kernel be scheduled as soon as every CTA of
+// this one is resident.  The chain of dependent launches (~40 per frame)
+// then no longer pays the full launch gap between kernels.
+// ----------------------------------------------------------------------------
+CSF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+CSF_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ----------------------------------------------------------------------------
 // error flag: first error code wins (0 = ok)

@@ -230,6 +230,8 @@ template <typename S>
 __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const double* __restrict__ depth, int w,
                                                          int h, const double* __restrict__ pose,
                                                          const double* __restrict__ intr, int Dp, int* upd) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   stage_pose_w2c<S>(pose, intr, Dp, sm);
   const long long n = static_cast<long long>(vol.nx) * vol.ny * vol.nz;
@@ -255,6 +257,8 @@ __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const
                                                           const double* __restrict__ depth, int w, int h,
                                                           const double* __restrict__ pose,
                                                           const double* __restrict__ intr, int Dp, int* upd) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   stage_pose_w2c<S>(pose, intr, Dp, sm);
   const int n_vis = counters[0];
@@ -277,6 +281,8 @@ __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const
 }
 
 __global__ void k_init_volume(double2* rw, double* fim, long long n, int Dp) {
+  pdl_wait();
+  pdl_trigger();
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < n;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
     rw[v] = make_double2(1.0, 0.0);
@@ -290,6 +296,8 @@ __global__ void k_init_volume(double2* rw, double* fim, long long n, int Dp) {
 __global__ void k_band(const double* __restrict__ depth, int w, int h, const double* __restrict__ pose,
                        const double* __restrict__ intr, int C, double mu, double vs, double ox, double oy, double oz,
                        int K, unsigned long long* __restrict__ cand) {
+  pdl_wait();
+  pdl_trigger();
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= w || y >= h) return;
   const long long pix = static_cast<long long>(y) * w + x;
@@ -332,6 +340,8 @@ CSF_DEV unsigned set_hash(unsigned long long key, int bits) {
 
 __global__ void k_touch(const unsigned long long* __restrict__ cand, int n, unsigned long long* set_keys,
                         int* set_first, int* set_slot, int bits, int* err, int* counters) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const unsigned long long key = cand[s];
@@ -358,6 +368,8 @@ __global__ void k_touch(const unsigned long long* __restrict__ cand, int n, unsi
 __global__ void k_flags(HashView vol, const unsigned long long* __restrict__ cand, int n,
                         const int* __restrict__ set_first, const int* __restrict__ set_slot, int* first_flag,
                         int* new_flag, int* cand_block) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int hs = set_slot[s];
@@ -398,6 +410,8 @@ __global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int
                          const int* __restrict__ first_flag, const int* __restrict__ new_flag,
                          const int* __restrict__ first_rank, const int* __restrict__ new_rank,
                          const int* __restrict__ cand_block, int* visible, int* err) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n || !first_flag[s]) return;
   int id = cand_block[s];
@@ -434,6 +448,8 @@ __global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int
 
 __global__ void k_alloc_finalize(int* n_blocks, int max_blocks, const int* first_flag, const int* new_flag,
                                  const int* first_rank, const int* new_rank, int n, int* counters) {
+  pdl_wait();
+  pdl_trigger();
   const int n_vis = n > 0 ? first_rank[n - 1] + first_flag[n - 1] : 0;
   const int n_new = n > 0 ? new_rank[n - 1] + new_flag[n - 1] : 0;
   const int old = *n_blocks;
@@ -525,6 +541,8 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
                                                        double2* __restrict__ hits, double* __restrict__ vre,
                                                        double* __restrict__ nre, const double* __restrict__ atab,
                                                        int n_tab) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double s_pose[16];
   const int C = 1 + Dp;
   if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
@@ -737,6 +755,8 @@ __global__ void __launch_bounds__(128) k_raycast_lift_all(V vol, const double* _
                                                           const double2* __restrict__ hits, double* __restrict__ vre,
                                                           double* __restrict__ nre, double* __restrict__ vim,
                                                           double* __restrict__ nim) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   const int C = 1 + Dp;
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
@@ -877,6 +897,8 @@ __global__ void __launch_bounds__(256) k_raycast_lift_coop(V vol, const double* 
                                                            const double2* __restrict__ hits, double* __restrict__ vre,
                                                            double* __restrict__ nre, double* __restrict__ vim,
                                                            double* __restrict__ nim) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   const int C = 1 + Dp;
   LiftRec* recs = reinterpret_cast<LiftRec*>(sm + 16 * C);
@@ -1052,6 +1074,8 @@ __global__ void __launch_bounds__(128) k_raycast_march_warp(V vol, const double*
                                                             double near_clip, double far_clip, double step, Box box,
                                                             double2* __restrict__ hits, double* __restrict__ vre,
                                                             double* __restrict__ nre) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double s_pose[16];
   const int C = 1 + Dp;
   if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
@@ -1168,6 +1192,8 @@ __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __res
                                                       const double2* __restrict__ hits, double* __restrict__ vre,
                                                       double* __restrict__ nre, double* __restrict__ vim,
                                                       double* __restrict__ nim) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   const int C = 1 + Dp;
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
@@ -1323,7 +1349,7 @@ static int sm_count() {
 }
 
 void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp) {
-  k_init_volume<<<sm_count() * 8, 256, 0, L.stream>>>(rw, fim, n, Dp);
+  launch_pdl(k_init_volume, dim3(sm_count() * 8), dim3(256), 0, L.stream, rw, fim, n, Dp);
   ++*L.launches;
   chk("init_volume");
 }
@@ -1350,9 +1376,9 @@ void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, c
   const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
   const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, sm_count() * 16LL));
   if (v.order == 2)
-    k_integrate_dense<B<1>><<<grid, 256, smem, L.stream>>>(view, depth, w, h, pose, intr, Dp, upd);
+    launch_pdl(k_integrate_dense<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, depth, w, h, pose, intr, Dp, upd);
   else
-    CSF_DISPATCH_G(G, (k_integrate_dense<Scal<kG>><<<grid, 256, smem, L.stream>>>(view, depth, w, h, pose, intr, Dp,
+    CSF_DISPATCH_G(G, (launch_pdl(k_integrate_dense<Scal<kG>>, dim3(grid), dim3(256), smem, L.stream, view, depth, w, h, pose, intr, Dp,
                                                                                   upd)));
   ++*L.launches;
   chk("integrate_dense");
@@ -1365,10 +1391,10 @@ void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, c
   const size_t smem = sizeof(double) * 19 * (1 + Dp);
   const int grid = sm_count() * 8;
   if (v.order == 2)
-    k_integrate_hashed<B<1>><<<grid, 256, smem, L.stream>>>(view, v.coords, a.visible, a.counters, depth, w, h, pose,
+    launch_pdl(k_integrate_hashed<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, v.coords, a.visible, a.counters, depth, w, h, pose,
                                                             intr, Dp, upd);
   else
-    CSF_DISPATCH_G(G, (k_integrate_hashed<Scal<kG>><<<grid, 256, smem, L.stream>>>(
+    CSF_DISPATCH_G(G, (launch_pdl(k_integrate_hashed<Scal<kG>>, dim3(grid), dim3(256), smem, L.stream, 
                           view, v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd)));
   ++*L.launches;
   chk("integrate_hashed");
@@ -1388,17 +1414,17 @@ void launch_allocate(const Launch& L, const HashDev& v, int Dp, AllocScratch& a,
   cudaMemsetAsync(a.set_keys, 0xFF, sizeof(unsigned long long) << a.set_bits, L.stream);
   cudaMemsetAsync(a.set_first, 0x7F, sizeof(int) << a.set_bits, L.stream);
   const dim3 b2(32, 8), g2((w + 31) / 32, (h + 7) / 8);
-  k_band<<<g2, b2, 0, L.stream>>>(depth, w, h, pose, intr, C, v.mu, v.vs, v.ox, v.oy, v.oz, K, a.cand);
+  launch_pdl(k_band, dim3(g2), dim3(b2), 0, L.stream, depth, w, h, pose, intr, C, v.mu, v.vs, v.ox, v.oy, v.oz, K, a.cand);
   const int tb = 256, gb = (n + tb - 1) / tb;
-  k_touch<<<gb, tb, 0, L.stream>>>(a.cand, n, a.set_keys, a.set_first, a.set_slot, a.set_bits, L.err, a.counters);
-  k_flags<<<gb, tb, 0, L.stream>>>(view, a.cand, n, a.set_first, a.set_slot, a.first_flag, a.new_flag, a.cand_block);
+  launch_pdl(k_touch, dim3(gb), dim3(tb), 0, L.stream, a.cand, n, a.set_keys, a.set_first, a.set_slot, a.set_bits, L.err, a.counters);
+  launch_pdl(k_flags, dim3(gb), dim3(tb), 0, L.stream, view, a.cand, n, a.set_first, a.set_slot, a.first_flag, a.new_flag, a.cand_block);
   size_t bytes = a.cub_tmp_bytes;
   cub::DeviceScan::ExclusiveSum(a.cub_tmp, bytes, a.first_flag, a.first_rank, n, L.stream);
   bytes = a.cub_tmp_bytes;
   cub::DeviceScan::ExclusiveSum(a.cub_tmp, bytes, a.new_flag, a.new_rank, n, L.stream);
-  k_insert<<<gb, tb, 0, L.stream>>>(view, v.heads, v.keys, v.next, v.coords, v.n_blocks, v.max_blocks, a.cand, n,
+  launch_pdl(k_insert, dim3(gb), dim3(tb), 0, L.stream, view, v.heads, v.keys, v.next, v.coords, v.n_blocks, v.max_blocks, a.cand, n,
                                     a.first_flag, a.new_flag, a.first_rank, a.new_rank, a.cand_block, a.visible, L.err);
-  k_alloc_finalize<<<1, 1, 0, L.stream>>>(v.n_blocks, v.max_blocks, a.first_flag, a.new_flag, a.first_rank,
+  launch_pdl(k_alloc_finalize, dim3(1), dim3(1), 0, L.stream, v.n_blocks, v.max_blocks, a.first_flag, a.new_flag, a.first_rank,
                                           a.new_rank, n, a.counters);
   *L.launches += 7;
   chk("allocate");
@@ -1423,10 +1449,10 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
                                                 ? std::atoll(std::getenv("CSF_MARCH_WARP_MAX"))
                                                 : 0;
     if (P <= warp_threshold)
-      k_raycast_march_warp<V><<<(P + 3) / 4, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip,
+      launch_pdl(k_raycast_march_warp<V>, dim3((P + 3) / 4), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp, near_clip, far_clip,
                                                                  step, box, hits, vre, nre);
     else
-      k_raycast_march<V><<<(P + 127) / 128, 128, 0, L.stream>>>(view, pose, intr, w, h, Dp, near_clip, far_clip,
+      launch_pdl(k_raycast_march<V>, dim3((P + 127) / 128), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp, near_clip, far_clip,
                                                                 step, box, hits, vre, nre, atab, n_tab);
     if (Dp > 0 && vim) {
       cudaMemsetAsync(vim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
@@ -1439,7 +1465,7 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
   if (order == 2) {
     // second order: one thread per (hit pixel, pair) in Bicomplex arithmetic
     const long long items = static_cast<long long>(P) * (Dp / 3);
-    k_raycast_lift<B<1>, V><<<static_cast<int>((items + 127) / 128), 128, smem, L.stream>>>(view, pose, intr, w, h,
+    launch_pdl(k_raycast_lift<B<1>, V>, dim3(static_cast<int>((items + 127) / 128)), dim3(128), smem, L.stream, view, pose, intr, w, h,
                                                                                           Dp, hits, vre, nre, vim, nim);
     *L.launches += 1;
     return;
@@ -1456,13 +1482,13 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
       cudaFuncSetAttribute(k_raycast_lift_coop<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
       attr = true;
     }
-    k_raycast_lift_coop<V><<<(P + kLiftPix - 1) / kLiftPix, 8 * kLiftPix, smem_c, L.stream>>>(
+    launch_pdl(k_raycast_lift_coop<V>, dim3((P + kLiftPix - 1) / kLiftPix), dim3(8 * kLiftPix), smem_c, L.stream, 
         view, pose, intr, w, h, Dp, hits, vre, nre, vim, nim);
     *L.launches += 1;
     return;
   }
   if (G > 0 && mode == 1) {
-    k_raycast_lift_all<V><<<(P + 127) / 128, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits, vre, nre, vim,
+    launch_pdl(k_raycast_lift_all<V>, dim3((P + 127) / 128), dim3(128), smem, L.stream, view, pose, intr, w, h, Dp, hits, vre, nre, vim,
                                                                     nim);
     *L.launches += 1;
     return;
@@ -1471,7 +1497,7 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
   const int passes = RG == 0 ? 1 : Dp / RG;
   const long long items = static_cast<long long>(P) * passes;
   const int grid = static_cast<int>((items + 127) / 128);
-  CSF_DISPATCH_RG(RG, (k_raycast_lift<Scal<kG>, V><<<grid, 128, smem, L.stream>>>(view, pose, intr, w, h, Dp, hits,
+  CSF_DISPATCH_RG(RG, (launch_pdl(k_raycast_lift<Scal<kG>, V>, dim3(grid), dim3(128), smem, L.stream, view, pose, intr, w, h, Dp, hits,
                                                                                   vre, nre, vim, nim)));
   *L.launches += 1;
 }
