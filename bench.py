@@ -383,6 +383,9 @@ def main():
         "profiled_ms_per_step": prof_ms / args.steps,
         ("hessian_pairs" if second else "gradient"): [float(x) for x in cols],
         "blocks_allocated": int(stats[-1, 3]),
+        "per_frame": {"visible_blocks": float(stats[:n, 4].mean()), "fused_voxels": float(stats[:n, 6].mean()),
+                      "icp_iterations": float(stats[1:n, 0].mean()) if n > 1 else 0.0,
+                      "correspondences": float(stats[1:n, 1].mean()) if n > 1 else 0.0},
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

@@ -124,9 +124,15 @@ CSF_DEV void count_updates(int* upd, bool fused) {
 // and each channel costs one 19-term contraction instead of a full lifted
 // re-evaluation (rounding differs from the per-operation rule by a few ulp).
 // Shared-memory layout as stage_pose_w2c: w2c[12][C], centre[3][C], intr[4][C].
+// NDP > 0: the channel count is a compile-time constant, so the voxel's
+// (F.re, W) and all channel loads are issued together as soon as the voxel is
+// known to fuse (one DRAM round trip instead of one per channel); NDP == 0
+// keeps the runtime channel loop.
+template <int NDP>
 CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, double py, double pz,
                                 const double* __restrict__ depth, int w, int h, double mu, double cap, int Dp,
                                 const double* sm) {
+  if constexpr (NDP > 0) Dp = NDP;
   const int C = 1 + Dp;
   double R[9], t[3], c[3];
 #pragma unroll
@@ -169,6 +175,22 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
   double psi = 1.0 < q ? 1.0 : q;
   psi = -1.0 > psi ? -1.0 : psi;
   const bool sat = 1.0 < q || -1.0 > q;
+  // issue the voxel's loads before the reverse sweep
+  double chan[NDP > 0 ? NDP : 1];
+  if constexpr (NDP > 0) {
+    const double* src = vox.fim + v * NDP;
+    if constexpr (NDP % 2 == 0) {
+#pragma unroll
+      for (int d = 0; d < NDP; d += 2) {
+        const double2 t = __ldcs(reinterpret_cast<const double2*>(src + d));
+        chan[d] = t.x;
+        chan[d + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < NDP; ++d) chan[d] = __ldcs(src + d);
+    }
+  }
   const double2 rw = vox.rw[v];
   const double wt = rw.y;
   const double fre = (wt * rw.x + psi) / (wt + 1.0);
@@ -214,11 +236,29 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
     }
     const double inv_w1 = 1.0 / (wt + 1.0);
     double* fim = vox.fim + v * vox.Dp;
-    for (int d = 0; d < Dp; ++d) {
-      double pim = 0.0;
+    if constexpr (NDP > 0) {
 #pragma unroll
-      for (int k = 0; k < 19; ++k) pim = fma(g[k], sm[k * C + 1 + d], pim);
-      fim[d] = (wt * fim[d] + pim) * inv_w1;
+      for (int d = 0; d < NDP; ++d) {
+        double pim = 0.0;
+#pragma unroll
+        for (int k = 0; k < 19; ++k) pim = fma(g[k], sm[k * C + 1 + d], pim);
+        chan[d] = (wt * chan[d] + pim) * inv_w1;
+      }
+      if constexpr (NDP % 2 == 0) {
+#pragma unroll
+        for (int d = 0; d < NDP; d += 2)
+          __stcs(reinterpret_cast<double2*>(fim + d), make_double2(chan[d], chan[d + 1]));
+      } else {
+#pragma unroll
+        for (int d = 0; d < NDP; ++d) __stcs(fim + d, chan[d]);
+      }
+    } else {
+      for (int d = 0; d < Dp; ++d) {
+        double pim = 0.0;
+#pragma unroll
+        for (int k = 0; k < 19; ++k) pim = fma(g[k], sm[k * C + 1 + d], pim);
+        fim[d] = (wt * fim[d] + pim) * inv_w1;
+      }
     }
   }
   const double wn = wt + 1.0;
@@ -226,7 +266,7 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
   return true;
 }
 
-template <typename S>
+template <typename S, int NDP = 0>
 __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const double* __restrict__ depth, int w,
                                                          int h, const double* __restrict__ pose,
                                                          const double* __restrict__ intr, int Dp, int* upd) {
@@ -244,13 +284,13 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     const double py = vol.oy + vol.vs * static_cast<double>(j);
     const double pz = vol.oz + vol.vs * static_cast<double>(k);
     if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
-      count_updates(upd, fuse_voxel_adjoint(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+      count_updates(upd, fuse_voxel_adjoint<NDP>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
     else
       count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
   }
 }
 
-template <typename S>
+template <typename S, int NDP = 0>
 __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const int* __restrict__ coords,
                                                           const int* __restrict__ visible,
                                                           const int* __restrict__ counters,
@@ -273,7 +313,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const
       const double pz = vol.oz + vol.vs * static_cast<double>(8 * bz + lz);
       const long long vv = static_cast<long long>(b) * kBlockVoxels + l;
       if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
-        count_updates(upd, fuse_voxel_adjoint(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+        count_updates(upd, fuse_voxel_adjoint<NDP>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
       else
         count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
     }
@@ -1296,6 +1336,22 @@ int pick_group(int D) {
     default: std::fprintf(stderr, "csf_b200: no kernel for group width %d\n", G); \
   }
 
+// Compile-time channel counts of the adjoint fusion kernels (all channel
+// loads of a voxel issued together); other counts use the runtime loop.
+static bool fixed_channels(int Dp) { return (Dp >= 1 && Dp <= 12) || Dp == 16 || Dp == 20 || Dp == 24; }
+#define CSF_DISPATCH_NDP(Dp, BODY)                                                       \
+  switch (Dp) {                                                                         \
+    case 1: { constexpr int kN = 1; BODY; } break;    case 2: { constexpr int kN = 2; BODY; } break;   \
+    case 3: { constexpr int kN = 3; BODY; } break;    case 4: { constexpr int kN = 4; BODY; } break;   \
+    case 5: { constexpr int kN = 5; BODY; } break;    case 6: { constexpr int kN = 6; BODY; } break;   \
+    case 7: { constexpr int kN = 7; BODY; } break;    case 8: { constexpr int kN = 8; BODY; } break;   \
+    case 9: { constexpr int kN = 9; BODY; } break;    case 10: { constexpr int kN = 10; BODY; } break; \
+    case 11: { constexpr int kN = 11; BODY; } break;  case 12: { constexpr int kN = 12; BODY; } break; \
+    case 16: { constexpr int kN = 16; BODY; } break;  case 20: { constexpr int kN = 20; BODY; } break; \
+    case 24: { constexpr int kN = 24; BODY; } break;                                               \
+    default: std::fprintf(stderr, "csf_b200: no fusion kernel for %d channels\n", Dp);            \
+  }
+
 // The raycast's lifted epilogue is register-heavy: it evaluates channel
 // groups of width 2 (or 1) regardless of the volume's group width.
 static int raycast_group(int G, int Dp) {
@@ -1377,9 +1433,12 @@ void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, c
   const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, sm_count() * 16LL));
   if (v.order == 2)
     launch_pdl(k_integrate_dense<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, depth, w, h, pose, intr, Dp, upd);
-  else
-    CSF_DISPATCH_G(G, (launch_pdl(k_integrate_dense<Scal<kG>>, dim3(grid), dim3(256), smem, L.stream, view, depth, w, h, pose, intr, Dp,
-                                                                                  upd)));
+  else if (kAdjointFusion && G > 0 && fixed_channels(Dp)) {
+    CSF_DISPATCH_NDP(Dp, (launch_pdl(k_integrate_dense<csfd::L<1>, kN>, dim3(grid), dim3(256), smem, L.stream, view,
+                                     depth, w, h, pose, intr, Dp, upd)));
+  } else
+    CSF_DISPATCH_G(G, (launch_pdl(k_integrate_dense<Scal<kG>>, dim3(grid), dim3(256), smem, L.stream, view, depth, w,
+                                  h, pose, intr, Dp, upd)));
   ++*L.launches;
   chk("integrate_dense");
 }
@@ -1391,11 +1450,14 @@ void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, c
   const size_t smem = sizeof(double) * 19 * (1 + Dp);
   const int grid = sm_count() * 8;
   if (v.order == 2)
-    launch_pdl(k_integrate_hashed<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, v.coords, a.visible, a.counters, depth, w, h, pose,
-                                                            intr, Dp, upd);
-  else
-    CSF_DISPATCH_G(G, (launch_pdl(k_integrate_hashed<Scal<kG>>, dim3(grid), dim3(256), smem, L.stream, 
-                          view, v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd)));
+    launch_pdl(k_integrate_hashed<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, v.coords, a.visible,
+               a.counters, depth, w, h, pose, intr, Dp, upd);
+  else if (kAdjointFusion && G > 0 && fixed_channels(Dp)) {
+    CSF_DISPATCH_NDP(Dp, (launch_pdl(k_integrate_hashed<csfd::L<1>, kN>, dim3(grid), dim3(256), smem, L.stream, view,
+                                     v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd)));
+  } else
+    CSF_DISPATCH_G(G, (launch_pdl(k_integrate_hashed<Scal<kG>>, dim3(grid), dim3(256), smem, L.stream, view,
+                                  v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd)));
   ++*L.launches;
   chk("integrate_hashed");
 }
