@@ -191,10 +191,23 @@ int csf_raycast(csf_volume vol, const double* pose, const double* intr, int w, i
                 double* vertices, double* normals);
 
 /* ---- icp: icp.cpp:169-244 ----------------------------------------------------
- * Coarse-to-fine tracking of one frame against a volume's real channel
- * (solver CSF_SOLVER_LINEARIZED; canonical slot-tiled reduction order). */
+ * Coarse-to-fine tracking of one frame against a volume's real channel, every
+ * solver family of the reference: linearized (canonical slot-tiled normal
+ * equations), Newton (CSFD gradient + Hessian of icp_energy, Levenberg
+ * damping and the -g line search of descent.hpp:109-144), gradient descent
+ * and Polak-Ribiere NCG (descent.hpp:58-101).  result->final_loss is the
+ * last iteration's loss_after / correspondences (icp.cpp:207-209). */
 int csf_track_frame(csf_volume vol, const double* depth, int w, int h, const double* init_pose,
                     const csf_intrinsics* k, const csf_icp_cfg* cfg, double* out_pose, csf_track_result* result);
+
+/* icp.hpp:70-91 — icp_energy(corrs, xi, base) with the pairwise_sum tree
+ * (diff.hpp:16-37); gradient (optional) = the 6 Complex passes of
+ * icp_gradient, hessian (optional, [36] row-major) = the 21 Bicomplex passes
+ * of icp_hessian, evaluated at xi (NULL = 0) as one packed device pass.
+ * corrs [n][9] = vertex (camera), model vertex, model normal (world) per
+ * correspondence (icp.hpp:27-31); base [12] camera->world. */
+int csf_icp_energy_derivs(csf_ctx ctx, const double* corrs, int n, const double* base, const double* xi, double h,
+                          double* energy, double* gradient, double* hessian);
 
 /* ---- pipeline ------------------------------------------------------------ */
 int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf_pipeline* out);

@@ -44,6 +44,7 @@ def lib() -> C.CDLL:
                                      dp, C.POINTER(_capi.TrackResult)]),
             "orc_workload": (ip, [ip, ip, ip, ip, fp, dp, C.POINTER(_capi.Intrinsics)]),
             "orc_pipeline_run": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, i32p, dp]),
+            "orc_icp_energy_derivs": (ip, [dp, ip, dp, dp, C.c_double, dp, dp, dp]),
             "orc_pipeline_hessian": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, dp, dp, i32p, dp]),
         }
         for name, (res, args) in sig.items():
@@ -210,3 +211,16 @@ def pipeline_hessian(cfg, depth, gt):
                                       _dp(g1), _dp(g2), C.byref(obj), _dp(poses),
                                       stats.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(secs)))
     return hess, g1, g2, obj.value, poses, stats, secs.value
+
+
+def icp_energy_derivs(corrs, base12, xi=None, h=1e-8):
+    """icp_energy / icp_gradient / icp_hessian of the reference restatement."""
+    c = np.ascontiguousarray(corrs, dtype=np.float64).reshape(-1, 9)
+    b = np.ascontiguousarray(base12, dtype=np.float64)
+    x = None if xi is None else np.ascontiguousarray(xi, dtype=np.float64)
+    E = C.c_double()
+    g = np.empty(6)
+    H = np.empty((6, 6))
+    _check(lib().orc_icp_energy_derivs(_dp(c) if c.size else None, c.shape[0], _dp(b), _dp(x) if x is not None else None,
+                                       h, C.byref(E), _dp(g), _dp(H)))
+    return E.value, g, H

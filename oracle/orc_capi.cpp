@@ -376,6 +376,38 @@ void write_stats(int n_frames, const std::vector<int>& it, const std::vector<int
 
 extern "C" {
 
+// icp_energy / icp_gradient / icp_hessian (icp.hpp:70-91) at xi (NULL = 0).
+int orc_icp_energy_derivs(const double* corrs, int n, const double* base, const double* xi, double h, double* E,
+                          double* g, double* H) {
+  return guard([&] {
+    std::vector<Correspondence> cs(n);
+    for (int i = 0; i < n; ++i) {
+      const double* c = corrs + 9 * i;
+      cs[i].vertex = Vec3d(c[0], c[1], c[2]);
+      cs[i].model_vertex = Vec3d(c[3], c[4], c[5]);
+      cs[i].model_normal = Vec3d(c[6], c[7], c[8]);
+    }
+    Pose b;
+    for (int e = 0; e < 9; ++e) b.rotation(e / 3, e % 3) = base[e];
+    for (int e = 0; e < 3; ++e) b.translation[e] = base[9 + e];
+    Vec6<double> x{};
+    if (xi)
+      for (int k = 0; k < 6; ++k) x[k] = xi[k];
+    const StepSize step(h);
+    auto f = [&](const auto& v) { return icp_energy(cs, v, b); };
+    if (E) *E = icp_energy(cs, x, b);
+    if (g) {
+      const Vec6<double> gr = csfd_gradient(f, x, step);
+      for (int k = 0; k < 6; ++k) g[k] = gr[k];
+    }
+    if (H) {
+      const Mat6d hs = csfd_hessian(f, x, step);
+      for (int r = 0; r < 6; ++r)
+        for (int c = 0; c < 6; ++c) H[6 * r + c] = hs[r][c];
+    }
+  });
+}
+
 // Second-order run: one Bicomplex pass per pair (csfd_hessian pattern).
 int orc_pipeline_hessian(const csf_pipeline_cfg* c, const float* depth, const double* gt_in, int n_frames,
                          double* hessian, double* grad1, double* grad2, double* objective, double* poses,

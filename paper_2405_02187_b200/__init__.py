@@ -32,6 +32,7 @@ from . import capi as _capi
 __all__ = [
     "InvalidArgument", "DomainError", "Context", "bilateral_filter", "downsample_depth", "build_depth_pyramid",
     "measure_surface", "TsdfVolume", "HashedVolume", "surface_update", "raycast", "track_frame", "TrackResult",
+    "icp_energy", "icp_loss", "icp_gradient", "icp_hessian", "icp_energy_derivs",
     "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
     "lift_pose", "lift_intrinsics", "library",
 ]
@@ -378,7 +379,8 @@ class TrackResult:
 
 
 def track_frame(volume: _Volume, depth, init_camera_to_world, k, cfg: Optional[_capi.IcpCfg] = None) -> TrackResult:
-    """icp.cpp:169-244 on the device (linearized solver)."""
+    """icp.cpp:169-244 on the device, every solver family (cfg.solver:
+    linearized, Newton — the reference default — gradient descent, NCG)."""
     ctx = volume.ctx
     d = _f64(depth)
     h, w = d.shape
@@ -389,6 +391,55 @@ def track_frame(volume: _Volume, depth, init_camera_to_world, k, cfg: Optional[_
     ctx.check(ctx.lib.csf_track_frame(volume.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg), _dp(out),
                                       C.byref(res)))
     return TrackResult(out, res.iterations, bool(res.converged), res.final_loss, res.correspondences)
+
+
+# ----------------------------------------------------------------------------- icp energy
+def _corrs(corrs) -> np.ndarray:
+    """Correspondences as (n, 9): vertex (camera), model vertex, model normal (world) — icp.hpp:27-31."""
+    c = np.ascontiguousarray(corrs, dtype=np.float64)
+    if c.ndim == 3 and c.shape[1:] == (3, 3):
+        c = c.reshape(-1, 9)
+    if c.ndim != 2 or c.shape[1] != 9:
+        raise InvalidArgument(f"correspondences must be (n, 9) or (n, 3, 3); got {c.shape}")
+    return np.ascontiguousarray(c)
+
+
+def _energy(corrs, base, xi, h, want_g, want_h, ctx):
+    c = _ctx(ctx)
+    cc = _corrs(corrs)
+    b = lift_pose(base, 0)[:, 0].copy()
+    x = np.zeros(6) if xi is None else _f64(xi).reshape(6)
+    E = C.c_double()
+    g = np.zeros(6)
+    H = np.zeros((6, 6))
+    c.check(c.lib.csf_icp_energy_derivs(c.h, _dp(cc) if cc.size else None, cc.shape[0], _dp(b), _dp(x), h,
+                                        C.byref(E), _dp(g) if want_g else None, _dp(H) if want_h else None))
+    return E.value, g, H
+
+
+def icp_energy(corrs, xi, base, ctx: Optional[Context] = None) -> float:
+    """icp.hpp:70-85: sum over correspondences of ((exp(xi) base v - mv) . mn)^2, pairwise_sum tree."""
+    return _energy(corrs, base, xi, 1e-8, False, False, ctx)[0]
+
+
+def icp_loss(corrs, base, ctx: Optional[Context] = None) -> float:
+    """icp.cpp:128-130: icp_energy at xi = 0."""
+    return _energy(corrs, base, None, 1e-8, False, False, ctx)[0]
+
+
+def icp_gradient(corrs, base, h: float = 1e-8, ctx: Optional[Context] = None) -> np.ndarray:
+    """icp.cpp:132-137: CSFD gradient (6 Complex passes, one packed device pass)."""
+    return _energy(corrs, base, None, h, True, False, ctx)[1]
+
+
+def icp_hessian(corrs, base, h: float = 1e-8, ctx: Optional[Context] = None) -> np.ndarray:
+    """icp.cpp:139-144: CSFD Hessian (21 Bicomplex passes, mirrored; one packed device pass)."""
+    return _energy(corrs, base, None, h, False, True, ctx)[2]
+
+
+def icp_energy_derivs(corrs, base, xi=None, h: float = 1e-8, ctx: Optional[Context] = None):
+    """(energy, gradient[6], hessian[6,6]) at xi in one device call (csf_icp_energy_derivs)."""
+    return _energy(corrs, base, xi, h, True, True, ctx)
 
 
 # ----------------------------------------------------------------------------- pipeline

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -16,6 +18,7 @@
 #include "../../include/csf_b200.h"
 #include "../../include/csf_detmath.h"
 #include "csf_internal.h"
+#include "geometry.cuh"
 
 namespace csfi {
 void icp_clock_enable(unsigned long long* buf);
@@ -57,6 +60,9 @@ struct csf_ctx_s {
   unsigned long long launches = 0;
   std::string last_error;
   Profiler prof;
+  EnergyScratch energy;     // icp energy / correspondence-list scratch
+  double* corr_upload = nullptr;
+  size_t corr_upload_cap = 0;
 };
 
 // Brackets a launch with events when profiling is on.
@@ -370,6 +376,8 @@ extern "C" int csf_ctx_destroy(csf_ctx ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_err) cudaFree(ctx->d_err);
+  energy_scratch_release(ctx->energy);
+  if (ctx->corr_upload) cudaFree(ctx->corr_upload);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return CSF_OK;
@@ -1044,6 +1052,126 @@ extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const d
 // ---------------------------------------------------------------------------
 // track_frame (real tracker on the device)
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// icp energy and its CSFD derivatives (icp.hpp:70-91)
+// ---------------------------------------------------------------------------
+extern "C" int csf_icp_energy_derivs(csf_ctx ctx, const double* corrs, int n, const double* base, const double* xi,
+                                     double h, double* energy, double* gradient, double* hessian) {
+  if (!ctx || (n > 0 && !corrs) || !base || n < 0) return CSF_EINVAL;
+  if (!(h > 0.0) || h > 1e-6) return fail(ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
+  cudaSetDevice(ctx->device);
+  const size_t need = static_cast<size_t>(std::max(n, 1)) * 9;
+  if (ctx->corr_upload_cap < need) {
+    if (ctx->corr_upload) cudaFree(ctx->corr_upload);
+    ctx->corr_upload = nullptr;
+    ctx->corr_upload_cap = 0;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->corr_upload, sizeof(double) * need));
+    ctx->corr_upload_cap = need;
+  }
+  if (n > 0)
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->corr_upload, corrs, sizeof(double) * 9 * n, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+  const int order = hessian ? 2 : (gradient ? 1 : 0);
+  const int rc = icp_energy_derivs(ctx->stream, ctx->energy, ctx->corr_upload, n, base, xi, h, order, energy, gradient,
+                                   hessian);
+  if (rc == 5) return fail(ctx, CSF_ENOMEM, "csf_icp_energy_derivs: out of device memory");
+  if (rc) return fail(ctx, CSF_ECUDA, "csf_icp_energy_derivs: CUDA error");
+  return sync_check(ctx, "csf_icp_energy_derivs");
+}
+
+// ---------------------------------------------------------------------------
+// track_frame (icp.cpp:169-244) — every solver family.  The per-pixel work
+// (bilateral filter, pyramid, raycast, association, normal equations,
+// energies and their CSFD derivatives) runs on the device; the 6-vector
+// step logic of descent.hpp stays on the host, as in the reference.
+// ---------------------------------------------------------------------------
+namespace {
+
+using Vec6h = std::array<double, 6>;
+
+double sum6h(const Vec6h& a) { return (a[0] + (a[1] + a[2])) + (a[3] + (a[4] + a[5])); }
+double dot6h(const Vec6h& a, const Vec6h& b) {
+  Vec6h p;
+  for (int i = 0; i < 6; ++i) p[i] = a[i] * b[i];
+  return sum6h(p);
+}
+double norm6h(const Vec6h& a) { return std::sqrt(dot6h(a, a)); }
+
+// descent.hpp:16-21 (LineSearchConfig defaults)
+struct LineSearch {
+  double initial_step = 1.0, shrink = 0.5, sufficient_decrease = 1e-4;
+  int max_backtracks = 25;
+};
+
+// descent.hpp:34-52
+template <typename F>
+bool backtracking(F&& loss_at, double loss0, double slope, const LineSearch& cfg, double* alpha_out,
+                  double* loss_out, int* err) {
+  double alpha = cfg.initial_step;
+  for (int k = 0; k < cfg.max_backtracks; ++k) {
+    const double trial = loss_at(alpha, err);
+    if (*err) return false;
+    if (trial <= loss0 + cfg.sufficient_decrease * alpha * slope) {
+      *alpha_out = alpha;
+      *loss_out = trial;
+      return true;
+    }
+    alpha *= cfg.shrink;
+  }
+  return false;
+}
+
+// descent.hpp:58-101 (GradientStepper: GD or Polak-Ribiere NCG with restarts)
+struct Stepper {
+  bool ncg;
+  int restart_every;
+  int since_restart = 0;
+  bool have_previous = false;
+  Vec6h prev_g{}, prev_d{};
+  void reset() {
+    have_previous = false;
+    since_restart = 0;
+  }
+  Vec6h propose(const Vec6h& g) {
+    Vec6h neg;
+    for (int i = 0; i < 6; ++i) neg[i] = -g[i];
+    if (!ncg) return neg;
+    bool restart = !have_previous || since_restart >= restart_every || dot6h(prev_g, prev_g) == 0.0;
+    Vec6h dir = neg;
+    if (!restart) {
+      Vec6h diff;
+      for (int i = 0; i < 6; ++i) diff[i] = g[i] - prev_g[i];
+      const double beta = std::max(0.0, dot6h(g, diff) / dot6h(prev_g, prev_g));
+      for (int i = 0; i < 6; ++i) dir[i] = neg[i] + beta * prev_d[i];
+      if (dot6h(g, dir) >= 0.0) {
+        dir = neg;
+        restart = true;
+      }
+    }
+    if (restart) since_restart = 0;
+    ++since_restart;
+    prev_g = g;
+    prev_d = dir;
+    have_previous = true;
+    return dir;
+  }
+};
+
+// apply_increment (se3.hpp:116-119) on the host with the device's exp_map
+// (same source, IEEE arithmetic without contraction on both sides).
+void apply_increment_h(const Vec6h& d, double* pose12) {
+  double xi[6];
+  for (int i = 0; i < 6; ++i) xi[i] = d[i];
+  csfd::Pose<double> cur;
+  for (int e = 0; e < 9; ++e) cur.R.m[e] = pose12[e];
+  for (int e = 0; e < 3; ++e) cur.t.v[e] = pose12[9 + e];
+  const csfd::Pose<double> np = csfd::compose(csfd::exp_map<double>(xi), cur);
+  for (int e = 0; e < 9; ++e) pose12[e] = np.R.m[e];
+  for (int e = 0; e < 3; ++e) pose12[9 + e] = np.t.v[e];
+}
+
+}  // namespace
+
 extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, const double* init_pose,
                                const csf_intrinsics* k, const csf_icp_cfg* cfg_in, double* out_pose,
                                csf_track_result* result) {
@@ -1054,8 +1182,10 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
     cfg = *cfg_in;
   else
     csf_default_icp_cfg(&cfg);
-  if (cfg.solver != CSF_SOLVER_LINEARIZED)
-    return fail(ctx, CSF_EINVAL, "csf_track_frame: the device tracker implements the linearized solver");
+  if (cfg.solver < CSF_SOLVER_LINEARIZED || cfg.solver > CSF_SOLVER_CONJUGATE_GRADIENT)
+    return fail(ctx, CSF_EINVAL, "csf_track_frame: unknown solver");
+  if (cfg.solver != CSF_SOLVER_LINEARIZED && (!(cfg.h > 0.0) || cfg.h > 1e-6))
+    return fail(ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
   cudaSetDevice(ctx->device);
   const int levels = std::clamp(cfg.levels, 1, 3);
   const size_t P = static_cast<size_t>(w) * h;
@@ -1077,19 +1207,21 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
   CUDA_TRY(ctx, intr.alloc(12));
   CUDA_TRY(ctx, partials.alloc(icp_partials_doubles(1, tiles_max)));
   CUDA_TRY(ctx, counts.alloc(icp_counts_ints(tiles_max)));
-  CUDA_TRY(ctx, cudaMemsetAsync(counts.p, 0, sizeof(int) * counts.n, ctx->stream));
   CUDA_TRY(ctx, st.alloc(1));
+  CUDA_TRY(ctx, cudaMemsetAsync(counts.p, 0, sizeof(int) * counts.n, ctx->stream));
   double kl[12];
   for (int l = 0; l < 3; ++l) {
-    const double s = static_cast<double>(1 << l);
-    kl[4 * l] = k->fx / s;
-    kl[4 * l + 1] = k->fy / s;
-    kl[4 * l + 2] = k->cx / s;
-    kl[4 * l + 3] = k->cy / s;
+    const double sc = static_cast<double>(1 << l);
+    kl[4 * l] = k->fx / sc;
+    kl[4 * l + 1] = k->fy / sc;
+    kl[4 * l + 2] = k->cx / sc;
+    kl[4 * l + 3] = k->cy / sc;
   }
   const Launch L = launch_of(ctx);
+  double hpose[12];
+  std::copy(init_pose, init_pose + 12, hpose);
   CUDA_TRY(ctx, cudaMemcpyAsync(dd.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(pose.p, init_pose, sizeof(double) * 12, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(pose.p, hpose, sizeof(double) * 12, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(intr.p, kl, sizeof(kl), cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemsetAsync(st.p, 0, sizeof(TrackState), ctx->stream));
   const double cos_max = csf_det::cos(cfg.theta_max_deg * M_PI / 180.0);
@@ -1109,29 +1241,152 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
   real_view.dense.order = real_view.hash.order = 1;
   csf_raycast_cfg rcfg;
   csf_default_raycast_cfg(&rcfg);
-  int tiles_last = 0;
+  const LineSearch ls;
+  Stepper stepper{cfg.solver == CSF_SOLVER_CONJUGATE_GRADIENT, cfg.ncg_restart};
+  double lambda = cfg.levenberg_lambda0;
+  int iteration = 0, n_corr = 0;
+  bool converged = false;
+  double final_loss = 0.0;
+  EnergyScratch& ws = ctx->energy;
+  int err = 0;
+  // icp_energy(corrs, d, pose) of the current correspondence list
+  auto energy_at = [&](const Vec6h& d, int n, const double* base, int* e) -> double {
+    double E = 0.0;
+    const int r = icp_energy_derivs(ctx->stream, ws, ws.corrs, n, base, d.data(), 1e-8, 0, &E, nullptr, nullptr);
+    if (r) *e = r;
+    return E;
+  };
   for (int li = 0; li < levels; ++li) {
     const int level = levels - 1 - li;
     const int wl = w >> level, hl = h >> level;
+    const double* kdev = intr.p + 4 * level;
+    // one model prediction per level, cast at the estimate entering it (icp.cpp:189-192)
+    CUDA_TRY(ctx, cudaMemcpyAsync(pose.p, hpose, sizeof(double) * 12, cudaMemcpyHostToDevice, ctx->stream));
     launch_level_begin(L, st.p, pose.p, pred.p, 0);
-    raycast_dev(&real_view, pred.p, intr.p + 4 * level, wl, hl, rcfg, hits.p, vre.p, nre.p, nullptr, nullptr);
+    raycast_dev(&real_view, pred.p, kdev, wl, hl, rcfg, hits.p, vre.p, nre.p, nullptr, nullptr);
+    stepper.reset();
     const int stride = std::max(1, cfg.level_pixel_stride[li]);
-    tiles_last = icp_tiles(wl, hl, stride);
     for (int it = 0; it < cfg.level_iterations[li]; ++it) {
-      launch_icp_reduce(L, 0, 0, st.p, pyr[level], wl, hl, stride, intr.p + 4 * level, pose.p, vre.p, nre.p, nullptr,
-                        nullptr, cfg.d_max, cos_max, partials.p, counts.p, level, cfg.step_tolerance);
+      int n = 0;
+      CUDA_TRY(ctx, cudaMemcpyAsync(pose.p, hpose, sizeof(double) * 12, cudaMemcpyHostToDevice, ctx->stream));
+      const double* pred_w2c = reinterpret_cast<const double*>(reinterpret_cast<const char*>(st.p) +
+                                                                   offsetof(TrackState, pred_w2c));
+      err = associate_list(ctx->stream, ws, pyr[level], wl, hl, stride, kdev, pose.p, pred_w2c, vre.p, nre.p,
+                           cfg.d_max, cos_max, &n);
+      if (err) break;
+      n_corr = n;
+      if (n < 12) break;  // icp.cpp:199
+      Vec6h delta{};
+      double loss_after = 0.0;
+      if (cfg.solver == CSF_SOLVER_LINEARIZED) {
+        // canonical slot-tiled normal equations + the real LDLT step on the
+        // device (the pipeline's kernels); loss_after = E(delta) (icp.cpp:36-47)
+        launch_icp_reduce(L, 0, 0, st.p, pyr[level], wl, hl, stride, kdev, pose.p, vre.p, nre.p, nullptr, nullptr,
+                          cfg.d_max, cos_max, partials.p, counts.p, level, cfg.step_tolerance);
+        TrackState hs;
+        CUDA_TRY(ctx, cudaMemcpyAsync(&hs, st.p, sizeof(TrackState), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < 6; ++i) delta[i] = hs.delta[i];
+        loss_after = energy_at(delta, n, hpose, &err);
+      } else {
+        double E0 = 0.0, g[6], H[36];
+        const int order = cfg.solver == CSF_SOLVER_NEWTON ? 2 : 1;
+        const double zero[6] = {0, 0, 0, 0, 0, 0};
+        err = icp_energy_derivs(ctx->stream, ws, ws.corrs, n, hpose, zero, cfg.h, order, &E0, g,
+                                order == 2 ? H : nullptr);
+        if (err) break;
+        Vec6h grad;
+        for (int i = 0; i < 6; ++i) grad[i] = g[i];
+        loss_after = E0;
+        if (cfg.solver == CSF_SOLVER_NEWTON) {
+          // levenberg_newton_step (descent.hpp:109-144)
+          bool done = false;
+          for (int attempt = 0; attempt < 8 && !done && !err; ++attempt) {
+            double a[21];
+            for (int r = 0; r < 6; ++r)
+              for (int c = 0; c <= r; ++c) a[csfd::tri(r, c)] = H[r * 6 + c] + lambda * (r == c ? 1.0 : 0.0);
+            double m[6][6];
+            int tr[6];
+            const bool ok = csfd::ldlt6_factor_reg<double>(a, m, tr);
+            if (ok) {
+              double ng[6], d[6];
+              for (int i = 0; i < 6; ++i) ng[i] = -grad[i];
+              csfd::ldlt6_apply_reg<double>(m, tr, ng, d);
+              bool finite = true;
+              for (int i = 0; i < 6; ++i) finite = finite && std::isfinite(d[i]);
+              if (finite) {
+                Vec6h dv;
+                for (int i = 0; i < 6; ++i) dv[i] = d[i];
+                const double trial = energy_at(dv, n, hpose, &err);
+                if (!err && trial < E0) {
+                  lambda = std::max(lambda * 0.1, 1e-12);
+                  loss_after = trial;
+                  delta = dv;
+                  done = true;
+                  break;
+                }
+              }
+            }
+            lambda *= 10.0;
+          }
+          if (!done && !err) {
+            const double slope = -dot6h(grad, grad);
+            double alpha = 0.0, lsl = 0.0;
+            if (slope < 0.0 &&
+                backtracking(
+                    [&](double al, int* e) {
+                      Vec6h dv;
+                      for (int i = 0; i < 6; ++i) dv[i] = -al * grad[i];
+                      return energy_at(dv, n, hpose, e);
+                    },
+                    E0, slope, ls, &alpha, &lsl, &err)) {
+              loss_after = lsl;
+              for (int i = 0; i < 6; ++i) delta[i] = -alpha * grad[i];
+            } else {
+              loss_after = E0;
+              delta = Vec6h{};
+            }
+          }
+        } else {
+          // first_order_outcome (icp.cpp:64-85)
+          const Vec6h dir = stepper.propose(grad);
+          const double slope = dot6h(grad, dir);
+          if (slope < 0.0) {
+            double alpha = 0.0, lsl = 0.0;
+            if (backtracking(
+                    [&](double al, int* e) {
+                      Vec6h dv;
+                      for (int i = 0; i < 6; ++i) dv[i] = al * dir[i];
+                      return energy_at(dv, n, hpose, e);
+                    },
+                    E0, slope, ls, &alpha, &lsl, &err)) {
+              for (int i = 0; i < 6; ++i) delta[i] = alpha * dir[i];
+              loss_after = lsl;
+            }
+          }
+        }
+      }
+      if (err) break;
+      apply_increment_h(delta, hpose);
+      ++iteration;
+      final_loss = loss_after / static_cast<double>(n);
+      if (norm6h(delta) < cfg.step_tolerance) {
+        if (level == 0) converged = true;
+        break;
+      }
     }
+    if (err) break;
   }
-  TrackState hs;
-  CUDA_TRY(ctx, cudaMemcpyAsync(out_pose, pose.p, sizeof(double) * 12, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(&hs, st.p, sizeof(TrackState), cudaMemcpyDeviceToHost, ctx->stream));
+  if (err == 5) return fail(ctx, CSF_ENOMEM, "csf_track_frame: out of device memory");
+  if (err) return fail(ctx, CSF_ECUDA, "csf_track_frame: CUDA error");
   const int rc = sync_check(ctx, "csf_track_frame");
   if (rc) return rc;
+  std::copy(hpose, hpose + 12, out_pose);
   if (result) {
-    result->iterations = hs.iterations;
-    result->converged = hs.converged;
-    result->correspondences = hs.n_corr;
-    result->final_loss = std::nan("");  // loss_after is not evaluated by the device tracker
+    result->iterations = iteration;
+    result->converged = converged;
+    result->correspondences = n_corr;
+    result->final_loss = final_loss;
   }
   return CSF_OK;
 }

@@ -72,7 +72,32 @@ struct TrackState {
   int pad[2];
   double pred_w2c[12];  // real inverse of the prediction pose (association)
   double cur_c2w[12];   // real current pose snapshot (unused by kernels)
+  double delta[6];      // real increment of the last solved ICP iteration
 };
+
+// ---- energy.cu: icp_energy / gradient / Hessian and the correspondence list
+struct EnergyScratch {
+  double* terms = nullptr;
+  size_t terms_cap = 0;
+  double* sub = nullptr;
+  size_t sub_cap = 0;
+  double* small = nullptr;
+  size_t small_cap = 0;
+  int* pairs = nullptr;
+  double* corrs = nullptr;  // [n][9] of the last associate_list
+  int* flags = nullptr;
+  size_t flags_cap = 0;
+  void* cub = nullptr;
+  size_t cub_bytes = 0;
+};
+// order 0: energy; 1: + gradient; 2: + Hessian.  Synchronous on `stream`.
+// Returns 0, 4 (CUDA error) or 5 (out of memory).
+int icp_energy_derivs(cudaStream_t stream, EnergyScratch& ws, const double* corrs, int n, const double* base,
+                      const double* xi, double h, int order, double* E, double* g, double* H);
+int associate_list(cudaStream_t stream, EnergyScratch& ws, const double* depth, int w, int h, int stride,
+                   const double* intr4, const double* pose12, const double* pred_w2c12, const double* vre,
+                   const double* nre, double d_max, double cos_max, int* n_out);
+void energy_scratch_release(EnergyScratch& ws);
 
 struct Launch {
   cudaStream_t stream;

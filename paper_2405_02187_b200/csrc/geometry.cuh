@@ -278,14 +278,14 @@ CSF_DEV bool measured_tsdf(const double* depth, int w, int h, const Pose<S>& w2c
 // ----------------------------------------------------------------------------
 // Ldlt6 — the oracle's restatement of Eigen::LDLT<Mat6d> (oracle/orc_icp.hpp)
 // ----------------------------------------------------------------------------
-CSF_DEV int tri(int r, int c) { return r * (r + 1) / 2 + c; }
+CSF_HD int tri(int r, int c) { return r * (r + 1) / 2 + c; }
 
-template <typename S> CSF_DEV void swap_s(S& a, S& b) {
+template <typename S> CSF_HD void swap_s(S& a, S& b) {
   const S t = a;
   a = b;
   b = t;
 }
-template <typename S> CSF_DEV double absre(const S& x) { return fabs(re(x)); }
+template <typename S> CSF_HD double absre(const S& x) { return fabs(re(x)); }
 
 // Factor the symmetric matrix given by its lower triangle and solve A x = rhs.
 // Returns false when Eigen would report info() != Success.  The pivoted
@@ -379,7 +379,7 @@ CSF_DEV bool ldlt6_solve(const S* a_lower, const S* rhs, S* dst, S* ws) {
 // `degenerate` (optional) reports a zero pivot or a pivot below the solve's
 // tolerance — the cases where the solve is not the linear operator A^-1.
 template <typename S>
-CSF_DEV bool ldlt6_factor_reg(const S* a_lower, S (&m)[6][6], int (&transp)[6], bool* degenerate = nullptr) {
+CSF_HD bool ldlt6_factor_reg(const S* a_lower, S (&m)[6][6], int (&transp)[6], bool* degenerate = nullptr) {
   bool ok = true, stop = false, degen = false;
 #pragma unroll
   for (int r = 0; r < 6; ++r)
@@ -462,7 +462,7 @@ CSF_DEV bool ldlt6_factor_reg(const S* a_lower, S (&m)[6][6], int (&transp)[6], 
 // M may be the factor of the same scalar type or, for the tangent solve,
 // plain double factors applied to a double right-hand side.
 template <typename S, typename M>
-CSF_DEV void ldlt6_apply_reg(const M (&m)[6][6], const int (&transp)[6], const S* rhs, S* dst) {
+CSF_HD void ldlt6_apply_reg(const M (&m)[6][6], const int (&transp)[6], const S* rhs, S* dst) {
   S x[6];
 #pragma unroll
   for (int i = 0; i < 6; ++i) x[i] = rhs[i];
@@ -500,12 +500,62 @@ CSF_DEV void ldlt6_apply_reg(const M (&m)[6][6], const int (&transp)[6], const S
 }
 
 template <typename S>
-CSF_DEV bool ldlt6_solve_reg(const S* a_lower, const S* rhs, S* dst) {
+CSF_HD bool ldlt6_solve_reg(const S* a_lower, const S* rhs, S* dst) {
   S m[6][6];
   int transp[6];
   const bool ok = ldlt6_factor_reg<S>(a_lower, m, transp);
   ldlt6_apply_reg<S>(m, transp, rhs, dst);
   return ok;
+}
+
+// Real measured vertex at (x, y) (frames.hpp:38-41 via measure_surface).
+CSF_DEV bool vertex_at(const double* depth, int w, int x, int y, double fx, double fy, double cx, double cy,
+                       V3<double>* v) {
+  const double d = depth[y * w + x];
+  if (!(d > 0.0)) return false;
+  *v = mk3<double>(d * (static_cast<double>(x) - cx) / fx, d * (static_cast<double>(y) - cy) / fy, d);
+  return true;
+}
+
+// associate (icp.cpp:89-126) for one strided slot (x, y): the measured
+// vertex/normal recomputed from the pyramid depth (measure_surface), the
+// real-part gates in the reference's order (z > 0, bounds, model normal
+// valid, distance, angle) and the lround pixel pick.  Returns true for a
+// correspondence with model pixel (u, v).
+CSF_DEV bool associate_slot(const double* __restrict__ depth, int w, int h, int x, int y, double fx, double fy,
+                            double cx, double cy, const Pose<double>& c2w, const Pose<double>& w2p,
+                            const double* __restrict__ vre, const double* __restrict__ nre, double d_max,
+                            double cos_max, int* u_out, int* v_out) {
+  V3<double> vert, vx, vy;
+  if (!(vertex_at(depth, w, x, y, fx, fy, cx, cy, &vert) && x + 1 < w && y + 1 < h &&
+        vertex_at(depth, w, x + 1, y, fx, fy, cx, cy, &vx) && vertex_at(depth, w, x, y + 1, fx, fy, cx, cy, &vy)))
+    return false;
+  V3<double> n = cross3(sub3(vx, vert), sub3(vy, vert));
+  const double len2 = dot3(n, n);
+  if (!(len2 > 0.0)) return false;
+  const double l = sqrt(len2);
+  n = mk3<double>(n.v[0] / l, n.v[1] / l, n.v[2] / l);
+  if (dot3(n, vert) > 0.0) n = mk3<double>(-n.v[0], -n.v[1], -n.v[2]);
+  if (!(dot3(n, n) > 0.5)) return false;
+  const V3<double> world = apply(c2w, vert);
+  const V3<double> inp = apply(w2p, world);
+  if (!(inp.v[2] > 0.0)) return false;
+  const double uvx = (fx * inp.v[0]) / inp.v[2] + cx;
+  const double uvy = (fy * inp.v[1]) / inp.v[2] + cy;
+  const int u = static_cast<int>(lround(uvx));
+  const int v = static_cast<int>(lround(uvy));
+  if (!(u >= 0 && u < w && v >= 0 && v < h)) return false;
+  const long long m = static_cast<long long>(v) * w + u;
+  const V3<double> mn = mk3<double>(nre[3 * m], nre[3 * m + 1], nre[3 * m + 2]);
+  if (!(dot3(mn, mn) > 0.5)) return false;
+  const V3<double> mv = mk3<double>(vre[3 * m], vre[3 * m + 1], vre[3 * m + 2]);
+  const V3<double> dd = sub3(world, mv);
+  if (sqrt(dot3(dd, dd)) > d_max) return false;
+  const V3<double> wn = matvec(c2w.R, n);
+  if (dot3(wn, mn) < cos_max) return false;
+  *u_out = u;
+  *v_out = v;
+  return true;
 }
 
 }  // namespace csfd

@@ -58,55 +58,7 @@ CSF_DEV void load_pose_real(const double* p, int C, Pose<double>* out) {
   for (int e = 0; e < 3; ++e) out->t.v[e] = p[(9 + e) * C];
 }
 
-// Real measured vertex at (x, y) (frames.hpp:38-41 via measure_surface).
-CSF_DEV bool vertex_at(const double* depth, int w, int x, int y, double fx, double fy, double cx, double cy,
-                       V3<double>* v) {
-  const double d = depth[y * w + x];
-  if (!(d > 0.0)) return false;
-  *v = mk3<double>(d * (static_cast<double>(x) - cx) / fx, d * (static_cast<double>(y) - cy) / fy, d);
-  return true;
-}
 
-// associate (icp.cpp:89-126) for one strided slot (x, y): the measured
-// vertex/normal recomputed from the pyramid depth (measure_surface), the
-// real-part gates in the reference's order (z > 0, bounds, model normal
-// valid, distance, angle) and the lround pixel pick.  Returns true for a
-// correspondence with model pixel (u, v).
-CSF_DEV bool associate_slot(const double* __restrict__ depth, int w, int h, int x, int y, double fx, double fy,
-                            double cx, double cy, const Pose<double>& c2w, const Pose<double>& w2p,
-                            const double* __restrict__ vre, const double* __restrict__ nre, double d_max,
-                            double cos_max, int* u_out, int* v_out) {
-  V3<double> vert, vx, vy;
-  if (!(vertex_at(depth, w, x, y, fx, fy, cx, cy, &vert) && x + 1 < w && y + 1 < h &&
-        vertex_at(depth, w, x + 1, y, fx, fy, cx, cy, &vx) && vertex_at(depth, w, x, y + 1, fx, fy, cx, cy, &vy)))
-    return false;
-  V3<double> n = cross3(sub3(vx, vert), sub3(vy, vert));
-  const double len2 = dot3(n, n);
-  if (!(len2 > 0.0)) return false;
-  const double l = sqrt(len2);
-  n = mk3<double>(n.v[0] / l, n.v[1] / l, n.v[2] / l);
-  if (dot3(n, vert) > 0.0) n = mk3<double>(-n.v[0], -n.v[1], -n.v[2]);
-  if (!(dot3(n, n) > 0.5)) return false;
-  const V3<double> world = apply(c2w, vert);
-  const V3<double> inp = apply(w2p, world);
-  if (!(inp.v[2] > 0.0)) return false;
-  const double uvx = (fx * inp.v[0]) / inp.v[2] + cx;
-  const double uvy = (fy * inp.v[1]) / inp.v[2] + cy;
-  const int u = static_cast<int>(lround(uvx));
-  const int v = static_cast<int>(lround(uvy));
-  if (!(u >= 0 && u < w && v >= 0 && v < h)) return false;
-  const long long m = static_cast<long long>(v) * w + u;
-  const V3<double> mn = mk3<double>(nre[3 * m], nre[3 * m + 1], nre[3 * m + 2]);
-  if (!(dot3(mn, mn) > 0.5)) return false;
-  const V3<double> mv = mk3<double>(vre[3 * m], vre[3 * m + 1], vre[3 * m + 2]);
-  const V3<double> dd = sub3(world, mv);
-  if (sqrt(dot3(dd, dd)) > d_max) return false;
-  const V3<double> wn = matvec(c2w.R, n);
-  if (dot3(wn, mn) < cos_max) return false;
-  *u_out = u;
-  *v_out = v;
-  return true;
-}
 
 // Canonical two-level cross-tile order (oracle/orc_icp.hpp, kGroup): the
 // last CTA to finish within a group of kGroup consecutive tiles sums the
@@ -305,6 +257,8 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_solve_t(TrackState* st, con
     const double nrm = sqrt((sq[0] + (sq[1] + sq[2])) + (sq[3] + (sq[4] + sq[5])));
     st->iterations += 1;
     st->n_corr = n;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) st->delta[i] = re(d[i]);
     if (nrm < tol) {
       st->level_done = 1;
       if (level == 0) st->converged = 1;

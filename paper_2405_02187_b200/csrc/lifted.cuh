@@ -101,9 +101,9 @@ template <int NP> struct Traits<B<NP>> {
   static constexpr int kOrder = 2;
 };
 
-template <typename S> CSF_DEV S lit(double x);
-template <> CSF_DEV double lit<double>(double x) { return x; }
-template <typename S> CSF_DEV S lit(double x) {
+template <typename S> CSF_HD S lit(double x);
+template <> CSF_HD double lit<double>(double x) { return x; }
+template <typename S> CSF_HD S lit(double x) {
   S o;
   o.re = x;
 #pragma unroll
@@ -111,7 +111,7 @@ template <typename S> CSF_DEV S lit(double x) {
   return o;
 }
 
-CSF_DEV double re(double x) { return x; }
+CSF_HD double re(double x) { return x; }
 template <int G> CSF_DEV double re(const L<G>& x) { return x.re; }
 
 // -- lifted (x) lifted -------------------------------------------------------
@@ -391,14 +391,14 @@ template <int G> CSF_DEV L<G> lift(const L<G>& z, double f, double d1) {
   for (int g = 0; g < G; ++g) o.im[g] = d1 * z.im[g];
   return o;
 }
-CSF_DEV double sqrt_s(double x) { return ::sqrt(x); }
+CSF_HD double sqrt_s(double x) { return ::sqrt(x); }
 template <int G> CSF_DEV L<G> sqrt_s(const L<G>& z) {
   const double f = ::sqrt(z.re);
   return lift(z, f, 0.5 / f);
 }
-CSF_DEV double sin_s(double x) { return csf_det::sin(x); }
+CSF_HD double sin_s(double x) { return csf_det::sin(x); }
 template <int G> CSF_DEV L<G> sin_s(const L<G>& z) { return lift(z, csf_det::sin(z.re), csf_det::cos(z.re)); }
-CSF_DEV double cos_s(double x) { return csf_det::cos(x); }
+CSF_HD double cos_s(double x) { return csf_det::cos(x); }
 template <int G> CSF_DEV L<G> cos_s(const L<G>& z) { return lift(z, csf_det::cos(z.re), -csf_det::sin(z.re)); }
 // Bicomplex lifts (csfd.hpp:230-245)
 template <int NP> CSF_DEV B<NP> sqrt_s(const B<NP>& z) {
@@ -424,7 +424,7 @@ template <typename S> CSF_DEV S clamp_s(const S& x, double lo, double hi) {
 }
 CSF_DEV int ifloor(double x) { return static_cast<int>(::floor(x)); }
 
-CSF_DEV bool finite_s(double x) { return isfinite(x); }
+CSF_HD bool finite_s(double x) { return isfinite(x); }
 template <int G> CSF_DEV bool finite_s(const L<G>& x) {
   bool ok = isfinite(x.re);
 #pragma unroll
@@ -442,31 +442,31 @@ template <typename S> struct M3 {
   S m[9];  // row-major
 };
 
-template <typename S> CSF_DEV V3<S> mk3(const S& a, const S& b, const S& c) {
+template <typename S> CSF_HD V3<S> mk3(const S& a, const S& b, const S& c) {
   V3<S> o;
   o.v[0] = a; o.v[1] = b; o.v[2] = c;
   return o;
 }
-template <typename S> CSF_DEV S sum3(const S& a0, const S& a1, const S& a2) { return a0 + (a1 + a2); }
-template <typename S> CSF_DEV S dot3(const V3<S>& a, const V3<S>& b) {
+template <typename S> CSF_HD S sum3(const S& a0, const S& a1, const S& a2) { return a0 + (a1 + a2); }
+template <typename S> CSF_HD S dot3(const V3<S>& a, const V3<S>& b) {
   return sum3(a.v[0] * b.v[0], a.v[1] * b.v[1], a.v[2] * b.v[2]);
 }
-template <typename S> CSF_DEV V3<S> add3(const V3<S>& a, const V3<S>& b) {
+template <typename S> CSF_HD V3<S> add3(const V3<S>& a, const V3<S>& b) {
   return mk3(a.v[0] + b.v[0], a.v[1] + b.v[1], a.v[2] + b.v[2]);
 }
-template <typename S> CSF_DEV V3<S> sub3(const V3<S>& a, const V3<S>& b) {
+template <typename S> CSF_HD V3<S> sub3(const V3<S>& a, const V3<S>& b) {
   return mk3(a.v[0] - b.v[0], a.v[1] - b.v[1], a.v[2] - b.v[2]);
 }
-template <typename S> CSF_DEV V3<S> cross3(const V3<S>& a, const V3<S>& b) {
+template <typename S> CSF_HD V3<S> cross3(const V3<S>& a, const V3<S>& b) {
   return mk3(a.v[1] * b.v[2] - a.v[2] * b.v[1], a.v[2] * b.v[0] - a.v[0] * b.v[2], a.v[0] * b.v[1] - a.v[1] * b.v[0]);
 }
-template <typename S> CSF_DEV V3<S> matvec(const M3<S>& m, const V3<S>& p) {
+template <typename S> CSF_HD V3<S> matvec(const M3<S>& m, const V3<S>& p) {
   V3<S> o;
 #pragma unroll
   for (int r = 0; r < 3; ++r) o.v[r] = sum3(m.m[3 * r] * p.v[0], m.m[3 * r + 1] * p.v[1], m.m[3 * r + 2] * p.v[2]);
   return o;
 }
-template <typename S> CSF_DEV M3<S> matmul(const M3<S>& a, const M3<S>& b) {
+template <typename S> CSF_HD M3<S> matmul(const M3<S>& a, const M3<S>& b) {
   M3<S> o;
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -475,7 +475,7 @@ template <typename S> CSF_DEV M3<S> matmul(const M3<S>& a, const M3<S>& b) {
       o.m[3 * r + c] = sum3(a.m[3 * r] * b.m[c], a.m[3 * r + 1] * b.m[3 + c], a.m[3 * r + 2] * b.m[6 + c]);
   return o;
 }
-template <typename S> CSF_DEV M3<S> transpose3(const M3<S>& a) {
+template <typename S> CSF_HD M3<S> transpose3(const M3<S>& a) {
   M3<S> o;
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -489,14 +489,14 @@ template <typename S> struct Pose {
   M3<S> R;
   V3<S> t;
 };
-template <typename S> CSF_DEV V3<S> apply(const Pose<S>& p, const V3<S>& x) { return add3(matvec(p.R, x), p.t); }
-template <typename S> CSF_DEV Pose<S> compose(const Pose<S>& a, const Pose<S>& b) {
+template <typename S> CSF_HD V3<S> apply(const Pose<S>& p, const V3<S>& x) { return add3(matvec(p.R, x), p.t); }
+template <typename S> CSF_HD Pose<S> compose(const Pose<S>& a, const Pose<S>& b) {
   Pose<S> o;
   o.R = matmul(a.R, b.R);
   o.t = add3(matvec(a.R, b.t), a.t);
   return o;
 }
-template <typename S> CSF_DEV Pose<S> inverse(const Pose<S>& p) {
+template <typename S> CSF_HD Pose<S> inverse(const Pose<S>& p) {
   Pose<S> o;
   o.R = transpose3(p.R);
   const V3<S> rt = matvec(o.R, p.t);
@@ -505,7 +505,7 @@ template <typename S> CSF_DEV Pose<S> inverse(const Pose<S>& p) {
 }
 
 // exp of a twist (rho, phi) — se3.hpp:77-105, same branch and order.
-template <typename S> CSF_DEV Pose<S> exp_map(const S xi[6]) {
+template <typename S> CSF_HD Pose<S> exp_map(const S xi[6]) {
   const V3<S> rho = mk3(xi[0], xi[1], xi[2]);
   const V3<S> phi = mk3(xi[3], xi[4], xi[5]);
   const S t2 = dot3(phi, phi);
