@@ -5,7 +5,10 @@
 //   bilateral_filter / build_depth_pyramid   frames.hpp:56-65, frames.cpp:7-75
 //   measure_surface                          frames.hpp:86-114
 //   TsdfVolume (+ HashedVolume), surface_update, raycast   tsdf.hpp:38-284
-//   track_frame                              icp.hpp:130-133
+//   track_frame (every solver family)        icp.hpp:130-133
+//   icp_energy / icp_loss / icp_gradient / icp_hessian   icp.hpp:70-91
+//   Pipeline: csfd_pipeline_gradient / csfd_pipeline_hessian (the CSFD
+//   frame-derivative run; first order or bicomplex pairs)
 // Errors are thrown as std::invalid_argument / std::domain_error /
 // std::runtime_error exactly where the reference throws them.  Scalars are
 // plain structs (no Eigen): Complex{re, im}, lifted values as (1+D) doubles.
@@ -201,6 +204,96 @@ inline TrackResult track_frame(Context& c, const Volume& vol, const Image<double
   r.correspondences = tr.correspondences;
   return r;
 }
+
+// icp.hpp:27-31
+struct Correspondence {
+  std::array<double, 3> vertex{}, model_vertex{}, model_normal{};
+};
+namespace detail {
+inline std::vector<double> pack(const std::vector<Correspondence>& corrs) {
+  std::vector<double> out(corrs.size() * 9);
+  for (size_t i = 0; i < corrs.size(); ++i)
+    for (int k = 0; k < 3; ++k) {
+      out[9 * i + k] = corrs[i].vertex[k];
+      out[9 * i + 3 + k] = corrs[i].model_vertex[k];
+      out[9 * i + 6 + k] = corrs[i].model_normal[k];
+    }
+  return out;
+}
+}  // namespace detail
+
+// icp.hpp:70-85 (real xi; pairwise_sum tree on the device)
+inline double icp_energy(Context& c, const std::vector<Correspondence>& corrs, const std::array<double, 6>& xi,
+                         const std::array<double, 12>& base) {
+  const std::vector<double> p = detail::pack(corrs);
+  double e = 0.0;
+  check(c.get(), csf_icp_energy_derivs(c.get(), p.data(), static_cast<int>(corrs.size()), base.data(), xi.data(),
+                                       1e-8, &e, nullptr, nullptr));
+  return e;
+}
+// icp.cpp:128-144
+inline double icp_loss(Context& c, const std::vector<Correspondence>& corrs, const std::array<double, 12>& base) {
+  return icp_energy(c, corrs, std::array<double, 6>{}, base);
+}
+inline std::array<double, 6> icp_gradient(Context& c, const std::vector<Correspondence>& corrs,
+                                          const std::array<double, 12>& base, double h = 1e-8) {
+  const std::vector<double> p = detail::pack(corrs);
+  std::array<double, 6> g{};
+  double e = 0.0;
+  check(c.get(), csf_icp_energy_derivs(c.get(), p.data(), static_cast<int>(corrs.size()), base.data(), nullptr, h, &e,
+                                       g.data(), nullptr));
+  return g;
+}
+inline std::array<std::array<double, 6>, 6> icp_hessian(Context& c, const std::vector<Correspondence>& corrs,
+                                                        const std::array<double, 12>& base, double h = 1e-8) {
+  const std::vector<double> p = detail::pack(corrs);
+  double hh[36];
+  double e = 0.0;
+  check(c.get(), csf_icp_energy_derivs(c.get(), p.data(), static_cast<int>(corrs.size()), base.data(), nullptr, h, &e,
+                                       nullptr, hh));
+  std::array<std::array<double, 6>, 6> out{};
+  for (int r = 0; r < 6; ++r)
+    for (int col = 0; col < 6; ++col) out[r][col] = hh[6 * r + col];
+  return out;
+}
+
+// The CSFD frame-derivative run; extension of the reference
+// API: gradient over first-order directions, or Hessian entries over
+// bicomplex pairs (csfd_hessian's pattern applied to the whole frame loop).
+class Pipeline {
+ public:
+  Pipeline(Context& c, const csf_pipeline_cfg& cfg) : ctx_(c.get()), cfg_(cfg) {
+    check(ctx_, csf_pipeline_create(ctx_, &cfg_, &p_));
+  }
+  ~Pipeline() { csf_pipeline_destroy(p_); }
+  Pipeline(const Pipeline&) = delete;
+  Pipeline& operator=(const Pipeline&) = delete;
+  // depth [n][h][w] float32 metres, gt [n][12]
+  std::vector<double> csfd_pipeline_gradient(const std::vector<float>& depth, const std::vector<double>& gt, int n,
+                                             double* objective = nullptr) {
+    if (cfg_.order == 2) throw std::invalid_argument("csfd_pipeline_gradient: pipeline has order 2");
+    std::vector<double> g(static_cast<size_t>(cfg_.n_dirs));
+    double obj = 0.0;
+    check(ctx_, csf_pipeline_run_host(p_, depth.data(), gt.data(), n, g.data(), &obj));
+    if (objective) *objective = obj;
+    return g;
+  }
+  // H_{pair_i[p], pair_j[p]} per pair
+  std::vector<double> csfd_pipeline_hessian(const std::vector<float>& depth, const std::vector<double>& gt, int n,
+                                            double* objective = nullptr) {
+    if (cfg_.order != 2) throw std::invalid_argument("csfd_pipeline_hessian: pipeline has order 1");
+    check(ctx_, csf_pipeline_upload(p_, depth.data(), gt.data(), n));
+    check(ctx_, csf_pipeline_run(p_, n));
+    std::vector<double> hs(static_cast<size_t>(cfg_.n_pairs));
+    check(ctx_, csf_pipeline_hessian(p_, hs.data(), nullptr, nullptr, objective, nullptr, nullptr));
+    return hs;
+  }
+
+ private:
+  csf_ctx ctx_;
+  csf_pipeline_cfg cfg_;
+  csf_pipeline p_ = nullptr;
+};
 
 }  // namespace b200
 }  // namespace csf

@@ -339,7 +339,7 @@ extern "C" void csf_default_raycast_cfg(csf_raycast_cfg* c) {
   c->near_clip = 0.0; c->far_clip = 10.0; c->step_fraction = 0.5;
 }
 extern "C" void csf_default_icp_cfg(csf_icp_cfg* c) {
-  c->solver = CSF_SOLVER_LINEARIZED;
+  c->solver = CSF_SOLVER_NEWTON;  // icp.hpp:41 (the lifted pipeline selects the linearized solver)
   c->d_max = 0.1;
   c->theta_max_deg = 30.0;
   c->levels = 3;

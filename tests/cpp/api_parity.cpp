@@ -163,7 +163,7 @@ int main() {
     std::printf("ok   raycast recovers the fused sphere (hits %d, mean err %.2e m)\n", hits, sum_e / hits);
   }
 
-  {  // test_icp.cpp:323-370 — tracking refines a perturbed pose (linearized solver), bit-identical rerun
+  {  // test_icp.cpp:323-370 — tracking refines a perturbed pose (default Newton solver), bit-identical rerun
     orc::Scene scene;
     scene.planes.push_back({orc::Vec3d(0, 0, 1), 0.0});
     scene.spheres.push_back({orc::Vec3d(0.0, 0.1, 0.55), 0.5});
@@ -185,7 +185,8 @@ int main() {
     const orc::Pose init = orc::apply_increment(orc::Vec6<double>{0.03, -0.02, 0.02, 0.02, -0.015, 0.015}, truth);
     const B::Image<double> frame = img(orc::render_depth(scene, truth, ko));
     csf_icp_cfg cfg;
-    csf_default_icp_cfg(&cfg);
+    csf_default_icp_cfg(&cfg);  // Newton, the reference default (icp.hpp:41)
+    CHECK(cfg.solver == CSF_SOLVER_NEWTON);
     const B::TrackResult r = B::track_frame(ctx, vol, frame, arr(init), k, &cfg);
     orc::Pose got;
     for (int e = 0; e < 9; ++e) got.rotation(e / 3, e % 3) = r.pose[e];
@@ -200,6 +201,47 @@ int main() {
     CHECK(again.pose == r.pose);
     std::printf("ok   track_frame: %d iterations, %d correspondences, %.2e m, %.3f deg\n", r.iterations,
                 r.correspondences, terr, rerr);
+  }
+
+  {  // icp.hpp:70-91 — energy, CSFD gradient and Hessian on the device equal the reference restatement
+    std::vector<B::Correspondence> cb;
+    std::vector<orc::Correspondence> co;
+    uint64_t st = 12345;
+    auto rnd = [&]() {
+      st = st * 6364136223846793005ULL + 1442695040888963407ULL;
+      return static_cast<double>(st >> 11) * 0x1.0p-53 - 0.5;
+    };
+    for (int i = 0; i < 2000; ++i) {
+      B::Correspondence c;
+      orc::Correspondence o;
+      for (int a = 0; a < 3; ++a) {
+        c.vertex[a] = rnd() + (a == 2 ? 2.0 : 0.0);
+        c.model_vertex[a] = c.vertex[a] + 0.01 * rnd();
+        c.model_normal[a] = rnd();
+      }
+      const double nn = std::sqrt(c.model_normal[0] * c.model_normal[0] + c.model_normal[1] * c.model_normal[1] +
+                                  c.model_normal[2] * c.model_normal[2]);
+      for (int a = 0; a < 3; ++a) c.model_normal[a] /= nn;
+      o.vertex = orc::Vec3d(c.vertex[0], c.vertex[1], c.vertex[2]);
+      o.model_vertex = orc::Vec3d(c.model_vertex[0], c.model_vertex[1], c.model_vertex[2]);
+      o.model_normal = orc::Vec3d(c.model_normal[0], c.model_normal[1], c.model_normal[2]);
+      cb.push_back(c);
+      co.push_back(o);
+    }
+    const orc::Pose base = orc::orbit_pose(orc::Vec3d(), 1.2, 0.4, 0.7);
+    const double e = B::icp_loss(ctx, cb, arr(base));
+    const auto g = B::icp_gradient(ctx, cb, arr(base));
+    const auto h = B::icp_hessian(ctx, cb, arr(base));
+    const auto go = orc::icp_gradient(co, base);
+    const auto ho = orc::icp_hessian(co, base);
+    CHECK(e == orc::icp_loss(co, base));
+    bool same = true;
+    for (int i = 0; i < 6; ++i) {
+      same = same && g[i] == go[i];
+      for (int j = 0; j < 6; ++j) same = same && h[i][j] == ho[i][j] && h[i][j] == h[j][i];
+    }
+    CHECK(same);
+    std::printf("ok   icp_loss / icp_gradient / icp_hessian bit-identical to the restatement (E %.6e)\n", e);
   }
 
   {  // error behaviour: invalid arguments throw std::invalid_argument
