@@ -25,6 +25,12 @@ fixed, so scaling is "strong".  --impl reference times the CPU oracle port
 (the reference's own CPU path restated) on a bounded sample of the same
 workload.
 
+--workload config5: BASELINE config 5 — the config-2 scene fused into a
+hashed TSDF (100 VGA frames at the ground-truth poses, untimed setup), then
+256 candidate views (seeded, free space) each raycast at 320x240 with the
+pose lifted on its 6 twist channels, scored by the builder-defined coverage
+objective.  Units = views x 6 directions (1536 per step).
+
 --workload config3: BASELINE config 3 — the same VGA scene, 30 frames, the
 full 10x10 Hessian as 55 second-order parameter pairs (one reference
 Bicomplex per pair, packed as channel slots of one evaluation).  Units =
@@ -63,7 +69,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["config2", "config3"], default="config2")
+    ap.add_argument("--workload", choices=["config2", "config3", "config5"], default="config2")
     ap.add_argument("--frames", type=int, default=0, help="0 = the workload's frame count (100 / 30)")
     ap.add_argument("--cpu-frames", type=int, default=5, help="CPU-baseline sample: frames")
     ap.add_argument("--cpu-dirs", type=int, default=2, help="CPU-baseline sample: directions (one pass each)")
@@ -176,6 +182,39 @@ def run_reference(args):
     import paper_2405_02187_b200 as csf
     from oracle import orc
     from paper_2405_02187_b200 import capi
+    if args.workload == "config5":
+        # bounded sample: a volume fused from 10 VGA frames (untimed), 2 views x 6 directions per step
+        nf = 10
+        depth, gt, k = orc.workload(2, nf)
+        hp = capi.HashParams(0.005, (__import__("ctypes").c_double * 3)(0, 0, 0), 0.025, 128.0, 20, 1 << 18)
+        vo = orc.Volume(hp, 6, True)
+        intr = np.zeros((4, 7))
+        intr[:, 0] = [k.fx, k.fy, k.cx, k.cy]
+        for f in range(nf):
+            pose = np.zeros((12, 7))
+            pose[:, 0] = gt[f]
+            vo.surface_update(depth[f].astype(np.float64), pose, intr)
+        views = csf.config5_views(256, seed=4)[:2]
+        kv = csf.intrinsics(k.fx / 2, k.fy / 2, k.cx / 2, k.cy / 2, 320, 240)
+        for _ in range(args.warmup):
+            vo.view_scores(views, kv)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            vo.view_scores(views, kv)
+        secs = time.perf_counter() - t0
+        value = len(views) * 6 * args.steps / secs
+        cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded procedural room, BASELINE config 5 shapes)",
+            "config": {"workload": "config5 bounded CPU sample: 2 views x 6 directions per step (320x240)",
+                       "views": 2, "directions": 6},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": "2 views x 6 directions per step, one Lifted<6> pass per view"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+        return
     frames = 3
     depth, gt, k = orc.workload(2, frames)
     second = args.workload == "config3"
@@ -235,8 +274,139 @@ def algorithmic_bytes_per_step(cat, stats, D, W, H, n_frames):
     return None, None
 
 
+def run_config5(args):
+    """BASELINE config 5: view scoring over a fused config-2 volume."""
+    import torch
+    import paper_2405_02187_b200 as csf
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    ctx = csf.Context(local)
+    n_frames = 100
+    depth, gt, k = csf.synth_workload(2, n_frames, ctx=ctx)
+    vol = csf.HashedVolume(0.005, (0.0, 0.0, 0.0), 0.025, 128.0, 20, 1 << 18, channels=6, ctx=ctx)
+    intr = np.zeros((4, 7))
+    intr[:, 0] = [k.fx, k.fy, k.cx, k.cy]
+    for f in range(n_frames):
+        pose = np.zeros((12, 7))
+        pose[:, 0] = gt[f]
+        vol.surface_update(depth[f].astype(np.float64), pose, intr)
+    views_all = csf.config5_views(256, seed=4)
+    from paper_2405_02187_b200.shard import shard_directions
+    _, mine = shard_directions(list(range(len(views_all))), world, rank)
+    views = views_all[mine]
+    kv = csf.intrinsics(k.fx / 2, k.fy / 2, k.cx / 2, k.cy / 2, 320, 240)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    for _ in range(max(args.warmup, 0)):
+        vol.view_scores(views, kv)
+    ctx.synchronize()
+    clocks = Clocks(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        sc, g = vol.view_scores(views, kv)
+    e1.record(stream)
+    ctx.synchronize()
+    t_e2e = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count - l0
+    clk = clocks.stop()
+    ctx.profile(True)
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        vol.view_scores(views, kv)
+    p1.record(stream)
+    ctx.synchronize()
+    prof_ms = p0.elapsed_time(p1)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    if dist is not None:
+        t = torch.tensor([ms, t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, t_e2e = float(t[0].item()), float(t[1].item())
+    units = len(views_all) * 6
+    value = units * args.steps / (ms / 1000.0)
+    peak, peak_src = measured_peak()
+    P = 320 * 240
+    rooflines = {}
+    for cat, (cat_ms, cat_n) in prof.items():
+        if cat_n == 0 or cat_ms <= 0:
+            continue
+        if cat == "raycast":
+            b, bd = P * (16 + 6 * 8 + 3 * 8), "per ray: hit alphas + real vertex/normal maps written (samples are L2 gathers)"
+        elif cat == "raycast_lift":
+            b, bd = P * 6 * 8 * 7, "per pixel: lifted vertex/normal maps written (7 channels)"
+        elif cat == "misc":
+            b, bd = P * (6 * 8 * 7 + 7 * 8), "per pixel: lifted vertex + normal read, 7 term slots written"
+        else:
+            continue
+        avg = cat_ms / cat_n
+        ach = b / (avg / 1000.0) / 1e9
+        rooflines[cat] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                          "traffic": traffic_for(cat, "config5"), "kernel": cat, "avg_launch_ms": avg,
+                          "launches": cat_n, "share_of_step": cat_ms / prof_ms, "algorithmic_bytes_per_launch": b,
+                          "bytes_model": bd, "peak_source": peak_src}
+    roofline = max(rooflines.values(), key=lambda r: r["share_of_step"]) if rooflines else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded procedural room; BASELINE config 5 shapes)",
+        "config": {"workload": "config5: 256 candidate views x 6 twist directions, 320x240 lifted raycast each, "
+                               "over the config-2 scene fused at 5 mm (hashed)", "views": len(views_all),
+                   "views_per_rank": len(views), "directions": 6, "order": 1,
+                   "parallelism": f"views sharded x{world}", "l2": "hashed volume (GBs) >> L2"},
+        "e2e": {"value": units * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(views.nbytes),
+                "d2h_bytes_per_step": int(len(views) * 7 * 8)},
+        "gpu_launches": int(launches), "roofline": roofline, "roofline_by_kernel": rooflines, "clocks": clk,
+        "kernel_ms_per_step": {c: v[0] / args.steps for c, v in prof.items()},
+        "profiled_ms_per_step": prof_ms / args.steps,
+        "scores_head": [float(x) for x in sc[:4]], "grad_head": [float(x) for x in g[0]],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle import orc
+            hp = __import__("paper_2405_02187_b200").capi.HashParams(0.005, (__import__("ctypes").c_double * 3)(0, 0, 0),
+                                                                     0.025, 128.0, 20, 1 << 18)
+            vo = orc.Volume(hp, 6, True)
+            for f in range(n_frames):
+                pose = np.zeros((12, 7))
+                pose[:, 0] = gt[f]
+                vo.surface_update(depth[f].astype(np.float64), pose, intr)
+            t1 = time.perf_counter()
+            nv = 4
+            vo.view_scores(views_all[:nv], kv)
+            secs = time.perf_counter() - t1
+            cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+            line["cpu_baseline"] = {"value": nv * 6 / secs, "unit": UNIT, "cores": cores, "kind": "port",
+                                    "sample": f"{nv} views x 6 directions, one Lifted<6> pass per view "
+                                              f"({nv * 6} units in {secs:.2f} s; volume fusion not timed)"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.workload == "config5" and args.impl != "reference":
+        run_config5(args)
+        return
     second = args.workload == "config3"
     if args.frames <= 0:
         args.frames = 30 if second else 100

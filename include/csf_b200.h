@@ -209,6 +209,19 @@ int csf_track_frame(csf_volume vol, const double* depth, int w, int h, const dou
 int csf_icp_energy_derivs(csf_ctx ctx, const double* corrs, int n, const double* base, const double* xi, double h,
                           double* energy, double* gradient, double* hessian);
 
+/* ---- BASELINE config 5: active-scanning view scoring --------------------------
+ * Builder-defined objective (the spec's task-gradient "smooth visibility
+ * score", is unimplemented in the reference): for each
+ * candidate camera->world view T [n][12], S(T) = pairwise_sum over the
+ * k->width x k->height pixels (row-major) of sigma(beta (w0 - W~(p))) at the
+ * raycast hit p (0 for misses), W~ = trilinear interpolation of the integral
+ * fusion weights — a soft count of weakly observed surface the view would
+ * see.  grads [n][6] (optional) = dS/dxi of exp(xi) T by CSFD (step h), one
+ * lifted raycast per view.  vol: hashed, created with 6 channels, fused with
+ * unperturbed poses. */
+int csf_view_scores(csf_volume vol, const double* poses, int n_views, const csf_intrinsics* k, double w0, double beta,
+                    double h, double* scores, double* grads);
+
 /* ---- pipeline ------------------------------------------------------------ */
 int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf_pipeline* out);
 int csf_pipeline_destroy(csf_pipeline p);

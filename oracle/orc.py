@@ -44,6 +44,8 @@ def lib() -> C.CDLL:
                                      dp, C.POINTER(_capi.TrackResult)]),
             "orc_workload": (ip, [ip, ip, ip, ip, fp, dp, C.POINTER(_capi.Intrinsics)]),
             "orc_pipeline_run": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, i32p, dp]),
+            "orc_view_scores": (ip, [vp, dp, ip, C.POINTER(_capi.Intrinsics), C.c_double, C.c_double, C.c_double,
+                                     dp, dp]),
             "orc_icp_energy_derivs": (ip, [dp, ip, dp, dp, C.c_double, dp, dp, dp]),
             "orc_pipeline_hessian": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, dp, dp, i32p, dp]),
         }
@@ -153,6 +155,14 @@ class Volume:
                                      nxt.ctypes.data_as(C.POINTER(C.c_int32)),
                                      coords.ctypes.data_as(C.POINTER(C.c_int32))))
         return heads, keys, nxt, coords
+
+    def view_scores(self, poses, k, w0=10.0, beta=0.5, h=1e-8):
+        """BASELINE config 5 objective and its view-twist gradient (builder-defined)."""
+        p = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 12)
+        sc = np.empty(p.shape[0])
+        g = np.empty((p.shape[0], 6))
+        _check(lib().orc_view_scores(self.h, _dp(p), p.shape[0], C.byref(k), w0, beta, h, _dp(sc), _dp(g)))
+        return sc, g
 
     def track_frame(self, depth, init_pose12, k, cfg, canonical=True):
         d = np.ascontiguousarray(depth, dtype=np.float64)

@@ -134,6 +134,8 @@ struct VolBase {
   virtual void hash_tables(int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords) const = 0;
   virtual TrackResult track(const Image<double>& depth, const Pose& init, const Intrinsics& k, const IcpConfig& cfg,
                             bool canonical) const = 0;
+  virtual void view_scores(const double* poses, int n, const Intrinsics& k, double w0, double beta, double h,
+                           double* scores, double* grads) const = 0;
 };
 
 template <int D, bool H>
@@ -196,6 +198,30 @@ struct Vol : VolBase {
   TrackResult track(const Image<double>& depth, const Pose& init, const Intrinsics& k, const IcpConfig& cfg,
                     bool canonical) const override {
     return track_frame(vol, depth, init, k, cfg, nullptr, canonical);
+  }
+  // config 5: one Lifted<6> pass per view over the volume's real field
+  void view_scores(const double* poses, int n, const Intrinsics& k, double w0, double beta, double h, double* scores,
+                   double* grads) const override {
+    if constexpr (H && D == 6) {
+      using S = Lifted<6>;
+      for (int v = 0; v < n; ++v) {
+        Vec6<S> xi;
+        for (int i = 0; i < 6; ++i) {
+          xi[i] = S(0.0);
+          xi[i].im[i] = h;
+        }
+        Pose base;
+        for (int e = 0; e < 9; ++e) base.rotation(e / 3, e % 3) = poses[12 * v + e];
+        for (int e = 0; e < 3; ++e) base.translation[e] = poses[12 * v + 9 + e];
+        const PoseT<S> view = exp_map(xi) * pose_cast<S>(base);
+        const S sc = view_coverage_score<S>(vol, view, k, w0, beta);
+        scores[v] = sc.re;
+        if (grads)
+          for (int d = 0; d < 6; ++d) grads[6 * v + d] = sc.im[d] / h;
+      }
+    } else {
+      throw std::invalid_argument("view_scores: needs a hashed volume with 6 channels");
+    }
   }
 };
 
@@ -375,6 +401,11 @@ void write_stats(int n_frames, const std::vector<int>& it, const std::vector<int
 }  // namespace
 
 extern "C" {
+
+int orc_view_scores(void* v, const double* poses, int n, const csf_intrinsics* k, double w0, double beta, double h,
+                    double* scores, double* grads) {
+  return guard([&] { static_cast<VolBase*>(v)->view_scores(poses, n, to_intr(*k), w0, beta, h, scores, grads); });
+}
 
 // icp_energy / icp_gradient / icp_hessian (icp.hpp:70-91) at xi (NULL = 0).
 int orc_icp_energy_derivs(const double* corrs, int n, const double* base, const double* xi, double h, double* E,

@@ -494,4 +494,55 @@ SurfaceMaps<S> raycast(const V& vol, const PoseT<S>& camera_to_world, const Intr
   return maps;
 }
 
+// ---------------------------------------------------------------------------
+// BUILDER-DEFINED (BASELINE config 5; the spec's unimplemented "smooth
+// visibility score"): soft count of weakly observed surface
+// seen from a view.  W~ = trilinear interpolation of the integral fusion
+// weights (sample_tsdf's cell and dk, dj, di order, tsdf.hpp:148-177;
+// unallocated corners count 0); score = pairwise_sum over all pixels
+// (row-major) of sigma(beta (w0 - W~(p))) at raycast hits (valid normal,
+// frames.hpp:73-81), 0 elsewhere.
+// ---------------------------------------------------------------------------
+template <typename S, typename V>
+S interpolated_weight(const V& vol, const Vec3<S>& p_world) {
+  const double vs = vol_voxel_size(vol);
+  const Vec3d& o = vol_origin(vol);
+  const S gx = (p_world.x() - S(o.x())) / S(vs);
+  const S gy = (p_world.y() - S(o.y())) / S(vs);
+  const S gz = (p_world.z() - S(o.z())) / S(vs);
+  const int i0 = ifloor_s(gx), j0 = ifloor_s(gy), k0 = ifloor_s(gz);
+  const S fx = gx - S(double(i0));
+  const S fy = gy - S(double(j0));
+  const S fz = gz - S(double(k0));
+  S accum = S(0.0);
+  for (int dk = 0; dk < 2; ++dk)
+    for (int dj = 0; dj < 2; ++dj)
+      for (int di = 0; di < 2; ++di) {
+        const typename V::field_type* f = nullptr;
+        double w = 0.0;
+        if (!vol.corner(i0 + di, j0 + dj, k0 + dk, &f, &w)) w = 0.0;
+        const S wx = di ? fx : S(1.0) - fx;
+        const S wy = dj ? fy : S(1.0) - fy;
+        const S wz = dk ? fz : S(1.0) - fz;
+        accum += wx * wy * wz * S(w);
+      }
+  return accum;
+}
+
+template <typename S, typename V, typename K>
+S view_coverage_score(const V& vol, const PoseT<S>& view, const IntrinsicsT<K>& k, double w0, double beta,
+                      const RaycastConfig& rc = {}) {
+  const SurfaceMaps<S> maps = raycast<S>(vol, view, k, rc);
+  std::vector<S> terms(maps.vertices.data.size(), S(0.0));
+  for (std::size_t i = 0; i < terms.size(); ++i) {
+    const Vec3<S>& n = maps.normals.data[i];
+    const double n0 = real_part(n[0]), n1 = real_part(n[1]), n2 = real_part(n[2]);
+    if (!(n0 * n0 + (n1 * n1 + n2 * n2) > 0.5)) continue;
+    const S wt = interpolated_weight<S>(vol, maps.vertices.data[i]);
+    const S z = S(beta) * (S(w0) - wt);
+    terms[i] = S(1.0) / (S(1.0) + exp(-z));
+  }
+  return pairwise_sum(terms);
+}
+
 }  // namespace orc

@@ -33,7 +33,7 @@ __all__ = [
     "InvalidArgument", "DomainError", "Context", "bilateral_filter", "downsample_depth", "build_depth_pyramid",
     "measure_surface", "TsdfVolume", "HashedVolume", "surface_update", "raycast", "track_frame", "TrackResult",
     "icp_energy", "icp_loss", "icp_gradient", "icp_hessian", "icp_energy_derivs",
-    "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
+    "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "look_at", "config5_views", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
     "lift_pose", "lift_intrinsics", "library",
 ]
 
@@ -356,6 +356,46 @@ class HashedVolume(_Volume):
             self.h, heads.ctypes.data_as(C.POINTER(C.c_int32)), keys.ctypes.data_as(C.POINTER(C.c_uint64)),
             nxt.ctypes.data_as(C.POINTER(C.c_int32)), coords.ctypes.data_as(C.POINTER(C.c_int32))))
         return heads, keys, nxt, coords
+
+    def view_scores(self, poses, k: _capi.Intrinsics, w0: float = 10.0, beta: float = 0.5, h: float = 1e-8):
+        """BASELINE config 5 (builder-defined objective, csf_view_scores): per candidate
+        camera->world view (n, 12) the soft count of weakly observed surface it would see
+        and its CSFD gradient w.r.t. the view's twist.  Needs channels == 6."""
+        P = _f64(poses).reshape(-1, 12)
+        sc = np.empty(P.shape[0])
+        g = np.empty((P.shape[0], 6))
+        self.ctx.check(self.ctx.lib.csf_view_scores(self.h, _dp(P), P.shape[0], C.byref(k), w0, beta, h, _dp(sc),
+                                                    _dp(g)))
+        return sc, g
+
+
+def look_at(eye, target, up=(0.0, 0.0, 1.0)) -> np.ndarray:
+    """camera->world pose (12,) of a camera at `eye` looking at `target` (z forward, y down)."""
+    eye, target, up = (np.asarray(a, dtype=np.float64) for a in (eye, target, up))
+    z = target - eye
+    z /= np.linalg.norm(z)
+    x = np.cross(z, up)
+    if np.linalg.norm(x) < 1e-9:
+        x = np.cross(z, np.array([1.0, 0.0, 0.0]))
+    x /= np.linalg.norm(x)
+    y = np.cross(z, x)
+    R = np.stack([x, y, z], axis=1)
+    return np.concatenate([R.reshape(9), eye])
+
+
+def config5_views(n: int = 256, seed: int = 4) -> np.ndarray:
+    """BASELINE config 5 candidate views (builder-defined, synthetic): n camera->world
+    poses (n, 12) with eyes uniform in the free annulus kept clear around the config-2
+    camera orbit (radius 0.9-1.5 m, height 0.9-1.7 m) looking at targets uniform in the
+    room interior, drawn from a seeded generator."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((n, 12))
+    for i in range(n):
+        r, th, z = rng.uniform(0.9, 1.5), rng.uniform(0.0, 2 * np.pi), rng.uniform(0.9, 1.7)
+        eye = np.array([r * np.cos(th), r * np.sin(th), z])
+        target = np.array([rng.uniform(-1.6, 1.6), rng.uniform(-1.6, 1.6), rng.uniform(0.3, 2.5)])
+        out[i] = look_at(eye, target)
+    return out
 
 
 def surface_update(volume: _Volume, depth, camera_to_world, k) -> int:

@@ -1053,6 +1053,62 @@ extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const d
 // track_frame (real tracker on the device)
 // ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
+// BASELINE config 5: view scoring (views.cu; builder-defined objective)
+// ---------------------------------------------------------------------------
+extern "C" int csf_view_scores(csf_volume v, const double* poses, int n_views, const csf_intrinsics* k, double w0,
+                               double beta, double h, double* scores, double* grads) {
+  if (!v || !poses || !k || n_views < 0 || !scores) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  if (!v->hashed || v->order != 1 || v->Dp != 6)
+    return fail(ctx, CSF_EINVAL, "csf_view_scores: needs a hashed volume created with 6 channels");
+  if (!(h > 0.0) || h > 1e-6) return fail(ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
+  if (k->width <= 0 || k->height <= 0) return fail(ctx, CSF_EINVAL, "csf_view_scores: bad image size");
+  cudaSetDevice(ctx->device);
+  const int W = k->width, H = k->height;
+  const size_t P = static_cast<size_t>(W) * H;
+  constexpr int C = 7;
+  const int chunk = std::max(1, std::min(n_views, static_cast<int>((size_t(1) << 27) / (C * P))));
+  CUDA_TRY(ctx, v->s_vre.alloc(3 * P));
+  CUDA_TRY(ctx, v->s_nre.alloc(3 * P));
+  CUDA_TRY(ctx, v->s_vim.alloc(3 * P * 6));
+  CUDA_TRY(ctx, v->s_nim.alloc(3 * P * 6));
+  CUDA_TRY(ctx, v->s_hits.alloc(2 * P));
+  CUDA_TRY(ctx, v->s_pose.alloc(12 * C + 12 * static_cast<size_t>(n_views)));
+  CUDA_TRY(ctx, v->s_intr.alloc(4 * C + 4));
+  DevBuf<double> terms;
+  CUDA_TRY(ctx, terms.alloc(static_cast<size_t>(chunk) * C * P));
+  double* d_pose = v->s_pose.p;
+  double* d_views = v->s_pose.p + 12 * C;
+  double* d_intr = v->s_intr.p;
+  double* d_k4 = v->s_intr.p + 4 * C;
+  const double k4[4] = {k->fx, k->fy, k->cx, k->cy};
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_views, poses, sizeof(double) * 12 * n_views, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_k4, k4, sizeof(k4), cudaMemcpyHostToDevice, ctx->stream));
+  csf_raycast_cfg rc;
+  csf_default_raycast_cfg(&rc);
+  const Launch L = launch_of(ctx);
+  std::vector<double> out(static_cast<size_t>(chunk) * C);
+  for (int v0 = 0; v0 < n_views; v0 += chunk) {
+    const int nv = std::min(chunk, n_views - v0);
+    for (int j = 0; j < nv; ++j) {
+      launch_view_seed(L, d_views + 12 * (v0 + j), d_k4, h, d_pose, d_intr);
+      raycast_dev(v, d_pose, d_intr, W, H, rc, v->s_hits.p, v->s_vre.p, v->s_nre.p, v->s_vim.p, v->s_nim.p);
+      PROF(ctx, kPMisc);
+      launch_view_terms(L, v->hash, v->s_vre.p, v->s_nre.p, v->s_vim.p, W, H, w0, beta, terms.p + j * C * P);
+    }
+    const int rc2 = tree_sum_slots(ctx->stream, ctx->energy, terms.p, static_cast<int>(P), nv * C, out.data());
+    if (rc2 == 5) return fail(ctx, CSF_ENOMEM, "csf_view_scores: out of device memory");
+    if (rc2) return fail(ctx, CSF_ECUDA, "csf_view_scores: CUDA error");
+    for (int j = 0; j < nv; ++j) {
+      scores[v0 + j] = out[j * C];
+      if (grads)
+        for (int d = 0; d < 6; ++d) grads[(v0 + j) * 6 + d] = out[j * C + 1 + d] / h;  // extract_derivative
+    }
+  }
+  return sync_check(ctx, "csf_view_scores");
+}
+
+// ---------------------------------------------------------------------------
 // icp energy and its CSFD derivatives (icp.hpp:70-91)
 // ---------------------------------------------------------------------------
 extern "C" int csf_icp_energy_derivs(csf_ctx ctx, const double* corrs, int n, const double* base, const double* xi,

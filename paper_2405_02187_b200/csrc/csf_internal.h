@@ -89,6 +89,8 @@ struct EnergyScratch {
   size_t flags_cap = 0;
   void* cub = nullptr;
   size_t cub_bytes = 0;
+  double* out = nullptr;  // tree_sum_slots results
+  size_t out_cap = 0;
 };
 // order 0: energy; 1: + gradient; 2: + Hessian.  Synchronous on `stream`.
 // Returns 0, 4 (CUDA error) or 5 (out of memory).
@@ -98,6 +100,10 @@ int associate_list(cudaStream_t stream, EnergyScratch& ws, const double* depth, 
                    const double* intr4, const double* pose12, const double* pred_w2c12, const double* vre,
                    const double* nre, double d_max, double cos_max, int* n_out);
 void energy_scratch_release(EnergyScratch& ws);
+// pairwise_sum of every slot of device terms [C][n] into out_host[C] (synchronous)
+int tree_sum_slots(cudaStream_t stream, EnergyScratch& ws, const double* terms, int n, int C, double* out_host);
+
+
 
 struct Launch {
   cudaStream_t stream;
@@ -163,5 +169,14 @@ void launch_objective2(const Launch& L, int Dp, int n_pairs, const double* traj,
                        int kind, double* out);
 void launch_linearized_corrs(const Launch& L, const double* corrs, int n, const double* base, double* partials,
                              int* counts);
+
+// ---- views.cu: BASELINE config 5 view scoring
+// pose_out [12][7]: exp(xi) * view with xi seeded h on the 6 twist channels;
+// intr_out [4][7] (zero channels)
+void launch_view_seed(const Launch& L, const double* view12, const double* k4, double h, double* pose_out,
+                      double* intr_out);
+// terms [7][w*h]: sigma(beta (w0 - W~(p))) of every raycast hit (0 elsewhere)
+void launch_view_terms(const Launch& L, const HashDev& v, const double* vre, const double* nre, const double* vim,
+                       int w, int h, double w0, double beta, double* terms);
 
 }  // namespace csfi

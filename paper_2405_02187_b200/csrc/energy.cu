@@ -314,6 +314,39 @@ int icp_energy_derivs(cudaStream_t stream, EnergyScratch& ws, const double* corr
   return 0;
 }
 
+// pairwise_sum (diff.hpp:16-37) of every slot of terms [C][n] (device) into
+// out_host[C]; synchronous.  Returns 0, 4 or 5 like icp_energy_derivs.
+int tree_sum_slots(cudaStream_t stream, EnergyScratch& ws, const double* terms, int n, int C, double* out_host) {
+  if (n <= 0) {
+    std::fill(out_host, out_host + C, 0.0);
+    return 0;
+  }
+  int d0 = 0;
+  while (d0 < 10 && (n >> d0) > 8) ++d0;
+  const int nsub = 1 << d0;
+  if (ws.sub_cap < static_cast<size_t>(C) * nsub || !ws.sub) {
+    if (ws.sub) cudaFree(ws.sub);
+    ws.sub = nullptr;
+    ws.sub_cap = 0;
+    if (cudaMalloc(&ws.sub, sizeof(double) * C * nsub) != cudaSuccess) return 5;
+    ws.sub_cap = static_cast<size_t>(C) * nsub;
+  }
+  if (ws.out_cap < static_cast<size_t>(C) || !ws.out) {
+    if (ws.out) cudaFree(ws.out);
+    ws.out = nullptr;
+    ws.out_cap = 0;
+    if (cudaMalloc(&ws.out, sizeof(double) * C) != cudaSuccess) return 5;
+    ws.out_cap = static_cast<size_t>(C);
+  }
+  double* out = ws.out;
+  launch_pdl(k_tree_sub, dim3((nsub + 127) / 128, C), dim3(128), 0, stream, terms, n, d0, ws.sub);
+  launch_pdl(k_tree_top, dim3(C), dim3(512), 0, stream, static_cast<const double*>(ws.sub), d0, out);
+  chk("tree_sum");
+  if (cudaMemcpyAsync(out_host, out, sizeof(double) * C, cudaMemcpyDeviceToHost, stream) != cudaSuccess) return 4;
+  if (cudaStreamSynchronize(stream) != cudaSuccess) return 4;
+  return 0;
+}
+
 void energy_scratch_release(EnergyScratch& ws) {
   if (ws.terms) cudaFree(ws.terms);
   if (ws.sub) cudaFree(ws.sub);
@@ -322,6 +355,7 @@ void energy_scratch_release(EnergyScratch& ws) {
   if (ws.corrs) cudaFree(ws.corrs);
   if (ws.flags) cudaFree(ws.flags);
   if (ws.cub) cudaFree(ws.cub);
+  if (ws.out) cudaFree(ws.out);
   ws = EnergyScratch{};
 }
 
