@@ -31,6 +31,13 @@ hashed TSDF (100 VGA frames at the ground-truth poses, untimed setup), then
 pose lifted on its 6 twist channels, scored by the builder-defined coverage
 objective.  Units = views x 6 directions (1536 per step).
 
+--workload config4: BASELINE config 4 — 500 VGA frames over a 60x60 m
+procedural terrain with 200 boxes (seed 3), hashed 2 cm voxels; 64
+directions = 6 first-frame twist + 4 intrinsics + 6 x 9 keyframe twists
+(keyframes every 50 frames).  The job is 8 directions per GPU at 8 GPUs:
+each rank runs its 8-direction share (rank r of the 8-way split), so the
+per-GPU work is fixed ("weak"); units = frames x directions over all ranks.
+
 --workload config3: BASELINE config 3 — the same VGA scene, 30 frames, the
 full 10x10 Hessian as 55 second-order parameter pairs (one reference
 Bicomplex per pair, packed as channel slots of one evaluation).  Units =
@@ -61,6 +68,7 @@ METRIC = "CSFD SLAM frame-derivatives/sec at 640×480 (frames×directions/s), 1/
 UNIT = "frame-derivatives/s"
 DIRS = list(range(10))  # 6 first-frame twist components (rho, phi) + fx, fy, cx, cy
 PAIRS = [(i, j) for i in range(10) for j in range(i, 10)]  # 55 Hessian pairs (config 3)
+DIRS4 = list(range(64))  # config 4: 0-5 first-frame twist, 6-9 intrinsics, 10-63 keyframes 1-9 (every 50 frames)
 
 
 def parse():
@@ -69,13 +77,20 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["config2", "config3", "config5"], default="config2")
+    ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5"], default="config2")
     ap.add_argument("--frames", type=int, default=0, help="0 = the workload's frame count (100 / 30)")
     ap.add_argument("--cpu-frames", type=int, default=5, help="CPU-baseline sample: frames")
     ap.add_argument("--cpu-dirs", type=int, default=2, help="CPU-baseline sample: directions (one pass each)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-json", default="")
     return ap.parse_args()
+
+
+def pipeline_cfg4(csf, capi, k, dirs, n_frames):
+    import ctypes as C
+    hp = capi.HashParams(0.02, (C.c_double * 3)(0.0, 0.0, 0.0), 5 * 0.02, 128.0, 20, 1 << 21)
+    return csf.make_pipeline_cfg(hashed=True, k=k, dirs=dirs, h=1e-8, objective=capi.OBJECTIVE_TRAJECTORY_ERROR,
+                                 max_frames=n_frames, hash_params=hp, keyframe_interval=50)
 
 
 def pipeline_cfg(csf, capi, k, dirs, n_frames, pairs=None):
@@ -160,6 +175,9 @@ def cpu_baseline(depth, gt, k, frames, ndirs, workload="config2"):
         if workload == "config3":
             cfg = pipeline_cfg(csf, capi, k, [], frames, pairs=[PAIRS[d]])
             secs += orc.pipeline_hessian(cfg, depth[:frames], gt[:frames])[-1]
+        elif workload == "config4":
+            cfg = pipeline_cfg4(csf, capi, k, [DIRS4[d]], frames)
+            secs += orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
         else:
             cfg = pipeline_cfg(csf, capi, k, [DIRS[d]], frames)
             secs += orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
@@ -216,9 +234,12 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
         return
     frames = 3
-    depth, gt, k = orc.workload(2, frames)
+    depth, gt, k = orc.workload(4 if args.workload == "config4" else 2, frames)
     second = args.workload == "config3"
-    cfg = pipeline_cfg(csf, capi, k, [0], frames, pairs=[PAIRS[1]] if second else None)
+    if args.workload == "config4":
+        cfg = pipeline_cfg4(csf, capi, k, [0], frames)
+    else:
+        cfg = pipeline_cfg(csf, capi, k, [0], frames, pairs=[PAIRS[1]] if second else None)
     run = (lambda: orc.pipeline_hessian(cfg, depth, gt)) if second else (lambda: orc.pipeline_run(cfg, depth, gt))
     for _ in range(args.warmup):
         run()
@@ -408,8 +429,9 @@ def main():
         run_config5(args)
         return
     second = args.workload == "config3"
+    four = args.workload == "config4"
     if args.frames <= 0:
-        args.frames = 30 if second else 100
+        args.frames = 30 if second else (500 if four else 100)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -429,10 +451,16 @@ def main():
     from paper_2405_02187_b200 import capi
     ctx = csf.Context(local)
     n = args.frames
-    depth, gt, k = csf.synth_workload(2, n, ctx=ctx)
-    units_all = PAIRS if second else DIRS          # the sharded work items
-    off, mine = shard_directions(units_all, world, rank)
-    cfg = pipeline_cfg(csf, capi, k, mine, n, pairs=mine if second else None)
+    depth, gt, k = csf.synth_workload(4 if four else 2, n, ctx=ctx)
+    if four:
+        # weak scaling: every rank runs one 8-direction share of the 8-GPU job
+        off, mine = shard_directions(DIRS4, 8, rank % 8)
+        units_all = [d for r in range(world) for d in shard_directions(DIRS4, 8, r % 8)[1]]
+        cfg = pipeline_cfg4(csf, capi, k, mine, n)
+    else:
+        units_all = PAIRS if second else DIRS          # the sharded work items
+        off, mine = shard_directions(units_all, world, rank)
+        cfg = pipeline_cfg(csf, capi, k, mine, n, pairs=mine if second else None)
     pipe = csf.Pipeline(cfg, ctx=ctx)
     pipe.upload(depth, gt)
     stream = torch.cuda.ExternalStream(ctx.stream)
@@ -475,6 +503,8 @@ def main():
         ms = float(t.item())
         cols = gather_columns(torch.from_numpy(np.asarray(local_cols)).cuda(), len(units_all), world,
                               rank).cpu().numpy()
+    if four and dist is None:
+        cols = local_cols
     else:
         cols = local_cols
 
@@ -531,15 +561,20 @@ def main():
                           "peak_source": peak_src}
     roofline = max(rooflines.values(), key=lambda r: r["share_of_step"]) if rooflines else None
 
-    if second:
+    if four:
+        workload = (f"config4: {n} VGA frames, 60x60 m terrain + 200 boxes, hashed 8^3 blocks 2 cm, 64 directions "
+                    f"(6 first-frame + 4 intrinsics + 54 keyframe twists), 8 directions per GPU")
+    elif second:
         workload = (f"config3: {n} VGA frames, hashed 8^3 blocks 5 mm, 2^20 buckets, 10x10 Hessian = "
                     f"{len(PAIRS)} bicomplex pairs")
     else:
         workload = f"config2: {n} VGA frames, hashed 8^3 blocks 5 mm, 2^20 buckets, {len(DIRS)} CSFD directions"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded procedural room rendered on device; BASELINE config 2 shapes)",
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak" if four else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": ("synthetic (seeded procedural terrain rendered on device; BASELINE config 4 shapes)" if four else
+                 "synthetic (seeded procedural room rendered on device; BASELINE config 2 shapes)"),
         "config": {"workload": workload, "frames": n, "directions": len(units_all),
                    "directions_per_rank": len(mine), "order": 2 if second else 1,
                    "parallelism": f"{'pairs' if second else 'directions'} sharded x{world}",

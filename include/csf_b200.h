@@ -40,7 +40,7 @@ extern "C" {
 #define CSF_ECUDA 4
 #define CSF_ENOMEM 5
 
-#define CSF_MAX_DIRECTIONS 36
+#define CSF_MAX_DIRECTIONS 64
 #define CSF_MAX_PAIRS 64
 
 typedef struct csf_ctx_s* csf_ctx;
@@ -115,6 +115,9 @@ typedef struct {
  * fx, fy, cx, cy), fuse frame 0 at exp(xi0*) T0, track + fuse frames
  * 1..N-1 with the lifted tracker, differentiate the objective.
  *
+ * Direction codes: 0..5 first-frame twist, 6..9 intrinsics, 10.. keyframe
+ * twists (keyframe_interval below).
+ *
  * order = 2 (BASELINE config 3): instead of dirs, n_pairs parameter pairs
  * (pair_i[p], pair_j[p]) each carried as one reference Bicomplex
  * (csfd.hpp:83-140; im1 seeded on pair_i, im2 on pair_j) packed as three
@@ -137,6 +140,11 @@ typedef struct {
   int n_pairs;                  /* order 2 */
   int pair_i[CSF_MAX_PAIRS];
   int pair_j[CSF_MAX_PAIRS];
+  /* Keyframe perturbations (BASELINE config 4, builder-defined): with
+   * keyframe_interval K > 0, direction code 10 + 6 (kf - 1) + c (kf >= 1,
+   * c = 0..5 in (rho, phi) order) perturbs the tracked pose of frame kf*K by
+   * exp(xi) (left increment, se3.hpp:116-119) before it is fused. */
+  int keyframe_interval;
 } csf_pipeline_cfg;
 
 /* ---- defaults (the reference's struct defaults) ------------------------- */

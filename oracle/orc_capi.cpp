@@ -372,6 +372,7 @@ PipelineConfig to_pipeline(const csf_pipeline_cfg* c) {
   cfg.h = StepSize(c->h).h;
   cfg.directions.assign(c->dirs, c->dirs + c->n_dirs);
   cfg.objective = static_cast<Objective>(c->objective);
+  cfg.keyframe_interval = c->keyframe_interval;
   return cfg;
 }
 void to_frames(const PipelineConfig& cfg, const float* depth, const double* gt_in, int n_frames,

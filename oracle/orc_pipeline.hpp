@@ -100,8 +100,10 @@ struct PipelineConfig {
   IcpConfig icp;
   RaycastConfig rc;
   double h = 1e-8;
-  std::vector<int> directions;  // parameter per channel: 0..5 twist (rho, phi), 6..9 fx, fy, cx, cy
+  std::vector<int> directions;  // parameter per channel: 0..5 twist (rho, phi), 6..9 fx, fy, cx, cy,
+                                // 10 + 6 (kf - 1) + c: keyframe kf's twist component c
   Objective objective = Objective::kFinalTranslationError;
+  int keyframe_interval = 0;    // BUILDER-DEFINED (config 4): keyframes at frames kf * K
 };
 
 struct PipelineResult {
@@ -134,6 +136,21 @@ struct LiftedRun {
   std::vector<int> iterations, correspondences, blocks, visible;
 };
 
+// Keyframe perturbation seeds of keyframe kf (first order only): exp(xi) *
+// pose with xi[c].im[d] = h for the channels coded 10 + 6 (kf - 1) + c.
+template <typename S>
+Vec6<S> keyframe_xi(const PipelineConfig& cfg, int kf) {
+  Vec6<S> xi;
+  for (int i = 0; i < 6; ++i) xi[i] = S(0.0);
+  if constexpr (!std::is_same_v<S, Bicomplex>) {
+    for (std::size_t d = 0; d < cfg.directions.size(); ++d) {
+      const int c = cfg.directions[d] - (10 + 6 * (kf - 1));
+      if (c >= 0 && c < 6) xi[c].im[d] = cfg.h;
+    }
+  }
+  return xi;
+}
+
 template <typename S, typename V>
 LiftedRun<S> run_lifted(V& vol, const PipelineConfig& cfg, const std::vector<Image<double>>& frames,
                         const std::vector<Pose>& gt, const Vec6<S>& xi, const IntrinsicsT<S>& ks) {
@@ -163,6 +180,10 @@ LiftedRun<S> run_lifted(V& vol, const PipelineConfig& cfg, const std::vector<Ima
     res.poses[f] = tr.pose;
     res.iterations[f] = tr.iterations;
     res.correspondences[f] = tr.correspondences;
+    if constexpr (!std::is_same_v<S, Bicomplex>) {
+      if (cfg.keyframe_interval > 0 && f % cfg.keyframe_interval == 0)
+        res.poses[f] = exp_map(keyframe_xi<S>(cfg, f / cfg.keyframe_interval)) * res.poses[f];
+    }
     integrate(f);
   }
   S obj(0.0);
@@ -210,7 +231,8 @@ PipelineResult run_pipeline_on(V& vol, const PipelineConfig& cfg, const std::vec
   Vec6<S> xi;
   for (int i = 0; i < 6; ++i) xi[i] = S(0.0);
   IntrinsicsT<S> ks = lift_intrinsics<S>(cfg.k);
-  for (int d = 0; d < D; ++d) seed_parameter(cfg.directions[d], xi, ks, [&](S& s) { s.im[d] = cfg.h; });
+  for (int d = 0; d < D; ++d)
+    if (cfg.directions[d] < 10) seed_parameter(cfg.directions[d], xi, ks, [&](S& s) { s.im[d] = cfg.h; });
   const LiftedRun<S> run = run_lifted<S>(vol, cfg, frames, gt, xi, ks);
   PipelineResult res;
   res.poses.assign(static_cast<std::size_t>(n) * 12 * (1 + D), 0.0);
@@ -319,6 +341,7 @@ inline PipelineResult run_pipeline_dyn(const PipelineConfig& cfg, const std::vec
     case 7: return run_pipeline<7>(cfg, frames, gt);
     case 8: return run_pipeline<8>(cfg, frames, gt);
     case 10: return run_pipeline<10>(cfg, frames, gt);
+    case 12: return run_pipeline<12>(cfg, frames, gt);
     default: throw std::invalid_argument("oracle pipeline: unsupported direction count");
   }
 }
@@ -404,11 +427,66 @@ inline HashParams config2_hash() {
   return hp;
 }
 
+// Config 4: 60x60 m procedural terrain (6 plane waves) + 200 boxes (seed 3),
+// VGA, depth range 0.3-20 m, sigma = 0.0012 z^2; the camera flies a half
+// circle of radius 10 m, 2 m above the ground, looking ~6 m ahead
+// (0.36 deg / 6.3 cm per frame over 500 frames); boxes keep clear of the
+// flight path (|r - 10| > 1.2 m + their footprint radius).  Hashed 2 cm voxels.
+inline Scene config4_scene(uint64_t seed = 3) {
+  Scene s;
+  Uniform53 u(seed);
+  double lip = 0.0;
+  for (int i = 0; i < 6; ++i) {
+    TerrainWave w;
+    const double amp = u.next(0.1, 0.4);
+    const double lambda = u.next(2.5, 20.0);
+    const double ang = u.next(0.0, 2.0 * M_PI);
+    const double phase = u.next(0.0, 2.0 * M_PI);
+    const double k = (2.0 * M_PI) / lambda;
+    w.a = amp;
+    w.kx = k * m_cos(ang);
+    w.ky = k * m_sin(ang);
+    w.phase = phase;
+    s.terrain.push_back(w);
+    lip = lip + amp * k;
+  }
+  s.terrain_inv_lip = 1.0 / std::sqrt(1.0 + lip * lip);
+  int placed = 0;
+  while (placed < 200) {
+    const double x = u.next(-30.0, 30.0);
+    const double y = u.next(-30.0, 30.0);
+    const double hx = u.next(0.3, 1.5), hy = u.next(0.3, 1.5), hz = u.next(0.3, 2.0);
+    const double r = std::sqrt(x * x + y * y);
+    if (std::fabs(r - 10.0) < 1.2 + std::sqrt(hx * hx + hy * hy)) continue;  // keep the flight path clear
+    s.boxes.push_back({Vec3d(x, y, s.height(x, y) + hz - 0.3), Vec3d(hx, hy, hz)});
+    ++placed;
+  }
+  return s;
+}
+inline Pose config4_pose(const Scene& s, int f) {
+  const double th = static_cast<double>(f) * (0.36 * M_PI / 180.0);
+  const double ex = 10.0 * m_cos(th), ey = 10.0 * m_sin(th);
+  const double tt = th + 0.6;
+  const double tx = 10.0 * m_cos(tt), ty = 10.0 * m_sin(tt);
+  return look_at_pose(Vec3d(ex, ey, s.height(ex, ey) + 2.0), Vec3d(tx, ty, s.height(tx, ty) + 0.5));
+}
+inline HashParams config4_hash() {
+  HashParams hp;
+  hp.voxel_size = 0.02;
+  hp.mu = 5.0 * hp.voxel_size;
+  hp.bucket_bits = 20;
+  hp.max_blocks = 1 << 21;
+  return hp;
+}
+
 inline Workload make_workload(int config, int n_frames, int width = 0, int height = 0) {
   Workload w;
   if (config == 1) {
     w.scene = config1_scene(0);
     w.k = config1_intrinsics();
+  } else if (config == 4) {
+    w.scene = config4_scene(3);
+    w.k = Intrinsics();
   } else {
     w.scene = config2_scene(1);
     w.k = Intrinsics();
@@ -420,13 +498,18 @@ inline Workload make_workload(int config, int n_frames, int width = 0, int heigh
     w.k.height = height;
   }
   for (int f = 0; f < n_frames; ++f) {
-    const Pose p = config == 1 ? config1_pose(f) : config2_pose(f);
+    const Pose p = config == 1 ? config1_pose(f) : config == 4 ? config4_pose(w.scene, f) : config2_pose(f);
     w.gt.push_back(p);
     Image<double> d = render_depth(w.scene, p, w.k);
-    if (config == 1)
+    if (config == 1) {
       d = add_depth_noise(d, 0.001, 1000 + f);
-    else
+    } else if (config == 4) {
+      d = add_depth_noise_quadratic(d, 0.0012, 0.0, 4000 + f);
+      for (auto& z : d.data)
+        if (z < 0.3) z = 0.0;  // depth range 0.3-20 m (the renderer stops at 20 m)
+    } else {
       d = add_depth_noise_quadratic(d, 0.0012, 0.05, 2000 + f);
+    }
     w.frames.push_back(to_float32(d));
   }
   return w;

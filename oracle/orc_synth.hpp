@@ -21,6 +21,11 @@ namespace orc {
 struct SdfSphere { Vec3d center; double radius = 0.5; };
 struct SdfBox { Vec3d center; Vec3d half_extents{0.25, 0.25, 0.25}; };
 struct SdfPlane { Vec3d normal{0.0, 0.0, 1.0}; double offset = 0.0; };
+// BUILDER-DEFINED (BASELINE config 4): a heightfield terrain as a sum of plane
+// waves, z = sum_i a_i sin(kx_i x + ky_i y + phase_i).  Its distance bound
+// (z - height) / sqrt(1 + L^2), L = sum_i |a_i| |k_i| >= |grad height|, keeps
+// sphere tracing Lipschitz-safe (SURVEY §8(d) "needs a Lipschitz-safe step").
+struct TerrainWave { double a = 0.0, kx = 0.0, ky = 0.0, phase = 0.0; };
 
 inline double vmax3(const Vec3d& q) { return std::max(q[0], std::max(q[1], q[2])); }
 
@@ -29,6 +34,13 @@ struct Scene {
   std::vector<SdfSphere> spheres;
   std::vector<SdfBox> boxes;
   std::vector<SdfPlane> planes;
+  std::vector<TerrainWave> terrain;
+  double terrain_inv_lip = 1.0;
+  double height(double x, double y) const {
+    double hgt = 0.0;
+    for (const auto& w : terrain) hgt = hgt + w.a * m_sin((w.kx * x + w.ky * y) + w.phase);
+    return hgt;
+  }
   double signed_distance(const Vec3d& p) const {
     double d = std::numeric_limits<double>::max();
     for (const auto& s : spheres) d = std::min(d, norm(p - s.center) - s.radius);
@@ -41,6 +53,7 @@ struct Scene {
       d = std::min(d, norm(outside) + inside);
     }
     for (const auto& pl : planes) d = std::min(d, dot(pl.normal, p) - pl.offset);
+    if (!terrain.empty()) d = std::min(d, (p[2] - height(p[0], p[1])) * terrain_inv_lip);
     return d;
   }
   // synth.cpp:36-45
@@ -90,6 +103,21 @@ inline Image<double> render_depth(const Scene& scene, const Pose& c2w, const Int
 // synth.cpp:92-105 (cos/sin through the deterministic kernels)
 inline Pose orbit_pose(const Vec3d& target, double radius, double height, double angle) {
   const Vec3d eye = target + Vec3d(radius * m_cos(angle), radius * m_sin(angle), height);
+  const Vec3d zc = normalized(target - eye);
+  const Vec3d xc = normalized(cross(zc, Vec3d(0.0, 0.0, 1.0)));
+  const Vec3d yc = cross(zc, xc);
+  Pose p;
+  for (int r = 0; r < 3; ++r) {
+    p.rotation(r, 0) = xc[r];
+    p.rotation(r, 1) = yc[r];
+    p.rotation(r, 2) = zc[r];
+  }
+  p.translation = eye;
+  return p;
+}
+
+// Camera at `eye` looking at `target` with the orbit_pose construction.
+inline Pose look_at_pose(const Vec3d& eye, const Vec3d& target) {
   const Vec3d zc = normalized(target - eye);
   const Vec3d xc = normalized(cross(zc, Vec3d(0.0, 0.0, 1.0)));
   const Vec3d yc = cross(zc, xc);

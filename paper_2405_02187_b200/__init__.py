@@ -577,10 +577,12 @@ def make_pipeline_cfg(*, hashed: bool, k: _capi.Intrinsics, dirs: Sequence[int],
                       max_frames: int, dense: Optional[_capi.VolumeParams] = None,
                       hash_params: Optional[_capi.HashParams] = None, icp: Optional[_capi.IcpCfg] = None,
                       rc: Optional[_capi.RaycastCfg] = None,
-                      pairs: Optional[Sequence[Tuple[int, int]]] = None) -> _capi.PipelineCfg:
+                      pairs: Optional[Sequence[Tuple[int, int]]] = None,
+                      keyframe_interval: int = 0) -> _capi.PipelineCfg:
     """Pipeline descriptor.  `dirs` = first-order parameters (0..5 twist, 6..9
     fx, fy, cx, cy); `pairs` (instead of dirs) = second-order parameter pairs
-    (i, j), order 2 (BASELINE config 3)."""
+    (i, j), order 2 (BASELINE config 3).  keyframe_interval K > 0 enables the
+    keyframe codes 10 + 6 (kf - 1) + c (BASELINE config 4)."""
     cfg = _capi.PipelineCfg()
     cfg.hashed = int(hashed)
     if dense is not None:
@@ -596,6 +598,7 @@ def make_pipeline_cfg(*, hashed: bool, k: _capi.Intrinsics, dirs: Sequence[int],
         cfg.dirs[i] = d
     cfg.objective = objective
     cfg.max_frames = max_frames
+    cfg.keyframe_interval = keyframe_interval
     cfg.order = 1
     if pairs is not None:
         if len(dirs):

@@ -13,7 +13,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ["CSF_B200_LIB"]) if os.environ.get("CSF_B200_LIB") else _HERE / "_build" / "libcsf_b200.so"
 
 CSF_OK, CSF_EINVAL, CSF_EDOMAIN, CSF_ERUNTIME, CSF_ECUDA, CSF_ENOMEM = 0, 1, 2, 3, 4, 5
-CSF_MAX_DIRECTIONS = 36
+CSF_MAX_DIRECTIONS = 64
 CSF_MAX_PAIRS = 64
 SOLVER_LINEARIZED, SOLVER_NEWTON, SOLVER_GRADIENT_DESCENT, SOLVER_CONJUGATE_GRADIENT = 0, 1, 2, 3
 OBJECTIVE_FINAL_TRANSLATION_ERROR, OBJECTIVE_TRAJECTORY_ERROR = 0, 1
@@ -67,7 +67,7 @@ class PipelineCfg(C.Structure):
                 ("icp", IcpCfg), ("rc", RaycastCfg), ("h", C.c_double), ("n_dirs", C.c_int),
                 ("dirs", C.c_int * CSF_MAX_DIRECTIONS), ("objective", C.c_int), ("max_frames", C.c_int),
                 ("order", C.c_int), ("n_pairs", C.c_int), ("pair_i", C.c_int * CSF_MAX_PAIRS),
-                ("pair_j", C.c_int * CSF_MAX_PAIRS)]
+                ("pair_j", C.c_int * CSF_MAX_PAIRS), ("keyframe_interval", C.c_int)]
 
 
 def load_library(path: os.PathLike | str | None = None) -> C.CDLL:

@@ -785,8 +785,14 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
     return fail(ctx, CSF_EINVAL, "csf_pipeline_create: n_dirs out of range");
   if (!(cfg->h > 0.0) || cfg->h > 1e-6)
     return fail(ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
-  for (int d = 0; d < cfg->n_dirs; ++d)
-    if (cfg->dirs[d] < 0 || cfg->dirs[d] > 9) return fail(ctx, CSF_EINVAL, "csf_pipeline_create: unknown direction");
+  if (cfg->keyframe_interval < 0) return fail(ctx, CSF_EINVAL, "csf_pipeline_create: negative keyframe_interval");
+  for (int d = 0; d < cfg->n_dirs; ++d) {
+    const int code = cfg->dirs[d];
+    const bool keyframe = cfg->keyframe_interval > 0 && code >= 10 &&
+                          1 + (code - 10) / 6 < (cfg->max_frames + cfg->keyframe_interval - 1) / cfg->keyframe_interval;
+    if (code < 0 || (code > 9 && !keyframe))
+      return fail(ctx, CSF_EINVAL, "csf_pipeline_create: unknown direction");
+  }
   if (order == 2) {
     if (cfg->n_pairs <= 0 || cfg->n_pairs > CSF_MAX_PAIRS || cfg->n_dirs != 0)
       return fail(ctx, CSF_EINVAL, "csf_pipeline_create: order 2 needs 1..CSF_MAX_PAIRS pairs and no dirs");
@@ -977,6 +983,8 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
         (void)tiles;
       }
     }
+    if (cfg.keyframe_interval > 0 && f % cfg.keyframe_interval == 0 && p->order == 1)
+      launch_keyframe_seed(L, p->G, p->Dp, p->dirs.p, p->D, cfg.h, f / cfg.keyframe_interval, p->pose.p);
     rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p, upd);
     if (rc) return rc;
     launch_frame_end(L, st, p->pose.p, p->traj.p, p->Dp, p->stats.p, nblk, counters);

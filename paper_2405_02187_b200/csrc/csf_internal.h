@@ -152,6 +152,8 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
 void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,
                  const double* intr_base, double* pose, double* intr_levels, int levels);
 void launch_frame_begin(const Launch& L, TrackState* st, int frame);
+// keyframe kf's twist seeds applied to the tracked pose (config 4)
+void launch_keyframe_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, int kf, double* pose);
 void launch_frame_end(const Launch& L, TrackState* st, const double* pose, double* traj, int Dp, int* stats,
                       const int* n_blocks, const int* counters);
 void launch_objective(const Launch& L, int G, int Dp, int D, const double* traj, const double* gt, int n_frames,

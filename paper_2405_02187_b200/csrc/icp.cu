@@ -107,7 +107,7 @@ CSF_DEV void group_sum(const double* __restrict__ partials, const int* __restric
 // systems (zero or sub-normal pivots) take the per-channel lifted LDLT
 // instead.  Then exp(delta) * T per channel thread (L<1>) and the break
 // decisions (icp.cpp:199,235) into TrackState.
-constexpr int kMaxC = 1 + 36;
+constexpr int kMaxC = 1 + 64;  // CSF_MAX_DIRECTIONS
 __global__ void __launch_bounds__(kRedThreads) k_icp_solve_t(TrackState* st, const double* __restrict__ gpartials,
                                                           const int* __restrict__ gcounts, int n_groups,
                                                           double* pose, int Dp, int level, double tol) {
@@ -497,6 +497,43 @@ __global__ void k_seed(const int* __restrict__ dirs, int D, double hstep, const 
   for (int l = 0; l < levels; ++l) {
     const double s = static_cast<double>(1 << l);
     for (int i = 0; i < 4; ++i) store_ch<S>(intr_levels + (l * 4 + i) * C, kk[i] / s, g0, G, gi == 0);
+  }
+}
+
+// Keyframe perturbation (config 4): pose <- exp(xi) pose, xi seeded on the
+// channels whose direction code is 10 + 6 (kf - 1) + c.  With no matching
+// channel exp(0) is the exact identity, so the real pose is unchanged.
+template <int G>
+__global__ void k_keyframe_seed(const int* __restrict__ dirs, int D, double hstep, int kf, double* pose, int Dp) {
+  pdl_wait();
+  pdl_trigger();
+  using S = Scal<G>;
+  const int C = 1 + Dp;
+  const int ngroups = G == 0 ? 1 : Dp / G;
+  const int gi = threadIdx.x;
+  const bool mine = gi < ngroups;
+  const int g0 = gi * G;
+  Pose<S> np;
+  if (mine) {
+    S xi[6];
+    for (int i = 0; i < 6; ++i) xi[i] = lit<S>(0.0);
+    if constexpr (G > 0) {
+      for (int g = 0; g < G; ++g) {
+        const int dd = g0 + g;
+        if (dd >= D) continue;
+        const int c = dirs[dd] - (10 + 6 * (kf - 1));
+        if (c >= 0 && c < 6) xi[c].im[g] = hstep;
+      }
+    }
+    Pose<S> cur;
+    for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+    for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
+    np = compose(exp_map<S>(xi), cur);
+  }
+  __syncthreads();  // every group has read the real part before group 0 rewrites it
+  if (mine) {
+    for (int e = 0; e < 9; ++e) store_ch<S>(pose + e * C, np.R.m[e], g0, G, gi == 0);
+    for (int e = 0; e < 3; ++e) store_ch<S>(pose + (9 + e) * C, np.t.v[e], g0, G, gi == 0);
   }
 }
 
@@ -977,6 +1014,15 @@ void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double 
     launch_pdl(k_seed<1>, dim3(1), dim3(64), 0, L.stream, dirs, D, h, gt0, intr_base, pose, intr_levels, levels, Dp);
   ++*L.launches;
   chk("seed");
+}
+
+void launch_keyframe_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, int kf, double* pose) {
+  if (G == 0)
+    launch_pdl(k_keyframe_seed<0>, dim3(1), dim3(64), 0, L.stream, dirs, D, h, kf, pose, Dp);
+  else
+    launch_pdl(k_keyframe_seed<1>, dim3(1), dim3(64), 0, L.stream, dirs, D, h, kf, pose, Dp);
+  ++*L.launches;
+  chk("keyframe_seed");
 }
 
 void launch_frame_begin(const Launch& L, TrackState* st, int frame) {

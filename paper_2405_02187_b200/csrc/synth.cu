@@ -17,11 +17,21 @@
 namespace csfd {
 
 struct SynthScene {
-  int n_spheres, n_boxes, n_planes;
+  int n_spheres, n_boxes, n_planes, n_waves;
   double sph[64][4];   // cx cy cz r
   double box[256][6];  // cx cy cz hx hy hz
   double pln[16][4];   // nx ny nz offset
+  double wave[8][4];   // terrain plane waves: a kx ky phase (config 4)
+  double inv_lip;      // 1 / sqrt(1 + L^2)
 };
+
+// config-4 terrain height (oracle Scene::height): sum of plane waves
+CSF_HD double terrain_height(const SynthScene& s, double x, double y) {
+  double hgt = 0.0;
+  for (int i = 0; i < s.n_waves; ++i)
+    hgt = hgt + s.wave[i][0] * csf_det::sin((s.wave[i][1] * x + s.wave[i][2] * y) + s.wave[i][3]);
+  return hgt;
+}
 
 __constant__ SynthScene c_scene;
 
@@ -45,6 +55,7 @@ CSF_DEV double scene_sdf(double px, double py, double pz) {
     const double* p = c_scene.pln[i];
     d = dmin(d, (p[0] * px + (p[1] * py + p[2] * pz)) - p[3]);
   }
+  if (c_scene.n_waves > 0) d = dmin(d, (pz - terrain_height(c_scene, px, py)) * c_scene.inv_lip);
   return d;
 }
 
@@ -136,9 +147,40 @@ static void add_room(csfd::SynthScene& s) {
   s.n_planes += 6;
 }
 
-// The oracle's config1_scene / config2_scene (oracle/orc_pipeline.hpp).
+// The oracle's config1_scene / config2_scene / config4_scene (oracle/orc_pipeline.hpp).
 static csfd::SynthScene config_scene(int config) {
   csfd::SynthScene s{};
+  s.inv_lip = 1.0;
+  if (config == 4) {
+    Uniform53 u(3);
+    double lip = 0.0;
+    for (int i = 0; i < 6; ++i) {
+      const double amp = u.next(0.1, 0.4);
+      const double lambda = u.next(2.5, 20.0);
+      const double ang = u.next(0.0, 2.0 * M_PI);
+      const double phase = u.next(0.0, 2.0 * M_PI);
+      const double k = (2.0 * M_PI) / lambda;
+      double* w = s.wave[s.n_waves++];
+      w[0] = amp;
+      w[1] = k * csf_det::cos(ang);
+      w[2] = k * csf_det::sin(ang);
+      w[3] = phase;
+      lip = lip + amp * k;
+    }
+    s.inv_lip = 1.0 / std::sqrt(1.0 + lip * lip);
+    int placed = 0;
+    while (placed < 200) {
+      const double x = u.next(-30.0, 30.0);
+      const double y = u.next(-30.0, 30.0);
+      const double hx = u.next(0.3, 1.5), hy = u.next(0.3, 1.5), hz = u.next(0.3, 2.0);
+      const double r = std::sqrt(x * x + y * y);
+      if (std::fabs(r - 10.0) < 1.2 + std::sqrt(hx * hx + hy * hy)) continue;  // keep the flight path clear
+      double* d = s.box[s.n_boxes++];
+      d[0] = x; d[1] = y; d[2] = csfd::terrain_height(s, x, y) + hz - 0.3; d[3] = hx; d[4] = hy; d[5] = hz;
+      ++placed;
+    }
+    return s;
+  }
   add_room(s);
   if (config == 1) {
     Uniform53 u(0);
@@ -197,10 +239,25 @@ static void orbit_pose(const double* target, double radius, double height, doubl
   P[9] = eye[0]; P[10] = eye[1]; P[11] = eye[2];
 }
 
+// oracle look_at_pose: the orbit_pose construction toward an explicit target
+static void look_at_pose(const double* eye, const double* target, double* P) {
+  double zc[3] = {target[0] - eye[0], target[1] - eye[1], target[2] - eye[2]};
+  normalize3(zc);
+  double xc[3] = {zc[1] * 1.0 - zc[2] * 0.0, zc[2] * 0.0 - zc[0] * 1.0, zc[0] * 0.0 - zc[1] * 0.0};
+  normalize3(xc);
+  const double yc[3] = {zc[1] * xc[2] - zc[2] * xc[1], zc[2] * xc[0] - zc[0] * xc[2], zc[0] * xc[1] - zc[1] * xc[0]};
+  for (int r = 0; r < 3; ++r) {
+    P[3 * r] = xc[r];
+    P[3 * r + 1] = yc[r];
+    P[3 * r + 2] = zc[r];
+  }
+  P[9] = eye[0]; P[10] = eye[1]; P[11] = eye[2];
+}
+
 int synth_workload(cudaStream_t stream, int config, int n_frames, int width, int height, float* depth_out,
                    double* gt_out, csf_intrinsics* k_out, std::string* err) {
-  if (config != 1 && config != 2) {
-    *err = "csf_synth_workload: config must be 1 or 2";
+  if (config != 1 && config != 2 && config != 4) {
+    *err = "csf_synth_workload: config must be 1, 2 or 4";
     return CSF_EINVAL;
   }
   csf_intrinsics k;
@@ -220,10 +277,19 @@ int synth_workload(cudaStream_t stream, int config, int n_frames, int width, int
   const csfd::SynthScene scene = config_scene(config);
   const double target[3] = {0.0, 0.0, 1.0};
   for (int f = 0; f < n_frames; ++f) {
-    if (config == 1)
+    if (config == 1) {
       orbit_pose(target, 1.0, 0.4, static_cast<double>(f) * (3.0 * M_PI / 180.0), gt_out + 12 * f);
-    else
+    } else if (config == 4) {
+      const double th = static_cast<double>(f) * (0.36 * M_PI / 180.0);
+      const double ex = 10.0 * csf_det::cos(th), ey = 10.0 * csf_det::sin(th);
+      const double tt = th + 0.6;
+      const double tx = 10.0 * csf_det::cos(tt), ty = 10.0 * csf_det::sin(tt);
+      const double eye[3] = {ex, ey, csfd::terrain_height(scene, ex, ey) + 2.0};
+      const double tgt[3] = {tx, ty, csfd::terrain_height(scene, tx, ty) + 0.5};
+      look_at_pose(eye, tgt, gt_out + 12 * f);
+    } else {
       orbit_pose(target, 1.2, 0.3, static_cast<double>(f) * (1.5 * M_PI / 180.0), gt_out + 12 * f);
+    }
   }
   const size_t P = static_cast<size_t>(k.width) * k.height;
   double* d_poses = nullptr;
@@ -258,6 +324,16 @@ int synth_workload(cudaStream_t stream, int config, int n_frames, int width, int
         const double n = d[i] + 0.001 * g.next();
         d[i] = n > 0.0 ? n : 0.0;
       }
+    } else if (config == 4) {
+      Gaussian g(4000 + f);
+      for (size_t i = 0; i < P; ++i) {
+        if (!(d[i] > 0.0)) continue;
+        const double sigma = 0.0012 * d[i] * d[i];
+        const double n = d[i] + sigma * g.next();
+        d[i] = n > 0.0 ? n : 0.0;
+      }
+      for (size_t i = 0; i < P; ++i)
+        if (d[i] < 0.3) d[i] = 0.0;  // depth range 0.3-20 m
     } else {
       const uint64_t seed = 2000 + f;
       Gaussian g(seed);
