@@ -1455,6 +1455,22 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
   return CSF_OK;
 }
 
+// Debug hook (not part of the public header): table-march statistics
+// (counted only in a -DCSF_MARCH_STATS build; tools/march_stats.py).
+namespace csfi { void march_stats_enable(unsigned long long* buf); }
+extern "C" int csf_debug_march_stats(unsigned long long* host_out /*[8]*/, int enable) {
+  static unsigned long long* dbuf = nullptr;
+  if (enable) {
+    if (!dbuf && cudaMalloc(&dbuf, 8 * sizeof(unsigned long long)) != cudaSuccess) return CSF_ENOMEM;
+    cudaMemset(dbuf, 0, 8 * sizeof(unsigned long long));
+    march_stats_enable(dbuf);
+    return CSF_OK;
+  }
+  march_stats_enable(nullptr);
+  if (dbuf && host_out) cudaMemcpy(host_out, dbuf, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return CSF_OK;
+}
+
 // Debug hook (not part of the public header): per-CTA ICP phase timestamps.
 extern "C" int csf_debug_icp_clock(unsigned long long* host_out, int enable) {
   static unsigned long long* dbuf = nullptr;

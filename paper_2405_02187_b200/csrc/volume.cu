@@ -574,6 +574,16 @@ CSF_DEV double box_exit(const HashView& vol, int bx, int by, int bz, int span, c
   return t;
 }
 
+// Debug statistics of the table march (tools/march_stats.py; null = off):
+// [0] rays, [1] loop trips, [2] super-block skips, [3] block skips,
+// [4] samples, [5] valid samples, [6] hits, [7] sum over warps of max trips.
+__device__ unsigned long long* g_march_stats = nullptr;
+#ifdef CSF_MARCH_STATS
+#define CSF_MSTAT(x) x
+#else
+#define CSF_MSTAT(x)
+#endif
+
 template <typename V>
 __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __restrict__ pose,
                                                        const double* __restrict__ intr, int w, int h, int Dp,
@@ -643,8 +653,26 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
       // Semantics are the loop below, sample for sample.
       const int nmax = n_tab - 1;  // atab[nmax] > t1 (sentinel)
       const double inv_step = 1.0 / step;
+#ifdef CSF_MARCH_STATS
+      unsigned long long* const dbg = g_march_stats;
+      unsigned trips = 0, sskip = 0, bskip = 0, nsamp = 0, nvalid = 0;
+      auto flush = [&](bool hit) {
+        if (!dbg) return;
+        atomicAdd(dbg + 0, 1ULL);
+        atomicAdd(dbg + 1, trips);
+        atomicAdd(dbg + 2, sskip);
+        atomicAdd(dbg + 3, bskip);
+        atomicAdd(dbg + 4, nsamp);
+        atomicAdd(dbg + 5, nvalid);
+        if (hit) atomicAdd(dbg + 6, 1ULL);
+        unsigned mx = trips;
+        for (int o2 = 16; o2 > 0; o2 >>= 1) mx = max(mx, __shfl_xor_sync(__activemask(), mx, o2));
+        if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(dbg + 7, mx);
+      };
+#endif
       int n = 0;
       while (n < nmax) {
+        CSF_MSTAT(++trips);
         const double alpha = atab[n];
         const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1],
                      pz = o.v[2] + alpha * dir.v[2];
@@ -657,6 +685,7 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
         else if (vol.block(bx, by, bz) < 0) span = 1;
         if (span > 0) {
           have_prev = false;
+          CSF_MSTAT(if (span == 8) ++sskip; else ++bskip;)
           const int m = span == 8 ? ~7 : ~0;
           const double lim = box_exit(vol, bx & m, by & m, bz & m, span, o, invd) - 1e-6;
           // first index > n whose alpha reaches lim (or the sentinel)
@@ -668,14 +697,17 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
           continue;
         }
         double f;
+        CSF_MSTAT(++nsamp);
         if (!sample_real(vol, px, py, pz, cache, &f)) {
           have_prev = false;
           ++n;
           continue;
         }
+        CSF_MSTAT(++nvalid);
         if (have_prev && f_prev > 0.0 && f < 0.0) {
           hits[pix] = make_double2(alpha_prev, alpha);
           hits[w * h + pix] = make_double2(f_prev, f);
+          CSF_MSTAT(flush(true));
           return;
         }
         have_prev = true;
@@ -683,6 +715,7 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
         f_prev = f;
         ++n;
       }
+      CSF_MSTAT(flush(false));
       return;
     }
   }
@@ -1461,6 +1494,8 @@ void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, c
   ++*L.launches;
   chk("integrate_hashed");
 }
+
+void march_stats_enable(unsigned long long* buf) { cudaMemcpyToSymbol(g_march_stats, &buf, sizeof(buf)); }
 
 int band_samples(double mu, double vs) {
   const int k = static_cast<int>(std::ceil((2.0 * mu) / vs)) + 1;
