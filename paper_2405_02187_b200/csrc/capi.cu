@@ -165,6 +165,7 @@ struct csf_volume_s {
   DevBuf<double2> s_hits;
   // raycast alpha table (hashed volumes) for (tab_near, tab_far, tab_step)
   DevBuf<double> alpha_tab;
+  DevBuf<unsigned> seg_first;  // segmented-march scratch
   double tab_near = 0.0, tab_far = -1.0, tab_step = 0.0;
 
   ~csf_volume_s() {
@@ -178,6 +179,7 @@ struct csf_volume_s {
     s_nim.release();
     s_hits.release();
     alpha_tab.release();
+    seg_first.release();
   }
 };
 
@@ -298,6 +300,11 @@ void raycast_dev(csf_volume v, const double* d_pose, const double* d_intr, int w
   if (v->hashed && ensure_alpha_table(v, rc.near_clip, rc.far_clip, step) != CSF_OK) {
     v->hash.alpha_tab = nullptr;  // fall back to the in-kernel repeated addition
     v->hash.alpha_n = 0;
+  }
+  if (v->hashed) {
+    if (v->seg_first.n < static_cast<size_t>(w) * h && v->seg_first.alloc(static_cast<size_t>(w) * h) != cudaSuccess)
+      v->seg_first.release();
+    v->hash.seg_first = v->seg_first.p;  // null: one thread per ray
   }
   for (int phase = 1; phase <= 2; ++phase) {
     PROF(v->ctx, phase == 1 ? kPRaycast : kPRaycastLift);

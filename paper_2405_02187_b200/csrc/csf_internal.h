@@ -40,6 +40,7 @@ struct HashDev {
   // (no slab clip), so it is tabulated once; a_{n_tab-1} > far is a sentinel.
   const double* alpha_tab = nullptr;
   int alpha_n = 0;
+  unsigned* seg_first = nullptr;  // [pixels] first crossing index of the segmented march
 };
 
 // Per-frame allocation scratch (hashed volumes).

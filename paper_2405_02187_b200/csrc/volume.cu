@@ -758,6 +758,135 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
   }
 }
 
+// Segmented march (hashed volumes, alpha table): the small pyramid levels
+// have few rays, so the level's time is the longest ray's sequential chain.
+// A ray's table indices are cut into S segments marched by S threads.  The
+// reference's crossing rule only carries the previous sample across a step
+// (have_prev resets on an invalid sample), so "crossing at index n" is a
+// pure predicate of samples n-1 and n: each segment evaluates the sample
+// before its first index to seed that state, marches its range with the
+// exact per-sample semantics, and the smallest crossing index over the
+// segments (atomicMin) is the sequential loop's first crossing.
+CSF_DEV bool table_sample(const HashView& vol, const V3<double>& o, const V3<double>& dir, double alpha, double* f) {
+  const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1], pz = o.v[2] + alpha * dir.v[2];
+  const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
+            k0 = ifloor((pz - vol.oz) / vol.vs);
+  const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
+  if (vol.super_occupied(bx, by, bz) == 0 || vol.block(bx, by, bz) < 0) return false;
+  NoCache c;
+  return sample_real(vol, px, py, pz, c, f);
+}
+
+CSF_DEV void ray_of(const double* s_pose, int x, int y, V3<double>* o, V3<double>* dir) {
+  Pose<double> c2w;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) c2w.R.m[e] = s_pose[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) c2w.t.v[e] = s_pose[9 + e];
+  const double fxk = s_pose[12], fyk = s_pose[13], cxk = s_pose[14], cyk = s_pose[15];
+  const V3<double> dc = mk3<double>((static_cast<double>(x) - cxk) / fxk, (static_cast<double>(y) - cyk) / fyk, 1.0);
+  const double rn = sqrt(dot3(dc, dc));
+  *dir = matvec(c2w.R, mk3<double>(dc.v[0] / rn, dc.v[1] / rn, dc.v[2] / rn));
+  *o = c2w.t;
+}
+
+__global__ void __launch_bounds__(128) k_raycast_march_seg(HashView vol, const double* __restrict__ pose,
+                                                           const double* __restrict__ intr, int w, int h, int Dp,
+                                                           int S, const double* __restrict__ atab, int n_tab,
+                                                           double step, unsigned* __restrict__ first) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double s_pose[16];
+  const int C = 1 + Dp;
+  if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
+  else if (threadIdx.x < 16) s_pose[threadIdx.x] = intr[(threadIdx.x - 12) * C];
+  __syncthreads();
+  const int P = w * h;
+  const long long item = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (item >= static_cast<long long>(P) * S) return;
+  const int seg = static_cast<int>(item / P), pix = static_cast<int>(item % P);
+  V3<double> o, dir;
+  ray_of(s_pose, pix % w, pix / w, &o, &dir);
+  V3<double> invd;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) invd.v[a] = dir.v[a] != 0.0 ? 1.0 / dir.v[a] : 0.0;
+  const int nmax = n_tab - 1;
+  const int n0 = static_cast<int>(static_cast<long long>(nmax) * seg / S);
+  const int n1 = static_cast<int>(static_cast<long long>(nmax) * (seg + 1) / S);
+  double f_prev = 0.0;
+  bool have_prev = n0 > 0 && table_sample(vol, o, dir, atab[n0 - 1], &f_prev);
+  const double inv_step = 1.0 / step;
+  int n = n0;
+  while (n < n1) {
+    const double alpha = atab[n];
+    const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1], pz = o.v[2] + alpha * dir.v[2];
+    const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
+              k0 = ifloor((pz - vol.oz) / vol.vs);
+    const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
+    const int occ = vol.super_occupied(bx, by, bz);
+    int span = 0;
+    if (occ == 0) span = 8;
+    else if (vol.block(bx, by, bz) < 0) span = 1;
+    if (span > 0) {
+      have_prev = false;
+      const int m = span == 8 ? ~7 : ~0;
+      const double lim = box_exit(vol, bx & m, by & m, bz & m, span, o, invd) - 1e-6;
+      int g = static_cast<int>(fmin(fmax((lim - atab[0]) * inv_step, 0.0), static_cast<double>(nmax)));
+      g = g < n + 1 ? n + 1 : g;
+      while (g > n + 1 && __ldg(atab + g - 1) >= lim) --g;
+      while (g < nmax && __ldg(atab + g) < lim) ++g;
+      n = g;
+      continue;
+    }
+    double f;
+    NoCache c;
+    if (!sample_real(vol, px, py, pz, c, &f)) {
+      have_prev = false;
+      ++n;
+      continue;
+    }
+    if (have_prev && f_prev > 0.0 && f < 0.0) {
+      atomicMin(first + pix, static_cast<unsigned>(n));
+      return;
+    }
+    have_prev = true;
+    f_prev = f;
+    ++n;
+  }
+}
+
+// Crossing of each pixel from the smallest segment index: the hit alphas and
+// the two sample values (re-evaluated, bit-identical), real maps cleared.
+__global__ void __launch_bounds__(128) k_raycast_march_fin(HashView vol, const double* __restrict__ pose,
+                                                           const double* __restrict__ intr, int w, int h, int Dp,
+                                                           const double* __restrict__ atab,
+                                                           const unsigned* __restrict__ first, double2* __restrict__ hits,
+                                                           double* __restrict__ vre, double* __restrict__ nre) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double s_pose[16];
+  const int C = 1 + Dp;
+  if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
+  else if (threadIdx.x < 16) s_pose[threadIdx.x] = intr[(threadIdx.x - 12) * C];
+  __syncthreads();
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= w * h) return;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) vre[3LL * pix + c] = nre[3LL * pix + c] = 0.0;
+  const unsigned n = first[pix];
+  if (n == 0xFFFFFFFFu) {
+    hits[pix] = make_double2(0.0, -1.0);
+    return;
+  }
+  V3<double> o, dir;
+  ray_of(s_pose, pix % w, pix / w, &o, &dir);
+  double f_prev = 0.0, f = 0.0;
+  table_sample(vol, o, dir, atab[n - 1], &f_prev);
+  table_sample(vol, o, dir, atab[n], &f);
+  hits[pix] = make_double2(atab[n - 1], atab[n]);
+  hits[w * h + pix] = make_double2(f_prev, f);
+}
+
 // Real trilinear sample that also returns what the channel pass needs: the
 // corner voxel ids, the corner weights and the derivative of the sample with
 // respect to the cell fractions (real parts of sample_tsdf<S>, bit-identical).
@@ -1537,7 +1666,7 @@ template <typename V>
 static void raycast_impl(const Launch& L, const V& view, Box box, int order, int G, int Dp, const double* pose,
                          const double* intr, int w, int h, double near_clip, double far_clip, double step,
                          double2* hits, double* vre, double* nre, double* vim, double* nim,
-                         const double* atab = nullptr, int n_tab = 0) {
+                         const double* atab = nullptr, int n_tab = 0, unsigned* seg_first = nullptr) {
   const int P = w * h;
   if (L.phase != 2) {
     // The warp-cooperative march measured slower than one thread per ray at
@@ -1545,7 +1674,26 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
     static const long long warp_threshold = std::getenv("CSF_MARCH_WARP_MAX")
                                                 ? std::atoll(std::getenv("CSF_MARCH_WARP_MAX"))
                                                 : 0;
-    if (P <= warp_threshold)
+    // segments per ray: enough threads to fill the GPU at the small levels
+    int S = 1;
+    if constexpr (V::kHashed) {
+      static const int seg_max = std::getenv("CSF_MARCH_SEG_MAX") ? std::atoi(std::getenv("CSF_MARCH_SEG_MAX")) : 16;
+      static const long long target =
+          std::getenv("CSF_MARCH_THREADS") ? std::atoll(std::getenv("CSF_MARCH_THREADS")) : 320000LL;
+      while (S < seg_max && static_cast<long long>(P) * S * 2 <= target) S *= 2;
+      if (!atab || !seg_first) S = 1;
+    }
+    if (S > 1) {
+      if constexpr (V::kHashed) {
+        cudaMemsetAsync(seg_first, 0xFF, sizeof(unsigned) * P, L.stream);
+        const long long items = static_cast<long long>(P) * S;
+        launch_pdl(k_raycast_march_seg, dim3(static_cast<unsigned>((items + 127) / 128)), dim3(128), 0, L.stream, view,
+                   pose, intr, w, h, Dp, S, atab, n_tab, step, seg_first);
+        launch_pdl(k_raycast_march_fin, dim3((P + 127) / 128), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp, atab,
+                   static_cast<const unsigned*>(seg_first), hits, vre, nre);
+        *L.launches += 1;
+      }
+    } else if (P <= warp_threshold)
       launch_pdl(k_raycast_march_warp<V>, dim3((P + 3) / 4), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp, near_clip, far_clip,
                                                                  step, box, hits, vre, nre);
     else
@@ -1620,7 +1768,7 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
   Box box;
   box.use = false;
   raycast_impl(L, view, box, v.order, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim,
-               v.alpha_tab, v.alpha_n);
+               v.alpha_tab, v.alpha_n, v.seg_first);
   chk("raycast_hashed");
 }
 
