@@ -67,7 +67,7 @@ CSF_DEV void load_pose_real(const double* p, int C, Pose<double>* out) {
 // wrote its own tile partials.
 constexpr int kGroup = 16;
 constexpr int kMaxGroupCtr = 256;  // tiles per launch <= kGroup * kMaxGroupCtr
-CSF_DEV void group_sum(const double* __restrict__ partials, const int* __restrict__ counts, int n_acc,
+CSF_DEV bool group_sum(const double* __restrict__ partials, const int* __restrict__ counts, int n_acc,
                        double* __restrict__ gpartials, int* __restrict__ gcounts, unsigned* __restrict__ group_ctr) {
   __shared__ bool s_last;
   __threadfence();
@@ -77,7 +77,7 @@ CSF_DEV void group_sum(const double* __restrict__ partials, const int* __restric
   const int gn = min(kGroup, static_cast<int>(gridDim.x) - first);
   if (threadIdx.x == 0) s_last = atomicAdd(group_ctr + grp, 1u) == static_cast<unsigned>(gn - 1);
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last) return false;
   if (threadIdx.x == 0) group_ctr[grp] = 0u;  // ready for the next launch
   __threadfence();
   for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
@@ -97,6 +97,7 @@ CSF_DEV void group_sum(const double* __restrict__ partials, const int* __restric
     for (int off = 16; off > 0; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
     if (threadIdx.x == 0) gcounts[grp] = c;
   }
+  return true;
 }
 
 // The solve of one ICP iteration (one CTA): group totals in group order, then
@@ -108,12 +109,9 @@ CSF_DEV void group_sum(const double* __restrict__ partials, const int* __restric
 // instead.  Then exp(delta) * T per channel thread (L<1>) and the break
 // decisions (icp.cpp:199,235) into TrackState.
 constexpr int kMaxC = 1 + 64;  // CSF_MAX_DIRECTIONS
-__global__ void __launch_bounds__(kRedThreads) k_icp_solve_t(TrackState* st, const double* __restrict__ gpartials,
-                                                          const int* __restrict__ gcounts, int n_groups,
-                                                          double* pose, int Dp, int level, double tol) {
-  pdl_wait();
-  pdl_trigger();
-  if (st->level_done) return;
+__device__ __noinline__ void icp_solve_body(TrackState* st, const double* __restrict__ gpartials,
+                                            const int* __restrict__ gcounts, int n_groups, double* pose, int Dp,
+                                            int level, double tol) {
   __shared__ double s_acc[27 * kMaxC];
   __shared__ double s_m[36], s_x[6];
   __shared__ int s_tr[6];
@@ -268,6 +266,15 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_solve_t(TrackState* st, con
   if (threadIdx.x == 0 && g_icp_clock) atomicAdd(&g_icp_clock_launch, 1u);
 }
 
+__global__ void __launch_bounds__(kRedThreads) k_icp_solve_t(TrackState* st, const double* __restrict__ gpartials,
+                                                          const int* __restrict__ gcounts, int n_groups,
+                                                          double* pose, int Dp, int level, double tol) {
+  pdl_wait();
+  pdl_trigger();
+  if (st->level_done) return;
+  icp_solve_body(st, gpartials, gcounts, n_groups, pose, Dp, level, tol);
+}
+
 template <int G>
 __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
                                                     int w, int h, int stride, const double* __restrict__ intr,
@@ -276,7 +283,9 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
                                                     const double* __restrict__ nim, double d_max, double cos_max,
                                                     int Dp, int chunk, double* __restrict__ partials,
                                                     int* __restrict__ counts, double* __restrict__ gpartials,
-                                                    int* __restrict__ gcounts, unsigned* __restrict__ group_ctr) {
+                                                    int* __restrict__ gcounts, unsigned* __restrict__ group_ctr,
+                                                    TrackState* st_rw, double* pose_rw, int level, double tol,
+                                                    int fused) {
   pdl_wait();
   pdl_trigger();
   if (st->level_done) return;
@@ -445,7 +454,19 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
   }
   if (threadIdx.x == 0) counts[blockIdx.x] = tile_count;
   clock_mark(2);
-  group_sum(partials, counts, n_acc, gpartials, gcounts, group_ctr);
+  const bool grouped = group_sum(partials, counts, n_acc, gpartials, gcounts, group_ctr);
+  if (!fused || !grouped) return;
+  // the CTA completing the last group runs the solve (no second launch)
+  __shared__ bool s_solve;
+  const int n_groups = (gridDim.x + kGroup - 1) / kGroup;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_solve = atomicAdd(group_ctr + kMaxGroupCtr - 1, 1u) == static_cast<unsigned>(n_groups - 1);
+  __syncthreads();
+  if (!s_solve) return;
+  if (threadIdx.x == 0) group_ctr[kMaxGroupCtr - 1] = 0u;
+  __threadfence();
+  icp_solve_body(st_rw, gpartials, gcounts, n_groups, pose_rw, Dp, level, tol);
 }
 
 // Level entry: the prediction pose is the current estimate (icp.cpp:191).
@@ -970,7 +991,11 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
   const size_t smem = sizeof(double) * (16 * C + static_cast<size_t>(chunk) * 7 * C);
   const int tiles = icp_tiles(w, h, stride);
   const int groups = (tiles + kGroup - 1) / kGroup;
-  if (groups > kMaxGroupCtr || Dp > kMaxC - 1) {
+  // the solve is its own (PDL) launch; CSF_ICP_FUSED=1 runs it in the CTA
+  // completing the last group instead (measured slower on B200: the solve
+  // then shares the big kernel's cold instruction stream)
+  static const bool fused = std::getenv("CSF_ICP_FUSED") != nullptr;
+  if (groups > kMaxGroupCtr - 1 || Dp > kMaxC - 1) {
     std::fprintf(stderr, "csf_b200: ICP frame too large (%d tiles) or too many channels (%d)\n", tiles, Dp);
     return;
   }
@@ -986,23 +1011,29 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       launch_pdl(k_icp_reduce<0>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
-                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
+                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
+                 pose, level, tol, fused ? 1 : 0);
       break;
     case 1:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       launch_pdl(k_icp_reduce<1>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
-                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
+                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
+                 pose, level, tol, fused ? 1 : 0);
       break;
     default:
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_icp_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       launch_pdl(k_icp_reduce<2>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
-                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
+                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
+                 pose, level, tol, fused ? 1 : 0);
   }
-  launch_pdl(k_icp_solve_t, dim3(1), dim3(kRedThreads), 0, L.stream, st, static_cast<const double*>(gpartials),
-             static_cast<const int*>(gcounts), groups, pose, Dp, level, tol);
-  *L.launches += 2;
+  if (!fused) {
+    launch_pdl(k_icp_solve_t, dim3(1), dim3(kRedThreads), 0, L.stream, st, static_cast<const double*>(gpartials),
+               static_cast<const int*>(gcounts), groups, pose, Dp, level, tol);
+    ++*L.launches;
+  }
+  *L.launches += 1;
   chk("icp_reduce");
 }
 
