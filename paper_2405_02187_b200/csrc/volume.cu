@@ -290,8 +290,12 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
   }
 }
 
+// resident CTAs per SM the fusion kernel is compiled for (register budget)
+#ifndef CSF_INT_MINB
+#define CSF_INT_MINB 2
+#endif
 template <typename S, int NDP = 0>
-__global__ void __launch_bounds__(256, 2) k_integrate_hashed(HashView vol, const int* __restrict__ coords,
+__global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView vol, const int* __restrict__ coords,
                                                           const int* __restrict__ visible,
                                                           const int* __restrict__ counters,
                                                           const double* __restrict__ depth, int w, int h,

@@ -9,8 +9,8 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-CATS = {"k_icp_reduce": "icp", "k_raycast_march": "raycast", "k_raycast_lift_coop": "raycast_lift",
-        "k_integrate_hashed": "integrate"}
+CATS = {"k_icp_reduce": "icp", "k_icp_solve_t": "icp_solve", "k_raycast_march": "raycast",
+        "k_raycast_march_seg": "raycast_seg", "k_raycast_lift_coop": "raycast_lift", "k_integrate_hashed": "integrate"}
 KEEP = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "dram__throughput",
         "sm__throughput", "launch__registers_per_thread", "sm__warps_active", "launch__occupancy_limit",
         "smsp__inst_executed", "sm__inst_executed_pipe_fp64", "l1tex__t_bytes", "lts__t_bytes", "launch__grid_size",
