@@ -189,6 +189,19 @@ int csf_volume_block_count(csf_volume vol, int* n_blocks);
 /* heads [2^bits], keys [n_blocks], next [n_blocks], coords [n_blocks][3] */
 int csf_volume_download_hash(csf_volume vol, int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords);
 
+/* tsdf.cpp:61-153 — save_volume / load_volume in the reference's "CSFVOL 1"
+ * container: text header (dims, voxel_size, origin, mu, weight_cap, channels)
+ * then float32 planes (field, weight, derivative channels only when any is
+ * non-zero).  A dense single-channel file is byte-compatible with the
+ * reference.  Extensions (builder-defined): D derivative planes for D
+ * channels; hashed volumes add "hashed <bucket_bits> <max_blocks>" and
+ * "blocks N" and an int32 N x 3 block-coordinate plane (pool order) before
+ * the voxel planes (block-major); loading rebuilds the canonical hash table.
+ * load: n_channels = -1 takes the file's channel count.  I/O errors map to
+ * CSF_ERUNTIME (std::runtime_error). */
+int csf_volume_save(csf_volume vol, const char* path);
+int csf_volume_load(csf_ctx ctx, const char* path, int n_channels, csf_volume* out);
+
 /* tsdf.cpp:11-40 — fuse one unperturbed depth frame at a lifted camera pose
  * with lifted intrinsics.  Hashed volumes first allocate the frame's
  * truncation-band blocks; *n_visible (optional) receives the visible count. */

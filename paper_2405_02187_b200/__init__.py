@@ -33,7 +33,7 @@ __all__ = [
     "InvalidArgument", "DomainError", "Context", "bilateral_filter", "downsample_depth", "build_depth_pyramid",
     "measure_surface", "TsdfVolume", "HashedVolume", "surface_update", "raycast", "track_frame", "TrackResult",
     "icp_energy", "icp_loss", "icp_gradient", "icp_hessian", "icp_energy_derivs",
-    "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "look_at", "config5_views", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
+    "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "look_at", "config5_views", "save_volume", "load_volume", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
     "lift_pose", "lift_intrinsics", "library",
 ]
 
@@ -306,6 +306,10 @@ class _Volume:
         wt = _f64(weight)
         self.ctx.check(self.ctx.lib.csf_volume_upload(self.h, _dp(f), _dp(wt)))
 
+    def save(self, path) -> None:
+        """save_volume (tsdf.cpp:61-97): the "CSFVOL 1" checkpoint."""
+        self.ctx.check(self.ctx.lib.csf_volume_save(self.h, str(path).encode()))
+
 
 class TsdfVolume(_Volume):
     """Dense lattice volume (tsdf.hpp:38-78), F carries `channels` perturbation channels."""
@@ -396,6 +400,39 @@ def config5_views(n: int = 256, seed: int = 4) -> np.ndarray:
         target = np.array([rng.uniform(-1.6, 1.6), rng.uniform(-1.6, 1.6), rng.uniform(0.3, 2.5)])
         out[i] = look_at(eye, target)
     return out
+
+
+def save_volume(path, volume: _Volume) -> None:
+    """tsdf.hpp:288 save_volume(path, volume)."""
+    volume.save(path)
+
+
+def load_volume(path, channels: int = -1, ctx: Optional[Context] = None) -> _Volume:
+    """tsdf.hpp:289 load_volume(path): a dense TsdfVolume (or, for the hashed
+    extension of the format, a HashedVolume) on the device; channels = -1 keeps
+    the file's derivative channels.  Errors: RuntimeError (std::runtime_error)."""
+    c = _ctx(ctx)
+    h = C.c_void_p()
+    c.check(c.lib.csf_volume_load(c.h, str(path).encode(), channels, C.byref(h)))
+    with open(path, "rb") as f:
+        head = f.read(4096).split(b"\ndata\n", 1)[0].decode(errors="replace").splitlines()
+    fields = {ln.split()[0]: ln.split()[1:] for ln in head[1:] if ln.strip()}
+    n_im = fields.get("channels", []).count("derivative")
+    ch = channels if channels >= 0 else n_im
+    vs, org = float(fields["voxel_size"][0]), tuple(float(x) for x in fields["origin"])
+    mu, cap = float(fields["mu"][0]), float(fields["weight_cap"][0])
+    if "hashed" in fields:
+        vol = HashedVolume.__new__(HashedVolume)
+        _Volume.__init__(vol, c, ch)
+        bits, mb = int(fields["hashed"][0]), int(fields["hashed"][1])
+        vol.params = _capi.HashParams(vs, (C.c_double * 3)(*org), mu, cap, bits, mb)
+    else:
+        vol = TsdfVolume.__new__(TsdfVolume)
+        _Volume.__init__(vol, c, ch)
+        dims = tuple(int(x) for x in fields["dims"])
+        vol.params = _capi.VolumeParams((C.c_int * 3)(*dims), vs, (C.c_double * 3)(*org), mu, cap)
+    vol.h = h
+    return vol
 
 
 def surface_update(volume: _Volume, depth, camera_to_world, k) -> int:

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <sstream>
+#include <fstream>
 #include <vector>
 
 #include "../../include/csf_b200.h"
@@ -1067,6 +1069,211 @@ extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const d
 // ---------------------------------------------------------------------------
 // track_frame (real tracker on the device)
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// checkpoints: the reference's "CSFVOL 1" container (tsdf.cpp:61-153)
+// ---------------------------------------------------------------------------
+namespace csfi {
+void launch_rebuild_index(cudaStream_t stream, const int* coords, int n_blocks, int* grid, unsigned* occ, int gbits);
+}
+
+namespace {
+// host copies of block_key / block_hash (geometry.cuh)
+uint64_t host_block_key(int bx, int by, int bz) {
+  constexpr int kBias = 1 << 20;
+  return (static_cast<uint64_t>(static_cast<uint32_t>(bx + kBias)) << 42) |
+         (static_cast<uint64_t>(static_cast<uint32_t>(by + kBias)) << 21) |
+         static_cast<uint64_t>(static_cast<uint32_t>(bz + kBias));
+}
+uint32_t host_block_hash(int bx, int by, int bz, int bits) {
+  return ((static_cast<uint32_t>(bx) * 73856093u) ^ (static_cast<uint32_t>(by) * 19349669u) ^
+          (static_cast<uint32_t>(bz) * 83492791u)) &
+         ((1u << bits) - 1u);
+}
+void write_plane(std::ofstream& out, const std::vector<float>& plane) {
+  out.write(reinterpret_cast<const char*>(plane.data()), static_cast<std::streamsize>(plane.size() * sizeof(float)));
+}
+bool read_plane(std::ifstream& in, std::vector<float>& plane) {
+  in.read(reinterpret_cast<char*>(plane.data()), static_cast<std::streamsize>(plane.size() * sizeof(float)));
+  return static_cast<size_t>(in.gcount()) == plane.size() * sizeof(float);
+}
+}  // namespace
+
+extern "C" int csf_volume_save(csf_volume v, const char* path) {
+  if (!v || !path) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  if (v->order != 1) return fail(ctx, CSF_EINVAL, "csf_volume_save: second-order volumes are not checkpointed");
+  cudaSetDevice(ctx->device);
+  const long long n = volume_voxels_now(v);
+  const int D = v->D, C = 1 + D;
+  std::vector<double> field(static_cast<size_t>(n) * C), weight(n);
+  int rc = n > 0 ? csf_volume_download(v, field.data(), weight.data()) : CSF_OK;
+  if (rc) return rc;
+  std::vector<int32_t> coords;
+  if (v->hashed) {
+    coords.resize(static_cast<size_t>(n / 512) * 3);
+    if (!coords.empty())
+      CUDA_TRY(ctx, cudaMemcpy(coords.data(), v->hash.coords, sizeof(int32_t) * coords.size(), cudaMemcpyDeviceToHost));
+  }
+  bool any_im = false;
+  for (long long i = 0; i < n && !any_im; ++i)
+    for (int d = 0; d < D; ++d)
+      if (field[i * C + 1 + d] != 0.0) {
+        any_im = true;
+        break;
+      }
+  std::ofstream out(path, std::ios::binary);
+  if (!out) return fail(ctx, CSF_ERUNTIME, std::string("cannot write volume: ") + path);
+  out.precision(17);
+  out << "CSFVOL 1\n";
+  if (v->hashed) {
+    const HashDev& hd = v->hash;
+    out << "hashed " << hd.bits << " " << hd.max_blocks << "\n";
+    out << "voxel_size " << hd.vs << "\n";
+    out << "origin " << hd.ox << " " << hd.oy << " " << hd.oz << "\n";
+    out << "mu " << hd.mu << "\n";
+    out << "weight_cap " << hd.cap << "\n";
+    out << "blocks " << n / 512 << "\n";
+  } else {
+    const DenseDev& dd = v->dense;
+    out << "dims " << dd.nx << " " << dd.ny << " " << dd.nz << "\n";
+    out << "voxel_size " << dd.vs << "\n";
+    out << "origin " << dd.ox << " " << dd.oy << " " << dd.oz << "\n";
+    out << "mu " << dd.mu << "\n";
+    out << "weight_cap " << dd.cap << "\n";
+  }
+  out << "channels field weight";
+  if (any_im)
+    for (int d = 0; d < D; ++d) out << " derivative";
+  out << "\n";
+  out << "data\n";
+  if (v->hashed && !coords.empty())
+    out.write(reinterpret_cast<const char*>(coords.data()), static_cast<std::streamsize>(coords.size() * 4));
+  std::vector<float> plane(n);
+  for (long long i = 0; i < n; ++i) plane[i] = static_cast<float>(field[i * C]);
+  write_plane(out, plane);
+  for (long long i = 0; i < n; ++i) plane[i] = static_cast<float>(weight[i]);
+  write_plane(out, plane);
+  if (any_im)
+    for (int d = 0; d < D; ++d) {
+      for (long long i = 0; i < n; ++i) plane[i] = static_cast<float>(field[i * C + 1 + d]);
+      write_plane(out, plane);
+    }
+  if (!out) return fail(ctx, CSF_ERUNTIME, std::string("short write: ") + path);
+  return CSF_OK;
+}
+
+extern "C" int csf_volume_load(csf_ctx ctx, const char* path, int n_channels, csf_volume* out_vol) {
+  if (!ctx || !path || !out_vol) return CSF_EINVAL;
+  *out_vol = nullptr;
+  std::ifstream in(path, std::ios::binary);
+  if (!in) return fail(ctx, CSF_ERUNTIME, std::string("cannot open volume: ") + path);
+  std::string line;
+  if (!std::getline(in, line) || line != "CSFVOL 1")
+    return fail(ctx, CSF_ERUNTIME, std::string("not a volume checkpoint: ") + path);
+  csf_volume_params vp{};
+  csf_hash_params hp{};
+  bool hashed = false, saw_data = false;
+  int n_im = 0;
+  long long n_blocks = -1;
+  while (std::getline(in, line)) {
+    std::istringstream ls(line);
+    std::string key;
+    ls >> key;
+    if (key == "data") {
+      saw_data = true;
+      break;
+    } else if (key == "dims") {
+      ls >> vp.dims[0] >> vp.dims[1] >> vp.dims[2];
+    } else if (key == "hashed") {
+      hashed = true;
+      ls >> hp.bucket_bits >> hp.max_blocks;
+    } else if (key == "blocks") {
+      ls >> n_blocks;
+    } else if (key == "voxel_size") {
+      ls >> vp.voxel_size;
+    } else if (key == "origin") {
+      ls >> vp.origin[0] >> vp.origin[1] >> vp.origin[2];
+    } else if (key == "mu") {
+      ls >> vp.mu;
+    } else if (key == "weight_cap") {
+      ls >> vp.weight_cap;
+    } else if (key == "channels") {
+      std::string tok;
+      while (ls >> tok) n_im += tok == "derivative";
+    } else {
+      return fail(ctx, CSF_ERUNTIME, "unknown checkpoint field '" + key + "': " + path);
+    }
+  }
+  if (!saw_data || !(vp.voxel_size > 0.0) ||
+      (hashed ? (n_blocks < 0 || hp.max_blocks < n_blocks) : (vp.dims[0] <= 0 || vp.dims[1] <= 0 || vp.dims[2] <= 0)))
+    return fail(ctx, CSF_ERUNTIME, std::string("malformed volume checkpoint: ") + path);
+  const int D = n_channels >= 0 ? n_channels : n_im;
+  if (n_im != 0 && n_im != D)
+    return fail(ctx, CSF_EINVAL, "csf_volume_load: the checkpoint carries " + std::to_string(n_im) + " channels");
+  csf_volume v = nullptr;
+  int rc;
+  std::vector<int32_t> coords;
+  if (hashed) {
+    hp.voxel_size = vp.voxel_size;
+    for (int a = 0; a < 3; ++a) hp.origin[a] = vp.origin[a];
+    hp.mu = vp.mu;
+    hp.weight_cap = vp.weight_cap;
+    coords.resize(static_cast<size_t>(n_blocks) * 3);
+    in.read(reinterpret_cast<char*>(coords.data()), static_cast<std::streamsize>(coords.size() * 4));
+    if (static_cast<size_t>(in.gcount()) != coords.size() * 4)
+      return fail(ctx, CSF_ERUNTIME, std::string("volume checkpoint truncated: ") + path);
+    rc = csf_volume_create_hashed(ctx, &hp, D, &v);
+  } else {
+    rc = csf_volume_create_dense(ctx, &vp, D, &v);
+  }
+  if (rc) return rc;
+  const long long n = hashed ? n_blocks * 512 : static_cast<long long>(vp.dims[0]) * vp.dims[1] * vp.dims[2];
+  std::vector<float> fpl(n), wpl(n);
+  bool ok = read_plane(in, fpl) && read_plane(in, wpl);
+  std::vector<std::vector<float>> ims(n_im, std::vector<float>(n));
+  for (int d = 0; d < n_im && ok; ++d) ok = read_plane(in, ims[d]);
+  if (!ok) {
+    csf_volume_destroy(v);
+    return fail(ctx, CSF_ERUNTIME, std::string("volume checkpoint truncated: ") + path);
+  }
+  if (hashed && n_blocks > 0) {
+    // the canonical hash structure: chains sorted by key, pool ids = file order
+    const int bits = hp.bucket_bits;
+    std::vector<int32_t> heads(size_t(1) << bits, -1), next(n_blocks, -1);
+    std::vector<uint64_t> keys(n_blocks);
+    for (long long b = 0; b < n_blocks; ++b) {
+      const int bx = coords[3 * b], by = coords[3 * b + 1], bz = coords[3 * b + 2];
+      keys[b] = host_block_key(bx, by, bz);
+      int32_t* link = &heads[host_block_hash(bx, by, bz, bits)];
+      while (*link >= 0 && keys[*link] < keys[b]) link = &next[*link];
+      next[b] = *link;
+      *link = static_cast<int32_t>(b);
+    }
+    const int nb = static_cast<int>(n_blocks);
+    CUDA_TRY(ctx, cudaMemcpy(v->hash.heads, heads.data(), sizeof(int32_t) * heads.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(v->hash.next, next.data(), sizeof(int32_t) * n_blocks, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(v->hash.keys, keys.data(), sizeof(uint64_t) * n_blocks, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(v->hash.coords, coords.data(), sizeof(int32_t) * coords.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(v->hash.n_blocks, &nb, sizeof(int), cudaMemcpyHostToDevice));
+    launch_rebuild_index(ctx->stream, v->hash.coords, nb, v->hash.grid, v->hash.occ, v->hash.gbits);
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  const int C = 1 + D;
+  std::vector<double> field(static_cast<size_t>(n) * C, 0.0), weight(n);
+  for (long long i = 0; i < n; ++i) {
+    field[i * C] = static_cast<double>(fpl[i]);
+    weight[i] = static_cast<double>(wpl[i]);
+    for (int d = 0; d < n_im; ++d) field[i * C + 1 + d] = static_cast<double>(ims[d][i]);
+  }
+  rc = n > 0 ? csf_volume_upload(v, field.data(), weight.data()) : CSF_OK;
+  if (rc) {
+    csf_volume_destroy(v);
+    return rc;
+  }
+  *out_vol = v;
+  return CSF_OK;
+}
+
 // ---------------------------------------------------------------------------
 // BASELINE config 5: view scoring (views.cu; builder-defined objective)
 // ---------------------------------------------------------------------------

@@ -1628,6 +1628,27 @@ void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, c
   chk("integrate_hashed");
 }
 
+// Derived lookup indices of a hashed volume whose table was loaded from a
+// checkpoint: the block-id window grid and the super-block occupancy bits.
+__global__ void k_rebuild_index(const int* __restrict__ coords, int n_blocks, int* grid, unsigned* occ, int gbits) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_blocks) return;
+  const int half = 1 << (gbits - 1);
+  const unsigned ux = static_cast<unsigned>(coords[3 * b] + half), uy = static_cast<unsigned>(coords[3 * b + 1] + half),
+                 uz = static_cast<unsigned>(coords[3 * b + 2] + half);
+  const unsigned side = 1u << gbits;
+  if (ux < side && uy < side && uz < side) {
+    grid[(static_cast<size_t>(uz) << gbits | uy) << gbits | ux] = b;
+    const int sb = gbits - 3;
+    const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
+    atomicOr(occ + (bit >> 5), 1u << (bit & 31));
+  }
+}
+
+void launch_rebuild_index(cudaStream_t stream, const int* coords, int n_blocks, int* grid, unsigned* occ, int gbits) {
+  if (n_blocks > 0) k_rebuild_index<<<(n_blocks + 255) / 256, 256, 0, stream>>>(coords, n_blocks, grid, occ, gbits);
+}
+
 void march_stats_enable(unsigned long long* buf) { cudaMemcpyToSymbol(g_march_stats, &buf, sizeof(buf)); }
 
 int band_samples(double mu, double vs) {
