@@ -221,6 +221,22 @@ int csf_raycast(csf_volume vol, const double* pose, const double* intr, int w, i
 int csf_track_frame(csf_volume vol, const double* depth, int w, int h, const double* init_pose,
                     const csf_intrinsics* k, const csf_icp_cfg* cfg, double* out_pose, csf_track_result* result);
 
+/* icp.cpp:89-126 — associate(measured, predicted, pose, prediction_pose, k,
+ * cfg, stride): maps [h][w][3] (vertices camera / world, normals), poses
+ * camera->world [12]; corrs [<= slots][9] in scan order, *n_corrs. */
+int csf_associate(csf_ctx ctx, const double* measured_vertices, const double* measured_normals,
+                  const double* predicted_vertices, const double* predicted_normals, int w, int h,
+                  const double* camera_to_world, const double* predicted_camera_to_world, const csf_intrinsics* k,
+                  const csf_icp_cfg* cfg, int pixel_stride, double* corrs, int* n_corrs);
+/* icp.cpp:146-153 — linearized_step(corrs, base): the normal equations in
+ * the canonical tiled order, LDLT solve of A d = -b, zero
+ * when not finite. */
+int csf_linearized_step(csf_ctx ctx, const double* corrs, int n, const double* base, double* delta);
+/* diff.hpp:16-37 — pairwise_sum of n terms with `channels` lanes each
+ * (terms [n][channels], e.g. a lifted value): the reference's fixed tree per
+ * lane, init 0. */
+int csf_pairwise_sum(csf_ctx ctx, const double* terms, int n, int channels, double* out);
+
 /* icp.hpp:70-91 — icp_energy(corrs, xi, base) with the pairwise_sum tree
  * (diff.hpp:16-37); gradient (optional) = the 6 Complex passes of
  * icp_gradient, hessian (optional, [36] row-major) = the 21 Bicomplex passes

@@ -44,6 +44,9 @@ def lib() -> C.CDLL:
                                      dp, C.POINTER(_capi.TrackResult)]),
             "orc_workload": (ip, [ip, ip, ip, ip, fp, dp, C.POINTER(_capi.Intrinsics)]),
             "orc_pipeline_run": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, i32p, dp]),
+            "orc_associate": (ip, [dp, dp, dp, dp, ip, ip, dp, dp, C.POINTER(_capi.Intrinsics), C.POINTER(_capi.IcpCfg),
+                                   ip, dp, C.POINTER(C.c_int)]),
+            "orc_linearized_step": (ip, [dp, ip, dp, ip, dp]),
             "orc_view_scores": (ip, [vp, dp, ip, C.POINTER(_capi.Intrinsics), C.c_double, C.c_double, C.c_double,
                                      dp, dp]),
             "orc_icp_energy_derivs": (ip, [dp, ip, dp, dp, C.c_double, dp, dp, dp]),
@@ -234,3 +237,36 @@ def icp_energy_derivs(corrs, base12, xi=None, h=1e-8):
     _check(lib().orc_icp_energy_derivs(_dp(c) if c.size else None, c.shape[0], _dp(b), _dp(x) if x is not None else None,
                                        h, C.byref(E), _dp(g), _dp(H)))
     return E.value, g, H
+
+
+def associate(mv, mn, pv, pn, c2w, pc2w, k, cfg, stride=1):
+    mv, mn, pv, pn = (np.ascontiguousarray(a, dtype=np.float64) for a in (mv, mn, pv, pn))
+    h, w = mv.shape[:2]
+    out = np.empty((w * h, 9))
+    n = C.c_int()
+    _check(lib().orc_associate(_dp(mv), _dp(mn), _dp(pv), _dp(pn), w, h, _dp(np.ascontiguousarray(c2w, dtype=float)),
+                               _dp(np.ascontiguousarray(pc2w, dtype=float)), C.byref(k), C.byref(cfg), stride, _dp(out),
+                               C.byref(n)))
+    return out[: n.value].copy()
+
+
+def linearized_step(corrs, base12, sequential=False):
+    c = np.ascontiguousarray(corrs, dtype=np.float64).reshape(-1, 9)
+    d = np.empty(6)
+    _check(lib().orc_linearized_step(_dp(c) if c.size else None, c.shape[0],
+                                     _dp(np.ascontiguousarray(base12, dtype=np.float64)), int(sequential), _dp(d)))
+    return d
+
+
+def pairwise_sum(terms):
+    """diff.hpp:16-37 restated in Python (test reference for the device tree)."""
+    def block(x):
+        if len(x) <= 8:
+            acc = x[0]
+            for v in x[1:]:
+                acc = acc + v
+            return acc
+        half = len(x) // 2
+        return block(x[:half]) + block(x[half:])
+    t = [float(v) for v in terms]
+    return 0.0 if not t else 0.0 + block(t)

@@ -408,6 +408,63 @@ int orc_view_scores(void* v, const double* poses, int n, const csf_intrinsics* k
   return guard([&] { static_cast<VolBase*>(v)->view_scores(poses, n, to_intr(*k), w0, beta, h, scores, grads); });
 }
 
+// associate (icp.cpp:89-126) over maps [h][w][3]; corrs [n][9]
+int orc_associate(const double* mv, const double* mn, const double* pv, const double* pn, int w, int h,
+                  const double* c2w, const double* pc2w, const csf_intrinsics* k, const csf_icp_cfg* cfg, int stride,
+                  double* corrs, int* n) {
+  return guard([&] {
+    SurfaceMaps<double> meas, pred;
+    meas.vertices = Image<Vec3d>(w, h, Vec3d());
+    meas.normals = Image<Vec3d>(w, h, Vec3d());
+    pred.vertices = Image<Vec3d>(w, h, Vec3d());
+    pred.normals = Image<Vec3d>(w, h, Vec3d());
+    for (int i = 0; i < w * h; ++i) {
+      meas.vertices.data[i] = Vec3d(mv[3 * i], mv[3 * i + 1], mv[3 * i + 2]);
+      meas.normals.data[i] = Vec3d(mn[3 * i], mn[3 * i + 1], mn[3 * i + 2]);
+      pred.vertices.data[i] = Vec3d(pv[3 * i], pv[3 * i + 1], pv[3 * i + 2]);
+      pred.normals.data[i] = Vec3d(pn[3 * i], pn[3 * i + 1], pn[3 * i + 2]);
+    }
+    Pose a, b;
+    for (int e = 0; e < 9; ++e) {
+      a.rotation(e / 3, e % 3) = c2w[e];
+      b.rotation(e / 3, e % 3) = pc2w[e];
+    }
+    for (int e = 0; e < 3; ++e) {
+      a.translation[e] = c2w[9 + e];
+      b.translation[e] = pc2w[9 + e];
+    }
+    Intrinsics kk = to_intr(*k);
+    kk.width = w;
+    kk.height = h;
+    const auto cs = associate(meas, pred, a, b, kk, to_icp(*cfg), stride);
+    for (std::size_t i = 0; i < cs.size(); ++i)
+      for (int c = 0; c < 3; ++c) {
+        corrs[9 * i + c] = cs[i].vertex[c];
+        corrs[9 * i + 3 + c] = cs[i].model_vertex[c];
+        corrs[9 * i + 6 + c] = cs[i].model_normal[c];
+      }
+    *n = static_cast<int>(cs.size());
+  });
+}
+
+// linearized_step (icp.cpp:146-153), canonical tiled or literal sequential order
+int orc_linearized_step(const double* corrs, int n, const double* base, int sequential, double* delta) {
+  return guard([&] {
+    std::vector<Correspondence> cs(n);
+    for (int i = 0; i < n; ++i) {
+      const double* c = corrs + 9 * i;
+      cs[i].vertex = Vec3d(c[0], c[1], c[2]);
+      cs[i].model_vertex = Vec3d(c[3], c[4], c[5]);
+      cs[i].model_normal = Vec3d(c[6], c[7], c[8]);
+    }
+    Pose b;
+    for (int e = 0; e < 9; ++e) b.rotation(e / 3, e % 3) = base[e];
+    for (int e = 0; e < 3; ++e) b.translation[e] = base[9 + e];
+    const Vec6<double> d = linearized_step(cs, b, sequential != 0);
+    for (int i = 0; i < 6; ++i) delta[i] = d[i];
+  });
+}
+
 // icp_energy / icp_gradient / icp_hessian (icp.hpp:70-91) at xi (NULL = 0).
 int orc_icp_energy_derivs(const double* corrs, int n, const double* base, const double* xi, double h, double* E,
                           double* g, double* H) {

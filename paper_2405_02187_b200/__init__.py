@@ -32,7 +32,8 @@ from . import capi as _capi
 __all__ = [
     "InvalidArgument", "DomainError", "Context", "bilateral_filter", "downsample_depth", "build_depth_pyramid",
     "measure_surface", "TsdfVolume", "HashedVolume", "surface_update", "raycast", "track_frame", "TrackResult",
-    "icp_energy", "icp_loss", "icp_gradient", "icp_hessian", "icp_energy_derivs",
+    "icp_energy", "icp_loss", "icp_gradient", "icp_hessian", "icp_energy_derivs", "associate", "linearized_step",
+    "pairwise_sum", "complex_depth", "perturb_depth",
     "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "look_at", "config5_views", "save_volume", "load_volume", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
     "lift_pose", "lift_intrinsics", "library",
 ]
@@ -468,6 +469,81 @@ def track_frame(volume: _Volume, depth, init_camera_to_world, k, cfg: Optional[_
     ctx.check(ctx.lib.csf_track_frame(volume.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg), _dp(out),
                                       C.byref(res)))
     return TrackResult(out, res.iterations, bool(res.converged), res.final_loss, res.correspondences)
+
+
+# ----------------------------------------------------------------------------- icp: associate / linearized step
+def associate(measured, predicted, camera_to_world, predicted_camera_to_world, k, cfg=None, pixel_stride: int = 1,
+              ctx: Optional[Context] = None) -> np.ndarray:
+    """icp.cpp:89-126: correspondences (n, 9) in scan order from measured (V camera, N) and
+    predicted (V, N world) maps of shape (h, w, 3) each."""
+    c = _ctx(ctx)
+    mv, mn = (_f64(a)[..., :3] if _f64(a).ndim == 3 else _f64(a)[..., :, 0] for a in measured)
+    pv, pn = (_f64(a)[..., :3] if _f64(a).ndim == 3 else _f64(a)[..., :, 0] for a in predicted)
+    mv, mn, pv, pn = (np.ascontiguousarray(a) for a in (mv, mn, pv, pn))
+    h, w = mv.shape[:2]
+    cw = lift_pose(camera_to_world, 0)[:, 0].copy()
+    pw = lift_pose(predicted_camera_to_world, 0)[:, 0].copy()
+    cfg = cfg if cfg is not None else default_icp_cfg()
+    stride = max(1, pixel_stride)
+    out = np.empty((((w + stride - 1) // stride) * ((h + stride - 1) // stride), 9))
+    n = C.c_int()
+    c.check(c.lib.csf_associate(c.h, _dp(mv), _dp(mn), _dp(pv), _dp(pn), w, h, _dp(cw), _dp(pw), C.byref(k),
+                                C.byref(cfg), stride, _dp(out), C.byref(n)))
+    return out[: n.value].copy()
+
+
+def linearized_step(corrs, base, ctx: Optional[Context] = None) -> np.ndarray:
+    """icp.cpp:146-153: the small-angle Gauss-Newton step (canonical tiled normal equations)."""
+    c = _ctx(ctx)
+    cc = _corrs(corrs)
+    b = lift_pose(base, 0)[:, 0].copy()
+    d = np.empty(6)
+    c.check(c.lib.csf_linearized_step(c.h, _dp(cc) if cc.size else None, cc.shape[0], _dp(b), _dp(d)))
+    return d
+
+
+def pairwise_sum(terms, ctx: Optional[Context] = None):
+    """diff.hpp:16-37: the reference's fixed summation tree (per lane of (n, C) terms)."""
+    c = _ctx(ctx)
+    t = _f64(terms)
+    scalar = t.ndim == 1
+    t = np.ascontiguousarray(t.reshape(-1, 1) if scalar else t.reshape(t.shape[0], int(np.prod(t.shape[1:]))))
+    out = np.empty(t.shape[1])
+    c.check(c.lib.csf_pairwise_sum(c.h, _dp(t) if t.size else None, t.shape[0], t.shape[1], _dp(out)))
+    return float(out[0]) if scalar else out
+
+
+# ----------------------------------------------------------------------------- frames: depth lifts
+def complex_depth(depth) -> np.ndarray:
+    """frames.cpp:77-81: depth lifted with a zero channel, shape (h, w, 2)."""
+    d = _f64(depth)
+    out = np.zeros(d.shape + (2,))
+    out[..., 0] = d
+    return out
+
+
+def perturb_depth(depth, x: int, y: int, h: float = 1e-8, delta_edge: float = 0.1) -> np.ndarray:
+    """frames.cpp:83-102: seed pixel (x, y) with im = h; refuses (InvalidArgument) out-of-bounds
+    pixels, pixels without depth and pixels on a depth discontinuity (an in-bounds 4-neighbour
+    invalid or more than delta_edge away)."""
+    if not (0.0 < h <= 1e-6):
+        raise InvalidArgument("StepSize: step must satisfy 0 < h <= 1e-6")
+    d = _f64(depth)
+    H, W = d.shape
+    if not (0 <= x < W and 0 <= y < H):
+        raise InvalidArgument("perturb_depth: pixel out of bounds")
+    center = d[y, x]
+    if not center > 0.0:
+        raise InvalidArgument("perturb_depth: pixel has no depth")
+    for nx, ny in ((x - 1, y), (x + 1, y), (x, y - 1), (x, y + 1)):
+        if not (0 <= nx < W and 0 <= ny < H):
+            continue
+        v = d[ny, nx]
+        if not v > 0.0 or abs(v - center) > delta_edge:
+            raise InvalidArgument("perturb_depth: pixel sits on a depth discontinuity")
+    out = complex_depth(d)
+    out[y, x, 1] = h
+    return out
 
 
 # ----------------------------------------------------------------------------- icp energy

@@ -1358,6 +1358,90 @@ extern "C" int csf_icp_energy_derivs(csf_ctx ctx, const double* corrs, int n, co
 }
 
 // ---------------------------------------------------------------------------
+// associate / linearized_step / pairwise_sum (icp.cpp:89-126, 146-153;
+// diff.hpp:16-37) on the device
+// ---------------------------------------------------------------------------
+extern "C" int csf_associate(csf_ctx ctx, const double* mvert, const double* mnorm, const double* pvert,
+                             const double* pnorm, int w, int h, const double* camera_to_world,
+                             const double* predicted_camera_to_world, const csf_intrinsics* k, const csf_icp_cfg* cfg,
+                             int pixel_stride, double* corrs, int* n_corrs) {
+  if (!ctx || !mvert || !mnorm || !pvert || !pnorm || !camera_to_world || !predicted_camera_to_world || !k || !cfg ||
+      !corrs || !n_corrs || w <= 0 || h <= 0)
+    return CSF_EINVAL;
+  cudaSetDevice(ctx->device);
+  double prm[28];
+  std::copy(camera_to_world, camera_to_world + 12, prm);
+  csfd::Pose<double> pp;
+  for (int e = 0; e < 9; ++e) pp.R.m[e] = predicted_camera_to_world[e];
+  for (int e = 0; e < 3; ++e) pp.t.v[e] = predicted_camera_to_world[9 + e];
+  const csfd::Pose<double> inv = csfd::inverse(pp);
+  for (int e = 0; e < 9; ++e) prm[12 + e] = inv.R.m[e];
+  for (int e = 0; e < 3; ++e) prm[21 + e] = inv.t.v[e];
+  prm[24] = k->fx; prm[25] = k->fy; prm[26] = k->cx; prm[27] = k->cy;
+  const double cos_max = csf_det::cos(cfg->theta_max_deg * M_PI / 180.0);
+  const int rc = associate_maps(ctx->stream, ctx->energy, mvert, mnorm, pvert, pnorm, w, h, std::max(1, pixel_stride),
+                                prm, cfg->d_max, cos_max, corrs, n_corrs);
+  if (rc == 5) return fail(ctx, CSF_ENOMEM, "csf_associate: out of device memory");
+  if (rc) return fail(ctx, CSF_ECUDA, "csf_associate: CUDA error");
+  return sync_check(ctx, "csf_associate");
+}
+
+extern "C" int csf_linearized_step(csf_ctx ctx, const double* corrs, int n, const double* base, double* delta) {
+  if (!ctx || (n > 0 && !corrs) || !base || !delta || n < 0) return CSF_EINVAL;
+  cudaSetDevice(ctx->device);
+  const size_t need = static_cast<size_t>(std::max(n, 1)) * 9;
+  if (ctx->corr_upload_cap < need) {
+    if (ctx->corr_upload) cudaFree(ctx->corr_upload);
+    ctx->corr_upload = nullptr;
+    ctx->corr_upload_cap = 0;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->corr_upload, sizeof(double) * need));
+    ctx->corr_upload_cap = need;
+  }
+  if (n > 0)
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->corr_upload, corrs, sizeof(double) * 9 * n, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+  const int tiles = (n + 255) / 256;
+  std::vector<double> part(static_cast<size_t>(tiles) * 27);
+  const int rc = linearized_tiles(ctx->stream, ctx->corr_upload, n, base, part.data());
+  if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "csf_linearized_step: device failure");
+  // canonical order: tiles in groups of 16 summed in order, group totals in order
+  double total[27] = {0}, group[27] = {0};
+  for (int t = 0; t < tiles; ++t) {
+    for (int a = 0; a < 27; ++a) group[a] = group[a] + part[static_cast<size_t>(t) * 27 + a];
+    if ((t + 1) % 16 == 0 || t + 1 == tiles) {
+      for (int a = 0; a < 27; ++a) {
+        total[a] = total[a] + group[a];
+        group[a] = 0.0;
+      }
+    }
+  }
+  double nb[6], m[6][6], d[6];
+  int tr[6];
+  for (int i = 0; i < 6; ++i) nb[i] = -total[21 + i];
+  csfd::ldlt6_factor_reg<double>(total, m, tr);
+  csfd::ldlt6_apply_reg<double>(m, tr, nb, d);
+  bool finite = true;
+  for (int i = 0; i < 6; ++i) finite = finite && std::isfinite(d[i]);
+  for (int i = 0; i < 6; ++i) delta[i] = finite ? d[i] : 0.0;  // delta.allFinite() (icp.cpp:152)
+  return CSF_OK;
+}
+
+extern "C" int csf_pairwise_sum(csf_ctx ctx, const double* terms, int n, int channels, double* out) {
+  if (!ctx || (n > 0 && !terms) || !out || n < 0 || channels <= 0) return CSF_EINVAL;
+  cudaSetDevice(ctx->device);
+  const size_t C = static_cast<size_t>(channels);
+  std::vector<double> t(static_cast<size_t>(n) * C);
+  for (int i = 0; i < n; ++i)
+    for (size_t c = 0; c < C; ++c) t[c * n + i] = terms[static_cast<size_t>(i) * C + c];  // slot-major
+  DevBuf<double> d;
+  CUDA_TRY(ctx, d.alloc(std::max<size_t>(t.size(), 1)));
+  if (n > 0) CUDA_TRY(ctx, cudaMemcpy(d.p, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
+  const int rc = tree_sum_slots(ctx->stream, ctx->energy, d.p, n, channels, out);
+  if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "csf_pairwise_sum: device failure");
+  return CSF_OK;
+}
+
+// ---------------------------------------------------------------------------
 // track_frame (icp.cpp:169-244) — every solver family.  The per-pixel work
 // (bilateral filter, pyramid, raycast, association, normal equations,
 // energies and their CSFD derivatives) runs on the device; the 6-vector

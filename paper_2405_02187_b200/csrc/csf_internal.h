@@ -101,6 +101,10 @@ int associate_list(cudaStream_t stream, EnergyScratch& ws, const double* depth, 
                    const double* intr4, const double* pose12, const double* pred_w2c12, const double* vre,
                    const double* nre, double d_max, double cos_max, int* n_out);
 void energy_scratch_release(EnergyScratch& ws);
+int associate_maps(cudaStream_t stream, EnergyScratch& ws, const double* mvert, const double* mnorm,
+                   const double* pvert, const double* pnorm, int w, int h, int stride, const double* prm28,
+                   double d_max, double cos_max, double* corrs_out, int* n_out);
+int linearized_tiles(cudaStream_t stream, const double* corrs, int n, const double* base12, double* tiles_out);
 // pairwise_sum of every slot of device terms [C][n] into out_host[C] (synchronous)
 int tree_sum_slots(cudaStream_t stream, EnergyScratch& ws, const double* terms, int n, int C, double* out_host);
 

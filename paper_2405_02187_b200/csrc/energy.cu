@@ -208,6 +208,120 @@ __global__ void k_assoc_scatter(const double* __restrict__ depth, int w, int str
   }
 }
 
+// associate (icp.cpp:89-126) over given measured / predicted maps (the
+// reference's signature): gates in the reference's order, scan-order list.
+__global__ void k_assoc_maps_flags(const double* __restrict__ mvert, const double* __restrict__ mnorm,
+                                   const double* __restrict__ pvert, const double* __restrict__ pnorm, int w, int h,
+                                   int stride, const double* __restrict__ prm /*c2w[12], w2p[12], k[4]*/,
+                                   double d_max, double cos_max, int* __restrict__ flags, int* __restrict__ uv) {
+  pdl_wait();
+  pdl_trigger();
+  const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= nxs * nys) return;
+  const int x = (slot % nxs) * stride, y = (slot / nxs) * stride;
+  const long long i = static_cast<long long>(y) * w + x;
+  flags[slot] = 0;
+  uv[slot] = -1;
+  const V3<double> vert = mk3<double>(mvert[3 * i], mvert[3 * i + 1], mvert[3 * i + 2]);
+  const V3<double> nrm = mk3<double>(mnorm[3 * i], mnorm[3 * i + 1], mnorm[3 * i + 2]);
+  if (!(vert.v[2] > 0.0) || !(dot3(nrm, nrm) > 0.5)) return;  // vertex_valid, normal_valid (frames.hpp:73-81)
+  Pose<double> c2w, w2p;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    c2w.R.m[e] = prm[e];
+    w2p.R.m[e] = prm[12 + e];
+  }
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    c2w.t.v[e] = prm[9 + e];
+    w2p.t.v[e] = prm[21 + e];
+  }
+  const double fx = prm[24], fy = prm[25], cx = prm[26], cy = prm[27];
+  const V3<double> world = apply(c2w, vert);
+  const V3<double> inp = apply(w2p, world);
+  if (!(inp.v[2] > 0.0)) return;
+  const int u = static_cast<int>(lround((fx * inp.v[0]) / inp.v[2] + cx));
+  const int v = static_cast<int>(lround((fy * inp.v[1]) / inp.v[2] + cy));
+  if (!(u >= 0 && u < w && v >= 0 && v < h)) return;
+  const long long m = static_cast<long long>(v) * w + u;
+  const V3<double> mn = mk3<double>(pnorm[3 * m], pnorm[3 * m + 1], pnorm[3 * m + 2]);
+  if (!(dot3(mn, mn) > 0.5)) return;
+  const V3<double> mv = mk3<double>(pvert[3 * m], pvert[3 * m + 1], pvert[3 * m + 2]);
+  const V3<double> dd = sub3(world, mv);
+  if (sqrt(dot3(dd, dd)) > d_max) return;
+  const V3<double> wn = matvec(c2w.R, nrm);
+  if (dot3(wn, mn) < cos_max) return;
+  flags[slot] = 1;
+  uv[slot] = static_cast<int>(m);
+}
+
+__global__ void k_assoc_maps_scatter(const double* __restrict__ mvert, const double* __restrict__ pvert,
+                                     const double* __restrict__ pnorm, int w, int stride, int n_slots,
+                                     const int* __restrict__ flags, const int* __restrict__ pos,
+                                     const int* __restrict__ uv, double* __restrict__ corrs, int* __restrict__ count) {
+  pdl_wait();
+  pdl_trigger();
+  const int nxs = (w + stride - 1) / stride;
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= n_slots) return;
+  if (slot == n_slots - 1) *count = pos[slot] + flags[slot];
+  if (!flags[slot]) return;
+  const long long i = static_cast<long long>((slot / nxs) * stride) * w + (slot % nxs) * stride;
+  const long long m = uv[slot];
+  double* c = corrs + 9LL * pos[slot];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    c[k] = mvert[3 * i + k];
+    c[3 + k] = pvert[3 * m + k];
+    c[6 + k] = pnorm[3 * m + k];
+  }
+}
+
+// Per-tile normal-equation sums over a correspondence list (the oracle's
+// canonical normal_equations(corrs, base, false): tiles of 256
+// correspondences summed sequentially); out [tiles][27].
+__global__ void __launch_bounds__(256) k_lin_tiles(const double* __restrict__ corrs, int n,
+                                                   const double* __restrict__ base, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double rows[256][7];
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  const int cnt = min(256, n - static_cast<int>(blockIdx.x) * 256);
+  if (static_cast<int>(threadIdx.x) < cnt) {
+    Pose<double> b;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) b.R.m[e] = base[e];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) b.t.v[e] = base[9 + e];
+    const double* c = corrs + 9LL * i;
+    const V3<double> p = apply(b, mk3<double>(c[0], c[1], c[2]));
+    const V3<double> mv = mk3<double>(c[3], c[4], c[5]), mn = mk3<double>(c[6], c[7], c[8]);
+    const double r = dot3(sub3(p, mv), mn);
+    const V3<double> pn = cross3(p, mn);
+    rows[threadIdx.x][0] = mn.v[0]; rows[threadIdx.x][1] = mn.v[1]; rows[threadIdx.x][2] = mn.v[2];
+    rows[threadIdx.x][3] = pn.v[0]; rows[threadIdx.x][4] = pn.v[1]; rows[threadIdx.x][5] = pn.v[2];
+    rows[threadIdx.x][6] = r;
+  }
+  __syncthreads();
+  const int a = threadIdx.x;
+  if (a < 27) {
+    int ja, jb;
+    if (a < 21) {
+      int r = 0;
+      while ((r + 1) * (r + 2) / 2 <= a) ++r;
+      ja = r;
+      jb = a - r * (r + 1) / 2;
+    } else {
+      ja = a - 21;
+      jb = 6;
+    }
+    double s = 0.0;
+    for (int e = 0; e < cnt; ++e) s = s + rows[e][ja] * rows[e][jb];
+    out[static_cast<long long>(blockIdx.x) * 27 + a] = s;
+  }
+}
+
 }  // namespace csfd
 
 // ============================================================================
@@ -403,6 +517,92 @@ int associate_list(cudaStream_t stream, EnergyScratch& ws, const double* depth, 
   if (cudaMemcpyAsync(n_out, count, sizeof(int), cudaMemcpyDeviceToHost, stream) != cudaSuccess) return 4;
   if (cudaStreamSynchronize(stream) != cudaSuccess) return 4;
   return 0;
+}
+
+// associate over host maps -> host corrs (synchronous); returns 0/4/5
+int associate_maps(cudaStream_t stream, EnergyScratch& ws, const double* mvert, const double* mnorm,
+                   const double* pvert, const double* pnorm, int w, int h, int stride, const double* prm28,
+                   double d_max, double cos_max, double* corrs_out, int* n_out) {
+  const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
+  const int n_slots = nxs * nys;
+  const size_t P = static_cast<size_t>(w) * h;
+  double* dm = nullptr;
+  if (cudaMalloc(&dm, sizeof(double) * (12 * P + 28)) != cudaSuccess) return 5;
+  double* d_mv = dm;
+  double* d_mn = dm + 3 * P;
+  double* d_pv = dm + 6 * P;
+  double* d_pn = dm + 9 * P;
+  double* d_prm = dm + 12 * P;
+  cudaMemcpyAsync(d_mv, mvert, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(d_mn, mnorm, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(d_pv, pvert, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(d_pn, pnorm, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(d_prm, prm28, sizeof(double) * 28, cudaMemcpyHostToDevice, stream);
+  int rc = 0;
+  const size_t need = static_cast<size_t>(std::max(n_slots, 1));
+  if (ws.flags_cap < need) {
+    if (ws.flags) cudaFree(ws.flags);
+    if (ws.corrs) cudaFree(ws.corrs);
+    if (ws.cub) cudaFree(ws.cub);
+    ws.flags = nullptr;
+    ws.corrs = nullptr;
+    ws.cub = nullptr;
+    ws.flags_cap = 0;
+    size_t cub_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, static_cast<int*>(nullptr), static_cast<int*>(nullptr),
+                                  static_cast<int>(need));
+    if (cudaMalloc(&ws.flags, sizeof(int) * (3 * need + 4)) != cudaSuccess ||
+        cudaMalloc(&ws.corrs, sizeof(double) * 9 * need) != cudaSuccess ||
+        cudaMalloc(&ws.cub, cub_bytes) != cudaSuccess)
+      rc = 5;
+    ws.cub_bytes = cub_bytes;
+    ws.flags_cap = need;
+  }
+  int n = 0;
+  if (!rc && n_slots > 0) {
+    int* flags = ws.flags;
+    int* pos = flags + need;
+    int* uv = pos + need;
+    int* count = uv + need;
+    launch_pdl(k_assoc_maps_flags, dim3((n_slots + 127) / 128), dim3(128), 0, stream, static_cast<const double*>(d_mv),
+               static_cast<const double*>(d_mn), static_cast<const double*>(d_pv), static_cast<const double*>(d_pn), w,
+               h, stride, static_cast<const double*>(d_prm), d_max, cos_max, flags, uv);
+    size_t bytes = ws.cub_bytes;
+    cub::DeviceScan::ExclusiveSum(ws.cub, bytes, flags, pos, n_slots, stream);
+    launch_pdl(k_assoc_maps_scatter, dim3((n_slots + 127) / 128), dim3(128), 0, stream,
+               static_cast<const double*>(d_mv), static_cast<const double*>(d_pv), static_cast<const double*>(d_pn), w,
+               stride, n_slots, static_cast<const int*>(flags), static_cast<const int*>(pos),
+               static_cast<const int*>(uv), ws.corrs, count);
+    if (cudaMemcpyAsync(&n, count, sizeof(int), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess)
+      rc = 4;
+    if (!rc && n > 0 &&
+        cudaMemcpy(corrs_out, ws.corrs, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = 4;
+  }
+  cudaStreamSynchronize(stream);
+  cudaFree(dm);
+  *n_out = n;
+  return rc;
+}
+
+// Tile partials [tiles][27] of the canonical normal equations over n device
+// correspondences (synchronous, to the host).
+int linearized_tiles(cudaStream_t stream, const double* corrs, int n, const double* base12, double* tiles_out) {
+  const int tiles = (n + 255) / 256;
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double) * (static_cast<size_t>(tiles) * 27 + 12)) != cudaSuccess) return 5;
+  double* d_base = d + static_cast<size_t>(tiles) * 27;
+  cudaMemcpyAsync(d_base, base12, sizeof(double) * 12, cudaMemcpyHostToDevice, stream);
+  if (tiles > 0)
+    launch_pdl(k_lin_tiles, dim3(tiles), dim3(256), 0, stream, corrs, n, static_cast<const double*>(d_base), d);
+  int rc = 0;
+  if (cudaMemcpyAsync(tiles_out, d, sizeof(double) * static_cast<size_t>(tiles) * 27, cudaMemcpyDeviceToHost,
+                      stream) != cudaSuccess ||
+      cudaStreamSynchronize(stream) != cudaSuccess)
+    rc = 4;
+  cudaFree(d);
+  return rc;
 }
 
 }  // namespace csfi
