@@ -189,6 +189,19 @@ int csf_volume_block_count(csf_volume vol, int* n_blocks);
 /* heads [2^bits], keys [n_blocks], next [n_blocks], coords [n_blocks][3] */
 int csf_volume_download_hash(csf_volume vol, int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords);
 
+/* Point queries.  tsdf.hpp:148-177 sample_tsdf / 181-196 sample_gradient at
+ * lifted world points [n][3][1+D] (D = the volume's channels): values
+ * [n][1+D] / gradients [n][3][1+D]; valid[i] = 0 where the reference returns
+ * std::nullopt (a corner unobserved / unallocated). */
+int csf_sample_tsdf(csf_volume vol, const double* points, int n, double* values, int32_t* valid);
+int csf_sample_gradient(csf_volume vol, const double* points, int n, double* gradients, int32_t* valid);
+/* tsdf.hpp:97-140 measured_tsdf at real voxel positions points [n][3]:
+ * unperturbed depth [h][w], lifted world->camera pose [12][1+D], lifted
+ * intrinsics [4][1+D], lifted camera centre [3][1+D]; psi [n][1+D]. */
+int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h, const double* world_to_camera,
+                      const double* intr, double mu, const double* points, const double* center, int n,
+                      int n_channels, double* psi, int32_t* valid);
+
 /* tsdf.cpp:61-153 — save_volume / load_volume in the reference's "CSFVOL 1"
  * container: text header (dims, voxel_size, origin, mu, weight_cap, channels)
  * then float32 planes (field, weight, derivative channels only when any is

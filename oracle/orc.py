@@ -47,6 +47,8 @@ def lib() -> C.CDLL:
             "orc_associate": (ip, [dp, dp, dp, dp, ip, ip, dp, dp, C.POINTER(_capi.Intrinsics), C.POINTER(_capi.IcpCfg),
                                    ip, dp, C.POINTER(C.c_int)]),
             "orc_linearized_step": (ip, [dp, ip, dp, ip, dp]),
+            "orc_sample_points": (ip, [vp, dp, ip, ip, dp, i32p]),
+            "orc_measured_points": (ip, [dp, ip, ip, dp, dp, C.c_double, dp, dp, ip, ip, dp, i32p]),
             "orc_view_scores": (ip, [vp, dp, ip, C.POINTER(_capi.Intrinsics), C.c_double, C.c_double, C.c_double,
                                      dp, dp]),
             "orc_icp_energy_derivs": (ip, [dp, ip, dp, dp, C.c_double, dp, dp, dp]),
@@ -159,6 +161,14 @@ class Volume:
                                      coords.ctypes.data_as(C.POINTER(C.c_int32))))
         return heads, keys, nxt, coords
 
+    def sample_points(self, pts, grad=False):
+        P = np.ascontiguousarray(pts, dtype=np.float64)
+        n = P.shape[0]
+        out = np.zeros((n, 3, 1 + self.channels) if grad else (n, 1 + self.channels))
+        ok = np.zeros(n, dtype=np.int32)
+        _check(lib().orc_sample_points(self.h, _dp(P), n, int(grad), _dp(out), ok.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out, ok.astype(bool)
+
     def view_scores(self, poses, k, w0=10.0, beta=0.5, h=1e-8):
         """BASELINE config 5 objective and its view-twist gradient (builder-defined)."""
         p = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 12)
@@ -270,3 +280,17 @@ def pairwise_sum(terms):
         return block(x[:half]) + block(x[half:])
     t = [float(v) for v in terms]
     return 0.0 if not t else 0.0 + block(t)
+
+
+def measured_tsdf(depth, w2c, intr, mu, pts, center):
+    d = np.ascontiguousarray(depth, dtype=np.float64)
+    h, w = d.shape
+    pose = np.ascontiguousarray(w2c, dtype=np.float64)
+    D = pose.shape[1] - 1
+    P = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros((P.shape[0], 1 + D))
+    ok = np.zeros(P.shape[0], dtype=np.int32)
+    _check(lib().orc_measured_points(_dp(d), w, h, _dp(pose), _dp(np.ascontiguousarray(intr, dtype=np.float64)), mu,
+                                     _dp(P), _dp(np.ascontiguousarray(center, dtype=np.float64)), P.shape[0], D,
+                                     _dp(out), ok.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out, ok.astype(bool)

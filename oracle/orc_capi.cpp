@@ -136,6 +136,7 @@ struct VolBase {
                             bool canonical) const = 0;
   virtual void view_scores(const double* poses, int n, const Intrinsics& k, double w0, double beta, double h,
                            double* scores, double* grads) const = 0;
+  virtual void sample_points(const double* pts, int n, int grad, double* out, int32_t* valid) const = 0;
 };
 
 template <int D, bool H>
@@ -198,6 +199,22 @@ struct Vol : VolBase {
   TrackResult track(const Image<double>& depth, const Pose& init, const Intrinsics& k, const IcpConfig& cfg,
                     bool canonical) const override {
     return track_frame(vol, depth, init, k, cfg, nullptr, canonical);
+  }
+  void sample_points(const double* pts, int n, int grad, double* out, int32_t* valid) const override {
+    for (int i = 0; i < n; ++i) {
+      Vec3<F> p;
+      for (int c = 0; c < 3; ++c) p[c] = load_s<D>(pts + (3 * i + c) * (1 + D));
+      if (!grad) {
+        const auto f = sample_tsdf<F>(vol, p);
+        valid[i] = f.has_value();
+        if (f) store_s<D>(out + i * (1 + D), *f);
+      } else {
+        const auto g = sample_gradient<F>(vol, p);
+        valid[i] = g.has_value();
+        if (g)
+          for (int c = 0; c < 3; ++c) store_s<D>(out + (3 * i + c) * (1 + D), (*g)[c]);
+      }
+    }
   }
   // config 5: one Lifted<6> pass per view over the volume's real field
   void view_scores(const double* poses, int n, const Intrinsics& k, double w0, double beta, double h, double* scores,
@@ -402,6 +419,38 @@ void write_stats(int n_frames, const std::vector<int>& it, const std::vector<int
 }  // namespace
 
 extern "C" {
+
+int orc_sample_points(void* v, const double* pts, int n, int grad, double* out, int32_t* valid) {
+  return guard([&] { static_cast<VolBase*>(v)->sample_points(pts, n, grad, out, valid); });
+}
+
+int orc_measured_points(const double* depth, int w, int h, const double* w2c, const double* intr, double mu,
+                        const double* pts, const double* center, int n, int D, double* out, int32_t* valid) {
+  return guard([&] {
+    auto run = [&](auto tag) {
+      constexpr int DD = decltype(tag)::value;
+      using S = FT<DD>;
+      Image<double> dimg = image_of(depth, w, h);
+      const PoseT<S> pose = load_pose<DD>(w2c);
+      const IntrinsicsT<S> k = load_intr<DD>(intr, w, h);
+      Vec3<S> c;
+      for (int e = 0; e < 3; ++e) c[e] = load_s<DD>(center + e * (1 + DD));
+      for (int i = 0; i < n; ++i) {
+        const Vec3<S> p(S(pts[3 * i]), S(pts[3 * i + 1]), S(pts[3 * i + 2]));
+        const auto m = measured_tsdf<S>(dimg, pose, k, mu, p, c);
+        valid[i] = m.has_value();
+        if (m) store_s<DD>(out + i * (1 + DD), *m);
+      }
+    };
+    switch (D) {
+      case 0: run(std::integral_constant<int, 0>{}); break;
+      case 1: run(std::integral_constant<int, 1>{}); break;
+      case 2: run(std::integral_constant<int, 2>{}); break;
+      case 3: run(std::integral_constant<int, 3>{}); break;
+      default: throw std::invalid_argument("orc_measured_points: unsupported channel count");
+    }
+  });
+}
 
 int orc_view_scores(void* v, const double* poses, int n, const csf_intrinsics* k, double w0, double beta, double h,
                     double* scores, double* grads) {

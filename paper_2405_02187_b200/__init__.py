@@ -34,7 +34,7 @@ __all__ = [
     "measure_surface", "TsdfVolume", "HashedVolume", "surface_update", "raycast", "track_frame", "TrackResult",
     "icp_energy", "icp_loss", "icp_gradient", "icp_hessian", "icp_energy_derivs", "associate", "linearized_step",
     "pairwise_sum", "complex_depth", "perturb_depth",
-    "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "look_at", "config5_views", "save_volume", "load_volume", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
+    "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "look_at", "config5_views", "save_volume", "load_volume", "measured_tsdf", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
     "lift_pose", "lift_intrinsics", "library",
 ]
 
@@ -307,6 +307,34 @@ class _Volume:
         wt = _f64(weight)
         self.ctx.check(self.ctx.lib.csf_volume_upload(self.h, _dp(f), _dp(wt)))
 
+    def _points(self, points):
+        P = _f64(points)
+        if P.ndim == 2 and P.shape[1] == 3:
+            Q = np.zeros((P.shape[0], 3, 1 + self.channels))
+            Q[..., 0] = P
+            P = Q
+        if P.ndim != 3 or P.shape[1:] != (3, 1 + self.channels):
+            raise InvalidArgument(f"points must be (n, 3) or (n, 3, {1 + self.channels})")
+        return np.ascontiguousarray(P)
+
+    def sample_tsdf(self, points):
+        """tsdf.hpp:148-177 at lifted world points: (values (n, 1+D), valid (n,) bool)."""
+        P = self._points(points)
+        out = np.zeros((P.shape[0], 1 + self.channels))
+        ok = np.zeros(P.shape[0], dtype=np.int32)
+        self.ctx.check(self.ctx.lib.csf_sample_tsdf(self.h, _dp(P), P.shape[0], _dp(out),
+                                                    ok.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out, ok.astype(bool)
+
+    def sample_gradient(self, points):
+        """tsdf.hpp:181-196: (gradients (n, 3, 1+D), valid (n,) bool)."""
+        P = self._points(points)
+        out = np.zeros((P.shape[0], 3, 1 + self.channels))
+        ok = np.zeros(P.shape[0], dtype=np.int32)
+        self.ctx.check(self.ctx.lib.csf_sample_gradient(self.h, _dp(P), P.shape[0], _dp(out),
+                                                        ok.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out, ok.astype(bool)
+
     def save(self, path) -> None:
         """save_volume (tsdf.cpp:61-97): the "CSFVOL 1" checkpoint."""
         self.ctx.check(self.ctx.lib.csf_volume_save(self.h, str(path).encode()))
@@ -401,6 +429,27 @@ def config5_views(n: int = 256, seed: int = 4) -> np.ndarray:
         target = np.array([rng.uniform(-1.6, 1.6), rng.uniform(-1.6, 1.6), rng.uniform(0.3, 2.5)])
         out[i] = look_at(eye, target)
     return out
+
+
+def measured_tsdf(depth, world_to_camera, k, mu: float, points, center, ctx: Optional[Context] = None):
+    """tsdf.hpp:97-140 at real voxel positions (n, 3): (psi (n, 1+D), valid (n,) bool); the
+    pose (12, 1+D), intrinsics (4, 1+D) and camera centre (3, 1+D) carry D channels."""
+    c = _ctx(ctx)
+    d = _f64(depth)
+    h, w = d.shape
+    pose = _f64(world_to_camera)
+    D = pose.shape[1] - 1 if pose.ndim == 2 else 0
+    pose = lift_pose(pose, D)
+    kk = lift_intrinsics(k, D)
+    cen = _f64(center).reshape(3, -1)
+    if cen.shape[1] != 1 + D:
+        cen = np.concatenate([cen[:, :1], np.zeros((3, D))], axis=1)
+    P = np.ascontiguousarray(_f64(points).reshape(-1, 3))
+    out = np.zeros((P.shape[0], 1 + D))
+    ok = np.zeros(P.shape[0], dtype=np.int32)
+    c.check(c.lib.csf_measured_tsdf(c.h, _dp(d), w, h, _dp(pose), _dp(kk), mu, _dp(P), _dp(np.ascontiguousarray(cen)),
+                                    P.shape[0], D, _dp(out), ok.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out, ok.astype(bool)
 
 
 def save_volume(path, volume: _Volume) -> None:

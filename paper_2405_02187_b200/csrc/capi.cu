@@ -1070,6 +1070,91 @@ extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const d
 // track_frame (real tracker on the device)
 // ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
+// point queries: sample_tsdf / sample_gradient (tsdf.hpp:148-196), measured_tsdf (tsdf.hpp:97-140)
+// ---------------------------------------------------------------------------
+static int sample_points_common(csf_volume v, const double* points, int n, int grad, double* out, int32_t* valid) {
+  if (!v || (n > 0 && (!points || !out || !valid)) || n < 0) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  if (v->order != 1) return fail(ctx, CSF_EINVAL, "point queries take first-order volumes");
+  cudaSetDevice(ctx->device);
+  const int D = v->D, Dp = v->Dp, C = 1 + D, Cp = 1 + Dp;
+  const size_t rows = static_cast<size_t>(n) * 3;
+  std::vector<double> pts(rows * Cp, 0.0);
+  for (size_t r = 0; r < rows; ++r)
+    for (int c = 0; c < C; ++c) pts[r * Cp + c] = points[r * C + c];
+  const size_t outn = static_cast<size_t>(n) * (grad ? 3 : 1) * Cp;
+  DevBuf<double> dp, dout;
+  DevBuf<int> dv;
+  CUDA_TRY(ctx, dp.alloc(std::max<size_t>(pts.size(), 1)));
+  CUDA_TRY(ctx, dout.alloc(std::max<size_t>(outn, 1)));
+  CUDA_TRY(ctx, dv.alloc(std::max(n, 1)));
+  if (n > 0) {
+    CUDA_TRY(ctx, cudaMemcpy(dp.p, pts.data(), sizeof(double) * pts.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemset(dout.p, 0, sizeof(double) * outn));
+  }
+  launch_sample_points(launch_of(ctx), v->hashed, v->dense, v->hash, Dp, dp.p, n, grad, dout.p, dv.p);
+  const int rc = sync_check(ctx, grad ? "csf_sample_gradient" : "csf_sample_tsdf");
+  if (rc) return rc;
+  std::vector<double> o(outn);
+  std::vector<int> vv(std::max(n, 1));
+  if (n > 0) {
+    CUDA_TRY(ctx, cudaMemcpy(o.data(), dout.p, sizeof(double) * outn, cudaMemcpyDeviceToHost));
+    CUDA_TRY(ctx, cudaMemcpy(vv.data(), dv.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  }
+  const size_t orow = static_cast<size_t>(n) * (grad ? 3 : 1);
+  for (size_t r = 0; r < orow; ++r)
+    for (int c = 0; c < C; ++c) out[r * C + c] = o[r * Cp + c];
+  for (int i = 0; i < n; ++i) valid[i] = vv[i];
+  return CSF_OK;
+}
+
+extern "C" int csf_sample_tsdf(csf_volume v, const double* points, int n, double* values, int32_t* valid) {
+  return sample_points_common(v, points, n, 0, values, valid);
+}
+extern "C" int csf_sample_gradient(csf_volume v, const double* points, int n, double* gradients, int32_t* valid) {
+  return sample_points_common(v, points, n, 1, gradients, valid);
+}
+
+extern "C" int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h, const double* world_to_camera,
+                                 const double* intr, double mu, const double* points, const double* center, int n,
+                                 int n_channels, double* psi, int32_t* valid) {
+  if (!ctx || !depth || !world_to_camera || !intr || !center || w <= 0 || h <= 0 || n < 0 || n_channels < 0 ||
+      n_channels > CSF_MAX_DIRECTIONS || (n > 0 && (!points || !psi || !valid)))
+    return CSF_EINVAL;
+  cudaSetDevice(ctx->device);
+  const int D = n_channels, C = 1 + D;
+  const size_t P = static_cast<size_t>(w) * h;
+  DevBuf<double> buf, dout;
+  DevBuf<int> dv;
+  CUDA_TRY(ctx, buf.alloc(P + 12 * C + 4 * C + 3 * C + 3 * static_cast<size_t>(std::max(n, 1))));
+  CUDA_TRY(ctx, dout.alloc(static_cast<size_t>(std::max(n, 1)) * C));
+  CUDA_TRY(ctx, dv.alloc(std::max(n, 1)));
+  double* d_depth = buf.p;
+  double* d_pose = d_depth + P;
+  double* d_intr = d_pose + 12 * C;
+  double* d_center = d_intr + 4 * C;
+  double* d_pts = d_center + 3 * C;
+  CUDA_TRY(ctx, cudaMemcpy(d_depth, depth, sizeof(double) * P, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(d_pose, world_to_camera, sizeof(double) * 12 * C, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(d_intr, intr, sizeof(double) * 4 * C, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(d_center, center, sizeof(double) * 3 * C, cudaMemcpyHostToDevice));
+  if (n > 0) {
+    CUDA_TRY(ctx, cudaMemcpy(d_pts, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemset(dout.p, 0, sizeof(double) * n * C));
+  }
+  launch_measured_points(launch_of(ctx), d_depth, w, h, d_pose, d_intr, mu, d_pts, d_center, n, D, dout.p, dv.p);
+  const int rc = sync_check(ctx, "csf_measured_tsdf");
+  if (rc) return rc;
+  if (n > 0) {
+    CUDA_TRY(ctx, cudaMemcpy(psi, dout.p, sizeof(double) * n * C, cudaMemcpyDeviceToHost));
+    std::vector<int> vv(n);
+    CUDA_TRY(ctx, cudaMemcpy(vv.data(), dv.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) valid[i] = vv[i];
+  }
+  return CSF_OK;
+}
+
+// ---------------------------------------------------------------------------
 // checkpoints: the reference's "CSFVOL 1" container (tsdf.cpp:61-153)
 // ---------------------------------------------------------------------------
 namespace csfi {

@@ -140,6 +140,12 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
                            int w, int h, double near_clip, double far_clip, double step, double2* hits, double* vre,
                            double* nre, double* vim, double* nim);
 void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp);
+// point queries (tsdf.hpp:97-196): pts [n][3][1+Dp] lifted (sample) or [n][3] real (measured)
+void launch_sample_points(const Launch& L, bool hashed, const DenseDev& dd, const HashDev& hd, int Dp,
+                          const double* pts, int n, int grad, double* out, int* valid);
+void launch_measured_points(const Launch& L, const double* depth, int w, int h, const double* w2c, const double* intr,
+                            double mu, const double* pts, const double* center, int n, int Dp, double* out,
+                            int* valid);
 
 // ---- icp.cu
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp);

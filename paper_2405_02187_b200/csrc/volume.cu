@@ -1570,6 +1570,121 @@ static int sm_count() {
   return n;
 }
 
+}  // namespace csfi
+
+namespace csfd {
+// ----------------------------------------------------------------------------
+// Point queries of the stage API (tsdf.hpp:97-196): one thread per (point,
+// channel) in L<1> (or double without channels); the real part is the
+// reference's and bit-identical in every channel thread.
+// ----------------------------------------------------------------------------
+template <typename S>
+CSF_DEV V3<S> load_point(const double* pts, int i, int C, int ch) {
+  V3<S> p;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) p.v[c] = load_ch<S>(pts + (3LL * i + c) * C, ch, 1);
+  return p;
+}
+
+template <typename V, typename S>
+__global__ void k_sample_points(V vol, const double* __restrict__ pts, int n, int Dp, int grad,
+                                double* __restrict__ out, int* __restrict__ valid) {
+  pdl_wait();
+  pdl_trigger();
+  const int lanes = Dp > 0 ? Dp : 1;
+  const long long item = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (item >= static_cast<long long>(n) * lanes) return;
+  const int i = static_cast<int>(item / lanes), ch = static_cast<int>(item % lanes);
+  const int C = 1 + Dp;
+  const V3<S> p = load_point<S>(pts, i, C, ch);
+  NoCache cache;
+  bool ok;
+  if (!grad) {
+    S f;
+    ok = sample_tsdf<S>(vol, p, ch, &f, cache);
+    if (ok) store_ch<S>(out + static_cast<long long>(i) * C, f, ch, Dp > 0 ? 1 : 0, ch == 0);
+  } else {
+    V3<S> g;
+    ok = sample_gradient<S>(vol, p, ch, &g, cache);
+    if (ok)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) store_ch<S>(out + (3LL * i + c) * C, g.v[c], ch, Dp > 0 ? 1 : 0, ch == 0);
+  }
+  if (ch == 0) valid[i] = ok ? 1 : 0;
+}
+
+// measured_tsdf at real voxel positions pts [n][3] for a lifted world->camera
+// pose, lifted intrinsics and lifted camera centre.
+template <typename S>
+__global__ void k_measured_points(const double* __restrict__ depth, int w, int h, const double* __restrict__ w2c,
+                                  const double* __restrict__ intr, double mu, const double* __restrict__ pts,
+                                  const double* __restrict__ center, int n, int Dp, double* __restrict__ out,
+                                  int* __restrict__ valid) {
+  pdl_wait();
+  pdl_trigger();
+  const int lanes = Dp > 0 ? Dp : 1;
+  const long long item = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (item >= static_cast<long long>(n) * lanes) return;
+  const int i = static_cast<int>(item / lanes), ch = static_cast<int>(item % lanes);
+  const int C = 1 + Dp, G = Dp > 0 ? 1 : 0;
+  Pose<S> pose;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) pose.R.m[e] = load_ch<S>(w2c + e * C, ch, G);
+#pragma unroll
+  for (int e = 0; e < 3; ++e) pose.t.v[e] = load_ch<S>(w2c + (9 + e) * C, ch, G);
+  Intr<S> k;
+  k.fx = load_ch<S>(intr, ch, G);
+  k.fy = load_ch<S>(intr + C, ch, G);
+  k.cx = load_ch<S>(intr + 2 * C, ch, G);
+  k.cy = load_ch<S>(intr + 3 * C, ch, G);
+  k.w = w;
+  k.h = h;
+  V3<S> c;
+#pragma unroll
+  for (int e = 0; e < 3; ++e) c.v[e] = load_ch<S>(center + e * C, ch, G);
+  S psi;
+  const bool ok = measured_tsdf<S>(depth, w, h, pose, k, mu, pts[3LL * i], pts[3LL * i + 1], pts[3LL * i + 2], c, &psi);
+  if (ok) store_ch<S>(out + static_cast<long long>(i) * C, psi, ch, G, ch == 0);
+  if (ch == 0) valid[i] = ok ? 1 : 0;
+}
+}  // namespace csfd
+
+namespace csfi {
+
+void launch_sample_points(const Launch& L, bool hashed, const DenseDev& dd, const HashDev& hd, int Dp,
+                          const double* pts, int n, int grad, double* out, int* valid) {
+  const long long items = static_cast<long long>(n) * (Dp > 0 ? Dp : 1);
+  const dim3 grid(static_cast<unsigned>((items + 127) / 128)), block(128);
+  if (items == 0) return;
+  if (hashed) {
+    const HashView v = hash_view(hd, Dp);
+    if (Dp > 0) launch_pdl(k_sample_points<HashView, csfd::L<1>>, grid, block, 0, L.stream, v, pts, n, Dp, grad, out, valid);
+    else launch_pdl(k_sample_points<HashView, double>, grid, block, 0, L.stream, v, pts, n, Dp, grad, out, valid);
+  } else {
+    const DenseView v = dense_view(dd, Dp);
+    if (Dp > 0) launch_pdl(k_sample_points<DenseView, csfd::L<1>>, grid, block, 0, L.stream, v, pts, n, Dp, grad, out, valid);
+    else launch_pdl(k_sample_points<DenseView, double>, grid, block, 0, L.stream, v, pts, n, Dp, grad, out, valid);
+  }
+  ++*L.launches;
+  chk("sample_points");
+}
+
+void launch_measured_points(const Launch& L, const double* depth, int w, int h, const double* w2c, const double* intr,
+                            double mu, const double* pts, const double* center, int n, int Dp, double* out,
+                            int* valid) {
+  const long long items = static_cast<long long>(n) * (Dp > 0 ? Dp : 1);
+  if (items == 0) return;
+  const dim3 grid(static_cast<unsigned>((items + 127) / 128)), block(128);
+  if (Dp > 0)
+    launch_pdl(k_measured_points<csfd::L<1>>, grid, block, 0, L.stream, depth, w, h, w2c, intr, mu, pts, center, n, Dp, out,
+               valid);
+  else
+    launch_pdl(k_measured_points<double>, grid, block, 0, L.stream, depth, w, h, w2c, intr, mu, pts, center, n, Dp,
+               out, valid);
+  ++*L.launches;
+  chk("measured_points");
+}
+
 void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp) {
   launch_pdl(k_init_volume, dim3(sm_count() * 8), dim3(256), 0, L.stream, rw, fim, n, Dp);
   ++*L.launches;
