@@ -272,6 +272,69 @@ int csf_icp_energy_derivs(csf_ctx ctx, const double* corrs, int n, const double*
 int csf_view_scores(csf_volume vol, const double* poses, int n_views, const csf_intrinsics* k, double w0, double beta,
                     double h, double* scores, double* grads);
 
+/* ---- relocalization: reloc.hpp --------------------------
+ * The reference implements reloc_energy<S> (reloc.hpp:48-69) and declares the
+ * rest without bodies; the builder-defined bodies follow the header comments
+ * and SPEC.md:533-600.  A csf_reloc is a RelocProblem
+ * (reloc.hpp:35-46) resident in HBM: the reference volume's observed voxels
+ * (W > 0, storage order: dense linear index, hashed pool block then local
+ * index) as centres + real field values, the query depth and intrinsics,
+ * mu = the volume's mu. */
+typedef struct csf_reloc_s* csf_reloc;
+#define CSF_RELOC_GRADIENT_DESCENT 0
+#define CSF_RELOC_NEWTON 1
+/* reloc.hpp:82-98 (RelocConfig with LineSearchConfig, descent.hpp:16-21) */
+typedef struct {
+  double switch_relative;  /* 0.5 */
+  double switch_absolute;  /* -1 = use switch_relative */
+  int max_iterations;      /* 50 */
+  int ls_max_backtracks;   /* 25 */
+  double step_tolerance;   /* 1e-6 */
+  double ls_initial_step, ls_shrink, ls_sufficient_decrease; /* 1, 0.5, 1e-4 */
+  double h;                /* StepSize, 1e-8 */
+  /* builder-defined safeguards: the overlap-restricted sum
+   * also falls when the view slides off the model, so a trial pose keeping
+   * fewer than min_overlap_ratio x the current overlap counts as +inf, and
+   * every direction is scaled to twist length <= max_step (the steepest-
+   * descent direction to exactly max_step). */
+  double max_step;          /* 0.05 */
+  double min_overlap_ratio; /* 0.9 */
+} csf_reloc_cfg;
+/* reloc.hpp:100-106 (RelocResult) */
+typedef struct {
+  int iterations;
+  int converged;
+  double final_loss;
+} csf_reloc_result;
+void csf_default_reloc_cfg(csf_reloc_cfg* cfg);
+/* RelocProblem(reference, query, k) (reloc.hpp:44-45): EINVAL when the
+ * volume has no observed voxel.  query depth [h][w] (host). */
+int csf_reloc_create(csf_volume reference, const double* query_depth, int w, int h, const csf_intrinsics* k,
+                     csf_reloc* out);
+int csf_reloc_destroy(csf_reloc r);
+/* voxel count and mu; centers [n][3] / values [n] (optional, host) */
+int csf_reloc_info(csf_reloc r, int* n_voxels, double* mu, double* centers, double* values);
+/* reloc_energy at the camera->world pose [12] (reloc.hpp:48-69), with the
+ * reloc_gradient (6 Complex passes) / reloc_hessian (21 Bicomplex passes) of
+ * reloc.hpp:75-80 at order 1 / 2 as one packed device pass each; overlap =
+ * mutually observed voxels.  ERUNTIME when no voxel overlaps. */
+int csf_reloc_energy(csf_reloc r, const double* pose, int order, double h, double* energy, double* gradient,
+                     double* hessian, long long* overlap);
+/* relocalize (reloc.hpp:116-124): gradient descent or eta-switched Newton
+ * with backtracking line search; losses / gradient_norms [max_iterations]
+ * (optional) = the trace rows (TraceRow::loss, gradient_norm). */
+int csf_relocalize(csf_reloc r, const double* initial_pose, int method, const csf_reloc_cfg* cfg, double* out_pose,
+                   csf_reloc_result* result, double* losses, double* gradient_norms);
+/* depth_cloud (reloc.hpp:126-129): world points [<= ceil(w/s) ceil(h/s)][3]
+ * of the valid pixels at the stride, row-major order. */
+int csf_depth_cloud(csf_ctx ctx, const double* depth, int w, int h, const csf_intrinsics* k,
+                    const double* camera_to_world, int stride, double* points, int* n_points);
+/* eval_nn_error (reloc.hpp:131-138): mean nearest-neighbour distance from
+ * transform * query to reference (brute force on the device); EINVAL on an
+ * empty cloud; outlier = mean > 0.1 m. */
+int csf_eval_nn_error(csf_ctx ctx, const double* transform, const double* query, int n_query, const double* reference,
+                      int n_reference, double* mean, int32_t* outlier);
+
 /* ---- pipeline ------------------------------------------------------------ */
 int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf_pipeline* out);
 int csf_pipeline_destroy(csf_pipeline p);

@@ -52,6 +52,13 @@ def lib() -> C.CDLL:
             "orc_view_scores": (ip, [vp, dp, ip, C.POINTER(_capi.Intrinsics), C.c_double, C.c_double, C.c_double,
                                      dp, dp]),
             "orc_icp_energy_derivs": (ip, [dp, ip, dp, dp, C.c_double, dp, dp, dp]),
+            "orc_reloc_create": (ip, [vp, dp, ip, ip, C.POINTER(_capi.Intrinsics), C.POINTER(vp)]),
+            "orc_reloc_destroy": (None, [vp]),
+            "orc_reloc_info": (ip, [vp, C.POINTER(C.c_int), dp, dp, dp]),
+            "orc_reloc_energy": (ip, [vp, dp, ip, C.c_double, dp, dp, dp, C.POINTER(C.c_long)]),
+            "orc_relocalize": (ip, [vp, dp, ip, C.POINTER(_capi.RelocCfg), dp, C.POINTER(_capi.RelocResult), dp, dp]),
+            "orc_depth_cloud": (ip, [dp, ip, ip, C.POINTER(_capi.Intrinsics), dp, ip, dp, C.POINTER(C.c_int)]),
+            "orc_nn_error": (ip, [dp, dp, ip, dp, ip, dp, C.POINTER(C.c_int)]),
             "orc_pipeline_hessian": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, dp, dp, i32p, dp]),
         }
         for name, (res, args) in sig.items():
@@ -294,3 +301,72 @@ def measured_tsdf(depth, w2c, intr, mu, pts, center):
                                      _dp(P), _dp(np.ascontiguousarray(center, dtype=np.float64)), P.shape[0], D,
                                      _dp(out), ok.ctypes.data_as(C.POINTER(C.c_int32))))
     return out, ok.astype(bool)
+
+
+class Reloc:
+    """RelocProblem (orc_reloc.hpp) over an oracle Volume."""
+
+    def __init__(self, vol: "Volume", depth, k):
+        d = np.ascontiguousarray(depth, dtype=np.float64)
+        h, w = d.shape
+        self.h = C.c_void_p()
+        _check(lib().orc_reloc_create(vol.h, _dp(d), w, h, C.byref(k), C.byref(self.h)))
+        n = C.c_int()
+        mu = C.c_double()
+        _check(lib().orc_reloc_info(self.h, C.byref(n), C.byref(mu), None, None))
+        self.n_voxels, self.mu = n.value, mu.value
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().orc_reloc_destroy(self.h)
+        except Exception:
+            pass
+
+    def arrays(self):
+        c = np.empty((self.n_voxels, 3))
+        v = np.empty(self.n_voxels)
+        n = C.c_int()
+        mu = C.c_double()
+        _check(lib().orc_reloc_info(self.h, C.byref(n), C.byref(mu), _dp(c), _dp(v)))
+        return c, v
+
+    def energy(self, pose, order=0, h=1e-8):
+        p = np.ascontiguousarray(pose, dtype=np.float64).reshape(12)
+        E = C.c_double()
+        g = np.zeros(6)
+        H = np.zeros((6, 6))
+        ov = C.c_long()
+        _check(lib().orc_reloc_energy(self.h, _dp(p), order, h, C.byref(E), _dp(g), _dp(H), C.byref(ov)))
+        return E.value, g, H, ov.value
+
+    def relocalize(self, init, method, cfg):
+        p = np.ascontiguousarray(init, dtype=np.float64).reshape(12)
+        out = np.empty(12)
+        res = _capi.RelocResult()
+        n = max(cfg.max_iterations, 1)
+        losses = np.zeros(n)
+        gn = np.zeros(n)
+        _check(lib().orc_relocalize(self.h, _dp(p), method, C.byref(cfg), _dp(out), C.byref(res), _dp(losses), _dp(gn)))
+        it = res.iterations
+        return out, it, bool(res.converged), res.final_loss, losses[:it].copy(), gn[:it].copy()
+
+
+def depth_cloud(depth, k, pose, stride=1):
+    d = np.ascontiguousarray(depth, dtype=np.float64)
+    h, w = d.shape
+    out = np.empty((max(w * h, 1), 3))
+    n = C.c_int()
+    _check(lib().orc_depth_cloud(_dp(d), w, h, C.byref(k), _dp(np.ascontiguousarray(pose, dtype=np.float64)), stride,
+                                 _dp(out), C.byref(n)))
+    return out[:n.value].copy()
+
+
+def nn_error(T, q, r):
+    q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 3)
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1, 3)
+    mean = C.c_double()
+    out = C.c_int()
+    _check(lib().orc_nn_error(_dp(np.ascontiguousarray(T, dtype=np.float64)), _dp(q), q.shape[0], _dp(r), r.shape[0],
+                              C.byref(mean), C.byref(out)))
+    return mean.value, bool(out.value)

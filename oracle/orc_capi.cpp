@@ -11,6 +11,7 @@
 
 #include "../include/csf_b200.h"
 #include "orc_pipeline.hpp"
+#include "orc_reloc.hpp"
 
 using namespace orc;
 
@@ -137,6 +138,7 @@ struct VolBase {
   virtual void view_scores(const double* poses, int n, const Intrinsics& k, double w0, double beta, double h,
                            double* scores, double* grads) const = 0;
   virtual void sample_points(const double* pts, int n, int grad, double* out, int32_t* valid) const = 0;
+  virtual RelocProblem reloc_problem(const Image<double>& query, const Intrinsics& k) const = 0;
 };
 
 template <int D, bool H>
@@ -199,6 +201,9 @@ struct Vol : VolBase {
   TrackResult track(const Image<double>& depth, const Pose& init, const Intrinsics& k, const IcpConfig& cfg,
                     bool canonical) const override {
     return track_frame(vol, depth, init, k, cfg, nullptr, canonical);
+  }
+  RelocProblem reloc_problem(const Image<double>& query, const Intrinsics& k) const override {
+    return make_reloc_problem(vol, query, k);
   }
   void sample_points(const double* pts, int n, int grad, double* out, int32_t* valid) const override {
     for (int i = 0; i < n; ++i) {
@@ -416,9 +421,109 @@ void write_stats(int n_frames, const std::vector<int>& it, const std::vector<int
     for (int j = 5; j < 8; ++j) stats[8 * f + j] = 0;
   }
 }
+
+Pose pose12(const double* p) {
+  Pose o;
+  for (int e = 0; e < 9; ++e) o.rotation(e / 3, e % 3) = p[e];
+  for (int e = 0; e < 3; ++e) o.translation[e] = p[9 + e];
+  return o;
+}
+void store_pose12(const Pose& o, double* p) {
+  for (int e = 0; e < 9; ++e) p[e] = o.rotation(e / 3, e % 3);
+  for (int e = 0; e < 3; ++e) p[9 + e] = o.translation[e];
+}
+std::vector<Vec3d> cloud_of(const double* p, int n) {
+  std::vector<Vec3d> o(n);
+  for (int i = 0; i < n; ++i) o[i] = Vec3d(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
+  return o;
+}
 }  // namespace
 
 extern "C" {
+
+// ---- relocalization (orc_reloc.hpp)
+int orc_reloc_create(void* v, const double* depth, int w, int h, const csf_intrinsics* k, void** out) {
+  return guard([&] {
+    Intrinsics kk = to_intr(*k);
+    kk.width = w;
+    kk.height = h;
+    *out = new RelocProblem(static_cast<VolBase*>(v)->reloc_problem(image_of(depth, w, h), kk));
+  });
+}
+void orc_reloc_destroy(void* p) { delete static_cast<RelocProblem*>(p); }
+int orc_reloc_info(void* p, int* n, double* mu, double* centers, double* values) {
+  return guard([&] {
+    const auto* r = static_cast<RelocProblem*>(p);
+    *n = static_cast<int>(r->voxel_centers.size());
+    *mu = r->mu;
+    if (centers)
+      for (int i = 0; i < *n; ++i)
+        for (int c = 0; c < 3; ++c) centers[3 * i + c] = r->voxel_centers[i][c];
+    if (values) std::memcpy(values, r->reference_values.data(), sizeof(double) * *n);
+  });
+}
+// order 0: E; 1: + g (6 Complex passes); 2: + H (21 Bicomplex passes)
+int orc_reloc_energy(void* p, const double* pose, int order, double h, double* E, double* g, double* H, long* overlap) {
+  return guard([&] {
+    const auto& r = *static_cast<RelocProblem*>(p);
+    const Pose ps = pose12(pose);
+    *E = reloc_energy<double>(r, ps, overlap);
+    if (order >= 1) {
+      const auto gg = reloc_gradient(r, ps, StepSize(h));
+      for (int i = 0; i < 6; ++i) g[i] = gg[i];
+    }
+    if (order >= 2) {
+      const auto hh = reloc_hessian(r, ps, StepSize(h));
+      for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) H[6 * i + j] = hh[i][j];
+    }
+  });
+}
+int orc_relocalize(void* p, const double* init, int method, const csf_reloc_cfg* cfg, double* out_pose,
+                   csf_reloc_result* res, double* losses, double* gnorms) {
+  return guard([&] {
+    RelocConfig c;
+    c.switch_relative = cfg->switch_relative;
+    c.switch_absolute = cfg->switch_absolute;
+    c.max_iterations = cfg->max_iterations;
+    c.step_tolerance = cfg->step_tolerance;
+    c.step = StepSize(cfg->h);
+    c.line_search.initial_step = cfg->ls_initial_step;
+    c.line_search.shrink = cfg->ls_shrink;
+    c.line_search.sufficient_decrease = cfg->ls_sufficient_decrease;
+    c.line_search.max_backtracks = cfg->ls_max_backtracks;
+    c.max_step = cfg->max_step;
+    c.min_overlap_ratio = cfg->min_overlap_ratio;
+    const RelocResult r = relocalize(*static_cast<RelocProblem*>(p), pose12(init),
+                                     method == CSF_RELOC_NEWTON ? RelocMethod::kNewton : RelocMethod::kGradientDescent, c);
+    store_pose12(r.pose, out_pose);
+    res->iterations = r.iterations;
+    res->converged = r.converged;
+    res->final_loss = r.final_loss;
+    for (int i = 0; i < r.iterations; ++i) {
+      if (losses) losses[i] = r.losses[i];
+      if (gnorms) gnorms[i] = r.gradient_norms[i];
+    }
+  });
+}
+int orc_depth_cloud(const double* depth, int w, int h, const csf_intrinsics* k, const double* pose, int stride,
+                    double* out, int* n) {
+  return guard([&] {
+    const auto c = depth_cloud(image_of(depth, w, h), to_intr(*k), pose12(pose), stride);
+    *n = static_cast<int>(c.size());
+    if (out)
+      for (std::size_t i = 0; i < c.size(); ++i)
+        for (int e = 0; e < 3; ++e) out[3 * i + e] = c[i][e];
+  });
+}
+int orc_nn_error(const double* transform, const double* query, int nq, const double* ref, int nr, double* mean,
+                 int* outlier) {
+  return guard([&] {
+    const NnError e = eval_nn_error(pose12(transform), cloud_of(query, nq), cloud_of(ref, nr));
+    *mean = e.mean;
+    *outlier = e.outlier;
+  });
+}
 
 int orc_sample_points(void* v, const double* pts, int n, int grad, double* out, int32_t* valid) {
   return guard([&] { static_cast<VolBase*>(v)->sample_points(pts, n, grad, out, valid); });

@@ -9,6 +9,7 @@ follow the reference:
     TsdfVolume / HashedVolume, surface_update, raycast         (tsdf.hpp:38-284)
     track_frame                                                (icp.hpp:130-133)
     Pipeline (the CSFD frame-derivative run)
+    RelocProblem, reloc_energy/gradient/hessian, relocalize   (reloc.hpp:35-138)
 
 Errors: CSF_EINVAL -> InvalidArgument (ValueError, std::invalid_argument),
 CSF_EDOMAIN -> DomainError (ArithmeticError, std::domain_error), everything
@@ -787,3 +788,13 @@ def synth_workload(config: int, n_frames: int, width: int = 0, height: int = 0, 
     gt = np.empty((n_frames, 12))
     c.check(c.lib.csf_synth_workload(c.h, config, n_frames, width, height, _fp(depth), _dp(gt), C.byref(k)))
     return depth, gt, k
+
+
+# ----------------------------------------------------------------------------- relocalization (reloc.hpp)
+from .reloc import (NnError, RelocMethod, RelocProblem, RelocResult, build_reference, default_reloc_cfg,  # noqa: E402
+                    depth_cloud, eval_nn_error, relocalize, reloc_energy, reloc_gradient, reloc_hessian, reloc_loss,
+                    select_reference_frames)
+
+__all__ += ["NnError", "RelocMethod", "RelocProblem", "RelocResult", "build_reference", "default_reloc_cfg",
+            "depth_cloud", "eval_nn_error", "relocalize", "reloc_energy", "reloc_gradient", "reloc_hessian",
+            "reloc_loss", "select_reference_frames"]

@@ -29,8 +29,10 @@ EXPORTS = (
     "csf_raycast", "csf_track_frame", "csf_icp_energy_derivs", "csf_view_scores", "csf_associate",
     "csf_linearized_step", "csf_pairwise_sum", "csf_pipeline_create", "csf_pipeline_destroy", "csf_pipeline_upload",
     "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_hessian", "csf_pipeline_run_host",
-    "csf_synth_workload",
+    "csf_synth_workload", "csf_default_reloc_cfg", "csf_reloc_create", "csf_reloc_destroy", "csf_reloc_info",
+    "csf_reloc_energy", "csf_relocalize", "csf_depth_cloud", "csf_eval_nn_error",
 )
+RELOC_GRADIENT_DESCENT, RELOC_NEWTON = 0, 1
 
 
 class Intrinsics(C.Structure):
@@ -62,6 +64,17 @@ class IcpCfg(C.Structure):
 class TrackResult(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("correspondences", C.c_int), ("pad", C.c_int),
                 ("final_loss", C.c_double)]
+
+
+class RelocCfg(C.Structure):
+    _fields_ = [("switch_relative", C.c_double), ("switch_absolute", C.c_double), ("max_iterations", C.c_int),
+                ("ls_max_backtracks", C.c_int), ("step_tolerance", C.c_double), ("ls_initial_step", C.c_double),
+                ("ls_shrink", C.c_double), ("ls_sufficient_decrease", C.c_double), ("h", C.c_double),
+                ("max_step", C.c_double), ("min_overlap_ratio", C.c_double)]
+
+
+class RelocResult(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("final_loss", C.c_double)]
 
 
 class PipelineCfg(C.Structure):
@@ -127,6 +140,14 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_default_volume_params": (None, [C.POINTER(VolumeParams)]),
         "csf_default_raycast_cfg": (None, [C.POINTER(RaycastCfg)]),
         "csf_default_icp_cfg": (None, [C.POINTER(IcpCfg)]),
+        "csf_default_reloc_cfg": (None, [C.POINTER(RelocCfg)]),
+        "csf_reloc_create": (ip, [vp, dp, ip, ip, C.POINTER(Intrinsics), C.POINTER(vp)]),
+        "csf_reloc_destroy": (ip, [vp]),
+        "csf_reloc_info": (ip, [vp, C.POINTER(C.c_int), dp, dp, dp]),
+        "csf_reloc_energy": (ip, [vp, dp, ip, C.c_double, dp, dp, dp, C.POINTER(C.c_longlong)]),
+        "csf_relocalize": (ip, [vp, dp, ip, C.POINTER(RelocCfg), dp, C.POINTER(RelocResult), dp, dp]),
+        "csf_depth_cloud": (ip, [vp, dp, ip, ip, C.POINTER(Intrinsics), dp, ip, dp, C.POINTER(C.c_int)]),
+        "csf_eval_nn_error": (ip, [vp, dp, dp, ip, dp, ip, dp, i32p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

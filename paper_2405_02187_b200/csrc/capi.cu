@@ -15,6 +15,8 @@
 #include <string>
 #include <sstream>
 #include <fstream>
+#include <limits>
+#include <memory>
 #include <vector>
 
 #include "../../include/csf_b200.h"
@@ -1877,5 +1879,266 @@ extern "C" int csf_synth_workload(csf_ctx ctx, int config, int n_frames, int wid
   const int rc = synth_workload(ctx->stream, config, n_frames, width, height, depth, gt, k, &err);
   ctx->launches += 1;
   if (rc) return fail(ctx, rc, err);
+  return CSF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// relocalization (reloc.hpp)
+// ---------------------------------------------------------------------------
+struct csf_reloc_s {
+  csf_ctx ctx = nullptr;
+  int n = 0, w = 0, h = 0;
+  double mu = 0.1;
+  DevBuf<double> centers, values, depth, k4;
+  ~csf_reloc_s() {
+    centers.release();
+    values.release();
+    depth.release();
+    k4.release();
+  }
+};
+
+extern "C" void csf_default_reloc_cfg(csf_reloc_cfg* c) {
+  if (!c) return;
+  c->switch_relative = 0.5;  // reloc.hpp:86-90
+  c->switch_absolute = -1.0;
+  c->max_iterations = 50;
+  c->step_tolerance = 1e-6;
+  c->ls_initial_step = 1.0;  // descent.hpp:16-21
+  c->ls_shrink = 0.5;
+  c->ls_sufficient_decrease = 1e-4;
+  c->ls_max_backtracks = 25;
+  c->h = 1e-8;  // csfd.hpp:16
+  c->max_step = 0.05;  // builder-defined safeguards
+  c->min_overlap_ratio = 0.9;
+}
+
+extern "C" int csf_reloc_create(csf_volume v, const double* depth, int w, int h, const csf_intrinsics* k,
+                                csf_reloc* out) {
+  if (!v || !depth || !k || !out || w <= 0 || h <= 0) return CSF_EINVAL;
+  csf_ctx ctx = v->ctx;
+  cudaSetDevice(ctx->device);
+  const long long nv = volume_voxels_now(v);
+  const double2* rw = v->hashed ? v->hash.rw : v->dense.rw;
+  const int* coords = v->hashed ? v->hash.coords : nullptr;
+  const double vs = v->hashed ? v->hash.vs : v->dense.vs;
+  const double origin[3] = {v->hashed ? v->hash.ox : v->dense.ox, v->hashed ? v->hash.oy : v->dense.oy,
+                            v->hashed ? v->hash.oz : v->dense.oz};
+  int n = 0;
+  int rc = reloc_flatten(ctx->stream, rw, nv, coords, v->dense.nx, v->dense.ny, vs, origin, nullptr, nullptr, &n);
+  if (rc == 1) return fail(ctx, CSF_EINVAL, "RelocProblem: volume too large to flatten");
+  if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "RelocProblem: flatten failed");
+  if (n == 0) return fail(ctx, CSF_EINVAL, "RelocProblem: reference has no observed voxels");
+  auto r = std::make_unique<csf_reloc_s>();
+  r->ctx = ctx;
+  r->w = w;
+  r->h = h;
+  r->mu = v->hashed ? v->hash.mu : v->dense.mu;
+  CUDA_TRY(ctx, r->centers.alloc(3 * static_cast<size_t>(n)));
+  CUDA_TRY(ctx, r->values.alloc(n));
+  CUDA_TRY(ctx, r->depth.alloc(static_cast<size_t>(w) * h));
+  CUDA_TRY(ctx, r->k4.alloc(4));
+  int n2 = 0;
+  rc = reloc_flatten(ctx->stream, rw, nv, coords, v->dense.nx, v->dense.ny, vs, origin, r->centers.p, r->values.p,
+                     &n2);
+  if (rc || n2 != n) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "RelocProblem: flatten failed");
+  r->n = n;
+  const double kk[4] = {k->fx, k->fy, k->cx, k->cy};
+  CUDA_TRY(ctx, cudaMemcpy(r->depth.p, depth, sizeof(double) * w * h, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(r->k4.p, kk, sizeof(kk), cudaMemcpyHostToDevice));
+  ctx->launches += 3;
+  *out = r.release();
+  return CSF_OK;
+}
+
+extern "C" int csf_reloc_destroy(csf_reloc r) {
+  if (!r) return CSF_EINVAL;
+  cudaSetDevice(r->ctx->device);
+  delete r;
+  return CSF_OK;
+}
+
+extern "C" int csf_reloc_info(csf_reloc r, int* n, double* mu, double* centers, double* values) {
+  if (!r) return CSF_EINVAL;
+  cudaSetDevice(r->ctx->device);
+  if (n) *n = r->n;
+  if (mu) *mu = r->mu;
+  if (centers) CUDA_TRY(r->ctx, cudaMemcpy(centers, r->centers.p, sizeof(double) * 3 * r->n, cudaMemcpyDeviceToHost));
+  if (values) CUDA_TRY(r->ctx, cudaMemcpy(values, r->values.p, sizeof(double) * r->n, cudaMemcpyDeviceToHost));
+  return CSF_OK;
+}
+
+// 0 ok; CSF_* on failure.  no_overlap -> ERUNTIME (reloc.hpp:65-66).
+static int reloc_eval(csf_reloc r, const double* pose, int order, double h, double* E, double* g, double* H,
+                      long long* overlap) {
+  csf_ctx ctx = r->ctx;
+  long long ov = 0;
+  const int rc = reloc_energy_derivs(ctx->stream, ctx->energy, r->centers.p, r->values.p, r->n, r->depth.p, r->w,
+                                     r->h, r->k4.p, r->mu, pose, order, h, E, g, H, &ov);
+  ctx->launches += 4;  // pose, terms, tree sub, tree top
+  if (rc == 5) return fail(ctx, CSF_ENOMEM, "reloc_energy: out of device memory");
+  if (rc) return fail(ctx, CSF_ECUDA, "reloc_energy: CUDA error");
+  if (overlap) *overlap = ov;
+  if (ov == 0) return fail(ctx, CSF_ERUNTIME, "relocalization energy: no overlapping voxels");
+  return CSF_OK;
+}
+
+extern "C" int csf_reloc_energy(csf_reloc r, const double* pose, int order, double h, double* E, double* g, double* H,
+                                long long* overlap) {
+  if (!r || !pose || !E || order < 0 || order > 2 || (order >= 1 && !g) || (order == 2 && !H)) return CSF_EINVAL;
+  if (order > 0 && (!(h > 0.0) || h > 1e-6)) return fail(r->ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
+  cudaSetDevice(r->ctx->device);
+  return reloc_eval(r, pose, order, h, E, g, H, overlap);
+}
+
+// relocalize (reloc.hpp:116-124; builder-defined body, DESIGN.md §3.9 and
+// oracle/orc_reloc.hpp): per-voxel work on the device, 6-vector logic here.
+extern "C" int csf_relocalize(csf_reloc r, const double* init, int method, const csf_reloc_cfg* cfg_in,
+                              double* out_pose, csf_reloc_result* res, double* losses, double* gnorms) {
+  if (!r || !init || !out_pose) return CSF_EINVAL;
+  if (method != CSF_RELOC_GRADIENT_DESCENT && method != CSF_RELOC_NEWTON)
+    return fail(r->ctx, CSF_EINVAL, "relocalize: unknown method");
+  csf_reloc_cfg cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    csf_default_reloc_cfg(&cfg);
+  if (!(cfg.h > 0.0) || cfg.h > 1e-6) return fail(r->ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
+  cudaSetDevice(r->ctx->device);
+  double pose[12];
+  std::copy(init, init + 12, pose);
+  double loss = 0.0;
+  long long cur_ov = 0, trial_ov = 0;
+  int rc = reloc_eval(r, pose, 0, cfg.h, &loss, nullptr, nullptr, &cur_ov);
+  if (rc) return rc;
+  const double threshold = cfg.switch_absolute >= 0.0 ? cfg.switch_absolute : cfg.switch_relative * loss;
+  LineSearch ls;
+  ls.initial_step = cfg.ls_initial_step;
+  ls.shrink = cfg.ls_shrink;
+  ls.sufficient_decrease = cfg.ls_sufficient_decrease;
+  ls.max_backtracks = cfg.ls_max_backtracks;
+  int iterations = 0;
+  bool converged = false;
+  // a trial pose with no overlapping voxel, or keeping fewer than
+  // min_overlap_ratio x the current overlap, counts as +inf
+  auto trial_loss = [&](const Vec6h& d, int* err) -> double {
+    double p[12];
+    std::copy(pose, pose + 12, p);
+    apply_increment_h(d, p);
+    double E = 0.0;
+    long long ov = 0;
+    const int e = reloc_energy_derivs(r->ctx->stream, r->ctx->energy, r->centers.p, r->values.p, r->n, r->depth.p,
+                                      r->w, r->h, r->k4.p, r->mu, p, 0, cfg.h, &E, nullptr, nullptr, &ov);
+    r->ctx->launches += 4;
+    if (e) {
+      *err = e;
+      return 0.0;
+    }
+    if (ov == 0) return std::numeric_limits<double>::infinity();
+    trial_ov = ov;
+    if (static_cast<double>(ov) < cfg.min_overlap_ratio * static_cast<double>(cur_ov))
+      return std::numeric_limits<double>::infinity();
+    return E;
+  };
+  int err = 0;
+  for (int it = 0; it < cfg.max_iterations; ++it) {
+    double gg[6], H[36];
+    const bool newton = method == CSF_RELOC_NEWTON && loss < threshold;
+    double e_lifted = 0.0;  // the real channel of the lifted pass == loss
+    rc = reloc_eval(r, pose, newton ? 2 : 1, cfg.h, &e_lifted, gg, H, nullptr);
+    if (rc) return rc;
+    Vec6h g, dir;
+    for (int i = 0; i < 6; ++i) g[i] = gg[i];
+    const double gn = norm6h(g);
+    const double sg = gn > 0.0 ? cfg.max_step / gn : 0.0;
+    for (int i = 0; i < 6; ++i) dir[i] = -g[i] * sg;
+    if (newton) {
+      double a[21];
+      for (int rr = 0; rr < 6; ++rr)
+        for (int c = 0; c <= rr; ++c) a[csfd::tri(rr, c)] = H[rr * 6 + c];
+      double m[6][6];
+      int tr[6];
+      if (csfd::ldlt6_factor_reg<double>(a, m, tr)) {
+        double ng[6], d[6];
+        for (int i = 0; i < 6; ++i) ng[i] = -g[i];
+        csfd::ldlt6_apply_reg<double>(m, tr, ng, d);
+        bool finite = true;
+        Vec6h nd;
+        for (int i = 0; i < 6; ++i) {
+          finite = finite && std::isfinite(d[i]);
+          nd[i] = d[i];
+        }
+        if (finite && dot6h(g, nd) < 0.0) {
+          const double nn = norm6h(nd);
+          if (nn > cfg.max_step) {
+            const double sn = cfg.max_step / nn;
+            for (int i = 0; i < 6; ++i) nd[i] = nd[i] * sn;
+          }
+          dir = nd;
+        }
+      }
+    }
+    const double slope = dot6h(g, dir);
+    if (!(slope < 0.0)) {
+      converged = gn == 0.0;
+      break;
+    }
+    double alpha = 0.0, lsl = 0.0;
+    const bool ok = backtracking(
+        [&](double al, int* e) {
+          Vec6h d;
+          for (int i = 0; i < 6; ++i) d[i] = al * dir[i];
+          return trial_loss(d, e);
+        },
+        loss, slope, ls, &alpha, &lsl, &err);
+    if (err) break;
+    if (!ok) break;
+    Vec6h step;
+    for (int i = 0; i < 6; ++i) step[i] = alpha * dir[i];
+    apply_increment_h(step, pose);
+    loss = lsl;
+    cur_ov = trial_ov;
+    if (losses) losses[iterations] = loss;
+    if (gnorms) gnorms[iterations] = gn;
+    ++iterations;
+    if (norm6h(step) < cfg.step_tolerance) {
+      converged = true;
+      break;
+    }
+  }
+  if (err == 5) return fail(r->ctx, CSF_ENOMEM, "relocalize: out of device memory");
+  if (err) return fail(r->ctx, CSF_ECUDA, "relocalize: CUDA error");
+  std::copy(pose, pose + 12, out_pose);
+  if (res) {
+    res->iterations = iterations;
+    res->converged = converged;
+    res->final_loss = loss;
+  }
+  return CSF_OK;
+}
+
+extern "C" int csf_depth_cloud(csf_ctx ctx, const double* depth, int w, int h, const csf_intrinsics* k,
+                               const double* c2w, int stride, double* points, int* n_points) {
+  if (!ctx || !depth || !k || !c2w || !n_points || w <= 0 || h <= 0) return CSF_EINVAL;
+  if (stride < 1) return fail(ctx, CSF_EINVAL, "depth_cloud: stride must be >= 1");
+  cudaSetDevice(ctx->device);
+  const double kk[4] = {k->fx, k->fy, k->cx, k->cy};
+  const int rc = depth_cloud_dev(ctx->stream, depth, w, h, kk, c2w, stride, points, n_points);
+  ctx->launches += 3;
+  if (rc == 5) return fail(ctx, CSF_ENOMEM, "depth_cloud: out of device memory");
+  if (rc) return fail(ctx, CSF_ECUDA, "depth_cloud: CUDA error");
+  return CSF_OK;
+}
+
+extern "C" int csf_eval_nn_error(csf_ctx ctx, const double* T, const double* q, int nq, const double* ref, int nr,
+                                 double* mean, int32_t* outlier) {
+  if (!ctx || !T || !mean || nq < 0 || nr < 0) return CSF_EINVAL;
+  if (nq == 0 || nr == 0 || !q || !ref) return fail(ctx, CSF_EINVAL, "eval_nn_error: empty cloud");
+  cudaSetDevice(ctx->device);
+  const int rc = nn_error_dev(ctx->stream, ctx->energy, T, q, nq, ref, nr, mean);
+  ctx->launches += 3;
+  if (rc == 5) return fail(ctx, CSF_ENOMEM, "eval_nn_error: out of device memory");
+  if (rc) return fail(ctx, CSF_ECUDA, "eval_nn_error: CUDA error");
+  if (outlier) *outlier = *mean > 0.1;
   return CSF_OK;
 }

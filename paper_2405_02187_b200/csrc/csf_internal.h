@@ -109,6 +109,18 @@ int linearized_tiles(cudaStream_t stream, const double* corrs, int n, const doub
 int tree_sum_slots(cudaStream_t stream, EnergyScratch& ws, const double* terms, int n, int C, double* out_host);
 
 
+// ---- reloc.cu: relocalization (reloc.hpp)
+// Observed voxels (W > 0) of rw [n_vox]: centers == nullptr counts only.
+// coords == nullptr: dense linear index over (nx, ny); else hashed pool coords.
+int reloc_flatten(cudaStream_t stream, const double2* rw, long long n_vox, const int* coords, int nx, int ny,
+                  double vs, const double* origin, double* centers, double* values, int* n_out);
+int reloc_energy_derivs(cudaStream_t stream, EnergyScratch& ws, const double* centers, const double* values, int n,
+                        const double* depth, int w, int h, const double* k4, double mu, const double* pose12,
+                        int order, double step, double* E, double* g, double* H, long long* overlap);
+int depth_cloud_dev(cudaStream_t stream, const double* depth_host, int w, int h, const double* k4,
+                    const double* pose12, int stride, double* out_host, int* n_out);
+int nn_error_dev(cudaStream_t stream, EnergyScratch& ws, const double* T12, const double* q, int nq, const double* r,
+                 int nr, double* mean);
 
 struct Launch {
   cudaStream_t stream;
