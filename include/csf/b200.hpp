@@ -124,6 +124,7 @@ class Volume {
   Volume(const Volume&) = delete;
   Volume& operator=(const Volume&) = delete;
   csf_volume get() const { return vol_; }
+  csf_ctx ctx() const { return ctx_; }
   int channels() const { return channels_; }
   size_t voxel_count() const {
     if (!hashed_) return n_;
@@ -255,6 +256,126 @@ inline std::array<std::array<double, 6>, 6> icp_hessian(Context& c, const std::v
   for (int r = 0; r < 6; ++r)
     for (int col = 0; col < 6; ++col) out[r][col] = hh[6 * r + col];
   return out;
+}
+
+// ---------------------------------------------------------------------------
+// reloc.hpp:35-138 — relocalization.  RelocProblem is device-resident; the
+// energy and its CSFD derivatives are one packed device pass each.
+// ---------------------------------------------------------------------------
+class RelocProblem {
+ public:
+  // reloc.hpp:44-45: throws std::invalid_argument if the reference has no
+  // observed voxels.
+  RelocProblem(const Volume& reference, const Image<double>& query, const csf_intrinsics& k)
+      : ctx_(reference.ctx()) {
+    check(ctx_, csf_reloc_create(reference.get(), query.data.data(), query.width, query.height, &k, &r_));
+    check(ctx_, csf_reloc_info(r_, &n_, &mu_, nullptr, nullptr));
+  }
+  ~RelocProblem() { csf_reloc_destroy(r_); }
+  RelocProblem(const RelocProblem&) = delete;
+  RelocProblem& operator=(const RelocProblem&) = delete;
+  csf_reloc get() const { return r_; }
+  csf_ctx ctx() const { return ctx_; }
+  int voxel_count() const { return n_; }
+  double mu() const { return mu_; }
+  // E (+ gradient, + Hessian [36]) at a camera->world pose; order 0/1/2
+  double energy(const std::array<double, 12>& pose, int order = 0, double h = 1e-8, double* g = nullptr,
+                double* hess = nullptr, long long* overlap = nullptr) const {
+    double e = 0.0, gg[6], hh[36];
+    check(ctx_, csf_reloc_energy(r_, pose.data(), order, h, &e, order >= 1 ? (g ? g : gg) : nullptr,
+                                 order == 2 ? (hess ? hess : hh) : nullptr, overlap));
+    return e;
+  }
+
+ private:
+  csf_ctx ctx_;
+  csf_reloc r_ = nullptr;
+  int n_ = 0;
+  double mu_ = 0.1;
+};
+
+// reloc.hpp:48-80
+inline double reloc_energy(const RelocProblem& p, const std::array<double, 12>& query_pose) {
+  return p.energy(query_pose);
+}
+inline double reloc_loss(const RelocProblem& p, const std::array<double, 12>& pose) { return p.energy(pose); }
+inline std::array<double, 6> reloc_gradient(const RelocProblem& p, const std::array<double, 12>& pose,
+                                            double h = 1e-8) {
+  std::array<double, 6> g{};
+  p.energy(pose, 1, h, g.data());
+  return g;
+}
+inline std::array<std::array<double, 6>, 6> reloc_hessian(const RelocProblem& p, const std::array<double, 12>& pose,
+                                                          double h = 1e-8) {
+  double hh[36], g[6];
+  p.energy(pose, 2, h, g, hh);
+  std::array<std::array<double, 6>, 6> out{};
+  for (int r = 0; r < 6; ++r)
+    for (int col = 0; col < 6; ++col) out[r][col] = hh[6 * r + col];
+  return out;
+}
+
+// reloc.hpp:82-124
+enum class RelocMethod { kGradientDescent = CSF_RELOC_GRADIENT_DESCENT, kNewton = CSF_RELOC_NEWTON };
+struct RelocResult {
+  std::array<double, 12> pose{};
+  int iterations = 0;
+  bool converged = false;
+  double final_loss = 0.0;
+  RelocMethod method = RelocMethod::kNewton;
+  std::vector<double> losses, gradient_norms;  // trace rows
+};
+inline csf_reloc_cfg default_reloc_config() {
+  csf_reloc_cfg c;
+  csf_default_reloc_cfg(&c);
+  return c;
+}
+inline RelocResult relocalize(const RelocProblem& p, const std::array<double, 12>& initial, RelocMethod method,
+                              const csf_reloc_cfg& cfg = default_reloc_config()) {
+  RelocResult r;
+  r.method = method;
+  const size_t n = static_cast<size_t>(cfg.max_iterations > 0 ? cfg.max_iterations : 1);
+  r.losses.resize(n);
+  r.gradient_norms.resize(n);
+  csf_reloc_result res{};
+  check(p.ctx(), csf_relocalize(p.get(), initial.data(), static_cast<int>(method), &cfg,
+                                                 r.pose.data(), &res, r.losses.data(), r.gradient_norms.data()));
+  r.iterations = res.iterations;
+  r.converged = res.converged != 0;
+  r.final_loss = res.final_loss;
+  r.losses.resize(res.iterations);
+  r.gradient_norms.resize(res.iterations);
+  return r;
+}
+
+// reloc.hpp:126-129
+inline std::vector<std::array<double, 3>> depth_cloud(Context& c, const Image<double>& depth, const csf_intrinsics& k,
+                                                      const std::array<double, 12>& camera_to_world, int stride = 1) {
+  const int s = stride > 0 ? stride : 1;
+  std::vector<double> buf(3 * static_cast<size_t>((depth.width + s - 1) / s) * ((depth.height + s - 1) / s) + 3);
+  int n = 0;
+  check(c.get(), csf_depth_cloud(c.get(), depth.data.data(), depth.width, depth.height, &k, camera_to_world.data(),
+                                 stride, buf.data(), &n));
+  std::vector<std::array<double, 3>> out(n);
+  for (int i = 0; i < n; ++i) out[i] = {buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]};
+  return out;
+}
+
+// reloc.hpp:131-138
+struct NnError {
+  double mean = 0.0;
+  bool outlier = false;
+};
+inline NnError eval_nn_error(Context& c, const std::array<double, 12>& transform,
+                             const std::vector<std::array<double, 3>>& query,
+                             const std::vector<std::array<double, 3>>& reference) {
+  NnError e;
+  int32_t out = 0;
+  check(c.get(), csf_eval_nn_error(c.get(), transform.data(), query.empty() ? nullptr : query[0].data(),
+                                   static_cast<int>(query.size()), reference.empty() ? nullptr : reference[0].data(),
+                                   static_cast<int>(reference.size()), &e.mean, &out));
+  e.outlier = out != 0;
+  return e;
 }
 
 // The CSFD frame-derivative run; extension of the reference

@@ -7,6 +7,7 @@
 
 #include "csf/b200.hpp"
 #include "orc_pipeline.hpp"
+#include "orc_reloc.hpp"
 
 namespace B = csf::b200;
 
@@ -242,6 +243,43 @@ int main() {
     }
     CHECK(same);
     std::printf("ok   icp_loss / icp_gradient / icp_hessian bit-identical to the restatement (E %.6e)\n", e);
+  }
+
+  {  // reloc.hpp:48-124 — reloc_energy / gradient / Hessian and relocalize against the restatement
+    orc::VolumeParams op;
+    op.dims[0] = op.dims[1] = op.dims[2] = 64;
+    op.voxel_size = 0.02;
+    op.origin = orc::Vec3d(-0.63, -0.63, -0.63);
+    op.mu = 0.1;
+    orc::TsdfVolumeT<double> ref_o(op);
+    for (const orc::Pose& p : poses)
+      orc::surface_update(ref_o, orc::render_depth(sphere, p, ko), orc::pose_cast<double>(p), ko);
+    const orc::Image<double> q = orc::render_depth(sphere, poses[3], ko);
+    const orc::RelocProblem po = orc::make_reloc_problem(ref_o, q, ko);
+    const B::RelocProblem pg(fused, img(q), k);
+    CHECK(pg.voxel_count() == static_cast<int>(po.voxel_centers.size()));
+    orc::Vec6<double> xi{0.02, -0.01, 0.015, 0.01, 0.02, -0.015};
+    const orc::Pose init = orc::apply_increment(xi, poses[3]);
+    CHECK(B::reloc_loss(pg, arr(init)) == orc::reloc_loss(po, init));
+    const auto g = B::reloc_gradient(pg, arr(init));
+    const auto h = B::reloc_hessian(pg, arr(init));
+    const auto go = orc::reloc_gradient(po, init);
+    const auto ho = orc::reloc_hessian(po, init);
+    bool same = true;
+    for (int i = 0; i < 6; ++i) {
+      same = same && g[i] == go[i];
+      for (int j = 0; j < 6; ++j) same = same && h[i][j] == ho[i][j];
+    }
+    CHECK(same);
+    const B::RelocResult rg = B::relocalize(pg, arr(init), B::RelocMethod::kNewton);
+    const orc::RelocResult ro = orc::relocalize(po, init, orc::RelocMethod::kNewton);
+    CHECK(rg.iterations == ro.iterations && rg.converged == ro.converged && rg.final_loss == ro.final_loss);
+    CHECK(rg.pose == arr(ro.pose));
+    // (a lone sphere fixes the pose only up to rotations about its centre,
+    // so the check is descent, not recovery; tests/test_reloc.py checks recovery)
+    CHECK(rg.iterations > 0 && rg.final_loss < orc::reloc_loss(po, init));
+    std::printf("ok   reloc energy/gradient/Hessian and Newton relocalize bit-identical (%d iterations, loss %.3e)\n",
+                rg.iterations, rg.final_loss);
   }
 
   {  // error behaviour: invalid arguments throw std::invalid_argument
