@@ -38,6 +38,9 @@ directions = 6 first-frame twist + 4 intrinsics + 6 x 9 keyframe twists
 each rank runs its 8-direction share (rank r of the 8-way split), so the
 per-GPU work is fixed ("weak"); units = frames x directions over all ranks.
 
+--workload reloc: camera relocalization on the config-2
+scene — 8 queries, eta-switched Newton; relocalizations/s (bench_reloc.py).
+
 --workload config3: BASELINE config 3 — the same VGA scene, 30 frames, the
 full 10x10 Hessian as 55 second-order parameter pairs (one reference
 Bicomplex per pair, packed as channel slots of one evaluation).  Units =
@@ -77,7 +80,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5"], default="config2")
+    ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5", "reloc"], default="config2")
     ap.add_argument("--frames", type=int, default=0, help="0 = the workload's frame count (100 / 30)")
     ap.add_argument("--cpu-frames", type=int, default=5, help="CPU-baseline sample: frames")
     ap.add_argument("--cpu-dirs", type=int, default=2, help="CPU-baseline sample: directions (one pass each)")
@@ -425,6 +428,13 @@ def run_config5(args):
 
 def main():
     args = parse()
+    if args.workload == "reloc":
+        import bench_reloc
+        if args.impl == "reference":
+            bench_reloc.run_reference(args)
+        else:
+            bench_reloc.run(args, measured_peak, Clocks)
+        return
     if args.workload == "config5" and args.impl != "reference":
         run_config5(args)
         return

@@ -1,0 +1,215 @@
+"""bench.py --workload reloc: camera relocalization (SURVEY §8(f) row 2,
+the paper's §5.2 task) on the config-2 scene.
+
+Setup (untimed): 100 VGA frames of the seeded procedural room; 8 query
+frames (every 12th from frame 5); each query's initial pose = ground truth
+perturbed by 3 deg / 5 cm (seeded; the SPEC.md:573 perturbation); reference
+model = the 10 frames nearest the initial estimate (select_reference_frames,
+the query frame excluded) fused into a hashed 5 mm TSDF at their poses
+(build_reference's rule); the RelocProblem (observed voxels flattened in HBM).
+
+Step: relocalize all 8 queries with the eta-switched Newton method (default
+RelocConfig).  value = relocalizations/s with the problems resident; e2e =
+the public API from host buffers (RelocProblem creation from the query depth
++ relocalize + pose read-back) per query.  Rooflines per energy-pass kind
+(loss / gradient / Hessian): algorithmic bytes per pass = n_voxels x
+(24 B centre + 8 B value + 2 x 8 C B terms written and read by the tree) for
+C slots (1 / 7 / 64), HBM-bound.  cpu_baseline: the oracle's relocalize
+of query 0 capped at 2 iterations (its gradient, Hessian and line-search
+passes on all host threads), extrapolated by the device run's mean
+iterations per query — stated in `sample`.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+import numpy as np
+
+QUERIES = list(range(5, 100, 12))  # 8 query frames
+
+
+def _perturb(pose12, deg, cm, rng):
+    a = rng.normal(size=3)
+    a *= np.deg2rad(deg) / np.linalg.norm(a)
+    t = rng.normal(size=3)
+    t *= cm / 100.0 / np.linalg.norm(t)
+    th = np.linalg.norm(a)
+    K = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]]) / th
+    R = np.eye(3) + np.sin(th) * K + (1 - np.cos(th)) * K @ K
+    out = np.empty(12)
+    out[:9] = (R @ pose12[:9].reshape(3, 3)).reshape(9)
+    out[9:] = R @ pose12[9:] + t
+    return out
+
+
+def setup(csf, ctx, n_frames=100):
+    depth, gt, k = csf.synth_workload(2, n_frames, ctx=ctx)
+    rng = np.random.default_rng(11)
+    items = []
+    for q in QUERIES:
+        init = _perturb(gt[q], 3.0, 5.0, rng)
+        cand = [i for i in range(n_frames) if i != q]
+        sel = [cand[i] for i in csf.select_reference_frames([gt[i] for i in cand], init, 10)]
+        vol = csf.HashedVolume(0.005, (0.0, 0.0, 0.0), 0.025, 128.0, 20, 1 << 18, channels=0, ctx=ctx)
+        for i in sel:
+            vol.surface_update(depth[i].astype(np.float64), gt[i], k)
+        items.append((q, init, sel, vol))
+    return depth, gt, k, items
+
+
+def cpu_sample(depth, gt, k, items, cfg, mean_iters):
+    """The oracle's relocalize of query 0 capped at 2 Newton-method iterations
+    (gradient passes, plus the Hessian once below the switch threshold, and
+    the line-search loss passes), all host threads; extrapolated per query by
+    `mean_iters`."""
+    from oracle import orc
+    from paper_2405_02187_b200 import capi
+    q, init, sel, _ = items[0]
+    hp = capi.HashParams(0.005, (capi.C.c_double * 3)(0, 0, 0), 0.025, 128.0, 20, 1 << 18)
+    vo = orc.Volume(hp, 0, True)
+    for i in sel:
+        vo.surface_update(depth[i].astype(np.float64), gt[i].reshape(12, 1), np.array([[k.fx], [k.fy], [k.cx], [k.cy]]))
+    ro = orc.Reloc(vo, depth[q].astype(np.float64), k)
+    c2 = capi.RelocCfg.from_buffer_copy(cfg)
+    c2.max_iterations = 2
+    t1 = time.perf_counter()
+    _, it2, _, _, _, _ = ro.relocalize(init, capi.RELOC_NEWTON, c2)
+    secs = time.perf_counter() - t1
+    per_iter = secs / max(it2, 1)
+    mean_it = max(mean_iters, 1.0)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": 1.0 / (per_iter * mean_it), "unit": "relocalizations/s", "cores": cores, "kind": "port",
+            "sample": f"oracle relocalize of query 0 capped at 2 iterations ({it2} taken in {secs:.2f} s; one "
+                      f"Complex pass per gradient direction, 21 Bicomplex passes per Hessian), extrapolated by "
+                      f"{mean_it:.1f} iterations/query"}
+
+
+def run_reference(args, mean_iters=8.0):
+    """--impl reference --workload reloc: the oracle port's relocalization
+    rate (rank 0; other ranks exit)."""
+    import paper_2405_02187_b200 as csf
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    ctx = csf.Context(int(os.environ.get("LOCAL_RANK", "0")))
+    depth, gt, k, items = setup(csf, ctx)
+    cfg = csf.default_reloc_cfg()
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(max(args.steps, 1)):
+        cb = cpu_sample(depth, gt, k, items, cfg, mean_iters)
+        vals.append(cb["value"])
+    secs = time.perf_counter() - t0
+    v = float(np.median(vals))
+    cb["value"] = v
+    print(json.dumps({"impl": "reference", "metric": "camera relocalizations/s (eta-switched Newton, CSFD gradient "
+                      "+ Hessian of reloc_energy)", "value": v, "unit": "relocalizations/s", "n_gpus": 1,
+                      "steps": args.steps, "warmup": 0, "ms_per_step": 1000.0 * secs / max(args.steps, 1),
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                      "data": "synthetic", "config": {"workload": "reloc"}, "cpu_baseline": cb,
+                      "e2e": {"value": v, "unit": "relocalizations/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def run(args, measured_peak, Clocks):
+    import torch
+    import paper_2405_02187_b200 as csf
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    torch.cuda.set_device(local)
+    if rank != 0:  # replicas only: queries are independent; rank 0 reports
+        return
+    ctx = csf.Context(local)
+    depth, gt, k, items = setup(csf, ctx)
+    probs = [csf.RelocProblem(vol, depth[q].astype(np.float64), k) for q, _, _, vol in items]
+    cfg = csf.default_reloc_cfg()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+
+    def step():
+        return [csf.relocalize(p, init, csf.RelocMethod.NEWTON, cfg) for p, (_, init, _, _) in zip(probs, items)]
+
+    for _ in range(max(args.warmup, 0)):
+        res = step()
+    ctx.synchronize()
+    clocks = Clocks(local)
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    e1.record(stream)
+    ctx.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count - l0
+    clk = clocks.stop()
+    # e2e: the public API from host buffers (problem creation incl. the query depth H2D)
+    host_depth = [np.ascontiguousarray(depth[q].astype(np.float64)) for q, _, _, _ in items]
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for (q, init, _, vol), d in zip(items, host_depth):
+            p = csf.RelocProblem(vol, d, k)
+            r = csf.relocalize(p, init, csf.RelocMethod.NEWTON, cfg)
+            p.close()
+    ctx.synchronize()
+    t_e2e = time.perf_counter() - t0
+    # profiled pass
+    ctx.profile(True)
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        step()
+    p1.record(stream)
+    ctx.synchronize()
+    prof_ms = p0.elapsed_time(p1)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+
+    nq = len(items)
+    value = nq * args.steps / (ms / 1000.0)
+    nvox = np.array([p.n_voxels for p in probs], dtype=np.float64)
+    peak, peak_src = measured_peak()
+    slots = {"reloc_loss": 1, "reloc_grad": 7, "reloc_hess": 64}
+    rooflines = {}
+    for cat, C in slots.items():
+        cat_ms, cat_n = prof.get(cat, (0.0, 0))
+        if cat_n == 0:
+            continue
+        b = float(nvox.mean()) * (24 + 8 + 2 * 8 * C)
+        avg = cat_ms / cat_n
+        ach = b / (avg / 1000.0) / 1e9
+        rooflines[cat] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                          "traffic": None, "kernel": cat, "avg_launch_ms": avg, "launches": cat_n,
+                          "share_of_step": cat_ms / prof_ms, "algorithmic_bytes_per_launch": b,
+                          "bytes_model": f"per energy pass: mean observed voxels x (24 B centre + 8 B value + "
+                                         f"2 x 8 x {C} B terms write+read)", "peak_source": peak_src}
+    roofline = max(rooflines.values(), key=lambda r: r["share_of_step"]) if rooflines else None
+    iters = [r.iterations for r in res]
+    terr = [float(np.linalg.norm(r.pose[9:] - gt[q][9:])) for r, (q, _, _, _) in zip(res, items)]
+    unit = "relocalizations/s"
+    line = {
+        "metric": "camera relocalizations/s (eta-switched Newton, CSFD gradient + Hessian of reloc_energy)",
+        "value": value, "unit": unit, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded procedural room; BASELINE config 2 shapes)",
+        "config": {"workload": "reloc: 8 VGA queries of the config-2 scene, (3 deg, 5 cm) initial perturbation, "
+                               "reference = 10 nearest frames fused at 5 mm (hashed)",
+                   "queries": nq, "mean_observed_voxels": float(nvox.mean()), "parallelism": "replicas only",
+                   "l2": "observed-voxel arrays + Hessian terms (GBs) >> L2"},
+        "e2e": {"value": nq * args.steps / t_e2e, "unit": unit,
+                "h2d_bytes_per_step": int(sum(d.nbytes for d in host_depth) + nq * 12 * 8),
+                "d2h_bytes_per_step": int(nq * 12 * 8)},
+        "gpu_launches": int(launches), "roofline": roofline, "roofline_by_kernel": rooflines, "clocks": clk,
+        "kernel_ms_per_step": {c: v[0] / args.steps for c, v in prof.items() if v[1]},
+        "iterations": iters, "translation_error_m": terr,
+    }
+    if not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_sample(depth, gt, k, items, cfg, float(np.mean(iters)))
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)

@@ -52,10 +52,11 @@ struct Profiler {
 };
 
 enum ProfCat {
-  kPBilateral = 0, kPDownsample, kPRaycast, kPRaycastLift, kPIcpReduce, kPIcpSolve, kPAlloc, kPIntegrate, kPMisc, kPN
+  kPBilateral = 0, kPDownsample, kPRaycast, kPRaycastLift, kPIcpReduce, kPIcpSolve, kPAlloc, kPIntegrate, kPMisc,
+  kPRelocLoss, kPRelocGrad, kPRelocHess, kPN
 };
 static const char* kProfNames[kPN] = {"bilateral", "downsample", "raycast", "raycast_lift", "icp", "icp_solve",
-                                      "allocate", "integrate", "misc"};
+                                      "allocate", "integrate", "misc", "reloc_loss", "reloc_grad", "reloc_hess"};
 
 struct csf_ctx_s {
   int device = 0;
@@ -1973,6 +1974,7 @@ static int reloc_eval(csf_reloc r, const double* pose, int order, double h, doub
                       long long* overlap) {
   csf_ctx ctx = r->ctx;
   long long ov = 0;
+  ProfScope ps(ctx, order == 0 ? kPRelocLoss : order == 1 ? kPRelocGrad : kPRelocHess);
   const int rc = reloc_energy_derivs(ctx->stream, ctx->energy, r->centers.p, r->values.p, r->n, r->depth.p, r->w,
                                      r->h, r->k4.p, r->mu, pose, order, h, E, g, H, &ov);
   ctx->launches += 4;  // pose, terms, tree sub, tree top
@@ -2027,6 +2029,7 @@ extern "C" int csf_relocalize(csf_reloc r, const double* init, int method, const
     apply_increment_h(d, p);
     double E = 0.0;
     long long ov = 0;
+    ProfScope ps(r->ctx, kPRelocLoss);
     const int e = reloc_energy_derivs(r->ctx->stream, r->ctx->energy, r->centers.p, r->values.p, r->n, r->depth.p,
                                       r->w, r->h, r->k4.p, r->mu, p, 0, cfg.h, &E, nullptr, nullptr, &ov);
     r->ctx->launches += 4;

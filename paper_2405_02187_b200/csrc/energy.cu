@@ -17,9 +17,10 @@
 //                    the linearized solver's loss_after)
 //
 // The tree is evaluated exactly in parallel: every node above depth d0 is
-// internal (its size exceeds 8), so the 2^d0 depth-d0 subtrees are summed
-// independently (recursively, one thread each) and combined pairwise level
-// by level — the same additions, in the same association, as the recursion.
+// internal (its size exceeds 8), so the 2^d0 depth-d0 subtrees (33..64 terms
+// each) are summed independently (recursively, one thread each) and combined
+// pairwise level by level in aligned 1024-node CTA reductions — the same
+// additions, in the same association, as the recursion.
 // The Newton / gradient trackers turn these derivative channels into the
 // real pose step, so this translation unit evaluates every channel division
 // as the reference's per-channel quotient (csfd.hpp:57, 114-121) — the real
@@ -129,16 +130,19 @@ __global__ void k_tree_sub(const double* __restrict__ terms, int n, int d0, doub
 }
 
 // Internal nodes above depth d0 (each has exactly two children): combine
-// left + right level by level; pairwise_sum adds the result to init = 0.
-__global__ void __launch_bounds__(512) k_tree_top(const double* __restrict__ sub, int d0, double* __restrict__ out) {
+// left + right level by level.  One CTA reduces r = 2^k consecutive nodes of
+// one slot (a complete, aligned subtree) to one; `last` adds the result to
+// pairwise_sum's init = 0.  in [C][m], out [C][m / r].
+__global__ void __launch_bounds__(512) k_tree_top(const double* __restrict__ in, int m, int r, int last,
+                                                  double* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
   __shared__ double v[1024];
-  const int nsub = 1 << d0;
-  const int slot = blockIdx.x;
-  for (int k = threadIdx.x; k < nsub; k += blockDim.x) v[k] = sub[static_cast<long long>(slot) * nsub + k];
+  const int slot = blockIdx.y;
+  const double* src = in + static_cast<long long>(slot) * m + static_cast<long long>(blockIdx.x) * r;
+  for (int k = threadIdx.x; k < r; k += blockDim.x) v[k] = src[k];
   __syncthreads();
-  for (int w = nsub; w > 1; w >>= 1) {
+  for (int w = r; w > 1; w >>= 1) {
     double a = 0.0;
     const int k = threadIdx.x;
     if (k < w / 2) a = v[2 * k] + v[2 * k + 1];
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(512) k_tree_top(const double* __restrict__ sub
     if (k < w / 2) v[k] = a;
     __syncthreads();
   }
-  if (threadIdx.x == 0) out[slot] = 0.0 + v[0];
+  if (threadIdx.x == 0) out[static_cast<long long>(slot) * (m / r) + blockIdx.x] = last ? 0.0 + v[0] : v[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -334,6 +338,36 @@ static void chk(const char* what) {
   if (e != cudaSuccess) std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
 }
 
+// pairwise_sum (diff.hpp:16-37) of every slot of terms [C][n] (n > 0) into
+// out [C] (device).  Depth d0 is chosen so every depth-d0 subtree holds
+// 33..64 terms (all nodes above are internal: their size exceeds 8), giving
+// 2^d0 independent subtree sums per slot — enough threads to stream the
+// terms at HBM rate — then aligned 1024-node CTA reductions to the root.
+// sub: scratch of tree_scratch_doubles(n, C).
+static int tree_depth(int n) {
+  int d0 = 0;
+  while (d0 < 20 && (n >> d0) > 64) ++d0;
+  return d0;
+}
+static size_t tree_scratch_doubles(int n, int C) {
+  const size_t nsub = size_t(1) << tree_depth(n);
+  return static_cast<size_t>(C) * (nsub + nsub / 1024 + 1);
+}
+static void launch_tree(cudaStream_t stream, const double* terms, int n, int C, double* sub, double* out) {
+  const int d0 = tree_depth(n);
+  const int nsub = 1 << d0;
+  launch_pdl(k_tree_sub, dim3((nsub + 127) / 128, C), dim3(128), 0, stream, terms, n, d0, sub);
+  if (nsub <= 1024) {
+    launch_pdl(k_tree_top, dim3(1, C), dim3(512), 0, stream, static_cast<const double*>(sub), nsub, nsub, 1, out);
+  } else {
+    double* mid = sub + static_cast<size_t>(C) * nsub;
+    launch_pdl(k_tree_top, dim3(nsub / 1024, C), dim3(512), 0, stream, static_cast<const double*>(sub), nsub, 1024, 0,
+               mid);
+    const int m = nsub / 1024;
+    launch_pdl(k_tree_top, dim3(1, C), dim3(512), 0, stream, static_cast<const double*>(mid), m, m, 1, out);
+  }
+}
+
 // Energy (and, for order > 0, the 21-pair CSFD derivatives) of n device
 // correspondences.  order 0: energy only; 1: + gradient (6 diagonal pairs);
 // 2: + Hessian (21 pairs).  Scratch is grown in `ws`.  Synchronous: results
@@ -362,9 +396,6 @@ int icp_energy_derivs(cudaStream_t stream, EnergyScratch& ws, const double* corr
     if (H) std::fill(H, H + 36, 0.0);
     return 0;
   }
-  int d0 = 0;
-  while (d0 < 10 && (n >> d0) > 8) ++d0;
-  const int nsub = 1 << d0;
   auto grow = [&](double*& p, size_t& cap, size_t need) -> cudaError_t {
     if (need <= cap && p) return cudaSuccess;
     if (p) cudaFree(p);
@@ -374,7 +405,7 @@ int icp_energy_derivs(cudaStream_t stream, EnergyScratch& ws, const double* corr
     return e;
   };
   cudaError_t e = grow(ws.terms, ws.terms_cap, static_cast<size_t>(C) * n);
-  if (e == cudaSuccess) e = grow(ws.sub, ws.sub_cap, static_cast<size_t>(C) * nsub);
+  if (e == cudaSuccess) e = grow(ws.sub, ws.sub_cap, tree_scratch_doubles(n, C));
   if (e == cudaSuccess) e = grow(ws.small, ws.small_cap, 12 * 64 + 64 + 64);
   if (e == cudaSuccess && !ws.pairs) e = cudaMalloc(&ws.pairs, sizeof(int) * 64);
   if (e != cudaSuccess) return 5;
@@ -404,9 +435,7 @@ int icp_energy_derivs(cudaStream_t stream, EnergyScratch& ws, const double* corr
     launch_pdl(k_energy_terms<B<1>>, dim3((n + 127) / 128, P), dim3(128), 0, stream, corrs, n,
                static_cast<const double*>(T), P, ws.terms);
   }
-  launch_pdl(k_tree_sub, dim3((nsub + 127) / 128, C), dim3(128), 0, stream, static_cast<const double*>(ws.terms), n,
-             d0, ws.sub);
-  launch_pdl(k_tree_top, dim3(C), dim3(512), 0, stream, static_cast<const double*>(ws.sub), d0, out);
+  launch_tree(stream, static_cast<const double*>(ws.terms), n, C, ws.sub, out);
   chk("icp_energy");
   std::vector<double> o(C);
   e = cudaMemcpyAsync(o.data(), out, sizeof(double) * C, cudaMemcpyDeviceToHost, stream);
@@ -435,15 +464,13 @@ int tree_sum_slots(cudaStream_t stream, EnergyScratch& ws, const double* terms, 
     std::fill(out_host, out_host + C, 0.0);
     return 0;
   }
-  int d0 = 0;
-  while (d0 < 10 && (n >> d0) > 8) ++d0;
-  const int nsub = 1 << d0;
-  if (ws.sub_cap < static_cast<size_t>(C) * nsub || !ws.sub) {
+  const size_t need = tree_scratch_doubles(n, C);
+  if (ws.sub_cap < need || !ws.sub) {
     if (ws.sub) cudaFree(ws.sub);
     ws.sub = nullptr;
     ws.sub_cap = 0;
-    if (cudaMalloc(&ws.sub, sizeof(double) * C * nsub) != cudaSuccess) return 5;
-    ws.sub_cap = static_cast<size_t>(C) * nsub;
+    if (cudaMalloc(&ws.sub, sizeof(double) * need) != cudaSuccess) return 5;
+    ws.sub_cap = need;
   }
   if (ws.out_cap < static_cast<size_t>(C) || !ws.out) {
     if (ws.out) cudaFree(ws.out);
@@ -453,8 +480,7 @@ int tree_sum_slots(cudaStream_t stream, EnergyScratch& ws, const double* terms, 
     ws.out_cap = static_cast<size_t>(C);
   }
   double* out = ws.out;
-  launch_pdl(k_tree_sub, dim3((nsub + 127) / 128, C), dim3(128), 0, stream, terms, n, d0, ws.sub);
-  launch_pdl(k_tree_top, dim3(C), dim3(512), 0, stream, static_cast<const double*>(ws.sub), d0, out);
+  launch_tree(stream, terms, n, C, ws.sub, out);
   chk("tree_sum");
   if (cudaMemcpyAsync(out_host, out, sizeof(double) * C, cudaMemcpyDeviceToHost, stream) != cudaSuccess) return 4;
   if (cudaStreamSynchronize(stream) != cudaSuccess) return 4;
