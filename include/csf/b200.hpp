@@ -378,6 +378,59 @@ inline NnError eval_nn_error(Context& c, const std::array<double, 12>& transform
   return e;
 }
 
+// ---------------------------------------------------------------------------
+// dataset.hpp:17-36 — on-disk formats (host file I/O; std::runtime_error)
+// ---------------------------------------------------------------------------
+namespace detail {
+inline void io_check(int rc) {
+  if (rc == CSF_OK) return;
+  if (rc == CSF_EINVAL) throw std::invalid_argument("csf_b200: invalid argument");
+  throw std::runtime_error(csf_io_last_error());
+}
+}  // namespace detail
+inline void write_depth_png16(const std::string& path, const Image<double>& depth, double scale) {
+  detail::io_check(csf_write_depth_png16(path.c_str(), depth.data.data(), depth.width, depth.height, scale));
+}
+inline Image<double> read_depth_png16(const std::string& path, double scale) {
+  int w = 0, h = 0;
+  detail::io_check(csf_read_depth_png16(path.c_str(), scale, nullptr, &w, &h));
+  Image<double> out(w, h);
+  detail::io_check(csf_read_depth_png16(path.c_str(), scale, out.data.data(), &w, &h));
+  return out;
+}
+inline csf_intrinsics read_intrinsics(const std::string& path) {
+  csf_intrinsics k{};
+  detail::io_check(csf_read_intrinsics(path.c_str(), &k));
+  return k;
+}
+inline void write_intrinsics(const std::string& path, const csf_intrinsics& k) {
+  detail::io_check(csf_write_intrinsics(path.c_str(), &k));
+}
+struct TrajectoryEntry {
+  double timestamp = 0.0;
+  std::array<double, 12> pose{};
+};
+inline std::vector<TrajectoryEntry> read_trajectory(const std::string& path) {
+  int n = 0;
+  detail::io_check(csf_read_trajectory(path.c_str(), nullptr, nullptr, 0, &n));
+  std::vector<double> ts(n), ps(12 * static_cast<size_t>(n));
+  detail::io_check(csf_read_trajectory(path.c_str(), ts.data(), ps.data(), n, &n));
+  std::vector<TrajectoryEntry> out(n);
+  for (int i = 0; i < n; ++i) {
+    out[i].timestamp = ts[i];
+    for (int e = 0; e < 12; ++e) out[i].pose[e] = ps[12 * i + e];
+  }
+  return out;
+}
+inline void write_trajectory(const std::string& path, const std::vector<TrajectoryEntry>& traj) {
+  std::vector<double> ts, ps;
+  for (const auto& e : traj) {
+    ts.push_back(e.timestamp);
+    ps.insert(ps.end(), e.pose.begin(), e.pose.end());
+  }
+  detail::io_check(csf_write_trajectory(path.c_str(), ts.data(), ps.data(), static_cast<int>(traj.size())));
+}
+
 // The CSFD frame-derivative run; extension of the reference
 // API: gradient over first-order directions, or Hessian entries over
 // bicomplex pairs (csfd_hessian's pattern applied to the whole frame loop).

@@ -335,6 +335,22 @@ int csf_depth_cloud(csf_ctx ctx, const double* depth, int w, int h, const csf_in
 int csf_eval_nn_error(csf_ctx ctx, const double* transform, const double* query, int n_query, const double* reference,
                       int n_reference, double* mean, int32_t* outlier);
 
+/* ---- on-disk formats: dataset.hpp / dataset.cpp -------
+ * Host-side file I/O (no context needed).  Failures return CSF_ERUNTIME
+ * (std::runtime_error) with the message in csf_io_last_error(). */
+const char* csf_io_last_error(void);
+/* dataset.cpp:30-68 — 16-bit grayscale PNG, q = round(d*scale) if 1..65535 else 0 */
+int csf_write_depth_png16(const char* path, const double* depth, int w, int h, double scale);
+/* dataset.cpp:70-107 — depth [h][w] = v/scale (0 where v = 0); depth NULL: size only */
+int csf_read_depth_png16(const char* path, double scale, double* depth, int* w, int* h);
+/* dataset.cpp:109-141 — "fx fy cx cy width height depth_scale", '#' comments */
+int csf_read_intrinsics(const char* path, csf_intrinsics* k);
+int csf_write_intrinsics(const char* path, const csf_intrinsics* k);
+/* dataset.cpp:143-177 — "t tx ty tz qx qy qz qw" lines; poses [n][12]
+ * camera->world; timestamps/poses NULL: count only (cap entries filled). */
+int csf_read_trajectory(const char* path, double* timestamps, double* poses, int cap, int* n);
+int csf_write_trajectory(const char* path, const double* timestamps, const double* poses, int n);
+
 /* ---- pipeline ------------------------------------------------------------ */
 int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf_pipeline* out);
 int csf_pipeline_destroy(csf_pipeline p);

@@ -798,3 +798,11 @@ from .reloc import (NnError, RelocMethod, RelocProblem, RelocResult, build_refer
 __all__ += ["NnError", "RelocMethod", "RelocProblem", "RelocResult", "build_reference", "default_reloc_cfg",
             "depth_cloud", "eval_nn_error", "relocalize", "reloc_energy", "reloc_gradient", "reloc_hessian",
             "reloc_loss", "select_reference_frames"]
+
+# ----------------------------------------------------------------------------- on-disk formats (dataset.hpp)
+from .dataset import (Sequence, SequenceFrame, TrajectoryEntry, open_sequence, read_depth_png16,  # noqa: E402
+                      read_intrinsics, read_trajectory, write_depth_png16, write_intrinsics, write_sequence,
+                      write_trajectory)
+
+__all__ += ["Sequence", "SequenceFrame", "TrajectoryEntry", "open_sequence", "read_depth_png16", "read_intrinsics",
+            "read_trajectory", "write_depth_png16", "write_intrinsics", "write_sequence", "write_trajectory"]

@@ -30,7 +30,9 @@ EXPORTS = (
     "csf_linearized_step", "csf_pairwise_sum", "csf_pipeline_create", "csf_pipeline_destroy", "csf_pipeline_upload",
     "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_hessian", "csf_pipeline_run_host",
     "csf_synth_workload", "csf_default_reloc_cfg", "csf_reloc_create", "csf_reloc_destroy", "csf_reloc_info",
-    "csf_reloc_energy", "csf_relocalize", "csf_depth_cloud", "csf_eval_nn_error",
+    "csf_reloc_energy", "csf_relocalize", "csf_depth_cloud", "csf_eval_nn_error", "csf_io_last_error",
+    "csf_write_depth_png16", "csf_read_depth_png16", "csf_read_intrinsics", "csf_write_intrinsics",
+    "csf_read_trajectory", "csf_write_trajectory",
 )
 RELOC_GRADIENT_DESCENT, RELOC_NEWTON = 0, 1
 
@@ -148,6 +150,13 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_relocalize": (ip, [vp, dp, ip, C.POINTER(RelocCfg), dp, C.POINTER(RelocResult), dp, dp]),
         "csf_depth_cloud": (ip, [vp, dp, ip, ip, C.POINTER(Intrinsics), dp, ip, dp, C.POINTER(C.c_int)]),
         "csf_eval_nn_error": (ip, [vp, dp, dp, ip, dp, ip, dp, i32p]),
+        "csf_io_last_error": (C.c_char_p, []),
+        "csf_write_depth_png16": (ip, [C.c_char_p, dp, ip, ip, C.c_double]),
+        "csf_read_depth_png16": (ip, [C.c_char_p, C.c_double, dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+        "csf_read_intrinsics": (ip, [C.c_char_p, C.POINTER(Intrinsics)]),
+        "csf_write_intrinsics": (ip, [C.c_char_p, C.POINTER(Intrinsics)]),
+        "csf_read_trajectory": (ip, [C.c_char_p, dp, dp, ip, C.POINTER(C.c_int)]),
+        "csf_write_trajectory": (ip, [C.c_char_p, dp, dp, ip]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
