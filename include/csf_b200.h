@@ -335,6 +335,48 @@ int csf_depth_cloud(csf_ctx ctx, const double* depth, int w, int h, const csf_in
 int csf_eval_nn_error(csf_ctx ctx, const double* transform, const double* query, int n_query, const double* reference,
                       int n_reference, double* mean, int32_t* outlier);
 
+/* ---- surfel (X-EF) front end: surfel.hpp / surfel.cpp ----
+ * A csf_surfels is a SurfelMap (surfel.hpp:24-31) resident in HBM whose
+ * position, normal and confidence carry D derivative channels (the
+ * reference's Complex is D = 1): positions / normals [n][3][1+D],
+ * confidence [n][1+D], radius [n], timestamp [n].  Indices are stable
+ * (append only). */
+typedef struct csf_surfels_s* csf_surfels;
+/* surfel.hpp:55-60, 84-91 */
+typedef struct {
+  double depth, normal_deg, distance, sigma; /* 0.05 m, 30 deg, 0.05 m, 0.025 m */
+  int one_to_many;                           /* 1 */
+} csf_surfel_cfg;
+void csf_default_surfel_cfg(csf_surfel_cfg* cfg);
+int csf_surfels_create(csf_ctx ctx, int n_channels, csf_surfels* out);
+int csf_surfels_destroy(csf_surfels m);
+int csf_surfels_count(csf_surfels m, int* n);
+/* host copies of the map (any output may be NULL) / replace the map */
+int csf_surfels_download(csf_surfels m, double* positions, double* normals, double* radius, double* confidence,
+                         int32_t* timestamps);
+int csf_surfels_upload(csf_surfels m, int n, const double* positions, const double* normals, const double* radius,
+                       const double* confidence, const int32_t* timestamps);
+/* surfel.cpp:30-64 — the 4x-supersampled index map at a real camera->world
+ * pose: offsets [16 w h + 1], entries [n] (nearest-first per cell). */
+int csf_render_index_map(csf_surfels m, const double* camera_to_world, const csf_intrinsics* k, uint32_t* offsets,
+                         int32_t* entries, int* n_entries);
+/* surfel.cpp:66-108 for every pixel of a lifted depth [h][w][1+D] at a lifted
+ * camera->world pose [12][1+D] (real intrinsics): counts [w h]; with
+ * indices/weights non-NULL (capacity cap) the lists in pixel scan order,
+ * candidate order within a pixel (weights [.][1+D]); *total = sum of counts. */
+int csf_associate_surfels(csf_surfels m, const double* depth, int w, int h, const double* camera_to_world,
+                          const csf_intrinsics* k, const csf_surfel_cfg* cfg, int32_t* counts, int32_t* indices,
+                          double* weights, int cap, int* total);
+/* surfel.cpp:121-236 — update_surfels(map, depth, camera_to_world, k, frame) */
+int csf_update_surfels(csf_surfels m, const double* depth, int w, int h, const double* camera_to_world,
+                       const csf_intrinsics* k, int frame_index, const csf_surfel_cfg* cfg, int* merged_pixels,
+                       int* created);
+/* surfel.cpp:238-263 — nearest-surfel splat: vertices / normals [h][w][3] */
+int csf_predict_maps(csf_surfels m, const double* camera_to_world, const csf_intrinsics* k, double* vertices,
+                     double* normals);
+/* surfel.cpp:110-119 */
+double csf_sample_confidence(const csf_intrinsics* k, int x, int y);
+
 /* ---- on-disk formats: dataset.hpp / dataset.cpp -------
  * Host-side file I/O (no context needed).  Failures return CSF_ERUNTIME
  * (std::runtime_error) with the message in csf_io_last_error(). */

@@ -59,6 +59,19 @@ def lib() -> C.CDLL:
             "orc_relocalize": (ip, [vp, dp, ip, C.POINTER(_capi.RelocCfg), dp, C.POINTER(_capi.RelocResult), dp, dp]),
             "orc_depth_cloud": (ip, [dp, ip, ip, C.POINTER(_capi.Intrinsics), dp, ip, dp, C.POINTER(C.c_int)]),
             "orc_nn_error": (ip, [dp, dp, ip, dp, ip, dp, C.POINTER(C.c_int)]),
+            "orc_surfels_create": (ip, [ip, C.POINTER(vp)]),
+            "orc_surfels_destroy": (None, [vp]),
+            "orc_surfels_count": (ip, [vp]),
+            "orc_surfels_download": (ip, [vp, dp, dp, dp, dp, i32p]),
+            "orc_surfels_upload": (ip, [vp, ip, dp, dp, dp, dp, i32p]),
+            "orc_update_surfels": (ip, [vp, dp, ip, ip, dp, C.POINTER(_capi.Intrinsics), ip,
+                                        C.POINTER(_capi.SurfelCfg), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+            "orc_render_index_map": (ip, [vp, dp, C.POINTER(_capi.Intrinsics), C.POINTER(C.c_uint32), i32p,
+                                          C.POINTER(C.c_int)]),
+            "orc_associate_surfels": (ip, [vp, dp, ip, ip, dp, C.POINTER(_capi.Intrinsics), C.POINTER(_capi.SurfelCfg),
+                                           i32p, i32p, dp, ip, C.POINTER(C.c_int)]),
+            "orc_predict_maps": (ip, [vp, dp, C.POINTER(_capi.Intrinsics), dp, dp]),
+            "orc_sample_confidence": (C.c_double, [C.POINTER(_capi.Intrinsics), ip, ip]),
             "orc_pipeline_hessian": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, dp, dp, i32p, dp]),
         }
         for name, (res, args) in sig.items():
@@ -370,3 +383,79 @@ def nn_error(T, q, r):
     _check(lib().orc_nn_error(_dp(np.ascontiguousarray(T, dtype=np.float64)), _dp(q), q.shape[0], _dp(r), r.shape[0],
                               C.byref(mean), C.byref(out)))
     return mean.value, bool(out.value)
+
+
+def _i32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+class Surfels:
+    """SurfelMapT<FT<D>> (orc_surfel.hpp)."""
+
+    def __init__(self, D: int):
+        self.D = D
+        self.h = C.c_void_p()
+        _check(lib().orc_surfels_create(D, C.byref(self.h)))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().orc_surfels_destroy(self.h)
+        except Exception:
+            pass
+
+    def size(self):
+        return lib().orc_surfels_count(self.h)
+
+    def download(self):
+        n, Cc = self.size(), 1 + self.D
+        out = {"position": np.zeros((n, 3, Cc)), "normal": np.zeros((n, 3, Cc)), "radius": np.zeros(n),
+               "confidence": np.zeros((n, Cc)), "timestamp": np.zeros(n, dtype=np.int32)}
+        if n:
+            _check(lib().orc_surfels_download(self.h, _dp(out["position"]), _dp(out["normal"]), _dp(out["radius"]),
+                                              _dp(out["confidence"]), _i32(out["timestamp"])))
+        return out
+
+    def upload(self, d):
+        arr = {k: np.ascontiguousarray(d[k], dtype=np.int32 if k == "timestamp" else np.float64) for k in d}
+        _check(lib().orc_surfels_upload(self.h, len(arr["radius"]), _dp(arr["position"]), _dp(arr["normal"]),
+                                        _dp(arr["radius"]), _dp(arr["confidence"]), _i32(arr["timestamp"])))
+
+    def update(self, depth, pose, k, frame, cfg):
+        d = np.ascontiguousarray(depth, dtype=np.float64)
+        h, w = d.shape[:2]
+        mp, cr = C.c_int(), C.c_int()
+        _check(lib().orc_update_surfels(self.h, _dp(d), w, h, _dp(np.ascontiguousarray(pose, dtype=np.float64)),
+                                        C.byref(k), frame, C.byref(cfg), C.byref(mp), C.byref(cr)))
+        return mp.value, cr.value
+
+    def index_map(self, pose12, k):
+        offs = np.zeros(16 * k.width * k.height + 1, dtype=np.uint32)
+        ent = np.zeros(max(self.size(), 1), dtype=np.int32)
+        m = C.c_int()
+        _check(lib().orc_render_index_map(self.h, _dp(np.ascontiguousarray(pose12, dtype=np.float64)), C.byref(k),
+                                          offs.ctypes.data_as(C.POINTER(C.c_uint32)), _i32(ent), C.byref(m)))
+        return offs, ent[:m.value].copy()
+
+    def associate(self, depth, pose, k, cfg, cap=1 << 22):
+        d = np.ascontiguousarray(depth, dtype=np.float64)
+        h, w = d.shape[:2]
+        counts = np.zeros((h, w), dtype=np.int32)
+        idx = np.zeros(cap, dtype=np.int32)
+        wts = np.zeros((cap, 1 + self.D))
+        T = C.c_int()
+        _check(lib().orc_associate_surfels(self.h, _dp(d), w, h, _dp(np.ascontiguousarray(pose, dtype=np.float64)),
+                                           C.byref(k), C.byref(cfg), _i32(counts), _i32(idx), _dp(wts), cap,
+                                           C.byref(T)))
+        return counts, idx[:T.value].copy(), wts[:T.value].copy()
+
+    def predict(self, pose12, k):
+        V = np.zeros((k.height, k.width, 3))
+        N = np.zeros_like(V)
+        _check(lib().orc_predict_maps(self.h, _dp(np.ascontiguousarray(pose12, dtype=np.float64)), C.byref(k), _dp(V),
+                                      _dp(N)))
+        return V, N
+
+
+def sample_confidence(k, x, y):
+    return lib().orc_sample_confidence(C.byref(k), x, y)

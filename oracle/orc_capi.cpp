@@ -12,6 +12,7 @@
 #include "../include/csf_b200.h"
 #include "orc_pipeline.hpp"
 #include "orc_reloc.hpp"
+#include "orc_surfel.hpp"
 
 using namespace orc;
 
@@ -439,7 +440,175 @@ std::vector<Vec3d> cloud_of(const double* p, int n) {
 }
 }  // namespace
 
+// ---- surfels (orc_surfel.hpp) over F = FT<D>
+struct SurfBase {
+  virtual ~SurfBase() = default;
+  virtual int channels() const = 0;
+  virtual int count() const = 0;
+  virtual void download(double* pos, double* nrm, double* rad, double* conf, int32_t* ts) const = 0;
+  virtual void upload(int n, const double* pos, const double* nrm, const double* rad, const double* conf,
+                      const int32_t* ts) = 0;
+  virtual void update(const double* depth, int w, int h, const double* c2w, const Intrinsics& k, int frame,
+                      const SurfelFusionConfig& cfg, int* merged, int* created) = 0;
+  virtual void index_map(const double* c2w12, const Intrinsics& k, uint32_t* offsets, int32_t* entries,
+                         int* n) const = 0;
+  virtual void associate(const double* depth, int w, int h, const double* c2w, const Intrinsics& k,
+                         const SurfelFusionConfig& cfg, int32_t* counts, int32_t* idx, double* wts, int cap,
+                         int* total) const = 0;
+  virtual void predict(const double* c2w12, const Intrinsics& k, double* V, double* N) const = 0;
+};
+
+template <int D>
+struct Surf : SurfBase {
+  using F = FT<D>;
+  SurfelMapT<F> map;
+  int channels() const override { return D; }
+  int count() const override { return static_cast<int>(map.size()); }
+  void download(double* pos, double* nrm, double* rad, double* conf, int32_t* ts) const override {
+    for (std::size_t i = 0; i < map.size(); ++i) {
+      const auto& s = map.surfels[i];
+      for (int c = 0; c < 3; ++c) {
+        if (pos) store_s<D>(pos + (3 * i + c) * (1 + D), s.position[c]);
+        if (nrm) store_s<D>(nrm + (3 * i + c) * (1 + D), s.normal[c]);
+      }
+      if (rad) rad[i] = s.radius;
+      if (conf) store_s<D>(conf + i * (1 + D), s.confidence);
+      if (ts) ts[i] = s.timestamp;
+    }
+  }
+  void upload(int n, const double* pos, const double* nrm, const double* rad, const double* conf,
+              const int32_t* ts) override {
+    map.surfels.assign(n, SurfelT<F>{});
+    for (int i = 0; i < n; ++i) {
+      auto& s = map.surfels[i];
+      for (int c = 0; c < 3; ++c) {
+        s.position[c] = load_s<D>(pos + (3 * i + c) * (1 + D));
+        s.normal[c] = load_s<D>(nrm + (3 * i + c) * (1 + D));
+      }
+      s.radius = rad[i];
+      s.confidence = load_s<D>(conf + i * (1 + D));
+      s.timestamp = ts[i];
+    }
+  }
+  Image<F> lifted_depth(const double* depth, int w, int h) const {
+    Image<F> d(w, h, F(0.0));
+    for (int i = 0; i < w * h; ++i) d.data[i] = load_s<D>(depth + static_cast<std::size_t>(i) * (1 + D));
+    return d;
+  }
+  void update(const double* depth, int w, int h, const double* c2w, const Intrinsics& k, int frame,
+              const SurfelFusionConfig& cfg, int* merged, int* created) override {
+    Intrinsics kk = k;
+    kk.width = w;
+    kk.height = h;
+    const auto st = update_surfels(map, lifted_depth(depth, w, h), load_pose<D>(c2w), kk, frame, cfg);
+    *merged = st.merged_pixels;
+    *created = st.created;
+  }
+  void index_map(const double* c2w12, const Intrinsics& k, uint32_t* offsets, int32_t* entries,
+                 int* n) const override {
+    Pose p;
+    for (int e = 0; e < 9; ++e) p.rotation(e / 3, e % 3) = c2w12[e];
+    for (int e = 0; e < 3; ++e) p.translation[e] = c2w12[9 + e];
+    const IndexMap im = render_index_map(map, p, k);
+    std::copy(im.offsets.begin(), im.offsets.end(), offsets);
+    if (entries) std::copy(im.entries.begin(), im.entries.end(), entries);
+    *n = static_cast<int>(im.entries.size());
+  }
+  void associate(const double* depth, int w, int h, const double* c2w, const Intrinsics& k,
+                 const SurfelFusionConfig& cfg, int32_t* counts, int32_t* idx, double* wts, int cap,
+                 int* total) const override {
+    Intrinsics kk = k;
+    kk.width = w;
+    kk.height = h;
+    const PoseT<F> pose = load_pose<D>(c2w);
+    const SurfaceMaps<F> frame = measure_surface<F>(lifted_depth(depth, w, h), kk);
+    const IndexMap im = render_index_map(map, real_pose(pose), kk);
+    int t = 0;
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x) {
+        auto slot = associate_one_to_many(x, y, frame, im, map, pose, cfg.thresholds);
+        if (!cfg.one_to_many && slot.size() > 1) {
+          std::size_t best = 0;
+          for (std::size_t j = 1; j < slot.size(); ++j)
+            if (real_part(slot[j].weight) > real_part(slot[best].weight)) best = j;
+          slot = {slot[best]};
+        }
+        counts[y * w + x] = static_cast<int32_t>(slot.size());
+        for (const auto& a : slot) {
+          if (idx && t < cap) {
+            idx[t] = a.index;
+            store_s<D>(wts + static_cast<std::size_t>(t) * (1 + D), a.weight);
+          }
+          ++t;
+        }
+      }
+    *total = t;
+  }
+  void predict(const double* c2w12, const Intrinsics& k, double* V, double* N) const override {
+    Pose p;
+    for (int e = 0; e < 9; ++e) p.rotation(e / 3, e % 3) = c2w12[e];
+    for (int e = 0; e < 3; ++e) p.translation[e] = c2w12[9 + e];
+    const SurfaceMaps<double> m = predict_maps(map, p, k);
+    for (int i = 0; i < k.width * k.height; ++i)
+      for (int c = 0; c < 3; ++c) {
+        V[3 * i + c] = m.vertices.data[i][c];
+        N[3 * i + c] = m.normals.data[i][c];
+      }
+  }
+};
+
+SurfelFusionConfig to_sfc(const csf_surfel_cfg* c) {
+  SurfelFusionConfig o;
+  if (c) {
+    o.thresholds.depth = c->depth;
+    o.thresholds.normal_deg = c->normal_deg;
+    o.thresholds.distance = c->distance;
+    o.thresholds.sigma = c->sigma;
+    o.one_to_many = c->one_to_many != 0;
+  }
+  return o;
+}
+
 extern "C" {
+
+int orc_surfels_create(int D, void** out) {
+  return guard([&] {
+    switch (D) {
+      case 0: *out = static_cast<SurfBase*>(new Surf<0>()); break;
+      case 1: *out = static_cast<SurfBase*>(new Surf<1>()); break;
+      case 2: *out = static_cast<SurfBase*>(new Surf<2>()); break;
+      case 6: *out = static_cast<SurfBase*>(new Surf<6>()); break;
+      default: throw std::invalid_argument("orc_surfels_create: channels must be 0, 1, 2 or 6");
+    }
+  });
+}
+void orc_surfels_destroy(void* m) { delete static_cast<SurfBase*>(m); }
+int orc_surfels_count(void* m) { return static_cast<SurfBase*>(m)->count(); }
+int orc_surfels_download(void* m, double* pos, double* nrm, double* rad, double* conf, int32_t* ts) {
+  return guard([&] { static_cast<SurfBase*>(m)->download(pos, nrm, rad, conf, ts); });
+}
+int orc_surfels_upload(void* m, int n, const double* pos, const double* nrm, const double* rad, const double* conf,
+                       const int32_t* ts) {
+  return guard([&] { static_cast<SurfBase*>(m)->upload(n, pos, nrm, rad, conf, ts); });
+}
+int orc_update_surfels(void* m, const double* depth, int w, int h, const double* c2w, const csf_intrinsics* k,
+                       int frame, const csf_surfel_cfg* cfg, int* merged, int* created) {
+  return guard([&] { static_cast<SurfBase*>(m)->update(depth, w, h, c2w, to_intr(*k), frame, to_sfc(cfg), merged,
+                                                       created); });
+}
+int orc_render_index_map(void* m, const double* c2w12, const csf_intrinsics* k, uint32_t* offsets, int32_t* entries,
+                         int* n) {
+  return guard([&] { static_cast<SurfBase*>(m)->index_map(c2w12, to_intr(*k), offsets, entries, n); });
+}
+int orc_associate_surfels(void* m, const double* depth, int w, int h, const double* c2w, const csf_intrinsics* k,
+                          const csf_surfel_cfg* cfg, int32_t* counts, int32_t* idx, double* wts, int cap, int* total) {
+  return guard([&] { static_cast<SurfBase*>(m)->associate(depth, w, h, c2w, to_intr(*k), to_sfc(cfg), counts, idx,
+                                                          wts, cap, total); });
+}
+int orc_predict_maps(void* m, const double* c2w12, const csf_intrinsics* k, double* V, double* N) {
+  return guard([&] { static_cast<SurfBase*>(m)->predict(c2w12, to_intr(*k), V, N); });
+}
+double orc_sample_confidence(const csf_intrinsics* k, int x, int y) { return sample_confidence(to_intr(*k), x, y); }
 
 // ---- relocalization (orc_reloc.hpp)
 int orc_reloc_create(void* v, const double* depth, int w, int h, const csf_intrinsics* k, void** out) {

@@ -384,6 +384,8 @@ template <typename S> Vec3<S> operator-(const Vec3<S>& a) { return {-a[0], -a[1]
 // scalar * vector: functor(scalar, coeff) (Eigen scalar_product_op(lhs, rhs))
 template <typename S> Vec3<S> operator*(const S& s, const Vec3<S>& a) { return {s * a[0], s * a[1], s * a[2]}; }
 template <typename S> Vec3<S> operator/(const Vec3<S>& a, const S& s) { return {a[0] / s, a[1] / s, a[2] / s}; }
+// vector * scalar: functor(coeff, scalar)
+template <typename S> Vec3<S> operator*(const Vec3<S>& a, const S& s) { return {a[0] * s, a[1] * s, a[2] * s}; }
 
 // 3-term redux: a0 + (a1 + a2)
 template <typename S> S sum3(const S& a0, const S& a1, const S& a2) { return a0 + (a1 + a2); }

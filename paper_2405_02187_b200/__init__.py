@@ -806,3 +806,12 @@ from .dataset import (Sequence, SequenceFrame, TrajectoryEntry, open_sequence, r
 
 __all__ += ["Sequence", "SequenceFrame", "TrajectoryEntry", "open_sequence", "read_depth_png16", "read_intrinsics",
             "read_trajectory", "write_depth_png16", "write_intrinsics", "write_sequence", "write_trajectory"]
+
+# ----------------------------------------------------------------------------- surfel front end (surfel.hpp)
+from .surfel import (IndexMap, SurfelMap, SurfelUpdateStats, associate_all, associate_one_to_many,  # noqa: E402
+                     default_surfel_cfg, predict_maps, render_index_map, sample_confidence, update_surfels,
+                     write_surfel_ply)
+
+__all__ += ["IndexMap", "SurfelMap", "SurfelUpdateStats", "associate_all", "associate_one_to_many",
+            "default_surfel_cfg", "predict_maps", "render_index_map", "sample_confidence", "update_surfels",
+            "write_surfel_ply"]

@@ -32,7 +32,9 @@ EXPORTS = (
     "csf_synth_workload", "csf_default_reloc_cfg", "csf_reloc_create", "csf_reloc_destroy", "csf_reloc_info",
     "csf_reloc_energy", "csf_relocalize", "csf_depth_cloud", "csf_eval_nn_error", "csf_io_last_error",
     "csf_write_depth_png16", "csf_read_depth_png16", "csf_read_intrinsics", "csf_write_intrinsics",
-    "csf_read_trajectory", "csf_write_trajectory",
+    "csf_read_trajectory", "csf_write_trajectory", "csf_default_surfel_cfg", "csf_surfels_create",
+    "csf_surfels_destroy", "csf_surfels_count", "csf_surfels_download", "csf_surfels_upload", "csf_render_index_map",
+    "csf_associate_surfels", "csf_update_surfels", "csf_predict_maps", "csf_sample_confidence",
 )
 RELOC_GRADIENT_DESCENT, RELOC_NEWTON = 0, 1
 
@@ -77,6 +79,11 @@ class RelocCfg(C.Structure):
 
 class RelocResult(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("final_loss", C.c_double)]
+
+
+class SurfelCfg(C.Structure):
+    _fields_ = [("depth", C.c_double), ("normal_deg", C.c_double), ("distance", C.c_double), ("sigma", C.c_double),
+                ("one_to_many", C.c_int)]
 
 
 class PipelineCfg(C.Structure):
@@ -151,6 +158,19 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_depth_cloud": (ip, [vp, dp, ip, ip, C.POINTER(Intrinsics), dp, ip, dp, C.POINTER(C.c_int)]),
         "csf_eval_nn_error": (ip, [vp, dp, dp, ip, dp, ip, dp, i32p]),
         "csf_io_last_error": (C.c_char_p, []),
+        "csf_default_surfel_cfg": (None, [C.POINTER(SurfelCfg)]),
+        "csf_surfels_create": (ip, [vp, ip, C.POINTER(vp)]),
+        "csf_surfels_destroy": (ip, [vp]),
+        "csf_surfels_count": (ip, [vp, C.POINTER(C.c_int)]),
+        "csf_surfels_download": (ip, [vp, dp, dp, dp, dp, i32p]),
+        "csf_surfels_upload": (ip, [vp, ip, dp, dp, dp, dp, i32p]),
+        "csf_render_index_map": (ip, [vp, dp, C.POINTER(Intrinsics), C.POINTER(C.c_uint32), i32p, C.POINTER(C.c_int)]),
+        "csf_associate_surfels": (ip, [vp, dp, ip, ip, dp, C.POINTER(Intrinsics), C.POINTER(SurfelCfg), i32p, i32p, dp,
+                                       ip, C.POINTER(C.c_int)]),
+        "csf_update_surfels": (ip, [vp, dp, ip, ip, dp, C.POINTER(Intrinsics), ip, C.POINTER(SurfelCfg),
+                                    C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+        "csf_predict_maps": (ip, [vp, dp, C.POINTER(Intrinsics), dp, dp]),
+        "csf_sample_confidence": (C.c_double, [C.POINTER(Intrinsics), ip, ip]),
         "csf_write_depth_png16": (ip, [C.c_char_p, dp, ip, ip, C.c_double]),
         "csf_read_depth_png16": (ip, [C.c_char_p, C.c_double, dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "csf_read_intrinsics": (ip, [C.c_char_p, C.POINTER(Intrinsics)]),

@@ -2145,3 +2145,265 @@ extern "C" int csf_eval_nn_error(csf_ctx ctx, const double* T, const double* q, 
   if (outlier) *outlier = *mean > 0.1;
   return CSF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// surfel (X-EF) front end (surfel.hpp)
+// ---------------------------------------------------------------------------
+struct csf_surfels_s {
+  csf_ctx ctx = nullptr;
+  int D = 0, n = 0, cap = 0;
+  DevBuf<double> pos, nrm, conf, rad;
+  DevBuf<int> ts;
+  DevBuf<double> in;  // depth [P][C] + pose [12][C] + intrinsics [4][C]
+  SurfelScratch ws;
+  ~csf_surfels_s() {
+    pos.release();
+    nrm.release();
+    conf.release();
+    rad.release();
+    ts.release();
+    in.release();
+    surfel_scratch_release(ws);
+  }
+  SurfelArrays arrays() { return SurfelArrays{pos.p, nrm.p, conf.p, rad.p, ts.p}; }
+};
+
+extern "C" void csf_default_surfel_cfg(csf_surfel_cfg* c) {
+  if (!c) return;
+  c->depth = 0.05;  // surfel.hpp:55-60
+  c->normal_deg = 30.0;
+  c->distance = 0.05;
+  c->sigma = 0.025;
+  c->one_to_many = 1;  // surfel.hpp:84-91
+}
+
+// grow the map's capacity to >= need, keeping the first n surfels
+static int surfels_reserve(csf_surfels m, int need) {
+  if (need <= m->cap && m->pos.p) return CSF_OK;
+  const int C = 1 + m->D;
+  const int cap = std::max({need, 2 * m->cap, 1024});
+  DevBuf<double> pos, nrm, conf, rad;
+  DevBuf<int> ts;
+  CUDA_TRY(m->ctx, pos.alloc(3 * static_cast<size_t>(cap) * C));
+  CUDA_TRY(m->ctx, nrm.alloc(3 * static_cast<size_t>(cap) * C));
+  CUDA_TRY(m->ctx, conf.alloc(static_cast<size_t>(cap) * C));
+  CUDA_TRY(m->ctx, rad.alloc(cap));
+  CUDA_TRY(m->ctx, ts.alloc(cap));
+  if (m->n > 0) {
+    const cudaStream_t s = m->ctx->stream;
+    CUDA_TRY(m->ctx, cudaMemcpyAsync(pos.p, m->pos.p, sizeof(double) * 3 * m->n * C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(m->ctx, cudaMemcpyAsync(nrm.p, m->nrm.p, sizeof(double) * 3 * m->n * C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(m->ctx, cudaMemcpyAsync(conf.p, m->conf.p, sizeof(double) * m->n * C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(m->ctx, cudaMemcpyAsync(rad.p, m->rad.p, sizeof(double) * m->n, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(m->ctx, cudaMemcpyAsync(ts.p, m->ts.p, sizeof(int) * m->n, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(m->ctx, cudaStreamSynchronize(s));
+  }
+  std::swap(m->pos, pos);
+  std::swap(m->nrm, nrm);
+  std::swap(m->conf, conf);
+  std::swap(m->rad, rad);
+  std::swap(m->ts, ts);
+  pos.release();
+  nrm.release();
+  conf.release();
+  rad.release();
+  ts.release();
+  m->cap = cap;
+  return CSF_OK;
+}
+
+extern "C" int csf_surfels_create(csf_ctx ctx, int n_channels, csf_surfels* out) {
+  if (!ctx || !out || n_channels < 0 || n_channels > CSF_MAX_DIRECTIONS) return CSF_EINVAL;
+  cudaSetDevice(ctx->device);
+  auto m = std::make_unique<csf_surfels_s>();
+  m->ctx = ctx;
+  m->D = n_channels;
+  const int rc = surfels_reserve(m.get(), 1024);
+  if (rc) return rc;
+  *out = m.release();
+  return CSF_OK;
+}
+extern "C" int csf_surfels_destroy(csf_surfels m) {
+  if (!m) return CSF_EINVAL;
+  cudaSetDevice(m->ctx->device);
+  delete m;
+  return CSF_OK;
+}
+extern "C" int csf_surfels_count(csf_surfels m, int* n) {
+  if (!m || !n) return CSF_EINVAL;
+  *n = m->n;
+  return CSF_OK;
+}
+extern "C" int csf_surfels_download(csf_surfels m, double* pos, double* nrm, double* rad, double* conf, int32_t* ts) {
+  if (!m) return CSF_EINVAL;
+  csf_ctx ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  const size_t C = 1 + m->D, n = m->n;
+  if (n == 0) return CSF_OK;
+  if (pos) CUDA_TRY(ctx, cudaMemcpy(pos, m->pos.p, sizeof(double) * 3 * n * C, cudaMemcpyDeviceToHost));
+  if (nrm) CUDA_TRY(ctx, cudaMemcpy(nrm, m->nrm.p, sizeof(double) * 3 * n * C, cudaMemcpyDeviceToHost));
+  if (rad) CUDA_TRY(ctx, cudaMemcpy(rad, m->rad.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  if (conf) CUDA_TRY(ctx, cudaMemcpy(conf, m->conf.p, sizeof(double) * n * C, cudaMemcpyDeviceToHost));
+  if (ts) CUDA_TRY(ctx, cudaMemcpy(ts, m->ts.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  return CSF_OK;
+}
+extern "C" int csf_surfels_upload(csf_surfels m, int n, const double* pos, const double* nrm, const double* rad,
+                                  const double* conf, const int32_t* ts) {
+  if (!m || n < 0 || (n > 0 && (!pos || !nrm || !rad || !conf || !ts))) return CSF_EINVAL;
+  csf_ctx ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  m->n = 0;
+  const int rc = surfels_reserve(m, n);
+  if (rc) return rc;
+  const size_t C = 1 + m->D;
+  if (n > 0) {
+    CUDA_TRY(ctx, cudaMemcpy(m->pos.p, pos, sizeof(double) * 3 * n * C, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(m->nrm.p, nrm, sizeof(double) * 3 * n * C, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(m->rad.p, rad, sizeof(double) * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(m->conf.p, conf, sizeof(double) * n * C, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(m->ts.p, ts, sizeof(int) * n, cudaMemcpyHostToDevice));
+  }
+  m->n = n;
+  return CSF_OK;
+}
+
+static void k4_of(const csf_intrinsics* k, double* k4) {
+  k4[0] = k->fx;
+  k4[1] = k->fy;
+  k4[2] = k->cx;
+  k4[3] = k->cy;
+}
+
+extern "C" int csf_render_index_map(csf_surfels m, const double* c2w, const csf_intrinsics* k, uint32_t* offsets,
+                                    int32_t* entries, int* n_entries) {
+  if (!m || !c2w || !k || !offsets || !n_entries || k->width <= 0 || k->height <= 0) return CSF_EINVAL;
+  csf_ctx ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  double k4[4];
+  k4_of(k, k4);
+  int cnt = 0;
+  const int rc = surfel_index_map(ctx->stream, m->ws, m->pos.p, m->n, m->D, c2w, k4, k->width, k->height, &cnt);
+  ctx->launches += 4;
+  if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "render_index_map: CUDA error");
+  const size_t cells = static_cast<size_t>(16) * k->width * k->height;
+  CUDA_TRY(ctx, cudaMemcpy(offsets, m->ws.offsets, sizeof(uint32_t) * (cells + 1), cudaMemcpyDeviceToHost));
+  if (entries && cnt > 0)
+    CUDA_TRY(ctx, cudaMemcpy(entries, m->ws.entries, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost));
+  *n_entries = cnt;
+  return CSF_OK;
+}
+
+// upload depth / pose / intrinsics and run index map + association
+static int surfels_assoc_common(csf_surfels m, const double* depth, int w, int h, const double* c2w,
+                                const csf_intrinsics* k, const csf_surfel_cfg* cfg_in, int* total, int* merged,
+                                double* c2w12, double* k4) {
+  csf_ctx ctx = m->ctx;
+  const int C = 1 + m->D;
+  const size_t P = static_cast<size_t>(w) * h;
+  csf_surfel_cfg cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    csf_default_surfel_cfg(&cfg);
+  CUDA_TRY(ctx, m->in.alloc(P * C + 16 * C));
+  double* d_depth = m->in.p;
+  double* d_pose = d_depth + P * C;
+  double* d_intr = d_pose + 12 * C;
+  std::vector<double> intr(4 * C, 0.0);
+  k4_of(k, k4);
+  for (int e = 0; e < 4; ++e) intr[e * C] = k4[e];
+  for (int e = 0; e < 12; ++e) c2w12[e] = c2w[e * C];
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_depth, depth, sizeof(double) * P * C, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_pose, c2w, sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_intr, intr.data(), sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
+  int cnt = 0;
+  int rc = surfel_index_map(ctx->stream, m->ws, m->pos.p, m->n, m->D, c2w12, k4, w, h, &cnt);
+  if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "surfels: index map failed");
+  AssocParams ap;
+  ap.depth = cfg.depth;
+  ap.cos_gate = std::cos(cfg.normal_deg * M_PI / 180.0);
+  ap.distance = cfg.distance;
+  ap.kernel_scale = -1.0 / (2.0 * cfg.sigma * cfg.sigma);
+  ap.one_to_many = cfg.one_to_many != 0;
+  rc = surfel_associate(ctx->stream, m->ws, m->pos.p, m->nrm.p, m->D, d_depth, d_pose, d_intr, c2w12, k4, w, h, ap,
+                        total, merged);
+  ctx->launches += 12;
+  if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "surfels: association failed");
+  return CSF_OK;
+}
+
+extern "C" int csf_associate_surfels(csf_surfels m, const double* depth, int w, int h, const double* c2w,
+                                     const csf_intrinsics* k, const csf_surfel_cfg* cfg, int32_t* counts,
+                                     int32_t* indices, double* weights, int cap, int* total) {
+  if (!m || !depth || !c2w || !k || !counts || !total || w <= 0 || h <= 0) return CSF_EINVAL;
+  csf_ctx ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  int T = 0, merged = 0;
+  double c2w12[12], k4[4];
+  const int rc = surfels_assoc_common(m, depth, w, h, c2w, k, cfg, &T, &merged, c2w12, k4);
+  if (rc) return rc;
+  const size_t P = static_cast<size_t>(w) * h, C = 1 + m->D;
+  CUDA_TRY(ctx, cudaMemcpy(counts, m->ws.pint + P, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+  if (indices && weights && T > 0) {
+    const int n = std::min(T, cap);
+    CUDA_TRY(ctx, cudaMemcpy(indices, m->ws.pidx, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(ctx, cudaMemcpy(weights, m->ws.pw, sizeof(double) * n * C, cudaMemcpyDeviceToHost));
+  }
+  *total = T;
+  return CSF_OK;
+}
+
+extern "C" int csf_update_surfels(csf_surfels m, const double* depth, int w, int h, const double* c2w,
+                                  const csf_intrinsics* k, int frame_index, const csf_surfel_cfg* cfg,
+                                  int* merged_pixels, int* created) {
+  if (!m || !depth || !c2w || !k || w <= 0 || h <= 0) return CSF_EINVAL;
+  csf_ctx ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  int T = 0, merged = 0, cr = 0;
+  double c2w12[12], k4[4];
+  int rc = surfels_assoc_common(m, depth, w, h, c2w, k, cfg, &T, &merged, c2w12, k4);
+  if (rc) return rc;
+  if (surfel_created_count(ctx->stream, m->ws, w * h, &cr)) return fail(ctx, CSF_ECUDA, "update_surfels: CUDA error");
+  rc = surfels_reserve(m, m->n + cr);
+  if (rc) return rc;
+  rc = surfel_commit(ctx->stream, m->ws, m->arrays(), m->n, m->D, T, c2w12, k4, w, h, frame_index,
+                     std::sqrt(2.0) / k->fx);
+  ctx->launches += 5;
+  if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "update_surfels: commit failed");
+  m->n += cr;
+  rc = sync_check(ctx, "update_surfels");
+  if (rc) return rc;
+  if (merged_pixels) *merged_pixels = merged;
+  if (created) *created = cr;
+  return CSF_OK;
+}
+
+extern "C" int csf_predict_maps(csf_surfels m, const double* c2w, const csf_intrinsics* k, double* V, double* N) {
+  if (!m || !c2w || !k || !V || !N || k->width <= 0 || k->height <= 0) return CSF_EINVAL;
+  csf_ctx ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  const size_t P = static_cast<size_t>(k->width) * k->height;
+  DevBuf<double> out;
+  CUDA_TRY(ctx, out.alloc(6 * P));
+  double k4[4];
+  k4_of(k, k4);
+  const int rc = surfel_predict(ctx->stream, m->ws, m->pos.p, m->nrm.p, m->n, m->D, c2w, k4, k->width, k->height,
+                                out.p, out.p + 3 * P);
+  ctx->launches += 5;
+  if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "predict_maps: CUDA error");
+  CUDA_TRY(ctx, cudaMemcpy(V, out.p, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(N, out.p + 3 * P, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost));
+  return CSF_OK;
+}
+
+// surfel.cpp:110-119 (host copy of the device function; deterministic exp)
+extern "C" double csf_sample_confidence(const csf_intrinsics* k, int x, int y) {
+  const double dx = static_cast<double>(x) - k->cx;
+  const double dy = static_cast<double>(y) - k->cy;
+  const double half_diagonal =
+      0.5 * std::sqrt(static_cast<double>(k->width) * k->width + static_cast<double>(k->height) * k->height);
+  double g = std::sqrt(dx * dx + dy * dy) / half_diagonal;
+  g = g < 0.0 ? 0.0 : (1.0 < g ? 1.0 : g);
+  return csf_det::exp(-g * g / 0.72);
+}

@@ -122,6 +122,49 @@ int depth_cloud_dev(cudaStream_t stream, const double* depth_host, int w, int h,
 int nn_error_dev(cudaStream_t stream, EnergyScratch& ws, const double* T12, const double* q, int nq, const double* r,
                  int nr, double* mean);
 
+// ---- surfel.cu: surfel (X-EF) front end (surfel.hpp)
+struct SurfelArrays {  // device map arrays (capacity >= count)
+  double* pos;   // [cap][3][1+D]
+  double* nrm;   // [cap][3][1+D]
+  double* conf;  // [cap][1+D]
+  double* rad;   // [cap]
+  int* ts;       // [cap]
+};
+struct SurfelScratch {
+  unsigned* offsets = nullptr; size_t offsets_cap = 0;          // index map offsets [16P+1]
+  unsigned* cellk = nullptr; size_t cellk_cap = 0;
+  unsigned long long* depthk = nullptr; size_t depthk_cap = 0;
+  int* sidx = nullptr; size_t sidx_cap = 0;
+  int* entries = nullptr;                                         // points into sidx
+  void* cub = nullptr; size_t cub_cap = 0;
+  double *V = nullptr, *N = nullptr, *VW = nullptr, *NW = nullptr;
+  size_t V_cap = 0, N_cap = 0, VW_cap = 0, NW_cap = 0;
+  int* pint = nullptr; size_t pint_cap = 0;                       // valid, counts, offs, cflag, crank, merged
+  int* pidx = nullptr; size_t pidx_cap = 0;                       // pair surfel index (+ sorted copy)
+  int* ppix = nullptr; size_t ppix_cap = 0;                       // pair pixel
+  double* pw = nullptr; size_t pw_cap = 0;                        // pair lifted weight [T][1+D]
+  int* seg = nullptr; size_t seg_cap = 0;
+  int* order = nullptr; size_t order_cap = 0;
+  unsigned long long* zbest = nullptr; size_t zbest_cap = 0;
+  int* ibest = nullptr; size_t ibest_cap = 0;
+  unsigned long long launches = 0;
+};
+struct AssocParams {
+  double depth, cos_gate, distance, kernel_scale;
+  int one_to_many;
+};
+int surfel_index_map(cudaStream_t s, SurfelScratch& ws, const double* pos, int n, int D, const double* c2w12,
+                     const double* k4, int w, int h, int* m_out);
+int surfel_associate(cudaStream_t s, SurfelScratch& ws, const double* spos, const double* snrm, int D,
+                     const double* depth, const double* c2w, const double* intr_lifted, const double* c2w12,
+                     const double* k4, int w, int h, const AssocParams& ap, int* total, int* merged);
+int surfel_created_count(cudaStream_t s, SurfelScratch& ws, int P, int* created);
+int surfel_commit(cudaStream_t s, SurfelScratch& ws, SurfelArrays m, int n, int D, int T, const double* c2w12,
+                  const double* k4, int w, int h, int frame, double radius_scale);
+int surfel_predict(cudaStream_t s, SurfelScratch& ws, const double* pos, const double* nrm, int n, int D,
+                   const double* c2w12, const double* k4, int w, int h, double* Vo, double* No);
+void surfel_scratch_release(SurfelScratch& ws);
+
 struct Launch {
   cudaStream_t stream;
   int* err;                // device error flag
