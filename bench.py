@@ -41,6 +41,9 @@ per-GPU work is fixed ("weak"); units = frames x directions over all ranks.
 --workload reloc: camera relocalization on the config-2
 scene — 8 queries, eta-switched Newton; relocalizations/s (bench_reloc.py).
 
+--workload surfel: the surfel (X-EF) front end — 100 VGA
+frames fused at poses lifted on 6 twist directions (bench_surfel.py).
+
 --workload config3: BASELINE config 3 — the same VGA scene, 30 frames, the
 full 10x10 Hessian as 55 second-order parameter pairs (one reference
 Bicomplex per pair, packed as channel slots of one evaluation).  Units =
@@ -80,7 +83,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5", "reloc"], default="config2")
+    ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5", "reloc", "surfel"], default="config2")
     ap.add_argument("--frames", type=int, default=0, help="0 = the workload's frame count (100 / 30)")
     ap.add_argument("--cpu-frames", type=int, default=5, help="CPU-baseline sample: frames")
     ap.add_argument("--cpu-dirs", type=int, default=2, help="CPU-baseline sample: directions (one pass each)")
@@ -428,6 +431,13 @@ def run_config5(args):
 
 def main():
     args = parse()
+    if args.workload == "surfel":
+        import bench_surfel
+        if args.impl == "reference":
+            bench_surfel.run_reference(args)
+        else:
+            bench_surfel.run(args, measured_peak, Clocks)
+        return
     if args.workload == "reloc":
         import bench_reloc
         if args.impl == "reference":

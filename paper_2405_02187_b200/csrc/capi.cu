@@ -2287,6 +2287,7 @@ extern "C" int csf_render_index_map(csf_surfels m, const double* c2w, const csf_
   ctx->launches += 4;
   if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "render_index_map: CUDA error");
   const size_t cells = static_cast<size_t>(16) * k->width * k->height;
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(ctx, cudaMemcpy(offsets, m->ws.offsets, sizeof(uint32_t) * (cells + 1), cudaMemcpyDeviceToHost));
   if (entries && cnt > 0)
     CUDA_TRY(ctx, cudaMemcpy(entries, m->ws.entries, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost));
@@ -2344,6 +2345,7 @@ extern "C" int csf_associate_surfels(csf_surfels m, const double* depth, int w, 
   const int rc = surfels_assoc_common(m, depth, w, h, c2w, k, cfg, &T, &merged, c2w12, k4);
   if (rc) return rc;
   const size_t P = static_cast<size_t>(w) * h, C = 1 + m->D;
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(ctx, cudaMemcpy(counts, m->ws.pint + P, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
   if (indices && weights && T > 0) {
     const int n = std::min(T, cap);
@@ -2392,6 +2394,7 @@ extern "C" int csf_predict_maps(csf_surfels m, const double* c2w, const csf_intr
                                 out.p, out.p + 3 * P);
   ctx->launches += 5;
   if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "predict_maps: CUDA error");
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(ctx, cudaMemcpy(V, out.p, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost));
   CUDA_TRY(ctx, cudaMemcpy(N, out.p + 3 * P, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost));
   return CSF_OK;

@@ -76,7 +76,7 @@ CSF_DEV V3<double> real3(const double* a, long long i, int C) {
 // ---------------------------------------------------------------------------
 __global__ void k_si_project(const double* __restrict__ pos, int n, int C, SurfCam cam,
                              unsigned* __restrict__ cellk, unsigned long long* __restrict__ depthk,
-                             int* __restrict__ idx) {
+                             int* __restrict__ flag) {
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -97,7 +97,20 @@ __global__ void k_si_project(const double* __restrict__ pos, int n, int C, SurfC
   }
   cellk[i] = cell;
   depthk[i] = dk;
-  idx[i] = i;
+  flag[i] = cell != 0xffffffffu ? 1 : 0;
+}
+
+// visible surfels compacted in index order (the sorts then see only them)
+__global__ void k_si_compact(const unsigned long long* __restrict__ depthk, const int* __restrict__ flag,
+                             const int* __restrict__ fpos, int n, unsigned long long* __restrict__ dk_out,
+                             int* __restrict__ idx_out) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !flag[i]) return;
+  const int j = fpos[i];
+  dk_out[j] = depthk[i];
+  idx_out[j] = i;
 }
 
 __global__ void k_si_gather_cell(const unsigned* __restrict__ cellk, const int* __restrict__ idx, int n,
@@ -334,6 +347,125 @@ __global__ void k_sf_commit(int n, int D, SurfCam cam, const int* __restrict__ s
   }
 }
 
+// segments of the surfel-sorted pair list: flag[j] = first pair of a surfel
+__global__ void k_sf_seg_flags(const int* __restrict__ key, int T, int* __restrict__ flag) {
+  pdl_wait();
+  pdl_trigger();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < T) flag[j] = (j == 0 || key[j] != key[j - 1]) ? 1 : 0;
+}
+__global__ void k_sf_seg_write(const int* __restrict__ key, const int* __restrict__ flag, const int* __restrict__ rank,
+                               int T, int* __restrict__ ustart, int* __restrict__ usurf) {
+  pdl_wait();
+  pdl_trigger();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= T) return;
+  if (flag[j]) {
+    ustart[rank[j]] = j;
+    usurf[rank[j]] = key[j];
+  }
+  if (j == T - 1) ustart[rank[j] + flag[j]] = T;
+}
+
+// lifted value from a cached real part and the channel ch read from memory
+template <typename S> CSF_DEV S with_re(const double* base, double r, int ch);
+template <> CSF_DEV double with_re<double>(const double*, double r, int) { return r; }
+template <> CSF_DEV L<1> with_re<L<1>>(const double* base, double r, int ch) {
+  L<1> o;
+  o.re = r;
+  o.im[0] = base[1 + ch];
+  return o;
+}
+
+// Commit over the touched surfels only: kLanes lanes per surfel, lane g
+// evaluating channels g, g + kLanes, ... (one Complex pass each).  Every lane
+// caches the surfel's old real state, the warp synchronises, then lane 0
+// writes the new real parts while each lane writes only its own channels.
+constexpr int kLanes = 8;
+template <typename S>
+__global__ void k_sf_commit_u(int U, int D, SurfCam cam, const int* __restrict__ ustart, const int* __restrict__ usurf,
+                              const int* __restrict__ order, const int* __restrict__ ppix,
+                              const double* __restrict__ pw, const double* __restrict__ V,
+                              const double* __restrict__ VW, const double* __restrict__ NW, CommitArgs a,
+                              double* __restrict__ spos, double* __restrict__ snrm, double* __restrict__ sconf,
+                              double* __restrict__ srad, int* __restrict__ sts) {
+  pdl_wait();
+  pdl_trigger();
+  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int u = static_cast<int>(t / kLanes), g = static_cast<int>(t % kLanes);
+  const bool active = u < U;
+  const int C = 1 + D;
+  constexpr int G = Traits<S>::G;
+  const int passes = G > 0 ? D : 1;
+  int i = 0, b = 0, e = 0;
+  double p_re[3] = {0, 0, 0}, n_re[3] = {0, 0, 0}, c_re = 0.0, r_old = 0.0;
+  if (active) {
+    i = usurf[u];
+    b = ustart[u];
+    e = ustart[u + 1];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      p_re[c] = spos[(3LL * i + c) * C];
+      n_re[c] = snrm[(3LL * i + c) * C];
+    }
+    c_re = sconf[static_cast<long long>(i) * C];
+    r_old = srad[i];
+  }
+  __syncwarp();
+  if (!active) return;
+  for (int ch = g; ch < passes; ch += kLanes) {
+    V3<S> ps = mk3<S>(lit<S>(0.0), lit<S>(0.0), lit<S>(0.0)), ns = ps;
+    S wsum = lit<S>(0.0);
+    double wre = 0.0, rsum = 0.0;
+    for (int j = b; j < e; ++j) {
+      const int q = order[j];
+      const int p = ppix[q];
+      const int x = p % cam.w, y = p / cam.w;
+      const double conf = sample_confidence_dev(cam.fx, cam.cx, cam.cy, cam.w, cam.h, x, y);
+      const S m = load_ch<S>(pw + static_cast<long long>(q) * C, ch, G) * conf;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        ps.v[c] = ps.v[c] + load_ch<S>(VW + (3LL * p + c) * C, ch, G) * m;
+        ns.v[c] = ns.v[c] + load_ch<S>(NW + (3LL * p + c) * C, ch, G) * m;
+      }
+      wsum = wsum + m;
+      if (ch == 0) {
+        const double radius = a.radius_scale * V[(3LL * p + 2) * C];
+        wre += re(m);
+        rsum += re(m) * radius;
+      }
+    }
+    const S c_old = with_re<S>(sconf + static_cast<long long>(i) * C, c_re, ch);
+    const S denom = c_old + wsum;
+    V3<S> np, bl;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      np.v[c] = (with_re<S>(spos + (3LL * i + c) * C, p_re[c], ch) * c_old + ps.v[c]) / denom;
+      bl.v[c] = (with_re<S>(snrm + (3LL * i + c) * C, n_re[c], ch) * c_old + ns.v[c]) / denom;
+    }
+    const S len2 = dot3(bl, bl);
+    const bool renorm = re(len2) > 0.0;
+    V3<S> nn = bl;
+    if (renorm) {
+      const S l = sqrt_s(len2);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) nn.v[c] = bl.v[c] / l;
+    }
+    const bool first = ch == 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      store_ch<S>(spos + (3LL * i + c) * C, np.v[c], ch, G, first);
+      if (renorm) store_ch<S>(snrm + (3LL * i + c) * C, nn.v[c], ch, G, first);
+    }
+    store_ch<S>(sconf + static_cast<long long>(i) * C, denom, ch, G, first);
+    if (first) {
+      sts[i] = a.frame;
+      const double averaged = (c_re * r_old + rsum) / (c_re + wre);
+      srad[i] = averaged < r_old ? averaged : r_old;  // std::min(radius, averaged)
+    }
+  }
+}
+
 // unmatched valid pixels appended in scan order (surfel.cpp:226-235)
 __global__ void k_sf_create(const int* __restrict__ cflag, const int* __restrict__ crank, int P, int n0, int D,
                             SurfCam cam, CommitArgs a, const double* __restrict__ V, const double* __restrict__ VW,
@@ -440,8 +572,11 @@ static cudaError_t grow(T*& p, size_t& cap, size_t need) {
   if (p) cudaFree(p);
   p = nullptr;
   cap = 0;
-  const cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(need, 1));
-  if (e == cudaSuccess) cap = need;
+  // headroom: the map grows every frame; re-allocating (and the implicit
+  // device synchronisation of cudaFree) per frame would dominate
+  const size_t want = need + need / 2 + 1024;
+  const cudaError_t e = cudaMalloc(&p, sizeof(T) * want);
+  if (e == cudaSuccess) cap = want;
   return e;
 }
 
@@ -472,41 +607,57 @@ int surfel_index_map(cudaStream_t s, SurfelScratch& ws, const double* pos, int n
   const int C = 1 + D;
   const SurfCam cam = make_cam(c2w12, k4, w, h);
   const size_t cells = static_cast<size_t>(16) * w * h;
-  if (grow(ws.offsets, ws.offsets_cap, cells + 1) || grow(ws.cellk, ws.cellk_cap, 2 * static_cast<size_t>(n)) ||
-      grow(ws.depthk, ws.depthk_cap, 2 * static_cast<size_t>(n)) ||
-      grow(ws.sidx, ws.sidx_cap, 2 * static_cast<size_t>(n)))
+  const size_t nn = static_cast<size_t>(std::max(n, 1));
+  if (grow(ws.offsets, ws.offsets_cap, cells + 1) || grow(ws.cellk, ws.cellk_cap, 2 * nn) ||
+      grow(ws.depthk, ws.depthk_cap, 3 * nn) || grow(ws.sidx, ws.sidx_cap, 4 * nn))
     return 5;
-  unsigned* cellA = ws.cellk;
-  unsigned* cellB = ws.cellk + n;
-  unsigned long long* dA = ws.depthk;
-  unsigned long long* dB = ws.depthk + n;
+  unsigned* cellA = ws.cellk;       // per surfel
+  unsigned* cellB = ws.cellk + nn;  // compacted, depth order / then sorted by cell
+  unsigned long long* d0 = ws.depthk;
+  unsigned long long* d1 = ws.depthk + nn;
+  unsigned long long* d2 = ws.depthk + 2 * nn;
   int* iA = ws.sidx;
-  int* iB = ws.sidx + n;
-  size_t need = 0, t1 = 0, t2 = 0, t3 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, t1, dA, dB, iA, iB, std::max(n, 1), 0, 64, s);
-  cub::DeviceRadixSort::SortPairs(nullptr, t2, cellA, cellB, iB, iA, std::max(n, 1), 0, 32, s);
+  int* iB = ws.sidx + nn;
+  int* flag = ws.sidx + 2 * nn;
+  int* fpos = ws.sidx + 3 * nn;
+  size_t t0 = 0, t3 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t0, flag, fpos, static_cast<int>(nn), s);
   cub::DeviceScan::ExclusiveSum(nullptr, t3, ws.offsets, ws.offsets, static_cast<int>(cells + 1), s);
-  need = std::max(t1, std::max(t2, t3));
-  if (grow(ws.cub, ws.cub_cap, need)) return 5;
+  if (grow(ws.cub, ws.cub_cap, std::max(t0, t3))) return 5;
   cudaMemsetAsync(ws.offsets, 0, sizeof(unsigned) * (cells + 1), s);
+  int m = 0;
   if (n > 0) {
-    launch_pdl(k_si_project, dim3(grid1(n)), dim3(256), 0, s, pos, n, C, cam, cellA, dA, iA);
+    launch_pdl(k_si_project, dim3(grid1(n)), dim3(256), 0, s, pos, n, C, cam, cellA, d0, flag);
+    size_t b0 = ws.cub_cap;
+    cub::DeviceScan::ExclusiveSum(ws.cub, b0, flag, fpos, n, s);
+    launch_pdl(k_si_compact, dim3(grid1(n)), dim3(256), 0, s, static_cast<const unsigned long long*>(d0),
+               static_cast<const int*>(flag), static_cast<const int*>(fpos), n, d1, iA);
+    int hv[2];
+    cudaMemcpyAsync(&hv[0], fpos + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&hv[1], flag + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return 4;
+    m = hv[0] + hv[1];
+  }
+  if (m > 0) {
+    size_t t1 = 0, t2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, d1, d2, iA, iB, m, 0, 64, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, cellB, cellB, iB, iA, m, 0, 32, s);
+    if (grow(ws.cub, ws.cub_cap, std::max(t1, t2))) return 5;
+    int bits = 1;  // cell keys < 16 w h
+    while (bits < 32 && (static_cast<size_t>(1) << bits) < cells) ++bits;
     size_t b1 = ws.cub_cap;
-    cub::DeviceRadixSort::SortPairs(ws.cub, b1, dA, dB, iA, iB, n, 0, 64, s);  // by depth (stable: index order)
-    launch_pdl(k_si_gather_cell, dim3(grid1(n)), dim3(256), 0, s, static_cast<const unsigned*>(cellA),
-               static_cast<const int*>(iB), n, cellB, ws.offsets);
+    cub::DeviceRadixSort::SortPairs(ws.cub, b1, d1, d2, iA, iB, m, 0, 64, s);  // by depth (stable: index order)
+    launch_pdl(k_si_gather_cell, dim3(grid1(m)), dim3(256), 0, s, static_cast<const unsigned*>(cellA),
+               static_cast<const int*>(iB), m, cellB, ws.offsets);
+    unsigned* cellC = reinterpret_cast<unsigned*>(d0);  // d0 is free after the compaction
     size_t b2 = ws.cub_cap;
-    cub::DeviceRadixSort::SortPairs(ws.cub, b2, cellB, cellA, iB, iA, n, 0, 32, s);  // then by cell (stable)
+    cub::DeviceRadixSort::SortPairs(ws.cub, b2, cellB, cellC, iB, iA, m, 0, bits, s);  // then by cell (stable)
   }
   size_t b3 = ws.cub_cap;
   cub::DeviceScan::ExclusiveSum(ws.cub, b3, ws.offsets, ws.offsets, static_cast<int>(cells + 1), s);
-  ws.entries = iA;  // sorted indices (first m valid)
+  ws.entries = iA;  // the m sorted surfel indices
   chk("surfel_index_map");
-  unsigned m = 0;
-  if (cudaMemcpyAsync(&m, ws.offsets + cells, sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess)
-    return 4;
-  *m_out = static_cast<int>(m);
+  *m_out = m;
   return 0;
 }
 
@@ -595,36 +746,50 @@ int surfel_commit(cudaStream_t s, SurfelScratch& ws, SurfelArrays m, int n, int 
   const int C = 1 + D;
   const int P = w * h;
   const SurfCam cam = make_cam(c2w12, k4, w, h);
-  if (grow(ws.seg, ws.seg_cap, static_cast<size_t>(n) + 2)) return 5;
+  const size_t TT = static_cast<size_t>(std::max(T, 1));
+  if (grow(ws.seg, ws.seg_cap, 4 * TT + 2)) return 5;
   int* sorted_idx = ws.pidx + T;  // second half of pidx
-  if (grow(ws.order, ws.order_cap, 2 * static_cast<size_t>(T) + 2)) return 5;
+  if (grow(ws.order, ws.order_cap, 2 * TT + 2)) return 5;
   int* qin = ws.order;
   int* qout = ws.order + T;
+  int* flag = ws.seg;
+  int* rank = ws.seg + TT;
+  int* ustart = ws.seg + 2 * TT;
+  int* usurf = ws.seg + 3 * TT + 1;
   size_t t1 = 0, t2 = 0;
   int bits = 1;
   while (bits < 31 && (1 << bits) < n) ++bits;
-  cub::DeviceRadixSort::SortPairs(nullptr, t1, ws.pidx, sorted_idx, qin, qout, std::max(T, 1), 0, bits, s);
-  cub::DeviceScan::ExclusiveSum(nullptr, t2, ws.seg, ws.seg, n + 1, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, ws.pidx, sorted_idx, qin, qout, static_cast<int>(TT), 0, bits, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, flag, rank, static_cast<int>(TT), s);
   if (grow(ws.cub, ws.cub_cap, std::max(t1, t2))) return 5;
   const CommitArgs a{radius_scale, frame};
-  cudaMemsetAsync(ws.seg, 0, sizeof(int) * (n + 1), s);
   if (T > 0) {
     launch_pdl(k_fill_iota, dim3(grid1(T)), dim3(256), 0, s, qin, T);
     size_t b = ws.cub_cap;
     cub::DeviceRadixSort::SortPairs(ws.cub, b, ws.pidx, sorted_idx, qin, qout, T, 0, bits, s);  // stable by surfel
-    launch_pdl(k_sf_seg_count, dim3(grid1(T)), dim3(256), 0, s, static_cast<const int*>(ws.pidx), T, ws.seg);
+    launch_pdl(k_sf_seg_flags, dim3(grid1(T)), dim3(256), 0, s, static_cast<const int*>(sorted_idx), T, flag);
     b = ws.cub_cap;
-    cub::DeviceScan::ExclusiveSum(ws.cub, b, ws.seg, ws.seg, n + 1, s);
+    cub::DeviceScan::ExclusiveSum(ws.cub, b, flag, rank, T, s);
+    launch_pdl(k_sf_seg_write, dim3(grid1(T)), dim3(256), 0, s, static_cast<const int*>(sorted_idx),
+               static_cast<const int*>(flag), static_cast<const int*>(rank), T, ustart, usurf);
+    int hv[2];
+    cudaMemcpyAsync(&hv[0], rank + T - 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&hv[1], flag + T - 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return 4;
+    const int U = hv[0] + hv[1];
+    const long long threads = static_cast<long long>(U) * kLanes;
     if (D > 0)
-      launch_pdl(k_sf_commit<L<1>>, dim3(grid1(n, 128)), dim3(128), 0, s, n, D, cam, static_cast<const int*>(ws.seg),
-                 static_cast<const int*>(qout), static_cast<const int*>(ws.ppix), static_cast<const double*>(ws.pw),
-                 static_cast<const double*>(ws.V), static_cast<const double*>(ws.VW),
-                 static_cast<const double*>(ws.NW), a, m.pos, m.nrm, m.conf, m.rad, m.ts);
+      launch_pdl(k_sf_commit_u<L<1>>, dim3(grid1(threads, 128)), dim3(128), 0, s, U, D, cam,
+                 static_cast<const int*>(ustart), static_cast<const int*>(usurf), static_cast<const int*>(qout),
+                 static_cast<const int*>(ws.ppix), static_cast<const double*>(ws.pw), static_cast<const double*>(ws.V),
+                 static_cast<const double*>(ws.VW), static_cast<const double*>(ws.NW), a, m.pos, m.nrm, m.conf, m.rad,
+                 m.ts);
     else
-      launch_pdl(k_sf_commit<double>, dim3(grid1(n, 128)), dim3(128), 0, s, n, D, cam, static_cast<const int*>(ws.seg),
-                 static_cast<const int*>(qout), static_cast<const int*>(ws.ppix), static_cast<const double*>(ws.pw),
-                 static_cast<const double*>(ws.V), static_cast<const double*>(ws.VW),
-                 static_cast<const double*>(ws.NW), a, m.pos, m.nrm, m.conf, m.rad, m.ts);
+      launch_pdl(k_sf_commit_u<double>, dim3(grid1(threads, 128)), dim3(128), 0, s, U, D, cam,
+                 static_cast<const int*>(ustart), static_cast<const int*>(usurf), static_cast<const int*>(qout),
+                 static_cast<const int*>(ws.ppix), static_cast<const double*>(ws.pw), static_cast<const double*>(ws.V),
+                 static_cast<const double*>(ws.VW), static_cast<const double*>(ws.NW), a, m.pos, m.nrm, m.conf, m.rad,
+                 m.ts);
   }
   launch_pdl(k_sf_create, dim3(grid1(P)), dim3(256), 0, s, static_cast<const int*>(ws.pint + 3 * P),
              static_cast<const int*>(ws.pint + 4 * P), P, n, D, cam, a, static_cast<const double*>(ws.V),
