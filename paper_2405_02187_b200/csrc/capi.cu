@@ -15,7 +15,9 @@
 #include <string>
 #include <sstream>
 #include <fstream>
+#include <atomic>
 #include <limits>
+#include <mutex>
 #include <memory>
 #include <vector>
 
@@ -111,6 +113,8 @@ Launch launch_of(csf_ctx ctx) { return Launch{ctx->stream, ctx->d_err, &ctx->lau
 int sync_check(csf_ctx ctx, const char* what) {
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(ctx, cudaGetLastError());
+  char lmsg[256];
+  if (take_launch_error(lmsg, sizeof(lmsg))) return fail(ctx, CSF_ECUDA, std::string(what) + ": " + lmsg);
   int err = 0;
   CUDA_TRY(ctx, cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err != 0) {
@@ -1007,6 +1011,8 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
     launch_objective(L, p->G, p->Dp, p->D, p->traj.p, p->gt.p, n_frames, cfg.objective, cfg.h, p->out.p);
   p->n_run = n_frames;
   CUDA_TRY(ctx, cudaGetLastError());
+  char lmsg[256];
+  if (take_launch_error(lmsg, sizeof(lmsg))) return fail(ctx, CSF_ECUDA, std::string("csf_pipeline_run: ") + lmsg);
   return CSF_OK;
 }
 
@@ -2410,3 +2416,24 @@ extern "C" double csf_sample_confidence(const csf_intrinsics* k, int x, int y) {
   g = g < 0.0 ? 0.0 : (1.0 < g ? 1.0 : g);
   return csf_det::exp(-g * g / 0.72);
 }
+
+// ---- sticky launch-error record (csf_internal.h)
+namespace csfi {
+static std::mutex g_launch_mu;
+static std::string g_launch_msg;
+static std::atomic<int> g_launch_pending{0};
+void note_launch_error(const char* what, cudaError_t e) {
+  std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  if (!g_launch_pending.load()) g_launch_msg = std::string("launch of ") + what + " failed: " + cudaGetErrorString(e);
+  g_launch_pending.store(1);
+}
+bool take_launch_error(char* msg, size_t cap) {
+  if (!g_launch_pending.load()) return false;
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  std::snprintf(msg, cap, "%s", g_launch_msg.c_str());
+  g_launch_pending.store(0);
+  return true;
+}
+}  // namespace csfi
+

@@ -165,6 +165,12 @@ int surfel_predict(cudaStream_t s, SurfelScratch& ws, const double* pos, const d
                    const double* c2w12, const double* k4, int w, int h, double* Vo, double* No);
 void surfel_scratch_release(SurfelScratch& ws);
 
+// Launch failures seen by the kernel translation units are recorded here and
+// surfaced as CSF_ECUDA by the next status check of the C-ABI (a failed
+// launch must never yield silently wrong results).
+void note_launch_error(const char* what, cudaError_t e);
+bool take_launch_error(char* msg, size_t cap);
+
 struct Launch {
   cudaStream_t stream;
   int* err;                // device error flag

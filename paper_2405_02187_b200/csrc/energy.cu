@@ -335,7 +335,7 @@ using namespace csfd;
 
 static void chk(const char* what) {
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
+  if (e != cudaSuccess) note_launch_error(what, e);
 }
 
 // pairwise_sum (diff.hpp:16-37) of every slot of terms [C][n] (n > 0) into

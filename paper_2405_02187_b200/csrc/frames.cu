@@ -171,9 +171,7 @@ namespace csfi {
 
 static void check_launch(const char* what) {
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
-  }
+  if (e != cudaSuccess) note_launch_error(what, e);
 }
 
 void launch_bilateral(const Launch& L, const float* in_f32, const double* in_f64, double* raw_out, double* out, int w,

@@ -926,7 +926,7 @@ using namespace csfd;
 
 static void chk(const char* what) {
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
+  if (e != cudaSuccess) note_launch_error(what, e);
 }
 
 #define CSF_DISPATCH_G(G, BODY)                       \
@@ -981,6 +981,16 @@ size_t icp_counts_ints(int max_tiles) {
 // sums) then k_icp_solve_t.  Scratch layout: partials = [tiles][27C] then
 // [groups][27C]; counts = [kMaxGroupCtr] self-resetting group counters (zero
 // at allocation), [tiles], [groups].
+// Dynamic shared memory above the 48 KB default needs the opt-in; the
+// threshold is on static + dynamic bytes, so opt in for every size (once per
+// kernel and high-water mark).
+static void opt_in_smem(const void* fn, size_t smem, size_t* set) {
+  if (smem <= *set) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  *set = smem;
+}
+static size_t smem_set[3] = {0, 0, 0};
+
 void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const double* depth, int w, int h,
                        int stride, const double* intr, double* pose, const double* vre, const double* nre,
                        const double* vim, const double* nim, double d_max, double cos_max, double* partials,
@@ -1008,22 +1018,19 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
   const int RG = G == 0 ? 0 : (std::getenv("CSF_ICP_RG2") ? (Dp % 2 == 0 ? 2 : 1) : 1);
   switch (RG) {
     case 0:
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_icp_reduce<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      opt_in_smem(reinterpret_cast<const void*>(k_icp_reduce<0>), smem, &smem_set[0]);
       launch_pdl(k_icp_reduce<0>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
                  pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
                  pose, level, tol, fused ? 1 : 0);
       break;
     case 1:
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_icp_reduce<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      opt_in_smem(reinterpret_cast<const void*>(k_icp_reduce<1>), smem, &smem_set[1]);
       launch_pdl(k_icp_reduce<1>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
                  pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
                  pose, level, tol, fused ? 1 : 0);
       break;
     default:
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_icp_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      opt_in_smem(reinterpret_cast<const void*>(k_icp_reduce<2>), smem, &smem_set[2]);
       launch_pdl(k_icp_reduce<2>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
                  pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
                  pose, level, tol, fused ? 1 : 0);

@@ -282,7 +282,7 @@ using namespace csfd;
 
 static void chk(const char* what) {
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
+  if (e != cudaSuccess) note_launch_error(what, e);
 }
 
 static int grid_of(long long n) {

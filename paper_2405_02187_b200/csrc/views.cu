@@ -134,7 +134,7 @@ void launch_view_terms(const Launch& L, const HashDev& v, const double* vre, con
   launch_pdl(k_view_terms, dim3((P + 127) / 128), dim3(128), 0, L.stream, view, vre, nre, vim, P, w0, beta, terms);
   ++*L.launches;
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) std::fprintf(stderr, "csf_b200: launch of view_terms failed: %s\n", cudaGetErrorString(e));
+  if (e != cudaSuccess) note_launch_error("view_terms", e);
 }
 
 }  // namespace csfi
