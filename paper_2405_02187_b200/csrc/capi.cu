@@ -162,6 +162,7 @@ struct csf_volume_s {
   DevBuf<double> fim;
   DevBuf<int> heads, next, coords, nblocks, grid;
   DevBuf<unsigned> occ;
+  DevBuf<unsigned char> sdist;
   DevBuf<unsigned long long> keys;
   // allocation scratch (hashed)
   AllocScratch alloc{};
@@ -181,6 +182,7 @@ struct csf_volume_s {
     rw.release(); fim.release(); heads.release(); next.release(); coords.release(); nblocks.release(); keys.release();
     grid.release();
     occ.release();
+    sdist.release();
     a_cand.release(); a_set_keys.release(); a_cand_block.release(); a_first_flag.release(); a_new_flag.release();
     a_first_rank.release(); a_new_rank.release(); a_set_first.release(); a_set_slot.release(); a_visible.release();
     a_counters.release(); a_cub.release();
@@ -566,7 +568,8 @@ static int create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, 
   const int gbits = 9;  // 512^3 block-id window (512 MiB of int32)
   const size_t ng = size_t(1) << (3 * gbits);
   const size_t nocc = (size_t(1) << (3 * (gbits - 3))) / 32;
-  if (v->grid.alloc(ng) != cudaSuccess || v->occ.alloc(nocc) != cudaSuccess) {
+  const size_t nsb = size_t(1) << (3 * (gbits - 3));
+  if (v->grid.alloc(ng) != cudaSuccess || v->occ.alloc(nocc) != cudaSuccess || v->sdist.alloc(2 * nsb) != cudaSuccess) {
     delete v;
     return fail(ctx, CSF_ENOMEM, "csf_volume_create_hashed: out of device memory (block grid)");
   }
@@ -588,6 +591,8 @@ static int create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, 
   d.n_blocks = v->nblocks.p;
   d.grid = v->grid.p;
   d.occ = v->occ.p;
+  d.sdist = v->sdist.p;
+  d.sdist_tmp = v->sdist.p + nsb;
   d.gbits = gbits;
   d.bits = p->bucket_bits;
   d.max_blocks = p->max_blocks;
@@ -601,6 +606,7 @@ static int create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, 
   cudaMemsetAsync(d.n_blocks, 0, sizeof(int), ctx->stream);
   cudaMemsetAsync(d.grid, 0xFF, sizeof(int) * ng, ctx->stream);
   cudaMemsetAsync(d.occ, 0, sizeof(unsigned) * nocc, ctx->stream);
+  launch_super_dist(ctx->stream, d);
   launch_init_volume(launch_of(ctx), d.rw, d.fim, v->n_vox, v->Dp);
   rc = sync_check(ctx, "csf_volume_create_hashed");
   if (rc) {
@@ -929,6 +935,7 @@ static int pipeline_reset_volume(csf_pipeline p) {
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.grid, 0xFF, sizeof(int) << (3 * v->hash.gbits), ctx->stream));
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.occ, 0, sizeof(unsigned) * ((size_t(1) << (3 * (v->hash.gbits - 3))) / 32),
                                     ctx->stream));
+      launch_super_dist(ctx->stream, v->hash);
       launch_init_volume(L, v->hash.rw, v->hash.fim, static_cast<long long>(nb) * 512, v->Dp);
     }
   } else {
@@ -1350,6 +1357,7 @@ extern "C" int csf_volume_load(csf_ctx ctx, const char* path, int n_channels, cs
     CUDA_TRY(ctx, cudaMemcpy(v->hash.coords, coords.data(), sizeof(int32_t) * coords.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(ctx, cudaMemcpy(v->hash.n_blocks, &nb, sizeof(int), cudaMemcpyHostToDevice));
     launch_rebuild_index(ctx->stream, v->hash.coords, nb, v->hash.grid, v->hash.occ, v->hash.gbits);
+    launch_super_dist(ctx->stream, v->hash);
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   }
   const int C = 1 + D;

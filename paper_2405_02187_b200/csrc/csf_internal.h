@@ -32,6 +32,9 @@ struct HashDev {
   int* n_blocks;                // device counter
   int* grid;                    // [2^(3*gbits)] dense block-id window (derived index)
   unsigned* occ;                // [2^(3*(gbits-3))/32] super-block occupancy bits
+  unsigned char* sdist = nullptr;  // [2^(3*(gbits-3))] Chebyshev distance (super-blocks) to the
+                                   // nearest occupied / out-of-window super-block, capped at 8
+  unsigned char* sdist_tmp = nullptr;
   int bits, max_blocks, gbits;
   double vs, ox, oy, oz, mu, cap;
   int order = 1;  // CSFD order of the channel slots (2: bicomplex pairs, 3 slots each)
@@ -201,6 +204,8 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
                            int w, int h, double near_clip, double far_clip, double step, double2* hits, double* vre,
                            double* nre, double* vim, double* nim);
 void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp);
+// super-block distance field of the occupancy bitmap (after every change of occ)
+void launch_super_dist(cudaStream_t stream, const HashDev& v);
 // point queries (tsdf.hpp:97-196): pts [n][3][1+Dp] lifted (sample) or [n][3] real (measured)
 void launch_sample_points(const Launch& L, bool hashed, const DenseDev& dd, const HashDev& hd, int Dp,
                           const double* pts, int n, int grad, double* out, int* valid);

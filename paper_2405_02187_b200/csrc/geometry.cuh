@@ -69,6 +69,7 @@ struct HashView {
   const int* next;
   const int* grid;
   const unsigned* occ;  // one bit per 8^3-block super-block of the window
+  const unsigned char* sdist;  // Chebyshev distance to the nearest occupied super-block (0: occupied)
   unsigned mask;
   int gbits;
   double vs, ox, oy, oz, mu, cap;
@@ -105,6 +106,17 @@ struct HashView {
     const int sb = gbits - 3;
     const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
     return (__ldg(occ + (bit >> 5)) >> (bit & 31)) & 1u;
+  }
+  // d > 0: every super-block within Chebyshev distance d - 1 of this one is
+  // inside the window and empty; 0: occupied or outside the window.
+  CSF_DEV int super_dist(int bx, int by, int bz) const {
+    const int half = 1 << (gbits - 1);
+    const unsigned ux = static_cast<unsigned>(bx + half), uy = static_cast<unsigned>(by + half),
+                   uz = static_cast<unsigned>(bz + half);
+    const unsigned side = 1u << gbits;
+    if (!(ux < side && uy < side && uz < side)) return 0;
+    const int sb = gbits - 3;
+    return __ldg(sdist + ((((uz >> 3) << sb | (uy >> 3)) << sb) | (ux >> 3)));
   }
   CSF_DEV long long voxel(int i, int j, int k) const {
     const int b = block(i >> 3, j >> 3, k >> 3);

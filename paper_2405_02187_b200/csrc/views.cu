@@ -127,6 +127,7 @@ void launch_view_terms(const Launch& L, const HashDev& v, const double* vre, con
   view.next = v.next;
   view.grid = v.grid;
   view.occ = v.occ;
+  view.sdist = v.sdist;
   view.gbits = v.gbits;
   view.mask = (1u << v.bits) - 1u;
   view.vs = v.vs; view.ox = v.ox; view.oy = v.oy; view.oz = v.oz; view.mu = v.mu; view.cap = v.cap;

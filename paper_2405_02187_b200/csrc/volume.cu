@@ -683,15 +683,22 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
         const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
                   k0 = ifloor((pz - vol.oz) / vol.vs);
         const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
-        const int occ = vol.super_occupied(bx, by, bz);
-        int span = 0;
-        if (occ == 0) span = 8;
-        else if (vol.block(bx, by, bz) < 0) span = 1;
+        // empty space: the cube of (2d - 1)^3 empty super-blocks around this
+        // one (distance field), else this unallocated block
+        const int sd = vol.super_dist(bx, by, bz);
+        int span = 0, lx = bx, ly = by, lz = bz;
+        if (sd > 0) {
+          span = 8 * (2 * sd - 1);
+          lx = ((bx >> 3) - (sd - 1)) << 3;
+          ly = ((by >> 3) - (sd - 1)) << 3;
+          lz = ((bz >> 3) - (sd - 1)) << 3;
+        } else if (vol.block(bx, by, bz) < 0) {
+          span = 1;
+        }
         if (span > 0) {
           have_prev = false;
-          CSF_MSTAT(if (span == 8) ++sskip; else ++bskip;)
-          const int m = span == 8 ? ~7 : ~0;
-          const double lim = box_exit(vol, bx & m, by & m, bz & m, span, o, invd) - 1e-6;
+          CSF_MSTAT(if (span >= 8) ++sskip; else ++bskip;)
+          const double lim = box_exit(vol, lx, ly, lz, span, o, invd) - 1e-6;
           // first index > n whose alpha reaches lim (or the sentinel)
           int g = static_cast<int>(fmin(fmax((lim - atab[0]) * inv_step, 0.0), static_cast<double>(nmax)));
           g = g < n + 1 ? n + 1 : g;
@@ -827,14 +834,19 @@ __global__ void __launch_bounds__(128) k_raycast_march_seg(HashView vol, const d
     const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
               k0 = ifloor((pz - vol.oz) / vol.vs);
     const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
-    const int occ = vol.super_occupied(bx, by, bz);
-    int span = 0;
-    if (occ == 0) span = 8;
-    else if (vol.block(bx, by, bz) < 0) span = 1;
+    const int sd = vol.super_dist(bx, by, bz);
+    int span = 0, lx = bx, ly = by, lz = bz;
+    if (sd > 0) {
+      span = 8 * (2 * sd - 1);
+      lx = ((bx >> 3) - (sd - 1)) << 3;
+      ly = ((by >> 3) - (sd - 1)) << 3;
+      lz = ((bz >> 3) - (sd - 1)) << 3;
+    } else if (vol.block(bx, by, bz) < 0) {
+      span = 1;
+    }
     if (span > 0) {
       have_prev = false;
-      const int m = span == 8 ? ~7 : ~0;
-      const double lim = box_exit(vol, bx & m, by & m, bz & m, span, o, invd) - 1e-6;
+      const double lim = box_exit(vol, lx, ly, lz, span, o, invd) - 1e-6;
       int g = static_cast<int>(fmin(fmax((lim - atab[0]) * inv_step, 0.0), static_cast<double>(nmax)));
       g = g < n + 1 ? n + 1 : g;
       while (g > n + 1 && __ldg(atab + g - 1) >= lim) --g;
@@ -1553,6 +1565,7 @@ static HashView hash_view(const HashDev& v, int Dp) {
   d.heads = v.heads; d.keys = v.keys; d.next = v.next;
   d.grid = v.grid;
   d.occ = v.occ;
+  d.sdist = v.sdist;
   d.gbits = v.gbits;
   d.mask = (1u << v.bits) - 1u;
   d.vs = v.vs; d.ox = v.ox; d.oy = v.oy; d.oz = v.oz; d.mu = v.mu; d.cap = v.cap;
@@ -1685,6 +1698,47 @@ void launch_measured_points(const Launch& L, const double* depth, int w, int h, 
   chk("measured_points");
 }
 
+// Super-block distance field: separable L-infinity distance transform of the
+// occupancy bitmap over the 2^(gbits-3) cube of super-blocks, capped at 8;
+// cells outside the window count as occupied (unknown).
+__global__ void k_sdist_axis(const unsigned* __restrict__ occ, const unsigned char* __restrict__ in, int sb, int axis,
+                             unsigned char* __restrict__ out) {
+  const int n = 1 << sb;
+  const long long cell = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (cell >= (1LL << (3 * sb))) return;
+  const int x = static_cast<int>(cell & (n - 1)), y = static_cast<int>((cell >> sb) & (n - 1)),
+            z = static_cast<int>(cell >> (2 * sb));
+  const int c[3] = {x, y, z};
+  int best = 8;
+  for (int d = -7; d <= 7; ++d) {
+    int q[3] = {c[0], c[1], c[2]};
+    q[axis] += d;
+    const int ad = d < 0 ? -d : d;
+    int v;
+    if (q[axis] < 0 || q[axis] >= n) {
+      v = 0;  // outside the window: treated as occupied
+    } else {
+      const long long qc = (static_cast<long long>(q[2]) << (2 * sb)) | (static_cast<long long>(q[1]) << sb) | q[0];
+      v = in ? in[qc] : static_cast<int>(!((occ[qc >> 5] >> (qc & 31)) & 1u)) * 8;  // 0 occupied, 8 empty
+    }
+    const int m = ad > v ? ad : v;
+    best = m < best ? m : best;
+  }
+  out[cell] = static_cast<unsigned char>(best);
+}
+
+void launch_super_dist(cudaStream_t stream, const HashDev& v) {
+  if (!v.sdist || !v.sdist_tmp) return;
+  const int sb = v.gbits - 3;
+  const long long cells = 1LL << (3 * sb);
+  const int grid = static_cast<int>((cells + 255) / 256);
+  k_sdist_axis<<<grid, 256, 0, stream>>>(v.occ, nullptr, sb, 0, v.sdist_tmp);
+  k_sdist_axis<<<grid, 256, 0, stream>>>(v.occ, v.sdist_tmp, sb, 1, v.sdist);
+  k_sdist_axis<<<grid, 256, 0, stream>>>(v.occ, v.sdist, sb, 2, v.sdist_tmp);
+  cudaMemcpyAsync(v.sdist, v.sdist_tmp, static_cast<size_t>(cells), cudaMemcpyDeviceToDevice, stream);
+  chk("super_dist");
+}
+
 void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp) {
   launch_pdl(k_init_volume, dim3(sm_count() * 8), dim3(256), 0, L.stream, rw, fim, n, Dp);
   ++*L.launches;
@@ -1792,7 +1846,8 @@ void launch_allocate(const Launch& L, const HashDev& v, int Dp, AllocScratch& a,
                                     a.first_flag, a.new_flag, a.first_rank, a.new_rank, a.cand_block, a.visible, L.err);
   launch_pdl(k_alloc_finalize, dim3(1), dim3(1), 0, L.stream, v.n_blocks, v.max_blocks, a.first_flag, a.new_flag, a.first_rank,
                                           a.new_rank, n, a.counters);
-  *L.launches += 7;
+  launch_super_dist(L.stream, v);
+  *L.launches += 10;
   chk("allocate");
 }
 
