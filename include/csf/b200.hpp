@@ -379,6 +379,87 @@ inline NnError eval_nn_error(Context& c, const std::array<double, 12>& transform
 }
 
 // ---------------------------------------------------------------------------
+// surfel.hpp — the surfel (X-EF) front end; the map lives on the device with
+// D derivative channels (the reference's Complex is D = 1).
+// ---------------------------------------------------------------------------
+struct SurfelHost {  // surfel.hpp:16-22, channels unpacked
+  std::vector<double> position, normal;  // [3][1+D]
+  double radius = 0.0;
+  std::vector<double> confidence;  // [1+D]
+  int timestamp = 0;
+};
+inline csf_surfel_cfg default_surfel_config() {
+  csf_surfel_cfg c;
+  csf_default_surfel_cfg(&c);
+  return c;
+}
+struct SurfelUpdateStats {  // surfel.hpp:93-96
+  int merged_pixels = 0;
+  int created = 0;
+};
+class SurfelMap {
+ public:
+  SurfelMap(Context& c, int channels = 1) : ctx_(c.get()), channels_(channels) {
+    check(ctx_, csf_surfels_create(ctx_, channels, &m_));
+  }
+  ~SurfelMap() { csf_surfels_destroy(m_); }
+  SurfelMap(const SurfelMap&) = delete;
+  SurfelMap& operator=(const SurfelMap&) = delete;
+  csf_surfels get() const { return m_; }
+  csf_ctx ctx() const { return ctx_; }
+  int channels() const { return channels_; }
+  std::size_t size() const {
+    int n = 0;
+    check(ctx_, csf_surfels_count(m_, &n));
+    return static_cast<std::size_t>(n);
+  }
+  std::vector<SurfelHost> download() const {
+    const std::size_t n = size(), C = 1 + channels_;
+    std::vector<double> p(3 * n * C), q(3 * n * C), r(n), c(n * C);
+    std::vector<int32_t> t(n);
+    if (n) check(ctx_, csf_surfels_download(m_, p.data(), q.data(), r.data(), c.data(), t.data()));
+    std::vector<SurfelHost> out(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      out[i].position.assign(p.begin() + 3 * i * C, p.begin() + 3 * (i + 1) * C);
+      out[i].normal.assign(q.begin() + 3 * i * C, q.begin() + 3 * (i + 1) * C);
+      out[i].radius = r[i];
+      out[i].confidence.assign(c.begin() + i * C, c.begin() + (i + 1) * C);
+      out[i].timestamp = t[i];
+    }
+    return out;
+  }
+
+ private:
+  csf_ctx ctx_;
+  csf_surfels m_ = nullptr;
+  int channels_ = 1;
+};
+// surfel.cpp:121-236: depth [h][w][1+D] lifted, pose lifted (channels = map's)
+inline SurfelUpdateStats update_surfels(SurfelMap& map, const std::vector<double>& lifted_depth, int w, int h,
+                                        const LiftedPose& camera_to_world, const csf_intrinsics& k, int frame_index,
+                                        const csf_surfel_cfg& cfg = default_surfel_config()) {
+  if (camera_to_world.channels != map.channels())
+    throw std::invalid_argument("update_surfels: channel count mismatch");
+  SurfelUpdateStats s;
+  check(map.ctx(), csf_update_surfels(map.get(), lifted_depth.data(), w, h, camera_to_world.v.data(), &k, frame_index,
+                                      &cfg, &s.merged_pixels, &s.created));
+  return s;
+}
+// surfel.cpp:238-263
+inline SurfaceMaps predict_maps(const SurfelMap& map, const std::array<double, 12>& camera_to_world,
+                                const csf_intrinsics& k) {
+  SurfaceMaps m;
+  m.width = k.width;
+  m.height = k.height;
+  m.vertices.resize(3 * static_cast<std::size_t>(k.width) * k.height);
+  m.normals.resize(m.vertices.size());
+  check(map.ctx(), csf_predict_maps(map.get(), camera_to_world.data(), &k, m.vertices.data(), m.normals.data()));
+  return m;
+}
+// surfel.cpp:110-119
+inline double sample_confidence(const csf_intrinsics& k, int x, int y) { return csf_sample_confidence(&k, x, y); }
+
+// ---------------------------------------------------------------------------
 // dataset.hpp:17-36 — on-disk formats (host file I/O; std::runtime_error)
 // ---------------------------------------------------------------------------
 namespace detail {

@@ -8,6 +8,7 @@
 #include "csf/b200.hpp"
 #include "orc_pipeline.hpp"
 #include "orc_reloc.hpp"
+#include "orc_surfel.hpp"
 
 namespace B = csf::b200;
 
@@ -280,6 +281,43 @@ int main() {
     CHECK(rg.iterations > 0 && rg.final_loss < orc::reloc_loss(po, init));
     std::printf("ok   reloc energy/gradient/Hessian and Newton relocalize bit-identical (%d iterations, loss %.3e)\n",
                 rg.iterations, rg.final_loss);
+  }
+
+  {  // surfel.cpp:121-263 — update_surfels / predict_maps through the C++ mirror vs the restatement
+    B::SurfelMap mg(ctx, 1);
+    orc::SurfelMapT<orc::Lifted<1>> mo;
+    for (int f = 0; f < 3; ++f) {
+      const orc::Image<double> d = orc::render_depth(sphere, poses[f], ko);
+      std::vector<double> lifted(2 * d.data.size(), 0.0);
+      orc::Image<orc::Lifted<1>> dl(d.width, d.height, orc::Lifted<1>(0.0));
+      for (std::size_t i = 0; i < d.data.size(); ++i) {
+        lifted[2 * i] = d.data[i];
+        dl.data[i] = orc::Lifted<1>(d.data[i]);
+      }
+      B::LiftedPose lp = B::LiftedPose::real(arr(poses[f]), 1);
+      lp.at(9, 1) = 1e-8;  // seed tx
+      orc::PoseT<orc::Lifted<1>> op = orc::pose_cast<orc::Lifted<1>>(poses[f]);
+      op.translation[0].im[0] = 1e-8;
+      const auto sg = B::update_surfels(mg, lifted, d.width, d.height, lp, k, f);
+      const auto so = orc::update_surfels(mo, dl, op, ko, f);
+      CHECK(sg.merged_pixels == so.merged_pixels && sg.created == so.created);
+    }
+    const auto hs = mg.download();
+    bool same = hs.size() == mo.size();
+    for (std::size_t i = 0; same && i < hs.size(); ++i)
+      for (int c = 0; c < 3; ++c)
+        same = same && hs[i].position[2 * c] == mo.surfels[i].position[c].re &&
+               hs[i].position[2 * c + 1] == mo.surfels[i].position[c].im[0] &&
+               hs[i].normal[2 * c] == mo.surfels[i].normal[c].re && hs[i].radius == mo.surfels[i].radius &&
+               hs[i].confidence[0] == mo.surfels[i].confidence.re;
+    CHECK(same);
+    const B::SurfaceMaps pm = B::predict_maps(mg, arr(poses[1]), k);
+    const auto po = orc::predict_maps(mo, poses[1], ko);
+    bool psame = true;
+    for (std::size_t i = 0; i < po.vertices.data.size(); ++i)
+      for (int c = 0; c < 3; ++c) psame = psame && pm.vertices[3 * i + c] == po.vertices.data[i][c];
+    CHECK(psame);
+    std::printf("ok   surfel update / predict bit-identical to the restatement (%zu surfels)\n", hs.size());
   }
 
   {  // error behaviour: invalid arguments throw std::invalid_argument
