@@ -116,9 +116,9 @@ int sync_check(csf_ctx ctx, const char* what) {
   char lmsg[256];
   if (take_launch_error(lmsg, sizeof(lmsg))) return fail(ctx, CSF_ECUDA, std::string(what) + ": " + lmsg);
   int err = 0;
-  CUDA_TRY(ctx, cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   if (err != 0) {
-    cudaMemset(ctx->d_err, 0, sizeof(int));
+    cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream);
     if (err == 2) return fail(ctx, CSF_EDOMAIN, std::string(what) + ": division by a zero real part");
     if (err == 5) return fail(ctx, CSF_ENOMEM, std::string(what) + ": hashed volume capacity exhausted");
     return fail(ctx, CSF_ERUNTIME, std::string(what) + ": device error");
@@ -294,7 +294,7 @@ int ensure_alpha_table(csf_volume v, double near_clip, double far_clip, double s
   a.push_back(alpha);  // sentinel > far
   CUDA_TRY(v->ctx, cudaStreamSynchronize(v->ctx->stream));
   CUDA_TRY(v->ctx, v->alpha_tab.alloc(a.size()));
-  CUDA_TRY(v->ctx, cudaMemcpy(v->alpha_tab.p, a.data(), sizeof(double) * a.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(v->ctx, cudaMemcpyAsync(v->alpha_tab.p, a.data(), sizeof(double) * a.size(), cudaMemcpyHostToDevice, v->ctx->stream));
   v->tab_near = near_clip;
   v->tab_far = far_clip;
   v->tab_step = step;
@@ -381,7 +381,9 @@ extern "C" int csf_ctx_create(int device, csf_ctx* out) {
   csf_ctx ctx = new csf_ctx_s();
   ctx->device = device;
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_err, 0, sizeof(int)) != cudaSuccess) {
+      cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess ||
+      cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
     delete ctx;
     return CSF_ECUDA;
   }
@@ -640,7 +642,7 @@ extern "C" int csf_volume_block_count(csf_volume v, int* n) {
   }
   cudaSetDevice(v->ctx->device);
   CUDA_TRY(v->ctx, cudaStreamSynchronize(v->ctx->stream));
-  CUDA_TRY(v->ctx, cudaMemcpy(n, v->hash.n_blocks, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(v->ctx, cudaMemcpyAsync(n, v->hash.n_blocks, sizeof(int), cudaMemcpyDeviceToHost, v->ctx->stream));
   return CSF_OK;
 }
 
@@ -663,8 +665,8 @@ extern "C" int csf_volume_upload(csf_volume v, const double* field, const double
     rw[i] = make_double2(field[i * C], weight[i]);
     for (int d = 0; d < v->D; ++d) fim[i * v->Dp + d] = field[i * C + 1 + d];
   }
-  CUDA_TRY(ctx, cudaMemcpy(v->rw.p, rw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
-  if (v->Dp > 0) CUDA_TRY(ctx, cudaMemcpy(v->fim.p, fim.data(), sizeof(double) * n * v->Dp, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpyAsync(v->rw.p, rw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, ctx->stream));
+  if (v->Dp > 0) CUDA_TRY(ctx, cudaMemcpyAsync(v->fim.p, fim.data(), sizeof(double) * n * v->Dp, cudaMemcpyHostToDevice, ctx->stream));
   return CSF_OK;
 }
 
@@ -676,8 +678,8 @@ extern "C" int csf_volume_download(csf_volume v, double* field, double* weight) 
   const long long n = volume_voxels_now(v);
   std::vector<double2> rw(n);
   std::vector<double> fim(static_cast<size_t>(n) * std::max(v->Dp, 1));
-  CUDA_TRY(ctx, cudaMemcpy(rw.data(), v->rw.p, sizeof(double2) * n, cudaMemcpyDeviceToHost));
-  if (v->Dp > 0) CUDA_TRY(ctx, cudaMemcpy(fim.data(), v->fim.p, sizeof(double) * n * v->Dp, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpyAsync(rw.data(), v->rw.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (v->Dp > 0) CUDA_TRY(ctx, cudaMemcpyAsync(fim.data(), v->fim.p, sizeof(double) * n * v->Dp, cudaMemcpyDeviceToHost, ctx->stream));
   const int C = 1 + v->D;
   for (long long i = 0; i < n; ++i) {
     field[i * C] = rw[i].x;
@@ -693,10 +695,10 @@ extern "C" int csf_volume_download_hash(csf_volume v, int32_t* heads, uint64_t* 
   int nb = 0;
   const int rc = csf_volume_block_count(v, &nb);
   if (rc) return rc;
-  if (heads) CUDA_TRY(ctx, cudaMemcpy(heads, v->hash.heads, sizeof(int) << v->hash.bits, cudaMemcpyDeviceToHost));
-  if (keys) CUDA_TRY(ctx, cudaMemcpy(keys, v->hash.keys, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost));
-  if (next) CUDA_TRY(ctx, cudaMemcpy(next, v->hash.next, sizeof(int) * nb, cudaMemcpyDeviceToHost));
-  if (coords) CUDA_TRY(ctx, cudaMemcpy(coords, v->hash.coords, sizeof(int) * 3 * nb, cudaMemcpyDeviceToHost));
+  if (heads) CUDA_TRY(ctx, cudaMemcpyAsync(heads, v->hash.heads, sizeof(int) << v->hash.bits, cudaMemcpyDeviceToHost, ctx->stream));
+  if (keys) CUDA_TRY(ctx, cudaMemcpyAsync(keys, v->hash.keys, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+  if (next) CUDA_TRY(ctx, cudaMemcpyAsync(next, v->hash.next, sizeof(int) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+  if (coords) CUDA_TRY(ctx, cudaMemcpyAsync(coords, v->hash.coords, sizeof(int) * 3 * nb, cudaMemcpyDeviceToHost, ctx->stream));
   return CSF_OK;
 }
 
@@ -721,7 +723,7 @@ extern "C" int csf_surface_update(csf_volume v, const double* depth, int w, int 
   if (rc) return rc;
   if (n_visible) {
     *n_visible = 0;
-    if (v->hashed) CUDA_TRY(ctx, cudaMemcpy(n_visible, v->alloc.counters, sizeof(int), cudaMemcpyDeviceToHost));
+    if (v->hashed) CUDA_TRY(ctx, cudaMemcpyAsync(n_visible, v->alloc.counters, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   }
   return CSF_OK;
 }
@@ -890,12 +892,13 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
     }
   }
   const double kb[4] = {cfg->k.fx, cfg->k.fy, cfg->k.cx, cfg->k.cy};
-  cudaMemcpy(p->kbase.p, kb, sizeof(kb), cudaMemcpyHostToDevice);
-  cudaMemcpy(p->dirs.p, cfg->dirs, sizeof(int) * CSF_MAX_DIRECTIONS, cudaMemcpyHostToDevice);
-  cudaMemcpy(p->pair_i.p, cfg->pair_i, sizeof(int) * CSF_MAX_PAIRS, cudaMemcpyHostToDevice);
-  cudaMemcpy(p->pair_j.p, cfg->pair_j, sizeof(int) * CSF_MAX_PAIRS, cudaMemcpyHostToDevice);
-  cudaMemset(p->st.p, 0, sizeof(TrackState));
-  cudaMemset(p->counts.p, 0, sizeof(int) * p->counts.n);
+  cudaMemcpyAsync(p->kbase.p, kb, sizeof(kb), cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(p->dirs.p, cfg->dirs, sizeof(int) * CSF_MAX_DIRECTIONS, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(p->pair_i.p, cfg->pair_i, sizeof(int) * CSF_MAX_PAIRS, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(p->pair_j.p, cfg->pair_j, sizeof(int) * CSF_MAX_PAIRS, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemsetAsync(p->st.p, 0, sizeof(TrackState), ctx->stream);
+  cudaMemsetAsync(p->counts.p, 0, sizeof(int) * p->counts.n, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
   *out = p;
   return CSF_OK;
 }
@@ -1031,7 +1034,7 @@ extern "C" int csf_pipeline_result(csf_pipeline p, double* gradient, double* obj
   int rc = sync_check(ctx, "csf_pipeline_run");
   if (rc) return rc;
   std::vector<double> out(2 + std::max(CSF_MAX_DIRECTIONS, 3 * CSF_MAX_PAIRS));
-  CUDA_TRY(ctx, cudaMemcpy(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, ctx->stream));
   if (objective) *objective = out[0];
   const double hh = p->cfg.h;
   if (gradient) {
@@ -1043,14 +1046,14 @@ extern "C" int csf_pipeline_result(csf_pipeline p, double* gradient, double* obj
   const int n = p->n_run;
   if (poses) {
     std::vector<double> t(static_cast<size_t>(n) * 12 * p->C);
-    CUDA_TRY(ctx, cudaMemcpy(t.data(), p->traj.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost));
+    CUDA_TRY(ctx, cudaMemcpyAsync(t.data(), p->traj.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost, ctx->stream));
     const int Cu = 1 + p->D;
     for (int f = 0; f < n; ++f)
       for (int e = 0; e < 12; ++e)
         for (int c = 0; c < Cu; ++c)
           poses[(static_cast<size_t>(f) * 12 + e) * Cu + c] = t[(static_cast<size_t>(f) * 12 + e) * p->C + c];
   }
-  if (stats) CUDA_TRY(ctx, cudaMemcpy(stats, p->stats.p, sizeof(int) * 8 * n, cudaMemcpyDeviceToHost));
+  if (stats) CUDA_TRY(ctx, cudaMemcpyAsync(stats, p->stats.p, sizeof(int) * 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
   return CSF_OK;
 }
 
@@ -1063,7 +1066,7 @@ extern "C" int csf_pipeline_hessian(csf_pipeline p, double* hessian, double* gra
   const int rc = csf_pipeline_result(p, nullptr, objective, poses, stats);
   if (rc) return rc;
   std::vector<double> out(2 + 3 * p->n_pairs);
-  CUDA_TRY(ctx, cudaMemcpy(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, ctx->stream));
   const double h = p->cfg.h;
   for (int q = 0; q < p->n_pairs; ++q) {
     if (hessian) hessian[q] = out[2 + 3 * q + 2] / (h * h);  // extract_hessian, csfd.hpp:319
@@ -1105,8 +1108,8 @@ static int sample_points_common(csf_volume v, const double* points, int n, int g
   CUDA_TRY(ctx, dout.alloc(std::max<size_t>(outn, 1)));
   CUDA_TRY(ctx, dv.alloc(std::max(n, 1)));
   if (n > 0) {
-    CUDA_TRY(ctx, cudaMemcpy(dp.p, pts.data(), sizeof(double) * pts.size(), cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemset(dout.p, 0, sizeof(double) * outn));
+    CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, pts.data(), sizeof(double) * pts.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(dout.p, 0, sizeof(double) * outn, ctx->stream));
   }
   launch_sample_points(launch_of(ctx), v->hashed, v->dense, v->hash, Dp, dp.p, n, grad, dout.p, dv.p);
   const int rc = sync_check(ctx, grad ? "csf_sample_gradient" : "csf_sample_tsdf");
@@ -1114,8 +1117,8 @@ static int sample_points_common(csf_volume v, const double* points, int n, int g
   std::vector<double> o(outn);
   std::vector<int> vv(std::max(n, 1));
   if (n > 0) {
-    CUDA_TRY(ctx, cudaMemcpy(o.data(), dout.p, sizeof(double) * outn, cudaMemcpyDeviceToHost));
-    CUDA_TRY(ctx, cudaMemcpy(vv.data(), dv.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(ctx, cudaMemcpyAsync(o.data(), dout.p, sizeof(double) * outn, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(vv.data(), dv.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
   }
   const size_t orow = static_cast<size_t>(n) * (grad ? 3 : 1);
   for (size_t r = 0; r < orow; ++r)
@@ -1150,21 +1153,21 @@ extern "C" int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h,
   double* d_intr = d_pose + 12 * C;
   double* d_center = d_intr + 4 * C;
   double* d_pts = d_center + 3 * C;
-  CUDA_TRY(ctx, cudaMemcpy(d_depth, depth, sizeof(double) * P, cudaMemcpyHostToDevice));
-  CUDA_TRY(ctx, cudaMemcpy(d_pose, world_to_camera, sizeof(double) * 12 * C, cudaMemcpyHostToDevice));
-  CUDA_TRY(ctx, cudaMemcpy(d_intr, intr, sizeof(double) * 4 * C, cudaMemcpyHostToDevice));
-  CUDA_TRY(ctx, cudaMemcpy(d_center, center, sizeof(double) * 3 * C, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_depth, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_pose, world_to_camera, sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_intr, intr, sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_center, center, sizeof(double) * 3 * C, cudaMemcpyHostToDevice, ctx->stream));
   if (n > 0) {
-    CUDA_TRY(ctx, cudaMemcpy(d_pts, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemset(dout.p, 0, sizeof(double) * n * C));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_pts, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(dout.p, 0, sizeof(double) * n * C, ctx->stream));
   }
   launch_measured_points(launch_of(ctx), d_depth, w, h, d_pose, d_intr, mu, d_pts, d_center, n, D, dout.p, dv.p);
   const int rc = sync_check(ctx, "csf_measured_tsdf");
   if (rc) return rc;
   if (n > 0) {
-    CUDA_TRY(ctx, cudaMemcpy(psi, dout.p, sizeof(double) * n * C, cudaMemcpyDeviceToHost));
+    CUDA_TRY(ctx, cudaMemcpyAsync(psi, dout.p, sizeof(double) * n * C, cudaMemcpyDeviceToHost, ctx->stream));
     std::vector<int> vv(n);
-    CUDA_TRY(ctx, cudaMemcpy(vv.data(), dv.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(ctx, cudaMemcpyAsync(vv.data(), dv.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
     for (int i = 0; i < n; ++i) valid[i] = vv[i];
   }
   return CSF_OK;
@@ -1213,7 +1216,7 @@ extern "C" int csf_volume_save(csf_volume v, const char* path) {
   if (v->hashed) {
     coords.resize(static_cast<size_t>(n / 512) * 3);
     if (!coords.empty())
-      CUDA_TRY(ctx, cudaMemcpy(coords.data(), v->hash.coords, sizeof(int32_t) * coords.size(), cudaMemcpyDeviceToHost));
+      CUDA_TRY(ctx, cudaMemcpyAsync(coords.data(), v->hash.coords, sizeof(int32_t) * coords.size(), cudaMemcpyDeviceToHost, ctx->stream));
   }
   bool any_im = false;
   for (long long i = 0; i < n && !any_im; ++i)
@@ -1351,11 +1354,11 @@ extern "C" int csf_volume_load(csf_ctx ctx, const char* path, int n_channels, cs
       *link = static_cast<int32_t>(b);
     }
     const int nb = static_cast<int>(n_blocks);
-    CUDA_TRY(ctx, cudaMemcpy(v->hash.heads, heads.data(), sizeof(int32_t) * heads.size(), cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(v->hash.next, next.data(), sizeof(int32_t) * n_blocks, cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(v->hash.keys, keys.data(), sizeof(uint64_t) * n_blocks, cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(v->hash.coords, coords.data(), sizeof(int32_t) * coords.size(), cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(v->hash.n_blocks, &nb, sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpyAsync(v->hash.heads, heads.data(), sizeof(int32_t) * heads.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(v->hash.next, next.data(), sizeof(int32_t) * n_blocks, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(v->hash.keys, keys.data(), sizeof(uint64_t) * n_blocks, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(v->hash.coords, coords.data(), sizeof(int32_t) * coords.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(v->hash.n_blocks, &nb, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
     launch_rebuild_index(ctx->stream, v->hash.coords, nb, v->hash.grid, v->hash.occ, v->hash.gbits);
     launch_super_dist(ctx->stream, v->hash);
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1537,7 +1540,7 @@ extern "C" int csf_pairwise_sum(csf_ctx ctx, const double* terms, int n, int cha
     for (size_t c = 0; c < C; ++c) t[c * n + i] = terms[static_cast<size_t>(i) * C + c];  // slot-major
   DevBuf<double> d;
   CUDA_TRY(ctx, d.alloc(std::max<size_t>(t.size(), 1)));
-  if (n > 0) CUDA_TRY(ctx, cudaMemcpy(d.p, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
+  if (n > 0) CUDA_TRY(ctx, cudaMemcpyAsync(d.p, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, ctx->stream));
   const int rc = tree_sum_slots(ctx->stream, ctx->energy, d.p, n, channels, out);
   if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "csf_pairwise_sum: device failure");
   return CSF_OK;
@@ -1959,8 +1962,8 @@ extern "C" int csf_reloc_create(csf_volume v, const double* depth, int w, int h,
   if (rc || n2 != n) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "RelocProblem: flatten failed");
   r->n = n;
   const double kk[4] = {k->fx, k->fy, k->cx, k->cy};
-  CUDA_TRY(ctx, cudaMemcpy(r->depth.p, depth, sizeof(double) * w * h, cudaMemcpyHostToDevice));
-  CUDA_TRY(ctx, cudaMemcpy(r->k4.p, kk, sizeof(kk), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpyAsync(r->depth.p, depth, sizeof(double) * w * h, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(r->k4.p, kk, sizeof(kk), cudaMemcpyHostToDevice, ctx->stream));
   ctx->launches += 3;
   *out = r.release();
   return CSF_OK;
@@ -1978,8 +1981,8 @@ extern "C" int csf_reloc_info(csf_reloc r, int* n, double* mu, double* centers, 
   cudaSetDevice(r->ctx->device);
   if (n) *n = r->n;
   if (mu) *mu = r->mu;
-  if (centers) CUDA_TRY(r->ctx, cudaMemcpy(centers, r->centers.p, sizeof(double) * 3 * r->n, cudaMemcpyDeviceToHost));
-  if (values) CUDA_TRY(r->ctx, cudaMemcpy(values, r->values.p, sizeof(double) * r->n, cudaMemcpyDeviceToHost));
+  if (centers) CUDA_TRY(r->ctx, cudaMemcpyAsync(centers, r->centers.p, sizeof(double) * 3 * r->n, cudaMemcpyDeviceToHost, r->ctx->stream));
+  if (values) CUDA_TRY(r->ctx, cudaMemcpyAsync(values, r->values.p, sizeof(double) * r->n, cudaMemcpyDeviceToHost, r->ctx->stream));
   return CSF_OK;
 }
 
@@ -2255,11 +2258,11 @@ extern "C" int csf_surfels_download(csf_surfels m, double* pos, double* nrm, dou
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   const size_t C = 1 + m->D, n = m->n;
   if (n == 0) return CSF_OK;
-  if (pos) CUDA_TRY(ctx, cudaMemcpy(pos, m->pos.p, sizeof(double) * 3 * n * C, cudaMemcpyDeviceToHost));
-  if (nrm) CUDA_TRY(ctx, cudaMemcpy(nrm, m->nrm.p, sizeof(double) * 3 * n * C, cudaMemcpyDeviceToHost));
-  if (rad) CUDA_TRY(ctx, cudaMemcpy(rad, m->rad.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
-  if (conf) CUDA_TRY(ctx, cudaMemcpy(conf, m->conf.p, sizeof(double) * n * C, cudaMemcpyDeviceToHost));
-  if (ts) CUDA_TRY(ctx, cudaMemcpy(ts, m->ts.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  if (pos) CUDA_TRY(ctx, cudaMemcpyAsync(pos, m->pos.p, sizeof(double) * 3 * n * C, cudaMemcpyDeviceToHost, ctx->stream));
+  if (nrm) CUDA_TRY(ctx, cudaMemcpyAsync(nrm, m->nrm.p, sizeof(double) * 3 * n * C, cudaMemcpyDeviceToHost, ctx->stream));
+  if (rad) CUDA_TRY(ctx, cudaMemcpyAsync(rad, m->rad.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (conf) CUDA_TRY(ctx, cudaMemcpyAsync(conf, m->conf.p, sizeof(double) * n * C, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ts) CUDA_TRY(ctx, cudaMemcpyAsync(ts, m->ts.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
   return CSF_OK;
 }
 extern "C" int csf_surfels_upload(csf_surfels m, int n, const double* pos, const double* nrm, const double* rad,
@@ -2272,11 +2275,11 @@ extern "C" int csf_surfels_upload(csf_surfels m, int n, const double* pos, const
   if (rc) return rc;
   const size_t C = 1 + m->D;
   if (n > 0) {
-    CUDA_TRY(ctx, cudaMemcpy(m->pos.p, pos, sizeof(double) * 3 * n * C, cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(m->nrm.p, nrm, sizeof(double) * 3 * n * C, cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(m->rad.p, rad, sizeof(double) * n, cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(m->conf.p, conf, sizeof(double) * n * C, cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(m->ts.p, ts, sizeof(int) * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpyAsync(m->pos.p, pos, sizeof(double) * 3 * n * C, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(m->nrm.p, nrm, sizeof(double) * 3 * n * C, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(m->rad.p, rad, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(m->conf.p, conf, sizeof(double) * n * C, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(m->ts.p, ts, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
   }
   m->n = n;
   return CSF_OK;
@@ -2302,9 +2305,9 @@ extern "C" int csf_render_index_map(csf_surfels m, const double* c2w, const csf_
   if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "render_index_map: CUDA error");
   const size_t cells = static_cast<size_t>(16) * k->width * k->height;
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpy(offsets, m->ws.offsets, sizeof(uint32_t) * (cells + 1), cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpyAsync(offsets, m->ws.offsets, sizeof(uint32_t) * (cells + 1), cudaMemcpyDeviceToHost, ctx->stream));
   if (entries && cnt > 0)
-    CUDA_TRY(ctx, cudaMemcpy(entries, m->ws.entries, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost));
+    CUDA_TRY(ctx, cudaMemcpyAsync(entries, m->ws.entries, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
   *n_entries = cnt;
   return CSF_OK;
 }
@@ -2360,11 +2363,11 @@ extern "C" int csf_associate_surfels(csf_surfels m, const double* depth, int w, 
   if (rc) return rc;
   const size_t P = static_cast<size_t>(w) * h, C = 1 + m->D;
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpy(counts, m->ws.pint + P, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpyAsync(counts, m->ws.pint + P, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, ctx->stream));
   if (indices && weights && T > 0) {
     const int n = std::min(T, cap);
-    CUDA_TRY(ctx, cudaMemcpy(indices, m->ws.pidx, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
-    CUDA_TRY(ctx, cudaMemcpy(weights, m->ws.pw, sizeof(double) * n * C, cudaMemcpyDeviceToHost));
+    CUDA_TRY(ctx, cudaMemcpyAsync(indices, m->ws.pidx, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(weights, m->ws.pw, sizeof(double) * n * C, cudaMemcpyDeviceToHost, ctx->stream));
   }
   *total = T;
   return CSF_OK;
@@ -2409,8 +2412,8 @@ extern "C" int csf_predict_maps(csf_surfels m, const double* c2w, const csf_intr
   ctx->launches += 5;
   if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "predict_maps: CUDA error");
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpy(V, out.p, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost));
-  CUDA_TRY(ctx, cudaMemcpy(N, out.p + 3 * P, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpyAsync(V, out.p, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(N, out.p + 3 * P, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
   return CSF_OK;
 }
 

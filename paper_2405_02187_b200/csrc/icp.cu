@@ -275,6 +275,89 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_solve_t(TrackState* st, con
   icp_solve_body(st, gpartials, gcounts, n_groups, pose, Dp, level, tol);
 }
 
+// One lifted (J, r) row of a correspondence (slot (x, y) -> model pixel
+// (u, v)) into row[7][C]: the canonical row both the fused reduce and the
+// split rows kernel write (same operations, bit-identical).
+CSF_DEV void icp_row(double* row, const double* __restrict__ depth, int w, int x, int y, int u, int v,
+                     const double* s_pose, const double* s_intr, int C, int Dp, const double* __restrict__ vre,
+                     const double* __restrict__ nre, const double* __restrict__ vim,
+                     const double* __restrict__ nim) {
+  // One lifted (J, r) row in tangent form: the real chain once, then each
+  // channel's im by the truncated-Complex rule of every operation
+  // (csfd.hpp:44-58) applied to the saved real intermediates.
+  const long long m = static_cast<long long>(v) * w + u;
+  const double d = depth[y * w + x];
+  // vertex: ((d*(x - cx))/fx, (d*(y - cy))/fy, d)
+  const double tx = static_cast<double>(x) - s_intr[2 * C], ty = static_cast<double>(y) - s_intr[3 * C];
+  const double nx = d * tx, ny = d * ty;
+  const double kfx = s_intr[0], kfy = s_intr[C];
+  const double vre3[3] = {nx / kfx, ny / kfy, d};
+  const double ifx = 1.0 / (kfx * kfx), ify = 1.0 / (kfy * kfy);
+  (void)ifx;
+  (void)ify;
+  double R[9], T[3], MV[3], MN[3], P[3], PR[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) R[e] = s_pose[e * C];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) T[e] = s_pose[(9 + e) * C];
+#pragma unroll
+  for (int c3 = 0; c3 < 3; ++c3) {
+    MV[c3] = vre[3 * m + c3];
+    MN[c3] = nre[3 * m + c3];
+  }
+#pragma unroll
+  for (int r3 = 0; r3 < 3; ++r3) {
+#pragma unroll
+    for (int c3 = 0; c3 < 3; ++c3) PR[3 * r3 + c3] = R[3 * r3 + c3] * vre3[c3];
+    P[r3] = (PR[3 * r3] + (PR[3 * r3 + 1] + PR[3 * r3 + 2])) + T[r3];
+  }
+  const double DF[3] = {P[0] - MV[0], P[1] - MV[1], P[2] - MV[2]};
+  const double rr = DF[0] * MN[0] + (DF[1] * MN[1] + DF[2] * MN[2]);
+  const double PN[3] = {P[1] * MN[2] - P[2] * MN[1], P[2] * MN[0] - P[0] * MN[2], P[0] * MN[1] - P[1] * MN[0]};
+  row[0] = MN[0];
+  row[C] = MN[1];
+  row[2 * C] = MN[2];
+  row[3 * C] = PN[0];
+  row[4 * C] = PN[1];
+  row[5 * C] = PN[2];
+  row[6 * C] = rr;
+  for (int ch = 1; ch <= Dp; ++ch) {
+    // vertex channels (intrinsics seeds): d*(x - cx) has im d*(-cx.im)
+    const double tnx = d * -s_intr[2 * C + ch], tny = d * -s_intr[3 * C + ch];
+    const double vim3[3] = {CSF_CH_DIV(tnx * kfx - nx * s_intr[ch], kfx * kfx, ifx),
+                            CSF_CH_DIV(tny * kfy - ny * s_intr[C + ch], kfy * kfy, ify), 0.0};
+    double Pi[3], MVi[3], MNi[3];
+#pragma unroll
+    for (int c3 = 0; c3 < 3; ++c3) {
+      MVi[c3] = vim[(3 * m + c3) * Dp + ch - 1];
+      MNi[c3] = nim[(3 * m + c3) * Dp + ch - 1];
+    }
+#pragma unroll
+    for (int r3 = 0; r3 < 3; ++r3) {
+      double qi[3];
+#pragma unroll
+      for (int c3 = 0; c3 < 3; ++c3) qi[c3] = R[3 * r3 + c3] * vim3[c3] + s_pose[(3 * r3 + c3) * C + ch] * vre3[c3];
+      Pi[r3] = (qi[0] + (qi[1] + qi[2])) + s_pose[(9 + r3) * C + ch];
+    }
+    const double DFi[3] = {Pi[0] - MVi[0], Pi[1] - MVi[1], Pi[2] - MVi[2]};
+    double ti[3];
+#pragma unroll
+    for (int c3 = 0; c3 < 3; ++c3) ti[c3] = DF[c3] * MNi[c3] + DFi[c3] * MN[c3];
+    const double ri = ti[0] + (ti[1] + ti[2]);
+    const double PNi[3] = {(P[1] * MNi[2] + Pi[1] * MN[2]) - (P[2] * MNi[1] + Pi[2] * MN[1]),
+                           (P[2] * MNi[0] + Pi[2] * MN[0]) - (P[0] * MNi[2] + Pi[0] * MN[2]),
+                           (P[0] * MNi[1] + Pi[0] * MN[1]) - (P[1] * MNi[0] + Pi[1] * MN[0])};
+    row[ch] = MNi[0];
+    row[C + ch] = MNi[1];
+    row[2 * C + ch] = MNi[2];
+    row[3 * C + ch] = PNi[0];
+    row[4 * C + ch] = PNi[1];
+    row[5 * C + ch] = PNi[2];
+    row[6 * C + ch] = ri;
+  }
+
+}
+
 template <int G>
 __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
                                                     int w, int h, int stride, const double* __restrict__ intr,
@@ -334,82 +417,8 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
       total += s_wsum[k];
     }
     const int pos = before + __popc(ballot & ((1u << lane) - 1u));
-    if (corr) {
-      // One lifted (J, r) row in tangent form: the real chain once, then each
-      // channel's im by the truncated-Complex rule of every operation
-      // (csfd.hpp:44-58) applied to the saved real intermediates.
-      const long long m = static_cast<long long>(v) * w + u;
-      double* row = s_jr + static_cast<long long>(pos) * 7 * C;
-      const double d = depth[y * w + x];
-      // vertex: ((d*(x - cx))/fx, (d*(y - cy))/fy, d)
-      const double tx = static_cast<double>(x) - s_intr[2 * C], ty = static_cast<double>(y) - s_intr[3 * C];
-      const double nx = d * tx, ny = d * ty;
-      const double kfx = s_intr[0], kfy = s_intr[C];
-      const double vre3[3] = {nx / kfx, ny / kfy, d};
-      const double ifx = 1.0 / (kfx * kfx), ify = 1.0 / (kfy * kfy);
-      (void)ifx;
-      (void)ify;
-      double R[9], T[3], MV[3], MN[3], P[3], PR[9];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) R[e] = s_pose[e * C];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) T[e] = s_pose[(9 + e) * C];
-#pragma unroll
-      for (int c3 = 0; c3 < 3; ++c3) {
-        MV[c3] = vre[3 * m + c3];
-        MN[c3] = nre[3 * m + c3];
-      }
-#pragma unroll
-      for (int r3 = 0; r3 < 3; ++r3) {
-#pragma unroll
-        for (int c3 = 0; c3 < 3; ++c3) PR[3 * r3 + c3] = R[3 * r3 + c3] * vre3[c3];
-        P[r3] = (PR[3 * r3] + (PR[3 * r3 + 1] + PR[3 * r3 + 2])) + T[r3];
-      }
-      const double DF[3] = {P[0] - MV[0], P[1] - MV[1], P[2] - MV[2]};
-      const double rr = DF[0] * MN[0] + (DF[1] * MN[1] + DF[2] * MN[2]);
-      const double PN[3] = {P[1] * MN[2] - P[2] * MN[1], P[2] * MN[0] - P[0] * MN[2], P[0] * MN[1] - P[1] * MN[0]};
-      row[0] = MN[0];
-      row[C] = MN[1];
-      row[2 * C] = MN[2];
-      row[3 * C] = PN[0];
-      row[4 * C] = PN[1];
-      row[5 * C] = PN[2];
-      row[6 * C] = rr;
-      for (int ch = 1; ch <= Dp; ++ch) {
-        // vertex channels (intrinsics seeds): d*(x - cx) has im d*(-cx.im)
-        const double tnx = d * -s_intr[2 * C + ch], tny = d * -s_intr[3 * C + ch];
-        const double vim3[3] = {CSF_CH_DIV(tnx * kfx - nx * s_intr[ch], kfx * kfx, ifx),
-                                CSF_CH_DIV(tny * kfy - ny * s_intr[C + ch], kfy * kfy, ify), 0.0};
-        double Pi[3], MVi[3], MNi[3];
-#pragma unroll
-        for (int c3 = 0; c3 < 3; ++c3) {
-          MVi[c3] = vim[(3 * m + c3) * Dp + ch - 1];
-          MNi[c3] = nim[(3 * m + c3) * Dp + ch - 1];
-        }
-#pragma unroll
-        for (int r3 = 0; r3 < 3; ++r3) {
-          double qi[3];
-#pragma unroll
-          for (int c3 = 0; c3 < 3; ++c3) qi[c3] = R[3 * r3 + c3] * vim3[c3] + s_pose[(3 * r3 + c3) * C + ch] * vre3[c3];
-          Pi[r3] = (qi[0] + (qi[1] + qi[2])) + s_pose[(9 + r3) * C + ch];
-        }
-        const double DFi[3] = {Pi[0] - MVi[0], Pi[1] - MVi[1], Pi[2] - MVi[2]};
-        double ti[3];
-#pragma unroll
-        for (int c3 = 0; c3 < 3; ++c3) ti[c3] = DF[c3] * MNi[c3] + DFi[c3] * MN[c3];
-        const double ri = ti[0] + (ti[1] + ti[2]);
-        const double PNi[3] = {(P[1] * MNi[2] + Pi[1] * MN[2]) - (P[2] * MNi[1] + Pi[2] * MN[1]),
-                               (P[2] * MNi[0] + Pi[2] * MN[0]) - (P[0] * MNi[2] + Pi[0] * MN[2]),
-                               (P[0] * MNi[1] + Pi[0] * MN[1]) - (P[1] * MNi[0] + Pi[1] * MN[0])};
-        row[ch] = MNi[0];
-        row[C + ch] = MNi[1];
-        row[2 * C + ch] = MNi[2];
-        row[3 * C + ch] = PNi[0];
-        row[4 * C + ch] = PNi[1];
-        row[5 * C + ch] = PNi[2];
-        row[6 * C + ch] = ri;
-      }
-    }
+    if (corr) icp_row(s_jr + static_cast<long long>(pos) * 7 * C, depth, w, x, y, u, v, s_pose, s_intr, C, Dp, vre,
+                      nre, vim, nim);
     __syncthreads();
     if (cbase == 0) clock_mark(1);
     // per-accumulator sequential sums in slot order
