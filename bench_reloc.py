@@ -86,15 +86,29 @@ def cpu_sample(depth, gt, k, items, cfg, mean_iters):
                       f"{mean_it:.1f} iterations/query"}
 
 
-def run_reference(args, mean_iters=8.0):
+def setup_cpu(csf, n_frames=100):
+    """The same inputs for query 0 from the oracle's renderer (bit-identical
+    to the device renderer) — no GPU work on the reference arm."""
+    from oracle import orc
+    depth, gt, k = orc.workload(2, n_frames)
+    rng = np.random.default_rng(11)
+    q = QUERIES[0]
+    init = _perturb(gt[q], 3.0, 5.0, rng)
+    cand = [i for i in range(n_frames) if i != q]
+    sel = [cand[i] for i in csf.select_reference_frames([gt[i] for i in cand], init, 10)]
+    return depth, gt, k, [(q, init, sel, None)]
+
+
+def run_reference(args, mean_iters=44.0):
     """--impl reference --workload reloc: the oracle port's relocalization
-    rate (rank 0; other ranks exit)."""
+    rate (rank 0; other ranks exit).  mean_iters = the device run's measured
+    mean iterations per query (profiles/r01_bench_reloc.json)."""
     import paper_2405_02187_b200 as csf
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    ctx = csf.Context(int(os.environ.get("LOCAL_RANK", "0")))
-    depth, gt, k, items = setup(csf, ctx)
-    cfg = csf.default_reloc_cfg()
+    depth, gt, k, items = setup_cpu(csf)
+    from paper_2405_02187_b200 import capi
+    cfg = capi.RelocCfg(0.5, -1.0, 50, 25, 1e-6, 1.0, 0.5, 1e-4, 1e-8, 0.05, 0.9)  # reloc.hpp / DESIGN §3.9 defaults
     vals = []
     t0 = time.perf_counter()
     for _ in range(max(args.steps, 1)):

@@ -154,10 +154,10 @@ def run_reference(args):
     from oracle import orc
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    ctx = csf.Context(int(os.environ.get("LOCAL_RANK", "0")))
-    depth, gt, k = csf.synth_workload(2, 3, ctx=ctx)
+    depth, gt, k = orc.workload(2, 3)  # the oracle renderer: no GPU work on the reference arm
     poses = lifted_poses(gt)
-    cfg = csf.default_surfel_cfg()
+    from paper_2405_02187_b200 import capi
+    cfg = capi.SurfelCfg(0.05, 30.0, 0.05, 0.025, 1)  # surfel.hpp defaults
     vals = []
     t0 = time.perf_counter()
     for _ in range(max(args.steps, 1)):
