@@ -494,6 +494,8 @@ extern "C" int csf_measure_surface(csf_ctx ctx, const double* depth, int w, int 
   if (!ctx || !depth || !intr || !vertices || !normals || w <= 0 || h <= 0 || n_channels < 0 ||
       n_channels > CSF_MAX_DIRECTIONS)
     return fail(ctx, CSF_EINVAL, "csf_measure_surface: bad arguments");
+  if (n_channels > 0 && (intr[0] == 0.0 || intr[1 + n_channels] == 0.0))
+    return fail(ctx, CSF_EDOMAIN, "csf_measure_surface: Complex division by zero real part (fx or fy = 0)");
   cudaSetDevice(ctx->device);
   const size_t P = static_cast<size_t>(w) * h, C = 1 + n_channels;
   DevBuf<double> dd, dk, dv, dn;
@@ -706,6 +708,8 @@ extern "C" int csf_surface_update(csf_volume v, const double* depth, int w, int 
                                   const double* intr, int* n_visible) {
   if (!v || !depth || !pose || !intr || w <= 1 || h <= 1) return CSF_EINVAL;
   csf_ctx ctx = v->ctx;
+  if (v->D > 0 && (intr[0] == 0.0 || intr[1 + v->D] == 0.0))
+    return fail(ctx, CSF_EDOMAIN, "csf_surface_update: Complex division by zero real part (fx or fy = 0)");
   cudaSetDevice(ctx->device);
   const size_t P = static_cast<size_t>(w) * h;
   const int C = 1 + v->Dp;
@@ -732,6 +736,8 @@ extern "C" int csf_raycast(csf_volume v, const double* pose, const double* intr,
                            const csf_raycast_cfg* cfg, double* vertices, double* normals) {
   if (!v || !pose || !intr || !vertices || !normals || w <= 0 || h <= 0) return CSF_EINVAL;
   csf_ctx ctx = v->ctx;
+  if (v->D > 0 && (intr[0] == 0.0 || intr[1 + v->D] == 0.0))
+    return fail(ctx, CSF_EDOMAIN, "csf_raycast: Complex division by zero real part (fx or fy = 0)");
   cudaSetDevice(ctx->device);
   csf_raycast_cfg rc;
   if (cfg)
@@ -1140,6 +1146,8 @@ extern "C" int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h,
   if (!ctx || !depth || !world_to_camera || !intr || !center || w <= 0 || h <= 0 || n < 0 || n_channels < 0 ||
       n_channels > CSF_MAX_DIRECTIONS || (n > 0 && (!points || !psi || !valid)))
     return CSF_EINVAL;
+  if (n_channels > 0 && (intr[0] == 0.0 || intr[1 + n_channels] == 0.0))
+    return fail(ctx, CSF_EDOMAIN, "csf_measured_tsdf: Complex division by zero real part (fx or fy = 0)");
   cudaSetDevice(ctx->device);
   const int D = n_channels, C = 1 + D;
   const size_t P = static_cast<size_t>(w) * h;
