@@ -193,9 +193,40 @@ def cpu_baseline(depth, gt, k, frames, ndirs, workload="config2"):
     if omp:
         cores = int(omp)
     what = "pair" if workload == "config3" else "direction"
-    return {"value": units / secs, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{workload} first {frames} VGA frames x {ndirs} {what}s, one pass per {what} "
-                      f"({units} units in {secs:.2f} s)"}
+    out = {"value": units / secs, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"{workload} first {frames} VGA frames x {ndirs} {what}s, one pass per {what} "
+                     f"({units} units in {secs:.2f} s)", "host": host_info()}
+    # also a single-core number (the same oracle on one OpenMP thread, 2 frames x 1 unit)
+    try:
+        import ctypes
+        gomp = ctypes.CDLL("libgomp.so.1")
+        gomp.omp_set_num_threads(1)
+        f1 = min(2, frames)
+        if workload == "config3":
+            t1 = orc.pipeline_hessian(pipeline_cfg(csf, capi, k, [], f1, pairs=[PAIRS[0]]), depth[:f1], gt[:f1])[-1]
+        elif workload == "config4":
+            t1 = orc.pipeline_run(pipeline_cfg4(csf, capi, k, [DIRS4[0]], f1), depth[:f1], gt[:f1])[-1]
+        else:
+            t1 = orc.pipeline_run(pipeline_cfg(csf, capi, k, [DIRS[0]], f1), depth[:f1], gt[:f1])[-1]
+        gomp.omp_set_num_threads(cores)
+        out["single_core"] = {"value": f1 / t1, "unit": UNIT, "cores": 1,
+                              "sample": f"first {f1} frames x 1 {what}, OMP 1 thread ({t1:.2f} s)"}
+    except Exception as e:  # pragma: no cover
+        out["single_core"] = {"value": None, "error": str(e)}
+    return out
+
+
+def host_info() -> dict:
+    """nproc, OMP_NUM_THREADS and the CPU model string."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS"), "cpu_model": model}
 
 
 def run_reference(args):
