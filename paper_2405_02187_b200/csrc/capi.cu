@@ -571,7 +571,7 @@ static int create_hashed(csf_ctx ctx, const csf_hash_params* p, int n_channels, 
   const size_t nb = size_t(1) << p->bucket_bits;
   const int gbits = 9;  // 512^3 block-id window (512 MiB of int32)
   const size_t ng = size_t(1) << (3 * gbits);
-  const size_t nocc = (size_t(1) << (3 * (gbits - 3))) / 32;
+  const size_t nocc = occ_words(gbits);
   const size_t nsb = size_t(1) << (3 * (gbits - 3));
   if (v->grid.alloc(ng) != cudaSuccess || v->occ.alloc(nocc) != cudaSuccess || v->sdist.alloc(2 * nsb) != cudaSuccess) {
     delete v;
@@ -942,8 +942,7 @@ static int pipeline_reset_volume(csf_pipeline p) {
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.next, 0xFF, sizeof(int) * v->hash.max_blocks, ctx->stream));
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.n_blocks, 0, sizeof(int), ctx->stream));
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.grid, 0xFF, sizeof(int) << (3 * v->hash.gbits), ctx->stream));
-      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.occ, 0, sizeof(unsigned) * ((size_t(1) << (3 * (v->hash.gbits - 3))) / 32),
-                                    ctx->stream));
+      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.occ, 0, sizeof(unsigned) * occ_words(v->hash.gbits), ctx->stream));
       launch_super_dist(ctx->stream, v->hash);
       launch_init_volume(L, v->hash.rw, v->hash.fim, static_cast<long long>(nb) * 512, v->Dp);
     }

@@ -12,6 +12,10 @@ namespace csfi {
 // uses the group width G chosen by pick_group(D) and stores Dp = ceil(D/G)*G
 // channels (padding channels stay zero).
 int pick_group(int D);
+// words of the occupancy pyramid (super-block, 4^3-block and 2^3-block bits)
+inline size_t occ_words(int gbits) {
+  return ((size_t(1) << (3 * (gbits - 3))) + (size_t(1) << (3 * (gbits - 2))) + (size_t(1) << (3 * (gbits - 1)))) / 32;
+}
 inline int padded_channels(int D, int G) { return G == 0 ? 0 : ((D + G - 1) / G) * G; }
 
 struct DenseDev {
@@ -31,7 +35,8 @@ struct HashDev {
   int* coords;                  // [max_blocks][3]
   int* n_blocks;                // device counter
   int* grid;                    // [2^(3*gbits)] dense block-id window (derived index)
-  unsigned* occ;                // [2^(3*(gbits-3))/32] super-block occupancy bits
+  unsigned* occ;                // occupancy bits: super-blocks [2^(3*(gbits-3))], then 4^3-block
+                                // cells [2^(3*(gbits-2))], then 2^3-block cells [2^(3*(gbits-1))]
   unsigned char* sdist = nullptr;  // [2^(3*(gbits-3))] Chebyshev distance (super-blocks) to the
                                    // nearest occupied / out-of-window super-block, capped at 8
   unsigned char* sdist_tmp = nullptr;

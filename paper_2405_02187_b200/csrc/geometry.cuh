@@ -107,6 +107,25 @@ struct HashView {
     const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
     return (__ldg(occ + (bit >> 5)) >> (bit & 31)) & 1u;
   }
+  // Block-occupancy pyramid below the super-block level: bitmaps at 4^3- and
+  // 2^3-block granularity stored after the super-block bits in `occ`.
+  // Returns the span (in blocks, 4 or 2) of the largest known-empty aligned
+  // cell containing block (bx, by, bz), or 0 (occupied / outside the window).
+  CSF_DEV int empty_span(int bx, int by, int bz) const {
+    const int half = 1 << (gbits - 1);
+    const unsigned ux = static_cast<unsigned>(bx + half), uy = static_cast<unsigned>(by + half),
+                   uz = static_cast<unsigned>(bz + half);
+    const unsigned side = 1u << gbits;
+    if (!(ux < side && uy < side && uz < side)) return 0;
+    const unsigned* occ4 = occ + ((1u << (3 * (gbits - 3))) >> 5);
+    const unsigned* occ2 = occ4 + ((1u << (3 * (gbits - 2))) >> 5);
+    const int s4 = gbits - 2, s2 = gbits - 1;
+    const unsigned b4 = ((uz >> 2) << s4 | (uy >> 2)) << s4 | (ux >> 2);
+    if (!((__ldg(occ4 + (b4 >> 5)) >> (b4 & 31)) & 1u)) return 4;
+    const unsigned b2 = ((uz >> 1) << s2 | (uy >> 1)) << s2 | (ux >> 1);
+    if (!((__ldg(occ2 + (b2 >> 5)) >> (b2 & 31)) & 1u)) return 2;
+    return 0;
+  }
   // d > 0: every super-block within Chebyshev distance d - 1 of this one is
   // inside the window and empty; 0: occupied or outside the window.
   CSF_DEV int super_dist(int bx, int by, int bz) const {

@@ -449,6 +449,19 @@ __device__ void chain_insert(int* heads, const unsigned long long* keys, int* ne
   }
 }
 
+// Mark block (ux, uy, uz) (window coordinates) in every occupancy level.
+CSF_DEV void occ_mark(unsigned* occ, int gbits, unsigned ux, unsigned uy, unsigned uz) {
+  const int sb = gbits - 3, s4 = gbits - 2, s2 = gbits - 1;
+  const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
+  atomicOr(occ + (bit >> 5), 1u << (bit & 31));
+  unsigned* occ4 = occ + ((1u << (3 * sb)) >> 5);
+  const unsigned b4 = ((uz >> 2) << s4 | (uy >> 2)) << s4 | (ux >> 2);
+  atomicOr(occ4 + (b4 >> 5), 1u << (b4 & 31));
+  unsigned* occ2 = occ4 + ((1u << (3 * s4)) >> 5);
+  const unsigned b2 = ((uz >> 1) << s2 | (uy >> 1)) << s2 | (ux >> 1);
+  atomicOr(occ2 + (b2 >> 5), 1u << (b2 & 31));
+}
+
 __global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int* next, int* coords, const int* n_blocks,
                          int max_blocks, const unsigned long long* __restrict__ cand, int n,
                          const int* __restrict__ first_flag, const int* __restrict__ new_flag,
@@ -482,9 +495,7 @@ __global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int
     const unsigned side = 1u << vol.gbits;
     if (ux < side && uy < side && uz < side) {
       const_cast<int*>(vol.grid)[(static_cast<size_t>(uz) << vol.gbits | uy) << vol.gbits | ux] = id;
-      const int sb = vol.gbits - 3;
-      const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
-      atomicOr(const_cast<unsigned*>(vol.occ) + (bit >> 5), 1u << (bit & 31));
+      occ_mark(const_cast<unsigned*>(vol.occ), vol.gbits, ux, uy, uz);
     }
   }
   visible[first_rank[s]] = id;
@@ -692,6 +703,12 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
           lx = ((bx >> 3) - (sd - 1)) << 3;
           ly = ((by >> 3) - (sd - 1)) << 3;
           lz = ((bz >> 3) - (sd - 1)) << 3;
+        } else if (const int es = vol.empty_span(bx, by, bz)) {
+          span = es;  // an empty aligned 4^3- or 2^3-block cell
+          const int m2 = ~(es - 1);
+          lx = bx & m2;
+          ly = by & m2;
+          lz = bz & m2;
         } else if (vol.block(bx, by, bz) < 0) {
           span = 1;
         }
@@ -841,6 +858,12 @@ __global__ void __launch_bounds__(128) k_raycast_march_seg(HashView vol, const d
       lx = ((bx >> 3) - (sd - 1)) << 3;
       ly = ((by >> 3) - (sd - 1)) << 3;
       lz = ((bz >> 3) - (sd - 1)) << 3;
+    } else if (const int es = vol.empty_span(bx, by, bz)) {
+      span = es;
+      const int m2 = ~(es - 1);
+      lx = bx & m2;
+      ly = by & m2;
+      lz = bz & m2;
     } else if (vol.block(bx, by, bz) < 0) {
       span = 1;
     }
@@ -1808,9 +1831,7 @@ __global__ void k_rebuild_index(const int* __restrict__ coords, int n_blocks, in
   const unsigned side = 1u << gbits;
   if (ux < side && uy < side && uz < side) {
     grid[(static_cast<size_t>(uz) << gbits | uy) << gbits | ux] = b;
-    const int sb = gbits - 3;
-    const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
-    atomicOr(occ + (bit >> 5), 1u << (bit & 31));
+    occ_mark(occ, gbits, ux, uy, uz);
   }
 }
 
