@@ -144,7 +144,7 @@ struct SurfelScratch {
   unsigned long long* depthk = nullptr; size_t depthk_cap = 0;
   int* sidx = nullptr; size_t sidx_cap = 0;
   int* entries = nullptr;                                         // points into sidx
-  void* cub = nullptr; size_t cub_cap = 0;
+  unsigned char* cub = nullptr; size_t cub_cap = 0;
   double *V = nullptr, *N = nullptr, *VW = nullptr, *NW = nullptr;
   size_t V_cap = 0, N_cap = 0, VW_cap = 0, NW_cap = 0;
   int* pint = nullptr; size_t pint_cap = 0;                       // valid, counts, offs, cflag, crank, merged
