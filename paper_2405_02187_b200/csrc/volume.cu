@@ -696,20 +696,21 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
         const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
         // empty space: the cube of (2d - 1)^3 empty super-blocks around this
         // one (distance field), else this unallocated block
-        const int sd = vol.super_dist(bx, by, bz);
+        int sd, es, blk;
+        vol.probe(bx, by, bz, &sd, &es, &blk);
         int span = 0, lx = bx, ly = by, lz = bz;
         if (sd > 0) {
           span = 8 * (2 * sd - 1);
           lx = ((bx >> 3) - (sd - 1)) << 3;
           ly = ((by >> 3) - (sd - 1)) << 3;
           lz = ((bz >> 3) - (sd - 1)) << 3;
-        } else if (const int es = vol.empty_span(bx, by, bz)) {
+        } else if (es) {
           span = es;  // an empty aligned 4^3- or 2^3-block cell
           const int m2 = ~(es - 1);
           lx = bx & m2;
           ly = by & m2;
           lz = bz & m2;
-        } else if (vol.block(bx, by, bz) < 0) {
+        } else if (blk < 0) {
           span = 1;
         }
         if (span > 0) {
@@ -851,20 +852,21 @@ __global__ void __launch_bounds__(128) k_raycast_march_seg(HashView vol, const d
     const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
               k0 = ifloor((pz - vol.oz) / vol.vs);
     const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
-    const int sd = vol.super_dist(bx, by, bz);
+    int sd, es, blk;
+    vol.probe(bx, by, bz, &sd, &es, &blk);
     int span = 0, lx = bx, ly = by, lz = bz;
     if (sd > 0) {
       span = 8 * (2 * sd - 1);
       lx = ((bx >> 3) - (sd - 1)) << 3;
       ly = ((by >> 3) - (sd - 1)) << 3;
       lz = ((bz >> 3) - (sd - 1)) << 3;
-    } else if (const int es = vol.empty_span(bx, by, bz)) {
+    } else if (es) {
       span = es;
       const int m2 = ~(es - 1);
       lx = bx & m2;
       ly = by & m2;
       lz = bz & m2;
-    } else if (vol.block(bx, by, bz) < 0) {
+    } else if (blk < 0) {
       span = 1;
     }
     if (span > 0) {
