@@ -554,9 +554,7 @@ def main():
         ms = float(t.item())
         cols = gather_columns(torch.from_numpy(np.asarray(local_cols)).cuda(), len(units_all), world,
                               rank).cpu().numpy()
-    if four and dist is None:
-        cols = local_cols
-    else:
+    if dist is None:
         cols = local_cols
 
     units_per_step = n * len(units_all)
