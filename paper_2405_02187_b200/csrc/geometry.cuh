@@ -126,9 +126,10 @@ struct HashView {
     if (!((__ldg(occ2 + (b2 >> 5)) >> (b2 & 31)) & 1u)) return 2;
     return 0;
   }
-  // All empty-space information of block (bx, by, bz) with the four loads
-  // (super-block distance, 4^3- and 2^3-cell bits, block id) issued
-  // together, so a march trip pays one memory latency instead of a chain.
+  // All empty-space information of block (bx, by, bz): the super-block
+  // distance, then (inside an occupied super-block) the 4^3- and 2^3-cell
+  // bits and the block id issued together, so a march trip pays at most two
+  // memory latencies instead of a chain of four.
   // sd: super_dist; es: empty_span; blk: block id (-1 unallocated).
   CSF_DEV void probe(int bx, int by, int bz, int* sd, int* es, int* blk) const {
     const int half = 1 << (gbits - 1);
@@ -148,10 +149,15 @@ struct HashView {
     const unsigned b4 = ((uz >> 2) << s4 | (uy >> 2)) << s4 | (ux >> 2);
     const unsigned b2 = ((uz >> 1) << s2 | (uy >> 1)) << s2 | (ux >> 1);
     const int d = __ldg(sdist + bsb);
+    *sd = d;
+    if (d > 0) {  // empty super-block neighbourhood: nothing finer needed
+      *es = 0;
+      *blk = -1;
+      return;
+    }
     const unsigned w4 = __ldg(occ4 + (b4 >> 5));
     const unsigned w2 = __ldg(occ2 + (b2 >> 5));
     const int id = __ldg(grid + ((static_cast<size_t>(uz) << gbits | uy) << gbits | ux));
-    *sd = d;
     *es = !((w4 >> (b4 & 31)) & 1u) ? 4 : (!((w2 >> (b2 & 31)) & 1u) ? 2 : 0);
     *blk = id;
   }
