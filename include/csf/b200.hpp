@@ -14,7 +14,9 @@
 // plain structs (no Eigen): Complex{re, im}, lifted values as (1+D) doubles.
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <cmath>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -190,15 +192,53 @@ struct TrackResult {
   double final_loss = 0.0;
   int correspondences = 0;
 };
+// icp.hpp:103-114
+struct TraceRow {
+  int iteration = 0;
+  double loss = 0.0, gradient_norm = 0.0, translation_error = 0.0, rotation_error = 0.0;
+};
+struct TrackTrace {
+  bool has_ground_truth = false;
+  std::array<double, 12> ground_truth{};
+  std::vector<TraceRow> rows;
+};
 inline TrackResult track_frame(Context& c, const Volume& vol, const Image<double>& depth,
                                const std::array<double, 12>& init_camera_to_world, const csf_intrinsics& k,
-                               const csf_icp_cfg* cfg = nullptr) {
+                               const csf_icp_cfg* cfg = nullptr, TrackTrace* trace = nullptr) {
   csf_icp_cfg def;
   csf_default_icp_cfg(&def);
+  const csf_icp_cfg& cf = cfg ? *cfg : def;
   TrackResult r;
   csf_track_result tr{};
-  check(c.get(), csf_track_frame(vol.get(), depth.data.data(), depth.width, depth.height, init_camera_to_world.data(),
-                                 &k, cfg ? cfg : &def, r.pose.data(), &tr));
+  if (!trace) {
+    check(c.get(), csf_track_frame(vol.get(), depth.data.data(), depth.width, depth.height,
+                                   init_camera_to_world.data(), &k, &cf, r.pose.data(), &tr));
+  } else {
+    const int cap = std::max(1, cf.level_iterations[0] + cf.level_iterations[1] + cf.level_iterations[2]);
+    std::vector<double> rows(15 * static_cast<size_t>(cap));
+    int n = 0;
+    check(c.get(), csf_track_frame_traced(vol.get(), depth.data.data(), depth.width, depth.height,
+                                          init_camera_to_world.data(), &k, &cf, r.pose.data(), &tr, rows.data(), cap,
+                                          &n));
+    for (int i = 0; i < n && i < cap; ++i) {
+      const double* w = rows.data() + 15 * i;
+      TraceRow row;
+      row.iteration = static_cast<int>(w[0]);
+      row.loss = w[1];
+      row.gradient_norm = w[2];
+      row.translation_error = row.rotation_error = std::nan("");
+      if (trace->has_ground_truth) {  // icp.cpp:220-226 (host arithmetic on the returned pose)
+        const auto& g = trace->ground_truth;
+        const double dx = w[12] - g[9], dy = w[13] - g[10], dz = w[14] - g[11];
+        row.translation_error = std::sqrt(dx * dx + (dy * dy + dz * dz));
+        double tr3 = 0.0;  // trace(g_R^T R)
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) tr3 += g[3 * b + a] * w[3 + 3 * b + a];
+        row.rotation_error = std::acos(std::max(-1.0, std::min(1.0, (tr3 - 1.0) / 2.0))) * 180.0 / M_PI;
+      }
+      trace->rows.push_back(row);
+    }
+  }
   r.iterations = tr.iterations;
   r.converged = tr.converged != 0;
   r.final_loss = tr.final_loss;

@@ -233,6 +233,14 @@ int csf_raycast(csf_volume vol, const double* pose, const double* intr, int w, i
  * last iteration's loss_after / correspondences (icp.cpp:207-209). */
 int csf_track_frame(csf_volume vol, const double* depth, int w, int h, const double* init_pose,
                     const csf_intrinsics* k, const csf_icp_cfg* cfg, double* out_pose, csf_track_result* result);
+/* track_frame(..., TrackTrace*) (icp.hpp:130-133, icp.cpp:213-228): also the
+ * trace rows [trace_cap][15] = iteration, mean loss, gradient norm (the
+ * solver's s.gradient: 2 b for linearized, the CSFD gradient otherwise), then
+ * the camera->world pose [12] after the step; *n_trace rows (may exceed
+ * trace_cap).  Ground-truth errors are host arithmetic on the poses (mirrors). */
+int csf_track_frame_traced(csf_volume vol, const double* depth, int w, int h, const double* init_pose,
+                           const csf_intrinsics* k, const csf_icp_cfg* cfg, double* out_pose,
+                           csf_track_result* result, double* trace, int trace_cap, int* n_trace);
 
 /* icp.cpp:89-126 — associate(measured, predicted, pose, prediction_pose, k,
  * cfg, stride): maps [h][w][3] (vertices camera / world, normals), poses

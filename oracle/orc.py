@@ -42,6 +42,8 @@ def lib() -> C.CDLL:
             "orc_volume_hash": (ip, [vp, i32p, u64p, i32p, i32p]),
             "orc_track_frame": (ip, [vp, dp, ip, ip, dp, C.POINTER(_capi.Intrinsics), C.POINTER(_capi.IcpCfg), ip,
                                      dp, C.POINTER(_capi.TrackResult)]),
+            "orc_track_frame_traced": (ip, [vp, dp, ip, ip, dp, C.POINTER(_capi.Intrinsics), C.POINTER(_capi.IcpCfg),
+                                            dp, C.POINTER(_capi.TrackResult), dp, ip, C.POINTER(C.c_int)]),
             "orc_workload": (ip, [ip, ip, ip, ip, fp, dp, C.POINTER(_capi.Intrinsics)]),
             "orc_pipeline_run": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, i32p, dp]),
             "orc_associate": (ip, [dp, dp, dp, dp, ip, ip, dp, dp, C.POINTER(_capi.Intrinsics), C.POINTER(_capi.IcpCfg),
@@ -206,6 +208,19 @@ class Volume:
         _check(lib().orc_track_frame(self.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg), int(canonical),
                                      _dp(out), C.byref(res)))
         return out, res
+
+    def track_frame_traced(self, depth, init_pose12, k, cfg):
+        d = np.ascontiguousarray(depth, dtype=np.float64)
+        h, w = d.shape
+        init = np.ascontiguousarray(init_pose12, dtype=np.float64)
+        out = np.empty(12)
+        res = _capi.TrackResult()
+        cap = 64
+        rows = np.zeros((cap, 3))
+        n = C.c_int()
+        _check(lib().orc_track_frame_traced(self.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg), _dp(out),
+                                            C.byref(res), _dp(rows), cap, C.byref(n)))
+        return out, res, rows[:n.value].copy()
 
 
 def workload(config: int, n_frames: int, width: int = 0, height: int = 0):

@@ -135,7 +135,7 @@ struct VolBase {
   virtual int blocks() const = 0;
   virtual void hash_tables(int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords) const = 0;
   virtual TrackResult track(const Image<double>& depth, const Pose& init, const Intrinsics& k, const IcpConfig& cfg,
-                            bool canonical) const = 0;
+                            bool canonical, std::vector<TraceRow>* trace = nullptr) const = 0;
   virtual void view_scores(const double* poses, int n, const Intrinsics& k, double w0, double beta, double h,
                            double* scores, double* grads) const = 0;
   virtual void sample_points(const double* pts, int n, int grad, double* out, int32_t* valid) const = 0;
@@ -200,8 +200,8 @@ struct Vol : VolBase {
     }
   }
   TrackResult track(const Image<double>& depth, const Pose& init, const Intrinsics& k, const IcpConfig& cfg,
-                    bool canonical) const override {
-    return track_frame(vol, depth, init, k, cfg, nullptr, canonical);
+                    bool canonical, std::vector<TraceRow>* trace = nullptr) const override {
+    return track_frame(vol, depth, init, k, cfg, trace, canonical);
   }
   RelocProblem reloc_problem(const Image<double>& query, const Intrinsics& k) const override {
     return make_reloc_problem(vol, query, k);
@@ -357,6 +357,34 @@ int orc_track_frame(void* v, const double* depth, int w, int h, const double* in
       res->converged = r.converged;
       res->correspondences = r.correspondences;
       res->final_loss = r.final_loss;
+    }
+  });
+}
+
+// track_frame with the trace rows [cap][3] (iteration, loss, gradient norm).
+int orc_track_frame_traced(void* v, const double* depth, int w, int h, const double* init_pose,
+                           const csf_intrinsics* k, const csf_icp_cfg* cfg, double* out_pose, csf_track_result* res,
+                           double* rows, int cap, int* n_rows) {
+  return guard([&] {
+    Pose init;
+    for (int e = 0; e < 9; ++e) init.rotation(e / 3, e % 3) = init_pose[e];
+    for (int e = 0; e < 3; ++e) init.translation[e] = init_pose[9 + e];
+    std::vector<TraceRow> tr;
+    const TrackResult r =
+        static_cast<VolBase*>(v)->track(image_of(depth, w, h), init, to_intr(*k), to_icp(*cfg), true, &tr);
+    for (int e = 0; e < 9; ++e) out_pose[e] = r.pose.rotation(e / 3, e % 3);
+    for (int e = 0; e < 3; ++e) out_pose[9 + e] = r.pose.translation[e];
+    if (res) {
+      res->iterations = r.iterations;
+      res->converged = r.converged;
+      res->correspondences = r.correspondences;
+      res->final_loss = r.final_loss;
+    }
+    *n_rows = static_cast<int>(tr.size());
+    for (int i = 0; i < static_cast<int>(tr.size()) && i < cap; ++i) {
+      rows[3 * i] = tr[i].iteration;
+      rows[3 * i + 1] = tr[i].loss;
+      rows[3 * i + 2] = tr[i].gradient_norm;
     }
   });
 }

@@ -33,6 +33,7 @@ from . import capi as _capi
 __all__ = [
     "InvalidArgument", "DomainError", "Context", "bilateral_filter", "downsample_depth", "build_depth_pyramid",
     "measure_surface", "TsdfVolume", "HashedVolume", "surface_update", "raycast", "track_frame", "TrackResult",
+    "TrackTrace", "TraceRow", "write_trace_csv",
     "icp_energy", "icp_loss", "icp_gradient", "icp_hessian", "icp_energy_derivs", "associate", "linearized_step",
     "pairwise_sum", "complex_depth", "perturb_depth",
     "Pipeline", "PipelineResult", "HessianResult", "synth_workload", "look_at", "config5_views", "save_volume", "load_volume", "measured_tsdf", "default_icp_cfg", "default_raycast_cfg", "intrinsics",
@@ -506,9 +507,32 @@ class TrackResult:
     correspondences: int
 
 
-def track_frame(volume: _Volume, depth, init_camera_to_world, k, cfg: Optional[_capi.IcpCfg] = None) -> TrackResult:
+@dataclass
+class TraceRow:
+    """icp.hpp:103-109"""
+    iteration: int
+    loss: float
+    gradient_norm: float
+    translation_error: float
+    rotation_error: float  # degrees
+
+
+@dataclass
+class TrackTrace:
+    """icp.hpp:111-114: optional ground truth (12,) and the per-iteration rows."""
+    ground_truth: Optional[np.ndarray] = None
+    rows: list = None
+
+    def __post_init__(self):
+        if self.rows is None:
+            self.rows = []
+
+
+def track_frame(volume: _Volume, depth, init_camera_to_world, k, cfg: Optional[_capi.IcpCfg] = None,
+                trace: Optional[TrackTrace] = None) -> TrackResult:
     """icp.cpp:169-244 on the device, every solver family (cfg.solver:
-    linearized, Newton — the reference default — gradient descent, NCG)."""
+    linearized, Newton — the reference default — gradient descent, NCG).
+    With `trace`, one TraceRow per iteration is appended (icp.cpp:213-228)."""
     ctx = volume.ctx
     d = _f64(depth)
     h, w = d.shape
@@ -516,9 +540,35 @@ def track_frame(volume: _Volume, depth, init_camera_to_world, k, cfg: Optional[_
     out = np.empty(12)
     res = _capi.TrackResult()
     cfg = cfg if cfg is not None else default_icp_cfg()
-    ctx.check(ctx.lib.csf_track_frame(volume.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg), _dp(out),
-                                      C.byref(res)))
+    if trace is None:
+        ctx.check(ctx.lib.csf_track_frame(volume.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg), _dp(out),
+                                          C.byref(res)))
+    else:
+        cap = max(int(sum(cfg.level_iterations)), 1)
+        rows = np.zeros((cap, 15))
+        n = C.c_int()
+        ctx.check(ctx.lib.csf_track_frame_traced(volume.h, _dp(d), w, h, _dp(init), C.byref(k), C.byref(cfg),
+                                                 _dp(out), C.byref(res), _dp(rows), cap, C.byref(n)))
+        gt = None if trace.ground_truth is None else lift_pose(trace.ground_truth, 0)[:, 0]
+        for r in rows[:min(n.value, cap)]:
+            te = re_ = float("nan")
+            if gt is not None:
+                dt = r[12:15] - gt[9:]
+                te = float(np.sqrt(dt[0] * dt[0] + (dt[1] * dt[1] + dt[2] * dt[2])))
+                rel = gt[:9].reshape(3, 3).T @ r[3:12].reshape(3, 3)
+                re_ = float(np.degrees(np.arccos(np.clip((np.trace(rel) - 1.0) / 2.0, -1.0, 1.0))))  # se3.hpp:109-113
+            trace.rows.append(TraceRow(int(r[0]), float(r[1]), float(r[2]), te, re_))
     return TrackResult(out, res.iterations, bool(res.converged), res.final_loss, res.correspondences)
+
+
+def write_trace_csv(path, trace: TrackTrace) -> None:
+    """icp.cpp:155-167"""
+    lines = ["iteration,loss,gradient norm,translation error,rotation error"]
+    g = lambda v: format(v, ".17g") if v == v else "nan"
+    for r in trace.rows:
+        lines.append(f"{r.iteration},{g(r.loss)},{g(r.gradient_norm)},{g(r.translation_error)},{g(r.rotation_error)}")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
 
 
 # ----------------------------------------------------------------------------- icp: associate / linearized step

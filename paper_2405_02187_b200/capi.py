@@ -26,7 +26,7 @@ EXPORTS = (
     "csf_volume_create_dense", "csf_volume_create_hashed", "csf_volume_destroy", "csf_volume_upload",
     "csf_volume_download", "csf_volume_block_count", "csf_volume_save", "csf_volume_load", "csf_sample_tsdf",
     "csf_sample_gradient", "csf_measured_tsdf", "csf_volume_download_hash", "csf_surface_update",
-    "csf_raycast", "csf_track_frame", "csf_icp_energy_derivs", "csf_view_scores", "csf_associate",
+    "csf_raycast", "csf_track_frame", "csf_track_frame_traced", "csf_icp_energy_derivs", "csf_view_scores", "csf_associate",
     "csf_linearized_step", "csf_pairwise_sum", "csf_pipeline_create", "csf_pipeline_destroy", "csf_pipeline_upload",
     "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_hessian", "csf_pipeline_run_host",
     "csf_synth_workload", "csf_default_reloc_cfg", "csf_reloc_create", "csf_reloc_destroy", "csf_reloc_info",
@@ -132,6 +132,8 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_track_frame": (ip, [vp, dp, ip, ip, dp, C.POINTER(Intrinsics), C.POINTER(IcpCfg), dp,
                                  C.POINTER(TrackResult)]),
         "csf_icp_energy_derivs": (ip, [vp, dp, ip, dp, dp, C.c_double, dp, dp, dp]),
+        "csf_track_frame_traced": (ip, [vp, dp, ip, ip, dp, C.POINTER(Intrinsics), C.POINTER(IcpCfg), dp,
+                                        C.POINTER(TrackResult), dp, ip, C.POINTER(C.c_int)]),
         "csf_associate": (ip, [vp, dp, dp, dp, dp, ip, ip, dp, dp, C.POINTER(Intrinsics), C.POINTER(IcpCfg), ip, dp,
                                C.POINTER(C.c_int)]),
         "csf_linearized_step": (ip, [vp, dp, ip, dp, dp]),

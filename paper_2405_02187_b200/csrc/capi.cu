@@ -1646,9 +1646,26 @@ void apply_increment_h(const Vec6h& d, double* pose12) {
 
 }  // namespace
 
+static int track_frame_impl(csf_volume v, const double* depth, int w, int h, const double* init_pose,
+                            const csf_intrinsics* k, const csf_icp_cfg* cfg_in, double* out_pose,
+                            csf_track_result* result, double* trace, int trace_cap, int* n_trace);
+
 extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, const double* init_pose,
                                const csf_intrinsics* k, const csf_icp_cfg* cfg_in, double* out_pose,
                                csf_track_result* result) {
+  return track_frame_impl(v, depth, w, h, init_pose, k, cfg_in, out_pose, result, nullptr, 0, nullptr);
+}
+
+extern "C" int csf_track_frame_traced(csf_volume v, const double* depth, int w, int h, const double* init_pose,
+                                      const csf_intrinsics* k, const csf_icp_cfg* cfg_in, double* out_pose,
+                                      csf_track_result* result, double* trace, int trace_cap, int* n_trace) {
+  if (!trace || !n_trace || trace_cap < 0) return CSF_EINVAL;
+  return track_frame_impl(v, depth, w, h, init_pose, k, cfg_in, out_pose, result, trace, trace_cap, n_trace);
+}
+
+static int track_frame_impl(csf_volume v, const double* depth, int w, int h, const double* init_pose,
+                            const csf_intrinsics* k, const csf_icp_cfg* cfg_in, double* out_pose,
+                            csf_track_result* result, double* trace, int trace_cap, int* n_trace) {
   if (!v || !depth || !init_pose || !k || !out_pose) return CSF_EINVAL;
   csf_ctx ctx = v->ctx;
   csf_icp_cfg cfg;
@@ -1716,6 +1733,7 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
   csf_raycast_cfg rcfg;
   csf_default_raycast_cfg(&rcfg);
   const LineSearch ls;
+  if (n_trace) *n_trace = 0;
   Stepper stepper{cfg.solver == CSF_SOLVER_CONJUGATE_GRADIENT, cfg.ncg_restart};
   double lambda = cfg.levenberg_lambda0;
   int iteration = 0, n_corr = 0;
@@ -1750,7 +1768,7 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
       if (err) break;
       n_corr = n;
       if (n < 12) break;  // icp.cpp:199
-      Vec6h delta{};
+      Vec6h delta{}, grad_it{};
       double loss_after = 0.0;
       if (cfg.solver == CSF_SOLVER_LINEARIZED) {
         // canonical slot-tiled normal equations + the real LDLT step on the
@@ -1760,7 +1778,10 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
         TrackState hs;
         CUDA_TRY(ctx, cudaMemcpyAsync(&hs, st.p, sizeof(TrackState), cudaMemcpyDeviceToHost, ctx->stream));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-        for (int i = 0; i < 6; ++i) delta[i] = hs.delta[i];
+        for (int i = 0; i < 6; ++i) {
+          delta[i] = hs.delta[i];
+          grad_it[i] = 2.0 * hs.b[i];  // s.gradient = 2 b (icp.cpp:41)
+        }
         loss_after = energy_at(delta, n, hpose, &err);
       } else {
         double E0 = 0.0, g[6], H[36];
@@ -1771,6 +1792,7 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
         if (err) break;
         Vec6h grad;
         for (int i = 0; i < 6; ++i) grad[i] = g[i];
+        grad_it = grad;
         loss_after = E0;
         if (cfg.solver == CSF_SOLVER_NEWTON) {
           // levenberg_newton_step (descent.hpp:109-144)
@@ -1844,6 +1866,16 @@ extern "C" int csf_track_frame(csf_volume v, const double* depth, int w, int h, 
       apply_increment_h(delta, hpose);
       ++iteration;
       final_loss = loss_after / static_cast<double>(n);
+      if (trace) {  // TraceRow (icp.hpp:103-109): iteration, loss, gradient norm, then the pose
+        if (*n_trace < trace_cap) {
+          double* row = trace + 15 * static_cast<size_t>(*n_trace);
+          row[0] = iteration;
+          row[1] = final_loss;
+          row[2] = norm6h(grad_it);
+          std::copy(hpose, hpose + 12, row + 3);
+        }
+        ++*n_trace;
+      }
       if (norm6h(delta) < cfg.step_tolerance) {
         if (level == 0) converged = true;
         break;

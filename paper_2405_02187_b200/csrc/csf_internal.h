@@ -82,6 +82,7 @@ struct TrackState {
   double pred_w2c[12];  // real inverse of the prediction pose (association)
   double cur_c2w[12];   // real current pose snapshot (unused by kernels)
   double delta[6];      // real increment of the last solved ICP iteration
+  double b[6];          // its real J^T r (the linearized solver's gradient / 2, icp.cpp:41)
 };
 
 // ---- energy.cu: icp_energy / gradient / Hessian and the correspondence list

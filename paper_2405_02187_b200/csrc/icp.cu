@@ -257,6 +257,8 @@ __device__ __noinline__ void icp_solve_body(TrackState* st, const double* __rest
     st->n_corr = n;
 #pragma unroll
     for (int i = 0; i < 6; ++i) st->delta[i] = re(d[i]);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) st->b[i] = s_acc[(21 + i) * C];
     if (nrm < tol) {
       st->level_done = 1;
       if (level == 0) st->converged = 1;

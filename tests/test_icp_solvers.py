@@ -78,3 +78,12 @@ def test_track_frame_solvers(gpu_ctx, orc, solver):
     assert bool(r_g.converged) == bool(r_o.converged)
     assert r_g.final_loss == r_o.final_loss and np.isfinite(r_g.final_loss)
     assert np.linalg.norm(r_g.pose[9:] - gt[4][9:]) < 0.02
+    # track_frame(..., TrackTrace*) (icp.cpp:213-228): the rows are bit-identical too
+    tr = csf.TrackTrace(ground_truth=gt[4])
+    r_t = csf.track_frame(vol_g, d[4].astype(np.float64), init, k, cfg, trace=tr)
+    _, _, rows_o = vol_o.track_frame_traced(d[4].astype(np.float64), init, k, cfg)
+    assert np.array_equal(r_t.pose, p_o) and len(tr.rows) == len(rows_o) == r_o.iterations
+    for row, ro in zip(tr.rows, rows_o):
+        assert (row.iteration, row.loss, row.gradient_norm) == (int(ro[0]), ro[1], ro[2])
+        assert np.isfinite(row.translation_error) and np.isfinite(row.rotation_error)
+    assert tr.rows[-1].loss == r_g.final_loss
