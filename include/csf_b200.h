@@ -359,6 +359,8 @@ void csf_default_surfel_cfg(csf_surfel_cfg* cfg);
 int csf_surfels_create(csf_ctx ctx, int n_channels, csf_surfels* out);
 int csf_surfels_destroy(csf_surfels m);
 int csf_surfels_count(csf_surfels m, int* n);
+/* empty the map, keeping its device capacity and scratch */
+int csf_surfels_clear(csf_surfels m);
 /* host copies of the map (any output may be NULL) / replace the map */
 int csf_surfels_download(csf_surfels m, double* positions, double* normals, double* radius, double* confidence,
                          int32_t* timestamps);

@@ -33,7 +33,7 @@ EXPORTS = (
     "csf_reloc_energy", "csf_relocalize", "csf_depth_cloud", "csf_eval_nn_error", "csf_io_last_error",
     "csf_write_depth_png16", "csf_read_depth_png16", "csf_read_intrinsics", "csf_write_intrinsics",
     "csf_read_trajectory", "csf_write_trajectory", "csf_default_surfel_cfg", "csf_surfels_create",
-    "csf_surfels_destroy", "csf_surfels_count", "csf_surfels_download", "csf_surfels_upload", "csf_render_index_map",
+    "csf_surfels_destroy", "csf_surfels_clear", "csf_surfels_count", "csf_surfels_download", "csf_surfels_upload", "csf_render_index_map",
     "csf_associate_surfels", "csf_update_surfels", "csf_predict_maps", "csf_sample_confidence",
 )
 RELOC_GRADIENT_DESCENT, RELOC_NEWTON = 0, 1
@@ -164,6 +164,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_surfels_create": (ip, [vp, ip, C.POINTER(vp)]),
         "csf_surfels_destroy": (ip, [vp]),
         "csf_surfels_count": (ip, [vp, C.POINTER(C.c_int)]),
+        "csf_surfels_clear": (ip, [vp]),
         "csf_surfels_download": (ip, [vp, dp, dp, dp, dp, i32p]),
         "csf_surfels_upload": (ip, [vp, ip, dp, dp, dp, dp, i32p]),
         "csf_render_index_map": (ip, [vp, dp, C.POINTER(Intrinsics), C.POINTER(C.c_uint32), i32p, C.POINTER(C.c_int)]),

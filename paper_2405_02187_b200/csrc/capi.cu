@@ -2285,6 +2285,11 @@ extern "C" int csf_surfels_destroy(csf_surfels m) {
   delete m;
   return CSF_OK;
 }
+extern "C" int csf_surfels_clear(csf_surfels m) {
+  if (!m) return CSF_EINVAL;
+  m->n = 0;  // capacity and scratch are kept (a new map without re-allocation)
+  return CSF_OK;
+}
 extern "C" int csf_surfels_count(csf_surfels m, int* n) {
   if (!m || !n) return CSF_EINVAL;
   *n = m->n;

@@ -49,6 +49,10 @@ class SurfelMap:
         except Exception:
             pass
 
+    def clear(self) -> None:
+        """An empty map that keeps its device capacity (no re-allocation)."""
+        self.ctx.check(self.ctx.lib.csf_surfels_clear(self.h))
+
     def size(self) -> int:
         n = C.c_int()
         self.ctx.check(self.ctx.lib.csf_surfels_count(self.h, C.byref(n)))
