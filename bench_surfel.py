@@ -60,10 +60,11 @@ def run(args, measured_peak, Clocks):
     depth, gt, k = csf.synth_workload(2, n_frames, ctx=ctx)
     poses = lifted_poses(gt)
     frames = []
-    for f in range(n_frames):
-        d = np.zeros(depth[f].shape + (1 + D,))
+    for f in range(n_frames):  # lifted host frames in pinned memory (as the headline's e2e)
+        t = torch.zeros(depth[f].shape + (1 + D,), dtype=torch.float64, pin_memory=True)
+        d = t.numpy()
         d[..., 0] = depth[f]
-        frames.append(np.ascontiguousarray(d))
+        frames.append(d)
     cfg = csf.default_surfel_cfg()
     stream = torch.cuda.ExternalStream(ctx.stream)
 
