@@ -381,6 +381,11 @@ int csf_associate_surfels(csf_surfels m, const double* depth, int w, int h, cons
 int csf_update_surfels(csf_surfels m, const double* depth, int w, int h, const double* camera_to_world,
                        const csf_intrinsics* k, int frame_index, const csf_surfel_cfg* cfg, int* merged_pixels,
                        int* created);
+/* the same with an unperturbed depth [h][w] (complex_depth, frames.cpp:77-81:
+ * zero channels; lifted on the device) */
+int csf_update_surfels_real(csf_surfels m, const double* depth, int w, int h, const double* camera_to_world,
+                            const csf_intrinsics* k, int frame_index, const csf_surfel_cfg* cfg, int* merged_pixels,
+                            int* created);
 /* surfel.cpp:238-263 — nearest-surfel splat: vertices / normals [h][w][3] */
 int csf_predict_maps(csf_surfels m, const double* camera_to_world, const csf_intrinsics* k, double* vertices,
                      double* normals);

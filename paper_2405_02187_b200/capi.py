@@ -34,7 +34,7 @@ EXPORTS = (
     "csf_write_depth_png16", "csf_read_depth_png16", "csf_read_intrinsics", "csf_write_intrinsics",
     "csf_read_trajectory", "csf_write_trajectory", "csf_default_surfel_cfg", "csf_surfels_create",
     "csf_surfels_destroy", "csf_surfels_clear", "csf_surfels_count", "csf_surfels_download", "csf_surfels_upload", "csf_render_index_map",
-    "csf_associate_surfels", "csf_update_surfels", "csf_predict_maps", "csf_sample_confidence",
+    "csf_associate_surfels", "csf_update_surfels", "csf_update_surfels_real", "csf_predict_maps", "csf_sample_confidence",
 )
 RELOC_GRADIENT_DESCENT, RELOC_NEWTON = 0, 1
 
@@ -172,6 +172,8 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
                                        ip, C.POINTER(C.c_int)]),
         "csf_update_surfels": (ip, [vp, dp, ip, ip, dp, C.POINTER(Intrinsics), ip, C.POINTER(SurfelCfg),
                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+        "csf_update_surfels_real": (ip, [vp, dp, ip, ip, dp, C.POINTER(Intrinsics), ip, C.POINTER(SurfelCfg),
+                                         C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "csf_predict_maps": (ip, [vp, dp, C.POINTER(Intrinsics), dp, dp]),
         "csf_sample_confidence": (C.c_double, [C.POINTER(Intrinsics), ip, ip]),
         "csf_write_depth_png16": (ip, [C.c_char_p, dp, ip, ip, C.c_double]),

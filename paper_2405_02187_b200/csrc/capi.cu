@@ -2211,6 +2211,7 @@ struct csf_surfels_s {
   DevBuf<double> pos, nrm, conf, rad;
   DevBuf<int> ts;
   DevBuf<double> in;  // depth [P][C] + pose [12][C] + intrinsics [4][C]
+  DevBuf<double> in_real;  // real depth [P] (csf_update_surfels_real)
   SurfelScratch ws;
   ~csf_surfels_s() {
     pos.release();
@@ -2219,6 +2220,7 @@ struct csf_surfels_s {
     rad.release();
     ts.release();
     in.release();
+    in_real.release();
     surfel_scratch_release(ws);
   }
   SurfelArrays arrays() { return SurfelArrays{pos.p, nrm.p, conf.p, rad.p, ts.p}; }
@@ -2359,7 +2361,7 @@ extern "C" int csf_render_index_map(csf_surfels m, const double* c2w, const csf_
 // upload depth / pose / intrinsics and run index map + association
 static int surfels_assoc_common(csf_surfels m, const double* depth, int w, int h, const double* c2w,
                                 const csf_intrinsics* k, const csf_surfel_cfg* cfg_in, int* total, int* merged,
-                                double* c2w12, double* k4) {
+                                double* c2w12, double* k4, bool real_depth = false) {
   csf_ctx ctx = m->ctx;
   const int C = 1 + m->D;
   const size_t P = static_cast<size_t>(w) * h;
@@ -2376,7 +2378,13 @@ static int surfels_assoc_common(csf_surfels m, const double* depth, int w, int h
   k4_of(k, k4);
   for (int e = 0; e < 4; ++e) intr[e * C] = k4[e];
   for (int e = 0; e < 12; ++e) c2w12[e] = c2w[e * C];
-  CUDA_TRY(ctx, cudaMemcpyAsync(d_depth, depth, sizeof(double) * P * C, cudaMemcpyHostToDevice, ctx->stream));
+  if (real_depth) {  // unperturbed depth: upload [P] and lift on the device (1/(1+D) of the bytes)
+    CUDA_TRY(ctx, m->in_real.alloc(P));
+    CUDA_TRY(ctx, cudaMemcpyAsync(m->in_real.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+    launch_expand_depth(ctx->stream, m->in_real.p, static_cast<long long>(P), C, d_depth);
+  } else {
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_depth, depth, sizeof(double) * P * C, cudaMemcpyHostToDevice, ctx->stream));
+  }
   CUDA_TRY(ctx, cudaMemcpyAsync(d_pose, c2w, sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(d_intr, intr.data(), sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
   int cnt = 0;
@@ -2417,15 +2425,28 @@ extern "C" int csf_associate_surfels(csf_surfels m, const double* depth, int w, 
   return CSF_OK;
 }
 
+static int update_surfels_impl(csf_surfels m, const double* depth, int w, int h, const double* c2w,
+                               const csf_intrinsics* k, int frame_index, const csf_surfel_cfg* cfg,
+                               int* merged_pixels, int* created, bool real_depth);
 extern "C" int csf_update_surfels(csf_surfels m, const double* depth, int w, int h, const double* c2w,
                                   const csf_intrinsics* k, int frame_index, const csf_surfel_cfg* cfg,
                                   int* merged_pixels, int* created) {
+  return update_surfels_impl(m, depth, w, h, c2w, k, frame_index, cfg, merged_pixels, created, false);
+}
+extern "C" int csf_update_surfels_real(csf_surfels m, const double* depth, int w, int h, const double* c2w,
+                                       const csf_intrinsics* k, int frame_index, const csf_surfel_cfg* cfg,
+                                       int* merged_pixels, int* created) {
+  return update_surfels_impl(m, depth, w, h, c2w, k, frame_index, cfg, merged_pixels, created, true);
+}
+static int update_surfels_impl(csf_surfels m, const double* depth, int w, int h, const double* c2w,
+                               const csf_intrinsics* k, int frame_index, const csf_surfel_cfg* cfg,
+                               int* merged_pixels, int* created, bool real_depth) {
   if (!m || !depth || !c2w || !k || w <= 0 || h <= 0) return CSF_EINVAL;
   csf_ctx ctx = m->ctx;
   cudaSetDevice(ctx->device);
   int T = 0, merged = 0, cr = 0;
   double c2w12[12], k4[4];
-  int rc = surfels_assoc_common(m, depth, w, h, c2w, k, cfg, &T, &merged, c2w12, k4);
+  int rc = surfels_assoc_common(m, depth, w, h, c2w, k, cfg, &T, &merged, c2w12, k4, real_depth);
   if (rc) return rc;
   if (surfel_created_count(ctx->stream, m->ws, w * h, &cr)) return fail(ctx, CSF_ECUDA, "update_surfels: CUDA error");
   rc = surfels_reserve(m, m->n + cr);

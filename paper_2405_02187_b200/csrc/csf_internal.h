@@ -173,6 +173,7 @@ int surfel_commit(cudaStream_t s, SurfelScratch& ws, SurfelArrays m, int n, int 
 int surfel_predict(cudaStream_t s, SurfelScratch& ws, const double* pos, const double* nrm, int n, int D,
                    const double* c2w12, const double* k4, int w, int h, double* Vo, double* No);
 void surfel_scratch_release(SurfelScratch& ws);
+void launch_expand_depth(cudaStream_t s, const double* real, long long P, int C, double* lifted);
 
 // Launch failures seen by the kernel translation units are recorded here and
 // surfaced as CSF_ECUDA by the next status check of the C-ABI (a failed

@@ -545,6 +545,14 @@ __global__ void k_fill_u64(unsigned long long* a, int n, unsigned long long v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
 }
+// real depth [P] -> lifted depth [P][C] with zero channels
+__global__ void k_expand_depth(const double* __restrict__ real, long long P, int C, double* __restrict__ lifted) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= P * C) return;
+  const long long p = i / C;
+  lifted[i] = (i % C) == 0 ? real[p] : 0.0;
+}
+
 __global__ void k_fill_iota(int* a, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = i;
@@ -816,6 +824,12 @@ int surfel_predict(cudaStream_t s, SurfelScratch& ws, const double* pos, const d
   launch_pdl(k_pred_write, dim3(grid1(P)), dim3(256), 0, s, static_cast<const int*>(ws.ibest), P, C, pos, nrm, Vo, No);
   chk("surfel_predict");
   return 0;
+}
+
+void launch_expand_depth(cudaStream_t s, const double* real, long long P, int C, double* lifted) {
+  const long long n = P * C;
+  if (n > 0) k_expand_depth<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(real, P, C, lifted);
+  chk("expand_depth");
 }
 
 void surfel_scratch_release(SurfelScratch& ws) {

@@ -161,13 +161,20 @@ def update_surfels(map: SurfelMap, depth, camera_to_world, k: _capi.Intrinsics, 
     """surfel.cpp:121-236: lifted depth (h, w[, 1+D]) at a lifted camera->world pose (12, 1+D)."""
     ctx = map.ctx
     D = map.channels
-    d = _lifted_depth(depth, D)
-    h, w = d.shape[:2]
     pose = np.ascontiguousarray(lift_pose(camera_to_world, D))
     cfg = cfg if cfg is not None else default_surfel_cfg()
     mp, cr = C.c_int(), C.c_int()
-    ctx.check(ctx.lib.csf_update_surfels(map.h, _dp(d), w, h, _dp(pose), C.byref(k), frame_index, C.byref(cfg),
-                                         C.byref(mp), C.byref(cr)))
+    raw = np.asarray(depth)
+    if raw.ndim == 2:  # unperturbed depth: lifted on the device
+        d = np.ascontiguousarray(raw, dtype=np.float64)
+        h, w = d.shape
+        ctx.check(ctx.lib.csf_update_surfels_real(map.h, _dp(d), w, h, _dp(pose), C.byref(k), frame_index,
+                                                  C.byref(cfg), C.byref(mp), C.byref(cr)))
+    else:
+        d = _lifted_depth(depth, D)
+        h, w = d.shape[:2]
+        ctx.check(ctx.lib.csf_update_surfels(map.h, _dp(d), w, h, _dp(pose), C.byref(k), frame_index, C.byref(cfg),
+                                             C.byref(mp), C.byref(cr)))
     return SurfelUpdateStats(mp.value, cr.value)
 
 

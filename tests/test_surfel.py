@@ -174,3 +174,20 @@ def test_surfel_ply_export(gpu_ctx, tmp_path):
     n = m.size()
     assert lines[0] == "ply" and lines[2] == f"element vertex {n}" and lines[12] == "end_header"
     assert len(lines) == 13 + n and len(lines[13].split()) == 9
+
+
+@pytest.mark.gpu
+def test_surfel_real_depth_path(gpu_ctx):
+    """An unperturbed (h, w) depth is lifted on the device: the same map as
+    the explicit zero-channel lifted depth, bit for bit."""
+    import paper_2405_02187_b200 as csf
+    depth, poses, gt, k = _frames(2, D=2)
+    a = csf.SurfelMap(2, ctx=gpu_ctx)
+    b = csf.SurfelMap(2, ctx=gpu_ctx)
+    for f in range(2):
+        sa = csf.update_surfels(a, depth[f], poses[f], k, f)
+        sb = csf.update_surfels(b, np.ascontiguousarray(depth[f][..., 0]), poses[f], k, f)
+        assert (sa.merged_pixels, sa.created) == (sb.merged_pixels, sb.created)
+    da, db = a.download(), b.download()
+    for key in da:
+        assert np.array_equal(da[key], db[key])
