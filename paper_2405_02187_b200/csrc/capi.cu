@@ -796,7 +796,13 @@ struct csf_pipeline_s {
   DevBuf<int> counts, stats, dirs, pair_i, pair_j;
   DevBuf<TrackState> st;
   DevBuf<double2> hits;
+  // run_host: frames uploaded on a copy stream, frame f's kernels wait on ev[f]
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> frame_ev;
+  bool wait_frames = false;
   ~csf_pipeline_s() {
+    for (cudaEvent_t e : frame_ev) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     hits.release();
     frames.release(); gt.release(); raw.release(); pyr0.release(); pyr1.release(); pyr2.release(); vre.release();
     nre.release(); vim.release(); nim.release(); partials.release(); pose.release(); pred_pose.release();
@@ -976,6 +982,7 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
   else
     launch_seed(L, p->G, p->Dp, p->dirs.p, p->D, cfg.h, p->gt.p, p->kbase.p, p->pose.p, p->intr_levels.p, p->levels);
   launch_frame_begin(L, st, 0);
+  if (p->wait_frames) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, p->frame_ev[0], 0));
   launch_bilateral(L, p->frames.p, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
   int* upd = &st->pad[1];
   rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p, upd);
@@ -984,6 +991,7 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
 
   for (int f = 1; f < n_frames; ++f) {
     launch_frame_begin(L, st, f);
+    if (p->wait_frames) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, p->frame_ev[f], 0));
     {
       PROF(ctx, kPBilateral);
       launch_bilateral(L, p->frames.p + P * f, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
@@ -1081,11 +1089,36 @@ extern "C" int csf_pipeline_hessian(csf_pipeline p, double* hessian, double* gra
   return CSF_OK;
 }
 
+// One end-to-end call.  The frames go up on a copy stream, one event per
+// frame, and frame f's kernels wait only for frame f's upload, so (from
+// pinned host memory) the H2D of later frames overlaps the device work of
+// earlier ones.
 extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames,
                                      double* gradient, double* objective) {
-  int rc = csf_pipeline_upload(p, depth, gt, n_frames);
-  if (rc) return rc;
-  rc = csf_pipeline_run(p, n_frames);
+  if (!p || !depth || !gt || n_frames <= 0) return CSF_EINVAL;
+  csf_ctx ctx = p->ctx;
+  if (n_frames > p->cfg.max_frames) return fail(ctx, CSF_EINVAL, "csf_pipeline_run_host: more frames than max_frames");
+  cudaSetDevice(ctx->device);
+  if (!p->copy_stream) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  while (static_cast<int>(p->frame_ev.size()) < n_frames) {
+    cudaEvent_t e;
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->frame_ev.push_back(e);
+  }
+  const size_t P = static_cast<size_t>(p->W) * p->H;
+  // the copy stream starts after everything already queued on the context
+  CUDA_TRY(ctx, cudaEventRecord(p->frame_ev[0], ctx->stream));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(p->copy_stream, p->frame_ev[0], 0));
+  CUDA_TRY(ctx, cudaMemcpyAsync(p->gt.p, gt, sizeof(double) * 12 * n_frames, cudaMemcpyHostToDevice, ctx->stream));
+  for (int f = 0; f < n_frames; ++f) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(p->frames.p + P * f, depth + P * f, sizeof(float) * P, cudaMemcpyHostToDevice,
+                                  p->copy_stream));
+    CUDA_TRY(ctx, cudaEventRecord(p->frame_ev[f], p->copy_stream));
+  }
+  p->n_uploaded = n_frames;
+  p->wait_frames = true;
+  int rc = csf_pipeline_run(p, n_frames);
+  p->wait_frames = false;
   if (rc) return rc;
   return csf_pipeline_result(p, gradient, objective, nullptr, nullptr);
 }
