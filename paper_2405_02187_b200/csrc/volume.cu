@@ -52,6 +52,21 @@ __device__ void stage_pose_w2c(const double* __restrict__ pose, const double* __
   __syncthreads();
 }
 
+// The 19 x NDP channel block of the staged inputs, restaged contiguous and
+// 16-byte aligned after them, so the fusion contraction reads two channels
+// per shared-memory load (double2) instead of one.
+__host__ __device__ constexpr int jac_offset(int C) { return (19 * C + 1) & ~1; }
+template <int NDP>
+CSF_DEV void stage_jacobian(double* sm) {
+  if constexpr (NDP > 0 && NDP % 2 == 0) {
+    constexpr int C = 1 + NDP;
+    double* sj = sm + jac_offset(C);
+    for (int i = threadIdx.x; i < 19 * NDP; i += blockDim.x) sj[i] = sm[(i / NDP) * C + 1 + i % NDP];
+    __syncthreads();
+  }
+}
+static size_t integrate_smem(int Dp) { return sizeof(double) * (jac_offset(1 + Dp) + 19 * Dp); }
+
 template <typename S>
 __device__ void load_pose_intr(const double* sm, int Dp, int g0, Pose<S>* w2c, V3<S>* center, Intr<S>* k) {
   const int C = 1 + Dp;
@@ -237,12 +252,28 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
     const double inv_w1 = 1.0 / (wt + 1.0);
     double* fim = vox.fim + v * vox.Dp;
     if constexpr (NDP > 0) {
+      if constexpr (NDP % 2 == 0) {
+        const double* sj = sm + jac_offset(C);
 #pragma unroll
-      for (int d = 0; d < NDP; ++d) {
-        double pim = 0.0;
+        for (int d = 0; d < NDP; d += 2) {
+          double pim0 = 0.0, pim1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < 19; ++k) pim = fma(g[k], sm[k * C + 1 + d], pim);
-        chan[d] = (wt * chan[d] + pim) * inv_w1;
+          for (int k = 0; k < 19; ++k) {
+            const double2 j = *reinterpret_cast<const double2*>(sj + k * NDP + d);
+            pim0 = fma(g[k], j.x, pim0);
+            pim1 = fma(g[k], j.y, pim1);
+          }
+          chan[d] = (wt * chan[d] + pim0) * inv_w1;
+          chan[d + 1] = (wt * chan[d + 1] + pim1) * inv_w1;
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < NDP; ++d) {
+          double pim = 0.0;
+#pragma unroll
+          for (int k = 0; k < 19; ++k) pim = fma(g[k], sm[k * C + 1 + d], pim);
+          chan[d] = (wt * chan[d] + pim) * inv_w1;
+        }
       }
       if constexpr (NDP % 2 == 0) {
 #pragma unroll
@@ -274,6 +305,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
   pdl_trigger();
   extern __shared__ double sm[];
   stage_pose_w2c<S>(pose, intr, Dp, sm);
+  if constexpr (kAdjointFusion && Traits<S>::kOrder == 1) stage_jacobian<NDP>(sm);
   const long long n = static_cast<long long>(vol.nx) * vol.ny * vol.nz;
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < n;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -305,6 +337,7 @@ __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView
   pdl_trigger();
   extern __shared__ double sm[];
   stage_pose_w2c<S>(pose, intr, Dp, sm);
+  if constexpr (kAdjointFusion && Traits<S>::kOrder == 1) stage_jacobian<NDP>(sm);
   const int n_vis = counters[0];
   for (int vb = blockIdx.x; vb < n_vis; vb += gridDim.x) {
     const int b = visible[vb];
@@ -1788,7 +1821,7 @@ void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, c
                             const double* pose, const double* intr, int* upd) {
   G = integrate_group(G, Dp);
   const DenseView view = dense_view(v, Dp);
-  const size_t smem = sizeof(double) * 19 * (1 + Dp);
+  const size_t smem = integrate_smem(Dp);
   const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
   const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, sm_count() * 16LL));
   if (v.order == 2)
@@ -1807,7 +1840,7 @@ void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, c
                              const double* depth, int w, int h, const double* pose, const double* intr, int* upd) {
   G = integrate_group(G, Dp);
   const HashView view = hash_view(v, Dp);
-  const size_t smem = sizeof(double) * 19 * (1 + Dp);
+  const size_t smem = integrate_smem(Dp);
   const int grid = sm_count() * 8;
   if (v.order == 2)
     launch_pdl(k_integrate_hashed<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, v.coords, a.visible,
