@@ -215,13 +215,16 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
 #pragma unroll
     for (int k = 0; k < 19; ++k) g[k] = 0.0;
     if (!sat) {
-      const double eb = 1.0 / mu;
-      const double sb = eb, distb = -eb / lam, lamb = eb * dist / (lam * lam);
-      const double Sb = lamb * (0.5 / lam);
+      // derivative-only quantities: reciprocals instead of divisions (the
+      // real chain above keeps every division)
+      const double eb = 1.0 / mu, ilam = 1.0 / lam;
+      const double sb = eb, distb = -eb * ilam, lamb = eb * dist * (ilam * ilam);
+      const double Sb = lamb * (0.5 * ilam);
       const double rxb = 2.0 * rx * Sb, ryb = 2.0 * ry * Sb;
-      double lxb = rxb / kfx, lyb = ryb / kfy;
-      double cxb = -rxb / kfx, cyb = -ryb / kfy;
-      double fxb = -rxb * rx / kfx, fyb = -ryb * ry / kfy;
+      const double ikfx = 1.0 / kfx, ikfy = 1.0 / kfy;
+      double lxb = rxb * ikfx, lyb = ryb * ikfy;
+      double cxb = -lxb, cyb = -lyb;
+      double fxb = -lxb * rx, fyb = -lyb * ry;
       const double topb = sb * (1.0 - fyf), botb = sb * fyf, fyfb = sb * (bot - top);
       const double fxfb = topb * (d10 - d00) + botb * (d11 - d01);
       lxb += fxfb;
