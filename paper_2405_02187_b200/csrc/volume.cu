@@ -123,12 +123,13 @@ constexpr bool kAdjointFusion = false;
 constexpr bool kAdjointFusion = true;
 #endif
 
-// Warp-aggregated count of fused voxels (bench's algorithmic-byte model).
-CSF_DEV void count_updates(int* upd, bool fused) {
+// Count of fused voxels (bench's algorithmic-byte model): per-thread in a
+// register, one warp-reduced atomic per warp at kernel end (a per-voxel-warp
+// atomic on one address serialises ~3.4e5 atomics per frame in one L2 slice).
+CSF_DEV void flush_updates(int* upd, int count) {
   if (!upd) return;
-  const unsigned m = __activemask();
-  const unsigned b = __ballot_sync(m, fused);
-  if ((threadIdx.x & 31) == __ffs(m) - 1 && b) atomicAdd(upd, __popc(b));
+  const int total = __reduce_add_sync(0xffffffffu, count);
+  if ((threadIdx.x & 31) == 0 && total) atomicAdd(upd, total);
 }
 
 // Fusion with adjoint-form channels.  The real channel is the reference's
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
   stage_pose_w2c<S>(pose, intr, Dp, sm);
   if constexpr (kAdjointFusion && Traits<S>::kOrder == 1) stage_jacobian<NDP>(sm);
   const long long n = static_cast<long long>(vol.nx) * vol.ny * vol.nz;
+  int fused = 0;
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < n;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int i = static_cast<int>(v % vol.nx);
@@ -319,10 +321,11 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     const double py = vol.oy + vol.vs * static_cast<double>(j);
     const double pz = vol.oz + vol.vs * static_cast<double>(k);
     if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
-      count_updates(upd, fuse_voxel_adjoint<NDP>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+      fused += fuse_voxel_adjoint<NDP>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
     else
-      count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+      fused += fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
   }
+  flush_updates(upd, fused);
 }
 
 // resident CTAs per SM the fusion kernel is compiled for (register budget)
@@ -342,6 +345,7 @@ __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView
   stage_pose_w2c<S>(pose, intr, Dp, sm);
   if constexpr (kAdjointFusion && Traits<S>::kOrder == 1) stage_jacobian<NDP>(sm);
   const int n_vis = counters[0];
+  int fused = 0;
   for (int vb = blockIdx.x; vb < n_vis; vb += gridDim.x) {
     const int b = visible[vb];
     if (b < 0) continue;
@@ -353,11 +357,12 @@ __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView
       const double pz = vol.oz + vol.vs * static_cast<double>(8 * bz + lz);
       const long long vv = static_cast<long long>(b) * kBlockVoxels + l;
       if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
-        count_updates(upd, fuse_voxel_adjoint<NDP>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+        fused += fuse_voxel_adjoint<NDP>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
       else
-        count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+        fused += fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
     }
   }
+  flush_updates(upd, fused);
 }
 
 __global__ void k_init_volume(double2* rw, double* fim, long long n, int Dp) {
