@@ -130,6 +130,24 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }  // function-local scratch is freed on every return path
   cudaError_t alloc(size_t count) {
     if (count <= n && p) return cudaSuccess;
     if (p) cudaFree(p);
@@ -173,6 +191,7 @@ struct csf_volume_s {
   // stage buffers for the single-call APIs
   DevBuf<double> s_depth, s_pose, s_intr, s_vre, s_nre, s_vim, s_nim;
   DevBuf<double2> s_hits;
+  DevBuf<double> s_terms;  // csf_view_scores per-pixel terms [views][C][P]
   // raycast alpha table (hashed volumes) for (tab_near, tab_far, tab_step)
   DevBuf<double> alpha_tab;
   DevBuf<unsigned> seg_first;  // segmented-march scratch
@@ -189,6 +208,7 @@ struct csf_volume_s {
     s_depth.release(); s_pose.release(); s_intr.release(); s_vre.release(); s_nre.release(); s_vim.release();
     s_nim.release();
     s_hits.release();
+    s_terms.release();
     alpha_tab.release();
     seg_first.release();
   }
@@ -1434,7 +1454,9 @@ extern "C" int csf_view_scores(csf_volume v, const double* poses, int n_views, c
   const int W = k->width, H = k->height;
   const size_t P = static_cast<size_t>(W) * H;
   constexpr int C = 7;
-  const int chunk = std::max(1, std::min(n_views, static_cast<int>((size_t(1) << 27) / (C * P))));
+  // views per pass: all of them while the terms fit 2 GB (one host sync per
+  // pass, for the sums)
+  const int chunk = std::max(1, std::min(n_views, static_cast<int>((size_t(1) << 28) / (C * P))));
   CUDA_TRY(ctx, v->s_vre.alloc(3 * P));
   CUDA_TRY(ctx, v->s_nre.alloc(3 * P));
   CUDA_TRY(ctx, v->s_vim.alloc(3 * P * 6));
@@ -1442,8 +1464,8 @@ extern "C" int csf_view_scores(csf_volume v, const double* poses, int n_views, c
   CUDA_TRY(ctx, v->s_hits.alloc(2 * P));
   CUDA_TRY(ctx, v->s_pose.alloc(12 * C + 12 * static_cast<size_t>(n_views)));
   CUDA_TRY(ctx, v->s_intr.alloc(4 * C + 4));
-  DevBuf<double> terms;
-  CUDA_TRY(ctx, terms.alloc(static_cast<size_t>(chunk) * C * P));
+  CUDA_TRY(ctx, v->s_terms.alloc(static_cast<size_t>(chunk) * C * P));
+  double* const terms = v->s_terms.p;
   double* d_pose = v->s_pose.p;
   double* d_views = v->s_pose.p + 12 * C;
   double* d_intr = v->s_intr.p;
@@ -1461,9 +1483,9 @@ extern "C" int csf_view_scores(csf_volume v, const double* poses, int n_views, c
       launch_view_seed(L, d_views + 12 * (v0 + j), d_k4, h, d_pose, d_intr);
       raycast_dev(v, d_pose, d_intr, W, H, rc, v->s_hits.p, v->s_vre.p, v->s_nre.p, v->s_vim.p, v->s_nim.p);
       PROF(ctx, kPMisc);
-      launch_view_terms(L, v->hash, v->s_vre.p, v->s_nre.p, v->s_vim.p, W, H, w0, beta, terms.p + j * C * P);
+      launch_view_terms(L, v->hash, v->s_vre.p, v->s_nre.p, v->s_vim.p, W, H, w0, beta, terms + j * C * P);
     }
-    const int rc2 = tree_sum_slots(ctx->stream, ctx->energy, terms.p, static_cast<int>(P), nv * C, out.data());
+    const int rc2 = tree_sum_slots(ctx->stream, ctx->energy, terms, static_cast<int>(P), nv * C, out.data());
     if (rc2 == 5) return fail(ctx, CSF_ENOMEM, "csf_view_scores: out of device memory");
     if (rc2) return fail(ctx, CSF_ECUDA, "csf_view_scores: CUDA error");
     for (int j = 0; j < nv; ++j) {
