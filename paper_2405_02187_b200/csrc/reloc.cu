@@ -188,9 +188,9 @@ __global__ void __launch_bounds__(256) k_reloc_terms(const double* __restrict__ 
       for (int g = 0; g < G; ++g) terms[static_cast<long long>(1 + G * grp + g) * n + i] = t.im[g];
     }
   }
-  if (grp == 0) {
-    const unsigned b = __ballot_sync(0xffffffffu, ok);
-    if ((threadIdx.x & 31) == 0 && b) atomicAdd(overlap, static_cast<unsigned long long>(__popc(b)));
+  if (grp == 0) {  // one atomic per block (per-warp atomics on one address serialise in L2)
+    const int cnt = __syncthreads_count(ok);
+    if (threadIdx.x == 0 && cnt) atomicAdd(overlap, static_cast<unsigned long long>(cnt));
   }
 }
 
