@@ -23,9 +23,8 @@
 
 namespace orc {
 
-constexpr int kTile = 264;  // slot-grid tiles: device icp.cu kTile (291 tiles per VGA level)
+constexpr int kTile = 256;
 constexpr int kGroup = 16;
-constexpr int kListTile = 256;  // correspondence-list tiles: csf_linearized_step (energy.cu k_lin_tiles)
 
 // icp.hpp:27-31
 struct Correspondence {
@@ -172,14 +171,14 @@ inline NormalEq<double> normal_equations(const std::vector<Correspondence>& corr
                                          bool sequential) {
   NormalEq<double> total;
   NormalEq<double> tile, group;
-  const std::size_t n_tiles = (corrs.size() + kListTile - 1) / kListTile;
+  const std::size_t n_tiles = (corrs.size() + kTile - 1) / kTile;
   for (std::size_t i = 0; i < corrs.size(); ++i) {
     double j[6], r;
     const Correspondence& c = corrs[i];
     jacobian_row<double>(c.vertex, c.model_vertex, c.model_normal, base, j, &r);
     accumulate_row(sequential ? total : tile, j, r);
-    if (!sequential && ((i + 1) % kListTile == 0 || i + 1 == corrs.size())) {
-      const std::size_t t = i / kListTile;
+    if (!sequential && ((i + 1) % kTile == 0 || i + 1 == corrs.size())) {
+      const std::size_t t = i / kTile;
       add_into(group, tile);
       tile = NormalEq<double>();
       if ((t + 1) % kGroup == 0 || t + 1 == n_tiles) {

@@ -26,11 +26,7 @@
 namespace csfd {
 
 using csfi::TrackState;
-// Slots per tile (the canonical order, oracle/orc_icp.hpp kTile).  264, not
-// 256: a VGA-level slot grid (76800 slots) then cuts into 291 tiles — two
-// full waves at one reduce CTA per SM on 148 SMs — where 256 gave 300 tiles
-// and a third wave of 4 CTAs (~1.5x the level's reduce time).
-constexpr int kTile = 264;
+constexpr int kTile = 256;
 
 // Optional phase timing (tools/icp_timing.py): per launch, per CTA
 // [start, after association/J, after sums, solve start, solve end] in ns.
@@ -49,8 +45,8 @@ CSF_DEV void clock_mark(int slot, int cta = -1) {
 // the solve kernel records into CTA slot 511 of the iteration's record
 constexpr int kSolveClockCta = 511;
 
-// kTile threads evaluate the tile's slots; all 320 sum accumulators
-// (27*(1+Dp) of them, one per thread up to Dp = 10), so no thread carries two.
+// 256 threads evaluate the tile's slots; all 320 sum accumulators (27*(1+Dp)
+// of them, one per thread up to Dp = 10), so no thread carries two.
 constexpr int kRedThreads = 320;
 __constant__ int c_tri_r[21] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5, 5, 5, 5};
 __constant__ int c_tri_c[21] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2, 3, 4, 5};
@@ -408,7 +404,7 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
     const int slot = blockIdx.x * kTile + cbase + threadIdx.x;
     bool corr = false;
     int x = 0, y = 0, u = 0, v = 0;
-    if (threadIdx.x < chunk && cbase + static_cast<int>(threadIdx.x) < kTile && slot < n_slots) {
+    if (threadIdx.x < chunk && slot < n_slots) {
       x = (slot % nxs) * stride;
       y = (slot / nxs) * stride;
       corr = associate_slot(depth, w, h, x, y, fx, fy, cx, cy, c2w, w2p, vre, nre, d_max, cos_max, &u, &v);
@@ -652,11 +648,10 @@ __global__ void k_objective(const double* __restrict__ traj, const double* __res
 //                  the real step to `stage`
 //   k_icp_commit   real pose + break decisions (TrackState)
 // ============================================================================
-constexpr int kTile2 = kTile;
-constexpr int kRed2Threads = (kTile2 + 31) / 32 * 32;
+constexpr int kTile2 = 256;
 
 template <typename S>
-__global__ void __launch_bounds__(kRed2Threads) k_icp_reduce2(const TrackState* st, const double* __restrict__ depth, int w,
+__global__ void __launch_bounds__(256) k_icp_reduce2(const TrackState* st, const double* __restrict__ depth, int w,
                                                      int h, int stride, const double* __restrict__ intr,
                                                      const double* __restrict__ pose, const double* __restrict__ vre,
                                                      const double* __restrict__ nre, const double* __restrict__ vim,
@@ -671,7 +666,7 @@ __global__ void __launch_bounds__(kRed2Threads) k_icp_reduce2(const TrackState* 
   const int g0 = blockIdx.y * G;
   extern __shared__ double sm[];
   S* rows = reinterpret_cast<S*>(sm);  // [kTile2][7]
-  __shared__ int s_wsum[kRed2Threads / 32];
+  __shared__ int s_wsum[8];
   Pose<double> c2w, w2p;
   load_pose_real(pose, C, &c2w);
 #pragma unroll
@@ -685,7 +680,7 @@ __global__ void __launch_bounds__(kRed2Threads) k_icp_reduce2(const TrackState* 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = 0, y = 0, u = 0, v = 0;
   bool corr = false;
-  if (static_cast<int>(threadIdx.x) < kTile2 && slot < n_slots) {
+  if (slot < n_slots) {
     x = (slot % nxs) * stride;
     y = (slot / nxs) * stride;
     corr = associate_slot(depth, w, h, x, y, fx, fy, cx, cy, c2w, w2p, vre, nre, d_max, cos_max, &u, &v);
@@ -695,7 +690,7 @@ __global__ void __launch_bounds__(kRed2Threads) k_icp_reduce2(const TrackState* 
   __syncthreads();
   int before = 0, total = 0;
 #pragma unroll
-  for (int k = 0; k < kRed2Threads / 32; ++k) {
+  for (int k = 0; k < 8; ++k) {
     if (k < warp) before += s_wsum[k];
     total += s_wsum[k];
   }
@@ -974,8 +969,9 @@ int icp_tiles(int w, int h, int stride) {
 // (one pass over the tile's 256 slots whenever the rows fit: measured faster
 // than two half-tile passes at two CTAs per SM, bench r01)
 static int reduce_chunk(int C) {
-  for (int chunk = kTile; chunk > 32; chunk = (chunk + 1) / 2)
-    if (8 * C * (16 + chunk * 7) <= 200 * 1024) return chunk;
+  if (8 * C * (16 + 256 * 7) <= 200 * 1024) return 256;
+  if (8 * C * (16 + 128 * 7) <= 200 * 1024) return 128;
+  if (8 * C * (16 + 64 * 7) <= 200 * 1024) return 64;
   return 32;
 }
 
@@ -1115,7 +1111,7 @@ void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double
     cudaFuncSetAttribute(k_icp_reduce2<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  launch_pdl(k_icp_reduce2<S>, dim3(dim3(tiles, pairs)), dim3(kRed2Threads), smem, L.stream, st, depth, w, h, stride, intr, pose, vre, nre, vim,
+  launch_pdl(k_icp_reduce2<S>, dim3(dim3(tiles, pairs)), dim3(kTile2), smem, L.stream, st, depth, w, h, stride, intr, pose, vre, nre, vim,
                                                                    nim, d_max, cos_max, Dp, partials, counts);
   launch_pdl(k_icp_solve2<S>, dim3(pairs), dim3(128), 0, L.stream, st, partials, counts, tiles, pose, Dp, stage);
   launch_pdl(k_icp_commit, dim3(1), dim3(1), 0, L.stream, st, pose, Dp, stage, level, tol);

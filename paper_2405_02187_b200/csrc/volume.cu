@@ -65,7 +65,11 @@ CSF_DEV void stage_jacobian(double* sm) {
     __syncthreads();
   }
 }
-static size_t integrate_smem(int Dp) { return sizeof(double) * (jac_offset(1 + Dp) + 19 * Dp); }
+// staged inputs, plus the aligned channel block when the kernel restages it
+// (first order, fixed even channel count)
+static size_t integrate_smem(int Dp, bool jac) {
+  return sizeof(double) * (jac ? jac_offset(1 + Dp) + 19 * Dp : 19 * (1 + Dp));
+}
 
 template <typename S>
 __device__ void load_pose_intr(const double* sm, int Dp, int g0, Pose<S>* w2c, V3<S>* center, Intr<S>* k) {
@@ -126,6 +130,15 @@ constexpr bool kAdjointFusion = true;
 // Count of fused voxels (bench's algorithmic-byte model): per-thread in a
 // register, one warp-reduced atomic per warp at kernel end (a per-voxel-warp
 // atomic on one address serialises ~3.4e5 atomics per frame in one L2 slice).
+// (The generic lifted fusion keeps the in-loop warp-aggregated atomic: an
+// extra live counter across its loop raised the order-2 kernel's spills from
+// 124 to 332 bytes.)
+CSF_DEV void count_updates(int* upd, bool fused) {
+  if (!upd) return;
+  const unsigned m = __activemask();
+  const unsigned b = __ballot_sync(m, fused);
+  if ((threadIdx.x & 31) == __ffs(m) - 1 && b) atomicAdd(upd, __popc(b));
+}
 CSF_DEV void flush_updates(int* upd, int count) {
   if (!upd) return;
   const int total = __reduce_add_sync(0xffffffffu, count);
@@ -323,7 +336,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
       fused += fuse_voxel_adjoint<NDP>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
     else
-      fused += fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
+      count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
   }
   flush_updates(upd, fused);
 }
@@ -359,7 +372,7 @@ __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView
       if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
         fused += fuse_voxel_adjoint<NDP>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
       else
-        fused += fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
+        count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
     }
   }
   flush_updates(upd, fused);
@@ -1829,7 +1842,7 @@ void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, c
                             const double* pose, const double* intr, int* upd) {
   G = integrate_group(G, Dp);
   const DenseView view = dense_view(v, Dp);
-  const size_t smem = integrate_smem(Dp);
+  const size_t smem = integrate_smem(Dp, v.order != 2 && Dp % 2 == 0 && Dp <= 24);
   const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
   const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, sm_count() * 16LL));
   if (v.order == 2)
@@ -1848,7 +1861,7 @@ void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, c
                              const double* depth, int w, int h, const double* pose, const double* intr, int* upd) {
   G = integrate_group(G, Dp);
   const HashView view = hash_view(v, Dp);
-  const size_t smem = integrate_smem(Dp);
+  const size_t smem = integrate_smem(Dp, v.order != 2 && Dp % 2 == 0 && Dp <= 24);
   const int grid = sm_count() * 8;
   if (v.order == 2)
     launch_pdl(k_integrate_hashed<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, v.coords, a.visible,

@@ -143,3 +143,26 @@ def test_pipeline_hessian_properties(gpu_ctx, orc):
     g = dict(zip([0, 6, 1, 7, 3], pipe.result().gradient))
     for p, (i, j) in enumerate(pairs):
         assert close(r.grad1[p], g[i], scale=1e-12)[0] and close(r.grad2[p], g[j], scale=1e-12)[0]
+
+
+@pytest.mark.gpu
+def test_pipeline_hessian_all_pairs_launches(gpu_ctx, orc):
+    """BASELINE config 3's width — all 55 pairs of the 10 directions (165
+    bicomplex slots) — on a small hashed run: every kernel launches at that
+    channel count (an integrate launch once failed there on the 48 KB
+    shared-memory threshold), the real channel matches the first-order run
+    bit for bit and mirrored pairs agree."""
+    n = 3
+    d, gt, k = orc.workload(2, n, 160, 120)
+    pairs = [(i, j) for i in range(10) for j in range(i, 10)]
+    r = _device(gpu_ctx, cfg_hashed(k, n, pairs=pairs), d, gt)
+    p1 = csf.Pipeline(cfg_hashed(k, n, dirs=list(range(10))), ctx=gpu_ctx)
+    p1.upload(d, gt)
+    p1.run()
+    first = p1.result()
+    assert r.objective == first.objective
+    assert np.array_equal(r.poses[..., 0], first.poses[..., 0])
+    assert np.all(np.isfinite(r.hessian)) and np.abs(r.hessian).max() > 0
+    for p, (i, j) in enumerate(pairs):
+        s = max(abs(first.gradient[i]), abs(first.gradient[j]), 1e-12)
+        assert abs(r.grad1[p] - first.gradient[i]) <= 1e-9 * s and abs(r.grad2[p] - first.gradient[j]) <= 1e-9 * s
