@@ -85,3 +85,22 @@ def test_argument_validation(gpu_ctx):
         csf.lift_pose(np.zeros(7))
     with pytest.raises(csf.InvalidArgument):
         csf.perturb_depth(np.ones((4, 4)), 1, 1, h=1e-3)
+
+
+def test_run_host_rejects_more_frames_than_configured(gpu_ctx, oracle_built):
+    """csf_pipeline_run_host validates the frame count against max_frames
+    before any upload (std::invalid_argument at the boundary), and the
+    pipeline stays usable afterwards."""
+    from oracle import orc
+    n = 3
+    d, gt, k = orc.workload(2, n + 1, 160, 120)
+    hp = capi.HashParams(0.02, (capi.C.c_double * 3)(0.0, 0.0, 0.0), 0.1, 128.0, 16, 1 << 14)
+    cfg = csf.make_pipeline_cfg(hashed=True, k=k, dirs=[0, 1], h=1e-8, objective=1, max_frames=n, hash_params=hp)
+    pipe = csf.Pipeline(cfg, ctx=gpu_ctx)
+    with pytest.raises(csf.InvalidArgument):
+        pipe.run_host(d, gt)
+    r = pipe.run_host(d[:n], gt[:n])
+    pipe.upload(d[:n], gt[:n])
+    pipe.run()
+    s = pipe.result()
+    assert r.objective == s.objective and np.array_equal(r.gradient, s.gradient)

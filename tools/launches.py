@@ -16,7 +16,7 @@ for r in rows[hi + 1:]:
     name = name.replace("void ", "")
     v = float(r[vi].replace(",", ""))
     u = r[ui]
-    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u, 1.0)
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}[u]
     agg[name][0] += 1
     agg[name][1] += v
 tot = sum(v[1] for v in agg.values())
