@@ -92,11 +92,20 @@ def parse():
     return ap.parse_args()
 
 
-def pipeline_cfg4(csf, capi, k, dirs, n_frames):
+def pipeline_cfg1(csf, capi, k, dirs, n_frames):
+    """BASELINE config 1: dense 128^3 at 2 cm (origin keeps the 4x4x3 m room
+    inside), mu = 6 cm, h = 1e-20, final-translation-error objective."""
+    import ctypes as C
+    dense = capi.VolumeParams((C.c_int * 3)(128, 128, 128), 0.02, (C.c_double * 3)(-2.1, -1.28, -0.1), 0.06, 128.0)
+    return csf.make_pipeline_cfg(hashed=False, k=k, dirs=dirs, h=1e-20,
+                                 objective=capi.OBJECTIVE_FINAL_TRANSLATION_ERROR, max_frames=n_frames, dense=dense)
+
+
+def pipeline_cfg4(csf, capi, k, dirs, n_frames, keyframe_interval=50):
     import ctypes as C
     hp = capi.HashParams(0.02, (C.c_double * 3)(0.0, 0.0, 0.0), 5 * 0.02, 128.0, 20, 1 << 21)
     return csf.make_pipeline_cfg(hashed=True, k=k, dirs=dirs, h=1e-8, objective=capi.OBJECTIVE_TRAJECTORY_ERROR,
-                                 max_frames=n_frames, hash_params=hp, keyframe_interval=50)
+                                 max_frames=n_frames, hash_params=hp, keyframe_interval=keyframe_interval)
 
 
 def pipeline_cfg(csf, capi, k, dirs, n_frames, pairs=None):

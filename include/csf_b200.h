@@ -424,6 +424,11 @@ int csf_pipeline_result(csf_pipeline p, double* gradient, double* objective, dou
  * (optional) [n][12][1 + 3 n_pairs] (re, then im1, im2, im12 per pair). */
 int csf_pipeline_hessian(csf_pipeline p, double* hessian, double* grad1, double* grad2, double* objective,
                          double* poses, int32_t* stats);
+/* The pipeline's volume after the last run, borrowed (owned by the pipeline:
+ * never pass it to csf_volume_destroy).  Read it with csf_volume_download /
+ * csf_volume_download_hash / csf_volume_block_count; it carries the run's
+ * channel slots (n_dirs, or 3 n_pairs at order 2). */
+int csf_pipeline_volume(csf_pipeline p, csf_volume* out);
 /* One end-to-end call from host buffers: upload, run, read back. */
 int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames, double* gradient,
                           double* objective);

@@ -46,6 +46,8 @@ def lib() -> C.CDLL:
                                             dp, C.POINTER(_capi.TrackResult), dp, ip, C.POINTER(C.c_int)]),
             "orc_workload": (ip, [ip, ip, ip, ip, fp, dp, C.POINTER(_capi.Intrinsics)]),
             "orc_pipeline_run": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, i32p, dp]),
+            "orc_pipeline_run_keep": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, i32p,
+                                           C.POINTER(vp)]),
             "orc_associate": (ip, [dp, dp, dp, dp, ip, ip, dp, dp, C.POINTER(_capi.Intrinsics), C.POINTER(_capi.IcpCfg),
                                    ip, dp, C.POINTER(C.c_int)]),
             "orc_linearized_step": (ip, [dp, ip, dp, ip, dp]),
@@ -121,12 +123,14 @@ def measure_surface(depth_lifted, intr_lifted):
 
 
 class Volume:
-    def __init__(self, params, channels: int, hashed: bool):
+    def __init__(self, params, channels: int, hashed: bool, handle=None):
         self.h = C.c_void_p()
         self.channels = channels
         self.hashed = hashed
         self.params = params
-        if hashed:
+        if handle is not None:  # adopt an oracle volume handle (orc_pipeline_run_keep)
+            self.h = handle
+        elif hashed:
             _check(lib().orc_volume_create_hashed(C.byref(params), channels, C.byref(self.h)))
         else:
             _check(lib().orc_volume_create_dense(C.byref(params), channels, C.byref(self.h)))
@@ -250,6 +254,24 @@ def pipeline_run(cfg, depth, gt):
                                   C.byref(obj), _dp(poses), stats.ctypes.data_as(C.POINTER(C.c_int32)),
                                   C.byref(secs)))
     return grad, obj.value, poses, stats, secs.value
+
+
+def pipeline_run_keep(cfg, depth, gt):
+    """pipeline_run that also returns the run's final volume (a Volume)."""
+    d = np.ascontiguousarray(depth, dtype=np.float32)
+    g = np.ascontiguousarray(gt, dtype=np.float64).reshape(-1, 12)
+    n = d.shape[0]
+    D = cfg.n_dirs
+    grad = np.empty(D)
+    obj = C.c_double()
+    poses = np.empty((n, 12, 1 + D))
+    stats = np.empty((n, 8), dtype=np.int32)
+    h = C.c_void_p()
+    _check(lib().orc_pipeline_run_keep(C.byref(cfg), d.ctypes.data_as(C.POINTER(C.c_float)), _dp(g), n, _dp(grad),
+                                       C.byref(obj), _dp(poses), stats.ctypes.data_as(C.POINTER(C.c_int32)),
+                                       C.byref(h)))
+    vol = Volume(cfg.hash if cfg.hashed else cfg.dense, D, bool(cfg.hashed), handle=h)
+    return grad, obj.value, poses, stats, vol
 
 
 def pipeline_hessian(cfg, depth, gt):

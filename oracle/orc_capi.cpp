@@ -439,15 +439,19 @@ void to_frames(const PipelineConfig& cfg, const float* depth, const double* gt_i
     gt->push_back(p);
   }
 }
-void write_stats(int n_frames, const std::vector<int>& it, const std::vector<int>& corr, const std::vector<int>& blocks,
-                 const std::vector<int>& vis, int32_t* stats) {
+// The device's per-frame stats row (csf_b200.h csf_pipeline_result):
+// iterations, correspondences, converged, blocks, visible, new blocks, fused voxels, 0.
+template <typename R>
+void write_stats(int n_frames, const R& r, int32_t* stats) {
   for (int f = 0; f < n_frames; ++f) {
-    stats[8 * f] = it[f];
-    stats[8 * f + 1] = corr[f];
-    stats[8 * f + 2] = 0;
-    stats[8 * f + 3] = blocks[f];
-    stats[8 * f + 4] = vis[f];
-    for (int j = 5; j < 8; ++j) stats[8 * f + j] = 0;
+    stats[8 * f] = r.iterations[f];
+    stats[8 * f + 1] = r.correspondences[f];
+    stats[8 * f + 2] = r.converged[f];
+    stats[8 * f + 3] = r.blocks[f];
+    stats[8 * f + 4] = r.visible[f];
+    stats[8 * f + 5] = r.fresh[f];
+    stats[8 * f + 6] = r.fused[f];
+    stats[8 * f + 7] = 0;
   }
 }
 
@@ -871,7 +875,50 @@ int orc_pipeline_hessian(const csf_pipeline_cfg* c, const float* depth, const do
       if (grad2) grad2[p] = r.grad2[p];
     }
     if (poses) std::memcpy(poses, r.poses.data(), sizeof(double) * r.poses.size());
-    if (stats) write_stats(n_frames, r.iterations, r.correspondences, r.blocks, r.visible, stats);
+    if (stats) write_stats(n_frames, r, stats);
+  });
+}
+
+// orc_pipeline_run that also hands back the run's final volume (an orc
+// volume handle: orc_volume_download / orc_volume_hash / orc_volume_destroy).
+int orc_pipeline_run_keep(const csf_pipeline_cfg* c, const float* depth, const double* gt_in, int n_frames,
+                          double* gradient, double* objective, double* poses, int32_t* stats, void** vol_out) {
+  return guard([&] {
+    const PipelineConfig cfg = to_pipeline(c);
+    std::vector<Image<double>> frames;
+    std::vector<Pose> gt;
+    to_frames(cfg, depth, gt_in, n_frames, &frames, &gt);
+    PipelineResult r;
+    VolBase* keep = nullptr;
+    auto run = [&](auto dtag) {
+      constexpr int D = decltype(dtag)::value;
+      if (cfg.hashed) {
+        auto* v = new Vol<D, true>(cfg.hash);
+        keep = v;
+        r = run_pipeline_on<D>(v->vol, cfg, frames, gt);
+      } else {
+        auto* v = new Vol<D, false>(cfg.dense);
+        keep = v;
+        r = run_pipeline_on<D>(v->vol, cfg, frames, gt);
+      }
+    };
+    switch (cfg.directions.size()) {
+      case 1: run(std::integral_constant<int, 1>{}); break;
+      case 2: run(std::integral_constant<int, 2>{}); break;
+      case 3: run(std::integral_constant<int, 3>{}); break;
+      case 4: run(std::integral_constant<int, 4>{}); break;
+      case 5: run(std::integral_constant<int, 5>{}); break;
+      case 6: run(std::integral_constant<int, 6>{}); break;
+      case 8: run(std::integral_constant<int, 8>{}); break;
+      case 10: run(std::integral_constant<int, 10>{}); break;
+      default: throw std::invalid_argument("orc_pipeline_run_keep: unsupported direction count");
+    }
+    if (objective) *objective = r.objective;
+    if (gradient)
+      for (int d = 0; d < c->n_dirs; ++d) gradient[d] = r.gradient[d];
+    if (poses) std::memcpy(poses, r.poses.data(), sizeof(double) * r.poses.size());
+    if (stats) write_stats(n_frames, r, stats);
+    *vol_out = keep;
   });
 }
 
@@ -890,7 +937,7 @@ int orc_pipeline_run(const csf_pipeline_cfg* c, const float* depth, const double
     if (gradient)
       for (int d = 0; d < c->n_dirs; ++d) gradient[d] = r.gradient[d];
     if (poses) std::memcpy(poses, r.poses.data(), sizeof(double) * r.poses.size());
-    if (stats) write_stats(n_frames, r.iterations, r.correspondences, r.blocks, r.visible, stats);
+    if (stats) write_stats(n_frames, r, stats);
   });
 }
 

@@ -114,6 +114,9 @@ struct PipelineResult {
   std::vector<int> correspondences;    // [N]
   std::vector<int> blocks;             // [N] allocated blocks after frame (hashed)
   std::vector<int> visible;            // [N] visible blocks of frame (hashed)
+  std::vector<int> converged;          // [N] track_frame converged at level 0
+  std::vector<int> fresh;              // [N] blocks newly allocated by the frame (hashed)
+  std::vector<int> fused;              // [N] voxels fused by the frame
 };
 
 template <int D>
@@ -133,7 +136,7 @@ template <typename S>
 struct LiftedRun {
   std::vector<PoseT<S>> poses;
   S objective = S(0.0);
-  std::vector<int> iterations, correspondences, blocks, visible;
+  std::vector<int> iterations, correspondences, blocks, visible, converged, fresh, fused;
 };
 
 // Keyframe perturbation seeds of keyframe kf (first order only): exp(xi) *
@@ -161,16 +164,20 @@ LiftedRun<S> run_lifted(V& vol, const PipelineConfig& cfg, const std::vector<Ima
   res.correspondences.assign(n, 0);
   res.blocks.assign(n, 0);
   res.visible.assign(n, 0);
+  res.converged.assign(n, 0);
+  res.fresh.assign(n, 0);
+  res.fused.assign(n, 0);
   const Intrinsics kr = cfg.k;
   auto integrate = [&](int f) {
     if constexpr (V::kHashed) {
       AllocStats st;
       const std::vector<int> visible = allocate_band(vol, frames[f], kr, real_pose(res.poses[f]), &st);
-      surface_update_blocks(vol, visible, frames[f], res.poses[f], ks);
+      res.fused[f] = static_cast<int>(surface_update_blocks(vol, visible, frames[f], res.poses[f], ks));
       res.blocks[f] = vol.n_blocks();
       res.visible[f] = st.touched;
+      res.fresh[f] = st.fresh;
     } else {
-      surface_update(vol, frames[f], res.poses[f], ks);
+      res.fused[f] = static_cast<int>(surface_update(vol, frames[f], res.poses[f], ks));
     }
   };
   res.poses[0] = exp_map(xi) * pose_cast<S>(gt[0]);
@@ -180,6 +187,7 @@ LiftedRun<S> run_lifted(V& vol, const PipelineConfig& cfg, const std::vector<Ima
     res.poses[f] = tr.pose;
     res.iterations[f] = tr.iterations;
     res.correspondences[f] = tr.correspondences;
+    res.converged[f] = tr.converged ? 1 : 0;
     if constexpr (!std::is_same_v<S, Bicomplex>) {
       if (cfg.keyframe_interval > 0 && f % cfg.keyframe_interval == 0)
         res.poses[f] = exp_map(keyframe_xi<S>(cfg, f / cfg.keyframe_interval)) * res.poses[f];
@@ -240,6 +248,9 @@ PipelineResult run_pipeline_on(V& vol, const PipelineConfig& cfg, const std::vec
   res.correspondences = run.correspondences;
   res.blocks = run.blocks;
   res.visible = run.visible;
+  res.converged = run.converged;
+  res.fresh = run.fresh;
+  res.fused = run.fused;
   res.objective = run.objective.re;
   res.gradient.resize(D);
   for (int d = 0; d < D; ++d) res.gradient[d] = run.objective.im[d] / cfg.h;
@@ -260,7 +271,7 @@ struct HessianResult {
   std::vector<double> grad2;     // [P]  d obj / d param j_p
   double objective = 0.0;
   std::vector<double> poses;     // [N][12][1 + 3P]: re, then (im1, im2, im12) per pair
-  std::vector<int> iterations, correspondences, blocks, visible;
+  std::vector<int> iterations, correspondences, blocks, visible, converged, fresh, fused;
 };
 
 template <typename V>
@@ -304,6 +315,9 @@ inline HessianResult run_pipeline_hessian(const PipelineConfig& cfg, const std::
       res.correspondences = run.correspondences;
       res.blocks = run.blocks;
       res.visible = run.visible;
+      res.converged = run.converged;
+      res.fresh = run.fresh;
+      res.fused = run.fused;
     }
     for (int f = 0; f < n; ++f)
       for (int e = 0; e < 12; ++e) {

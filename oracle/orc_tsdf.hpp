@@ -202,15 +202,17 @@ std::optional<S> measured_tsdf(const Image<DS>& depth, const PoseT<S>& world_to_
 }
 
 // tsdf.cpp:11-40 — dense fusion over every voxel (OpenMP over z slices).
+// Returns the number of voxels fused (the device's stats column 6).
 template <typename F, typename DS, typename K>
-void surface_update(TsdfVolumeT<F>& volume, const Image<DS>& depth, const PoseT<F>& camera_to_world,
-                    const IntrinsicsT<K>& k) {
+long long surface_update(TsdfVolumeT<F>& volume, const Image<DS>& depth, const PoseT<F>& camera_to_world,
+                         const IntrinsicsT<K>& k) {
   const PoseT<F> world_to_camera = camera_to_world.inverse();
   const Vec3<F>& center = camera_to_world.translation;
   const VolumeParams& vp = volume.params;
   const double cap = vp.weight_cap;
   const int nx = vp.dims[0], ny = vp.dims[1], nz = vp.dims[2];
-#pragma omp parallel for schedule(static)
+  long long fused = 0;
+#pragma omp parallel for schedule(static) reduction(+ : fused)
   for (int kk = 0; kk < nz; ++kk)
     for (int jj = 0; jj < ny; ++jj)
       for (int ii = 0; ii < nx; ++ii) {
@@ -223,7 +225,9 @@ void surface_update(TsdfVolumeT<F>& volume, const Image<DS>& depth, const PoseT<
         F& f = volume.tsdf[idx];
         f = (F(w) * f + *sample) / F(w + 1.0);
         volume.weight[idx] = std::min(w + 1.0, cap);
+        ++fused;
       }
+  return fused;
 }
 
 // ---------------------------------------------------------------------------
@@ -308,12 +312,13 @@ std::vector<int> allocate_band(HashedVolumeT<F>& vol, const Image<double>& depth
 // Fusion over the visible blocks with the reference's per-voxel rule
 // (tsdf.cpp:25-37).
 template <typename F, typename DS, typename K>
-void surface_update_blocks(HashedVolumeT<F>& vol, const std::vector<int>& visible, const Image<DS>& depth,
-                           const PoseT<F>& camera_to_world, const IntrinsicsT<K>& k) {
+long long surface_update_blocks(HashedVolumeT<F>& vol, const std::vector<int>& visible, const Image<DS>& depth,
+                                const PoseT<F>& camera_to_world, const IntrinsicsT<K>& k) {
   const PoseT<F> world_to_camera = camera_to_world.inverse();
   const Vec3<F>& center = camera_to_world.translation;
   const double cap = vol.params.weight_cap, mu = vol.params.mu;
-#pragma omp parallel for schedule(static)
+  long long fused = 0;
+#pragma omp parallel for schedule(static) reduction(+ : fused)
   for (std::ptrdiff_t vb = 0; vb < static_cast<std::ptrdiff_t>(visible.size()); ++vb) {
     const int b = visible[vb];
     const int bx = vol.coords[3 * b], by = vol.coords[3 * b + 1], bz = vol.coords[3 * b + 2];
@@ -329,8 +334,10 @@ void surface_update_blocks(HashedVolumeT<F>& vol, const std::vector<int>& visibl
           F& f = vol.tsdf[idx];
           f = (F(w) * f + *sample) / F(w + 1.0);
           vol.weight[idx] = std::min(w + 1.0, cap);
+          ++fused;
         }
   }
+  return fused;
 }
 
 // ---------------------------------------------------------------------------

@@ -750,6 +750,21 @@ class Pipeline:
             S.ctypes.data_as(C.POINTER(C.c_int32)) if S is not None else None))
         return PipelineResult(g[: self.D].copy(), obj.value, P, S)
 
+    def volume(self) -> "_Volume":
+        """The pipeline's volume after the last run (csf_pipeline_volume):
+        borrowed from the pipeline, which it keeps alive; read-only use
+        (download, hash_tables, block_count, sample_*)."""
+        h = C.c_void_p()
+        self.ctx.check(self.ctx.lib.csf_pipeline_volume(self.h, C.byref(h)))
+        cls = HashedVolume if self.cfg.hashed else TsdfVolume
+        v = cls.__new__(cls)
+        _Volume.__init__(v, self.ctx, self.slots)
+        v.h = h
+        v.params = self.cfg.hash if self.cfg.hashed else self.cfg.dense
+        v._owner = self
+        v.close = lambda: None  # the pipeline owns the handle
+        return v
+
     def run_host(self, depth: np.ndarray, gt: np.ndarray) -> PipelineResult:
         """End-to-end call from host buffers (upload + run + read back)."""
         d = np.ascontiguousarray(depth, dtype=np.float32)

@@ -109,6 +109,14 @@ int fail(csf_ctx ctx, int code, const std::string& msg) {
 
 Launch launch_of(csf_ctx ctx) { return Launch{ctx->stream, ctx->d_err, &ctx->launches}; }
 
+// Device->host copy that is complete when it returns: host buffers are only
+// borrowed for the duration of a call (csf_b200.h), and a pinned destination
+// would otherwise still be in flight when the caller reads it.
+cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(s);
+}
+
 // Synchronise and translate the device error flag into a status code.
 int sync_check(csf_ctx ctx, const char* what) {
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -116,7 +124,7 @@ int sync_check(csf_ctx ctx, const char* what) {
   char lmsg[256];
   if (take_launch_error(lmsg, sizeof(lmsg))) return fail(ctx, CSF_ECUDA, std::string(what) + ": " + lmsg);
   int err = 0;
-  CUDA_TRY(ctx, cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(&err, ctx->d_err, sizeof(int), ctx->stream));
   if (err != 0) {
     cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream);
     if (err == 2) return fail(ctx, CSF_EDOMAIN, std::string(what) + ": division by a zero real part");
@@ -486,7 +494,7 @@ extern "C" int csf_bilateral_filter(csf_ctx ctx, const double* depth, int w, int
   CUDA_TRY(ctx, dout.alloc(P));
   CUDA_TRY(ctx, cudaMemcpyAsync(din.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
   launch_bilateral(launch_of(ctx), nullptr, din.p, nullptr, dout.p, w, h, sigma_s, sigma_r, radius);
-  CUDA_TRY(ctx, cudaMemcpyAsync(out, dout.p, sizeof(double) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(out, dout.p, sizeof(double) * P, ctx->stream));
   const int rc = sync_check(ctx, "csf_bilateral_filter");
   din.release();
   dout.release();
@@ -502,7 +510,7 @@ extern "C" int csf_downsample_depth(csf_ctx ctx, const double* depth, int w, int
   CUDA_TRY(ctx, dout.alloc(Po));
   CUDA_TRY(ctx, cudaMemcpyAsync(din.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
   launch_downsample(launch_of(ctx), din.p, dout.p, w, h, sigma_r);
-  CUDA_TRY(ctx, cudaMemcpyAsync(out, dout.p, sizeof(double) * Po, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(out, dout.p, sizeof(double) * Po, ctx->stream));
   const int rc = sync_check(ctx, "csf_downsample_depth");
   din.release();
   dout.release();
@@ -526,8 +534,8 @@ extern "C" int csf_measure_surface(csf_ctx ctx, const double* depth, int w, int 
   CUDA_TRY(ctx, cudaMemcpyAsync(dd.p, depth, sizeof(double) * P * C, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(dk.p, intr, sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
   launch_measure(launch_of(ctx), dd.p, w, h, dk.p, n_channels, dv.p, dn.p);
-  CUDA_TRY(ctx, cudaMemcpyAsync(vertices, dv.p, sizeof(double) * P * 3 * C, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(normals, dn.p, sizeof(double) * P * 3 * C, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(vertices, dv.p, sizeof(double) * P * 3 * C, ctx->stream));
+  CUDA_TRY(ctx, d2h(normals, dn.p, sizeof(double) * P * 3 * C, ctx->stream));
   const int rc = sync_check(ctx, "csf_measure_surface");
   dd.release(); dk.release(); dv.release(); dn.release();
   return rc;
@@ -664,7 +672,7 @@ extern "C" int csf_volume_block_count(csf_volume v, int* n) {
   }
   cudaSetDevice(v->ctx->device);
   CUDA_TRY(v->ctx, cudaStreamSynchronize(v->ctx->stream));
-  CUDA_TRY(v->ctx, cudaMemcpyAsync(n, v->hash.n_blocks, sizeof(int), cudaMemcpyDeviceToHost, v->ctx->stream));
+  CUDA_TRY(v->ctx, d2h(n, v->hash.n_blocks, sizeof(int), v->ctx->stream));
   return CSF_OK;
 }
 
@@ -700,8 +708,8 @@ extern "C" int csf_volume_download(csf_volume v, double* field, double* weight) 
   const long long n = volume_voxels_now(v);
   std::vector<double2> rw(n);
   std::vector<double> fim(static_cast<size_t>(n) * std::max(v->Dp, 1));
-  CUDA_TRY(ctx, cudaMemcpyAsync(rw.data(), v->rw.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (v->Dp > 0) CUDA_TRY(ctx, cudaMemcpyAsync(fim.data(), v->fim.p, sizeof(double) * n * v->Dp, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(rw.data(), v->rw.p, sizeof(double2) * n, ctx->stream));
+  if (v->Dp > 0) CUDA_TRY(ctx, d2h(fim.data(), v->fim.p, sizeof(double) * n * v->Dp, ctx->stream));
   const int C = 1 + v->D;
   for (long long i = 0; i < n; ++i) {
     field[i * C] = rw[i].x;
@@ -717,10 +725,10 @@ extern "C" int csf_volume_download_hash(csf_volume v, int32_t* heads, uint64_t* 
   int nb = 0;
   const int rc = csf_volume_block_count(v, &nb);
   if (rc) return rc;
-  if (heads) CUDA_TRY(ctx, cudaMemcpyAsync(heads, v->hash.heads, sizeof(int) << v->hash.bits, cudaMemcpyDeviceToHost, ctx->stream));
-  if (keys) CUDA_TRY(ctx, cudaMemcpyAsync(keys, v->hash.keys, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, ctx->stream));
-  if (next) CUDA_TRY(ctx, cudaMemcpyAsync(next, v->hash.next, sizeof(int) * nb, cudaMemcpyDeviceToHost, ctx->stream));
-  if (coords) CUDA_TRY(ctx, cudaMemcpyAsync(coords, v->hash.coords, sizeof(int) * 3 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+  if (heads) CUDA_TRY(ctx, d2h(heads, v->hash.heads, sizeof(int) << v->hash.bits, ctx->stream));
+  if (keys) CUDA_TRY(ctx, d2h(keys, v->hash.keys, sizeof(uint64_t) * nb, ctx->stream));
+  if (next) CUDA_TRY(ctx, d2h(next, v->hash.next, sizeof(int) * nb, ctx->stream));
+  if (coords) CUDA_TRY(ctx, d2h(coords, v->hash.coords, sizeof(int) * 3 * nb, ctx->stream));
   return CSF_OK;
 }
 
@@ -747,7 +755,7 @@ extern "C" int csf_surface_update(csf_volume v, const double* depth, int w, int 
   if (rc) return rc;
   if (n_visible) {
     *n_visible = 0;
-    if (v->hashed) CUDA_TRY(ctx, cudaMemcpyAsync(n_visible, v->alloc.counters, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (v->hashed) CUDA_TRY(ctx, d2h(n_visible, v->alloc.counters, sizeof(int), ctx->stream));
   }
   return CSF_OK;
 }
@@ -779,11 +787,11 @@ extern "C" int csf_raycast(csf_volume v, const double* pose, const double* intr,
   CUDA_TRY(ctx, cudaMemcpyAsync(v->s_intr.p, kp.data(), sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
   raycast_dev(v, v->s_pose.p, v->s_intr.p, w, h, rc, v->s_hits.p, v->s_vre.p, v->s_nre.p, v->s_vim.p, v->s_nim.p);
   std::vector<double> vre(P * 3), nre(P * 3), vim(P * 3 * std::max(v->Dp, 1)), nim(P * 3 * std::max(v->Dp, 1));
-  CUDA_TRY(ctx, cudaMemcpyAsync(vre.data(), v->s_vre.p, sizeof(double) * P * 3, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(nre.data(), v->s_nre.p, sizeof(double) * P * 3, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(vre.data(), v->s_vre.p, sizeof(double) * P * 3, ctx->stream));
+  CUDA_TRY(ctx, d2h(nre.data(), v->s_nre.p, sizeof(double) * P * 3, ctx->stream));
   if (v->Dp > 0) {
-    CUDA_TRY(ctx, cudaMemcpyAsync(vim.data(), v->s_vim.p, sizeof(double) * P * 3 * v->Dp, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaMemcpyAsync(nim.data(), v->s_nim.p, sizeof(double) * P * 3 * v->Dp, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, d2h(vim.data(), v->s_vim.p, sizeof(double) * P * 3 * v->Dp, ctx->stream));
+    CUDA_TRY(ctx, d2h(nim.data(), v->s_nim.p, sizeof(double) * P * 3 * v->Dp, ctx->stream));
   }
   const int r = sync_check(ctx, "csf_raycast");
   if (r) return r;
@@ -860,6 +868,8 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
     return fail(ctx, CSF_EINVAL, "csf_pipeline_create: the lifted tracker implements the linearized solver");
   if (cfg->icp.levels < 1 || cfg->icp.levels > 3 || cfg->max_frames <= 0 || cfg->k.width <= 0 || cfg->k.height <= 0)
     return fail(ctx, CSF_EINVAL, "csf_pipeline_create: bad levels/frames/size");
+  if (!icp_frame_fits(cfg->k.width, cfg->k.height, 1))
+    return fail(ctx, CSF_EINVAL, "csf_pipeline_create: frame too large for the ICP reduction");
   cudaSetDevice(ctx->device);
   csf_pipeline p = new csf_pipeline_s();
   p->ctx = ctx;
@@ -961,7 +971,7 @@ static int pipeline_reset_volume(csf_pipeline p) {
   const Launch L = launch_of(ctx);
   if (v->hashed) {
     int nb = 0;
-    CUDA_TRY(ctx, cudaMemcpyAsync(&nb, v->hash.n_blocks, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, d2h(&nb, v->hash.n_blocks, sizeof(int), ctx->stream));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     if (nb > 0) {
       CUDA_TRY(ctx, cudaMemsetAsync(v->hash.heads, 0xFF, sizeof(int) << v->hash.bits, ctx->stream));
@@ -1067,7 +1077,7 @@ extern "C" int csf_pipeline_result(csf_pipeline p, double* gradient, double* obj
   int rc = sync_check(ctx, "csf_pipeline_run");
   if (rc) return rc;
   std::vector<double> out(2 + std::max(CSF_MAX_DIRECTIONS, 3 * CSF_MAX_PAIRS));
-  CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(out.data(), p->out.p, sizeof(double) * out.size(), ctx->stream));
   if (objective) *objective = out[0];
   const double hh = p->cfg.h;
   if (gradient) {
@@ -1079,14 +1089,14 @@ extern "C" int csf_pipeline_result(csf_pipeline p, double* gradient, double* obj
   const int n = p->n_run;
   if (poses) {
     std::vector<double> t(static_cast<size_t>(n) * 12 * p->C);
-    CUDA_TRY(ctx, cudaMemcpyAsync(t.data(), p->traj.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, d2h(t.data(), p->traj.p, sizeof(double) * t.size(), ctx->stream));
     const int Cu = 1 + p->D;
     for (int f = 0; f < n; ++f)
       for (int e = 0; e < 12; ++e)
         for (int c = 0; c < Cu; ++c)
           poses[(static_cast<size_t>(f) * 12 + e) * Cu + c] = t[(static_cast<size_t>(f) * 12 + e) * p->C + c];
   }
-  if (stats) CUDA_TRY(ctx, cudaMemcpyAsync(stats, p->stats.p, sizeof(int) * 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (stats) CUDA_TRY(ctx, d2h(stats, p->stats.p, sizeof(int) * 8 * n, ctx->stream));
   return CSF_OK;
 }
 
@@ -1099,13 +1109,19 @@ extern "C" int csf_pipeline_hessian(csf_pipeline p, double* hessian, double* gra
   const int rc = csf_pipeline_result(p, nullptr, objective, poses, stats);
   if (rc) return rc;
   std::vector<double> out(2 + 3 * p->n_pairs);
-  CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), p->out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(out.data(), p->out.p, sizeof(double) * out.size(), ctx->stream));
   const double h = p->cfg.h;
   for (int q = 0; q < p->n_pairs; ++q) {
     if (hessian) hessian[q] = out[2 + 3 * q + 2] / (h * h);  // extract_hessian, csfd.hpp:319
     if (grad1) grad1[q] = out[2 + 3 * q] / h;
     if (grad2) grad2[q] = out[2 + 3 * q + 1] / h;
   }
+  return CSF_OK;
+}
+
+extern "C" int csf_pipeline_volume(csf_pipeline p, csf_volume* out) {
+  if (!p || !out) return CSF_EINVAL;
+  *out = p->vol;
   return CSF_OK;
 }
 
@@ -1139,7 +1155,11 @@ extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const d
   p->wait_frames = true;
   int rc = csf_pipeline_run(p, n_frames);
   p->wait_frames = false;
-  if (rc) return rc;
+  if (rc) {
+    // the uploads still read the caller's buffer: finish them before returning
+    cudaStreamSynchronize(p->copy_stream);
+    return rc;
+  }
   return csf_pipeline_result(p, gradient, objective, nullptr, nullptr);
 }
 
@@ -1175,8 +1195,8 @@ static int sample_points_common(csf_volume v, const double* points, int n, int g
   std::vector<double> o(outn);
   std::vector<int> vv(std::max(n, 1));
   if (n > 0) {
-    CUDA_TRY(ctx, cudaMemcpyAsync(o.data(), dout.p, sizeof(double) * outn, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaMemcpyAsync(vv.data(), dv.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, d2h(o.data(), dout.p, sizeof(double) * outn, ctx->stream));
+    CUDA_TRY(ctx, d2h(vv.data(), dv.p, sizeof(int) * n, ctx->stream));
   }
   const size_t orow = static_cast<size_t>(n) * (grad ? 3 : 1);
   for (size_t r = 0; r < orow; ++r)
@@ -1225,9 +1245,9 @@ extern "C" int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h,
   const int rc = sync_check(ctx, "csf_measured_tsdf");
   if (rc) return rc;
   if (n > 0) {
-    CUDA_TRY(ctx, cudaMemcpyAsync(psi, dout.p, sizeof(double) * n * C, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, d2h(psi, dout.p, sizeof(double) * n * C, ctx->stream));
     std::vector<int> vv(n);
-    CUDA_TRY(ctx, cudaMemcpyAsync(vv.data(), dv.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, d2h(vv.data(), dv.p, sizeof(int) * n, ctx->stream));
     for (int i = 0; i < n; ++i) valid[i] = vv[i];
   }
   return CSF_OK;
@@ -1276,7 +1296,7 @@ extern "C" int csf_volume_save(csf_volume v, const char* path) {
   if (v->hashed) {
     coords.resize(static_cast<size_t>(n / 512) * 3);
     if (!coords.empty())
-      CUDA_TRY(ctx, cudaMemcpyAsync(coords.data(), v->hash.coords, sizeof(int32_t) * coords.size(), cudaMemcpyDeviceToHost, ctx->stream));
+      CUDA_TRY(ctx, d2h(coords.data(), v->hash.coords, sizeof(int32_t) * coords.size(), ctx->stream));
   }
   bool any_im = false;
   for (long long i = 0; i < n && !any_im; ++i)
@@ -1732,6 +1752,8 @@ static int track_frame_impl(csf_volume v, const double* depth, int w, int h, con
     return fail(ctx, CSF_EINVAL, "csf_track_frame: unknown solver");
   if (cfg.solver != CSF_SOLVER_LINEARIZED && (!(cfg.h > 0.0) || cfg.h > 1e-6))
     return fail(ctx, CSF_EINVAL, "StepSize: step must satisfy 0 < h <= 1e-6");
+  if (w <= 0 || h <= 0) return fail(ctx, CSF_EINVAL, "csf_track_frame: empty frame");
+  if (!icp_frame_fits(w, h, 1)) return fail(ctx, CSF_EINVAL, "csf_track_frame: frame too large for the ICP reduction");
   cudaSetDevice(ctx->device);
   const int levels = std::clamp(cfg.levels, 1, 3);
   const size_t P = static_cast<size_t>(w) * h;
@@ -1831,7 +1853,7 @@ static int track_frame_impl(csf_volume v, const double* depth, int w, int h, con
         launch_icp_reduce(L, 0, 0, st.p, pyr[level], wl, hl, stride, kdev, pose.p, vre.p, nre.p, nullptr, nullptr,
                           cfg.d_max, cos_max, partials.p, counts.p, level, cfg.step_tolerance);
         TrackState hs;
-        CUDA_TRY(ctx, cudaMemcpyAsync(&hs, st.p, sizeof(TrackState), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(ctx, d2h(&hs, st.p, sizeof(TrackState), ctx->stream));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
         for (int i = 0; i < 6; ++i) {
           delta[i] = hs.delta[i];
@@ -2075,8 +2097,8 @@ extern "C" int csf_reloc_info(csf_reloc r, int* n, double* mu, double* centers, 
   cudaSetDevice(r->ctx->device);
   if (n) *n = r->n;
   if (mu) *mu = r->mu;
-  if (centers) CUDA_TRY(r->ctx, cudaMemcpyAsync(centers, r->centers.p, sizeof(double) * 3 * r->n, cudaMemcpyDeviceToHost, r->ctx->stream));
-  if (values) CUDA_TRY(r->ctx, cudaMemcpyAsync(values, r->values.p, sizeof(double) * r->n, cudaMemcpyDeviceToHost, r->ctx->stream));
+  if (centers) CUDA_TRY(r->ctx, d2h(centers, r->centers.p, sizeof(double) * 3 * r->n, r->ctx->stream));
+  if (values) CUDA_TRY(r->ctx, d2h(values, r->values.p, sizeof(double) * r->n, r->ctx->stream));
   return CSF_OK;
 }
 
@@ -2359,11 +2381,11 @@ extern "C" int csf_surfels_download(csf_surfels m, double* pos, double* nrm, dou
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   const size_t C = 1 + m->D, n = m->n;
   if (n == 0) return CSF_OK;
-  if (pos) CUDA_TRY(ctx, cudaMemcpyAsync(pos, m->pos.p, sizeof(double) * 3 * n * C, cudaMemcpyDeviceToHost, ctx->stream));
-  if (nrm) CUDA_TRY(ctx, cudaMemcpyAsync(nrm, m->nrm.p, sizeof(double) * 3 * n * C, cudaMemcpyDeviceToHost, ctx->stream));
-  if (rad) CUDA_TRY(ctx, cudaMemcpyAsync(rad, m->rad.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (conf) CUDA_TRY(ctx, cudaMemcpyAsync(conf, m->conf.p, sizeof(double) * n * C, cudaMemcpyDeviceToHost, ctx->stream));
-  if (ts) CUDA_TRY(ctx, cudaMemcpyAsync(ts, m->ts.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (pos) CUDA_TRY(ctx, d2h(pos, m->pos.p, sizeof(double) * 3 * n * C, ctx->stream));
+  if (nrm) CUDA_TRY(ctx, d2h(nrm, m->nrm.p, sizeof(double) * 3 * n * C, ctx->stream));
+  if (rad) CUDA_TRY(ctx, d2h(rad, m->rad.p, sizeof(double) * n, ctx->stream));
+  if (conf) CUDA_TRY(ctx, d2h(conf, m->conf.p, sizeof(double) * n * C, ctx->stream));
+  if (ts) CUDA_TRY(ctx, d2h(ts, m->ts.p, sizeof(int) * n, ctx->stream));
   return CSF_OK;
 }
 extern "C" int csf_surfels_upload(csf_surfels m, int n, const double* pos, const double* nrm, const double* rad,
@@ -2406,9 +2428,9 @@ extern "C" int csf_render_index_map(csf_surfels m, const double* c2w, const csf_
   if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "render_index_map: CUDA error");
   const size_t cells = static_cast<size_t>(16) * k->width * k->height;
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(offsets, m->ws.offsets, sizeof(uint32_t) * (cells + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(offsets, m->ws.offsets, sizeof(uint32_t) * (cells + 1), ctx->stream));
   if (entries && cnt > 0)
-    CUDA_TRY(ctx, cudaMemcpyAsync(entries, m->ws.entries, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, d2h(entries, m->ws.entries, sizeof(int32_t) * cnt, ctx->stream));
   *n_entries = cnt;
   return CSF_OK;
 }
@@ -2470,11 +2492,11 @@ extern "C" int csf_associate_surfels(csf_surfels m, const double* depth, int w, 
   if (rc) return rc;
   const size_t P = static_cast<size_t>(w) * h, C = 1 + m->D;
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(counts, m->ws.pint + P, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(counts, m->ws.pint + P, sizeof(int32_t) * P, ctx->stream));
   if (indices && weights && T > 0) {
     const int n = std::min(T, cap);
-    CUDA_TRY(ctx, cudaMemcpyAsync(indices, m->ws.pidx, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaMemcpyAsync(weights, m->ws.pw, sizeof(double) * n * C, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, d2h(indices, m->ws.pidx, sizeof(int32_t) * n, ctx->stream));
+    CUDA_TRY(ctx, d2h(weights, m->ws.pw, sizeof(double) * n * C, ctx->stream));
   }
   *total = T;
   return CSF_OK;
@@ -2532,8 +2554,8 @@ extern "C" int csf_predict_maps(csf_surfels m, const double* c2w, const csf_intr
   ctx->launches += 5;
   if (rc) return fail(ctx, rc == 5 ? CSF_ENOMEM : CSF_ECUDA, "predict_maps: CUDA error");
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(V, out.p, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(N, out.p + 3 * P, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, d2h(V, out.p, sizeof(double) * 3 * P, ctx->stream));
+  CUDA_TRY(ctx, d2h(N, out.p + 3 * P, sizeof(double) * 3 * P, ctx->stream));
   return CSF_OK;
 }
 
@@ -2548,23 +2570,57 @@ extern "C" double csf_sample_confidence(const csf_intrinsics* k, int x, int y) {
   return csf_det::exp(-g * g / 0.72);
 }
 
-// ---- sticky launch-error record (csf_internal.h)
+// ---- sticky launch-error record (csf_internal.h).  Per host thread: calls on
+// one context are serialized by the caller and different contexts run on
+// different host threads (csf_b200.h), so an error is reported by the call on
+// the thread whose launch failed, never by another context's call.
 namespace csfi {
-static std::mutex g_launch_mu;
-static std::string g_launch_msg;
-static std::atomic<int> g_launch_pending{0};
+static thread_local std::string t_launch_msg;
+static thread_local bool t_launch_pending = false;
+void note_error(const std::string& msg) {
+  if (!t_launch_pending) t_launch_msg = msg;  // the first error wins
+  t_launch_pending = true;
+}
 void note_launch_error(const char* what, cudaError_t e) {
-  std::fprintf(stderr, "csf_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
-  std::lock_guard<std::mutex> lk(g_launch_mu);
-  if (!g_launch_pending.load()) g_launch_msg = std::string("launch of ") + what + " failed: " + cudaGetErrorString(e);
-  g_launch_pending.store(1);
+  note_error(std::string("launch of ") + what + " failed: " + cudaGetErrorString(e));
 }
 bool take_launch_error(char* msg, size_t cap) {
-  if (!g_launch_pending.load()) return false;
-  std::lock_guard<std::mutex> lk(g_launch_mu);
-  std::snprintf(msg, cap, "%s", g_launch_msg.c_str());
-  g_launch_pending.store(0);
+  if (!t_launch_pending) return false;
+  std::snprintf(msg, cap, "%s", t_launch_msg.c_str());
+  t_launch_pending = false;
   return true;
+}
+
+// Function attributes and device properties are per device: cache them per
+// (device, kernel) under a lock so concurrent contexts on several GPUs each
+// get their own opt-in (csf_internal.h / lifted.cuh).
+static std::mutex g_attr_mu;
+static std::vector<std::pair<std::pair<int, const void*>, size_t>> g_smem_set;
+void ensure_dyn_smem(const void* fn, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  for (auto& e : g_smem_set)
+    if (e.first.first == dev && e.first.second == fn) {
+      if (e.second >= bytes) return;
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)) ==
+          cudaSuccess)
+        e.second = bytes;
+      return;
+    }
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)) == cudaSuccess)
+    g_smem_set.push_back({{dev, fn}, bytes});
+}
+int sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n > 0) return n;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  cache[dev].store(n, std::memory_order_relaxed);
+  return n;
 }
 }  // namespace csfi
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 namespace csfi {
 
@@ -179,6 +180,7 @@ void launch_expand_depth(cudaStream_t s, const double* real, long long P, int C,
 // surfaced as CSF_ECUDA by the next status check of the C-ABI (a failed
 // launch must never yield silently wrong results).
 void note_launch_error(const char* what, cudaError_t e);
+void note_error(const std::string& msg);  // a launch that could not be issued (no kernel for the shape)
 bool take_launch_error(char* msg, size_t cap);
 
 struct Launch {
@@ -223,6 +225,9 @@ void launch_measured_points(const Launch& L, const double* depth, int w, int h, 
 // ---- icp.cu
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp);
 int icp_tiles(int w, int h, int stride);
+// Whether a w x h frame at this pixel stride fits the ICP reduction's group
+// counters (callers reject larger frames with CSF_EINVAL).
+bool icp_frame_fits(int w, int h, int stride);
 // ICP scratch sizes for frames of up to max_tiles tiles (icp_tiles at stride 1);
 // the counts buffer must be zeroed once at allocation.
 size_t icp_partials_doubles(int C, int max_tiles);

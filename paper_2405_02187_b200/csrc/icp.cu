@@ -368,9 +368,7 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
                                                     const double* __restrict__ nim, double d_max, double cos_max,
                                                     int Dp, int chunk, double* __restrict__ partials,
                                                     int* __restrict__ counts, double* __restrict__ gpartials,
-                                                    int* __restrict__ gcounts, unsigned* __restrict__ group_ctr,
-                                                    TrackState* st_rw, double* pose_rw, int level, double tol,
-                                                    int fused) {
+                                                    int* __restrict__ gcounts, unsigned* __restrict__ group_ctr) {
   pdl_wait();
   pdl_trigger();
   if (st->level_done) return;
@@ -465,19 +463,7 @@ __global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st
   }
   if (threadIdx.x == 0) counts[blockIdx.x] = tile_count;
   clock_mark(2);
-  const bool grouped = group_sum(partials, counts, n_acc, gpartials, gcounts, group_ctr);
-  if (!fused || !grouped) return;
-  // the CTA completing the last group runs the solve (no second launch)
-  __shared__ bool s_solve;
-  const int n_groups = (gridDim.x + kGroup - 1) / kGroup;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_solve = atomicAdd(group_ctr + kMaxGroupCtr - 1, 1u) == static_cast<unsigned>(n_groups - 1);
-  __syncthreads();
-  if (!s_solve) return;
-  if (threadIdx.x == 0) group_ctr[kMaxGroupCtr - 1] = 0u;
-  __threadfence();
-  icp_solve_body(st_rw, gpartials, gcounts, n_groups, pose_rw, Dp, level, tol);
+  group_sum(partials, counts, n_acc, gpartials, gcounts, group_ctr);
 }
 
 // Level entry: the prediction pose is the current estimate (icp.cpp:191).
@@ -949,7 +935,7 @@ static void chk(const char* what) {
     case 4: { constexpr int kG = 4; BODY; } break;    \
     case 5: { constexpr int kG = 5; BODY; } break;    \
     case 6: { constexpr int kG = 6; BODY; } break;    \
-    default: std::fprintf(stderr, "csf_b200: no kernel for group width %d\n", G); \
+    default: note_error("csf_b200: no kernel for group width " + std::to_string(G)); \
   }
 
 // Debug: enable per-CTA phase timestamps into a device buffer of
@@ -961,8 +947,12 @@ void icp_clock_enable(unsigned long long* buf) {
 }
 
 int icp_tiles(int w, int h, int stride) {
-  const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
-  return (nxs * nys + kTile - 1) / kTile;
+  const long long nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
+  return static_cast<int>((nxs * nys + kTile - 1) / kTile);
+}
+bool icp_frame_fits(int w, int h, int stride) {
+  const int tiles = icp_tiles(w, h, stride);
+  return (tiles + kGroup - 1) / kGroup <= kMaxGroupCtr - 1;
 }
 
 // Slots per shared-memory chunk of the (J, r) rows.
@@ -992,16 +982,6 @@ size_t icp_counts_ints(int max_tiles) {
 // sums) then k_icp_solve_t.  Scratch layout: partials = [tiles][27C] then
 // [groups][27C]; counts = [kMaxGroupCtr] self-resetting group counters (zero
 // at allocation), [tiles], [groups].
-// Dynamic shared memory above the 48 KB default needs the opt-in; the
-// threshold is on static + dynamic bytes, so opt in for every size (once per
-// kernel and high-water mark).
-static void opt_in_smem(const void* fn, size_t smem, size_t* set) {
-  if (smem <= *set) return;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  *set = smem;
-}
-static size_t smem_set[3] = {0, 0, 0};
-
 void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const double* depth, int w, int h,
                        int stride, const double* intr, double* pose, const double* vre, const double* nre,
                        const double* vim, const double* nim, double d_max, double cos_max, double* partials,
@@ -1012,46 +992,26 @@ void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const dou
   const size_t smem = sizeof(double) * (16 * C + static_cast<size_t>(chunk) * 7 * C);
   const int tiles = icp_tiles(w, h, stride);
   const int groups = (tiles + kGroup - 1) / kGroup;
-  // the solve is its own (PDL) launch; CSF_ICP_FUSED=1 runs it in the CTA
-  // completing the last group instead (measured slower on B200: the solve
-  // then shares the big kernel's cold instruction stream)
-  static const bool fused = std::getenv("CSF_ICP_FUSED") != nullptr;
   if (groups > kMaxGroupCtr - 1 || Dp > kMaxC - 1) {
-    std::fprintf(stderr, "csf_b200: ICP frame too large (%d tiles) or too many channels (%d)\n", tiles, Dp);
+    note_error("csf_b200: ICP frame too large (" + std::to_string(tiles) + " tiles) or too many channels (" +
+               std::to_string(Dp) + ")");
     return;
   }
   unsigned* ctr = reinterpret_cast<unsigned*>(counts);
   int* tcounts = counts + kMaxGroupCtr;
   int* gcounts = tcounts + tiles;
   double* gpartials = partials + static_cast<size_t>(tiles) * n_acc;
-  // J/r rows are evaluated in channel groups of 1 (or 2): register-light,
-  // any width that divides Dp addresses the same channel layout.
-  const int RG = G == 0 ? 0 : (std::getenv("CSF_ICP_RG2") ? (Dp % 2 == 0 ? 2 : 1) : 1);
-  switch (RG) {
-    case 0:
-      opt_in_smem(reinterpret_cast<const void*>(k_icp_reduce<0>), smem, &smem_set[0]);
-      launch_pdl(k_icp_reduce<0>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
-                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
-                 pose, level, tol, fused ? 1 : 0);
-      break;
-    case 1:
-      opt_in_smem(reinterpret_cast<const void*>(k_icp_reduce<1>), smem, &smem_set[1]);
-      launch_pdl(k_icp_reduce<1>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
-                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
-                 pose, level, tol, fused ? 1 : 0);
-      break;
-    default:
-      opt_in_smem(reinterpret_cast<const void*>(k_icp_reduce<2>), smem, &smem_set[2]);
-      launch_pdl(k_icp_reduce<2>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr,
-                 pose, vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr, st,
-                 pose, level, tol, fused ? 1 : 0);
-  }
-  if (!fused) {
-    launch_pdl(k_icp_solve_t, dim3(1), dim3(kRedThreads), 0, L.stream, st, static_cast<const double*>(gpartials),
-               static_cast<const int*>(gcounts), groups, pose, Dp, level, tol);
-    ++*L.launches;
-  }
-  *L.launches += 1;
+  // J/r rows are evaluated one channel at a time: register-light, and any
+  // channel-group width addresses the same channel layout.
+  if (G == 0)
+    launch_pdl(k_icp_reduce<0>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr, pose,
+               vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
+  else
+    launch_pdl(k_icp_reduce<1>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr, pose,
+               vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
+  launch_pdl(k_icp_solve_t, dim3(1), dim3(kRedThreads), 0, L.stream, st, static_cast<const double*>(gpartials),
+             static_cast<const int*>(gcounts), groups, pose, Dp, level, tol);
+  *L.launches += 2;
   chk("icp_reduce");
 }
 
@@ -1106,11 +1066,6 @@ void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double
   const int tiles = icp_tiles(w, h, stride);
   const int pairs = Dp / 3;
   const size_t smem = sizeof(S) * kTile2 * 7;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_icp_reduce2<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = true;
-  }
   launch_pdl(k_icp_reduce2<S>, dim3(dim3(tiles, pairs)), dim3(kTile2), smem, L.stream, st, depth, w, h, stride, intr, pose, vre, nre, vim,
                                                                    nim, d_max, cos_max, Dp, partials, counts);
   launch_pdl(k_icp_solve2<S>, dim3(pairs), dim3(128), 0, L.stream, st, partials, counts, tiles, pose, Dp, stage);

@@ -35,9 +35,20 @@ namespace csfd {
 CSF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 CSF_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
+}  // namespace csfd
+namespace csfi {
+// Opt `fn` into `bytes` of dynamic shared memory on the current device
+// (cudaFuncSetAttribute is per device); thread-safe, cached per (device, fn).
+void ensure_dyn_smem(const void* fn, size_t bytes);
+// SM count of the current device (cached per device).
+int sm_count();
+}  // namespace csfi
+namespace csfd {
+
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        Args... args) {
+  if (smem > 48 * 1024) csfi::ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

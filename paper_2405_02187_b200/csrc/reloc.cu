@@ -286,13 +286,7 @@ static void chk(const char* what) {
 }
 
 static int grid_of(long long n) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = sm_count();
   const long long want = (n + 255) / 256;
   return static_cast<int>(std::max<long long>(1, std::min<long long>(want, 8LL * sms)));
 }

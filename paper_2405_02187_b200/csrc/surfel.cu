@@ -542,6 +542,8 @@ __global__ void k_pred_write(const int* __restrict__ ibest, int P, int C, const 
 }
 
 __global__ void k_fill_u64(unsigned long long* a, int n, unsigned long long v) {
+  pdl_wait();  // PDL-launched: order against the previous kernel on the stream
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
 }
@@ -554,10 +556,14 @@ __global__ void k_expand_depth(const double* __restrict__ real, long long P, int
 }
 
 __global__ void k_fill_iota(int* a, int n) {
+  pdl_wait();  // PDL-launched: order against the previous kernel on the stream
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = i;
 }
 __global__ void k_fill_i32(int* a, int n, int v) {
+  pdl_wait();  // PDL-launched: order against the previous kernel on the stream
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
 }

@@ -1042,139 +1042,13 @@ CSF_DEV double sample_channel(const VoxelStore& vox, const int* vid, const doubl
   return t;
 }
 
-// Lifted epilogue, one thread per hit pixel: the real chain once (bit-identical
-// to the L<G> evaluation), then every channel in tangent form from the saved
-// real intermediates (per-operation truncated-Complex rules; the trilinear
-// samples use the weight/gradient form of sample_tsdf<S>).
-template <typename V>
-__global__ void __launch_bounds__(128) k_raycast_lift_all(V vol, const double* __restrict__ pose,
-                                                          const double* __restrict__ intr, int w, int h, int Dp,
-                                                          const double2* __restrict__ hits, double* __restrict__ vre,
-                                                          double* __restrict__ nre, double* __restrict__ vim,
-                                                          double* __restrict__ nim) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ double sm[];
-  const int C = 1 + Dp;
-  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
-  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
-  __syncthreads();
-  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pix >= w * h) return;
-  const double2 hit = hits[pix];
-  if (hit.y < 0.0) return;
-  const double a0 = hit.x, a1 = hit.y;
-  const int x = pix % w, y = pix / w;
-  const double* kk = sm + 12 * C;
-  // ---- real chain (as the L<G> code's real parts)
-  double R[9], T[3];
-#pragma unroll
-  for (int e = 0; e < 9; ++e) R[e] = sm[e * C];
-#pragma unroll
-  for (int e = 0; e < 3; ++e) T[e] = sm[(9 + e) * C];
-  const double fxk = kk[0], fyk = kk[C], cxk = kk[2 * C], cyk = kk[3 * C];
-  const double tx = static_cast<double>(x) - cxk, ty = static_cast<double>(y) - cyk;
-  const double dc[3] = {tx / fxk, ty / fyk, 1.0};
-  const double dot_dc = dc[0] * dc[0] + (dc[1] * dc[1] + 1.0 * 1.0);
-  const double rn = sqrt(dot_dc);
-  const double dn[3] = {dc[0] / rn, dc[1] / rn, dc[2] / rn};
-  double dir[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r) dir[r] = R[3 * r] * dn[0] + (R[3 * r + 1] * dn[1] + R[3 * r + 2] * dn[2]);
-  int vid[8][8];
-  double wgt[8][8], dsv[8][3], f[8];
-  const double q0[3] = {T[0] + a0 * dir[0], T[1] + a0 * dir[1], T[2] + a0 * dir[2]};
-  const double q1[3] = {T[0] + a1 * dir[0], T[1] + a1 * dir[1], T[2] + a1 * dir[2]};
-  sample_real_ex(vol, q0[0], q0[1], q0[2], &f[0], vid[0], wgt[0], dsv[0]);
-  sample_real_ex(vol, q1[0], q1[1], q1[2], &f[1], vid[1], wgt[1], dsv[1]);
-  const double span = a1 - a0;
-  const double num = span * f[0], den = f[1] - f[0];
-  const double qq = num / den;
-  const double astar = a0 - qq;
-  const double vv[3] = {T[0] + astar * dir[0], T[1] + astar * dir[1], T[2] + astar * dir[2]};
-  const double hv = vol.vs;
-  double grad[3];
-#pragma unroll
-  for (int axis = 0; axis < 3; ++axis) {
-    double lo[3] = {vv[0], vv[1], vv[2]}, hi[3] = {vv[0], vv[1], vv[2]};
-    lo[axis] = lo[axis] - hv;
-    hi[axis] = hi[axis] + hv;
-    if (!sample_real_ex(vol, lo[0], lo[1], lo[2], &f[2 + 2 * axis], vid[2 + 2 * axis], wgt[2 + 2 * axis],
-                        dsv[2 + 2 * axis]))
-      return;
-    if (!sample_real_ex(vol, hi[0], hi[1], hi[2], &f[3 + 2 * axis], vid[3 + 2 * axis], wgt[3 + 2 * axis],
-                        dsv[3 + 2 * axis]))
-      return;
-    grad[axis] = (f[3 + 2 * axis] - f[2 + 2 * axis]) / (2.0 * hv);
-  }
-  const double len2 = grad[0] * grad[0] + (grad[1] * grad[1] + grad[2] * grad[2]);
-  if (!(len2 > 0.0)) return;
-  const double ln = sqrt(len2);
-  const double nn[3] = {grad[0] / ln, grad[1] / ln, grad[2] / ln};
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    vre[3LL * pix + c] = vv[c];
-    nre[3LL * pix + c] = nn[c];
-  }
-  // ---- channels
-  const double inv_fx2 = 1.0 / (fxk * fxk), inv_fy2 = 1.0 / (fyk * fyk), inv_rn2 = 1.0 / (rn * rn);
-  const double inv_vs2 = 1.0 / (hv * hv), inv_den2 = 1.0 / (den * den), inv_2h2 = 1.0 / ((2.0 * hv) * (2.0 * hv));
-  const double inv_ln2 = 1.0 / (ln * ln), half_rn = 0.5 / rn, half_ln = 0.5 / ln;
-  (void)inv_fx2; (void)inv_fy2; (void)inv_rn2; (void)inv_vs2; (void)inv_den2; (void)inv_2h2; (void)inv_ln2;
-  for (int d = 0; d < Dp; ++d) {
-    const int ch = 1 + d;
-    // dir_cam = ((x - cx)/fx, (y - cy)/fy, 1)
-    const double dci[3] = {CSF_CH_DIV(-kk[2 * C + ch] * fxk - tx * kk[ch], fxk * fxk, inv_fx2),
-                           CSF_CH_DIV(-kk[3 * C + ch] * fyk - ty * kk[C + ch], fyk * fyk, inv_fy2), 0.0};
-    const double doti = (dc[0] * dci[0] + dci[0] * dc[0]) + ((dc[1] * dci[1] + dci[1] * dc[1]) + 0.0);
-    const double rni = half_rn * doti;
-    double dni[3], diri[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) dni[a] = CSF_CH_DIV(dci[a] * rn - dc[a] * rni, rn * rn, inv_rn2);
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const double t0 = R[3 * r] * dni[0] + sm[(3 * r) * C + ch] * dn[0];
-      const double t1 = R[3 * r + 1] * dni[1] + sm[(3 * r + 1) * C + ch] * dn[1];
-      const double t2 = R[3 * r + 2] * dni[2] + sm[(3 * r + 2) * C + ch] * dn[2];
-      diri[r] = t0 + (t1 + t2);
-    }
-    const double Ti[3] = {sm[9 * C + ch], sm[10 * C + ch], sm[11 * C + ch]};
-    const double q0i[3] = {Ti[0] + a0 * diri[0], Ti[1] + a0 * diri[1], Ti[2] + a0 * diri[2]};
-    const double q1i[3] = {Ti[0] + a1 * diri[0], Ti[1] + a1 * diri[1], Ti[2] + a1 * diri[2]};
-    const double f0i = sample_channel(vol.vox, vid[0], wgt[0], dsv[0], q0i, hv, inv_vs2, d);
-    const double f1i = sample_channel(vol.vox, vid[1], wgt[1], dsv[1], q1i, hv, inv_vs2, d);
-    const double numi = span * f0i, deni = f1i - f0i;
-    const double qqi = CSF_CH_DIV(numi * den - num * deni, den * den, inv_den2);
-    const double asti = -qqi;
-    double vvi[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) vvi[a] = Ti[a] + (astar * diri[a] + asti * dir[a]);
-    double gi[3];
-#pragma unroll
-    for (int axis = 0; axis < 3; ++axis) {
-      const double lo = sample_channel(vol.vox, vid[2 + 2 * axis], wgt[2 + 2 * axis], dsv[2 + 2 * axis], vvi, hv,
-                                       inv_vs2, d);
-      const double hi = sample_channel(vol.vox, vid[3 + 2 * axis], wgt[3 + 2 * axis], dsv[3 + 2 * axis], vvi, hv,
-                                       inv_vs2, d);
-      gi[axis] = CSF_CH_DIV((hi - lo) * (2.0 * hv), (2.0 * hv) * (2.0 * hv), inv_2h2);
-    }
-    const double l2i = (grad[0] * gi[0] + gi[0] * grad[0]) + ((grad[1] * gi[1] + gi[1] * grad[1]) +
-                                                             (grad[2] * gi[2] + gi[2] * grad[2]));
-    const double lni = half_ln * l2i;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      vim[(3LL * pix + c) * Dp + d] = vvi[c];
-      nim[(3LL * pix + c) * Dp + d] = CSF_CH_DIV(gi[c] * ln - grad[c] * lni, ln * ln, inv_ln2);
-    }
-  }
-}
-
 // Cooperative lift: the per-pixel real chain (2 crossing samples, 6
 // gradient samples) is split over 8 lanes per pixel and its intermediates go
 // to shared memory; then one thread per (pixel, channel) evaluates the
 // tangent-form channel from them.  Real parts are bit-identical to the L<G>
-// evaluation (same sample_real_ex arithmetic); channels follow
-// k_raycast_lift_all.  Many light threads keep far more voxel-channel gathers
+// evaluation (same sample_real_ex arithmetic); each channel follows the
+// truncated-Complex rule of every operation (csfd.hpp:44-58) applied to the
+// saved real intermediates.  Many light threads keep far more voxel-channel gathers
 // in flight than one heavy thread per (pixel, group).
 struct LiftRec {
   double wgt[8][8];
@@ -1357,132 +1231,6 @@ __global__ void __launch_bounds__(256) k_raycast_lift_coop(V vol, const double* 
   }
 }
 
-// Warp-cooperative march for the small pyramid levels, where a few long
-// (grazing) rays set the kernel time: one warp per ray evaluates 32
-// consecutive alpha steps at once.  Each lane forms its alpha by the same
-// repeated additions as the sequential loop (bit-identical), samples it, and
-// the reference's sequential rule (have_prev reset on an invalid sample,
-// crossing on f_prev > 0 > f) is resolved across the window with one shuffle
-// and one ballot.  Empty-space skipping is the per-thread kernel's, applied
-// uniformly at window starts.
-template <typename V>
-__global__ void __launch_bounds__(128) k_raycast_march_warp(V vol, const double* __restrict__ pose,
-                                                            const double* __restrict__ intr, int w, int h, int Dp,
-                                                            double near_clip, double far_clip, double step, Box box,
-                                                            double2* __restrict__ hits, double* __restrict__ vre,
-                                                            double* __restrict__ nre) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double s_pose[16];
-  const int C = 1 + Dp;
-  if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
-  else if (threadIdx.x < 16) s_pose[threadIdx.x] = intr[(threadIdx.x - 12) * C];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int pix = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (pix >= w * h) return;
-  const int x = pix % w, y = pix / w;
-  Pose<double> c2w;
-#pragma unroll
-  for (int e = 0; e < 9; ++e) c2w.R.m[e] = s_pose[e];
-#pragma unroll
-  for (int e = 0; e < 3; ++e) c2w.t.v[e] = s_pose[9 + e];
-  const double fxk = s_pose[12], fyk = s_pose[13], cxk = s_pose[14], cyk = s_pose[15];
-  const V3<double> dc = mk3<double>((static_cast<double>(x) - cxk) / fxk, (static_cast<double>(y) - cyk) / fyk, 1.0);
-  const double rn = sqrt(dot3(dc, dc));
-  const V3<double> dir = matvec(c2w.R, mk3<double>(dc.v[0] / rn, dc.v[1] / rn, dc.v[2] / rn));
-  const V3<double> o = c2w.t;
-  if (lane < 3) {
-    vre[3LL * pix + lane] = 0.0;
-    nre[3LL * pix + lane] = 0.0;
-  }
-  if (lane == 0) hits[pix] = make_double2(0.0, -1.0);
-  double t0 = near_clip, t1 = far_clip;
-  if (box.use) {
-    bool hit_box = true;
-#pragma unroll
-    for (int axis = 0; axis < 3; ++axis) {
-      const double od = o.v[axis], dd = dir.v[axis];
-      if (fabs(dd) < 1e-12) {
-        if (od < box.lo[axis] || od > box.hi[axis]) hit_box = false;
-        continue;
-      }
-      double ta = (box.lo[axis] - od) / dd;
-      double tb = (box.hi[axis] - od) / dd;
-      if (ta > tb) {
-        const double t = ta;
-        ta = tb;
-        tb = t;
-      }
-      t0 = t0 < ta ? ta : t0;
-      t1 = tb < t1 ? tb : t1;
-    }
-    if (!hit_box) return;
-  }
-  if (t0 >= t1) return;
-  typename V::Cache cache;
-  cache.reset();
-  V3<double> invd;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) invd.v[a] = dir.v[a] != 0.0 ? 1.0 / dir.v[a] : 0.0;
-  bool have_prev = false;
-  double alpha_prev = 0.0, f_prev = 0.0;
-  double alpha = t0;  // alpha of the window's first step
-  while (alpha <= t1) {
-    if constexpr (V::kHashed) {
-      const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1], pz = o.v[2] + alpha * dir.v[2];
-      const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
-                k0 = ifloor((pz - vol.oz) / vol.vs);
-      const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
-      const int occ = vol.super_occupied(bx, by, bz);
-      int span = 0;
-      if (occ == 0) span = 8;
-      else if (vol.block(bx, by, bz) < 0) span = 1;
-      if (span > 0) {
-        have_prev = false;
-        const int m = span == 8 ? ~7 : ~0;
-        const double lim = box_exit(vol, bx & m, by & m, bz & m, span, o, invd) - 1e-6;
-        alpha += step;
-        while (alpha < lim && alpha <= t1) alpha += step;
-        continue;
-      }
-    }
-    // this lane's alpha: the window start plus `lane` sequential additions
-    double a = alpha;
-    for (int i = 0; i < lane; ++i) a += step;
-    const bool in_range = a <= t1;
-    double f = 0.0;
-    bool ok = false;
-    if (in_range)
-      ok = sample_real(vol, o.v[0] + a * dir.v[0], o.v[1] + a * dir.v[1], o.v[2] + a * dir.v[2], cache, &f);
-    // predecessor of this lane in the sequential order
-    const double pf = __shfl_up_sync(0xffffffffu, f, 1);
-    const bool pok = __shfl_up_sync(0xffffffffu, ok, 1);
-    const double pa = __shfl_up_sync(0xffffffffu, a, 1);
-    const bool prev_ok = lane == 0 ? have_prev : pok;
-    const double prev_f = lane == 0 ? f_prev : pf;
-    const double prev_a = lane == 0 ? alpha_prev : pa;
-    const bool cross = in_range && ok && prev_ok && prev_f > 0.0 && f < 0.0;
-    const unsigned bal = __ballot_sync(0xffffffffu, cross);
-    if (bal) {
-      const int c = __ffs(bal) - 1;
-      if (lane == c) {
-        hits[pix] = make_double2(prev_a, a);
-        hits[w * h + pix] = make_double2(prev_f, f);
-      }
-      return;
-    }
-    // carry the state of the window's last in-range step
-    const unsigned inr = __ballot_sync(0xffffffffu, in_range);
-    const int last = 31 - __clz(inr);
-    have_prev = __shfl_sync(0xffffffffu, ok, last);
-    f_prev = __shfl_sync(0xffffffffu, f, last);
-    alpha_prev = __shfl_sync(0xffffffffu, a, last);
-    const double a31 = __shfl_sync(0xffffffffu, a, 31);
-    alpha = a31 + step;
-  }
-}
-
 template <typename S, typename V>
 __global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __restrict__ pose,
                                                       const double* __restrict__ intr, int w, int h, int Dp,
@@ -1590,7 +1338,7 @@ int pick_group(int D) {
     case 4: { constexpr int kG = 4; BODY; } break;    \
     case 5: { constexpr int kG = 5; BODY; } break;    \
     case 6: { constexpr int kG = 6; BODY; } break;    \
-    default: std::fprintf(stderr, "csf_b200: no kernel for group width %d\n", G); \
+    default: note_error("csf_b200: no kernel for group width " + std::to_string(G)); \
   }
 
 // Compile-time channel counts of the adjoint fusion kernels (all channel
@@ -1606,29 +1354,7 @@ static bool fixed_channels(int Dp) { return (Dp >= 1 && Dp <= 12) || Dp == 16 ||
     case 11: { constexpr int kN = 11; BODY; } break;  case 12: { constexpr int kN = 12; BODY; } break; \
     case 16: { constexpr int kN = 16; BODY; } break;  case 20: { constexpr int kN = 20; BODY; } break; \
     case 24: { constexpr int kN = 24; BODY; } break;                                               \
-    default: std::fprintf(stderr, "csf_b200: no fusion kernel for %d channels\n", Dp);            \
-  }
-
-// The raycast's lifted epilogue is register-heavy: it evaluates channel
-// groups of width 2 (or 1) regardless of the volume's group width.
-static int raycast_group(int G, int Dp) {
-  if (G == 0) return 0;
-  static int forced = -2;
-  if (forced == -2) {
-    const char* e = std::getenv("CSF_LIFT_G");
-    forced = e ? std::atoi(e) : -1;
-  }
-  if ((forced == 1 || forced == 2 || forced == 5) && Dp % forced == 0) return forced;
-  if (Dp % 5 == 0) return 5;
-  return (Dp % 2 == 0) ? 2 : 1;
-}
-#define CSF_DISPATCH_RG(G, BODY)                      \
-  switch (G) {                                        \
-    case 0: { constexpr int kG = 0; BODY; } break;    \
-    case 1: { constexpr int kG = 1; BODY; } break;    \
-    case 2: { constexpr int kG = 2; BODY; } break;    \
-    case 5: { constexpr int kG = 5; BODY; } break;    \
-    default: std::fprintf(stderr, "csf_b200: no raycast kernel for group width %d\n", G); \
+    default: note_error("csf_b200: no fusion kernel for " + std::to_string(Dp) + " channels");     \
   }
 
 static DenseView dense_view(const DenseDev& v, int Dp) {
@@ -1649,17 +1375,6 @@ static HashView hash_view(const HashDev& v, int Dp) {
   d.mask = (1u << v.bits) - 1u;
   d.vs = v.vs; d.ox = v.ox; d.oy = v.oy; d.oz = v.oz; d.mu = v.mu; d.cap = v.cap;
   return d;
-}
-
-static int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
 }
 
 }  // namespace csfi
@@ -1824,23 +1539,8 @@ void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, 
   chk("init_volume");
 }
 
-// Channel-group width of the fusion kernels.  Any width dividing Dp
-// addresses the same channel layout; narrower groups trade a recomputed real
-// channel for registers (occupancy).  CSF_INTEGRATE_G overrides (tuning).
-static int integrate_group(int G, int Dp) {
-  if (G == 0) return 0;
-  static int forced = -2;
-  if (forced == -2) {
-    const char* e = std::getenv("CSF_INTEGRATE_G");
-    forced = e ? std::atoi(e) : -1;
-  }
-  if (forced > 0 && forced <= 6 && Dp % forced == 0) return forced;
-  return G;
-}
-
 void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* depth, int w, int h,
                             const double* pose, const double* intr, int* upd) {
-  G = integrate_group(G, Dp);
   const DenseView view = dense_view(v, Dp);
   const size_t smem = integrate_smem(Dp, v.order != 2 && Dp % 2 == 0 && Dp <= 24);
   const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
@@ -1859,7 +1559,6 @@ void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, c
 
 void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, const AllocScratch& a,
                              const double* depth, int w, int h, const double* pose, const double* intr, int* upd) {
-  G = integrate_group(G, Dp);
   const HashView view = hash_view(v, Dp);
   const size_t smem = integrate_smem(Dp, v.order != 2 && Dp % 2 == 0 && Dp <= 24);
   const int grid = sm_count() * 8;
@@ -1935,24 +1634,19 @@ size_t alloc_scan_bytes(int n) {
 }
 
 template <typename V>
-static void raycast_impl(const Launch& L, const V& view, Box box, int order, int G, int Dp, const double* pose,
+static void raycast_impl(const Launch& L, const V& view, Box box, int order, int Dp, const double* pose,
                          const double* intr, int w, int h, double near_clip, double far_clip, double step,
                          double2* hits, double* vre, double* nre, double* vim, double* nim,
                          const double* atab = nullptr, int n_tab = 0, unsigned* seg_first = nullptr) {
   const int P = w * h;
   if (L.phase != 2) {
-    // The warp-cooperative march measured slower than one thread per ray at
-    // every level on B200 (bench r01), so it is opt-in.
-    static const long long warp_threshold = std::getenv("CSF_MARCH_WARP_MAX")
-                                                ? std::atoll(std::getenv("CSF_MARCH_WARP_MAX"))
-                                                : 0;
-    // segments per ray: enough threads to fill the GPU at the small levels
+    // Segments per ray (hashed volumes): enough threads to fill the GPU at
+    // the small levels, where the longest ray sets the kernel time.
     int S = 1;
     if constexpr (V::kHashed) {
-      static const int seg_max = std::getenv("CSF_MARCH_SEG_MAX") ? std::atoi(std::getenv("CSF_MARCH_SEG_MAX")) : 16;
-      static const long long target =
-          std::getenv("CSF_MARCH_THREADS") ? std::atoll(std::getenv("CSF_MARCH_THREADS")) : 320000LL;
-      while (S < seg_max && static_cast<long long>(P) * S * 2 <= target) S *= 2;
+      constexpr int kSegMax = 16;
+      constexpr long long kTargetThreads = 320000;
+      while (S < kSegMax && static_cast<long long>(P) * S * 2 <= kTargetThreads) S *= 2;
       if (!atab || !seg_first) S = 1;
     }
     if (S > 1) {
@@ -1965,12 +1659,10 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
                    static_cast<const unsigned*>(seg_first), hits, vre, nre);
         *L.launches += 1;
       }
-    } else if (P <= warp_threshold)
-      launch_pdl(k_raycast_march_warp<V>, dim3((P + 3) / 4), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp, near_clip, far_clip,
-                                                                 step, box, hits, vre, nre);
-    else
-      launch_pdl(k_raycast_march<V>, dim3((P + 127) / 128), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp, near_clip, far_clip,
-                                                                step, box, hits, vre, nre, atab, n_tab);
+    } else {
+      launch_pdl(k_raycast_march<V>, dim3((P + 127) / 128), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp,
+                 near_clip, far_clip, step, box, hits, vre, nre, atab, n_tab);
+    }
     if (Dp > 0 && vim) {
       cudaMemsetAsync(vim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
       cudaMemsetAsync(nim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
@@ -1982,40 +1674,16 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
   if (order == 2) {
     // second order: one thread per (hit pixel, pair) in Bicomplex arithmetic
     const long long items = static_cast<long long>(P) * (Dp / 3);
-    launch_pdl(k_raycast_lift<B<1>, V>, dim3(static_cast<int>((items + 127) / 128)), dim3(128), smem, L.stream, view, pose, intr, w, h,
-                                                                                          Dp, hits, vre, nre, vim, nim);
+    launch_pdl(k_raycast_lift<B<1>, V>, dim3(static_cast<int>((items + 127) / 128)), dim3(128), smem, L.stream, view,
+               pose, intr, w, h, Dp, hits, vre, nre, vim, nim);
     *L.launches += 1;
     return;
   }
-  // one thread per hit pixel with tangent-form channels (CSF_LIFT_ALL=1) or
-  // one thread per (hit pixel, channel group) — the default: more memory
-  // parallelism wins over the recomputed real chain on B200.
-  static const char* mode_env = std::getenv("CSF_LIFT_MODE");
-  static const int mode = mode_env ? std::atoi(mode_env) : 0;  // 0 coop, 1 per pixel, 2 per group
-  if (mode == 0) {
-    const size_t smem_c = smem + sizeof(LiftRec) * kLiftPix;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_raycast_lift_coop<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      attr = true;
-    }
-    launch_pdl(k_raycast_lift_coop<V>, dim3((P + kLiftPix - 1) / kLiftPix), dim3(8 * kLiftPix), smem_c, L.stream, 
-        view, pose, intr, w, h, Dp, hits, vre, nre, vim, nim);
-    *L.launches += 1;
-    return;
-  }
-  if (G > 0 && mode == 1) {
-    launch_pdl(k_raycast_lift_all<V>, dim3((P + 127) / 128), dim3(128), smem, L.stream, view, pose, intr, w, h, Dp, hits, vre, nre, vim,
-                                                                    nim);
-    *L.launches += 1;
-    return;
-  }
-  const int RG = raycast_group(G, Dp);
-  const int passes = RG == 0 ? 1 : Dp / RG;
-  const long long items = static_cast<long long>(P) * passes;
-  const int grid = static_cast<int>((items + 127) / 128);
-  CSF_DISPATCH_RG(RG, (launch_pdl(k_raycast_lift<Scal<kG>, V>, dim3(grid), dim3(128), smem, L.stream, view, pose, intr, w, h, Dp, hits,
-                                                                                  vre, nre, vim, nim)));
+  // first order: the cooperative lift (8 lanes per pixel for the real chain,
+  // then one thread per (pixel, channel))
+  const size_t smem_c = smem + sizeof(LiftRec) * kLiftPix;
+  launch_pdl(k_raycast_lift_coop<V>, dim3((P + kLiftPix - 1) / kLiftPix), dim3(8 * kLiftPix), smem_c, L.stream, view,
+             pose, intr, w, h, Dp, hits, vre, nre, vim, nim);
   *L.launches += 1;
 }
 
@@ -2029,7 +1697,7 @@ void launch_raycast_dense(const Launch& L, const DenseDev& v, int G, int Dp, con
   box.hi[0] = v.ox + v.vs * (static_cast<double>(v.nx) - 1.0);
   box.hi[1] = v.oy + v.vs * (static_cast<double>(v.ny) - 1.0);
   box.hi[2] = v.oz + v.vs * (static_cast<double>(v.nz) - 1.0);
-  raycast_impl(L, view, box, v.order, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
+  raycast_impl(L, view, box, v.order, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim);
   chk("raycast_dense");
 }
 
@@ -2039,7 +1707,7 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
   const HashView view = hash_view(v, Dp);
   Box box;
   box.use = false;
-  raycast_impl(L, view, box, v.order, G, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim,
+  raycast_impl(L, view, box, v.order, Dp, pose, intr, w, h, near_clip, far_clip, step, hits, vre, nre, vim, nim,
                v.alpha_tab, v.alpha_n, v.seg_first);
   chk("raycast_hashed");
 }
