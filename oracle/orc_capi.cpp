@@ -911,6 +911,7 @@ int orc_pipeline_run_keep(const csf_pipeline_cfg* c, const float* depth, const d
       case 6: run(std::integral_constant<int, 6>{}); break;
       case 8: run(std::integral_constant<int, 8>{}); break;
       case 10: run(std::integral_constant<int, 10>{}); break;
+      case 20: run(std::integral_constant<int, 20>{}); break;
       default: throw std::invalid_argument("orc_pipeline_run_keep: unsupported direction count");
     }
     if (objective) *objective = r.objective;

@@ -8,11 +8,11 @@
 //
 // Reduction order of the normal equations: the reference sums sequentially
 // (icp.cpp:19-27).  The canonical order used by the tracker (and by the GPU)
-// is "slot-tiled": slots are cut into tiles of kTile consecutive slots, each
-// tile is summed sequentially in slot order, tile partials are summed
-// sequentially within groups of kGroup consecutive tiles, and group totals
-// are summed sequentially in group order (the device sums a group as soon as
-// its last tile is done, so the cross-tile sum is a short chain).
+// is "slot-tiled" (tiled_normal_equations below: tiles of the strided slot
+// grid, 32 correspondence streams per tile combined by a fixed butterfly,
+// tiles summed in groups of kGroup).  The correspondence-list form
+// (normal_equations, csf_linearized_step) cuts the list into tiles of kTile
+// entries summed sequentially, the tiles in groups of kGroup.
 // normal_equations(..., sequential=true) keeps the reference's literal order
 // for the KAT pins.
 #pragma once
@@ -279,23 +279,58 @@ struct Ldlt6 {
   }
 };
 
-// Canonical slot-tiled normal equations over the strided slot grid.
+// Canonical tiling of the tracker's normal equations (builder-defined,
+// SURVEY H3; the device's k_icp_level / k_icp_reduce2, icp.cu):
+//   * the strided slot grid (row-major) is cut into at most kLevelMaxTiles
+//     tiles of T = 32 * ceil(n_slots / (32 * kLevelMaxTiles)) slots;
+//   * inside a tile the correspondences, in slot order, are dealt to 32
+//     streams (entry e of the tile to stream e mod 32), each summed
+//     sequentially from 0;
+//   * the 32 streams are combined by the fixed halving tree
+//     s[l] = s[l] + s[l + off] for off = 16, 8, 4, 2, 1 (l < off), i.e. lane
+//     0 of an xor butterfly;
+//   * tile partials are summed from 0 in tile order within groups of kGroup
+//     tiles, group totals from 0 in group order.
+constexpr int kLevelMaxTiles = 148;
+inline int icp_tile_slots(long long n_slots) {
+  const long long u = (n_slots + 32LL * kLevelMaxTiles - 1) / (32LL * kLevelMaxTiles);
+  return static_cast<int>(32 * (u > 0 ? u : 1));
+}
+
 template <typename S>
 NormalEq<S> tiled_normal_equations(const std::vector<CorrIndex>& idx, int width, int height, int stride,
                                    const SurfaceMaps<S>& measured, const SurfaceMaps<S>& predicted,
                                    const PoseT<S>& base) {
   const int nxs = (width + stride - 1) / stride;
   const int nys = (height + stride - 1) / stride;
-  const int n_slots = nxs * nys;
-  const int n_tiles = (n_slots + kTile - 1) / kTile;
+  const long long n_slots = static_cast<long long>(nxs) * nys;
+  const int T = icp_tile_slots(n_slots);
+  const int n_tiles = static_cast<int>((n_slots + T - 1) / T);
   std::vector<NormalEq<S>> partial(n_tiles);
-  for (const CorrIndex& c : idx) {
-    const int slot = (c.y / stride) * nxs + c.x / stride;
+  std::vector<NormalEq<S>> streams(32);
+  int cur = -1, entries = 0;
+  auto finish = [&]() {
+    if (cur < 0) return;
+    for (int off = 16; off > 0; off >>= 1)
+      for (int l = 0; l < off; ++l) add_into(streams[l], streams[l + off]);
+    partial[cur] = streams[0];
+    for (auto& st : streams) st = NormalEq<S>();
+  };
+  for (const CorrIndex& c : idx) {  // scan order == slot order
+    const long long slot = static_cast<long long>(c.y / stride) * nxs + c.x / stride;
+    const int t = static_cast<int>(slot / T);
+    if (t != cur) {
+      finish();
+      cur = t;
+      entries = 0;
+    }
     S j[6], r;
     jacobian_row<S>(measured.vertices.at(c.x, c.y), predicted.vertices.at(c.u, c.v), predicted.normals.at(c.u, c.v),
                     base, j, &r);
-    accumulate_row(partial[slot / kTile], j, r);
+    accumulate_row(streams[entries % 32], j, r);
+    ++entries;
   }
+  finish();
   NormalEq<S> total, group;
   for (int t = 0; t < n_tiles; ++t) {
     add_into(group, partial[t]);

@@ -356,6 +356,7 @@ inline PipelineResult run_pipeline_dyn(const PipelineConfig& cfg, const std::vec
     case 8: return run_pipeline<8>(cfg, frames, gt);
     case 10: return run_pipeline<10>(cfg, frames, gt);
     case 12: return run_pipeline<12>(cfg, frames, gt);
+    case 20: return run_pipeline<20>(cfg, frames, gt);
     default: throw std::invalid_argument("oracle pipeline: unsupported direction count");
   }
 }

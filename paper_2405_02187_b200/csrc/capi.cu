@@ -27,7 +27,6 @@
 #include "geometry.cuh"
 
 namespace csfi {
-void icp_clock_enable(unsigned long long* buf);
 int synth_workload(cudaStream_t stream, int config, int n_frames, int width, int height, float* depth_out,
                    double* gt_out, csf_intrinsics* k_out, std::string* err);
 int band_samples(double mu, double vs);
@@ -892,7 +891,6 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   p->levels = cfg->icp.levels;
   const size_t P = static_cast<size_t>(p->W) * p->H;
   const int C = p->C;
-  const int max_tiles = icp_tiles(p->W, p->H, 1);
   cudaError_t e = cudaSuccess;
   auto A = [&](cudaError_t r) {
     if (r != cudaSuccess && e == cudaSuccess) e = r;
@@ -907,8 +905,8 @@ extern "C" int csf_pipeline_create(csf_ctx ctx, const csf_pipeline_cfg* cfg, csf
   A(p->nre.alloc(P * 3));
   A(p->vim.alloc(P * 3 * std::max(p->Dp, 1)));
   A(p->nim.alloc(P * 3 * std::max(p->Dp, 1)));
-  A(p->partials.alloc(icp_partials_doubles(C, max_tiles)));
-  A(p->counts.alloc(icp_counts_ints(max_tiles)));
+  A(p->partials.alloc(icp_partials_doubles(C)));
+  A(p->counts.alloc(icp_counts_ints()));
   A(p->pose.alloc(12 * C));
   A(p->pred_pose.alloc(12 * C));
   A(p->intr_levels.alloc(3 * 4 * C));
@@ -1038,18 +1036,17 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
       launch_level_begin(L, st, p->pose.p, p->pred_pose.p, p->Dp);
       raycast_dev(v, p->pred_pose.p, kl, wl, hl, cfg.rc, p->hits.p, p->vre.p, p->nre.p, p->vim.p, p->nim.p);
       const int stride = std::max(1, cfg.icp.level_pixel_stride[li]);
-      const int tiles = icp_tiles(wl, hl, stride);
-      for (int it = 0; it < cfg.icp.level_iterations[li]; ++it) {
-        PROF(ctx, kPIcpReduce);
-        if (p->order == 2)
+      PROF(ctx, kPIcpReduce);
+      if (p->order == 2) {
+        for (int it = 0; it < cfg.icp.level_iterations[li]; ++it)
           launch_icp_iteration2(L, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p,
                                 p->vim.p, p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p, p->stage.p,
                                 level, cfg.icp.step_tolerance);
-        else
-          launch_icp_reduce(L, p->G, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p,
-                            p->vim.p, p->nim.p, cfg.icp.d_max, cos_max, p->partials.p, p->counts.p, level,
-                            cfg.icp.step_tolerance);
-        (void)tiles;
+      } else {
+        // every iteration of the level in one cooperative launch (breaks on the device)
+        launch_icp_level(L, p->Dp, st, pyr[level], wl, hl, stride, kl, p->pose.p, p->vre.p, p->nre.p, p->vim.p,
+                         p->nim.p, cfg.icp.d_max, cos_max, cfg.icp.level_iterations[li], level,
+                         cfg.icp.step_tolerance, p->partials.p, p->counts.p);
       }
     }
     if (cfg.keyframe_interval > 0 && f % cfg.keyframe_interval == 0 && p->order == 1)
@@ -1761,7 +1758,6 @@ static int track_frame_impl(csf_volume v, const double* depth, int w, int h, con
   DevBuf<int> counts;
   DevBuf<TrackState> st;
   DevBuf<double2> hits;
-  const int tiles_max = icp_tiles(w, h, 1);
   CUDA_TRY(ctx, hits.alloc(2 * P));
   CUDA_TRY(ctx, dd.alloc(P));
   CUDA_TRY(ctx, raw.alloc(P));
@@ -1773,8 +1769,8 @@ static int track_frame_impl(csf_volume v, const double* depth, int w, int h, con
   CUDA_TRY(ctx, pose.alloc(12));
   CUDA_TRY(ctx, pred.alloc(12));
   CUDA_TRY(ctx, intr.alloc(12));
-  CUDA_TRY(ctx, partials.alloc(icp_partials_doubles(1, tiles_max)));
-  CUDA_TRY(ctx, counts.alloc(icp_counts_ints(tiles_max)));
+  CUDA_TRY(ctx, partials.alloc(icp_partials_doubles(1)));
+  CUDA_TRY(ctx, counts.alloc(icp_counts_ints()));
   CUDA_TRY(ctx, st.alloc(1));
   CUDA_TRY(ctx, cudaMemsetAsync(counts.p, 0, sizeof(int) * counts.n, ctx->stream));
   double kl[12];
@@ -1850,8 +1846,8 @@ static int track_frame_impl(csf_volume v, const double* depth, int w, int h, con
       if (cfg.solver == CSF_SOLVER_LINEARIZED) {
         // canonical slot-tiled normal equations + the real LDLT step on the
         // device (the pipeline's kernels); loss_after = E(delta) (icp.cpp:36-47)
-        launch_icp_reduce(L, 0, 0, st.p, pyr[level], wl, hl, stride, kdev, pose.p, vre.p, nre.p, nullptr, nullptr,
-                          cfg.d_max, cos_max, partials.p, counts.p, level, cfg.step_tolerance);
+        launch_icp_level(L, 0, st.p, pyr[level], wl, hl, stride, kdev, pose.p, vre.p, nre.p, nullptr, nullptr,
+                         cfg.d_max, cos_max, 1, level, cfg.step_tolerance, partials.p, counts.p);
         TrackState hs;
         CUDA_TRY(ctx, d2h(&hs, st.p, sizeof(TrackState), ctx->stream));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1990,10 +1986,12 @@ extern "C" int csf_debug_march_stats(unsigned long long* host_out /*[8]*/, int e
   return CSF_OK;
 }
 
-// Debug hook (not part of the public header): per-CTA ICP phase timestamps.
+// Debug hook (not part of the public header): the ICP level kernel's
+// per-CTA phase timeline (64 launches x 256 CTAs x 32 iterations x 16 phases).
+namespace csfi { void icp_clock_enable(unsigned long long* buf); }
 extern "C" int csf_debug_icp_clock(unsigned long long* host_out, int enable) {
   static unsigned long long* dbuf = nullptr;
-  const size_t n = size_t(4096) * 512 * 8;
+  const size_t n = size_t(64) * 256 * 32 * 16;
   if (enable) {
     if (!dbuf && cudaMalloc(&dbuf, n * sizeof(unsigned long long)) != cudaSuccess) return CSF_ENOMEM;
     cudaMemset(dbuf, 0, n * sizeof(unsigned long long));

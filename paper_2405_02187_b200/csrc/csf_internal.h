@@ -71,6 +71,18 @@ struct AllocScratch {
   int max_cand;                 // P*K
 };
 
+// ---- canonical ICP tiling (builder-defined; oracle/orc_icp.hpp restates it)
+// The strided slot grid of a level is cut into at most kIcpMaxTiles tiles of
+// a multiple of 32 consecutive slots; the level kernel runs one CTA of
+// 32 * kIcpLevelWarps threads per tile, one CTA per SM (148 SMs on B200).
+constexpr int kIcpLevelWarps = 16;
+constexpr int kIcpMaxTiles = 148;
+constexpr int kIcpGroup = 16;  // tiles per group of the cross-tile sum
+inline int icp_tile_slots(long long n_slots) {
+  const long long u = (n_slots + 32LL * kIcpMaxTiles - 1) / (32LL * kIcpMaxTiles);
+  return static_cast<int>(32 * (u > 0 ? u : 1));
+}
+
 // Tracker state (device)
 struct TrackState {
   int level_done;
@@ -84,6 +96,27 @@ struct TrackState {
   double cur_c2w[12];   // real current pose snapshot (unused by kernels)
   double delta[6];      // real increment of the last solved ICP iteration
   double b[6];          // its real J^T r (the linearized solver's gradient / 2, icp.cpp:41)
+};
+
+// Arguments of the first-order ICP level kernel (icp.cu).
+struct IcpLevelArgs {
+  TrackState* st;
+  const double* depth;
+  int w, h, stride;
+  const double* intr;  // [4][1+Dp] level intrinsics
+  double* pose;        // [12][1+Dp] current pose (in / out)
+  const double *vre, *nre, *vim, *nim;
+  double d_max, cos_max;
+  int Dp;
+  int iterations;
+  int level;
+  double tol;
+  int tile_slots, n_tiles;
+  double* partials;   // [kIcpMaxTiles][27(1+Dp)]
+  double* gpartials;  // [groups][27(1+Dp)]
+  double* totals;     // [27(1+Dp)]
+  int* counts;        // tiles, groups, total
+  unsigned* sync;     // group counters, total counter, release generation
 };
 
 // ---- energy.cu: icp_energy / gradient / Hessian and the correspondence list
@@ -228,16 +261,18 @@ int icp_tiles(int w, int h, int stride);
 // Whether a w x h frame at this pixel stride fits the ICP reduction's group
 // counters (callers reject larger frames with CSF_EINVAL).
 bool icp_frame_fits(int w, int h, int stride);
-// ICP scratch sizes for frames of up to max_tiles tiles (icp_tiles at stride 1);
-// the counts buffer must be zeroed once at allocation.
-size_t icp_partials_doubles(int C, int max_tiles);
-size_t icp_counts_ints(int max_tiles);
-// One ICP iteration: association + lifted normal equations per tile, and the
-// last CTA solves and updates the pose (TrackState::pad[0] is its counter).
-void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const double* depth, int w, int h,
-                       int stride, const double* intr, double* pose, const double* vre, const double* nre,
-                       const double* vim, const double* nim, double d_max, double cos_max, double* partials,
-                       int* counts, int level, double tol);
+// ICP scratch (level kernel and second-order reduce); the counts buffer must
+// be zeroed once at allocation.
+size_t icp_partials_doubles(int C);
+size_t icp_counts_ints();
+// All iterations of one ICP pyramid level (icp.cpp:193-238) in one
+// cooperative launch: association, lifted normal equations, the 6x6 solve
+// and the pose update per iteration; the level's break rules on the device.
+// Updates pose and TrackState (iterations, n_corr, converged, delta, b).
+void launch_icp_level(const Launch& L, int Dp, TrackState* st, const double* depth, int w, int h, int stride,
+                      const double* intr, double* pose, const double* vre, const double* nre, const double* vim,
+                      const double* nim, double d_max, double cos_max, int iterations, int level, double tol,
+                      double* partials, int* counts);
 void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,
                  const double* intr_base, double* pose, double* intr_levels, int levels);
 void launch_frame_begin(const Launch& L, TrackState* st, int frame);

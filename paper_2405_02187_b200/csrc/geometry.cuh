@@ -591,11 +591,19 @@ CSF_DEV bool vertex_at(const double* depth, int w, int x, int y, double fx, doub
 CSF_DEV bool associate_slot(const double* __restrict__ depth, int w, int h, int x, int y, double fx, double fy,
                             double cx, double cy, const Pose<double>& c2w, const Pose<double>& w2p,
                             const double* __restrict__ vre, const double* __restrict__ nre, double d_max,
-                            double cos_max, int* u_out, int* v_out) {
-  V3<double> vert, vx, vy;
-  if (!(vertex_at(depth, w, x, y, fx, fy, cx, cy, &vert) && x + 1 < w && y + 1 < h &&
-        vertex_at(depth, w, x + 1, y, fx, fy, cx, cy, &vx) && vertex_at(depth, w, x, y + 1, fx, fy, cx, cy, &vy)))
-    return false;
+                            double cos_max, int* u_out, int* v_out, double* mv_out = nullptr,
+                            double* mn_out = nullptr) {
+  // the three depths are fetched together (one memory round trip), then the
+  // validity tests run in the reference's order
+  const double d0 = depth[y * w + x];
+  const double d1 = x + 1 < w ? depth[y * w + x + 1] : 0.0;
+  const double d2 = y + 1 < h ? depth[(y + 1) * w + x] : 0.0;
+  if (!(d0 > 0.0 && x + 1 < w && y + 1 < h && d1 > 0.0 && d2 > 0.0)) return false;
+  const double tx0 = static_cast<double>(x) - cx, tx1 = static_cast<double>(x + 1) - cx;
+  const double ty0 = static_cast<double>(y) - cy, ty1 = static_cast<double>(y + 1) - cy;
+  const V3<double> vert = mk3<double>(d0 * tx0 / fx, d0 * ty0 / fy, d0);
+  const V3<double> vx = mk3<double>(d1 * tx1 / fx, d1 * ty0 / fy, d1);
+  const V3<double> vy = mk3<double>(d2 * tx0 / fx, d2 * ty1 / fy, d2);
   V3<double> n = cross3(sub3(vx, vert), sub3(vy, vert));
   const double len2 = dot3(n, n);
   if (!(len2 > 0.0)) return false;
@@ -612,15 +620,23 @@ CSF_DEV bool associate_slot(const double* __restrict__ depth, int w, int h, int 
   const int v = static_cast<int>(lround(uvy));
   if (!(u >= 0 && u < w && v >= 0 && v < h)) return false;
   const long long m = static_cast<long long>(v) * w + u;
+  // both model values are loaded together (one memory round trip); the
+  // tests keep the reference's order (normal valid, then distance)
   const V3<double> mn = mk3<double>(nre[3 * m], nre[3 * m + 1], nre[3 * m + 2]);
-  if (!(dot3(mn, mn) > 0.5)) return false;
   const V3<double> mv = mk3<double>(vre[3 * m], vre[3 * m + 1], vre[3 * m + 2]);
+  if (!(dot3(mn, mn) > 0.5)) return false;
   const V3<double> dd = sub3(world, mv);
   if (sqrt(dot3(dd, dd)) > d_max) return false;
   const V3<double> wn = matvec(c2w.R, n);
   if (dot3(wn, mn) < cos_max) return false;
   *u_out = u;
   *v_out = v;
+  if (mv_out)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mv_out[k] = mv.v[k];
+  if (mn_out)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mn_out[k] = mn.v[k];
   return true;
 }
 

@@ -26,30 +26,53 @@
 namespace csfd {
 
 using csfi::TrackState;
-constexpr int kTile = 256;
+using csfi::IcpLevelArgs;
 
-// Optional phase timing (tools/icp_timing.py): per launch, per CTA
-// [start, after association/J, after sums, solve start, solve end] in ns.
-__device__ unsigned long long* g_icp_clock = nullptr;
-__device__ unsigned g_icp_clock_launch = 0;
-CSF_DEV unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-CSF_DEV void clock_mark(int slot, int cta = -1) {
-  if (g_icp_clock && threadIdx.x == 0 && g_icp_clock_launch < 4096)
-    g_icp_clock[(static_cast<unsigned long long>(g_icp_clock_launch) * 512 + (cta < 0 ? blockIdx.x : cta)) * 8 + slot] =
-        gtimer();
-}
-// the solve kernel records into CTA slot 511 of the iteration's record
-constexpr int kSolveClockCta = 511;
+// ============================================================================
+// First-order ICP: one cooperative launch per pyramid level runs every
+// iteration of the level (icp.cpp:193-238) without returning to the host.
+//
+// Grid = the level's tiles (<= kLvMaxTiles, co-resident at 2 CTAs per SM).
+// Per iteration every CTA
+//   A  associates its tile's slots (icp.cpp:89-126, real-part gates) and
+//      compacts the correspondences, in slot order, into shared-memory
+//      records of the real row and the real intermediates its channels need;
+//   B  accumulates the normal equations (icp.cpp:15-28): warp w owns channel
+//      c = w (+ 11 p), lane l the correspondence stream e = l (mod 32);
+//      the real channel adds re(J_a) re(J_b) in plain double (bit-exact with
+//      the oracle), every perturbation channel the truncated-Complex product
+//      term re(J_a) im(J_b) + im(J_a) re(J_b) (csfd.hpp:50-53);
+//   C  reduces the 32 streams with a fixed xor butterfly and writes its tile
+//      partial; the last CTA of each group of kLvGroup tiles sums the group
+//      in tile order, the last group sums the groups in order and releases
+//      the grid barrier;
+//   D  every CTA solves the same 6x6 system redundantly from the totals (the
+//      real LDLT in the oracle's Ldlt6 order, channels in tangent form
+//      against the real factors), applies exp(delta) T per channel and takes
+//      the break decisions (icp.cpp:199,235) — identical bits in every CTA,
+//      so no second barrier is needed.
+// The canonical order of the real sums (tile size, streams, butterfly, groups)
+// is builder-defined and restated in oracle/orc_icp.hpp.
+// ============================================================================
+constexpr int kLvWarps = csfi::kIcpLevelWarps;
+constexpr int kLvThreads = 32 * kLvWarps;
+constexpr int kRounds = 2;                         // slots per thread in one association pass
+constexpr int kSegSlots = 576;                     // slots per shared-memory record segment (a VGA tile is 544)
+static_assert(kSegSlots <= kRounds * kLvThreads, "one association pass covers a segment");
+constexpr int kLvMaxTiles = csfi::kIcpMaxTiles;
+constexpr int kLvGroup = csfi::kIcpGroup;
+constexpr int kLvMaxGroups = (kLvMaxTiles + kLvGroup - 1) / kLvGroup;
+constexpr int kMaxC = 1 + 64;  // CSF_MAX_DIRECTIONS
+// Barrier words: group counters and the total counter share one line; the
+// release generation that every CTA polls sits 256 bytes away, so the polls
+// never queue in front of the counters' atomics in the same L2 line.
+constexpr int kFlagWord = 64;
 
-// 256 threads evaluate the tile's slots; all 320 sum accumulators (27*(1+Dp)
-// of them, one per thread up to Dp = 10), so no thread carries two.
-constexpr int kRedThreads = 320;
-__constant__ int c_tri_r[21] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5, 5, 5, 5};
-__constant__ int c_tri_c[21] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2, 3, 4, 5};
+// shared-memory record fields of one correspondence (structure of arrays)
+enum RecField : int {
+  kRD = 0, kRNX, kRNY, kRV0, kRV1, kRP0, kRP1, kRP2, kRDF0, kRDF1, kRDF2,
+  kRMN0, kRMN1, kRMN2, kRPN0, kRPN1, kRPN2, kRRR, kRecFields
+};
 
 CSF_DEV void load_pose_real(const double* p, int C, Pose<double>* out) {
 #pragma unroll
@@ -58,412 +81,763 @@ CSF_DEV void load_pose_real(const double* p, int C, Pose<double>* out) {
   for (int e = 0; e < 3; ++e) out->t.v[e] = p[(9 + e) * C];
 }
 
-
-
-// Canonical two-level cross-tile order (oracle/orc_icp.hpp, kGroup): the
-// last CTA to finish within a group of kGroup consecutive tiles sums the
-// group's tile partials in tile order into gpartials[group]; the solve then
-// sums the (few) group totals in group order.  Called by every CTA after it
-// wrote its own tile partials.
-constexpr int kGroup = 16;
-constexpr int kMaxGroupCtr = 256;  // tiles per launch <= kGroup * kMaxGroupCtr
-CSF_DEV bool group_sum(const double* __restrict__ partials, const int* __restrict__ counts, int n_acc,
-                       double* __restrict__ gpartials, int* __restrict__ gcounts, unsigned* __restrict__ group_ctr) {
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  const int grp = blockIdx.x / kGroup;
-  const int first = grp * kGroup;
-  const int gn = min(kGroup, static_cast<int>(gridDim.x) - first);
-  if (threadIdx.x == 0) s_last = atomicAdd(group_ctr + grp, 1u) == static_cast<unsigned>(gn - 1);
-  __syncthreads();
-  if (!s_last) return false;
-  if (threadIdx.x == 0) group_ctr[grp] = 0u;  // ready for the next launch
-  __threadfence();
-  for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
-    double v[kGroup];
-#pragma unroll
-    for (int u = 0; u < kGroup; ++u)
-      v[u] = u < gn ? __ldcg(partials + static_cast<long long>(first + u) * n_acc + a) : 0.0;
-    double total = 0.0;
-#pragma unroll
-    for (int u = 0; u < kGroup; ++u)
-      if (u < gn) total = total + v[u];
-    gpartials[static_cast<long long>(grp) * n_acc + a] = total;
-  }
-  if (threadIdx.x < 32) {
-    int c = static_cast<int>(threadIdx.x) < gn ? __ldcg(counts + first + threadIdx.x) : 0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
-    if (threadIdx.x == 0) gcounts[grp] = c;
-  }
-  return true;
+// (row a, row b) of accumulator q: 21 lower-triangle entries of J J^T, then
+// the 6 entries of J r (row b = 6, the residual).
+CSF_HD constexpr int acc_row_a(int q) {
+  return q < 21 ? (q < 1 ? 0 : q < 3 ? 1 : q < 6 ? 2 : q < 10 ? 3 : q < 15 ? 4 : 5) : q - 21;
+}
+CSF_HD constexpr int acc_row_b(int q) {
+  return q < 21 ? q - (acc_row_a(q) * (acc_row_a(q) + 1)) / 2 : 6;
 }
 
-// The solve of one ICP iteration (one CTA): group totals in group order, then
-// the real 6x6 LDLT once (thread 0, the oracle's Ldlt6 order, bit-identical
-// real step) and every perturbation channel in tangent form against the real
-// factors, d.im = A^-1 (nb.im - A.im d.re) — the first-order quantity the
-// truncated-Complex LDLT computes, ~1 ulp per operation apart.  Degenerate
-// systems (zero or sub-normal pivots) take the per-channel lifted LDLT
-// instead.  Then exp(delta) * T per channel thread (L<1>) and the break
-// decisions (icp.cpp:199,235) into TrackState.
-constexpr int kMaxC = 1 + 64;  // CSF_MAX_DIRECTIONS
-__device__ __noinline__ void icp_solve_body(TrackState* st, const double* __restrict__ gpartials,
-                                            const int* __restrict__ gcounts, int n_groups, double* pose, int Dp,
-                                            int level, double tol) {
-  __shared__ double s_acc[27 * kMaxC];
-  __shared__ double s_m[36], s_x[6];
-  __shared__ int s_tr[6];
-  __shared__ int s_n, s_degen, s_finite;
-  const int C = 1 + Dp;
-  const int n_acc = 27 * C;
-  clock_mark(3, kSolveClockCta);
-  for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
-    double v[32];
-    double total = 0.0;
-    for (int g0 = 0; g0 < n_groups; g0 += 32) {
+// The measured side of phase A — the vertex and normal of every slot of a
+// segment (measure_surface, frames.hpp:86-114, recomputed from the pyramid
+// depth) — does not depend on the pose, so it is computed once per level
+// (per segment visit for multi-segment tiles) into s_meas[6][kSegSlots];
+// an invalid slot stores vertex z = 0.  Every division / sqrt runs on valid
+// data only (a zero or NaN operand sends the IEEE division down its slow path).
+__device__ __noinline__ void level_measure(const IcpLevelArgs& a, int seg0, int seg1, const double* s_intr,
+                                           double* s_meas) {
+  const int C = 1 + a.Dp;
+  const int nxs = (a.w + a.stride - 1) / a.stride;
+  const int w = a.w, h = a.h;
+  const double fx = s_intr[0], fy = s_intr[C], cx = s_intr[2 * C], cy = s_intr[3 * C];
+  bool ok[kRounds];
+  int xs[kRounds], ys[kRounds];
+  double d0[kRounds], d1[kRounds], d2[kRounds];
 #pragma unroll
-      for (int u = 0; u < 32; ++u)
-        v[u] = g0 + u < n_groups ? __ldcg(gpartials + static_cast<long long>(g0 + u) * n_acc + a) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 32; ++u)
-        if (g0 + u < n_groups) total = total + v[u];
-    }
-    s_acc[a] = total;
+  for (int r = 0; r < kRounds; ++r) {
+    const int slot = seg0 + r * kLvThreads + static_cast<int>(threadIdx.x);
+    ok[r] = slot < seg1;  // seg1 <= seg0 + kSegSlots
+    xs[r] = ok[r] ? (slot % nxs) * a.stride : 0;
+    ys[r] = ok[r] ? (slot / nxs) * a.stride : 0;
+    const int x = xs[r], y = ys[r];
+    d0[r] = ok[r] ? a.depth[y * w + x] : 0.0;
+    d1[r] = ok[r] && x + 1 < w ? a.depth[y * w + x + 1] : 0.0;
+    d2[r] = ok[r] && y + 1 < h ? a.depth[(y + 1) * w + x] : 0.0;
   }
-  if (threadIdx.x < 32) {
-    int c = 0;
-    for (int g = threadIdx.x; g < n_groups; g += 32) c += __ldcg(gcounts + g);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
-    if (threadIdx.x == 0) {
-      s_n = c;
-      s_finite = 1;
+  for (int r = 0; r < kRounds; ++r) {
+    const int e = r * kLvThreads + static_cast<int>(threadIdx.x);
+    if (e >= kSegSlots) continue;
+    const int x = xs[r], y = ys[r];
+    bool valid = ok[r] && d0[r] > 0.0 && x + 1 < w && y + 1 < h && d1[r] > 0.0 && d2[r] > 0.0;
+    V3<double> vert = mk3<double>(0.0, 0.0, 0.0), n = mk3<double>(0.0, 0.0, 0.0);
+    if (valid) {
+      const double tx0 = static_cast<double>(x) - cx, tx1 = static_cast<double>(x + 1) - cx;
+      const double ty0 = static_cast<double>(y) - cy, ty1 = static_cast<double>(y + 1) - cy;
+      vert = mk3<double>(d0[r] * tx0 / fx, d0[r] * ty0 / fy, d0[r]);
+      const V3<double> vx = mk3<double>(d1[r] * tx1 / fx, d1[r] * ty0 / fy, d1[r]);
+      const V3<double> vy = mk3<double>(d2[r] * tx0 / fx, d2[r] * ty1 / fy, d2[r]);
+      n = cross3(sub3(vx, vert), sub3(vy, vert));
+      const double len2 = dot3(n, n);
+      valid = len2 > 0.0;
+      if (valid) {
+        const double l = sqrt(len2);
+        n = mk3<double>(n.v[0] / l, n.v[1] / l, n.v[2] / l);
+        if (dot3(n, vert) > 0.0) n = mk3<double>(-n.v[0], -n.v[1], -n.v[2]);
+        valid = dot3(n, n) > 0.5;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      s_meas[k * kSegSlots + e] = vert.v[k];
+      s_meas[(3 + k) * kSegSlots + e] = n.v[k];
+    }
+    if (!valid) s_meas[2 * kSegSlots + e] = 0.0;
+  }
+}
+
+// Phase A (pose-dependent part) over one segment, kRounds slots per thread
+// with every round's model loads in flight together: the association of
+// icp.cpp:89-126 for each slot — the same operations as associate_slot
+// (geometry.cuh) on the measured vertex/normal of level_measure, whose tests
+// carry no side effects, so evaluating all of them and combining gives the
+// reference's answer — then the slot-order compaction of the correspondences
+// into the shared-memory records.  Returns the segment's correspondence count.
+__device__ __noinline__ int level_associate(const IcpLevelArgs& a, int seg0, int seg1, const double* s_pose,
+                                            const double* s_intr, const Pose<double>& w2p, const double* s_meas,
+                                            double* s_rec, int* s_m, int* s_wsum) {
+  const int C = 1 + a.Dp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nxs = (a.w + a.stride - 1) / a.stride;
+  const int w = a.w, h = a.h;
+  const double fx = s_intr[0], fy = s_intr[C], cx = s_intr[2 * C], cy = s_intr[3 * C];
+  Pose<double> c2w;
+  load_pose_real(s_pose, C, &c2w);
+  bool ok[kRounds];
+  int xs[kRounds], ys[kRounds];
+  double d0[kRounds];
+  V3<double> world[kRounds], nrm[kRounds];
+  long long mi[kRounds];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int e = r * kLvThreads + static_cast<int>(threadIdx.x);
+    const int slot = seg0 + e;
+    ok[r] = slot < seg1 && e < kSegSlots;
+    xs[r] = ok[r] ? (slot % nxs) * a.stride : 0;
+    ys[r] = ok[r] ? (slot / nxs) * a.stride : 0;
+    d0[r] = ok[r] ? s_meas[2 * kSegSlots + e] : 0.0;
+    ok[r] = ok[r] && d0[r] > 0.0;
+    mi[r] = 0;
+    if (ok[r]) {
+      const V3<double> vert = mk3<double>(s_meas[e], s_meas[kSegSlots + e], d0[r]);
+      nrm[r] = mk3<double>(s_meas[3 * kSegSlots + e], s_meas[4 * kSegSlots + e], s_meas[5 * kSegSlots + e]);
+      world[r] = apply(c2w, vert);
+      const V3<double> inp = apply(w2p, world[r]);
+      ok[r] = inp.v[2] > 0.0;
+      if (ok[r]) {
+        const double uvx = (fx * inp.v[0]) / inp.v[2] + cx;
+        const double uvy = (fy * inp.v[1]) / inp.v[2] + cy;
+        const long long u = llround(uvx), v = llround(uvy);
+        ok[r] = u >= 0 && u < w && v >= 0 && v < h;
+        mi[r] = ok[r] ? v * w + u : 0;
+      }
     }
   }
-  __syncthreads();
-  clock_mark(5, kSolveClockCta);
-  const int n = s_n;
-  if (n < 12) {
-    if (threadIdx.x == 0) {
-      st->n_corr = n;
-      st->level_done = 1;
-      if (g_icp_clock) atomicAdd(&g_icp_clock_launch, 1u);
+  double MV[kRounds][3], MN[kRounds][3];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      MN[r][k] = ok[r] ? a.nre[3 * mi[r] + k] : 0.0;
+      MV[r][k] = ok[r] ? a.vre[3 * mi[r] + k] : 0.0;
+    }
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    if (!ok[r]) continue;
+    const V3<double> mn = mk3<double>(MN[r][0], MN[r][1], MN[r][2]);
+    const V3<double> mv = mk3<double>(MV[r][0], MV[r][1], MV[r][2]);
+    ok[r] = dot3(mn, mn) > 0.5;
+    const V3<double> dd = sub3(world[r], mv);
+    ok[r] = ok[r] && !(sqrt(dot3(dd, dd)) > a.d_max);
+    const V3<double> wn = matvec(c2w.R, nrm[r]);
+    ok[r] = ok[r] && !(dot3(wn, mn) < a.cos_max);
+  }
+  // slot-order compaction, round by round
+  int total = 0;
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const unsigned ballot = __ballot_sync(0xffffffffu, ok[r]);
+    if (lane == 0) s_wsum[r * kLvWarps + warp] = __popc(ballot);
+    __syncthreads();
+    int before = 0, rtotal = 0;
+#pragma unroll
+    for (int k = 0; k < kLvWarps; ++k) {
+      const int c = s_wsum[r * kLvWarps + k];
+      if (k < warp) before += c;
+      rtotal += c;
+    }
+    if (ok[r]) {
+      // the real row of normal_equations (icp.cpp:20-24): vertex =
+      // backproject(K, x, y, d) (frames.hpp:38-41), p = base * vertex,
+      // r = (p - mv) . mn, J = [mn; p x mn] — the oracle's operation order
+      const int e = total + before + __popc(ballot & ((1u << lane) - 1u));
+      const int x = xs[r], y = ys[r];
+      const int sl = r * kLvThreads + static_cast<int>(threadIdx.x);
+      const double d = d0[r];
+      const double nx = d * (static_cast<double>(x) - cx), ny = d * (static_cast<double>(y) - cy);
+      const double vv[3] = {s_meas[sl], s_meas[kSegSlots + sl], d};  // (nx / fx, ny / fy, d)
+      double P[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const double p0 = c2w.R.m[3 * q] * vv[0], p1 = c2w.R.m[3 * q + 1] * vv[1], p2 = c2w.R.m[3 * q + 2] * vv[2];
+        P[q] = (p0 + (p1 + p2)) + c2w.t.v[q];
+      }
+      const double DF[3] = {P[0] - MV[r][0], P[1] - MV[r][1], P[2] - MV[r][2]};
+      double* rec = s_rec + e;
+      rec[kRD * kSegSlots] = d;
+      rec[kRNX * kSegSlots] = nx;
+      rec[kRNY * kSegSlots] = ny;
+      rec[kRV0 * kSegSlots] = vv[0];
+      rec[kRV1 * kSegSlots] = vv[1];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        rec[(kRP0 + q) * kSegSlots] = P[q];
+        rec[(kRDF0 + q) * kSegSlots] = DF[q];
+        rec[(kRMN0 + q) * kSegSlots] = MN[r][q];
+      }
+      rec[kRPN0 * kSegSlots] = P[1] * MN[r][2] - P[2] * MN[r][1];
+      rec[kRPN1 * kSegSlots] = P[2] * MN[r][0] - P[0] * MN[r][2];
+      rec[kRPN2 * kSegSlots] = P[0] * MN[r][1] - P[1] * MN[r][0];
+      rec[kRRR * kSegSlots] = DF[0] * MN[r][0] + (DF[1] * MN[r][1] + DF[2] * MN[r][2]);
+      s_m[e] = static_cast<int>(mi[r]);
+      if (a.Dp > 0) {
+        // the channel warps of phase B read this pixel's model channels
+        // (3 Dp contiguous doubles in each map): start their L1 fills now
+        const double* pv = a.vim + 3 * mi[r] * a.Dp;
+        const double* pn = a.nim + 3 * mi[r] * a.Dp;
+        for (int o = 0; o < 3 * a.Dp; o += 16) {
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(pv + o));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(pn + o));
+        }
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pv + 3 * a.Dp - 1));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pn + 3 * a.Dp - 1));
+      }
+    }
+    total += rtotal;
+  }
+  return total;
+}
+
+// Phase B: lane `lane` of the warp owning channel c accumulates its stream's
+// entries (global entry index = lane mod 32) among [e0, e0 + n).
+CSF_DEV void level_accumulate(const IcpLevelArgs& a, int c, int ebase, int e0, int n, const double* s_pose,
+                              const double* s_intr, const double* s_rec, const int* s_m, double (&acc)[27]) {
+  const int lane = threadIdx.x & 31;
+  const int C = 1 + a.Dp;
+  const int first = (lane - ((ebase + e0) & 31) + 32) & 31;
+  if (c == 0) {
+    for (int e = e0 + first; e < e0 + n; e += 32) {
+      double row[7];
+      row[0] = s_rec[kRMN0 * kSegSlots + e];
+      row[1] = s_rec[kRMN1 * kSegSlots + e];
+      row[2] = s_rec[kRMN2 * kSegSlots + e];
+      row[3] = s_rec[kRPN0 * kSegSlots + e];
+      row[4] = s_rec[kRPN1 * kSegSlots + e];
+      row[5] = s_rec[kRPN2 * kSegSlots + e];
+      row[6] = s_rec[kRRR * kSegSlots + e];
+#pragma unroll
+      for (int q = 0; q < 27; ++q) acc[q] = acc[q] + row[acc_row_a(q)] * row[acc_row_b(q)];
     }
     return;
   }
-  if (threadIdx.x == 0) {
-    double a[21], nb[6], m[6][6], x[6];
-    int tr[6];
+  // perturbation channel c: the truncated-Complex rule of every operation of
+  // the row (csfd.hpp:44-58) applied to the saved real intermediates
+  const double kfx = s_intr[0], kfy = s_intr[C];
+  const double fxc = s_intr[c], fyc = s_intr[C + c], cxc = s_intr[2 * C + c], cyc = s_intr[3 * C + c];
+  const double ifx = 1.0 / (kfx * kfx), ify = 1.0 / (kfy * kfy);
+  (void)ifx;
+  (void)ify;
+  const int Dp = a.Dp;
+  for (int e = e0 + first; e < e0 + n; e += 32) {
+    // the model-map channels of the correspondence (prefetched into L1 by phase A)
+    const long long m = s_m[e];
+    double MVi[3], MNi[3];
 #pragma unroll
-    for (int q = 0; q < 21; ++q) a[q] = s_acc[q * C];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) nb[i] = -s_acc[(21 + i) * C];
-    bool degen = false;
-    ldlt6_factor_reg<double>(a, m, tr, &degen);
-    ldlt6_apply_reg<double>(m, tr, nb, x);
-#pragma unroll
-    for (int r = 0; r < 6; ++r)
-#pragma unroll
-      for (int c = 0; c < 6; ++c) s_m[6 * r + c] = m[r][c];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      s_tr[i] = tr[i];
-      s_x[i] = x[i];
+    for (int k = 0; k < 3; ++k) {
+      MVi[k] = __ldg(a.vim + (3 * m + k) * Dp + c - 1);
+      MNi[k] = __ldg(a.nim + (3 * m + k) * Dp + c - 1);
     }
-    s_degen = degen;
+    const double d = s_rec[kRD * kSegSlots + e];
+    const double vv[3] = {s_rec[kRV0 * kSegSlots + e], s_rec[kRV1 * kSegSlots + e], d};
+    const double tnx = d * -cxc, tny = d * -cyc;
+    const double vi[3] = {CSF_CH_DIV(__fma_rn(tnx, kfx, -s_rec[kRNX * kSegSlots + e] * fxc), kfx * kfx, ifx),
+                          CSF_CH_DIV(__fma_rn(tny, kfy, -s_rec[kRNY * kSegSlots + e] * fyc), kfy * kfy, ify), 0.0};
+    double P[3], DF[3], MN[3], Pi[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      P[r] = s_rec[(kRP0 + r) * kSegSlots + e];
+      DF[r] = s_rec[(kRDF0 + r) * kSegSlots + e];
+      MN[r] = s_rec[(kRMN0 + r) * kSegSlots + e];
+      double qi[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) qi[k] = __fma_rn(s_pose[(3 * r + k) * C], vi[k], s_pose[(3 * r + k) * C + c] * vv[k]);
+      Pi[r] = (qi[0] + (qi[1] + qi[2])) + s_pose[(9 + r) * C + c];
+    }
+    const double DFi[3] = {Pi[0] - MVi[0], Pi[1] - MVi[1], Pi[2] - MVi[2]};
+    double ti[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ti[k] = __fma_rn(DF[k], MNi[k], DFi[k] * MN[k]);
+    double ch[7], row[7];
+    ch[0] = MNi[0];
+    ch[1] = MNi[1];
+    ch[2] = MNi[2];
+    ch[3] = __fma_rn(P[1], MNi[2], Pi[1] * MN[2]) - __fma_rn(P[2], MNi[1], Pi[2] * MN[1]);
+    ch[4] = __fma_rn(P[2], MNi[0], Pi[2] * MN[0]) - __fma_rn(P[0], MNi[2], Pi[0] * MN[2]);
+    ch[5] = __fma_rn(P[0], MNi[1], Pi[0] * MN[1]) - __fma_rn(P[1], MNi[0], Pi[1] * MN[0]);
+    ch[6] = ti[0] + (ti[1] + ti[2]);
+    row[0] = MN[0];
+    row[1] = MN[1];
+    row[2] = MN[2];
+    row[3] = s_rec[kRPN0 * kSegSlots + e];
+    row[4] = s_rec[kRPN1 * kSegSlots + e];
+    row[5] = s_rec[kRPN2 * kSegSlots + e];
+    row[6] = s_rec[kRRR * kSegSlots + e];
+#pragma unroll
+    for (int q = 0; q < 27; ++q)
+      acc[q] = __fma_rn(row[acc_row_a(q)], ch[acc_row_b(q)], __fma_rn(ch[acc_row_a(q)], row[acc_row_b(q)], acc[q]));
   }
+}
+
+// Grid barrier of the level kernel: the CTA that completes the last group
+// publishes generation `gen`; everyone waits for it.
+CSF_DEV void release_gen(unsigned* flag, unsigned gen) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(gen) : "memory");
+}
+CSF_DEV unsigned acquire_gen(const unsigned* flag) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  return v;
+}
+// The spin itself polls with relaxed loads (an acquire load invalidates the
+// SM's L1 on every poll, which evicts the co-resident CTA's cached gathers
+// and spills); one acquire fence follows the successful poll.
+CSF_DEV unsigned poll_gen(const unsigned* flag) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  return v;
+}
+CSF_DEV void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+CSF_DEV unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Degenerate real factorization: the channel's own lifted LDLT (rare path,
+// kept out of the solve's register budget).
+__device__ __noinline__ void solve_channel_lifted(const double* s_tot, int C, int t, L<1> (&d)[6]) {
+  L<1> am[21], nb[6];
+#pragma unroll
+  for (int q = 0; q < 21; ++q) am[q] = load_ch<L<1>>(s_tot + q * C, t, 1);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) nb[i] = -load_ch<L<1>>(s_tot + (21 + i) * C, t, 1);
+  ldlt6_solve_reg<L<1>>(am, nb, d);
+}
+__device__ __noinline__ void increment_pose(const L<1> (&d)[6], const Pose<L<1>>& cur, Pose<L<1>>* out) {
+  *out = compose(exp_map<L<1>>(d), cur);
+}
+
+// Phase D of k_icp_level: the 6x6 solve from the totals (every CTA, same
+// bits).  The real LDLT runs lane-parallel in warp 0 — lane tri(r, c) holds
+// m[r][c] of the lower triangle and performs exactly the operations the
+// oracle's Ldlt6 (orc_icp.hpp, Eigen::LDLT's order) performs on that element:
+// the pivot search on the diagonal, the symmetric transposition (a lane
+// permutation: m'[r][c] = m[s(r)][s(c)]), the column update with the
+// sequential dot product, the division by the pivot.  Then every channel
+// thread applies the factors: the real step d.re (identical in every
+// thread) and the channel in tangent form d.im = A^-1 (nb.im - A.im d.re)
+// (the per-channel lifted LDLT for degenerate systems); delta is zeroed
+// unless every channel is finite (delta.allFinite(), icp.cpp:45); then
+// exp(delta) * T per channel thread (apply_increment, se3.hpp:116-119) and the
+// step-tolerance break (icp.cpp:235).  dre: the real delta (thread 0).
+CSF_DEV void lv_mark(unsigned seq, int it, int phase);
+struct LevelSolveShared {
+  double fm[36];  // factors, row-major (lower triangle and diagonal)
+  int ftr[6];
+  int degen, finite, done, conv;
+};
+
+CSF_HD constexpr int tri_row(int l) { return l < 1 ? 0 : l < 3 ? 1 : l < 6 ? 2 : l < 10 ? 3 : l < 15 ? 4 : 5; }
+
+__device__ __noinline__ void ldlt6_warp(const double* a_lower, int stride, LevelSolveShared* ls) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int l = lane < 21 ? lane : 0;
+  const int r = tri_row(l), c = l - r * (r + 1) / 2;
+  const bool col_lane = lane < 21;
+  double v = col_lane ? a_lower[l * stride] : 0.0;
+  bool ok = true, stop = false, degen = false;
+  int transp[6] = {0, 1, 2, 3, 4, 5};
+#pragma unroll 1
+  for (int k = 0; k < 6; ++k) {
+    if (stop) continue;
+    // pivot: the first strictly largest |m[i][i]|, i >= k
+    double best = fabs(__shfl_sync(kFull, v, tri(k, k)));
+    int piv = k;
+#pragma unroll 1
+    for (int i = k + 1; i < 6; ++i) {
+      const double di = fabs(__shfl_sync(kFull, v, tri(i, i)));
+      if (di > best) {
+        best = di;
+        piv = i;
+      }
+    }
+    transp[k] = piv;
+    if (piv != k) {
+      const int sr = r == k ? piv : (r == piv ? k : r);
+      const int sc = c == k ? piv : (c == piv ? k : c);
+      const int src = sr >= sc ? tri(sr, sc) : tri(sc, sr);
+      v = __shfl_sync(kFull, v, col_lane ? src : lane);
+    }
+    if (k > 0) {
+      // temp[j] = m[j][j] m[k][j]; m[i][k] -= m[i][0] temp[0] + m[i][1] temp[1] + ...
+      double sacc = 0.0;
+#pragma unroll 1
+      for (int j = 0; j < k; ++j) {
+        const double tj = __shfl_sync(kFull, v, tri(j, j)) * __shfl_sync(kFull, v, tri(k, j));
+        const double mij = __shfl_sync(kFull, v, r > j ? tri(r, j) : 0);
+        const double prod = mij * tj;
+        sacc = j == 0 ? prod : sacc + prod;
+      }
+      if (col_lane && c == k) v = v - sacc;
+    }
+    const double akk = __shfl_sync(kFull, v, tri(k, k));
+    const bool pivot_valid = fabs(akk) > 0.0;
+    if (!pivot_valid) degen = true;
+    if (k == 0 && !pivot_valid) {
+      ok = false;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) transp[j] = j;
+      stop = true;
+      continue;
+    }
+    if (k < 5) {
+      const bool below = col_lane && c == k && r > k;
+      if (pivot_valid) {
+        if (below) v = v / akk;
+      } else {
+        ok = ok && __all_sync(kFull, !below || v == 0.0);
+      }
+    }
+  }
+  const double tol = 2.2250738585072014e-308;  // numeric_limits<double>::min()
+#pragma unroll 1
+  for (int i = 0; i < 6; ++i)
+    if (!(fabs(__shfl_sync(kFull, v, tri(i, i))) > tol)) degen = true;
+  if (col_lane) {
+    ls->fm[6 * r + c] = v;
+    ls->fm[6 * c + r] = v;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) ls->ftr[i] = transp[i];
+    ls->degen = degen || stop;
+  }
+  (void)ok;
+}
+
+// ldlt6_apply_reg (geometry.cuh) with the factors in shared memory.
+CSF_DEV void ldlt6_apply_smem(const double* fm, const int* tr, const double* rhs, double* dst) {
+  double x[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) x[i] = rhs[i];
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (tr[k] == i) swap_s(x[k], x[i]);
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = i + 1; j < 6; ++j) x[j] = x[j] - x[i] * fm[6 * j + i];
+  const double tol = 2.2250738585072014e-308;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double mii = fm[7 * i];
+    x[i] = fabs(mii) > tol ? x[i] / mii : 0.0;
+  }
+#pragma unroll
+  for (int i = 4; i >= 0; --i) {
+    double sacc = fm[6 * (i + 1) + i] * x[i + 1];
+#pragma unroll
+    for (int j = i + 2; j < 6; ++j) sacc = sacc + fm[6 * j + i] * x[j];
+    x[i] = x[i] - sacc;
+  }
+#pragma unroll
+  for (int k = 5; k >= 0; --k)
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (tr[k] == i) swap_s(x[k], x[i]);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) dst[i] = x[i];
+}
+
+__device__ __noinline__ void level_solve(const IcpLevelArgs& a, const double* s_tot, double* s_pose,
+                                         LevelSolveShared* ls, double (&dre)[6], unsigned seq, int it) {
+  const int C = 1 + a.Dp;
+  const int tid = threadIdx.x;
+  if (tid < 32) ldlt6_warp(s_tot, C, ls);
   __syncthreads();
-  clock_mark(6, kSolveClockCta);
-  // channel threads: thread t < max(Dp, 1) owns channel t (thread 0 also the real part)
-  const bool mine = static_cast<int>(threadIdx.x) < (Dp > 0 ? Dp : 1);
+  lv_mark(seq, it, 8);
+  // channel threads: thread t < max(Dp, 1) owns channel t + 1 (thread 0 also the real part)
+  const bool mine = tid < (a.Dp > 0 ? a.Dp : 1);
   L<1> d[6];
   if (mine) {
-    const int ch = 1 + threadIdx.x;
-    if (Dp == 0) {
+    const int ch = 1 + tid;
+    double nb[6], x[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) nb[i] = -s_tot[(21 + i) * C];
+    ldlt6_apply_smem(ls->fm, ls->ftr, nb, x);  // the real step (the same bits in every thread)
+    if (a.Dp == 0) {
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        d[i].re = s_x[i];
+        d[i].re = x[i];
         d[i].im[0] = 0.0;
       }
-    } else if (!s_degen) {
-      double m[6][6];
-      int tr[6];
-#pragma unroll
-      for (int r = 0; r < 6; ++r)
-#pragma unroll
-        for (int c = 0; c < 6; ++c) m[r][c] = s_m[6 * r + c];
-#pragma unroll
-      for (int i = 0; i < 6; ++i) tr[i] = s_tr[i];
+    } else if (!ls->degen) {
       double rhs[6], dx[6];
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
         double ax = 0.0;
 #pragma unroll
-        for (int j = 0; j < 6; ++j) ax = ax + s_acc[(i >= j ? tri(i, j) : tri(j, i)) * C + ch] * s_x[j];
-        rhs[i] = -s_acc[(21 + i) * C + ch] - ax;
+        for (int j = 0; j < 6; ++j) ax = ax + s_tot[(i >= j ? tri(i, j) : tri(j, i)) * C + ch] * x[j];
+        rhs[i] = -s_tot[(21 + i) * C + ch] - ax;
       }
-      ldlt6_apply_reg<double>(m, tr, rhs, dx);
+      ldlt6_apply_smem(ls->fm, ls->ftr, rhs, dx);
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        d[i].re = s_x[i];
+        d[i].re = x[i];
         d[i].im[0] = dx[i];
       }
     } else {
-      L<1> a[21], nb[6];
-#pragma unroll
-      for (int q = 0; q < 21; ++q) a[q] = load_ch<L<1>>(s_acc + q * C, threadIdx.x, 1);
-#pragma unroll
-      for (int i = 0; i < 6; ++i) nb[i] = -load_ch<L<1>>(s_acc + (21 + i) * C, threadIdx.x, 1);
-      ldlt6_solve_reg<L<1>>(a, nb, d);
+      solve_channel_lifted(s_tot, C, tid, d);
     }
     bool fin = true;
 #pragma unroll
     for (int i = 0; i < 6; ++i) fin = fin && finite_s(d[i]);
-    if (!fin) atomicAnd(&s_finite, 0);
+    if (!fin) atomicAnd(&ls->finite, 0);  // delta.allFinite() over every channel
   }
   __syncthreads();
-  clock_mark(7, kSolveClockCta);
+  lv_mark(seq, it, 9);
   Pose<L<1>> np;
   if (mine) {
-    if (!s_finite)
+    if (!ls->finite)
 #pragma unroll
       for (int i = 0; i < 6; ++i) d[i] = lit<L<1>>(0.0);
-    const int g0 = Dp > 0 ? static_cast<int>(threadIdx.x) : 0;
-    const int nv = Dp > 0 ? 1 : 0;
+    const int g0 = a.Dp > 0 ? tid : 0;
+    const int nv = a.Dp > 0 ? 1 : 0;
     Pose<L<1>> cur;
 #pragma unroll
-    for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<L<1>>(pose + e * C, g0, nv);
+    for (int e = 0; e < 9; ++e) cur.R.m[e] = load_ch<L<1>>(s_pose + e * C, g0, nv);
 #pragma unroll
-    for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<L<1>>(pose + (9 + e) * C, g0, nv);
-    np = compose(exp_map<L<1>>(d), cur);
+    for (int e = 0; e < 3; ++e) cur.t.v[e] = load_ch<L<1>>(s_pose + (9 + e) * C, g0, nv);
+    increment_pose(d, cur, &np);  // apply_increment (se3.hpp:116-119)
   }
-  __syncthreads();
+  __syncthreads();  // every channel thread has read the current pose
+  lv_mark(seq, it, 10);
   if (mine) {
-    const int g0 = Dp > 0 ? static_cast<int>(threadIdx.x) : 0;
-    const int nv = Dp > 0 ? 1 : 0;
+    const int g0 = a.Dp > 0 ? tid : 0;
+    const int nv = a.Dp > 0 ? 1 : 0;
 #pragma unroll
-    for (int e = 0; e < 9; ++e) store_ch<L<1>>(pose + e * C, np.R.m[e], g0, nv, threadIdx.x == 0);
+    for (int e = 0; e < 9; ++e) store_ch<L<1>>(s_pose + e * C, np.R.m[e], g0, nv, tid == 0);
 #pragma unroll
-    for (int e = 0; e < 3; ++e) store_ch<L<1>>(pose + (9 + e) * C, np.t.v[e], g0, nv, threadIdx.x == 0);
+    for (int e = 0; e < 3; ++e) store_ch<L<1>>(s_pose + (9 + e) * C, np.t.v[e], g0, nv, tid == 0);
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     double sq[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) sq[i] = re(d[i]) * re(d[i]);
     const double nrm = sqrt((sq[0] + (sq[1] + sq[2])) + (sq[3] + (sq[4] + sq[5])));
-    st->iterations += 1;
-    st->n_corr = n;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) st->delta[i] = re(d[i]);
-#pragma unroll
-    for (int i = 0; i < 6; ++i) st->b[i] = s_acc[(21 + i) * C];
-    if (nrm < tol) {
-      st->level_done = 1;
-      if (level == 0) st->converged = 1;
+    if (nrm < a.tol) {
+      ls->done = 1;
+      ls->conv = a.level == 0 ? 1 : 0;
     }
   }
-  clock_mark(4, kSolveClockCta);
-  if (threadIdx.x == 0 && g_icp_clock) atomicAdd(&g_icp_clock_launch, 1u);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) dre[i] = tid == 0 ? re(d[i]) : 0.0;
 }
 
-__global__ void __launch_bounds__(kRedThreads) k_icp_solve_t(TrackState* st, const double* __restrict__ gpartials,
-                                                          const int* __restrict__ gcounts, int n_groups,
-                                                          double* pose, int Dp, int level, double tol) {
-  pdl_wait();
-  pdl_trigger();
-  if (st->level_done) return;
-  icp_solve_body(st, gpartials, gcounts, n_groups, pose, Dp, level, tol);
+// Debug timeline (tools/icp_timing.py, csf_debug_icp_clock): per launch, CTA,
+// iteration and phase, the %globaltimer in ns (64 launches x 256 CTAs x 32
+// iterations x 16 phases); off (nullptr) by default.
+__device__ unsigned long long* g_lv_clock = nullptr;
+__device__ unsigned g_lv_seq = 0;
+__device__ __forceinline__ void lv_mark(unsigned seq, int it, int phase) {
+  unsigned long long* b = g_lv_clock;
+  if (b && threadIdx.x == 0 && it < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    b[((static_cast<unsigned long long>(seq & 63) * 256 + blockIdx.x) * 32 + it) * 16 + phase] = t;
+  }
 }
 
-// One lifted (J, r) row of a correspondence (slot (x, y) -> model pixel
-// (u, v)) into row[7][C]: the canonical row both the fused reduce and the
-// split rows kernel write (same operations, bit-identical).
-CSF_DEV void icp_row(double* row, const double* __restrict__ depth, int w, int x, int y, int u, int v,
-                     const double* s_pose, const double* s_intr, int C, int Dp, const double* __restrict__ vre,
-                     const double* __restrict__ nre, const double* __restrict__ vim,
-                     const double* __restrict__ nim) {
-  // One lifted (J, r) row in tangent form: the real chain once, then each
-  // channel's im by the truncated-Complex rule of every operation
-  // (csfd.hpp:44-58) applied to the saved real intermediates.
-  const long long m = static_cast<long long>(v) * w + u;
-  const double d = depth[y * w + x];
-  // vertex: ((d*(x - cx))/fx, (d*(y - cy))/fy, d)
-  const double tx = static_cast<double>(x) - s_intr[2 * C], ty = static_cast<double>(y) - s_intr[3 * C];
-  const double nx = d * tx, ny = d * ty;
-  const double kfx = s_intr[0], kfy = s_intr[C];
-  const double vre3[3] = {nx / kfx, ny / kfy, d};
-  const double ifx = 1.0 / (kfx * kfx), ify = 1.0 / (kfy * kfy);
-  (void)ifx;
-  (void)ify;
-  double R[9], T[3], MV[3], MN[3], P[3], PR[9];
-#pragma unroll
-  for (int e = 0; e < 9; ++e) R[e] = s_pose[e * C];
-#pragma unroll
-  for (int e = 0; e < 3; ++e) T[e] = s_pose[(9 + e) * C];
-#pragma unroll
-  for (int c3 = 0; c3 < 3; ++c3) {
-    MV[c3] = vre[3 * m + c3];
-    MN[c3] = nre[3 * m + c3];
-  }
-#pragma unroll
-  for (int r3 = 0; r3 < 3; ++r3) {
-#pragma unroll
-    for (int c3 = 0; c3 < 3; ++c3) PR[3 * r3 + c3] = R[3 * r3 + c3] * vre3[c3];
-    P[r3] = (PR[3 * r3] + (PR[3 * r3 + 1] + PR[3 * r3 + 2])) + T[r3];
-  }
-  const double DF[3] = {P[0] - MV[0], P[1] - MV[1], P[2] - MV[2]};
-  const double rr = DF[0] * MN[0] + (DF[1] * MN[1] + DF[2] * MN[2]);
-  const double PN[3] = {P[1] * MN[2] - P[2] * MN[1], P[2] * MN[0] - P[0] * MN[2], P[0] * MN[1] - P[1] * MN[0]};
-  row[0] = MN[0];
-  row[C] = MN[1];
-  row[2 * C] = MN[2];
-  row[3 * C] = PN[0];
-  row[4 * C] = PN[1];
-  row[5 * C] = PN[2];
-  row[6 * C] = rr;
-  for (int ch = 1; ch <= Dp; ++ch) {
-    // vertex channels (intrinsics seeds): d*(x - cx) has im d*(-cx.im)
-    const double tnx = d * -s_intr[2 * C + ch], tny = d * -s_intr[3 * C + ch];
-    const double vim3[3] = {CSF_CH_DIV(tnx * kfx - nx * s_intr[ch], kfx * kfx, ifx),
-                            CSF_CH_DIV(tny * kfy - ny * s_intr[C + ch], kfy * kfy, ify), 0.0};
-    double Pi[3], MVi[3], MNi[3];
-#pragma unroll
-    for (int c3 = 0; c3 < 3; ++c3) {
-      MVi[c3] = vim[(3 * m + c3) * Dp + ch - 1];
-      MNi[c3] = nim[(3 * m + c3) * Dp + ch - 1];
-    }
-#pragma unroll
-    for (int r3 = 0; r3 < 3; ++r3) {
-      double qi[3];
-#pragma unroll
-      for (int c3 = 0; c3 < 3; ++c3) qi[c3] = R[3 * r3 + c3] * vim3[c3] + s_pose[(3 * r3 + c3) * C + ch] * vre3[c3];
-      Pi[r3] = (qi[0] + (qi[1] + qi[2])) + s_pose[(9 + r3) * C + ch];
-    }
-    const double DFi[3] = {Pi[0] - MVi[0], Pi[1] - MVi[1], Pi[2] - MVi[2]};
-    double ti[3];
-#pragma unroll
-    for (int c3 = 0; c3 < 3; ++c3) ti[c3] = DF[c3] * MNi[c3] + DFi[c3] * MN[c3];
-    const double ri = ti[0] + (ti[1] + ti[2]);
-    const double PNi[3] = {(P[1] * MNi[2] + Pi[1] * MN[2]) - (P[2] * MNi[1] + Pi[2] * MN[1]),
-                           (P[2] * MNi[0] + Pi[2] * MN[0]) - (P[0] * MNi[2] + Pi[0] * MN[2]),
-                           (P[0] * MNi[1] + Pi[0] * MN[1]) - (P[1] * MNi[0] + Pi[1] * MN[0])};
-    row[ch] = MNi[0];
-    row[C + ch] = MNi[1];
-    row[2 * C + ch] = MNi[2];
-    row[3 * C + ch] = PNi[0];
-    row[4 * C + ch] = PNi[1];
-    row[5 * C + ch] = PNi[2];
-    row[6 * C + ch] = ri;
-  }
-
-}
-
-template <int G>
-__global__ void __launch_bounds__(kRedThreads) k_icp_reduce(const TrackState* st, const double* __restrict__ depth,
-                                                    int w, int h, int stride, const double* __restrict__ intr,
-                                                    const double* pose, const double* __restrict__ vre,
-                                                    const double* __restrict__ nre, const double* __restrict__ vim,
-                                                    const double* __restrict__ nim, double d_max, double cos_max,
-                                                    int Dp, int chunk, double* __restrict__ partials,
-                                                    int* __restrict__ counts, double* __restrict__ gpartials,
-                                                    int* __restrict__ gcounts, unsigned* __restrict__ group_ctr) {
-  pdl_wait();
-  pdl_trigger();
-  if (st->level_done) return;
-  clock_mark(0);
-  using S = Scal<G>;
+__global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
   extern __shared__ double sm[];
-  const int C = 1 + Dp;
-  double* s_pose = sm;
-  double* s_intr = s_pose + 12 * C;
-  double* s_jr = s_intr + 4 * C;
-  __shared__ int s_wsum[kRedThreads / 32];
-  for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) s_pose[i] = pose[i];
-  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_intr[i] = intr[i];
-  __syncthreads();
-
-  Pose<double> c2w, w2p;
-  load_pose_real(s_pose, C, &c2w);
-#pragma unroll
-  for (int e = 0; e < 9; ++e) w2p.R.m[e] = st->pred_w2c[e];
-#pragma unroll
-  for (int e = 0; e < 3; ++e) w2p.t.v[e] = st->pred_w2c[9 + e];
-  const double fx = s_intr[0], fy = s_intr[C], cx = s_intr[2 * C], cy = s_intr[3 * C];
-  const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
-  const int n_slots = nxs * nys;
+  const int C = 1 + a.Dp;
   const int n_acc = 27 * C;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  int tile_count = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-  for (int cbase = 0; cbase < kTile; cbase += chunk) {
-    const int slot = blockIdx.x * kTile + cbase + threadIdx.x;
-    bool corr = false;
-    int x = 0, y = 0, u = 0, v = 0;
-    if (threadIdx.x < chunk && slot < n_slots) {
-      x = (slot % nxs) * stride;
-      y = (slot / nxs) * stride;
-      corr = associate_slot(depth, w, h, x, y, fx, fy, cx, cy, c2w, w2p, vre, nre, d_max, cos_max, &u, &v);
-    }
-    // order-preserving compaction within the chunk
-    const unsigned ballot = __ballot_sync(0xffffffffu, corr);
-    if (lane == 0) s_wsum[warp] = __popc(ballot);
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int k = 0; k < kRedThreads / 32; ++k) {
-      if (k < warp) before += s_wsum[k];
-      total += s_wsum[k];
-    }
-    const int pos = before + __popc(ballot & ((1u << lane) - 1u));
-    if (corr) icp_row(s_jr + static_cast<long long>(pos) * 7 * C, depth, w, x, y, u, v, s_pose, s_intr, C, Dp, vre,
-                      nre, vim, nim);
-    __syncthreads();
-    if (cbase == 0) clock_mark(1);
-    // per-accumulator sequential sums in slot order
+  double* s_pose = sm;                                        // [12][C]
+  double* s_intr = s_pose + 12 * C;                           // [4][C]
+  double* s_tot = s_intr + 4 * C;                             // [27][C]
+  double* s_rec = s_tot + n_acc;                              // [kRecFields][kSegSlots]
+  double* s_meas = s_rec + kRecFields * kSegSlots;            // [6][kSegSlots]
+  int* s_m = reinterpret_cast<int*>(s_meas + 6 * kSegSlots);  // [kSegSlots]
+  __shared__ int s_wsum[kRounds * kLvWarps];
+  __shared__ int s_n, s_last;
+  __shared__ LevelSolveShared ls;
+  __shared__ double s_w2p[12];
+  __shared__ unsigned s_gen;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  for (int i = tid; i < 12 * C; i += blockDim.x) s_pose[i] = a.pose[i];
+  for (int i = tid; i < 4 * C; i += blockDim.x) s_intr[i] = a.intr[i];
+  if (tid < 12) s_w2p[tid] = a.st->pred_w2c[tid];
+  const unsigned seq = g_lv_clock ? *(volatile unsigned*)&g_lv_seq : 0u;
+  if (tid == 0) s_gen = acquire_gen(a.sync + kFlagWord);
+  __syncthreads();
+  const unsigned gen = s_gen;
+  Pose<double> w2p;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int a = threadIdx.x + kRedThreads * j;
-      if (a >= n_acc) break;
-      const int q = a / C, c = a % C;
-      int ja, jb;
-      if (q < 21) {
-        ja = c_tri_r[q];
-        jb = c_tri_c[q];
-      } else {
-        ja = q - 21;
-        jb = 6;
+  for (int e = 0; e < 9; ++e) w2p.R.m[e] = s_w2p[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) w2p.t.v[e] = s_w2p[9 + e];
+
+  const int nxs = (a.w + a.stride - 1) / a.stride, nys = (a.h + a.stride - 1) / a.stride;
+  const int n_slots = nxs * nys;
+  const int t0 = tile * a.tile_slots;
+  const int t1 = min(n_slots, t0 + a.tile_slots);
+  const int n_segs = (t1 - t0 + kSegSlots - 1) / kSegSlots;
+  const int passes = (C + kLvWarps - 1) / kLvWarps;
+  const int n_groups = (a.n_tiles + kLvGroup - 1) / kLvGroup;
+  const int grp = tile / kLvGroup;
+  int taken = 0, last_n = 0;
+  double last_delta[6] = {0, 0, 0, 0, 0, 0}, last_b[6] = {0, 0, 0, 0, 0, 0};
+  bool converged = false;
+  // single-segment tiles (VGA and below): the measured side once per level
+  if (n_segs == 1) level_measure(a, t0, t1, s_intr, s_meas);
+
+  for (int it = 0; it < a.iterations; ++it) {
+    lv_mark(seq, it, 0);
+    // ---- A + B: this tile's partial normal equations, segment by segment
+    // (one segment at VGA; a multi-segment tile re-associates per pass)
+    int count = 0;
+    for (int p = 0; p < passes; ++p) {
+      const int c = warp + kLvWarps * p;
+      double acc[27];
+#pragma unroll
+      for (int q = 0; q < 27; ++q) acc[q] = 0.0;
+      int ebase = 0;
+      for (int sg = 0; sg < n_segs; ++sg) {
+        int n;
+        if (n_segs > 1 || p == 0) {
+          __syncthreads();  // the previous segment's records are consumed
+          const int s0 = t0 + sg * kSegSlots, s1 = min(t1, s0 + kSegSlots);
+          if (n_segs > 1) {
+            level_measure(a, s0, s1, s_intr, s_meas);
+            __syncthreads();
+          }
+          n = level_associate(a, s0, s1, s_pose, s_intr, w2p, s_meas, s_rec, s_m, s_wsum);
+          __syncthreads();
+          if (tid == 0) s_n = n;  // kept for the passes that reuse the records
+        } else {
+          n = s_n;
+        }
+        if (p == 0) count += n;
+        if (p == 0 && sg == 0) lv_mark(seq, it, 1);
+        if (c < C) level_accumulate(a, c, ebase, 0, n, s_pose, s_intr, s_rec, s_m, acc);
+        ebase += n;
       }
-      const int stride = 7 * C;
-      const double* pa = s_jr + ja * C;
-      const double* pb = s_jr + jb * C;
-      double s = acc[j];
-      // the add chain is sequential (canonical order); the shared-memory
-      // loads of the next entries are independent and are issued ahead
-      if (c == 0) {
-#pragma unroll 8
-        for (int e = 0; e < total; ++e) s = s + pa[e * stride] * pb[e * stride];
-      } else {
-#pragma unroll 8
-        for (int e = 0; e < total; ++e) {
-          const int o = e * stride;
-          s = s + (pa[o] * pb[o + c] + pa[o + c] * pb[o]);
+      if (c < C) {
+        // the 32 streams: fixed xor butterfly (every lane ends with the total)
+#pragma unroll
+        for (int q = 0; q < 27; ++q) {
+          double v = acc[q];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, off);
+          acc[q] = v;
+        }
+        double mine = 0.0;
+#pragma unroll
+        for (int q = 0; q < 27; ++q)
+          if (lane == q) mine = acc[q];
+        if (lane < 27) a.partials[static_cast<long long>(tile) * n_acc + lane * C + c] = mine;
+      }
+    }
+    if (tid == 0) a.counts[tile] = count;
+    // ---- C: group sums in tile order, then group totals in group order.
+    // One thread per CTA publishes with an acq_rel atomic after the CTA
+    // barrier (the barrier orders the CTA's partial writes before it); the
+    // last arrival reads the others' partials through L2 (__ldcg).
+    __syncthreads();
+    lv_mark(seq, it, 2);
+    const int first = grp * kLvGroup;
+    const int gn = min(kLvGroup, a.n_tiles - first);
+    if (tid == 0) s_last = atom_add_acq_rel(a.sync + grp, 1u) == static_cast<unsigned>(gn - 1);
+    __syncthreads();
+    if (s_last) {
+      if (tid == 0) a.sync[grp] = 0u;
+      for (int q = tid; q < n_acc; q += blockDim.x) {
+        double v[kLvGroup];
+#pragma unroll
+        for (int u = 0; u < kLvGroup; ++u)
+          v[u] = u < gn ? __ldcg(a.partials + static_cast<long long>(first + u) * n_acc + q) : 0.0;
+        double total = 0.0;
+#pragma unroll
+        for (int u = 0; u < kLvGroup; ++u)
+          if (u < gn) total = total + v[u];
+        a.gpartials[static_cast<long long>(grp) * n_acc + q] = total;
+      }
+      if (tid < 32) {
+        int cn = tid < gn ? __ldcg(a.counts + first + tid) : 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) cn += __shfl_down_sync(0xffffffffu, cn, off);
+        if (tid == 0) a.counts[kLvMaxTiles + grp] = cn;
+      }
+      __syncthreads();
+      lv_mark(seq, it, 6);
+      if (tid == 0) s_last = atom_add_acq_rel(a.sync + kLvMaxGroups, 1u) == static_cast<unsigned>(n_groups - 1);
+      __syncthreads();
+      if (s_last) {
+        lv_mark(seq, it, 7);
+        if (tid == 0) a.sync[kLvMaxGroups] = 0u;
+        for (int q = tid; q < n_acc; q += blockDim.x) {
+          double v[kLvMaxGroups];
+#pragma unroll
+          for (int g = 0; g < kLvMaxGroups; ++g)
+            v[g] = g < n_groups ? __ldcg(a.gpartials + static_cast<long long>(g) * n_acc + q) : 0.0;
+          double total = 0.0;
+#pragma unroll
+          for (int g = 0; g < kLvMaxGroups; ++g)
+            if (g < n_groups) total = total + v[g];
+          a.totals[q] = total;
+        }
+        if (tid < 32) {
+          int cn = 0;
+          for (int g = tid; g < n_groups; g += 32) cn += __ldcg(a.counts + kLvMaxTiles + g);
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) cn += __shfl_down_sync(0xffffffffu, cn, off);
+          if (tid == 0) a.counts[kLvMaxTiles + kLvMaxGroups] = cn;
+        }
+        __syncthreads();
+        lv_mark(seq, it, 3);
+        if (tid == 0) release_gen(a.sync + kFlagWord, gen + it + 1);
+      }
+    }
+    // ---- grid barrier
+    if (tid == 0) {
+      while (static_cast<int>(poll_gen(a.sync + kFlagWord) - (gen + it + 1)) < 0) __nanosleep(32);
+      fence_acquire();
+    }
+    __syncthreads();
+    lv_mark(seq, it, 4);
+    for (int q = tid; q < n_acc; q += blockDim.x) s_tot[q] = __ldcg(a.totals + q);
+    if (tid == 0) {
+      s_n = __ldcg(a.counts + kLvMaxTiles + kLvMaxGroups);
+      ls.done = 0;
+      ls.conv = 0;
+      ls.finite = 1;
+    }
+    __syncthreads();
+    // ---- D: the solve (every CTA, identical bits)
+    const int n = s_n;
+    last_n = n;
+    if (n < 12) break;  // icp.cpp:199, before the step
+    double dre[6];
+    level_solve(a, s_tot, s_pose, &ls, dre, seq, it);
+    lv_mark(seq, it, 5);
+    ++taken;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      last_delta[i] = dre[i];
+      last_b[i] = s_tot[(21 + i) * C];
+    }
+    __syncthreads();
+    if (ls.done) {
+      converged = ls.conv != 0;
+      break;
+    }
+  }
+  // the level's result: CTA 0 writes the pose and the tracker state
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    for (int i = tid; i < 12 * C; i += blockDim.x) a.pose[i] = s_pose[i];
+    if (tid == 0) {
+      TrackState* st = a.st;
+      st->iterations += taken;
+      st->n_corr = last_n;
+      if (taken > 0) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          st->delta[i] = last_delta[i];
+          st->b[i] = last_b[i];
         }
       }
-      acc[j] = s;
+      if (converged) st->converged = 1;
+      st->level_done = 1;
+      if (g_lv_clock) atomicAdd(&g_lv_seq, 1u);
     }
-    tile_count += total;
-    __syncthreads();
   }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int a = threadIdx.x + kRedThreads * j;
-    if (a < n_acc) partials[static_cast<long long>(blockIdx.x) * n_acc + a] = acc[j];
-  }
-  if (threadIdx.x == 0) counts[blockIdx.x] = tile_count;
-  clock_mark(2);
-  group_sum(partials, counts, n_acc, gpartials, gcounts, group_ctr);
 }
 
 // Level entry: the prediction pose is the current estimate (icp.cpp:191).
@@ -582,6 +956,7 @@ __global__ void k_frame_end(const TrackState* st, const double* pose, double* tr
     s[4] = counters ? counters[0] : 0;
     s[5] = counters ? counters[1] : 0;
     s[6] = st->pad[1];
+    s[7] = 0;
   }
 }
 
@@ -634,25 +1009,31 @@ __global__ void k_objective(const double* __restrict__ traj, const double* __res
 //                  the real step to `stage`
 //   k_icp_commit   real pose + break decisions (TrackState)
 // ============================================================================
-constexpr int kTile2 = 256;
+constexpr int kR2Warps = 8;
+constexpr int kR2Threads = 32 * kR2Warps;
 
 template <typename S>
-__global__ void __launch_bounds__(256) k_icp_reduce2(const TrackState* st, const double* __restrict__ depth, int w,
-                                                     int h, int stride, const double* __restrict__ intr,
-                                                     const double* __restrict__ pose, const double* __restrict__ vre,
-                                                     const double* __restrict__ nre, const double* __restrict__ vim,
-                                                     const double* __restrict__ nim, double d_max, double cos_max,
-                                                     int Dp, double* __restrict__ partials, int* __restrict__ counts) {
+__global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st, const double* __restrict__ depth,
+                                                             int w, int h, int stride, const double* __restrict__ intr,
+                                                             const double* __restrict__ pose,
+                                                             const double* __restrict__ vre,
+                                                             const double* __restrict__ nre,
+                                                             const double* __restrict__ vim,
+                                                             const double* __restrict__ nim, double d_max,
+                                                             double cos_max, int Dp, int tile_slots,
+                                                             double* __restrict__ partials, int* __restrict__ counts) {
   pdl_wait();
   pdl_trigger();
   if (st->level_done) return;
   constexpr int G = Traits<S>::G;
   constexpr int CG = 1 + G;
+  constexpr int NA = 27 * CG;  // accumulator threads
   const int C = 1 + Dp;
   const int g0 = blockIdx.y * G;
   extern __shared__ double sm[];
-  S* rows = reinterpret_cast<S*>(sm);  // [kTile2][7]
-  __shared__ int s_wsum[8];
+  S* rows = reinterpret_cast<S*>(sm);                 // [kR2Threads][7]
+  double* streams = sm + sizeof(S) / 8 * kR2Threads * 7;  // [NA][33]: the canonical 32 streams
+  __shared__ int s_wsum[kR2Warps];
   Pose<double> c2w, w2p;
   load_pose_real(pose, C, &c2w);
 #pragma unroll
@@ -662,84 +1043,95 @@ __global__ void __launch_bounds__(256) k_icp_reduce2(const TrackState* st, const
   const double fx = intr[0], fy = intr[C], cx = intr[2 * C], cy = intr[3 * C];
   const int nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
   const int n_slots = nxs * nys;
-  const int slot = blockIdx.x * kTile2 + threadIdx.x;
+  const int t0 = blockIdx.x * tile_slots, t1 = min(n_slots, t0 + tile_slots);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = 0, y = 0, u = 0, v = 0;
-  bool corr = false;
-  if (slot < n_slots) {
-    x = (slot % nxs) * stride;
-    y = (slot / nxs) * stride;
-    corr = associate_slot(depth, w, h, x, y, fx, fy, cx, cy, c2w, w2p, vre, nre, d_max, cos_max, &u, &v);
-  }
-  const unsigned ballot = __ballot_sync(0xffffffffu, corr);
-  if (lane == 0) s_wsum[warp] = __popc(ballot);
-  __syncthreads();
-  int before = 0, total = 0;
+  for (int i = threadIdx.x; i < NA * 33; i += blockDim.x) streams[i] = 0.0;
+  int ebase = 0;
+  for (int c0 = t0; c0 < t1; c0 += kR2Threads) {
+    const int slot = c0 + threadIdx.x;
+    int x = 0, y = 0, u = 0, v = 0;
+    bool corr = false;
+    if (slot < t1) {
+      x = (slot % nxs) * stride;
+      y = (slot / nxs) * stride;
+      corr = associate_slot(depth, w, h, x, y, fx, fy, cx, cy, c2w, w2p, vre, nre, d_max, cos_max, &u, &v);
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, corr);
+    __syncthreads();  // the previous chunk's rows are consumed
+    if (lane == 0) s_wsum[warp] = __popc(ballot);
+    __syncthreads();
+    int before = 0, total = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    if (k < warp) before += s_wsum[k];
-    total += s_wsum[k];
-  }
-  if (corr) {
-    const int pos = before + __popc(ballot & ((1u << lane) - 1u));
-    // jacobian_row (icp.cpp:20-24): vertex = backproject(K, x, y, d) in S
-    // (frames.hpp:38-41), p = base * vertex, r = (p - mv) . mn, J = [mn; p x mn]
-    const double d = depth[y * w + x];
-    const S kfx = load_ch<S>(intr, g0, G), kfy = load_ch<S>(intr + C, g0, G);
-    const S kcx = load_ch<S>(intr + 2 * C, g0, G), kcy = load_ch<S>(intr + 3 * C, g0, G);
-    const V3<S> vert = mk3<S>((d * (static_cast<double>(x) - kcx)) / kfx, (d * (static_cast<double>(y) - kcy)) / kfy,
-                              lit<S>(d));
-    Pose<S> base;
+    for (int k = 0; k < kR2Warps; ++k) {
+      if (k < warp) before += s_wsum[k];
+      total += s_wsum[k];
+    }
+    if (corr) {
+      const int pos = before + __popc(ballot & ((1u << lane) - 1u));
+      // jacobian_row (icp.cpp:20-24): vertex = backproject(K, x, y, d) in S
+      // (frames.hpp:38-41), p = base * vertex, r = (p - mv) . mn, J = [mn; p x mn]
+      const double d = depth[y * w + x];
+      const S kfx = load_ch<S>(intr, g0, G), kfy = load_ch<S>(intr + C, g0, G);
+      const S kcx = load_ch<S>(intr + 2 * C, g0, G), kcy = load_ch<S>(intr + 3 * C, g0, G);
+      const V3<S> vert = mk3<S>((d * (static_cast<double>(x) - kcx)) / kfx,
+                                (d * (static_cast<double>(y) - kcy)) / kfy, lit<S>(d));
+      Pose<S> base;
 #pragma unroll
-    for (int e = 0; e < 9; ++e) base.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+      for (int e = 0; e < 9; ++e) base.R.m[e] = load_ch<S>(pose + e * C, g0, G);
 #pragma unroll
-    for (int e = 0; e < 3; ++e) base.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
-    const long long m = static_cast<long long>(v) * w + u;
-    V3<S> mv, mn;
+      for (int e = 0; e < 3; ++e) base.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
+      const long long m = static_cast<long long>(v) * w + u;
+      V3<S> mv, mn;
 #pragma unroll
-    for (int c3 = 0; c3 < 3; ++c3) {
-      mv.v[c3].re = vre[3 * m + c3];
-      mn.v[c3].re = nre[3 * m + c3];
+      for (int c3 = 0; c3 < 3; ++c3) {
+        mv.v[c3].re = vre[3 * m + c3];
+        mn.v[c3].re = nre[3 * m + c3];
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        mv.v[c3].im[g] = vim[(3 * m + c3) * Dp + g0 + g];
-        mn.v[c3].im[g] = nim[(3 * m + c3) * Dp + g0 + g];
+        for (int g = 0; g < G; ++g) {
+          mv.v[c3].im[g] = vim[(3 * m + c3) * Dp + g0 + g];
+          mn.v[c3].im[g] = nim[(3 * m + c3) * Dp + g0 + g];
+        }
+      }
+      const V3<S> pw = apply(base, vert);
+      const S r = dot3(sub3(pw, mv), mn);
+      const V3<S> pn = cross3(pw, mn);
+      S* row = rows + 7 * pos;
+      row[0] = mn.v[0]; row[1] = mn.v[1]; row[2] = mn.v[2];
+      row[3] = pn.v[0]; row[4] = pn.v[1]; row[5] = pn.v[2];
+      row[6] = r;
+    }
+    __syncthreads();
+    // accumulate_row (orc_icp.hpp): one thread per (accumulator, slot) adds
+    // the S product of the two row entries into the correspondence's stream
+    // (global entry index mod 32), streams in entry order
+    const int acc = threadIdx.x;
+    if (acc < NA) {
+      const int q = acc / CG, c = acc % CG;
+      const int ja = acc_row_a(q), jb = acc_row_b(q);
+      double* str = streams + acc * 33;
+      for (int e = 0; e < total; ++e) {
+        const S prod = rows[7 * e + ja] * rows[7 * e + jb];
+        const int k = (ebase + e) & 31;
+        str[k] = str[k] + (c == 0 ? prod.re : prod.im[c - 1]);
       }
     }
-    const V3<S> pw = apply(base, vert);
-    const S r = dot3(sub3(pw, mv), mn);
-    const V3<S> pn = cross3(pw, mn);
-    S* row = rows + 7 * pos;
-    row[0] = mn.v[0]; row[1] = mn.v[1]; row[2] = mn.v[2];
-    row[3] = pn.v[0]; row[4] = pn.v[1]; row[5] = pn.v[2];
-    row[6] = r;
+    ebase += total;
   }
-  __syncthreads();
-  // accumulate_row (orc_icp.hpp): one thread per (accumulator, slot), the
-  // S product of the two row entries, summed in slot order within the tile
-  const int a = threadIdx.x;
-  if (a < 27 * CG) {
-    const int q = a / CG, c = a % CG;
-    int ja, jb;
-    if (q < 21) {
-      ja = c_tri_r[q];
-      jb = c_tri_c[q];
-    } else {
-      ja = q - 21;
-      jb = 6;
-    }
-    double acc = 0.0;
-    for (int e = 0; e < total; ++e) {
-      const S prod = rows[7 * e + ja] * rows[7 * e + jb];
-      acc = acc + (c == 0 ? prod.re : prod.im[c - 1]);
-    }
+  if (threadIdx.x == 0 && blockIdx.y == 0) counts[blockIdx.x] = ebase;
+  const int acc = threadIdx.x;
+  if (acc < NA) {
+    // the fixed butterfly of the first-order kernel, lane 0's value
+    double* str = streams + acc * 33;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+      for (int l = 0; l < off; ++l) str[l] = str[l] + str[l + off];
+    const int q = acc / CG, c = acc % CG;
     if (c == 0) {
-      if (blockIdx.y == 0) partials[static_cast<long long>(blockIdx.x) * 27 * C + q * C] = acc;
+      if (blockIdx.y == 0) partials[static_cast<long long>(blockIdx.x) * 27 * C + q * C] = str[0];
     } else {
-      partials[static_cast<long long>(blockIdx.x) * 27 * C + q * C + g0 + c] = acc;
+      partials[static_cast<long long>(blockIdx.x) * 27 * C + q * C + g0 + c] = str[0];
     }
   }
-  if (threadIdx.x == 0 && blockIdx.y == 0) counts[blockIdx.x] = total;
 }
 
 // stage: [0..11] new real pose, [12] |delta.re|, [13] correspondence count,
@@ -761,17 +1153,17 @@ __global__ void __launch_bounds__(128) k_icp_solve2(const TrackState* st, const 
   for (int a = threadIdx.x; a < 27 * CG; a += blockDim.x) {
     const int q = a / CG, c = a % CG;
     const long long off = static_cast<long long>(q) * C + (c == 0 ? 0 : g0 + c);
-    // canonical two-level order: tiles in order within groups of kGroup,
+    // canonical two-level order: tiles in order within groups of kLvGroup,
     // group totals in order (oracle tiled_normal_equations)
     double total = 0.0;
-    for (int t = 0; t < n_tiles; t += kGroup) {
-      double vals[kGroup];
+    for (int t = 0; t < n_tiles; t += kLvGroup) {
+      double vals[kLvGroup];
 #pragma unroll
-      for (int k = 0; k < kGroup; ++k)
+      for (int k = 0; k < kLvGroup; ++k)
         vals[k] = t + k < n_tiles ? __ldcg(partials + static_cast<long long>(t + k) * 27 * C + off) : 0.0;
       double gsum = 0.0;
 #pragma unroll
-      for (int k = 0; k < kGroup; ++k)
+      for (int k = 0; k < kLvGroup; ++k)
         if (t + k < n_tiles) gsum = gsum + vals[k];
       total = total + gsum;
     }
@@ -938,31 +1330,21 @@ static void chk(const char* what) {
     default: note_error("csf_b200: no kernel for group width " + std::to_string(G)); \
   }
 
-// Debug: enable per-CTA phase timestamps into a device buffer of
-// 4096 launches x 512 CTAs x 5 slots (nullptr disables).
 void icp_clock_enable(unsigned long long* buf) {
-  cudaMemcpyToSymbol(g_icp_clock, &buf, sizeof(buf));
+  cudaMemcpyToSymbol(g_lv_clock, &buf, sizeof(buf));
   const unsigned z = 0;
-  cudaMemcpyToSymbol(g_icp_clock_launch, &z, sizeof(z));
+  cudaMemcpyToSymbol(g_lv_seq, &z, sizeof(z));
 }
 
 int icp_tiles(int w, int h, int stride) {
   const long long nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
-  return static_cast<int>((nxs * nys + kTile - 1) / kTile);
+  const long long n = nxs * nys;
+  const long long t = icp_tile_slots(n);
+  return static_cast<int>((n + t - 1) / t);
 }
 bool icp_frame_fits(int w, int h, int stride) {
-  const int tiles = icp_tiles(w, h, stride);
-  return (tiles + kGroup - 1) / kGroup <= kMaxGroupCtr - 1;
-}
-
-// Slots per shared-memory chunk of the (J, r) rows.
-// (one pass over the tile's 256 slots whenever the rows fit: measured faster
-// than two half-tile passes at two CTAs per SM, bench r01)
-static int reduce_chunk(int C) {
-  if (8 * C * (16 + 256 * 7) <= 200 * 1024) return 256;
-  if (8 * C * (16 + 128 * 7) <= 200 * 1024) return 128;
-  if (8 * C * (16 + 64 * 7) <= 200 * 1024) return 64;
-  return 32;
+  const long long nxs = (w + stride - 1) / stride, nys = (h + stride - 1) / stride;
+  return nxs * nys <= (1LL << 30) && icp_tiles(w, h, stride) <= kIcpMaxTiles;
 }
 
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp) {
@@ -971,48 +1353,81 @@ void launch_level_begin(const Launch& L, TrackState* st, const double* pose, dou
   chk("level_begin");
 }
 
-size_t icp_partials_doubles(int C, int max_tiles) {
-  return static_cast<size_t>(max_tiles + (max_tiles + kGroup - 1) / kGroup) * 27 * C;
+// Scratch of the level kernel (and of the second-order reduce, which uses the
+// first kIcpMaxTiles rows / counts): partials [kIcpMaxTiles][27C], group
+// totals [groups][27C], totals [27C]; counts [kIcpMaxTiles] + [groups] + [1],
+// then the barrier words [groups] + [1] + [1] (zero at allocation, self-resetting).
+size_t icp_partials_doubles(int C) {
+  return static_cast<size_t>(kIcpMaxTiles + kLvMaxGroups + 1) * 27 * C;
 }
-size_t icp_counts_ints(int max_tiles) {
-  return static_cast<size_t>(kMaxGroupCtr + max_tiles + (max_tiles + kGroup - 1) / kGroup);
+size_t icp_counts_ints() { return static_cast<size_t>(kIcpMaxTiles + kLvMaxGroups + 1 + 64 + kFlagWord + 32); }
+
+static size_t level_smem(int C) {
+  return sizeof(double) * (43 * static_cast<size_t>(C) + (kRecFields + 6) * kSegSlots) + sizeof(int) * kSegSlots;
 }
 
-// One ICP iteration: k_icp_reduce (association, lifted rows, tile sums, group
-// sums) then k_icp_solve_t.  Scratch layout: partials = [tiles][27C] then
-// [groups][27C]; counts = [kMaxGroupCtr] self-resetting group counters (zero
-// at allocation), [tiles], [groups].
-void launch_icp_reduce(const Launch& L, int G, int Dp, TrackState* st, const double* depth, int w, int h,
-                       int stride, const double* intr, double* pose, const double* vre, const double* nre,
-                       const double* vim, const double* nim, double d_max, double cos_max, double* partials,
-                       int* counts, int level, double tol) {
+void launch_icp_level(const Launch& L, int Dp, TrackState* st, const double* depth, int w, int h, int stride,
+                      const double* intr, double* pose, const double* vre, const double* nre, const double* vim,
+                      const double* nim, double d_max, double cos_max, int iterations, int level, double tol,
+                      double* partials, int* counts) {
+  if (iterations <= 0) return;
   const int C = 1 + Dp;
-  const int n_acc = 27 * C;
-  const int chunk = reduce_chunk(C);
-  const size_t smem = sizeof(double) * (16 * C + static_cast<size_t>(chunk) * 7 * C);
-  const int tiles = icp_tiles(w, h, stride);
-  const int groups = (tiles + kGroup - 1) / kGroup;
-  if (groups > kMaxGroupCtr - 1 || Dp > kMaxC - 1) {
-    note_error("csf_b200: ICP frame too large (" + std::to_string(tiles) + " tiles) or too many channels (" +
-               std::to_string(Dp) + ")");
+  if (Dp > kMaxC - 1 || !icp_frame_fits(w, h, stride)) {
+    note_error("csf_b200: ICP level too large (" + std::to_string(w) + "x" + std::to_string(h) + ") or too many "
+               "channels (" + std::to_string(Dp) + ")");
     return;
   }
-  unsigned* ctr = reinterpret_cast<unsigned*>(counts);
-  int* tcounts = counts + kMaxGroupCtr;
-  int* gcounts = tcounts + tiles;
-  double* gpartials = partials + static_cast<size_t>(tiles) * n_acc;
-  // J/r rows are evaluated one channel at a time: register-light, and any
-  // channel-group width addresses the same channel layout.
-  if (G == 0)
-    launch_pdl(k_icp_reduce<0>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr, pose,
-               vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
-  else
-    launch_pdl(k_icp_reduce<1>, dim3(tiles), dim3(kRedThreads), smem, L.stream, st, depth, w, h, stride, intr, pose,
-               vre, nre, vim, nim, d_max, cos_max, Dp, chunk, partials, tcounts, gpartials, gcounts, ctr);
-  launch_pdl(k_icp_solve_t, dim3(1), dim3(kRedThreads), 0, L.stream, st, static_cast<const double*>(gpartials),
-             static_cast<const int*>(gcounts), groups, pose, Dp, level, tol);
-  *L.launches += 2;
-  chk("icp_reduce");
+  IcpLevelArgs a{};
+  a.st = st;
+  a.depth = depth;
+  a.w = w;
+  a.h = h;
+  a.stride = stride;
+  a.intr = intr;
+  a.pose = pose;
+  a.vre = vre;
+  a.nre = nre;
+  a.vim = vim;
+  a.nim = nim;
+  a.d_max = d_max;
+  a.cos_max = cos_max;
+  a.Dp = Dp;
+  a.iterations = iterations;
+  a.level = level;
+  a.tol = tol;
+  const long long n_slots = static_cast<long long>((w + stride - 1) / stride) * ((h + stride - 1) / stride);
+  a.tile_slots = icp_tile_slots(n_slots);
+  a.n_tiles = icp_tiles(w, h, stride);
+  const int n_acc = 27 * C;
+  a.partials = partials;
+  a.gpartials = partials + static_cast<size_t>(kIcpMaxTiles) * n_acc;
+  a.totals = a.gpartials + static_cast<size_t>(kLvMaxGroups) * n_acc;
+  a.counts = counts;
+  // the barrier words start on their own 256-byte boundary (counts is cudaMalloc-aligned)
+  a.sync = reinterpret_cast<unsigned*>(counts + ((kIcpMaxTiles + kLvMaxGroups + 1 + 63) / 64) * 64);
+  const size_t smem = level_smem(C);
+  ensure_dyn_smem(reinterpret_cast<const void*>(k_icp_level), smem);
+  // every CTA waits at the level's grid barrier: a cooperative launch
+  // guarantees they are co-resident (the tile count is capped for 2 CTAs/SM)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.n_tiles);
+  cfg.blockDim = dim3(kLvThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = L.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_icp_level, a);
+  if (e != cudaSuccess) {
+    int per_sm = -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_icp_level, kLvThreads, smem);
+    note_error(std::string("launch of icp_level failed: ") + cudaGetErrorString(e) + " (" +
+               std::to_string(a.n_tiles) + " tiles, " + std::to_string(per_sm) + " resident per SM at " +
+               std::to_string(smem) + " B shared)");
+  }
+  ++*L.launches;
 }
 
 void launch_seed(const Launch& L, int G, int Dp, const int* dirs, int D, double h, const double* gt0,
@@ -1065,9 +1480,11 @@ void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double
   using S = B<1>;
   const int tiles = icp_tiles(w, h, stride);
   const int pairs = Dp / 3;
-  const size_t smem = sizeof(S) * kTile2 * 7;
-  launch_pdl(k_icp_reduce2<S>, dim3(dim3(tiles, pairs)), dim3(kTile2), smem, L.stream, st, depth, w, h, stride, intr, pose, vre, nre, vim,
-                                                                   nim, d_max, cos_max, Dp, partials, counts);
+  const size_t smem = sizeof(S) * kR2Threads * 7 + sizeof(double) * 27 * (1 + Traits<S>::G) * 33;
+  const long long n_slots = static_cast<long long>((w + stride - 1) / stride) * ((h + stride - 1) / stride);
+  const int tile_slots = icp_tile_slots(n_slots);
+  launch_pdl(k_icp_reduce2<S>, dim3(tiles, pairs), dim3(kR2Threads), smem, L.stream, st, depth, w, h, stride, intr,
+             pose, vre, nre, vim, nim, d_max, cos_max, Dp, tile_slots, partials, counts);
   launch_pdl(k_icp_solve2<S>, dim3(pairs), dim3(128), 0, L.stream, st, partials, counts, tiles, pose, Dp, stage);
   launch_pdl(k_icp_commit, dim3(1), dim3(1), 0, L.stream, st, pose, Dp, stage, level, tol);
   *L.launches += 3;

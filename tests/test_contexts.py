@@ -7,8 +7,8 @@
   * host buffers are only borrowed for the duration of a call — a pinned
     destination handed to csf_pipeline_result holds the final values when
     the call returns;
-  * frames too large for the ICP reduction are rejected up front
-    (CSF_EINVAL -> ValueError), not silently skipped.
+  * an empty frame is rejected up front (CSF_EINVAL -> ValueError), and
+    frames above VGA (multi-segment ICP tiles) track exactly like the oracle.
 """
 import ctypes as C
 import threading
@@ -101,10 +101,40 @@ def test_pinned_result_buffers(gpu_ctx, oracle_built):
         stats.zero_()
 
 
-def test_oversize_frame_rejected(gpu_ctx):
-    k = csf.intrinsics(1000.0, 1000.0, 2047.5, 2047.5, 4096, 4096)
+def test_empty_frame_rejected(gpu_ctx):
+    """A frame with no pixels is rejected up front (CSF_EINVAL -> ValueError)."""
+    k = csf.intrinsics(100.0, 100.0, 0.0, 0.0, 0, 0)
     hp = capi.HashParams(0.02, (C.c_double * 3)(0.0, 0.0, 0.0), 0.1, 128.0, 16, 1 << 10)
     cfg = csf.make_pipeline_cfg(hashed=True, k=k, dirs=[0], h=1e-8, objective=capi.OBJECTIVE_TRAJECTORY_ERROR,
                                 max_frames=1, hash_params=hp)
     with pytest.raises(ValueError):
         csf.Pipeline(cfg, ctx=gpu_ctx)
+
+
+def test_multi_segment_tiles_1280x960(gpu_ctx, oracle_built):
+    """Frames above VGA make the ICP tiles longer than one shared-memory
+    segment (1280x960: 307200 slots at levels 0 and 1, 2080-slot tiles, four
+    segments), and 20 directions (the 10 of config 2 plus the keyframe twists
+    of frames 1 and 2) need two channel passes of the 16 warps: the level
+    kernel re-measures and re-associates per segment and pass.  Real channel,
+    stats and hash tables bit-identical to the oracle, derivatives within 1e-9."""
+    from oracle import orc
+    n = 3
+    d, gt, k = orc.workload(2, n, 1280, 960)
+    hp = capi.HashParams(0.01, (C.c_double * 3)(0.0, 0.0, 0.0), 0.05, 128.0, 20, 1 << 17)
+    cfg = csf.make_pipeline_cfg(hashed=True, k=k, dirs=list(range(20)), h=1e-8,
+                                objective=capi.OBJECTIVE_TRAJECTORY_ERROR, max_frames=n, hash_params=hp,
+                                keyframe_interval=1)
+    p = csf.Pipeline(cfg, ctx=gpu_ctx)
+    p.upload(d, gt)
+    p.run()
+    r = p.result()
+    g_o, obj_o, poses_o, stats_o, vol_o = orc.pipeline_run_keep(cfg, d, gt)
+    assert r.objective == obj_o
+    assert np.array_equal(r.poses[..., 0], poses_o[..., 0])
+    assert np.array_equal(r.stats[:, :7], stats_o[:, :7])
+    for x, y in zip(p.volume().hash_tables(), vol_o.hash_tables()):
+        assert np.array_equal(x, y)
+    s = np.maximum(np.maximum(np.abs(r.gradient), np.abs(g_o)), 1e-12)
+    assert (np.abs(r.gradient - g_o) <= 1e-9 * s).all(), (r.gradient, g_o)
+    assert r.stats[1:, 1].min() > 100
