@@ -759,29 +759,14 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
       if (tid == 0) s_last = atom_add_acq_rel(a.sync + kLvMaxGroups, 1u) == static_cast<unsigned>(n_groups - 1);
       __syncthreads();
       if (s_last) {
+        // every group total is published: release the grid (each CTA sums
+        // the group totals itself, in group order)
         lv_mark(seq, it, 7);
-        if (tid == 0) a.sync[kLvMaxGroups] = 0u;
-        for (int q = tid; q < n_acc; q += blockDim.x) {
-          double v[kLvMaxGroups];
-#pragma unroll
-          for (int g = 0; g < kLvMaxGroups; ++g)
-            v[g] = g < n_groups ? __ldcg(a.gpartials + static_cast<long long>(g) * n_acc + q) : 0.0;
-          double total = 0.0;
-#pragma unroll
-          for (int g = 0; g < kLvMaxGroups; ++g)
-            if (g < n_groups) total = total + v[g];
-          a.totals[q] = total;
+        if (tid == 0) {
+          a.sync[kLvMaxGroups] = 0u;
+          release_gen(a.sync + kFlagWord, gen + it + 1);
         }
-        if (tid < 32) {
-          int cn = 0;
-          for (int g = tid; g < n_groups; g += 32) cn += __ldcg(a.counts + kLvMaxTiles + g);
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) cn += __shfl_down_sync(0xffffffffu, cn, off);
-          if (tid == 0) a.counts[kLvMaxTiles + kLvMaxGroups] = cn;
-        }
-        __syncthreads();
         lv_mark(seq, it, 3);
-        if (tid == 0) release_gen(a.sync + kFlagWord, gen + it + 1);
       }
     }
     // ---- grid barrier
@@ -791,9 +776,25 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
     }
     __syncthreads();
     lv_mark(seq, it, 4);
-    for (int q = tid; q < n_acc; q += blockDim.x) s_tot[q] = __ldcg(a.totals + q);
+    for (int q = tid; q < n_acc; q += blockDim.x) {
+      double v[kLvMaxGroups];
+#pragma unroll
+      for (int g = 0; g < kLvMaxGroups; ++g)
+        v[g] = g < n_groups ? __ldcg(a.gpartials + static_cast<long long>(g) * n_acc + q) : 0.0;
+      double total = 0.0;
+#pragma unroll
+      for (int g = 0; g < kLvMaxGroups; ++g)
+        if (g < n_groups) total = total + v[g];
+      s_tot[q] = total;
+    }
+    if (tid < 32) {
+      int cn = 0;
+      for (int g = tid; g < n_groups; g += 32) cn += __ldcg(a.counts + kLvMaxTiles + g);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) cn += __shfl_down_sync(0xffffffffu, cn, off);
+      if (tid == 0) s_n = cn;
+    }
     if (tid == 0) {
-      s_n = __ldcg(a.counts + kLvMaxTiles + kLvMaxGroups);
       ls.done = 0;
       ls.conv = 0;
       ls.finite = 1;
