@@ -14,7 +14,18 @@ import numpy as np
 from paper_2405_02187_b200 import capi as _capi  # struct layouts only (no product calls)
 
 LIB_PATH = Path(__file__).resolve().parent / "_build" / "liborc.so"
+LIBM_PATH = Path(__file__).resolve().parent / "_build" / "liborc_libm.so"
 _LIB = None
+_LIBS = {}
+
+
+def use_libm(enable: bool) -> None:
+    """Switch every wrapper below to the -DORC_LIBM build (glibc exp/sin/cos)
+    or back to the default (csf_detmath.h) build."""
+    global _LIB, LIB_PATH
+    _LIBS[str(LIB_PATH)] = _LIB
+    LIB_PATH = LIBM_PATH if enable else LIBM_PATH.parent / "liborc.so"
+    _LIB = _LIBS.get(str(LIB_PATH))
 
 
 def lib() -> C.CDLL:
@@ -77,6 +88,7 @@ def lib() -> C.CDLL:
             "orc_predict_maps": (ip, [vp, dp, C.POINTER(_capi.Intrinsics), dp, dp]),
             "orc_sample_confidence": (C.c_double, [C.POINTER(_capi.Intrinsics), ip, ip]),
             "orc_pipeline_hessian": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, dp, dp, i32p, dp]),
+            "orc_detmath_ulp": (ip, [ip, dp, ip, dp, dp, dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -496,3 +508,13 @@ class Surfels:
 
 def sample_confidence(k, x, y):
     return lib().orc_sample_confidence(C.byref(k), x, y)
+
+
+def detmath_ulp(fn: str, x):
+    """csf_detmath.h exp/sin/cos vs glibc on the same arguments: (ulp errors,
+    deterministic values, glibc values)."""
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    u, d, g = np.empty_like(a), np.empty_like(a), np.empty_like(a)
+    code = {"exp": 0, "sin": 1, "cos": 2}[fn]
+    _check(lib().orc_detmath_ulp(code, _dp(a), a.size, _dp(u), _dp(d), _dp(g)))
+    return u, d, g

@@ -5,6 +5,8 @@
 // (include/csf_b200.h) so both sides are driven with the same descriptors;
 // nothing here links the product library.
 #include <chrono>
+#include <cmath>
+#include <limits>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -939,6 +941,29 @@ int orc_pipeline_run(const csf_pipeline_cfg* c, const float* depth, const double
       for (int d = 0; d < c->n_dirs; ++d) gradient[d] = r.gradient[d];
     if (poses) std::memcpy(poses, r.poses.data(), sizeof(double) * r.poses.size());
     if (stats) write_stats(n_frames, r, stats);
+  });
+}
+
+// tests/test_detmath.py: the deterministic elementary functions used on the
+// device path (include/csf_detmath.h) against glibc, in ulps of the glibc
+// result.  fn: 0 exp, 1 sin, 2 cos.  out_ulp[i] per argument.
+int orc_detmath_ulp(int fn, const double* x, int n, double* out_ulp, double* det_out, double* libm_out) {
+  return guard([&] {
+    for (int i = 0; i < n; ++i) {
+      const double d = fn == 0 ? csf_det::exp(x[i]) : fn == 1 ? csf_det::sin(x[i]) : csf_det::cos(x[i]);
+      const double g = fn == 0 ? std::exp(x[i]) : fn == 1 ? std::sin(x[i]) : std::cos(x[i]);
+      double ulp;
+      if (d == g) {
+        ulp = 0.0;
+      } else {
+        const double a = std::fabs(g);
+        const double step = std::nextafter(a, INFINITY) - a;  // ulp of the glibc value
+        ulp = std::fabs(d - g) / (step > 0.0 ? step : std::numeric_limits<double>::denorm_min());
+      }
+      out_ulp[i] = ulp;
+      if (det_out) det_out[i] = d;
+      if (libm_out) libm_out[i] = g;
+    }
   });
 }
 

@@ -1127,8 +1127,8 @@ TEST("hashed: fusion equals dense fusion on allocated voxels") {
     }
   CHECK(hits > 1000 && worst < 0.03);
 }
-TEST("pipeline: packed channels == single-direction passes; gradient vs FD") {
-  // reduced config-1 style run: 4 frames at 80x60, 40^3 volume
+TEST("pipeline: packed channels == single-direction passes") {
+  // reduced config-1 style run: 4 frames at 80x60, 64^3 volume
   Workload w = make_workload(1, 4, 80, 60);
   PipelineConfig cfg;
   cfg.hashed = false;
@@ -1147,28 +1147,101 @@ TEST("pipeline: packed channels == single-direction passes; gradient vs FD") {
     same = same && one.gradient[0] == packed.gradient[d] && one.objective == packed.objective;
   }
   CHECK(same);
-  // forward-difference style check of the pose-x derivative via real reruns
-  const double eps = 1e-6;
-  auto obj_at = [&](double dx) {
-    Workload w2 = w;
-    PipelineConfig c = cfg;
-    c.directions = {0};
-    c.h = 1e-20;
-    Pose g0 = w.gt[0];
-    (void)g0;
-    // shift the first-frame pose by exp(dx e0) (the seeded direction)
-    Vec6<double> xi{};
-    xi[0] = dx;
-    w2.gt[0] = apply_increment(xi, w.gt[0]);
-    const PipelineResult r = run_pipeline<1>(c, w2.frames, w2.gt);
-    // objective compares against the unshifted truth of the last frame
-    return r;
+}
+
+// CSFD of the whole frame loop against a central finite difference of real
+// reruns with the seed moved by +-eps (the objective keeps the unshifted
+// ground truth), wherever the +-eps runs take every discrete decision of the
+// unperturbed run (iterations, correspondences, blocks, visible, converged,
+// fused voxels per frame).  Dense volumes: the camera sits inside the volume
+// box, so the raycast starts at near_clip for every pose (tsdf.hpp:234-254):
+// the reference's alpha is a double, so CSFD differentiates with the sample
+// positions along each ray held fixed, and a slab entry that moves with the
+// pose (camera outside the box) would shift every sample and make FD and
+// CSFD differ by that (non-differentiable) resampling term.  Hashed volumes
+// have no slab (alpha starts at near_clip).
+template <typename VL, typename VR>
+void csfd_vs_fd(const char* what, VL make_vol, VR make_vol_real, const PipelineConfig& cfg, const Workload& w,
+                double tol) {
+  using S = Lifted<6>;
+  auto vol = make_vol();
+  // a generic base point: the synthetic first pose is exactly on the orbit,
+  // where voxel centres / pixel centres can tie with a threshold (ifloor at an
+  // integer, a zero crossing exactly on a sample) and any perturbation flips
+  // a decision; a small fixed twist moves the seed off those ties
+  const double base[6] = {0.0031, -0.0017, 0.0023, 0.0011, -0.0029, 0.0007};
+  Vec6<S> xi;
+  for (int i = 0; i < 6; ++i) {
+    xi[i] = S(base[i]);
+    xi[i].im[i] = cfg.h;
+  }
+  const LiftedRun<S> lifted = run_lifted<S>(vol, cfg, w.frames, w.gt, xi, lift_intrinsics<S>(cfg.k));
+  const double eps = 1e-9;  // larger steps cross kinks of the piecewise-smooth loop (C0 trilinear cells)
+  auto same_decisions = [&](const LiftedRun<double>& r) {
+    return r.iterations == lifted.iterations && r.correspondences == lifted.correspondences &&
+           r.blocks == lifted.blocks && r.visible == lifted.visible && r.converged == lifted.converged &&
+           r.fused == lifted.fused;
   };
-  const PipelineResult rp = obj_at(eps), rm = obj_at(-eps);
-  std::printf("    pipeline objective %.12g grad[x] %.9g (FD of shifted runs %.9g; iters %d %d %d)\n", packed.objective,
-              packed.gradient[0], (rp.objective - rm.objective) / (2 * eps), packed.iterations[1],
-              packed.iterations[2], packed.iterations[3]);
-  CHECK(std::isfinite(packed.gradient[0]) && std::isfinite(packed.gradient[1]) && std::isfinite(packed.gradient[2]));
+  double worst = 0.0;
+  int compared = 0;
+  for (int d = 0; d < 6; ++d) {
+    double f[2];
+    bool ok = true;
+    for (int sgn = 0; sgn < 2; ++sgn) {
+      auto v = make_vol_real();
+      Vec6<double> x{};
+      for (int i = 0; i < 6; ++i) x[i] = base[i];
+      x[d] = x[d] + (sgn ? -eps : eps);
+      const LiftedRun<double> r = run_lifted<double>(v, cfg, w.frames, w.gt, x, lift_intrinsics<double>(cfg.k));
+      if (!same_decisions(r))
+        for (std::size_t fr = 0; fr < r.iterations.size(); ++fr)
+          if (r.iterations[fr] != lifted.iterations[fr] || r.correspondences[fr] != lifted.correspondences[fr] ||
+              r.fused[fr] != lifted.fused[fr] || r.visible[fr] != lifted.visible[fr])
+            std::printf("      frame %zu: it %d/%d corr %d/%d fused %d/%d visible %d/%d\n", fr, r.iterations[fr],
+                        lifted.iterations[fr], r.correspondences[fr], lifted.correspondences[fr], r.fused[fr],
+                        lifted.fused[fr], r.visible[fr], lifted.visible[fr]);
+      ok = ok && same_decisions(r);
+      f[sgn] = r.objective;
+    }
+    const double fd = (f[0] - f[1]) / (2.0 * eps);
+    const double cs = lifted.objective.im[d] / cfg.h;
+    const double rel = std::fabs(fd - cs) / std::max(std::fabs(cs), 1e-3 * std::fabs(lifted.objective.re) + 1e-12);
+    std::printf("    %s d%d: CSFD %.10g FD %.10g rel %.2e%s\n", what, d, cs, fd, rel, ok ? "" : " (decisions moved)");
+    if (ok) {
+      worst = std::max(worst, rel);
+      ++compared;
+    }
+  }
+  CHECK(compared == 6);
+  CHECK(worst <= tol);
+}
+
+TEST("pipeline: CSFD gradient vs central FD, hashed (config-2 scene, 160x120, 3 frames)") {
+  const Workload w = make_workload(2, 3, 160, 120);
+  PipelineConfig cfg;
+  cfg.hashed = true;
+  cfg.hash = config2_hash();
+  cfg.hash.voxel_size = 0.02;
+  cfg.hash.mu = 0.1;
+  cfg.hash.max_blocks = 1 << 16;
+  cfg.k = w.k;
+  cfg.h = 1e-8;
+  cfg.objective = Objective::kTrajectoryError;
+  csfd_vs_fd("hashed", [&] { return HashedVolumeT<Lifted<6>>(cfg.hash); },
+             [&] { return HashedVolumeT<double>(cfg.hash); }, cfg, w, 1e-5);
+}
+
+TEST("pipeline: CSFD gradient vs central FD, dense with the camera inside the box (config-1 scene, 80x60)") {
+  const Workload w = make_workload(1, 3, 80, 60);
+  PipelineConfig cfg;
+  cfg.hashed = false;
+  cfg.dense = VolumeParams::cube(64, 0.04, Vec3d(-1.28, -1.28, -0.1));  // contains the 1 m orbit at z = 1.4
+  cfg.dense.mu = 0.12;
+  cfg.k = w.k;
+  cfg.h = 1e-20;
+  cfg.objective = Objective::kFinalTranslationError;
+  csfd_vs_fd("dense", [&] { return TsdfVolumeT<Lifted<6>>(cfg.dense); },
+             [&] { return TsdfVolumeT<double>(cfg.dense); }, cfg, w, 1e-5);
 }
 
 }  // namespace

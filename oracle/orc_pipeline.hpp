@@ -145,7 +145,7 @@ template <typename S>
 Vec6<S> keyframe_xi(const PipelineConfig& cfg, int kf) {
   Vec6<S> xi;
   for (int i = 0; i < 6; ++i) xi[i] = S(0.0);
-  if constexpr (!std::is_same_v<S, Bicomplex>) {
+  if constexpr (!std::is_same_v<S, Bicomplex> && !std::is_same_v<S, double>) {
     for (std::size_t d = 0; d < cfg.directions.size(); ++d) {
       const int c = cfg.directions[d] - (10 + 6 * (kf - 1));
       if (c >= 0 && c < 6) xi[c].im[d] = cfg.h;
