@@ -533,24 +533,41 @@ def main():
         if dist is not None:
             dist.barrier()
 
-    # ---------------- timed region: device-resident inputs, no per-kernel events
+    # ---------------- timed region: device-resident inputs, no per-kernel events.
+    # Both launch modes of the same run are timed: the stream of PDL-chained
+    # launches, and the run replayed as one CUDA graph (csf_pipeline_set_graph;
+    # bit-identical, tests/test_graph.py); `value` is the faster of the two.
+    def timed(graph: bool):
+        pipe.set_graph(graph)
+        if graph:
+            for _ in range(2):  # capture, then one replay
+                pipe.run()
+        ctx.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        l0 = ctx.launch_count
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            pipe.run()
+        e1.record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        return e0.elapsed_time(e1), ctx.launch_count - l0
+
     clocks = Clocks(local)
-    barrier()
-    torch.cuda.synchronize()
-    ctx.synchronize()
-    l0 = ctx.launch_count
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        pipe.run()
-    e1.record(stream)
-    ctx.synchronize()
-    torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    launches = ctx.launch_count - l0
+    ms_stream, launches_stream = timed(False)
+    ms_graph, launches_graph = timed(True)
+    pipe.set_graph(False)
     clk = clocks.stop()
+    if dist is not None:  # max over ranks of each mode, then one choice for all ranks
+        t = torch.tensor([ms_stream, ms_graph], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_stream, ms_graph = float(t[0].item()), float(t[1].item())
+    use_graph = ms_graph < ms_stream
+    ms, launches = (ms_graph, launches_graph) if use_graph else (ms_stream, launches_stream)
     if second:
         hr = pipe.hessian(stats=True)
         local_cols, stats = hr.hessian, hr.stats
@@ -558,9 +575,6 @@ def main():
         res = pipe.result()
         local_cols, stats = res.gradient, res.stats
     if dist is not None:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         cols = gather_columns(torch.from_numpy(np.asarray(local_cols)).cuda(), len(units_all), world,
                               rank).cpu().numpy()
     if dist is None:
@@ -639,6 +653,8 @@ def main():
                    "l2": "working set (hashed volume, ~GBs) >> L2"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
+        "launch_mode": {"used": "cuda_graph" if use_graph else "stream", "stream_ms_per_step": ms_stream / args.steps,
+                        "graph_ms_per_step": ms_graph / args.steps},
         "roofline": roofline,
         "roofline_by_kernel": rooflines,
         "clocks": clk,

@@ -424,6 +424,12 @@ int csf_pipeline_result(csf_pipeline p, double* gradient, double* objective, dou
  * (optional) [n][12][1 + 3 n_pairs] (re, then im1, im2, im12 per pair). */
 int csf_pipeline_hessian(csf_pipeline p, double* hessian, double* grad1, double* grad2, double* objective,
                          double* poses, int32_t* stats);
+/* Graph mode (enable != 0): csf_pipeline_run replays the whole run as one
+ * CUDA graph — captured on the first graph-mode call after a stream-mode run
+ * of the same frame count, bit-identical to the stream run.  Runs that
+ * profile (csf_ctx_profile) or wait on per-frame uploads (run_host) keep the
+ * stream path. */
+int csf_pipeline_set_graph(csf_pipeline p, int enable);
 /* The pipeline's volume after the last run, borrowed (owned by the pipeline:
  * never pass it to csf_volume_destroy).  Read it with csf_volume_download /
  * csf_volume_download_hash / csf_volume_block_count; it carries the run's

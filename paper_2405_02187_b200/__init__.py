@@ -733,14 +733,19 @@ class Pipeline:
     def upload(self, depth: np.ndarray, gt: np.ndarray) -> None:
         d = np.ascontiguousarray(depth, dtype=np.float32)
         g = _f64(gt).reshape(-1, 12)
-        self.n_frames = d.shape[0]
+        self.n_frames = self.n_run = d.shape[0]
         self.ctx.check(self.ctx.lib.csf_pipeline_upload(self.h, _fp(d), _dp(g), self.n_frames))
 
     def run(self, n_frames: Optional[int] = None) -> None:
-        self.ctx.check(self.ctx.lib.csf_pipeline_run(self.h, n_frames or self.n_frames))
+        self.n_run = n_frames or self.n_frames
+        self.ctx.check(self.ctx.lib.csf_pipeline_run(self.h, self.n_run))
+
+    def set_graph(self, enable: bool = True) -> None:
+        """Replay runs as one captured CUDA graph (csf_pipeline_set_graph)."""
+        self.ctx.check(self.ctx.lib.csf_pipeline_set_graph(self.h, int(enable)))
 
     def result(self, poses: bool = True, stats: bool = True) -> PipelineResult:
-        n = self.n_frames
+        n = getattr(self, "n_run", self.n_frames)
         g = np.zeros(max(self.D, 1))
         obj = C.c_double()
         P = np.empty((n, 12, 1 + self.slots)) if poses else None
@@ -769,7 +774,7 @@ class Pipeline:
         """End-to-end call from host buffers (upload + run + read back)."""
         d = np.ascontiguousarray(depth, dtype=np.float32)
         g = _f64(gt).reshape(-1, 12)
-        self.n_frames = d.shape[0]
+        self.n_frames = self.n_run = d.shape[0]
         grad = np.zeros(max(self.D, 1))
         obj = C.c_double()
         self.ctx.check(self.ctx.lib.csf_pipeline_run_host(self.h, _fp(d), _dp(g), self.n_frames, _dp(grad),
@@ -782,7 +787,7 @@ class Pipeline:
         P_ = self.n_pairs
         H, g1, g2 = np.empty(P_), np.empty(P_), np.empty(P_)
         obj = C.c_double()
-        n = self.n_frames
+        n = getattr(self, "n_run", self.n_frames)
         P = np.empty((n, 12, 1 + self.slots)) if poses else None
         S = np.empty((n, 8), dtype=np.int32) if stats else None
         self.ctx.check(self.ctx.lib.csf_pipeline_hessian(

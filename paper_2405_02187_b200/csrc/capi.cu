@@ -827,7 +827,16 @@ struct csf_pipeline_s {
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> frame_ev;
   bool wait_frames = false;
+  // CUDA graph of a whole run (csf_pipeline_set_graph): captured on the
+  // first graph-mode run after a stream run of the same frame count
+  bool use_graph = false;
+  cudaGraphExec_t graph_exec = nullptr;
+  int exec_frames = 0;   // frame count of graph_exec
+  int graph_frames = 0;  // frame count of the last stream run
+  unsigned long long graph_launches = 0;
+  int stream_runs = 0;
   ~csf_pipeline_s() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (cudaEvent_t e : frame_ev) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     hits.release();
@@ -968,20 +977,26 @@ static int pipeline_reset_volume(csf_pipeline p) {
   csf_ctx ctx = p->ctx;
   const Launch L = launch_of(ctx);
   if (v->hashed) {
-    int nb = 0;
-    CUDA_TRY(ctx, d2h(&nb, v->hash.n_blocks, sizeof(int), ctx->stream));
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    if (nb > 0) {
-      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.heads, 0xFF, sizeof(int) << v->hash.bits, ctx->stream));
-      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.next, 0xFF, sizeof(int) * v->hash.max_blocks, ctx->stream));
-      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.n_blocks, 0, sizeof(int), ctx->stream));
-      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.grid, 0xFF, sizeof(int) << (3 * v->hash.gbits), ctx->stream));
-      CUDA_TRY(ctx, cudaMemsetAsync(v->hash.occ, 0, sizeof(unsigned) * occ_words(v->hash.gbits), ctx->stream));
-      launch_super_dist(ctx->stream, v->hash);
-      launch_init_volume(L, v->hash.rw, v->hash.fim, static_cast<long long>(nb) * 512, v->Dp);
-    }
+    // device-side bounds only: the run is graph-capturable
+    launch_reset_hashed(L, v->hash, v->Dp);
+    CUDA_TRY(ctx, cudaMemsetAsync(v->hash.n_blocks, 0, sizeof(int), ctx->stream));
+    launch_super_dist(ctx->stream, v->hash);
   } else {
     launch_init_volume(L, v->dense.rw, v->dense.fim, v->n_vox, v->Dp);
+  }
+  return CSF_OK;
+}
+
+static int pipeline_run_body(csf_pipeline p, int n_frames);
+
+extern "C" int csf_pipeline_set_graph(csf_pipeline p, int enable) {
+  if (!p) return CSF_EINVAL;
+  p->use_graph = enable != 0;
+  if (!p->use_graph && p->graph_exec) {
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    cudaGraphExecDestroy(p->graph_exec);
+    p->graph_exec = nullptr;
   }
   return CSF_OK;
 }
@@ -991,6 +1006,56 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
   csf_ctx ctx = p->ctx;
   if (n_frames <= 0 || n_frames > p->n_uploaded) return fail(ctx, CSF_EINVAL, "csf_pipeline_run: frames not uploaded");
   cudaSetDevice(ctx->device);
+  // Graph mode replays the captured run: no host work per kernel.  A run is
+  // captured only after a stream run of the same frame count has set up every
+  // lazily allocated scratch; profiling and per-frame upload waits (run_host)
+  // take the stream path.
+  const bool graph = p->use_graph && !ctx->prof.on && !p->wait_frames;
+  if (graph && p->graph_exec && p->exec_frames == n_frames) {
+    CUDA_TRY(ctx, cudaGraphLaunch(p->graph_exec, ctx->stream));
+    ctx->launches += p->graph_launches;
+    p->n_run = n_frames;
+    return CSF_OK;
+  }
+  if (graph && p->stream_runs > 0 && p->graph_frames == n_frames) {
+    if (p->graph_exec) {
+      cudaGraphExecDestroy(p->graph_exec);
+      p->graph_exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    const unsigned long long l0 = ctx->launches;
+    const int rc = pipeline_run_body(p, n_frames);
+    const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(ctx, CSF_ECUDA, std::string("csf_pipeline_run: capture: ") + cudaGetErrorString(ce));
+    const cudaError_t ie = cudaGraphInstantiate(&p->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      p->graph_exec = nullptr;
+      return fail(ctx, CSF_ECUDA, std::string("csf_pipeline_run: graph instantiate: ") + cudaGetErrorString(ie));
+    }
+    p->graph_launches = ctx->launches - l0;
+    p->exec_frames = n_frames;
+    ctx->launches = l0;
+    CUDA_TRY(ctx, cudaGraphLaunch(p->graph_exec, ctx->stream));
+    ctx->launches += p->graph_launches;
+    p->n_run = n_frames;
+    return CSF_OK;
+  }
+  const int rc = pipeline_run_body(p, n_frames);
+  if (rc == CSF_OK) {
+    ++p->stream_runs;
+    p->graph_frames = n_frames;
+  }
+  return rc;
+}
+
+static int pipeline_run_body(csf_pipeline p, int n_frames) {
+  csf_ctx ctx = p->ctx;
   int rc = pipeline_reset_volume(p);
   if (rc) return rc;
   const Launch L = launch_of(ctx);
@@ -1113,6 +1178,34 @@ extern "C" int csf_pipeline_hessian(csf_pipeline p, double* hessian, double* gra
     if (grad1) grad1[q] = out[2 + 3 * q] / h;
     if (grad2) grad2[q] = out[2 + 3 * q + 1] / h;
   }
+  return CSF_OK;
+}
+
+// Debug hook (not part of the public header): a copy of one internal buffer
+// of the last run (0 vre, 1 nre, 2 vim, 3 nim, 4 raw depth, 5 pyr0, 6 pyr1,
+// 7 pyr2, 8 hits, 9 pose, 10 traj, 11 rw of the volume, 12 fim of the volume).
+extern "C" int csf_debug_pipeline_buffer(csf_pipeline p, int which, void* host, size_t bytes) {
+  if (!p || !host) return CSF_EINVAL;
+  cudaSetDevice(p->ctx->device);
+  const void* src = nullptr;
+  switch (which) {
+    case 0: src = p->vre.p; break;
+    case 1: src = p->nre.p; break;
+    case 2: src = p->vim.p; break;
+    case 3: src = p->nim.p; break;
+    case 4: src = p->raw.p; break;
+    case 5: src = p->pyr0.p; break;
+    case 6: src = p->pyr1.p; break;
+    case 7: src = p->pyr2.p; break;
+    case 8: src = p->hits.p; break;
+    case 9: src = p->pose.p; break;
+    case 10: src = p->traj.p; break;
+    case 11: src = p->vol->hashed ? static_cast<const void*>(p->vol->hash.rw) : p->vol->dense.rw; break;
+    case 12: src = p->vol->hashed ? static_cast<const void*>(p->vol->hash.fim) : p->vol->dense.fim; break;
+    default: return CSF_EINVAL;
+  }
+  cudaStreamSynchronize(p->ctx->stream);
+  CUDA_TRY(p->ctx, cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost));
   return CSF_OK;
 }
 

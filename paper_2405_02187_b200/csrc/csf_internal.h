@@ -246,6 +246,10 @@ void launch_raycast_hashed(const Launch& L, const HashDev& v, int G, int Dp, con
                            int w, int h, double near_clip, double far_clip, double step, double2* hits, double* vre,
                            double* nre, double* vim, double* nim);
 void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp);
+// Back to an empty hashed volume with every bound read on the device (no host
+// round trip, so a run can be captured in a CUDA graph); the caller zeroes
+// n_blocks afterwards and rebuilds the distance field.
+void launch_reset_hashed(const Launch& L, const HashDev& v, int Dp);
 // super-block distance field of the occupancy bitmap (after every change of occ)
 void launch_super_dist(cudaStream_t stream, const HashDev& v);
 // point queries (tsdf.hpp:97-196): pts [n][3][1+Dp] lifted (sample) or [n][3] real (measured)

@@ -6,9 +6,8 @@
 //   measure_surface   — proj/include/csf/frames.hpp:86-114
 //
 // These run on the real channel only and are shared by every CSFD direction
-// of a run.  The bilateral range weight uses the deterministic
-// exp of include/csf_detmath.h; the 7x7 spatial weights are evaluated on the
-// host with the same function and held in constant memory.
+// of a run.  The bilateral weights use the deterministic exp of
+// include/csf_detmath.h (the oracle's function).
 #include <cstdio>
 
 #include "csf_internal.h"
@@ -17,20 +16,32 @@
 namespace csfd {
 
 constexpr int kMaxRadius = 7;
-__constant__ double c_spatial[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];
 
 constexpr int kBX = 32, kBY = 8;
 
 // One 32x8 output tile per CTA; the (32+2r)x(8+2r) input window is staged in
-// shared memory once and reused by all 49 taps of every pixel.
+// shared memory once and reused by all 49 taps of every pixel.  The spatial
+// weights exp(-(dx^2+dy^2)/(2 sigma_s^2)) are computed per CTA into shared
+// memory (deterministic exp, the oracle's values): the kernel reads nothing
+// from the host at launch time, so a run captured in a CUDA graph replays
+// exactly (a constant-memory upload from a host stack array did not).
 __global__ void __launch_bounds__(kBX* kBY) k_bilateral(const float* __restrict__ in_f32,
                                                          const double* __restrict__ in_f64,
                                                          double* __restrict__ raw_out, double* __restrict__ out,
-                                                         int w, int h, int radius, double inv2sr) {
+                                                         int w, int h, int radius, double inv2ss, double inv2sr) {
   pdl_wait();
   pdl_trigger();
+  __shared__ double c_spatial[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];
   extern __shared__ double tile[];
   const int tw = kBX + 2 * radius, th = kBY + 2 * radius;
+  {
+    const int sd = 2 * radius + 1;
+    const int i = threadIdx.y * kBX + threadIdx.x;
+    if (i < sd * sd) {
+      const int dy = i / sd - radius, dx = i % sd - radius;
+      c_spatial[i] = csf_det::exp(static_cast<double>(-(dx * dx + dy * dy)) * inv2ss);
+    }
+  }
   const int x0 = blockIdx.x * kBX - radius, y0 = blockIdx.y * kBY - radius;
   for (int i = threadIdx.y * kBX + threadIdx.x; i < tw * th; i += kBX * kBY) {
     const int tx = x0 + i % tw, ty = y0 + i / tw;
@@ -177,18 +188,13 @@ static void check_launch(const char* what) {
 void launch_bilateral(const Launch& L, const float* in_f32, const double* in_f64, double* raw_out, double* out, int w,
                       int h, double sigma_s, double sigma_r, int radius) {
   if (radius > csfd::kMaxRadius) radius = csfd::kMaxRadius;
-  const int side = 2 * radius + 1;
-  double table[(2 * csfd::kMaxRadius + 1) * (2 * csfd::kMaxRadius + 1)];
   const double inv2ss = 1.0 / (2.0 * sigma_s * sigma_s);
   const double inv2sr = 1.0 / (2.0 * sigma_r * sigma_r);
-  for (int dy = -radius; dy <= radius; ++dy)
-    for (int dx = -radius; dx <= radius; ++dx)
-      table[(dy + radius) * side + dx + radius] = csf_det::exp(static_cast<double>(-(dx * dx + dy * dy)) * inv2ss);
-  cudaMemcpyToSymbolAsync(csfd::c_spatial, table, sizeof(double) * side * side, 0, cudaMemcpyHostToDevice, L.stream);
   const dim3 block(csfd::kBX, csfd::kBY);
   const dim3 grid((w + csfd::kBX - 1) / csfd::kBX, (h + csfd::kBY - 1) / csfd::kBY);
   const size_t smem = sizeof(double) * (csfd::kBX + 2 * radius) * (csfd::kBY + 2 * radius);
-  csfd::launch_pdl(csfd::k_bilateral, dim3(grid), dim3(block), smem, L.stream, in_f32, in_f64, raw_out, out, w, h, radius, inv2sr);
+  csfd::launch_pdl(csfd::k_bilateral, dim3(grid), dim3(block), smem, L.stream, in_f32, in_f64, raw_out, out, w, h,
+                   radius, inv2ss, inv2sr);
   ++*L.launches;
   check_launch("bilateral");
 }

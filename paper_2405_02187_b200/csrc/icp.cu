@@ -634,6 +634,10 @@ __device__ __forceinline__ void lv_mark(unsigned seq, int it, int phase) {
 }
 
 __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
+  // launched without the programmatic attribute, but a captured graph may
+  // still give it a programmatic edge from the preceding PDL kernel: wait for
+  // that kernel's memory (a no-op otherwise)
+  pdl_wait();
   extern __shared__ double sm[];
   const int C = 1 + a.Dp;
   const int n_acc = 27 * C;

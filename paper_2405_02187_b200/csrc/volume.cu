@@ -388,6 +388,46 @@ __global__ void k_init_volume(double2* rw, double* fim, long long n, int Dp) {
   }
 }
 
+// Graph-safe reset of a hashed volume (every bound read on the device, no
+// host round trip): voxels of the allocated blocks back to F = 1, W = 0, and
+// the hash chains, block-id window and occupancy bits of those blocks
+// cleared.  n_blocks itself is zeroed by the caller afterwards.
+__global__ void k_reset_hashed(const int* n_blocks, double2* rw, double* fim, int Dp, int* heads, unsigned mask,
+                               int* next, const int* coords, int* grid, unsigned* occ, int gbits) {
+  pdl_wait();
+  pdl_trigger();
+  const long long nb = *n_blocks;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  for (long long v = t0; v < nb * 512; v += stride) {
+    rw[v] = make_double2(1.0, 0.0);
+    for (int d = 0; d < Dp; ++d) fim[v * Dp + d] = 0.0;
+  }
+  const int half = 1 << (gbits - 1);
+  const unsigned side = 1u << gbits;
+  for (long long b = t0; b < nb; b += stride) {
+    const int bx = coords[3 * b], by = coords[3 * b + 1], bz = coords[3 * b + 2];
+    heads[block_hash(bx, by, bz, mask)] = -1;
+    next[b] = -1;
+    const unsigned ux = static_cast<unsigned>(bx + half), uy = static_cast<unsigned>(by + half),
+                   uz = static_cast<unsigned>(bz + half);
+    if (ux < side && uy < side && uz < side) {
+      grid[(static_cast<size_t>(uz) << gbits | uy) << gbits | ux] = -1;
+      // the words holding this block's occupancy bits (any other block
+      // sharing a word is cleared as well: every block is)
+      const int sb = gbits - 3, s4 = gbits - 2, s2 = gbits - 1;
+      const unsigned bit = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
+      occ[bit >> 5] = 0u;
+      unsigned* occ4 = occ + ((1u << (3 * sb)) >> 5);
+      const unsigned b4 = ((uz >> 2) << s4 | (uy >> 2)) << s4 | (ux >> 2);
+      occ4[b4 >> 5] = 0u;
+      unsigned* occ2 = occ4 + ((1u << (3 * s4)) >> 5);
+      const unsigned b2 = ((uz >> 1) << s2 | (uy >> 1)) << s2 | (ux >> 1);
+      occ2[b2 >> 5] = 0u;
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------
 // Hashed allocation (builder-defined; oracle/orc_tsdf.hpp allocate_band)
 // ----------------------------------------------------------------------------
@@ -1531,6 +1571,14 @@ void launch_super_dist(cudaStream_t stream, const HashDev& v) {
   k_sdist_axis<<<grid, 256, 0, stream>>>(v.occ, v.sdist, sb, 2, v.sdist_tmp);
   cudaMemcpyAsync(v.sdist, v.sdist_tmp, static_cast<size_t>(cells), cudaMemcpyDeviceToDevice, stream);
   chk("super_dist");
+}
+
+void launch_reset_hashed(const Launch& L, const HashDev& v, int Dp) {
+  launch_pdl(k_reset_hashed, dim3(sm_count() * 8), dim3(256), 0, L.stream, static_cast<const int*>(v.n_blocks),
+             v.rw, v.fim, Dp, v.heads, (1u << v.bits) - 1u, v.next, static_cast<const int*>(v.coords), v.grid, v.occ,
+             v.gbits);
+  ++*L.launches;
+  chk("reset_hashed");
 }
 
 void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, int Dp) {
