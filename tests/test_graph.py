@@ -2,14 +2,16 @@
 bit-identical to the stream run, on every replay.
 
 Round 1 found a graph replay whose frame-1 association differed from the
-stream run and settled after two replays.  Cause: the volume reset read the
-previous run's block count on the host (a D2H + sync inside csf_pipeline_run)
-and sized its memsets and the voxel re-initialisation from it, so a captured
-run froze the block count seen at capture time — zero when the capture came
-before the first run — and its replays fused into a volume whose blocks were
-never reset.  The reset is now one kernel that reads n_blocks on the device
-(launch_reset_hashed), so the run has no host-side dependence on device state
-and captures exactly."""
+stream run and settled after a couple of replays.  Root cause: the bilateral
+filter uploaded its 7x7 spatial weights with cudaMemcpyToSymbolAsync from an
+array on the host stack.  In a stream the pageable copy is staged at call
+time; captured, the memcpy node re-reads that dead stack frame on every
+replay, so the replays filtered with whatever the stack held (the frame-1
+pyramid differed in every pixel; the raw depth did not).  The weights are now
+computed per CTA on the device.  A second capture hazard went with it: the
+volume reset read the previous run's block count on the host; it is now one
+kernel that reads n_blocks on the device (launch_reset_hashed).
+"""
 import ctypes as C
 
 import numpy as np
