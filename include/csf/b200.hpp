@@ -18,6 +18,7 @@
 #include <array>
 #include <cmath>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -121,6 +122,14 @@ class Volume {
   }
   Volume(Context& c, const csf_hash_params& p, int channels) : ctx_(c.get()), channels_(channels), hashed_(true) {
     check(ctx_, csf_volume_create_hashed(ctx_, &p, channels, &vol_));
+  }
+  // adopts a handle from csf_volume_load
+  Volume(Context& c, csf_volume v) : ctx_(c.get()), vol_(v) {
+    int hashed = 0;
+    long long n = 0;
+    check(ctx_, csf_volume_info(vol_, &channels_, &hashed, &n));
+    hashed_ = hashed != 0;
+    n_ = static_cast<size_t>(n);
   }
   ~Volume() { csf_volume_destroy(vol_); }
   Volume(const Volume&) = delete;
@@ -498,6 +507,222 @@ inline SurfaceMaps predict_maps(const SurfelMap& map, const std::array<double, 1
 }
 // surfel.cpp:110-119
 inline double sample_confidence(const csf_intrinsics& k, int x, int y) { return csf_sample_confidence(&k, x, y); }
+
+
+// ---------------------------------------------------------------------------
+// frames.hpp:86-114 measure_surface: depth [h][w] real (or [h][w][1+D] lifted
+// with the intrinsics' D channels); maps [h][w][3][1+D]
+// ---------------------------------------------------------------------------
+inline SurfaceMaps measure_surface(Context& c, const Image<double>& depth, const csf_intrinsics& k) {
+  SurfaceMaps m;
+  m.width = depth.width;
+  m.height = depth.height;
+  m.vertices.resize(static_cast<size_t>(depth.width) * depth.height * 3);
+  m.normals.resize(m.vertices.size());
+  const LiftedIntrinsics kk(k, 0);
+  check(c.get(), csf_measure_surface(c.get(), depth.data.data(), depth.width, depth.height, kk.v.data(), 0,
+                                     m.vertices.data(), m.normals.data()));
+  return m;
+}
+inline SurfaceMaps measure_surface(Context& c, const std::vector<double>& lifted_depth, int w, int h,
+                                   const LiftedIntrinsics& k) {
+  if (lifted_depth.size() != static_cast<size_t>(w) * h * (1 + k.channels))
+    throw std::invalid_argument("measure_surface: lifted depth size");
+  SurfaceMaps m;
+  m.width = w;
+  m.height = h;
+  m.channels = k.channels;
+  m.vertices.resize(static_cast<size_t>(w) * h * 3 * (1 + k.channels));
+  m.normals.resize(m.vertices.size());
+  check(c.get(), csf_measure_surface(c.get(), lifted_depth.data(), w, h, k.v.data(), k.channels, m.vertices.data(),
+                                     m.normals.data()));
+  return m;
+}
+
+// tsdf.cpp:11-40 with the reference's Image<Complex> depth (tsdf.hpp:144-145):
+// lifted depth [h][w][1+D], D = the volume's channels
+inline int surface_update(Context& c, Volume& vol, const std::vector<double>& lifted_depth, int w, int h,
+                          const LiftedPose& camera_to_world, const LiftedIntrinsics& k) {
+  if (camera_to_world.channels != vol.channels() || k.channels != vol.channels() ||
+      lifted_depth.size() != static_cast<size_t>(w) * h * (1 + vol.channels()))
+    throw std::invalid_argument("surface_update: channel count mismatch");
+  int n_visible = 0;
+  check(c.get(), csf_surface_update_lifted(vol.get(), lifted_depth.data(), w, h, camera_to_world.v.data(),
+                                           k.v.data(), &n_visible));
+  return n_visible;
+}
+
+// tsdf.hpp:148-196 sample_tsdf / sample_gradient at a lifted world point
+// [3][1+D] (D = the volume's channels): std::nullopt where the reference
+// returns no value.
+using Lifted = std::vector<double>;  // [1+D]
+inline std::optional<Lifted> sample_tsdf(const Volume& vol, const std::vector<double>& point) {
+  const int C = 1 + vol.channels();
+  if (point.size() != static_cast<size_t>(3 * C)) throw std::invalid_argument("sample_tsdf: point is [3][1+D]");
+  Lifted out(C);
+  int32_t ok = 0;
+  check(vol.ctx(), csf_sample_tsdf(vol.get(), point.data(), 1, out.data(), &ok));
+  if (!ok) return std::nullopt;
+  return out;
+}
+inline std::optional<std::array<Lifted, 3>> sample_gradient(const Volume& vol, const std::vector<double>& point) {
+  const int C = 1 + vol.channels();
+  if (point.size() != static_cast<size_t>(3 * C)) throw std::invalid_argument("sample_gradient: point is [3][1+D]");
+  std::vector<double> out(3 * C);
+  int32_t ok = 0;
+  check(vol.ctx(), csf_sample_gradient(vol.get(), point.data(), 1, out.data(), &ok));
+  if (!ok) return std::nullopt;
+  std::array<Lifted, 3> g;
+  for (int a = 0; a < 3; ++a) g[a].assign(out.begin() + a * C, out.begin() + (a + 1) * C);
+  return g;
+}
+
+// tsdf.hpp:97-140 measured_tsdf(depth, world_to_camera, k, mu, p_world,
+// camera_center): depth real [h][w] or lifted [h][w][1+D]; psi [1+D]
+inline std::optional<Lifted> measured_tsdf(Context& c, const std::vector<double>& depth, int w, int h,
+                                           const LiftedPose& world_to_camera, const LiftedIntrinsics& k, double mu,
+                                           const std::array<double, 3>& p_world,
+                                           const std::vector<double>& camera_center) {
+  const int D = world_to_camera.channels, C = 1 + D;
+  if (k.channels != D || camera_center.size() != static_cast<size_t>(3 * C))
+    throw std::invalid_argument("measured_tsdf: channel count mismatch");
+  const size_t P = static_cast<size_t>(w) * h;
+  const bool lifted = depth.size() == P * C && D > 0;
+  if (!lifted && depth.size() != P) throw std::invalid_argument("measured_tsdf: depth size");
+  Lifted psi(C);
+  int32_t ok = 0;
+  check(c.get(), (lifted ? csf_measured_tsdf_lifted : csf_measured_tsdf)(
+                     c.get(), depth.data(), w, h, world_to_camera.v.data(), k.v.data(), mu, p_world.data(),
+                     camera_center.data(), 1, D, psi.data(), &ok));
+  if (!ok) return std::nullopt;
+  return psi;
+}
+
+// tsdf.hpp:288-289 / tsdf.cpp:61-153 — the "CSFVOL 1" checkpoint
+inline void save_volume(const std::string& path, const Volume& vol) {
+  check(vol.ctx(), csf_volume_save(vol.get(), path.c_str()));
+}
+inline std::unique_ptr<Volume> load_volume(Context& c, const std::string& path, int channels = -1) {
+  csf_volume v = nullptr;
+  check(c.get(), csf_volume_load(c.get(), path.c_str(), channels, &v));
+  return std::unique_ptr<Volume>(new Volume(c, v));
+}
+
+// icp.cpp:89-126 associate(measured, predicted, camera_to_world,
+// prediction_camera_to_world, k, cfg, stride): real maps [h][w][3]
+inline std::vector<Correspondence> associate(Context& c, const SurfaceMaps& measured, const SurfaceMaps& predicted,
+                                             const std::array<double, 12>& camera_to_world,
+                                             const std::array<double, 12>& prediction_camera_to_world,
+                                             const csf_intrinsics& k, const csf_icp_cfg& cfg, int pixel_stride = 1) {
+  if (measured.channels != 0 || predicted.channels != 0) throw std::invalid_argument("associate: real maps");
+  const size_t P = static_cast<size_t>(measured.width) * measured.height;
+  std::vector<double> flat(P * 9);
+  int n = 0;
+  check(c.get(), csf_associate(c.get(), measured.vertices.data(), measured.normals.data(), predicted.vertices.data(),
+                               predicted.normals.data(), measured.width, measured.height, camera_to_world.data(),
+                               prediction_camera_to_world.data(), &k, &cfg, pixel_stride, flat.data(), &n));
+  std::vector<Correspondence> out(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i)
+    for (int q = 0; q < 3; ++q) {
+      out[i].vertex[q] = flat[9 * i + q];
+      out[i].model_vertex[q] = flat[9 * i + 3 + q];
+      out[i].model_normal[q] = flat[9 * i + 6 + q];
+    }
+  return out;
+}
+// icp.cpp:146-153 linearized_step(corrs, base)
+inline std::array<double, 6> linearized_step(Context& c, const std::vector<Correspondence>& corrs,
+                                             const std::array<double, 12>& base) {
+  const std::vector<double> flat = detail::pack(corrs);
+  std::array<double, 6> d{};
+  check(c.get(), csf_linearized_step(c.get(), flat.data(), static_cast<int>(corrs.size()), base.data(), d.data()));
+  return d;
+}
+
+// diff.hpp:16-37 pairwise_sum(terms, init = 0) — the reference's fixed tree
+inline double pairwise_sum(Context& c, const std::vector<double>& terms, double init = 0.0) {
+  double out = 0.0;
+  check(c.get(), csf_pairwise_sum(c.get(), terms.data(), static_cast<int>(terms.size()), 1, &out));
+  return init + out;
+}
+
+// ---------------------------------------------------------------------------
+// csfd.hpp:33-140 truncated first- and second-order CSFD scalars and
+// diff.hpp:46-72 csfd_gradient / csfd_hessian of a user function f(x) with x
+// a 6-vector of those scalars.  Host arithmetic (f is user code); the
+// concrete functions of the hot path (icp_gradient / icp_hessian,
+// reloc_gradient / reloc_hessian, the pipeline) run as packed device passes.
+// ---------------------------------------------------------------------------
+struct Complex {
+  double re = 0.0, im = 0.0;
+  Complex() = default;
+  Complex(double r, double i = 0.0) : re(r), im(i) {}
+};
+inline Complex operator+(Complex a, Complex b) { return {a.re + b.re, a.im + b.im}; }
+inline Complex operator-(Complex a, Complex b) { return {a.re - b.re, a.im - b.im}; }
+inline Complex operator-(Complex a) { return {-a.re, -a.im}; }
+inline Complex operator*(Complex a, Complex b) { return {a.re * b.re, a.re * b.im + a.im * b.re}; }
+inline Complex operator/(Complex a, Complex b) {
+  if (b.re == 0.0) throw std::domain_error("Complex division by zero real part");
+  return {a.re / b.re, (a.im * b.re - a.re * b.im) / (b.re * b.re)};
+}
+inline Complex sqrt(Complex a) {
+  const double r = std::sqrt(a.re);
+  return {r, a.im * (0.5 / r)};
+}
+inline Complex sin(Complex a) { return {std::sin(a.re), std::cos(a.re) * a.im}; }
+inline Complex cos(Complex a) { return {std::cos(a.re), -std::sin(a.re) * a.im}; }
+inline Complex exp(Complex a) {
+  const double e = std::exp(a.re);
+  return {e, e * a.im};
+}
+struct Bicomplex {
+  double re = 0.0, im1 = 0.0, im2 = 0.0, im12 = 0.0;
+  Bicomplex() = default;
+  Bicomplex(double r, double a = 0.0, double b = 0.0, double ab = 0.0) : re(r), im1(a), im2(b), im12(ab) {}
+};
+inline Bicomplex operator+(Bicomplex a, Bicomplex b) {
+  return {a.re + b.re, a.im1 + b.im1, a.im2 + b.im2, a.im12 + b.im12};
+}
+inline Bicomplex operator-(Bicomplex a, Bicomplex b) {
+  return {a.re - b.re, a.im1 - b.im1, a.im2 - b.im2, a.im12 - b.im12};
+}
+inline Bicomplex operator-(Bicomplex a) { return {-a.re, -a.im1, -a.im2, -a.im12}; }
+inline Bicomplex operator*(Bicomplex a, Bicomplex b) {
+  return {a.re * b.re, a.re * b.im1 + a.im1 * b.re, a.re * b.im2 + a.im2 * b.re,
+          a.re * b.im12 + a.im12 * b.re + a.im1 * b.im2 + a.im2 * b.im1};
+}
+inline Bicomplex operator/(Bicomplex a, Bicomplex b) {
+  if (b.re == 0.0) throw std::domain_error("Bicomplex division by zero real part");
+  const double inv = 1.0 / b.re, inv2 = inv * inv;
+  const double q1 = (a.im1 * b.re - a.re * b.im1) * inv2;
+  const double q2 = (a.im2 * b.re - a.re * b.im2) * inv2;
+  const double q12 = (a.im12 - (a.re * inv) * b.im12 - q1 * b.im2 - q2 * b.im1) * inv;
+  return {a.re * inv, q1, q2, q12};
+}
+template <typename F>
+std::array<double, 6> csfd_gradient(F&& f, const std::array<double, 6>& x, double h = 1e-8) {
+  if (!(h > 0.0) || h > 1e-6) throw std::invalid_argument("StepSize: step must satisfy 0 < h <= 1e-6");
+  std::array<double, 6> g{};
+  for (int i = 0; i < 6; ++i) {
+    std::array<Complex, 6> xc;
+    for (int j = 0; j < 6; ++j) xc[j] = Complex(x[j], i == j ? h : 0.0);
+    g[i] = f(xc).im / h;
+  }
+  return g;
+}
+template <typename F>
+std::array<std::array<double, 6>, 6> csfd_hessian(F&& f, const std::array<double, 6>& x, double h = 1e-8) {
+  if (!(h > 0.0) || h > 1e-6) throw std::invalid_argument("StepSize: step must satisfy 0 < h <= 1e-6");
+  std::array<std::array<double, 6>, 6> H{};
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j <= i; ++j) {
+      std::array<Bicomplex, 6> xb;
+      for (int k = 0; k < 6; ++k) xb[k] = Bicomplex(x[k], k == i ? h : 0.0, k == j ? h : 0.0, 0.0);
+      H[i][j] = H[j][i] = f(xb).im12 / (h * h);
+    }
+  return H;
+}
 
 // ---------------------------------------------------------------------------
 // dataset.hpp:17-36 — on-disk formats (host file I/O; std::runtime_error)

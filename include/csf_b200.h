@@ -186,6 +186,9 @@ int csf_volume_destroy(csf_volume vol);
 int csf_volume_upload(csf_volume vol, const double* field, const double* weight);
 int csf_volume_download(csf_volume vol, double* field, double* weight);
 int csf_volume_block_count(csf_volume vol, int* n_blocks);
+/* The volume's channel count, kind (hashed 1 / dense 0) and voxel count (dense
+ * lattice size, or allocated blocks x 512). */
+int csf_volume_info(csf_volume vol, int* n_channels, int* hashed, long long* n_voxels);
 /* heads [2^bits], keys [n_blocks], next [n_blocks], coords [n_blocks][3] */
 int csf_volume_download_hash(csf_volume vol, int32_t* heads, uint64_t* keys, int32_t* next, int32_t* coords);
 
@@ -201,6 +204,12 @@ int csf_sample_gradient(csf_volume vol, const double* points, int n, double* gra
 int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h, const double* world_to_camera,
                       const double* intr, double mu, const double* points, const double* center, int n,
                       int n_channels, double* psi, int32_t* valid);
+/* measured_tsdf with a lifted depth image [h][w][1+n_channels]
+ * (tsdf.hpp:97-102 takes Image<S> depth): d psi / d depth = bilinear weight / mu
+ * (test_tsdf.cpp:194-231). */
+int csf_measured_tsdf_lifted(csf_ctx ctx, const double* depth, int w, int h, const double* world_to_camera,
+                             const double* intr, double mu, const double* points, const double* center, int n,
+                             int n_channels, double* psi, int32_t* valid);
 
 /* tsdf.cpp:61-153 — save_volume / load_volume in the reference's "CSFVOL 1"
  * container: text header (dims, voxel_size, origin, mu, weight_cap, channels)
@@ -220,6 +229,13 @@ int csf_volume_load(csf_ctx ctx, const char* path, int n_channels, csf_volume* o
  * truncation-band blocks; *n_visible (optional) receives the visible count. */
 int csf_surface_update(csf_volume vol, const double* depth, int w, int h, const double* pose, const double* intr,
                        int* n_visible);
+/* surface_update with a lifted depth image [h][w][1+D] — the reference's
+ * Image<Complex> depth (tsdf.hpp:144-145): the depth's own perturbation
+ * channels enter psi through the bilinear sample (tsdf.hpp:96-140), e.g. a
+ * depth pixel seeded with perturb_depth (frames.cpp:77-102).  First-order
+ * volumes; validity, the edge test and the hashed allocation read real parts. */
+int csf_surface_update_lifted(csf_volume v, const double* depth, int w, int h, const double* pose,
+                              const double* intr, int* n_visible);
 /* tsdf.hpp:209-284 — lifted raycast; outputs [w*h][3][1+D] world-frame maps */
 int csf_raycast(csf_volume vol, const double* pose, const double* intr, int w, int h, const csf_raycast_cfg* cfg,
                 double* vertices, double* normals);

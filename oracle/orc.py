@@ -63,7 +63,8 @@ def lib() -> C.CDLL:
                                    ip, dp, C.POINTER(C.c_int)]),
             "orc_linearized_step": (ip, [dp, ip, dp, ip, dp]),
             "orc_sample_points": (ip, [vp, dp, ip, ip, dp, i32p]),
-            "orc_measured_points": (ip, [dp, ip, ip, dp, dp, C.c_double, dp, dp, ip, ip, dp, i32p]),
+            "orc_measured_points": (ip, [dp, ip, ip, dp, dp, C.c_double, dp, dp, ip, ip, dp, i32p, ip]),
+            "orc_surface_update_lifted": (ip, [vp, dp, ip, ip, dp, dp, C.POINTER(C.c_int)]),
             "orc_view_scores": (ip, [vp, dp, ip, C.POINTER(_capi.Intrinsics), C.c_double, C.c_double, C.c_double,
                                      dp, dp]),
             "orc_icp_energy_derivs": (ip, [dp, ip, dp, dp, C.c_double, dp, dp, dp]),
@@ -155,12 +156,14 @@ class Volume:
             pass
 
     def surface_update(self, depth, pose, intr) -> int:
+        """depth (h, w) real or (h, w, 1+D) lifted."""
         d = np.ascontiguousarray(depth, dtype=np.float64)
-        h, w = d.shape
+        h, w = d.shape[:2]
         p = np.ascontiguousarray(pose, dtype=np.float64)
         k = np.ascontiguousarray(intr, dtype=np.float64)
         nv = C.c_int()
-        _check(lib().orc_surface_update(self.h, _dp(d), w, h, _dp(p), _dp(k), C.byref(nv)))
+        fn = lib().orc_surface_update_lifted if d.ndim == 3 else lib().orc_surface_update
+        _check(fn(self.h, _dp(d), w, h, _dp(p), _dp(k), C.byref(nv)))
         return nv.value
 
     def raycast(self, pose, intr, w, h, cfg=None):
@@ -352,8 +355,9 @@ def pairwise_sum(terms):
 
 
 def measured_tsdf(depth, w2c, intr, mu, pts, center):
+    """depth (h, w) real or (h, w, 1+D) lifted (the reference's Image<S> depth)."""
     d = np.ascontiguousarray(depth, dtype=np.float64)
-    h, w = d.shape
+    h, w = d.shape[:2]
     pose = np.ascontiguousarray(w2c, dtype=np.float64)
     D = pose.shape[1] - 1
     P = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
@@ -361,7 +365,7 @@ def measured_tsdf(depth, w2c, intr, mu, pts, center):
     ok = np.zeros(P.shape[0], dtype=np.int32)
     _check(lib().orc_measured_points(_dp(d), w, h, _dp(pose), _dp(np.ascontiguousarray(intr, dtype=np.float64)), mu,
                                      _dp(P), _dp(np.ascontiguousarray(center, dtype=np.float64)), P.shape[0], D,
-                                     _dp(out), ok.ctypes.data_as(C.POINTER(C.c_int32))))
+                                     _dp(out), ok.ctypes.data_as(C.POINTER(C.c_int32)), int(d.ndim == 3)))
     return out, ok.astype(bool)
 
 

@@ -129,6 +129,9 @@ struct VolBase {
   virtual ~VolBase() = default;
   virtual int channels() const = 0;
   virtual void fuse(const Image<double>& depth, const double* pose, const double* intr, int* n_visible) = 0;
+  // lifted depth [h][w][1+D]: the reference's Image<Complex> depth (tsdf.hpp:144-145)
+  virtual void fuse_lifted(const double* depth, int w, int h, const double* pose, const double* intr,
+                           int* n_visible) = 0;
   virtual void raycast(const double* pose, const double* intr, int w, int h, const RaycastConfig& rc, double* vert,
                        double* norm) = 0;
   virtual long long voxels() const = 0;
@@ -162,6 +165,26 @@ struct Vol : VolBase {
       if (n_visible) *n_visible = st.touched;
     } else {
       surface_update(vol, depth, c2w, k);
+      if (n_visible) *n_visible = 0;
+    }
+  }
+  void fuse_lifted(const double* depth, int w, int h, const double* pose, const double* intr, int* n_visible) override {
+    Image<F> dl(w, h, F(0.0));
+    Image<double> dr(w, h, 0.0);
+    for (int i = 0; i < w * h; ++i) {
+      dl.data[i] = load_s<D>(depth + static_cast<std::size_t>(i) * (1 + D));
+      dr.data[i] = depth[static_cast<std::size_t>(i) * (1 + D)];
+    }
+    const PoseT<F> c2w = load_pose<D>(pose);
+    const IntrinsicsT<F> k = load_intr<D>(intr, w, h);
+    if constexpr (H) {
+      Intrinsics kr = real_intrinsics(k);
+      AllocStats st;
+      const auto vis = allocate_band(vol, dr, kr, real_pose(c2w), &st);
+      surface_update_blocks(vol, vis, dl, c2w, k);
+      if (n_visible) *n_visible = st.touched;
+    } else {
+      surface_update(vol, dl, c2w, k);
       if (n_visible) *n_visible = 0;
     }
   }
@@ -328,6 +351,10 @@ void orc_volume_destroy(void* v) { delete static_cast<VolBase*>(v); }
 int orc_surface_update(void* v, const double* depth, int w, int h, const double* pose, const double* intr,
                        int* n_visible) {
   return guard([&] { static_cast<VolBase*>(v)->fuse(image_of(depth, w, h), pose, intr, n_visible); });
+}
+int orc_surface_update_lifted(void* v, const double* depth, int w, int h, const double* pose, const double* intr,
+                              int* n_visible) {
+  return guard([&] { static_cast<VolBase*>(v)->fuse_lifted(depth, w, h, pose, intr, n_visible); });
 }
 int orc_raycast(void* v, const double* pose, const double* intr, int w, int h, const csf_raycast_cfg* rc, double* vert,
                 double* norm) {
@@ -732,22 +759,32 @@ int orc_sample_points(void* v, const double* pts, int n, int grad, double* out, 
   return guard([&] { static_cast<VolBase*>(v)->sample_points(pts, n, grad, out, valid); });
 }
 
+// lifted != 0: depth is [h][w][1+D] (tsdf.hpp:97-102 takes Image<S> depth)
 int orc_measured_points(const double* depth, int w, int h, const double* w2c, const double* intr, double mu,
-                        const double* pts, const double* center, int n, int D, double* out, int32_t* valid) {
+                        const double* pts, const double* center, int n, int D, double* out, int32_t* valid,
+                        int lifted) {
   return guard([&] {
     auto run = [&](auto tag) {
       constexpr int DD = decltype(tag)::value;
       using S = FT<DD>;
-      Image<double> dimg = image_of(depth, w, h);
       const PoseT<S> pose = load_pose<DD>(w2c);
       const IntrinsicsT<S> k = load_intr<DD>(intr, w, h);
       Vec3<S> c;
       for (int e = 0; e < 3; ++e) c[e] = load_s<DD>(center + e * (1 + DD));
-      for (int i = 0; i < n; ++i) {
-        const Vec3<S> p(S(pts[3 * i]), S(pts[3 * i + 1]), S(pts[3 * i + 2]));
-        const auto m = measured_tsdf<S>(dimg, pose, k, mu, p, c);
-        valid[i] = m.has_value();
-        if (m) store_s<DD>(out + i * (1 + DD), *m);
+      auto eval = [&](const auto& dimg) {
+        for (int i = 0; i < n; ++i) {
+          const Vec3<S> p(S(pts[3 * i]), S(pts[3 * i + 1]), S(pts[3 * i + 2]));
+          const auto m = measured_tsdf<S>(dimg, pose, k, mu, p, c);
+          valid[i] = m.has_value();
+          if (m) store_s<DD>(out + i * (1 + DD), *m);
+        }
+      };
+      if (lifted) {
+        Image<S> dl(w, h, S(0.0));
+        for (int i = 0; i < w * h; ++i) dl.data[i] = load_s<DD>(depth + static_cast<std::size_t>(i) * (1 + DD));
+        eval(dl);
+      } else {
+        eval(image_of(depth, w, h));
       }
     };
     switch (D) {

@@ -275,13 +275,22 @@ class _Volume:
             pass
 
     def surface_update(self, depth, pose, k) -> int:
-        """tsdf.cpp:11-40; returns the visible block count (hashed) or 0."""
+        """tsdf.cpp:11-40; returns the visible block count (hashed) or 0.
+        depth (h, w) real, or (h, w, 1+D) lifted: the reference's
+        Image<Complex> depth, whose channels enter psi (tsdf.hpp:144-145)."""
         d = _f64(depth)
-        h, w = d.shape
         p = lift_pose(pose, self.channels)
         kk = lift_intrinsics(k, self.channels)
         nv = C.c_int(0)
-        self.ctx.check(self.ctx.lib.csf_surface_update(self.h, _dp(d), w, h, _dp(p), _dp(kk), C.byref(nv)))
+        if d.ndim == 3:
+            h, w, cc = d.shape
+            if cc != 1 + self.channels:
+                raise InvalidArgument(f"lifted depth must have 1 + {self.channels} channels")
+            self.ctx.check(self.ctx.lib.csf_surface_update_lifted(self.h, _dp(d), w, h, _dp(p), _dp(kk),
+                                                                  C.byref(nv)))
+        else:
+            h, w = d.shape
+            self.ctx.check(self.ctx.lib.csf_surface_update(self.h, _dp(d), w, h, _dp(p), _dp(kk), C.byref(nv)))
         return nv.value
 
     def raycast(self, pose, k, width: int, height: int, cfg: Optional[_capi.RaycastCfg] = None):
@@ -438,9 +447,16 @@ def measured_tsdf(depth, world_to_camera, k, mu: float, points, center, ctx: Opt
     pose (12, 1+D), intrinsics (4, 1+D) and camera centre (3, 1+D) carry D channels."""
     c = _ctx(ctx)
     d = _f64(depth)
-    h, w = d.shape
     pose = _f64(world_to_camera)
     D = pose.shape[1] - 1 if pose.ndim == 2 else 0
+    lifted = d.ndim == 3
+    if lifted:  # (h, w, 1+D): the depth carries its own channels (tsdf.hpp:97-102)
+        h, w, cc = d.shape
+        D = max(D, cc - 1)
+        if cc != 1 + D:
+            raise InvalidArgument("lifted depth and pose channel counts differ")
+    else:
+        h, w = d.shape
     pose = lift_pose(pose, D)
     kk = lift_intrinsics(k, D)
     cen = _f64(center).reshape(3, -1)
@@ -449,8 +465,9 @@ def measured_tsdf(depth, world_to_camera, k, mu: float, points, center, ctx: Opt
     P = np.ascontiguousarray(_f64(points).reshape(-1, 3))
     out = np.zeros((P.shape[0], 1 + D))
     ok = np.zeros(P.shape[0], dtype=np.int32)
-    c.check(c.lib.csf_measured_tsdf(c.h, _dp(d), w, h, _dp(pose), _dp(kk), mu, _dp(P), _dp(np.ascontiguousarray(cen)),
-                                    P.shape[0], D, _dp(out), ok.ctypes.data_as(C.POINTER(C.c_int32))))
+    fn = c.lib.csf_measured_tsdf_lifted if lifted else c.lib.csf_measured_tsdf
+    c.check(fn(c.h, _dp(d), w, h, _dp(pose), _dp(kk), mu, _dp(P), _dp(np.ascontiguousarray(cen)), P.shape[0], D,
+               _dp(out), ok.ctypes.data_as(C.POINTER(C.c_int32))))
     return out, ok.astype(bool)
 
 

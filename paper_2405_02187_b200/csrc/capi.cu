@@ -196,7 +196,7 @@ struct csf_volume_s {
       a_counters;
   DevBuf<unsigned char> a_cub;
   // stage buffers for the single-call APIs
-  DevBuf<double> s_depth, s_pose, s_intr, s_vre, s_nre, s_vim, s_nim;
+  DevBuf<double> s_depth, s_dch, s_pose, s_intr, s_vre, s_nre, s_vim, s_nim;
   DevBuf<double2> s_hits;
   DevBuf<double> s_terms;  // csf_view_scores per-pixel terms [views][C][P]
   // raycast alpha table (hashed volumes) for (tab_near, tab_far, tab_step)
@@ -212,7 +212,7 @@ struct csf_volume_s {
     a_cand.release(); a_set_keys.release(); a_cand_block.release(); a_first_flag.release(); a_new_flag.release();
     a_first_rank.release(); a_new_rank.release(); a_set_first.release(); a_set_slot.release(); a_visible.release();
     a_counters.release(); a_cub.release();
-    s_depth.release(); s_pose.release(); s_intr.release(); s_vre.release(); s_nre.release(); s_vim.release();
+    s_depth.release(); s_dch.release(); s_pose.release(); s_intr.release(); s_vre.release(); s_nre.release(); s_vim.release();
     s_nim.release();
     s_hits.release();
     s_terms.release();
@@ -287,7 +287,7 @@ int volume_init_common(csf_volume v, int n_channels, int order) {
 // Fuse one double depth frame already on the device.  upd (nullable) counts
 // the fused voxels.
 int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double* d_pose, const double* d_intr,
-                int* upd = nullptr) {
+                int* upd = nullptr, const double* d_dch = nullptr) {
   const Launch L = launch_of(v->ctx);
   if (v->hashed) {
     const int rc = ensure_alloc_scratch(v, w, h);
@@ -297,10 +297,10 @@ int volume_fuse(csf_volume v, const double* d_depth, int w, int h, const double*
       launch_allocate(L, v->hash, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr);
     }
     PROF(v->ctx, kPIntegrate);
-    launch_integrate_hashed(L, v->hash, v->G, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr, upd);
+    launch_integrate_hashed(L, v->hash, v->G, v->Dp, v->alloc, d_depth, w, h, d_pose, d_intr, upd, d_dch);
   } else {
     PROF(v->ctx, kPIntegrate);
-    launch_integrate_dense(L, v->dense, v->G, v->Dp, d_depth, w, h, d_pose, d_intr, upd);
+    launch_integrate_dense(L, v->dense, v->G, v->Dp, d_depth, w, h, d_pose, d_intr, upd, d_dch);
   }
   return CSF_OK;
 }
@@ -663,6 +663,24 @@ extern "C" int csf_volume_destroy(csf_volume vol) {
   return CSF_OK;
 }
 
+extern "C" int csf_volume_block_count(csf_volume v, int* n);
+extern "C" int csf_volume_info(csf_volume v, int* n_channels, int* hashed, long long* n_voxels) {
+  if (!v) return CSF_EINVAL;
+  if (n_channels) *n_channels = v->D;
+  if (hashed) *hashed = v->hashed ? 1 : 0;
+  if (n_voxels) {
+    if (v->hashed) {
+      int nb = 0;
+      const int rc = csf_volume_block_count(v, &nb);
+      if (rc) return rc;
+      *n_voxels = static_cast<long long>(nb) * 512;
+    } else {
+      *n_voxels = v->n_vox;
+    }
+  }
+  return CSF_OK;
+}
+
 extern "C" int csf_volume_block_count(csf_volume v, int* n) {
   if (!v || !n) return CSF_EINVAL;
   if (!v->hashed) {
@@ -731,12 +749,16 @@ extern "C" int csf_volume_download_hash(csf_volume v, int32_t* heads, uint64_t* 
   return CSF_OK;
 }
 
-extern "C" int csf_surface_update(csf_volume v, const double* depth, int w, int h, const double* pose,
-                                  const double* intr, int* n_visible) {
+// lifted: depth is [h][w][1+D] (the reference's Image<Complex> depth,
+// tsdf.hpp:144-145), else [h][w] real.
+static int surface_update_impl(csf_volume v, const double* depth, bool lifted, int w, int h, const double* pose,
+                               const double* intr, int* n_visible) {
   if (!v || !depth || !pose || !intr || w <= 1 || h <= 1) return CSF_EINVAL;
   csf_ctx ctx = v->ctx;
   if (v->D > 0 && (intr[0] == 0.0 || intr[1 + v->D] == 0.0))
     return fail(ctx, CSF_EDOMAIN, "csf_surface_update: Complex division by zero real part (fx or fy = 0)");
+  if (lifted && v->order != 1)
+    return fail(ctx, CSF_EINVAL, "csf_surface_update_lifted: lifted depth takes first-order volumes");
   cudaSetDevice(ctx->device);
   const size_t P = static_cast<size_t>(w) * h;
   const int C = 1 + v->Dp;
@@ -745,10 +767,27 @@ extern "C" int csf_surface_update(csf_volume v, const double* depth, int w, int 
   CUDA_TRY(ctx, v->s_depth.alloc(P));
   CUDA_TRY(ctx, v->s_pose.alloc(12 * C));
   CUDA_TRY(ctx, v->s_intr.alloc(4 * C));
-  CUDA_TRY(ctx, cudaMemcpyAsync(v->s_depth.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  const bool channels = lifted && v->Dp > 0;
+  if (!lifted) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(v->s_depth.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    // split [P][1+D] into the real image and the channels [P][Dp] (padding zero)
+    std::vector<double> re(P), ch(channels ? P * v->Dp : 0, 0.0);
+    for (size_t i = 0; i < P; ++i) {
+      re[i] = depth[i * (1 + v->D)];
+      for (int d = 0; d < v->D && channels; ++d) ch[i * v->Dp + d] = depth[i * (1 + v->D) + 1 + d];
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(v->s_depth.p, re.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+    if (channels) {
+      CUDA_TRY(ctx, v->s_dch.alloc(P * v->Dp));
+      CUDA_TRY(ctx, cudaMemcpyAsync(v->s_dch.p, ch.data(), sizeof(double) * P * v->Dp, cudaMemcpyHostToDevice,
+                                    ctx->stream));
+    }
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // re / ch are local
+  }
   CUDA_TRY(ctx, cudaMemcpyAsync(v->s_pose.p, pp.data(), sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(v->s_intr.p, kp.data(), sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
-  int rc = volume_fuse(v, v->s_depth.p, w, h, v->s_pose.p, v->s_intr.p);
+  int rc = volume_fuse(v, v->s_depth.p, w, h, v->s_pose.p, v->s_intr.p, nullptr, channels ? v->s_dch.p : nullptr);
   if (rc) return rc;
   rc = sync_check(ctx, "csf_surface_update");
   if (rc) return rc;
@@ -757,6 +796,16 @@ extern "C" int csf_surface_update(csf_volume v, const double* depth, int w, int 
     if (v->hashed) CUDA_TRY(ctx, d2h(n_visible, v->alloc.counters, sizeof(int), ctx->stream));
   }
   return CSF_OK;
+}
+
+extern "C" int csf_surface_update(csf_volume v, const double* depth, int w, int h, const double* pose,
+                                  const double* intr, int* n_visible) {
+  return surface_update_impl(v, depth, false, w, h, pose, intr, n_visible);
+}
+
+extern "C" int csf_surface_update_lifted(csf_volume v, const double* depth, int w, int h, const double* pose,
+                                         const double* intr, int* n_visible) {
+  return surface_update_impl(v, depth, true, w, h, pose, intr, n_visible);
 }
 
 extern "C" int csf_raycast(csf_volume v, const double* pose, const double* intr, int w, int h,
@@ -1302,9 +1351,28 @@ extern "C" int csf_sample_gradient(csf_volume v, const double* points, int n, do
   return sample_points_common(v, points, n, 1, gradients, valid);
 }
 
+static int measured_tsdf_impl(csf_ctx ctx, const double* depth, bool lifted, int w, int h,
+                              const double* world_to_camera, const double* intr, double mu, const double* points,
+                              const double* center, int n, int n_channels, double* psi, int32_t* valid);
+
 extern "C" int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h, const double* world_to_camera,
                                  const double* intr, double mu, const double* points, const double* center, int n,
                                  int n_channels, double* psi, int32_t* valid) {
+  return measured_tsdf_impl(ctx, depth, false, w, h, world_to_camera, intr, mu, points, center, n, n_channels, psi,
+                            valid);
+}
+
+extern "C" int csf_measured_tsdf_lifted(csf_ctx ctx, const double* depth, int w, int h,
+                                        const double* world_to_camera, const double* intr, double mu,
+                                        const double* points, const double* center, int n, int n_channels,
+                                        double* psi, int32_t* valid) {
+  return measured_tsdf_impl(ctx, depth, true, w, h, world_to_camera, intr, mu, points, center, n, n_channels, psi,
+                            valid);
+}
+
+static int measured_tsdf_impl(csf_ctx ctx, const double* depth, bool lifted, int w, int h,
+                              const double* world_to_camera, const double* intr, double mu, const double* points,
+                              const double* center, int n, int n_channels, double* psi, int32_t* valid) {
   if (!ctx || !depth || !world_to_camera || !intr || !center || w <= 0 || h <= 0 || n < 0 || n_channels < 0 ||
       n_channels > CSF_MAX_DIRECTIONS || (n > 0 && (!points || !psi || !valid)))
     return CSF_EINVAL;
@@ -1315,7 +1383,9 @@ extern "C" int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h,
   const size_t P = static_cast<size_t>(w) * h;
   DevBuf<double> buf, dout;
   DevBuf<int> dv;
-  CUDA_TRY(ctx, buf.alloc(P + 12 * C + 4 * C + 3 * C + 3 * static_cast<size_t>(std::max(n, 1))));
+  const bool channels = lifted && D > 0;
+  CUDA_TRY(ctx, buf.alloc(P + 12 * C + 4 * C + 3 * C + 3 * static_cast<size_t>(std::max(n, 1)) +
+                          (channels ? P * D : 0)));
   CUDA_TRY(ctx, dout.alloc(static_cast<size_t>(std::max(n, 1)) * C));
   CUDA_TRY(ctx, dv.alloc(std::max(n, 1)));
   double* d_depth = buf.p;
@@ -1323,7 +1393,21 @@ extern "C" int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h,
   double* d_intr = d_pose + 12 * C;
   double* d_center = d_intr + 4 * C;
   double* d_pts = d_center + 3 * C;
-  CUDA_TRY(ctx, cudaMemcpyAsync(d_depth, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  double* d_dch = channels ? d_pts + 3 * static_cast<size_t>(std::max(n, 1)) : nullptr;
+  std::vector<double> re, ch;
+  if (!lifted) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_depth, depth, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    re.resize(P);
+    ch.assign(channels ? P * D : 0, 0.0);
+    for (size_t i = 0; i < P; ++i) {
+      re[i] = depth[i * C];
+      for (int d = 0; d < D && channels; ++d) ch[i * D + d] = depth[i * C + 1 + d];
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_depth, re.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+    if (channels)
+      CUDA_TRY(ctx, cudaMemcpyAsync(d_dch, ch.data(), sizeof(double) * P * D, cudaMemcpyHostToDevice, ctx->stream));
+  }
   CUDA_TRY(ctx, cudaMemcpyAsync(d_pose, world_to_camera, sizeof(double) * 12 * C, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(d_intr, intr, sizeof(double) * 4 * C, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemcpyAsync(d_center, center, sizeof(double) * 3 * C, cudaMemcpyHostToDevice, ctx->stream));
@@ -1331,7 +1415,8 @@ extern "C" int csf_measured_tsdf(csf_ctx ctx, const double* depth, int w, int h,
     CUDA_TRY(ctx, cudaMemcpyAsync(d_pts, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(ctx, cudaMemsetAsync(dout.p, 0, sizeof(double) * n * C, ctx->stream));
   }
-  launch_measured_points(launch_of(ctx), d_depth, w, h, d_pose, d_intr, mu, d_pts, d_center, n, D, dout.p, dv.p);
+  launch_measured_points(launch_of(ctx), d_depth, w, h, d_pose, d_intr, mu, d_pts, d_center, n, D, dout.p, dv.p,
+                         d_dch);
   const int rc = sync_check(ctx, "csf_measured_tsdf");
   if (rc) return rc;
   if (n > 0) {

@@ -231,11 +231,13 @@ void launch_measure(const Launch& L, const double* depth, int w, int h, const do
                     double* norm);
 
 // ---- volume.cu
-// upd (nullable): incremented by the number of voxels fused
+// upd (nullable): incremented by the number of voxels fused; dch (nullable):
+// the depth image's perturbation channels [w*h][Dp] (a lifted depth image)
 void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* depth, int w, int h,
-                            const double* pose, const double* intr, int* upd);
+                            const double* pose, const double* intr, int* upd, const double* dch = nullptr);
 void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, const AllocScratch& a,
-                             const double* depth, int w, int h, const double* pose, const double* intr, int* upd);
+                             const double* depth, int w, int h, const double* pose, const double* intr, int* upd,
+                             const double* dch = nullptr);
 void launch_allocate(const Launch& L, const HashDev& v, int Dp, AllocScratch& a, const double* depth, int w, int h,
                      const double* pose, const double* intr);
 // hits: [w*h] scratch (alpha_prev, alpha) of the zero crossing per pixel
@@ -257,7 +259,7 @@ void launch_sample_points(const Launch& L, bool hashed, const DenseDev& dd, cons
                           const double* pts, int n, int grad, double* out, int* valid);
 void launch_measured_points(const Launch& L, const double* depth, int w, int h, const double* w2c, const double* intr,
                             double mu, const double* pts, const double* center, int n, int Dp, double* out,
-                            int* valid);
+                            int* valid, const double* dch = nullptr);
 
 // ---- icp.cu
 void launch_level_begin(const Launch& L, TrackState* st, const double* pose, double* pred_pose, int Dp);

@@ -304,10 +304,16 @@ template <typename S> struct Intr {
   int w, h;
 };
 
-// measured_tsdf (tsdf.hpp:97-140) against an unperturbed depth image.
+// measured_tsdf (tsdf.hpp:97-140).  depth: the real depth image; dch
+// (nullable): its perturbation channels [h*w][dstride] (a lifted depth image,
+// "the depth image carries its own channels", tsdf.hpp:96-102 / 144-145),
+// channel g of this channel group at dch[pixel * dstride + g0 + g].  Validity
+// and the edge test read real corner depths; the bilinear sample carries the
+// corners' channels (bilinear_depth<S>, frames.hpp:127-145).
 template <typename S>
 CSF_DEV bool measured_tsdf(const double* depth, int w, int h, const Pose<S>& w2c, const Intr<S>& k, double mu,
-                           double px, double py, double pz, const V3<S>& center, S* psi) {
+                           double px, double py, double pz, const V3<S>& center, S* psi,
+                           const double* __restrict__ dch = nullptr, int dstride = 0, int g0 = 0) {
   V3<S> pc;
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -327,9 +333,31 @@ CSF_DEV bool measured_tsdf(const double* depth, int w, int h, const Pose<S>& w2c
   if (farv - nearv > 0.1) return false;
   const S fx = lx - static_cast<double>(x0);
   const S fy = ly - static_cast<double>(y0);
-  const S top = d00 + fx * (d10 - d00);
-  const S bot = d01 + fx * (d11 - d01);
-  const S sampled = top + fy * (bot - top);
+  S sampled;
+  if constexpr (Traits<S>::G > 0) {
+    if (dch) {
+      auto corner = [&](int cx_, int cy_, double re_) {
+        S c = lit<S>(re_);
+        const double* src = dch + static_cast<long long>(cy_ * w + cx_) * dstride + g0;
+#pragma unroll
+        for (int g = 0; g < Traits<S>::G; ++g) c.im[g] = src[g];
+        return c;
+      };
+      const S c00 = corner(x0, y0, d00), c10 = corner(x0 + 1, y0, d10);
+      const S c01 = corner(x0, y0 + 1, d01), c11 = corner(x0 + 1, y0 + 1, d11);
+      const S top = c00 + fx * (c10 - c00);
+      const S bot = c01 + fx * (c11 - c01);
+      sampled = top + fy * (bot - top);
+    } else {
+      const S top = d00 + fx * (d10 - d00);
+      const S bot = d01 + fx * (d11 - d01);
+      sampled = top + fy * (bot - top);
+    }
+  } else {
+    const S top = d00 + fx * (d10 - d00);
+    const S bot = d01 + fx * (d11 - d01);
+    sampled = top + fy * (bot - top);
+  }
   const S rx = (lx - k.cx) / k.fx;
   const S ry = (ly - k.cy) / k.fy;
   const S one = lit<S>(1.0);

@@ -92,7 +92,7 @@ __device__ void load_pose_intr(const double* sm, int Dp, int g0, Pose<S>* w2c, V
 template <typename S>
 __device__ bool fuse_voxel(const VoxelStore& vox, long long v, double px, double py, double pz,
                            const double* __restrict__ depth, int w, int h, double mu, double cap, int Dp,
-                           const double* sm) {
+                           const double* sm, const double* __restrict__ dch = nullptr) {
   constexpr int G = Traits<S>::G;
   const int passes = G == 0 ? 1 : Dp / G;
   double2 rw = make_double2(0.0, 0.0);
@@ -105,7 +105,7 @@ __device__ bool fuse_voxel(const VoxelStore& vox, long long v, double px, double
     load_pose_intr<S>(sm, Dp, g0, &w2c, &c, &k);
     S psi;
     // validity depends on real parts only: the first pass decides for all
-    if (!measured_tsdf<S>(depth, w, h, w2c, k, mu, px, py, pz, c, &psi)) return false;
+    if (!measured_tsdf<S>(depth, w, h, w2c, k, mu, px, py, pz, c, &psi, dch, Dp, g0)) return false;
     if (gi == 0) rw = vox.rw[v];
     const S f = field_at<S>(vox, v, rw.x, g0);
     const S fn = (rw.y * f + psi) / (rw.y + 1.0);
@@ -314,15 +314,20 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
   return true;
 }
 
-template <typename S, int NDP = 0>
+// LD: the depth image carries perturbation channels (dch [P][Dp]): the
+// generic lifted evaluation (the adjoint form's 19 partials omit the depth
+// corners' channels).
+template <typename S, int NDP = 0, bool LD = false>
 __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const double* __restrict__ depth, int w,
                                                          int h, const double* __restrict__ pose,
-                                                         const double* __restrict__ intr, int Dp, int* upd) {
+                                                         const double* __restrict__ intr, int Dp, int* upd,
+                                                         const double* __restrict__ dch) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double sm[];
+  constexpr bool kAdj = kAdjointFusion && Traits<S>::kOrder == 1 && !LD;
   stage_pose_w2c<S>(pose, intr, Dp, sm);
-  if constexpr (kAdjointFusion && Traits<S>::kOrder == 1) stage_jacobian<NDP>(sm);
+  if constexpr (kAdj) stage_jacobian<NDP>(sm);
   const long long n = static_cast<long long>(vol.nx) * vol.ny * vol.nz;
   int fused = 0;
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < n;
@@ -333,10 +338,10 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     const double px = vol.ox + vol.vs * static_cast<double>(i);
     const double py = vol.oy + vol.vs * static_cast<double>(j);
     const double pz = vol.oz + vol.vs * static_cast<double>(k);
-    if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
+    if constexpr (kAdj)
       fused += fuse_voxel_adjoint<NDP>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
     else
-      count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+      count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm, dch));
   }
   flush_updates(upd, fused);
 }
@@ -345,18 +350,20 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
 #ifndef CSF_INT_MINB
 #define CSF_INT_MINB 2
 #endif
-template <typename S, int NDP = 0>
+template <typename S, int NDP = 0, bool LD = false>
 __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView vol, const int* __restrict__ coords,
                                                           const int* __restrict__ visible,
                                                           const int* __restrict__ counters,
                                                           const double* __restrict__ depth, int w, int h,
                                                           const double* __restrict__ pose,
-                                                          const double* __restrict__ intr, int Dp, int* upd) {
+                                                          const double* __restrict__ intr, int Dp, int* upd,
+                                                          const double* __restrict__ dch) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double sm[];
+  constexpr bool kAdj = kAdjointFusion && Traits<S>::kOrder == 1 && !LD;
   stage_pose_w2c<S>(pose, intr, Dp, sm);
-  if constexpr (kAdjointFusion && Traits<S>::kOrder == 1) stage_jacobian<NDP>(sm);
+  if constexpr (kAdj) stage_jacobian<NDP>(sm);
   const int n_vis = counters[0];
   int fused = 0;
   for (int vb = blockIdx.x; vb < n_vis; vb += gridDim.x) {
@@ -369,10 +376,10 @@ __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView
       const double py = vol.oy + vol.vs * static_cast<double>(8 * by + ly);
       const double pz = vol.oz + vol.vs * static_cast<double>(8 * bz + lz);
       const long long vv = static_cast<long long>(b) * kBlockVoxels + l;
-      if constexpr (kAdjointFusion && Traits<S>::kOrder == 1)
+      if constexpr (kAdj)
         fused += fuse_voxel_adjoint<NDP>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
       else
-        count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
+        count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm, dch));
     }
   }
   flush_updates(upd, fused);
@@ -1466,7 +1473,7 @@ template <typename S>
 __global__ void k_measured_points(const double* __restrict__ depth, int w, int h, const double* __restrict__ w2c,
                                   const double* __restrict__ intr, double mu, const double* __restrict__ pts,
                                   const double* __restrict__ center, int n, int Dp, double* __restrict__ out,
-                                  int* __restrict__ valid) {
+                                  int* __restrict__ valid, const double* __restrict__ dch) {
   pdl_wait();
   pdl_trigger();
   const int lanes = Dp > 0 ? Dp : 1;
@@ -1490,7 +1497,8 @@ __global__ void k_measured_points(const double* __restrict__ depth, int w, int h
 #pragma unroll
   for (int e = 0; e < 3; ++e) c.v[e] = load_ch<S>(center + e * C, ch, G);
   S psi;
-  const bool ok = measured_tsdf<S>(depth, w, h, pose, k, mu, pts[3LL * i], pts[3LL * i + 1], pts[3LL * i + 2], c, &psi);
+  const bool ok = measured_tsdf<S>(depth, w, h, pose, k, mu, pts[3LL * i], pts[3LL * i + 1], pts[3LL * i + 2], c, &psi,
+                                   dch, Dp, ch);
   if (ok) store_ch<S>(out + static_cast<long long>(i) * C, psi, ch, G, ch == 0);
   if (ch == 0) valid[i] = ok ? 1 : 0;
 }
@@ -1518,16 +1526,16 @@ void launch_sample_points(const Launch& L, bool hashed, const DenseDev& dd, cons
 
 void launch_measured_points(const Launch& L, const double* depth, int w, int h, const double* w2c, const double* intr,
                             double mu, const double* pts, const double* center, int n, int Dp, double* out,
-                            int* valid) {
+                            int* valid, const double* dch) {
   const long long items = static_cast<long long>(n) * (Dp > 0 ? Dp : 1);
   if (items == 0) return;
   const dim3 grid(static_cast<unsigned>((items + 127) / 128)), block(128);
   if (Dp > 0)
     launch_pdl(k_measured_points<csfd::L<1>>, grid, block, 0, L.stream, depth, w, h, w2c, intr, mu, pts, center, n, Dp, out,
-               valid);
+               valid, dch);
   else
     launch_pdl(k_measured_points<double>, grid, block, 0, L.stream, depth, w, h, w2c, intr, mu, pts, center, n, Dp,
-               out, valid);
+               out, valid, static_cast<const double*>(nullptr));
   ++*L.launches;
   chk("measured_points");
 }
@@ -1588,37 +1596,49 @@ void launch_init_volume(const Launch& L, double2* rw, double* fim, long long n, 
 }
 
 void launch_integrate_dense(const Launch& L, const DenseDev& v, int G, int Dp, const double* depth, int w, int h,
-                            const double* pose, const double* intr, int* upd) {
+                            const double* pose, const double* intr, int* upd, const double* dch) {
   const DenseView view = dense_view(v, Dp);
-  const size_t smem = integrate_smem(Dp, v.order != 2 && Dp % 2 == 0 && Dp <= 24);
+  const bool jac = v.order != 2 && !dch && Dp % 2 == 0 && Dp <= 24;
+  const size_t smem = integrate_smem(Dp, jac);
   const long long n = static_cast<long long>(v.nx) * v.ny * v.nz;
   const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, sm_count() * 16LL));
+  const double* nd = nullptr;
   if (v.order == 2)
-    launch_pdl(k_integrate_dense<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, depth, w, h, pose, intr, Dp, upd);
-  else if (kAdjointFusion && G > 0 && fixed_channels(Dp)) {
+    launch_pdl(k_integrate_dense<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, depth, w, h, pose, intr, Dp, upd,
+               nd);
+  else if (dch && G > 0) {
+    CSF_DISPATCH_G(G, (launch_pdl(k_integrate_dense<Scal<kG>, 0, true>, dim3(grid), dim3(256), smem, L.stream, view,
+                                  depth, w, h, pose, intr, Dp, upd, dch)));
+  } else if (kAdjointFusion && G > 0 && fixed_channels(Dp)) {
     CSF_DISPATCH_NDP(Dp, (launch_pdl(k_integrate_dense<csfd::L<1>, kN>, dim3(grid), dim3(256), smem, L.stream, view,
-                                     depth, w, h, pose, intr, Dp, upd)));
+                                     depth, w, h, pose, intr, Dp, upd, nd)));
   } else
     CSF_DISPATCH_G(G, (launch_pdl(k_integrate_dense<Scal<kG>>, dim3(grid), dim3(256), smem, L.stream, view, depth, w,
-                                  h, pose, intr, Dp, upd)));
+                                  h, pose, intr, Dp, upd, nd)));
   ++*L.launches;
   chk("integrate_dense");
 }
 
 void launch_integrate_hashed(const Launch& L, const HashDev& v, int G, int Dp, const AllocScratch& a,
-                             const double* depth, int w, int h, const double* pose, const double* intr, int* upd) {
+                             const double* depth, int w, int h, const double* pose, const double* intr, int* upd,
+                             const double* dch) {
   const HashView view = hash_view(v, Dp);
-  const size_t smem = integrate_smem(Dp, v.order != 2 && Dp % 2 == 0 && Dp <= 24);
+  const bool jac = v.order != 2 && !dch && Dp % 2 == 0 && Dp <= 24;
+  const size_t smem = integrate_smem(Dp, jac);
   const int grid = sm_count() * 8;
+  const double* nd = nullptr;
   if (v.order == 2)
     launch_pdl(k_integrate_hashed<B<1>>, dim3(grid), dim3(256), smem, L.stream, view, v.coords, a.visible,
-               a.counters, depth, w, h, pose, intr, Dp, upd);
-  else if (kAdjointFusion && G > 0 && fixed_channels(Dp)) {
+               a.counters, depth, w, h, pose, intr, Dp, upd, nd);
+  else if (dch && G > 0) {
+    CSF_DISPATCH_G(G, (launch_pdl(k_integrate_hashed<Scal<kG>, 0, true>, dim3(grid), dim3(256), smem, L.stream,
+                                  view, v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd, dch)));
+  } else if (kAdjointFusion && G > 0 && fixed_channels(Dp)) {
     CSF_DISPATCH_NDP(Dp, (launch_pdl(k_integrate_hashed<csfd::L<1>, kN>, dim3(grid), dim3(256), smem, L.stream, view,
-                                     v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd)));
+                                     v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd, nd)));
   } else
     CSF_DISPATCH_G(G, (launch_pdl(k_integrate_hashed<Scal<kG>>, dim3(grid), dim3(256), smem, L.stream, view,
-                                  v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd)));
+                                  v.coords, a.visible, a.counters, depth, w, h, pose, intr, Dp, upd, nd)));
   ++*L.launches;
   chk("integrate_hashed");
 }

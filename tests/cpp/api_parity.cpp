@@ -6,6 +6,7 @@
 #include <cstdio>
 
 #include "csf/b200.hpp"
+#include "csf/csf.hpp"
 #include "orc_pipeline.hpp"
 #include "orc_reloc.hpp"
 #include "orc_surfel.hpp"
@@ -318,6 +319,170 @@ int main() {
       for (int c = 0; c < 3; ++c) psame = psame && pm.vertices[3 * i + c] == po.vertices.data[i][c];
     CHECK(psame);
     std::printf("ok   surfel update / predict bit-identical to the restatement (%zu surfels)\n", hs.size());
+  }
+
+  {  // the reference-signature layer (include/csf/csf.hpp, namespace csf, default
+     // context): measure_surface, surface_update, sample_tsdf / sample_gradient,
+     // measured_tsdf, associate + linearized_step, pairwise_sum, csfd_gradient /
+     // csfd_hessian, save_volume / load_volume, lifted-depth surface_update
+    csf_volume_params p;
+    p.dims[0] = p.dims[1] = p.dims[2] = 32;
+    p.voxel_size = 0.04;
+    p.origin[0] = -0.64; p.origin[1] = -0.64; p.origin[2] = -0.64;
+    p.mu = 0.12;
+    p.weight_cap = 128;
+    csf::Volume vol(csf::default_context(), p, 0);
+    orc::VolumeParams vpo = orc::VolumeParams::cube(32, 0.04, orc::Vec3d(-0.64, -0.64, -0.64));
+    vpo.mu = 0.12;
+    orc::TsdfVolumeT<double> vo(vpo);
+    for (int f = 0; f < 3; ++f) {
+      const orc::Image<double> d = orc::render_depth(sphere, poses[f], ko);
+      csf::surface_update(vol, img(d), csf::Pose::from(arr(poses[f])), k);
+      orc::surface_update(vo, d, poses[f], ko);
+    }
+    // sample_tsdf / sample_gradient on a line through the sphere surface
+    int hits = 0;
+    bool same = true;
+    // points along camera 0's optical axis through the sphere surface
+    const orc::Vec3d cam0 = poses[0].translation;
+    const orc::Vec3d axis = orc::normalized(orc::Vec3d(0.0, 0.0, 0.0) - cam0);
+    auto along = [&](int i) {
+      const double t = (std::sqrt(cam0[0] * cam0[0] + cam0[1] * cam0[1] + cam0[2] * cam0[2]) - 0.5) - 0.12 + 0.0012 * i;
+      const orc::Vec3d q = cam0 + axis * t + orc::Vec3d(0.0007 * (i % 7), -0.0005 * (i % 5), 0.0);
+      return std::array<double, 3>{q[0], q[1], q[2]};
+    };
+    for (int i = 0; i < 200; ++i) {
+      const std::array<double, 3> q = along(i);
+      const auto a = csf::sample_tsdf(vol, q);
+      const auto b = orc::sample_tsdf<double>(vo, orc::Vec3d(q[0], q[1], q[2]));
+      same = same && a.has_value() == b.has_value() && (!a || *a == *b);
+      const auto ga = csf::sample_gradient(vol, q);
+      const auto gb = orc::sample_gradient<double>(vo, orc::Vec3d(q[0], q[1], q[2]));
+      same = same && ga.has_value() == gb.has_value();
+      if (ga && gb) {
+        ++hits;
+        for (int c = 0; c < 3; ++c) same = same && (*ga)[c] == (*gb)[c];
+      }
+    }
+    if (!(same && hits > 20)) std::printf("    sample: same %d hits %d\n", int(same), hits);
+    CHECK(same && hits > 20);
+    // measured_tsdf at voxel centres
+    const orc::Image<double> d0 = orc::render_depth(sphere, poses[0], ko);
+    const orc::Pose w2c = poses[0].inverse();
+    bool msame = true;
+    int mcount = 0;
+    for (int i = 0; i < 200; ++i) {
+      const std::array<double, 3> q = along(i);
+      const auto a = csf::measured_tsdf(img(d0), csf::Pose::from(arr(w2c)), k, 0.12, q,
+                                        {poses[0].translation[0], poses[0].translation[1], poses[0].translation[2]});
+      const auto b = orc::measured_tsdf<double>(d0, w2c, ko, 0.12, orc::Vec3d(q[0], q[1], q[2]), poses[0].translation);
+      msame = msame && a.has_value() == b.has_value() && (!a || *a == *b);
+      mcount += a.has_value();
+    }
+    if (!(msame && mcount > 50)) std::printf("    measured: same %d count %d\n", int(msame), mcount);
+    CHECK(msame && mcount > 50);
+    // measure_surface + associate + linearized_step against the raycast prediction
+    const orc::Image<double> d1 = orc::render_depth(sphere, poses[1], ko);
+    const csf::SurfaceMaps meas = csf::measure_surface(img(d1), k);
+    const auto meas_o = orc::measure_surface<double>(d1, ko);
+    bool vsame = true;
+    for (std::size_t i = 0; i < meas_o.vertices.data.size(); ++i)
+      for (int c = 0; c < 3; ++c)
+        vsame = vsame && meas.vertices[3 * i + c] == meas_o.vertices.data[i][c] &&
+                meas.normals[3 * i + c] == meas_o.normals.data[i][c];
+    CHECK(vsame);
+    const csf::SurfaceMaps pred = csf::raycast(vol, csf::Pose::from(arr(poses[1])), k);
+    orc::SurfaceMaps<double> pred_o;
+    pred_o.vertices = orc::Image<orc::Vec3d>(k.width, k.height, orc::Vec3d());
+    pred_o.normals = orc::Image<orc::Vec3d>(k.width, k.height, orc::Vec3d());
+    for (std::size_t i = 0; i < pred_o.vertices.data.size(); ++i)
+      for (int c = 0; c < 3; ++c) {
+        pred_o.vertices.data[i][c] = pred.vertices[3 * i + c];
+        pred_o.normals.data[i][c] = pred.normals[3 * i + c];
+      }
+    csf_icp_cfg icfg;
+    csf_default_icp_cfg(&icfg);
+    orc::IcpConfig icfg_o;
+    const auto corrs = csf::associate(meas, pred, csf::Pose::from(arr(poses[1])), csf::Pose::from(arr(poses[1])), k,
+                                      icfg, 1);
+    const auto corrs_o = orc::associate(meas_o, pred_o, poses[1], poses[1], ko, icfg_o, 1);
+    bool csame = corrs.size() == corrs_o.size() && corrs.size() > 100;
+    for (std::size_t i = 0; csame && i < corrs.size(); ++i)
+      for (int c = 0; c < 3; ++c)
+        csame = csame && corrs[i].vertex[c] == corrs_o[i].vertex[c] &&
+                corrs[i].model_vertex[c] == corrs_o[i].model_vertex[c] &&
+                corrs[i].model_normal[c] == corrs_o[i].model_normal[c];
+    CHECK(csame);
+    const std::array<double, 6> step = csf::linearized_step(corrs, csf::Pose::from(arr(poses[1])));
+    const auto step_o = orc::linearized_step(corrs_o, poses[1], false);
+    bool ssame = true;
+    for (int i = 0; i < 6; ++i) ssame = ssame && step[i] == step_o[i];
+    CHECK(ssame);
+    // pairwise_sum: the reference's fixed tree
+    std::vector<double> terms(1237);
+    for (std::size_t i = 0; i < terms.size(); ++i) terms[i] = std::sin(0.37 * double(i)) * 1e-3 + 1.0 / (1.0 + i);
+    CHECK(csf::pairwise_sum(terms, 0.25) == orc::pairwise_sum(terms, 0.25));
+    // csfd_gradient / csfd_hessian (diff.hpp:46-72) of f(x) = sum_i x_i^2 x_{i+1} + x_0 / (1 + x_5^2)
+    auto f = [](const auto& x) {
+      using T = std::decay_t<decltype(x[0])>;
+      T acc = T(0.0);
+      for (int i = 0; i < 5; ++i) acc = acc + x[i] * x[i] * x[i + 1];
+      return acc + x[0] / (T(1.0) + x[5] * x[5]);
+    };
+    const std::array<double, 6> x{0.3, -0.7, 1.1, 0.2, -0.4, 0.9};
+    const auto g = csf::csfd_gradient(f, x);
+    const auto H = csf::csfd_hessian(f, x);
+    const double den = 1.0 + x[5] * x[5];
+    double g_an[6] = {2 * x[0] * x[1] + 1.0 / den, x[0] * x[0] + 2 * x[1] * x[2], x[1] * x[1] + 2 * x[2] * x[3],
+                      x[2] * x[2] + 2 * x[3] * x[4], x[3] * x[3] + 2 * x[4] * x[5],
+                      x[4] * x[4] - 2 * x[0] * x[5] / (den * den)};
+    bool gok = true;
+    for (int i = 0; i < 6; ++i) gok = gok && std::fabs(g[i] - g_an[i]) <= 1e-12 * (1 + std::fabs(g_an[i]));
+    CHECK(gok);
+    CHECK(std::fabs(H[0][1] - 2 * x[0]) < 1e-9 && std::fabs(H[1][1] - 2 * x[2]) < 1e-9 && H[0][1] == H[1][0]);
+    // save_volume / load_volume round trip (tsdf.cpp:61-153)
+    csf::save_volume("/tmp/csf_api_parity.csfvol", vol);
+    const auto back = csf::load_volume("/tmp/csf_api_parity.csfvol");
+    std::vector<double> fa, wa, fb, wb;
+    vol.download(fa, wa);
+    back->download(fb, wb);
+    // the format stores float32 planes (tsdf.cpp:61-97)
+    for (auto& x : fa) x = static_cast<double>(static_cast<float>(x));
+    for (auto& x : wa) x = static_cast<double>(static_cast<float>(x));
+    if (!(fa == fb && wa == wb)) {
+      std::size_t nd = 0;
+      for (std::size_t i = 0; i < std::min(fa.size(), fb.size()); ++i) nd += fa[i] != fb[i];
+      std::printf("    save/load: sizes %zu %zu %zu %zu, field diffs %zu\n", fa.size(), fb.size(), wa.size(), wb.size(),
+                  nd);
+    }
+    CHECK(fa == fb && wa == wb);
+    // lifted depth (the reference's Image<Complex> depth): one pixel seeded
+    csf::Volume vl(csf::default_context(), p, 1);
+    orc::TsdfVolumeT<orc::Complex> vlo(vpo);
+    std::vector<double> ld(2 * static_cast<std::size_t>(k.width) * k.height, 0.0);
+    orc::Image<orc::Complex> ldo(k.width, k.height, orc::Complex(0.0));
+    for (int i = 0; i < k.width * k.height; ++i) {
+      ld[2 * i] = d0.data[i];
+      ldo.data[i] = orc::Complex(d0.data[i]);
+    }
+    const int seed = (k.height / 2) * k.width + k.width / 2;
+    ld[2 * seed + 1] = 1e-8;
+    ldo.data[seed].im = 1e-8;
+    csf::surface_update(vl, ld, B::LiftedPose::real(arr(poses[0]), 1), k);
+    orc::surface_update(vlo, ldo, orc::pose_cast<orc::Complex>(poses[0]), ko);
+    std::vector<double> fl, wl;
+    vl.download(fl, wl);
+    bool lsame = true;
+    int touched = 0;
+    for (std::size_t i = 0; i < vlo.tsdf.size(); ++i) {
+      lsame = lsame && fl[2 * i] == vlo.tsdf[i].re && wl[i] == vlo.weight[i] &&
+              std::fabs(fl[2 * i + 1] - vlo.tsdf[i].im) <= 1e-9 * std::max(1e-8, std::fabs(vlo.tsdf[i].im));
+      touched += vlo.tsdf[i].im != 0.0;
+    }
+    CHECK(lsame && touched > 0);
+    std::printf("ok   csf:: reference signatures: sample (%d hits), measured_tsdf (%d), measure/associate (%zu "
+                "corrs)/linearized_step, pairwise_sum, csfd_gradient/hessian, save/load, lifted depth (%d voxels)\n",
+                hits, mcount, corrs.size(), touched);
   }
 
   {  // error behaviour: invalid arguments throw std::invalid_argument

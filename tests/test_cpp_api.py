@@ -29,7 +29,8 @@ def test_cpp_api_compiles():
 
 @pytest.mark.gpu
 def test_cpp_api_reference_cases_on_device():
-    if not BIN.exists():
+    if not BIN.exists() or BIN.stat().st_mtime < max(SRC.stat().st_mtime, (ROOT / "include" / "csf" / "b200.hpp").stat().st_mtime,
+                                                     (ROOT / "include" / "csf" / "csf.hpp").stat().st_mtime):
         build()
     r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
