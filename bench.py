@@ -85,30 +85,35 @@ def parse():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5", "reloc", "surfel"], default="config2")
     ap.add_argument("--frames", type=int, default=0, help="0 = the workload's frame count (100 / 30)")
-    ap.add_argument("--cpu-frames", type=int, default=5, help="CPU-baseline sample: frames")
-    ap.add_argument("--cpu-dirs", type=int, default=2, help="CPU-baseline sample: directions (one pass each)")
+    ap.add_argument("--cpu-frames", type=int, default=CPU_FRAMES, help="CPU-baseline sample: frames")
+    ap.add_argument("--cpu-dirs", type=int, default=CPU_UNITS, help="CPU-baseline sample: directions (one pass each)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-json", default="")
     return ap.parse_args()
 
 
-def pipeline_cfg1(csf, capi, k, dirs, n_frames):
+# The descriptors below are plain ctypes structs (make_pipeline_cfg is pure
+# Python); `icp` defaults to the product's csf_default_icp_cfg, and the CPU
+# legs pass the oracle's copy of the reference defaults instead, so
+# --impl reference never loads the product library.
+def pipeline_cfg1(csf, capi, k, dirs, n_frames, icp=None):
     """BASELINE config 1: dense 128^3 at 2 cm (origin keeps the 4x4x3 m room
     inside), mu = 6 cm, h = 1e-20, final-translation-error objective."""
     import ctypes as C
     dense = capi.VolumeParams((C.c_int * 3)(128, 128, 128), 0.02, (C.c_double * 3)(-2.1, -1.28, -0.1), 0.06, 128.0)
     return csf.make_pipeline_cfg(hashed=False, k=k, dirs=dirs, h=1e-20,
-                                 objective=capi.OBJECTIVE_FINAL_TRANSLATION_ERROR, max_frames=n_frames, dense=dense)
+                                 objective=capi.OBJECTIVE_FINAL_TRANSLATION_ERROR, max_frames=n_frames, dense=dense,
+                                 icp=icp)
 
 
-def pipeline_cfg4(csf, capi, k, dirs, n_frames, keyframe_interval=50):
+def pipeline_cfg4(csf, capi, k, dirs, n_frames, keyframe_interval=50, icp=None):
     import ctypes as C
     hp = capi.HashParams(0.02, (C.c_double * 3)(0.0, 0.0, 0.0), 5 * 0.02, 128.0, 20, 1 << 21)
     return csf.make_pipeline_cfg(hashed=True, k=k, dirs=dirs, h=1e-8, objective=capi.OBJECTIVE_TRAJECTORY_ERROR,
-                                 max_frames=n_frames, hash_params=hp, keyframe_interval=keyframe_interval)
+                                 max_frames=n_frames, hash_params=hp, keyframe_interval=keyframe_interval, icp=icp)
 
 
-def pipeline_cfg(csf, capi, k, dirs, n_frames, pairs=None):
+def pipeline_cfg(csf, capi, k, dirs, n_frames, pairs=None, icp=None):
     import ctypes as C
     # block pool: config 2 allocates ~68k blocks over 100 frames; second-order
     # voxels carry 3 slots per pair, so the pool is sized to the 30-frame run
@@ -116,7 +121,22 @@ def pipeline_cfg(csf, capi, k, dirs, n_frames, pairs=None):
     hp = capi.HashParams(0.005, (C.c_double * 3)(0.0, 0.0, 0.0), 5 * 0.005, 128.0, 20, max_blocks)
     return csf.make_pipeline_cfg(hashed=True, k=k, dirs=[] if pairs is not None else dirs, h=1e-8,
                                  objective=capi.OBJECTIVE_TRAJECTORY_ERROR, max_frames=n_frames, hash_params=hp,
-                                 pairs=pairs)
+                                 pairs=pairs, icp=icp)
+
+
+def reference_icp():
+    """The reference's tracker defaults (icp.hpp:33-53) from the oracle, with
+    the lifted pipeline's linearized solver — no product library call."""
+    from oracle import orc
+    from paper_2405_02187_b200 import capi
+    return orc.default_icp_cfg(solver=capi.SOLVER_LINEARIZED)
+
+
+# The bounded CPU sample shared by the GPU arm's cpu_baseline and by
+# --impl reference: the workload's first CPU_FRAMES frames x CPU_UNITS
+# directions (pairs for config 3), one oracle pass per direction — the
+# reference's own pattern (diff.hpp:46-72).
+CPU_FRAMES, CPU_UNITS = 3, 2
 
 
 class Clocks:
@@ -178,24 +198,37 @@ def traffic_for(cat, workload):
         return None
 
 
-def cpu_baseline(depth, gt, k, frames, ndirs, workload="config2"):
-    """Oracle port, one Complex-style pass per direction (the reference's
-    pattern, diff.hpp:46-56) or one Bicomplex pass per pair (diff.hpp:58-72),
-    all host threads (OpenMP)."""
+def cpu_sample(depth, gt, k, frames, units, workload, packed=False):
+    """One run of the CPU sample: seconds for `units` one-pass-per-direction
+    oracle runs over the first `frames` frames (packed=True: one Lifted<10>
+    pass over all 10 directions instead, a labelled variant)."""
     from oracle import orc
     import paper_2405_02187_b200 as csf
     from paper_2405_02187_b200 import capi
+    icp = reference_icp()
     secs = 0.0
-    for d in range(ndirs):
+    if packed:
+        cfg = pipeline_cfg(csf, capi, k, DIRS, frames, icp=icp)
+        return orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
+    for d in range(units):
         if workload == "config3":
-            cfg = pipeline_cfg(csf, capi, k, [], frames, pairs=[PAIRS[d]])
+            cfg = pipeline_cfg(csf, capi, k, [], frames, pairs=[PAIRS[d]], icp=icp)
             secs += orc.pipeline_hessian(cfg, depth[:frames], gt[:frames])[-1]
         elif workload == "config4":
-            cfg = pipeline_cfg4(csf, capi, k, [DIRS4[d]], frames)
+            cfg = pipeline_cfg4(csf, capi, k, [DIRS4[d]], frames, icp=icp)
             secs += orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
         else:
-            cfg = pipeline_cfg(csf, capi, k, [DIRS[d]], frames)
+            cfg = pipeline_cfg(csf, capi, k, [DIRS[d]], frames, icp=icp)
             secs += orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
+    return secs
+
+
+def cpu_baseline(depth, gt, k, frames, ndirs, workload="config2"):
+    """Oracle port, one Complex-style pass per direction (the reference's
+    pattern, diff.hpp:46-56) or one Bicomplex pass per pair (diff.hpp:58-72),
+    all host threads (OpenMP); plus, labelled, the packed Lifted<10> CPU pass
+    (config 2) and a single-core number."""
+    secs = cpu_sample(depth, gt, k, frames, ndirs, workload)
     units = frames * ndirs
     cores = os.cpu_count() or 1
     omp = os.environ.get("OMP_NUM_THREADS")
@@ -205,18 +238,18 @@ def cpu_baseline(depth, gt, k, frames, ndirs, workload="config2"):
     out = {"value": units / secs, "unit": UNIT, "cores": cores, "kind": "port",
            "sample": f"{workload} first {frames} VGA frames x {ndirs} {what}s, one pass per {what} "
                      f"({units} units in {secs:.2f} s)", "host": host_info()}
+    if workload == "config2":
+        ps = cpu_sample(depth, gt, k, frames, ndirs, workload, packed=True)
+        out["packed_cpu"] = {"value": frames * len(DIRS) / ps, "unit": UNIT, "cores": cores,
+                             "sample": f"first {frames} frames x {len(DIRS)} directions in ONE Lifted<10> oracle pass "
+                                       f"({ps:.2f} s; the builder's packed CPU variant, not the reference's pattern)"}
     # also a single-core number (the same oracle on one OpenMP thread, 2 frames x 1 unit)
     try:
         import ctypes
         gomp = ctypes.CDLL("libgomp.so.1")
         gomp.omp_set_num_threads(1)
         f1 = min(2, frames)
-        if workload == "config3":
-            t1 = orc.pipeline_hessian(pipeline_cfg(csf, capi, k, [], f1, pairs=[PAIRS[0]]), depth[:f1], gt[:f1])[-1]
-        elif workload == "config4":
-            t1 = orc.pipeline_run(pipeline_cfg4(csf, capi, k, [DIRS4[0]], f1), depth[:f1], gt[:f1])[-1]
-        else:
-            t1 = orc.pipeline_run(pipeline_cfg(csf, capi, k, [DIRS[0]], f1), depth[:f1], gt[:f1])[-1]
+        t1 = cpu_sample(depth, gt, k, f1, 1, workload)
         gomp.omp_set_num_threads(cores)
         out["single_core"] = {"value": f1 / t1, "unit": UNIT, "cores": 1,
                               "sample": f"first {f1} frames x 1 {what}, OMP 1 thread ({t1:.2f} s)"}
@@ -279,22 +312,15 @@ def run_reference(args):
                              "sample": "2 views x 6 directions per step, one Lifted<6> pass per view"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
         return
-    frames = 3
+    frames, units = CPU_FRAMES, CPU_UNITS
     depth, gt, k = orc.workload(4 if args.workload == "config4" else 2, frames)
     second = args.workload == "config3"
-    if args.workload == "config4":
-        cfg = pipeline_cfg4(csf, capi, k, [0], frames)
-    else:
-        cfg = pipeline_cfg(csf, capi, k, [0], frames, pairs=[PAIRS[1]] if second else None)
-    run = (lambda: orc.pipeline_hessian(cfg, depth, gt)) if second else (lambda: orc.pipeline_run(cfg, depth, gt))
     for _ in range(args.warmup):
-        run()
-    t0 = time.perf_counter()
+        cpu_sample(depth, gt, k, frames, units, args.workload)
+    secs = 0.0
     for _ in range(args.steps):
-        run()
-    secs = time.perf_counter() - t0
-    units = frames * 1 * args.steps
-    value = units / secs
+        secs += cpu_sample(depth, gt, k, frames, units, args.workload)
+    value = frames * units * args.steps / secs
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     what = "pair (Bicomplex pass)" if second else "direction"
     line = {
@@ -302,13 +328,19 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded procedural room, BASELINE {args.workload} shapes)",
-        "config": {"workload": f"{args.workload} VGA hashed 5mm, bounded CPU sample: 3 frames x 1 {what} per step",
-                   "frames": frames, "directions": 1},
+        "config": {"workload": f"{args.workload} VGA hashed, bounded CPU sample: first {frames} frames x {units} "
+                               f"{what}s per step", "frames": frames, "directions": units},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"3 VGA frames x 1 {what} per step (oracle/ restatement; the reference needs "
-                                   "Eigen/libpng/doctest, absent)"},
+                         "sample": f"first {frames} VGA frames x {units} {what}s per step, one oracle pass per {what} "
+                                   "(oracle/ restatement; the reference needs Eigen/libpng/doctest, absent); the same "
+                                   "sample as the GPU arm's cpu_baseline", "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.workload == "config2":
+        ps = cpu_sample(depth, gt, k, frames, units, args.workload, packed=True)
+        line["packed_cpu"] = {"value": frames * len(DIRS) / ps, "unit": UNIT, "cores": cores,
+                              "sample": f"first {frames} frames x {len(DIRS)} directions in one Lifted<10> pass "
+                                        f"({ps:.2f} s; builder's packed CPU variant, labelled, not the value)"}
     print(json.dumps(line), flush=True)
 
 
@@ -497,7 +529,7 @@ def main():
         return
     import torch
     import paper_2405_02187_b200 as csf
-    from paper_2405_02187_b200.shard import gather_columns, shard_directions
+    from paper_2405_02187_b200.shard import attach_native_comm, gather_columns_native, shard_directions
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -575,8 +607,9 @@ def main():
         res = pipe.result()
         local_cols, stats = res.gradient, res.stats
     if dist is not None:
-        cols = gather_columns(torch.from_numpy(np.asarray(local_cols)).cuda(), len(units_all), world,
-                              rank).cpu().numpy()
+        # collective C2 in the C-ABI: csf_gather_columns over the context's NCCL communicator
+        attach_native_comm(ctx, world, rank)
+        cols = gather_columns_native(ctx, np.asarray(local_cols), len(units_all), world)
     if dist is None:
         cols = local_cols
 

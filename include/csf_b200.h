@@ -455,6 +455,17 @@ int csf_pipeline_volume(csf_pipeline p, csf_volume* out);
 int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames, double* gradient,
                           double* objective);
 
+/* ---- direction-sharded runs (collective C2) ------------------
+ * Rank r of N packs a contiguous block of the directions (or pairs) as its
+ * channels; the derivative columns are gathered at the end over an NCCL
+ * communicator owned by the context (libnccl.so.2 opened at runtime).
+ * Rank 0 creates the 128-byte unique id, every rank attaches with it. */
+int csf_comm_unique_id(unsigned char* id /* [128] */);
+int csf_ctx_attach_comm(csf_ctx ctx, int n_ranks, int rank, const unsigned char* id /* [128] */);
+/* counts[r] columns from rank r, in rank order, into out[sum counts] on every
+ * rank (host buffers; local = this rank's counts[rank] columns). */
+int csf_gather_columns(csf_ctx ctx, const double* local, const int* counts, double* out);
+
 /* ---- synthetic inputs (harness; not on the timed path) ----------------------
  * BASELINE configs 1 and 2 rendered on the device with the reference's
  * sphere tracer (synth.cpp:55-90) and the builder-defined sensor model;

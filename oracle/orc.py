@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
             "orc_sample_confidence": (C.c_double, [C.POINTER(_capi.Intrinsics), ip, ip]),
             "orc_pipeline_hessian": (ip, [C.POINTER(_capi.PipelineCfg), fp, dp, ip, dp, dp, dp, dp, dp, i32p, dp]),
             "orc_detmath_ulp": (ip, [ip, dp, ip, dp, dp, dp]),
+            "orc_default_icp_cfg": (None, [C.POINTER(_capi.IcpCfg)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -522,3 +523,16 @@ def detmath_ulp(fn: str, x):
     code = {"exp": 0, "sin": 1, "cos": 2}[fn]
     _check(lib().orc_detmath_ulp(code, _dp(a), a.size, _dp(u), _dp(d), _dp(g)))
     return u, d, g
+
+
+def default_icp_cfg(**kw):
+    """The reference's IcpConfig defaults (icp.hpp:33-53) from the oracle
+    (no product library involved); keyword overrides as the product's."""
+    c = _capi.IcpCfg()
+    lib().orc_default_icp_cfg(C.byref(c))
+    for k, v in kw.items():
+        if k in ("level_iterations", "level_pixel_stride"):
+            getattr(c, k)[:] = list(v)
+        else:
+            setattr(c, k, v)
+    return c

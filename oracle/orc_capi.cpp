@@ -981,6 +981,25 @@ int orc_pipeline_run(const csf_pipeline_cfg* c, const float* depth, const double
   });
 }
 
+// The reference's IcpConfig defaults (icp.hpp:33-53, restated in
+// orc_icp.hpp) in the shared descriptor: bench.py's --impl reference builds
+// its configuration from these, so that arm never loads the product library.
+void orc_default_icp_cfg(csf_icp_cfg* c) {
+  const IcpConfig d;
+  c->solver = static_cast<int>(d.solver);
+  c->d_max = d.d_max;
+  c->theta_max_deg = d.theta_max_deg;
+  c->levels = d.levels;
+  for (int i = 0; i < 3; ++i) {
+    c->level_iterations[i] = d.level_iterations[i];
+    c->level_pixel_stride[i] = d.level_pixel_stride[i];
+  }
+  c->step_tolerance = d.step_tolerance;
+  c->levenberg_lambda0 = d.levenberg_lambda0;
+  c->ncg_restart = d.ncg_restart;
+  c->h = d.step.h;
+}
+
 // tests/test_detmath.py: the deterministic elementary functions used on the
 // device path (include/csf_detmath.h) against glibc, in ulps of the glibc
 // result.  fn: 0 exp, 1 sin, 2 cos.  out_ulp[i] per argument.

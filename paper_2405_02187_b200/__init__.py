@@ -110,6 +110,22 @@ class Context:
     def synchronize(self) -> None:
         self.check(self.lib.csf_ctx_synchronize(self.h))
 
+    def attach_comm(self, n_ranks: int, rank: int, unique_id: bytes) -> None:
+        """The context's NCCL communicator for csf_gather_columns (rank 0's
+        comm_unique_id(), shared with every rank)."""
+        if len(unique_id) != 128:
+            raise InvalidArgument("unique_id must be 128 bytes")
+        self.check(self.lib.csf_ctx_attach_comm(self.h, n_ranks, rank, unique_id))
+
+    def gather_columns(self, local, counts) -> np.ndarray:
+        """csf_gather_columns: counts[r] columns from every rank r, in rank
+        order, on every rank (SURVEY §8(e) collective C2)."""
+        loc = _f64(np.asarray(local, dtype=np.float64).reshape(-1))
+        cnt = (C.c_int * len(counts))(*[int(c) for c in counts])
+        out = np.zeros(int(sum(counts)))
+        self.check(self.lib.csf_gather_columns(self.h, _dp(loc), cnt, _dp(out)))
+        return out
+
     @property
     def launch_count(self) -> int:
         n = C.c_ulonglong()
@@ -425,6 +441,15 @@ def look_at(eye, target, up=(0.0, 0.0, 1.0)) -> np.ndarray:
     y = np.cross(z, x)
     R = np.stack([x, y, z], axis=1)
     return np.concatenate([R.reshape(9), eye])
+
+
+def comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (csf_comm_unique_id), created on rank 0."""
+    buf = C.create_string_buffer(128)
+    rc = library().csf_comm_unique_id(buf)
+    if rc != _capi.CSF_OK:
+        raise RuntimeError("csf_comm_unique_id failed (libnccl.so.2 unavailable?)")
+    return buf.raw
 
 
 def config5_views(n: int = 256, seed: int = 4) -> np.ndarray:

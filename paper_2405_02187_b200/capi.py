@@ -27,6 +27,7 @@ EXPORTS = (
     "csf_volume_download", "csf_volume_block_count", "csf_volume_save", "csf_volume_load", "csf_sample_tsdf",
     "csf_sample_gradient", "csf_measured_tsdf", "csf_volume_download_hash", "csf_surface_update",
     "csf_surface_update_lifted", "csf_measured_tsdf_lifted", "csf_volume_info",
+    "csf_comm_unique_id", "csf_ctx_attach_comm", "csf_gather_columns",
     "csf_raycast", "csf_track_frame", "csf_track_frame_traced", "csf_icp_energy_derivs", "csf_view_scores", "csf_associate",
     "csf_linearized_step", "csf_pairwise_sum", "csf_pipeline_create", "csf_pipeline_destroy", "csf_pipeline_upload",
     "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_hessian", "csf_pipeline_run_host", "csf_pipeline_volume", "csf_pipeline_set_graph",
@@ -132,6 +133,9 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_surface_update": (ip, [vp, dp, ip, ip, dp, dp, C.POINTER(C.c_int)]),
         "csf_surface_update_lifted": (ip, [vp, dp, ip, ip, dp, dp, C.POINTER(C.c_int)]),
         "csf_volume_info": (ip, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]),
+        "csf_comm_unique_id": (ip, [C.c_char_p]),
+        "csf_ctx_attach_comm": (ip, [vp, ip, ip, C.c_char_p]),
+        "csf_gather_columns": (ip, [vp, dp, C.POINTER(C.c_int), dp]),
         "csf_raycast": (ip, [vp, dp, dp, ip, ip, C.POINTER(RaycastCfg), dp, dp]),
         "csf_track_frame": (ip, [vp, dp, ip, ip, dp, C.POINTER(Intrinsics), C.POINTER(IcpCfg), dp,
                                  C.POINTER(TrackResult)]),

@@ -21,6 +21,9 @@
 #include <memory>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is opened at runtime (csf_ctx_attach_comm)
+
 #include "../../include/csf_b200.h"
 #include "../../include/csf_detmath.h"
 #include "csf_internal.h"
@@ -69,6 +72,11 @@ struct csf_ctx_s {
   EnergyScratch energy;     // icp energy / correspondence-list scratch
   double* corr_upload = nullptr;
   size_t corr_upload_cap = 0;
+  // direction-sharded runs: the NCCL communicator of csf_gather_columns
+  ncclComm_t comm = nullptr;
+  int n_ranks = 1, rank = 0;
+  double* gather_buf = nullptr;
+  size_t gather_cap = 0;
 };
 
 // Brackets a launch with events when profiling is on.
@@ -418,10 +426,124 @@ extern "C" int csf_ctx_create(int device, csf_ctx* out) {
   return CSF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// NCCL, opened at runtime: no link-time dependency, and in a process that
+// already mapped a libnccl.so.2 (torch's) that same library is used.
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.err = std::string("libnccl.so.2 not found: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(sym("ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(sym("ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
+    api.broadcast = reinterpret_cast<decltype(api.broadcast)>(sym("ncclBroadcast"));
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.broadcast && api.group_start &&
+             api.group_end && api.error_string;
+    if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
+  });
+  return api;
+}
+}  // namespace
+
+extern "C" int csf_comm_unique_id(unsigned char* id) {
+  if (!id) return CSF_EINVAL;
+  const NcclApi& n = nccl();
+  if (!n.ok) return CSF_ERUNTIME;
+  ncclUniqueId u;
+  if (n.get_unique_id(&u) != ncclSuccess) return CSF_ERUNTIME;
+  std::memcpy(id, &u, sizeof(u));
+  return CSF_OK;
+}
+
+extern "C" int csf_ctx_attach_comm(csf_ctx ctx, int n_ranks, int rank, const unsigned char* id) {
+  if (!ctx || !id || n_ranks <= 0 || rank < 0 || rank >= n_ranks) return CSF_EINVAL;
+  const NcclApi& n = nccl();
+  if (!n.ok) return fail(ctx, CSF_ERUNTIME, "csf_ctx_attach_comm: " + n.err);
+  cudaSetDevice(ctx->device);
+  if (ctx->comm) {
+    n.comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  const ncclResult_t r = n.comm_init_rank(&ctx->comm, n_ranks, u, rank);
+  if (r != ncclSuccess) {
+    ctx->comm = nullptr;
+    return fail(ctx, CSF_ERUNTIME, std::string("csf_ctx_attach_comm: ") + n.error_string(r));
+  }
+  ctx->n_ranks = n_ranks;
+  ctx->rank = rank;
+  return CSF_OK;
+}
+
+extern "C" int csf_gather_columns(csf_ctx ctx, const double* local, const int* counts, double* out) {
+  if (!ctx || !counts || !out) return CSF_EINVAL;
+  if (!ctx->comm) return fail(ctx, CSF_EINVAL, "csf_gather_columns: no communicator (csf_ctx_attach_comm)");
+  const NcclApi& n = nccl();
+  cudaSetDevice(ctx->device);
+  std::vector<size_t> off(ctx->n_ranks + 1, 0);
+  for (int r = 0; r < ctx->n_ranks; ++r) {
+    if (counts[r] < 0) return CSF_EINVAL;
+    off[r + 1] = off[r] + static_cast<size_t>(counts[r]);
+  }
+  const size_t total = off[ctx->n_ranks];
+  if (counts[ctx->rank] > 0 && !local) return CSF_EINVAL;
+  if (total > ctx->gather_cap) {
+    if (ctx->gather_buf) cudaFree(ctx->gather_buf);
+    ctx->gather_buf = nullptr;
+    ctx->gather_cap = 0;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->gather_buf, sizeof(double) * std::max<size_t>(total, 1)));
+    ctx->gather_cap = total;
+  }
+  double* buf = ctx->gather_buf;
+  if (counts[ctx->rank] > 0)
+    CUDA_TRY(ctx, cudaMemcpyAsync(buf + off[ctx->rank], local, sizeof(double) * counts[ctx->rank],
+                                  cudaMemcpyHostToDevice, ctx->stream));
+  // every rank's block broadcast from its owner, in place (one NCCL group)
+  n.group_start();
+  for (int r = 0; r < ctx->n_ranks; ++r)
+    if (counts[r] > 0) {
+      const ncclResult_t e = n.broadcast(buf + off[r], buf + off[r], counts[r], ncclDouble, r, ctx->comm, ctx->stream);
+      if (e != ncclSuccess) {
+        n.group_end();
+        return fail(ctx, CSF_ERUNTIME, std::string("csf_gather_columns: ") + n.error_string(e));
+      }
+    }
+  const ncclResult_t ge = n.group_end();
+  if (ge != ncclSuccess) return fail(ctx, CSF_ERUNTIME, std::string("csf_gather_columns: ") + n.error_string(ge));
+  if (total > 0) CUDA_TRY(ctx, d2h(out, buf, sizeof(double) * total, ctx->stream));
+  return CSF_OK;
+}
+
 extern "C" int csf_ctx_destroy(csf_ctx ctx) {
   if (!ctx) return CSF_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) nccl().comm_destroy(ctx->comm);
+  if (ctx->gather_buf) cudaFree(ctx->gather_buf);
   if (ctx->d_err) cudaFree(ctx->d_err);
   energy_scratch_release(ctx->energy);
   if (ctx->corr_upload) cudaFree(ctx->corr_upload);
