@@ -185,10 +185,7 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def traffic_for(cat, workload):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
-    category's kernel from the committed ncu --set full capture
-    (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
+def _ncu_record(cat, workload):
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
@@ -196,6 +193,38 @@ def traffic_for(cat, workload):
         return json.loads(p.read_text()).get(workload, {}).get(cat)
     except Exception:
         return None
+
+
+def traffic_for(cat, workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
+    category's kernel from the committed ncu --set full capture
+    (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
+    r = _ncu_record(cat, workload)
+    return r.get("dram_bytes") if isinstance(r, dict) else r
+
+
+def fp64_peak():
+    """The FP64 pipe peak measured on this pool (tools/fp64_peak.cu, committed
+    under profiles/): (TFLOP/s with FMA, source)."""
+    for p in sorted((ROOT / "profiles").glob("*fp64_peak.json"), reverse=True):
+        try:
+            return float(json.loads(p.read_text())["fp64_tflops_fma"]), f"measured ({p.name})"
+        except Exception:
+            continue
+    return None, "not measured"
+
+
+def fp64_roofline(cat, workload):
+    """FP64 throughput of the category's captured launch (ncu thread-instruction
+    counts / ncu duration) against the measured FP64 peak."""
+    r = _ncu_record(cat, workload)
+    if not isinstance(r, dict) or not r.get("duration_s"):
+        return None
+    peak, src = fp64_peak()
+    ach = r["fp64_flops"] / r["duration_s"] / 1e12
+    return {"achieved_tflops": ach, "peak_tflops": peak, "frac": ach / peak if peak else None,
+            "pipe_active_pct": r.get("fp64_pipe_active_pct"), "peak_source": src,
+            "source": "one level-0 launch under ncu (profiles/traffic.json): 2 dfma + dadd + dmul per duration"}
 
 
 def cpu_sample(depth, gt, k, frames, units, workload, packed=False):
@@ -361,13 +390,23 @@ def algorithmic_bytes_per_step(cat, stats, D, W, H, n_frames):
         return 3 * vis_vox * 16 * tracked / max(n_frames, 1) + tracked * P_tot * (6 * 8 + 16), \
             "3 levels x visible voxels x 16 B (F.re, W) + real vertex/normal maps and hit alphas written"
     if cat == "raycast_lift":
-        return 3 * vis_vox * 8 * D * tracked / max(n_frames, 1) + tracked * P_tot * 6 * 8 * (1 + D), \
-            "3 levels x visible voxels x 8D B (channels) + lifted vertex/normal maps written"
+        # per pixel: the lifted vertex/normal written (48 (1+D) B) and the hit
+        # record read (32 B); per hit pixel one trilinear cell of channel data
+        # (8 voxels x 8D B) — its other samples' cells are the neighbours'
+        # (L2 reuse).  Hits ~ the frame's correspondences' share of pixels.
+        hit_frac = float(stats[1:n_frames, 1].mean()) / (P / 4) if n_frames > 1 else 0.5
+        hit_frac = min(max(hit_frac, 0.0), 1.0)
+        return tracked * P_tot * (6 * 8 * (1 + D) + 32 + hit_frac * 8 * 8 * D), \
+            "per pixel: lifted vertex/normal written 48(1+D) B + hit record 32 B; per hit pixel one " \
+            "trilinear cell of channels 64D B (hit fraction from the level-0 correspondence count)"
     if cat == "icp":
         its = float(stats[1:n_frames, 0].sum())
         corr = float(stats[1:n_frames, 1].mean()) if n_frames > 1 else 0.0
-        per_it = 76800 * 3 * 8 + corr * 6 * 8 * (1 + D) + 300 * 27 * (1 + D) * 8 * 2
-        return its * per_it, "per taken iteration: depth reads + model vertex/normal (1+D ch) per correspondence + tile partials"
+        per_it = corr * 6 * 8 * (1 + D) + 148 * 27 * (1 + D) * 8 * 2
+        per_level = (P // 4) * 3 * 8  # the level's measured depth (3 taps per slot), read once per level launch
+        return its * per_it + 3 * tracked * per_level, \
+            "per taken iteration: model vertex/normal (1+D channels) per correspondence + 148 tile partials " \
+            "written and read; per level launch the measured depth once"
     if cat == "bilateral":
         return tracked * (4 + 8 + 8) * P, "float32 depth in, raw + filtered float64 out"
     return None, None
@@ -663,7 +702,7 @@ def main():
                           "frac": achieved / peak, "traffic": traffic_for(cat, args.workload), "kernel": cat,
                           "avg_launch_ms": avg_ms, "launches": cat_n, "share_of_step": cat_ms / prof_ms,
                           "algorithmic_bytes_per_launch": bytes_per_launch, "bytes_model": bytes_def,
-                          "peak_source": peak_src}
+                          "peak_source": peak_src, "fp64": fp64_roofline(cat, args.workload)}
     roofline = max(rooflines.values(), key=lambda r: r["share_of_step"]) if rooflines else None
 
     if four:
