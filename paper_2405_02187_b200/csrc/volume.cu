@@ -1107,14 +1107,19 @@ struct LiftRec {
   int ok;
   int pad_;
 };
-constexpr int kLiftPix = 32;  // pixels per block (8 lanes each in the real pass)
+constexpr int kLiftPix = 32;  // max pixels per block (8 lanes each in the real pass)
+// pixels per block: as many as keep the channel pass to one round of items
+inline int lift_pixels(int Dp) { return Dp <= 8 ? kLiftPix : (Dp >= 256 ? 1 : 256 / Dp); }
 
 template <typename V>
-__global__ void __launch_bounds__(256) k_raycast_lift_coop(V vol, const double* __restrict__ pose,
+#ifndef CSF_LIFT_MINB
+#define CSF_LIFT_MINB 2
+#endif
+__global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol, const double* __restrict__ pose,
                                                            const double* __restrict__ intr, int w, int h, int Dp,
                                                            const double2* __restrict__ hits, double* __restrict__ vre,
                                                            double* __restrict__ nre, double* __restrict__ vim,
-                                                           double* __restrict__ nim) {
+                                                           double* __restrict__ nim, int npix) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double sm[];
@@ -1129,10 +1134,10 @@ __global__ void __launch_bounds__(256) k_raycast_lift_coop(V vol, const double* 
   // ---- real pass: lane s of pixel p
   {
     const int p = threadIdx.x >> 3, s = threadIdx.x & 7;
-    const int pix = blockIdx.x * kLiftPix + p;
-    LiftRec& r = recs[p];
+    const int pix = blockIdx.x * npix + p;
+    LiftRec& r = recs[p < npix ? p : 0];
     double2 hit = make_double2(0.0, -1.0);
-    if (pix < P) hit = hits[pix];
+    if (p < npix && pix < P) hit = hits[pix];
     const bool active = hit.y >= 0.0;
     const int x = pix % w, y = pix / w;
     double R[9], T[3];
@@ -1182,7 +1187,7 @@ __global__ void __launch_bounds__(256) k_raycast_lift_coop(V vol, const double* 
     double fs[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) fs[k] = __shfl_sync(0xffffffffu, g, lane0 + 2 + k);
-    if (s == 0) {
+    if (s == 0 && p < npix) {
       bool good = active && group_ok;
       double grad[3], ln = 0.0;
 #pragma unroll
@@ -1223,11 +1228,19 @@ __global__ void __launch_bounds__(256) k_raycast_lift_coop(V vol, const double* 
   const double inv_fx2 = 1.0 / (fxk * fxk), inv_fy2 = 1.0 / (fyk * fyk), inv_vs2 = 1.0 / (hv * hv);
   const double inv_2h2 = 1.0 / ((2.0 * hv) * (2.0 * hv));
   (void)inv_fx2; (void)inv_fy2; (void)inv_vs2; (void)inv_2h2;
-  for (int it = threadIdx.x; it < kLiftPix * Dp; it += blockDim.x) {
+  for (int it = threadIdx.x; it < npix * Dp; it += blockDim.x) {
     const int p = it / Dp, d = it - p * Dp;
     const LiftRec& r = recs[p];
-    if (!r.ok) continue;
-    const int pix = blockIdx.x * kLiftPix + p;
+    const int pix = blockIdx.x * npix + p;
+    if (pix >= P) continue;
+    if (!r.ok) {  // no surface: zero channels (no separate memset of the maps)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        vim[(3LL * pix + c) * Dp + d] = 0.0;
+        nim[(3LL * pix + c) * Dp + d] = 0.0;
+      }
+      continue;
+    }
     const int x = pix % w, y = pix / w;
     const int ch = 1 + d;
     const double tx = static_cast<double>(x) - kk[2 * C], ty = static_cast<double>(y) - kk[3 * C];
@@ -1731,7 +1744,7 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
       launch_pdl(k_raycast_march<V>, dim3((P + 127) / 128), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp,
                  near_clip, far_clip, step, box, hits, vre, nre, atab, n_tab);
     }
-    if (Dp > 0 && vim) {
+    if (Dp > 0 && vim && order == 2) {  // the first-order lift writes every pixel
       cudaMemsetAsync(vim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
       cudaMemsetAsync(nim, 0, sizeof(double) * 3 * Dp * static_cast<size_t>(P), L.stream);
     }
@@ -1749,9 +1762,10 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
   }
   // first order: the cooperative lift (8 lanes per pixel for the real chain,
   // then one thread per (pixel, channel))
-  const size_t smem_c = smem + sizeof(LiftRec) * kLiftPix;
-  launch_pdl(k_raycast_lift_coop<V>, dim3((P + kLiftPix - 1) / kLiftPix), dim3(8 * kLiftPix), smem_c, L.stream, view,
-             pose, intr, w, h, Dp, hits, vre, nre, vim, nim);
+  const int npix = lift_pixels(Dp);
+  const size_t smem_c = smem + sizeof(LiftRec) * npix;
+  launch_pdl(k_raycast_lift_coop<V>, dim3((P + npix - 1) / npix), dim3(8 * kLiftPix), smem_c, L.stream, view,
+             pose, intr, w, h, Dp, hits, vre, nre, vim, nim, npix);
   *L.launches += 1;
 }
 
