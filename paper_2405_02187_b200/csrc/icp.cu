@@ -56,9 +56,14 @@ using csfi::IcpLevelArgs;
 // ============================================================================
 constexpr int kLvWarps = csfi::kIcpLevelWarps;
 constexpr int kLvThreads = 32 * kLvWarps;
+// Association runs on warps 0..kAsWarps-1; the last warp is the channel warp
+// of the overlapped solve (it applies the channel step of iteration k while
+// the other warps associate iteration k + 1).
+constexpr int kAsWarps = kLvWarps - 1;
+constexpr int kAsThreads = 32 * kAsWarps;
 constexpr int kRounds = 2;                         // slots per thread in one association pass
 constexpr int kSegSlots = 576;                     // slots per shared-memory record segment (a VGA tile is 544)
-static_assert(kSegSlots <= kRounds * kLvThreads, "one association pass covers a segment");
+static_assert(kSegSlots <= kRounds * kAsThreads, "one association pass covers a segment");
 constexpr int kLvMaxTiles = csfi::kIcpMaxTiles;
 constexpr int kLvGroup = csfi::kIcpGroup;
 constexpr int kLvMaxGroups = (kLvMaxTiles + kLvGroup - 1) / kLvGroup;
@@ -154,7 +159,9 @@ __device__ __noinline__ void level_measure(const IcpLevelArgs& a, int seg0, int 
 // (geometry.cuh) on the measured vertex/normal of level_measure, whose tests
 // carry no side effects, so evaluating all of them and combining gives the
 // reference's answer — then the slot-order compaction of the correspondences
-// into the shared-memory records.  Returns the segment's correspondence count.
+// into the shared-memory records.  Runs on the kAsThreads threads of warps
+// 0..kAsWarps-1 (named barrier 1).  Returns the segment's correspondence count.
+CSF_DEV void assoc_barrier() { asm volatile("bar.sync 1, %0;" ::"n"(kAsThreads) : "memory"); }
 __device__ __noinline__ int level_associate(const IcpLevelArgs& a, int seg0, int seg1, const double* s_pose,
                                             const double* s_intr, const Pose<double>& w2p, const double* s_meas,
                                             double* s_rec, int* s_m, int* s_wsum) {
@@ -172,7 +179,7 @@ __device__ __noinline__ int level_associate(const IcpLevelArgs& a, int seg0, int
   long long mi[kRounds];
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
-    const int e = r * kLvThreads + static_cast<int>(threadIdx.x);
+    const int e = r * kAsThreads + static_cast<int>(threadIdx.x);
     const int slot = seg0 + e;
     ok[r] = slot < seg1 && e < kSegSlots;
     xs[r] = ok[r] ? (slot % nxs) * a.stride : 0;
@@ -220,10 +227,10 @@ __device__ __noinline__ int level_associate(const IcpLevelArgs& a, int seg0, int
   for (int r = 0; r < kRounds; ++r) {
     const unsigned ballot = __ballot_sync(0xffffffffu, ok[r]);
     if (lane == 0) s_wsum[r * kLvWarps + warp] = __popc(ballot);
-    __syncthreads();
+    assoc_barrier();
     int before = 0, rtotal = 0;
 #pragma unroll
-    for (int k = 0; k < kLvWarps; ++k) {
+    for (int k = 0; k < kAsWarps; ++k) {
       const int c = s_wsum[r * kLvWarps + k];
       if (k < warp) before += c;
       rtotal += c;
@@ -234,7 +241,7 @@ __device__ __noinline__ int level_associate(const IcpLevelArgs& a, int seg0, int
       // r = (p - mv) . mn, J = [mn; p x mn] — the oracle's operation order
       const int e = total + before + __popc(ballot & ((1u << lane) - 1u));
       const int x = xs[r], y = ys[r];
-      const int sl = r * kLvThreads + static_cast<int>(threadIdx.x);
+      const int sl = r * kAsThreads + static_cast<int>(threadIdx.x);
       const double d = d0[r];
       const double nx = d * (static_cast<double>(x) - cx), ny = d * (static_cast<double>(y) - cy);
       const double vv[3] = {s_meas[sl], s_meas[kSegSlots + sl], d};  // (nx / fx, ny / fy, d)
@@ -415,8 +422,11 @@ __device__ __noinline__ void increment_pose(const L<1> (&d)[6], const Pose<L<1>>
 CSF_DEV void lv_mark(unsigned seq, int it, int phase);
 struct LevelSolveShared {
   double fm[36];  // factors, row-major (lower triangle and diagonal)
+  double x[6];    // the real step (overlapped solve)
+  double prev[12];  // the real pose before the step (overlapped solve)
   int ftr[6];
   int degen, finite, done, conv;
+  int fin_re;  // the real step is finite (overlapped solve)
 };
 
 CSF_HD constexpr int tri_row(int l) { return l < 1 ? 0 : l < 3 ? 1 : l < 6 ? 2 : l < 10 ? 3 : l < 15 ? 4 : 5; }
@@ -535,11 +545,14 @@ CSF_DEV void ldlt6_apply_smem(const double* fm, const int* tr, const double* rhs
 }
 
 __device__ __noinline__ void level_solve(const IcpLevelArgs& a, const double* s_tot, double* s_pose,
-                                         LevelSolveShared* ls, double (&dre)[6], unsigned seq, int it) {
+                                         LevelSolveShared* ls, double (&dre)[6], unsigned seq, int it,
+                                         bool factored) {
   const int C = 1 + a.Dp;
   const int tid = threadIdx.x;
-  if (tid < 32) ldlt6_warp(s_tot, C, ls);
-  __syncthreads();
+  if (!factored) {
+    if (tid < 32) ldlt6_warp(s_tot, C, ls);
+    __syncthreads();
+  }
   lv_mark(seq, it, 8);
   // channel threads: thread t < max(Dp, 1) owns channel t + 1 (thread 0 also the real part)
   const bool mine = tid < (a.Dp > 0 ? a.Dp : 1);
@@ -619,6 +632,118 @@ __device__ __noinline__ void level_solve(const IcpLevelArgs& a, const double* s_
   for (int i = 0; i < 6; ++i) dre[i] = tid == 0 ? re(d[i]) : 0.0;
 }
 
+// Overlapped solve (single-segment tiles, 1 <= Dp < 32), after ldlt6_warp:
+//   real_step (thread 0): the real step x from the factors, the real pose
+//     exp(x) T (exp_map<double>: the real parts of the lifted evaluation, the
+//     same operations) and the step-tolerance decision — assuming every
+//     channel is finite — then warps 0..kAsWarps-1 associate the next
+//     iteration;
+//   channel_step (the channel warp, lane l = channel l + 1), concurrently:
+//     the real step again, the channel step in tangent form and exp(delta) T
+//     on the channels, against the real pose before the step (ls->prev);
+//     delta.allFinite() (icp.cpp:45) is a warp vote, and if it fails delta is
+//     zero for every channel and the kernel reverts the real pose
+//     (exp(0) T of the saved pose) and decides again.
+__device__ __noinline__ void real_step(const IcpLevelArgs& a, const double* s_tot, double* s_pose,
+                                       LevelSolveShared* ls, bool revert, unsigned seq, int it) {
+  const int C = 1 + a.Dp;
+  double x[6];
+  if (revert) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) x[i] = 0.0;
+  } else {
+    double nb[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) nb[i] = -s_tot[(21 + i) * C];
+    ldlt6_apply_smem(ls->fm, ls->ftr, nb, x);
+    bool fin = true;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) fin = fin && isfinite(x[i]);
+    ls->fin_re = fin ? 1 : 0;
+    if (!fin)
+#pragma unroll
+      for (int i = 0; i < 6; ++i) x[i] = 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) ls->x[i] = x[i];
+  Pose<double> cur;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) cur.R.m[e] = ls->prev[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) cur.t.v[e] = ls->prev[9 + e];
+  lv_mark(seq, it, 11);
+  const Pose<double> ex = exp_map<double>(x);
+  lv_mark(seq, it, 12);
+  const Pose<double> np = compose(ex, cur);  // apply_increment (se3.hpp:116-119)
+#pragma unroll
+  for (int e = 0; e < 9; ++e) s_pose[e * C] = np.R.m[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) s_pose[(9 + e) * C] = np.t.v[e];
+  double sq[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) sq[i] = x[i] * x[i];
+  const double nrm = sqrt((sq[0] + (sq[1] + sq[2])) + (sq[3] + (sq[4] + sq[5])));
+  ls->done = 0;
+  ls->conv = 0;
+  if (nrm < a.tol) {
+    ls->done = 1;
+    ls->conv = a.level == 0 ? 1 : 0;
+  }
+}
+
+__device__ __noinline__ void channel_step(const IcpLevelArgs& a, const double* s_tot, double* s_pose,
+                                          LevelSolveShared* ls) {
+  const int C = 1 + a.Dp;
+  const int lane = threadIdx.x & 31;
+  const bool mine = lane < a.Dp;
+  const int ch = 1 + lane;
+  L<1> d[6];
+  bool fin = true;
+  if (mine) {
+    // the real step (the same bits as real_step's)
+    double nb[6], x[6], rhs[6], dx[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) nb[i] = -s_tot[(21 + i) * C];
+    ldlt6_apply_smem(ls->fm, ls->ftr, nb, x);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) fin = fin && isfinite(x[i]);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      double ax = 0.0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) ax = ax + s_tot[(i >= j ? tri(i, j) : tri(j, i)) * C + ch] * x[j];
+      rhs[i] = -s_tot[(21 + i) * C + ch] - ax;
+    }
+    ldlt6_apply_smem(ls->fm, ls->ftr, rhs, dx);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      d[i].re = x[i];
+      d[i].im[0] = dx[i];
+      fin = fin && isfinite(dx[i]);
+    }
+  }
+  const bool all_fin = __all_sync(0xffffffffu, !mine || fin);
+  if (!mine) return;
+  if (!all_fin)
+#pragma unroll
+    for (int i = 0; i < 6; ++i) d[i] = lit<L<1>>(0.0);
+  Pose<L<1>> cur, np;
+#pragma unroll
+  for (int e = 0; e < 12; ++e) {
+    L<1> v;
+    v.re = ls->prev[e];
+    v.im[0] = s_pose[e * C + ch];
+    if (e < 9) cur.R.m[e] = v;
+    else cur.t.v[e - 9] = v;
+  }
+  increment_pose(d, cur, &np);
+#pragma unroll
+  for (int e = 0; e < 9; ++e) s_pose[e * C + ch] = np.R.m[e].im[0];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) s_pose[(9 + e) * C + ch] = np.t.v[e].im[0];
+  if (lane == 0 && !all_fin) ls->finite = 0;
+}
+
 // Debug timeline (tools/icp_timing.py, csf_debug_icp_clock): per launch, CTA,
 // iteration and phase, the %globaltimer in ns (64 launches x 256 CTAs x 32
 // iterations x 16 phases); off (nullptr) by default.
@@ -648,7 +773,7 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
   double* s_meas = s_rec + kRecFields * kSegSlots;            // [6][kSegSlots]
   int* s_m = reinterpret_cast<int*>(s_meas + 6 * kSegSlots);  // [kSegSlots]
   __shared__ int s_wsum[kRounds * kLvWarps];
-  __shared__ int s_n, s_last;
+  __shared__ int s_n, s_last, s_na;
   __shared__ LevelSolveShared ls;
   __shared__ double s_w2p[12];
   __shared__ unsigned s_gen;
@@ -680,6 +805,10 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
   bool converged = false;
   // single-segment tiles (VGA and below): the measured side once per level
   if (n_segs == 1) level_measure(a, t0, t1, s_intr, s_meas);
+  // overlapped solve: the channel step of iteration k runs on the channel warp
+  // while warps 0..kAsWarps-1 associate iteration k + 1
+  const bool overlap = n_segs == 1 && passes == 1 && a.Dp >= 1 && a.Dp < 32;
+  bool pre_assoc = false;  // this iteration's association already ran
 
   for (int it = 0; it < a.iterations; ++it) {
     lv_mark(seq, it, 0);
@@ -694,15 +823,21 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
       int ebase = 0;
       for (int sg = 0; sg < n_segs; ++sg) {
         int n;
-        if (n_segs > 1 || p == 0) {
+        if (pre_assoc) {
+          n = s_na;
+        } else if (n_segs > 1 || p == 0) {
           __syncthreads();  // the previous segment's records are consumed
           const int s0 = t0 + sg * kSegSlots, s1 = min(t1, s0 + kSegSlots);
           if (n_segs > 1) {
             level_measure(a, s0, s1, s_intr, s_meas);
             __syncthreads();
           }
-          n = level_associate(a, s0, s1, s_pose, s_intr, w2p, s_meas, s_rec, s_m, s_wsum);
+          if (warp < kAsWarps) {
+            n = level_associate(a, s0, s1, s_pose, s_intr, w2p, s_meas, s_rec, s_m, s_wsum);
+            if (tid == 0) s_na = n;
+          }
           __syncthreads();
+          n = s_na;
           if (tid == 0) s_n = n;  // kept for the passes that reuse the records
         } else {
           n = s_n;
@@ -803,13 +938,45 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
       ls.conv = 0;
       ls.finite = 1;
     }
+    if (tid < 12) ls.prev[tid] = s_pose[tid * C];  // the pose before the step (overlapped solve)
     __syncthreads();
     // ---- D: the solve (every CTA, identical bits)
     const int n = s_n;
     last_n = n;
     if (n < 12) break;  // icp.cpp:199, before the step
     double dre[6];
-    level_solve(a, s_tot, s_pose, &ls, dre, seq, it);
+    if (tid < 32) ldlt6_warp(s_tot, C, &ls);
+    __syncthreads();
+    lv_mark(seq, it, 13);
+    pre_assoc = false;
+    if (overlap && !ls.degen) {
+      if (warp == kAsWarps) {
+        channel_step(a, s_tot, s_pose, &ls);
+      } else {
+        if (tid == 0) real_step(a, s_tot, s_pose, &ls, false, seq, it);
+        assoc_barrier();
+        lv_mark(seq, it, 8);
+        if (!ls.done && it + 1 < a.iterations) {
+          const int na = level_associate(a, t0, t1, s_pose, s_intr, w2p, s_meas, s_rec, s_m, s_wsum);
+          if (tid == 0) s_na = na;
+        }
+      }
+      __syncthreads();
+      lv_mark(seq, it, 9);
+      pre_assoc = !ls.done && it + 1 < a.iterations;
+      if (!ls.finite && ls.fin_re) {
+        // a channel of delta is not finite: delta = 0 (icp.cpp:45), the real
+        // pose is exp(0) T of the saved one, and the next association reruns
+        if (tid == 0) real_step(a, s_tot, s_pose, &ls, true, seq, it);
+        __syncthreads();
+        pre_assoc = false;
+      }
+      lv_mark(seq, it, 10);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) dre[i] = tid == 0 ? ls.x[i] : 0.0;
+    } else {
+      level_solve(a, s_tot, s_pose, &ls, dre, seq, it, true);
+    }
     lv_mark(seq, it, 5);
     ++taken;
 #pragma unroll

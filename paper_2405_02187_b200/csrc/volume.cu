@@ -1078,15 +1078,32 @@ CSF_DEV bool sample_real_ex(const V& vol, double px, double py, double pz, doubl
   return true;
 }
 
-// Channel d of a sample at a position with channel `pim` (3 values).
-CSF_DEV double sample_channel(const VoxelStore& vox, const int* vid, const double* wgt, const double* ds,
-                              const double* pim, double vs, double inv_vs2, int d) {
-  double t = 0.0;
+// Channels d .. d + CH - 1 of a sample at positions with channels pim[k]
+// (CH = 2: one 16-byte load per corner; needs Dp and d even).
+template <int CH>
+CSF_DEV void sample_channels(const VoxelStore& vox, const int* vid, const double* wgt, const double* ds,
+                             const double (*pim)[3], double vs, double inv_vs2, int d, double* out) {
+  double fv[8][CH];
+  if constexpr (CH == 2) {
 #pragma unroll
-  for (int a = 0; a < 3; ++a) t += ds[a] * CSF_CH_DIV(pim[a] * vs, vs * vs, inv_vs2);
+    for (int c = 0; c < 8; ++c) {
+      const double2 v2 = __ldg(reinterpret_cast<const double2*>(vox.fim + static_cast<long long>(vid[c]) * vox.Dp + d));
+      fv[c][0] = v2.x;
+      fv[c][1] = v2.y;
+    }
+  } else {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) t += wgt[c] * vox.fim[static_cast<long long>(vid[c]) * vox.Dp + d];
-  return t;
+    for (int c = 0; c < 8; ++c) fv[c][0] = __ldg(vox.fim + static_cast<long long>(vid[c]) * vox.Dp + d);
+  }
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    double t = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) t += ds[a] * CSF_CH_DIV(pim[k][a] * vs, vs * vs, inv_vs2);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) t += wgt[c] * fv[c][k];
+    out[k] = t;
+  }
 }
 
 // Cooperative lift: the per-pixel real chain (2 crossing samples, 6
@@ -1109,12 +1126,13 @@ struct LiftRec {
 };
 constexpr int kLiftPix = 32;  // max pixels per block (8 lanes each in the real pass)
 // pixels per block: as many as keep the channel pass to one round of items
-inline int lift_pixels(int Dp) { return Dp <= 8 ? kLiftPix : (Dp >= 256 ? 1 : 256 / Dp); }
+// (items = channel-pass items per pixel)
+inline int lift_pixels(int items) { return items <= 8 ? kLiftPix : (items >= 256 ? 1 : 256 / items); }
 
-template <typename V>
 #ifndef CSF_LIFT_MINB
 #define CSF_LIFT_MINB 2
 #endif
+template <typename V, int CH>
 __global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol, const double* __restrict__ pose,
                                                            const double* __restrict__ intr, int w, int h, int Dp,
                                                            const double2* __restrict__ hits, double* __restrict__ vre,
@@ -1223,70 +1241,97 @@ __global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol,
   }
   __syncthreads();
   if (Dp == 0) return;
-  // ---- channel pass: one thread per (pixel, channel)
+  // ---- channel pass: one thread per (pixel, CH channels); CH = 2 gathers
+  // each corner's two channels with one 16-byte load (twice the pixels per
+  // warp-wide gather, so adjacent pixels' shared voxels cost one L1 line)
   const double fxk = kk[0], fyk = kk[C];
   const double inv_fx2 = 1.0 / (fxk * fxk), inv_fy2 = 1.0 / (fyk * fyk), inv_vs2 = 1.0 / (hv * hv);
   const double inv_2h2 = 1.0 / ((2.0 * hv) * (2.0 * hv));
   (void)inv_fx2; (void)inv_fy2; (void)inv_vs2; (void)inv_2h2;
-  for (int it = threadIdx.x; it < npix * Dp; it += blockDim.x) {
-    const int p = it / Dp, d = it - p * Dp;
+  const int Dh = Dp / CH;
+  for (int it = threadIdx.x; it < npix * Dh; it += blockDim.x) {
+    const int p = it / Dh, d = (it - p * Dh) * CH;
     const LiftRec& r = recs[p];
     const int pix = blockIdx.x * npix + p;
     if (pix >= P) continue;
     if (!r.ok) {  // no surface: zero channels (no separate memset of the maps)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        vim[(3LL * pix + c) * Dp + d] = 0.0;
-        nim[(3LL * pix + c) * Dp + d] = 0.0;
-      }
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          vim[(3LL * pix + c) * Dp + d + k] = 0.0;
+          nim[(3LL * pix + c) * Dp + d + k] = 0.0;
+        }
       continue;
     }
     const int x = pix % w, y = pix / w;
-    const int ch = 1 + d;
     const double tx = static_cast<double>(x) - kk[2 * C], ty = static_cast<double>(y) - kk[3 * C];
     const double rn = r.rn, den = r.den, num = r.num, ln = r.ln;
     const double inv_rn2 = 1.0 / (rn * rn), inv_den2 = 1.0 / (den * den), inv_ln2 = 1.0 / (ln * ln);
     (void)inv_rn2; (void)inv_den2; (void)inv_ln2;
-    const double dci[3] = {CSF_CH_DIV(-kk[2 * C + ch] * fxk - tx * kk[ch], fxk * fxk, inv_fx2),
-                           CSF_CH_DIV(-kk[3 * C + ch] * fyk - ty * kk[C + ch], fyk * fyk, inv_fy2), 0.0};
-    const double doti = (r.dc[0] * dci[0] + dci[0] * r.dc[0]) + ((r.dc[1] * dci[1] + dci[1] * r.dc[1]) + 0.0);
-    const double rni = (0.5 / rn) * doti;
-    double dni[3], diri[3];
+    double diri[CH][3], Ti[CH][3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) dni[a] = CSF_CH_DIV(dci[a] * rn - r.dc[a] * rni, rn * rn, inv_rn2);
+    for (int k = 0; k < CH; ++k) {
+      const int ch = 1 + d + k;
+      const double dci[3] = {CSF_CH_DIV(-kk[2 * C + ch] * fxk - tx * kk[ch], fxk * fxk, inv_fx2),
+                             CSF_CH_DIV(-kk[3 * C + ch] * fyk - ty * kk[C + ch], fyk * fyk, inv_fy2), 0.0};
+      const double doti = (r.dc[0] * dci[0] + dci[0] * r.dc[0]) + ((r.dc[1] * dci[1] + dci[1] * r.dc[1]) + 0.0);
+      const double rni = (0.5 / rn) * doti;
+      double dni[3];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const double t0 = sm[(3 * q) * C] * dni[0] + sm[(3 * q) * C + ch] * r.dn[0];
-      const double t1 = sm[(3 * q + 1) * C] * dni[1] + sm[(3 * q + 1) * C + ch] * r.dn[1];
-      const double t2 = sm[(3 * q + 2) * C] * dni[2] + sm[(3 * q + 2) * C + ch] * r.dn[2];
-      diri[q] = t0 + (t1 + t2);
+      for (int a2 = 0; a2 < 3; ++a2) dni[a2] = CSF_CH_DIV(dci[a2] * rn - r.dc[a2] * rni, rn * rn, inv_rn2);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const double t0 = sm[(3 * q) * C] * dni[0] + sm[(3 * q) * C + ch] * r.dn[0];
+        const double t1 = sm[(3 * q + 1) * C] * dni[1] + sm[(3 * q + 1) * C + ch] * r.dn[1];
+        const double t2 = sm[(3 * q + 2) * C] * dni[2] + sm[(3 * q + 2) * C + ch] * r.dn[2];
+        diri[k][q] = t0 + (t1 + t2);
+        Ti[k][q] = sm[(9 + q) * C + ch];
+      }
     }
-    const double Ti[3] = {sm[9 * C + ch], sm[10 * C + ch], sm[11 * C + ch]};
-    const double q0i[3] = {Ti[0] + r.a0 * diri[0], Ti[1] + r.a0 * diri[1], Ti[2] + r.a0 * diri[2]};
-    const double q1i[3] = {Ti[0] + r.a1 * diri[0], Ti[1] + r.a1 * diri[1], Ti[2] + r.a1 * diri[2]};
-    const double f0i = sample_channel(vol.vox, r.vid[0], r.wgt[0], r.ds[0], q0i, hv, inv_vs2, d);
-    const double f1i = sample_channel(vol.vox, r.vid[1], r.wgt[1], r.ds[1], q1i, hv, inv_vs2, d);
-    const double numi = (r.a1 - r.a0) * f0i, deni = f1i - f0i;
-    const double asti = -CSF_CH_DIV(numi * den - num * deni, den * den, inv_den2);
-    double vvi[3];
+    double f0i[CH], f1i[CH];
+    {
+      double q0i[CH][3], q1i[CH][3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) vvi[a] = Ti[a] + (r.astar * diri[a] + asti * r.dir[a]);
-    double gi[3];
+      for (int k = 0; k < CH; ++k)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          q0i[k][q] = Ti[k][q] + r.a0 * diri[k][q];
+          q1i[k][q] = Ti[k][q] + r.a1 * diri[k][q];
+        }
+      sample_channels<CH>(vol.vox, r.vid[0], r.wgt[0], r.ds[0], q0i, hv, inv_vs2, d, f0i);
+      sample_channels<CH>(vol.vox, r.vid[1], r.wgt[1], r.ds[1], q1i, hv, inv_vs2, d, f1i);
+    }
+    double vvi[CH][3];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const double numi = (r.a1 - r.a0) * f0i[k], deni = f1i[k] - f0i[k];
+      const double asti = -CSF_CH_DIV(numi * den - num * deni, den * den, inv_den2);
+#pragma unroll
+      for (int a2 = 0; a2 < 3; ++a2) vvi[k][a2] = Ti[k][a2] + (r.astar * diri[k][a2] + asti * r.dir[a2]);
+    }
+    double gi[CH][3];
 #pragma unroll
     for (int axis = 0; axis < 3; ++axis) {
-      const double lo = sample_channel(vol.vox, r.vid[2 + 2 * axis], r.wgt[2 + 2 * axis], r.ds[2 + 2 * axis], vvi,
-                                       hv, inv_vs2, d);
-      const double hi = sample_channel(vol.vox, r.vid[3 + 2 * axis], r.wgt[3 + 2 * axis], r.ds[3 + 2 * axis], vvi,
-                                       hv, inv_vs2, d);
-      gi[axis] = CSF_CH_DIV((hi - lo) * (2.0 * hv), (2.0 * hv) * (2.0 * hv), inv_2h2);
-    }
-    const double l2i = (r.grad[0] * gi[0] + gi[0] * r.grad[0]) +
-                       ((r.grad[1] * gi[1] + gi[1] * r.grad[1]) + (r.grad[2] * gi[2] + gi[2] * r.grad[2]));
-    const double lni = (0.5 / ln) * l2i;
+      double lo[CH], hi[CH];
+      sample_channels<CH>(vol.vox, r.vid[2 + 2 * axis], r.wgt[2 + 2 * axis], r.ds[2 + 2 * axis], vvi, hv, inv_vs2, d,
+                          lo);
+      sample_channels<CH>(vol.vox, r.vid[3 + 2 * axis], r.wgt[3 + 2 * axis], r.ds[3 + 2 * axis], vvi, hv, inv_vs2, d,
+                          hi);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      vim[(3LL * pix + c) * Dp + d] = vvi[c];
-      nim[(3LL * pix + c) * Dp + d] = CSF_CH_DIV(gi[c] * ln - r.grad[c] * lni, ln * ln, inv_ln2);
+      for (int k = 0; k < CH; ++k)
+        gi[k][axis] = CSF_CH_DIV((hi[k] - lo[k]) * (2.0 * hv), (2.0 * hv) * (2.0 * hv), inv_2h2);
+    }
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const double l2i = (r.grad[0] * gi[k][0] + gi[k][0] * r.grad[0]) +
+                         ((r.grad[1] * gi[k][1] + gi[k][1] * r.grad[1]) + (r.grad[2] * gi[k][2] + gi[k][2] * r.grad[2]));
+      const double lni = (0.5 / ln) * l2i;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        vim[(3LL * pix + c) * Dp + d + k] = vvi[k][c];
+        nim[(3LL * pix + c) * Dp + d + k] = CSF_CH_DIV(gi[k][c] * ln - r.grad[c] * lni, ln * ln, inv_ln2);
+      }
     }
   }
 }
@@ -1762,10 +1807,19 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
   }
   // first order: the cooperative lift (8 lanes per pixel for the real chain,
   // then one thread per (pixel, channel))
-  const int npix = lift_pixels(Dp);
+#ifdef CSF_LIFT_SCALAR
+  const bool pair = false;
+#else
+  const bool pair = Dp % 2 == 0;
+#endif
+  const int npix = lift_pixels(pair ? Dp / 2 : Dp);
   const size_t smem_c = smem + sizeof(LiftRec) * npix;
-  launch_pdl(k_raycast_lift_coop<V>, dim3((P + npix - 1) / npix), dim3(8 * kLiftPix), smem_c, L.stream, view,
-             pose, intr, w, h, Dp, hits, vre, nre, vim, nim, npix);
+  if (pair)
+    launch_pdl(k_raycast_lift_coop<V, 2>, dim3((P + npix - 1) / npix), dim3(8 * kLiftPix), smem_c, L.stream, view,
+               pose, intr, w, h, Dp, hits, vre, nre, vim, nim, npix);
+  else
+    launch_pdl(k_raycast_lift_coop<V, 1>, dim3((P + npix - 1) / npix), dim3(8 * kLiftPix), smem_c, L.stream, view,
+               pose, intr, w, h, Dp, hits, vre, nre, vim, nim, npix);
   *L.launches += 1;
 }
 
