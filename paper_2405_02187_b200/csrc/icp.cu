@@ -440,13 +440,13 @@ __device__ __noinline__ void ldlt6_warp(const double* a_lower, int stride, Level
   double v = col_lane ? a_lower[l * stride] : 0.0;
   bool ok = true, stop = false, degen = false;
   int transp[6] = {0, 1, 2, 3, 4, 5};
-#pragma unroll 1
+#pragma unroll
   for (int k = 0; k < 6; ++k) {
     if (stop) continue;
     // pivot: the first strictly largest |m[i][i]|, i >= k
     double best = fabs(__shfl_sync(kFull, v, tri(k, k)));
     int piv = k;
-#pragma unroll 1
+#pragma unroll
     for (int i = k + 1; i < 6; ++i) {
       const double di = fabs(__shfl_sync(kFull, v, tri(i, i)));
       if (di > best) {
@@ -464,7 +464,7 @@ __device__ __noinline__ void ldlt6_warp(const double* a_lower, int stride, Level
     if (k > 0) {
       // temp[j] = m[j][j] m[k][j]; m[i][k] -= m[i][0] temp[0] + m[i][1] temp[1] + ...
       double sacc = 0.0;
-#pragma unroll 1
+#pragma unroll
       for (int j = 0; j < k; ++j) {
         const double tj = __shfl_sync(kFull, v, tri(j, j)) * __shfl_sync(kFull, v, tri(k, j));
         const double mij = __shfl_sync(kFull, v, r > j ? tri(r, j) : 0);
@@ -493,7 +493,7 @@ __device__ __noinline__ void ldlt6_warp(const double* a_lower, int stride, Level
     }
   }
   const double tol = 2.2250738585072014e-308;  // numeric_limits<double>::min()
-#pragma unroll 1
+#pragma unroll
   for (int i = 0; i < 6; ++i)
     if (!(fabs(__shfl_sync(kFull, v, tri(i, i))) > tol)) degen = true;
   if (col_lane) {
