@@ -419,11 +419,16 @@ __device__ __noinline__ void increment_pose(const L<1> (&d)[6], const Pose<L<1>>
 // unless every channel is finite (delta.allFinite(), icp.cpp:45); then
 // exp(delta) * T per channel thread (apply_increment, se3.hpp:116-119) and the
 // step-tolerance break (icp.cpp:235).  dre: the real delta (thread 0).
-CSF_DEV void lv_mark(unsigned seq, int it, int phase);
+CSF_DEV void lv_mark(unsigned seq, int it, int phase, int by = 0);
 struct LevelSolveShared {
   double fm[36];  // factors, row-major (lower triangle and diagonal)
   double x[6];    // the real step (overlapped solve)
   double prev[12];  // the real pose before the step (overlapped solve)
+  // real intermediates of exp_map(x) (overlapped solve): t, sin t, t/2,
+  // sin(t/2), a, b, c, and exp(x) itself (R row-major, then t)
+  double et, es1, eth, esh, ea, eb, ec;
+  double ex[12];
+  int small;  // t^2 < 1e-14 (the series branch of exp_map)
   int ftr[6];
   int degen, finite, done, conv;
   int fin_re;  // the real step is finite (overlapped solve)
@@ -644,6 +649,132 @@ __device__ __noinline__ void level_solve(const IcpLevelArgs& a, const double* s_
 //     delta.allFinite() (icp.cpp:45) is a warp vote, and if it fails delta is
 //     zero for every channel and the kernel reverts the real pose
 //     (exp(0) T of the saved pose) and decides again.
+// exp_map<double> (lifted.cuh, se3.hpp:77-105) with its expensive real
+// intermediates recorded for the channels' tangent evaluation.
+CSF_DEV Pose<double> exp_map_record(const double xi[6], LevelSolveShared* ls) {
+  const double phi[3] = {xi[3], xi[4], xi[5]};
+  const double t2 = phi[0] * phi[0] + (phi[1] * phi[1] + phi[2] * phi[2]);
+  double a, b, c;
+  ls->small = re(t2) < 1e-14 ? 1 : 0;
+  if (ls->small) {
+    a = 1.0 - t2 / 6.0;
+    b = 0.5 - t2 / 24.0;
+    c = 1.0 / 6.0 - t2 / 120.0;
+  } else {
+    const double t = sqrt_s(t2);
+    const double s1 = sin_s(t);
+    a = s1 / t;
+    const double th = t / 2.0;
+    const double sh = sin_s(th);
+    b = 2.0 * sh * sh / t2;
+    c = (t - s1) / (t2 * t);
+    ls->et = t;
+    ls->es1 = s1;
+    ls->eth = th;
+    ls->esh = sh;
+  }
+  ls->ea = a;
+  ls->eb = b;
+  ls->ec = c;
+  M3<double> px;
+  px.m[0] = 0.0;     px.m[1] = -phi[2]; px.m[2] = phi[1];
+  px.m[3] = phi[2];  px.m[4] = 0.0;     px.m[5] = -phi[0];
+  px.m[6] = -phi[1]; px.m[7] = phi[0];  px.m[8] = 0.0;
+  const M3<double> px2 = matmul(px, px);
+  Pose<double> out;
+  M3<double> v;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    const double id = (e == 0 || e == 4 || e == 8) ? 1.0 : 0.0;
+    out.R.m[e] = (id + a * px.m[e]) + b * px2.m[e];
+    v.m[e] = (id + b * px.m[e]) + c * px2.m[e];
+  }
+  out.t = matvec(v, mk3(xi[0], xi[1], xi[2]));
+#pragma unroll
+  for (int e = 0; e < 9; ++e) ls->ex[e] = out.R.m[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) ls->ex[9 + e] = out.t.v[e];
+  return out;
+}
+
+// One channel of exp(d) * T (increment_pose with S = L<1>) from the recorded
+// real intermediates: every operation of exp_map<L<1>> and compose applies
+// the truncated-Complex rule of lifted.cuh to (re, im) with the re parts
+// taken from the real evaluation — the same bits as the lifted evaluation,
+// without its sqrt / sin / division chains (the series branch is not
+// recorded: the caller uses increment_pose there).
+struct Tg {
+  double re, im;
+};
+CSF_DEV Tg tg_add(Tg a, Tg b) { return {a.re + b.re, a.im + b.im}; }
+CSF_DEV Tg tg_neg(Tg a) { return {-a.re, -a.im}; }
+CSF_DEV Tg tg_mul(Tg a, Tg b) { return {a.re * b.re, a.re * b.im + a.im * b.re}; }
+// a / b with the quotient's real part supplied
+CSF_DEV Tg tg_div(Tg a, Tg b, double q) {
+  const double den = b.re * b.re;
+  const double inv = 1.0 / den;
+  (void)inv;
+  return {q, CSF_CH_DIV(a.im * b.re - a.re * b.im, den, inv)};
+}
+CSF_DEV Tg tg_sum3(Tg a0, Tg a1, Tg a2) { return tg_add(a0, tg_add(a1, a2)); }
+
+CSF_DEV void increment_pose_tangent(const double xr[6], const double xim[6], const LevelSolveShared* ls,
+                                    const double cur_im[12], double out_im[12]) {
+  Tg xi[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) xi[i] = {xr[i], xim[i]};
+  const Tg phi[3] = {xi[3], xi[4], xi[5]};
+  const Tg t2 = tg_sum3(tg_mul(phi[0], phi[0]), tg_mul(phi[1], phi[1]), tg_mul(phi[2], phi[2]));
+  // t = sqrt_s(t2): lift(z, f, 0.5 / f)
+  const double tr = ls->et;
+  const Tg t = {tr, (0.5 / tr) * t2.im};
+  // sin_s(t): lift(z, sin, cos)
+  const Tg s1 = {ls->es1, csf_det::cos(tr) * t.im};
+  const Tg a = tg_div(s1, t, ls->ea);
+  const Tg two = {2.0, 0.0};
+  const Tg th = tg_div(t, two, ls->eth);
+  const Tg sh = {ls->esh, csf_det::cos(th.re) * th.im};
+  const Tg q2 = tg_mul(tg_mul(two, sh), sh);
+  const Tg b = tg_div(q2, t2, ls->eb);
+  const Tg n = {tr - ls->es1, t.im - s1.im};
+  const Tg c = tg_div(n, tg_mul(t2, t), ls->ec);
+  const Tg z = {0.0, 0.0};
+  Tg px[9];
+  px[0] = z;              px[1] = tg_neg(phi[2]); px[2] = phi[1];
+  px[3] = phi[2];         px[4] = z;              px[5] = tg_neg(phi[0]);
+  px[6] = tg_neg(phi[1]); px[7] = phi[0];         px[8] = z;
+  Tg px2[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+      px2[3 * r + cc] = tg_sum3(tg_mul(px[3 * r], px[cc]), tg_mul(px[3 * r + 1], px[3 + cc]),
+                                tg_mul(px[3 * r + 2], px[6 + cc]));
+  Tg R[9], v[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    const Tg id = {(e == 0 || e == 4 || e == 8) ? 1.0 : 0.0, 0.0};
+    R[e] = tg_add(tg_add(id, tg_mul(a, px[e])), tg_mul(b, px2[e]));
+    v[e] = tg_add(tg_add(id, tg_mul(b, px[e])), tg_mul(c, px2[e]));
+  }
+  Tg tv[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) tv[r] = tg_sum3(tg_mul(v[3 * r], xi[0]), tg_mul(v[3 * r + 1], xi[1]), tg_mul(v[3 * r + 2], xi[2]));
+  // compose(exp, cur): R = R_ex R_cur, t = R_ex t_cur + t_ex
+  Tg cr[12];
+#pragma unroll
+  for (int e = 0; e < 12; ++e) cr[e] = {ls->prev[e], cur_im[e]};
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+      out_im[3 * r + cc] =
+          tg_sum3(tg_mul(R[3 * r], cr[cc]), tg_mul(R[3 * r + 1], cr[3 + cc]), tg_mul(R[3 * r + 2], cr[6 + cc])).im;
+    out_im[9 + r] =
+        tg_add(tg_sum3(tg_mul(R[3 * r], cr[9]), tg_mul(R[3 * r + 1], cr[10]), tg_mul(R[3 * r + 2], cr[11])), tv[r]).im;
+  }
+}
+
 __device__ __noinline__ void real_step(const IcpLevelArgs& a, const double* s_tot, double* s_pose,
                                        LevelSolveShared* ls, bool revert, unsigned seq, int it) {
   const int C = 1 + a.Dp;
@@ -672,7 +803,7 @@ __device__ __noinline__ void real_step(const IcpLevelArgs& a, const double* s_to
 #pragma unroll
   for (int e = 0; e < 3; ++e) cur.t.v[e] = ls->prev[9 + e];
   lv_mark(seq, it, 11);
-  const Pose<double> ex = exp_map<double>(x);
+  const Pose<double> ex = exp_map_record(x, ls);
   lv_mark(seq, it, 12);
   const Pose<double> np = compose(ex, cur);  // apply_increment (se3.hpp:116-119)
 #pragma unroll
@@ -723,24 +854,41 @@ __device__ __noinline__ void channel_step(const IcpLevelArgs& a, const double* s
     }
   }
   const bool all_fin = __all_sync(0xffffffffu, !mine || fin);
+  // real_step's intermediates (named barrier 2: warp 0 arrives after it)
+  asm volatile("bar.sync 2, 64;" ::: "memory");
   if (!mine) return;
-  if (!all_fin)
+  double cur_im[12], out_im[12];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) d[i] = lit<L<1>>(0.0);
-  Pose<L<1>> cur, np;
+  for (int e = 0; e < 12; ++e) cur_im[e] = s_pose[e * C + ch];
+  if (all_fin && !ls->small) {
+    double xr[6], xim[6];
 #pragma unroll
-  for (int e = 0; e < 12; ++e) {
-    L<1> v;
-    v.re = ls->prev[e];
-    v.im[0] = s_pose[e * C + ch];
-    if (e < 9) cur.R.m[e] = v;
-    else cur.t.v[e - 9] = v;
+    for (int i = 0; i < 6; ++i) {
+      xr[i] = d[i].re;
+      xim[i] = d[i].im[0];
+    }
+    increment_pose_tangent(xr, xim, ls, cur_im, out_im);
+  } else {
+    if (!all_fin)
+#pragma unroll
+      for (int i = 0; i < 6; ++i) d[i] = lit<L<1>>(0.0);
+    Pose<L<1>> cur, np;
+#pragma unroll
+    for (int e = 0; e < 12; ++e) {
+      L<1> v;
+      v.re = ls->prev[e];
+      v.im[0] = cur_im[e];
+      if (e < 9) cur.R.m[e] = v;
+      else cur.t.v[e - 9] = v;
+    }
+    increment_pose(d, cur, &np);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) out_im[e] = np.R.m[e].im[0];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) out_im[9 + e] = np.t.v[e].im[0];
   }
-  increment_pose(d, cur, &np);
 #pragma unroll
-  for (int e = 0; e < 9; ++e) s_pose[e * C + ch] = np.R.m[e].im[0];
-#pragma unroll
-  for (int e = 0; e < 3; ++e) s_pose[(9 + e) * C + ch] = np.t.v[e].im[0];
+  for (int e = 0; e < 12; ++e) s_pose[e * C + ch] = out_im[e];
   if (lane == 0 && !all_fin) ls->finite = 0;
 }
 
@@ -749,9 +897,9 @@ __device__ __noinline__ void channel_step(const IcpLevelArgs& a, const double* s
 // iterations x 16 phases); off (nullptr) by default.
 __device__ unsigned long long* g_lv_clock = nullptr;
 __device__ unsigned g_lv_seq = 0;
-__device__ __forceinline__ void lv_mark(unsigned seq, int it, int phase) {
+__device__ __forceinline__ void lv_mark(unsigned seq, int it, int phase, int by) {
   unsigned long long* b = g_lv_clock;
-  if (b && threadIdx.x == 0 && it < 32) {
+  if (b && threadIdx.x == by && it < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     b[((static_cast<unsigned long long>(seq & 63) * 256 + blockIdx.x) * 32 + it) * 16 + phase] = t;
@@ -952,13 +1100,16 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
     if (overlap && !ls.degen) {
       if (warp == kAsWarps) {
         channel_step(a, s_tot, s_pose, &ls);
+        lv_mark(seq, it, 14, 32 * kAsWarps);
       } else {
         if (tid == 0) real_step(a, s_tot, s_pose, &ls, false, seq, it);
+        if (warp == 0) asm volatile("bar.arrive 2, 64;" ::: "memory");  // the channel warp may read ls
         assoc_barrier();
         lv_mark(seq, it, 8);
         if (!ls.done && it + 1 < a.iterations) {
           const int na = level_associate(a, t0, t1, s_pose, s_intr, w2p, s_meas, s_rec, s_m, s_wsum);
           if (tid == 0) s_na = na;
+          lv_mark(seq, it, 15);
         }
       }
       __syncthreads();

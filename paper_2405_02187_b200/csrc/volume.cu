@@ -1770,8 +1770,14 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
     // the small levels, where the longest ray sets the kernel time.
     int S = 1;
     if constexpr (V::kHashed) {
-      constexpr int kSegMax = 16;
-      constexpr long long kTargetThreads = 320000;
+#ifndef CSF_SEG_MAX
+#define CSF_SEG_MAX 16
+#endif
+#ifndef CSF_SEG_TARGET
+#define CSF_SEG_TARGET 320000
+#endif
+      constexpr int kSegMax = CSF_SEG_MAX;
+      constexpr long long kTargetThreads = CSF_SEG_TARGET;
       while (S < kSegMax && static_cast<long long>(P) * S * 2 <= kTargetThreads) S *= 2;
       if (!atab || !seg_first) S = 1;
     }

@@ -50,7 +50,9 @@ for L in range(64):
                     f"{(bar.max() - s) / 1e3:5.1f}, solve {np.median(sol - bar) / 1e3:5.1f} us [ldlt "
                     f"{np.median(b[L, used, it, 8] - bar) / 1e3:4.1f} channels {np.median(b[L, used, it, 9] - b[L, used, it, 8]) / 1e3:4.1f}"
                     f" exp {np.median(b[L, used, it, 10] - b[L, used, it, 9]) / 1e3:4.1f} tail {np.median(sol - b[L, used, it, 10]) / 1e3:4.1f}]"
-                    f" (totals+ldlt {np.median(b[L, used, it, 13] - bar) / 1e3:4.1f} apply {np.median(b[L, used, it, 11] - b[L, used, it, 13]) / 1e3:4.1f} expmap {np.median(b[L, used, it, 12] - b[L, used, it, 11]) / 1e3:4.1f})")
+                    f" (chan-warp {np.median(b[L, used, it, 14] - b[L, used, it, 13]) / 1e3:4.1f} (max {(b[L, used, it, 14] - b[L, used, it, 13]).max() / 1e3:4.1f})"
+                    f" assoc-end {np.median(b[L, used, it, 15] - b[L, used, it, 8]) / 1e3:4.1f} (max {(b[L, used, it, 15] - b[L, used, it, 8]).max() / 1e3:4.1f})"
+                    f" totals+ldlt {np.median(b[L, used, it, 13] - bar) / 1e3:4.1f} apply {np.median(b[L, used, it, 11] - b[L, used, it, 13]) / 1e3:4.1f} expmap {np.median(b[L, used, it, 12] - b[L, used, it, 11]) / 1e3:4.1f})")
         rc = np.argmax(b[L, :, it, 3])
         rows.append(f"      releasing CTA {rc}: partial {(b[L, rc, it, 2] - s) / 1e3:5.1f} group-sum-done "
                     f"{(b[L, rc, it, 6] - s) / 1e3:5.1f} last-decided {(b[L, rc, it, 7] - s) / 1e3:5.1f} release "
