@@ -44,6 +44,11 @@ scene — 8 queries, eta-switched Newton; relocalizations/s (bench_reloc.py).
 --workload surfel: the surfel (X-EF) front end — 100 VGA
 frames fused at poses lifted on 6 twist directions (bench_surfel.py).
 
+--workload config1: BASELINE config 1 — the toy room (3 spheres, seed 0), 10
+frames at 160x120 (fx = fy = 120), dense 128^3 TSDF at 2 cm (mu 6 cm),
+3-level ICP 10/5/4, h = 1e-20, gradient of the final translation error
+w.r.t. the 6 first-frame twist parameters.  Units = frames x 6 directions.
+
 --workload config3: BASELINE config 3 — the same VGA scene, 30 frames, the
 full 10x10 Hessian as 55 second-order parameter pairs (one reference
 Bicomplex per pair, packed as channel slots of one evaluation).  Units =
@@ -74,6 +79,7 @@ METRIC = "CSFD SLAM frame-derivatives/sec at 640×480 (frames×directions/s), 1/
 UNIT = "frame-derivatives/s"
 DIRS = list(range(10))  # 6 first-frame twist components (rho, phi) + fx, fy, cx, cy
 PAIRS = [(i, j) for i in range(10) for j in range(i, 10)]  # 55 Hessian pairs (config 3)
+DIRS1 = list(range(6))  # config 1: the 6 first-frame twist parameters
 DIRS4 = list(range(64))  # config 4: 0-5 first-frame twist, 6-9 intrinsics, 10-63 keyframes 1-9 (every 50 frames)
 
 
@@ -83,7 +89,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5", "reloc", "surfel"], default="config2")
+    ap.add_argument("--workload", choices=["config1", "config2", "config3", "config4", "config5", "reloc", "surfel"], default="config2")
     ap.add_argument("--frames", type=int, default=0, help="0 = the workload's frame count (100 / 30)")
     ap.add_argument("--cpu-frames", type=int, default=CPU_FRAMES, help="CPU-baseline sample: frames")
     ap.add_argument("--cpu-dirs", type=int, default=CPU_UNITS, help="CPU-baseline sample: directions (one pass each)")
@@ -246,6 +252,9 @@ def cpu_sample(depth, gt, k, frames, units, workload, packed=False):
         elif workload == "config4":
             cfg = pipeline_cfg4(csf, capi, k, [DIRS4[d]], frames, icp=icp)
             secs += orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
+        elif workload == "config1":
+            cfg = pipeline_cfg1(csf, capi, k, [DIRS1[d]], frames, icp=icp)
+            secs += orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
         else:
             cfg = pipeline_cfg(csf, capi, k, [DIRS[d]], frames, icp=icp)
             secs += orc.pipeline_run(cfg, depth[:frames], gt[:frames])[-1]
@@ -342,7 +351,7 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
         return
     frames, units = CPU_FRAMES, CPU_UNITS
-    depth, gt, k = orc.workload(4 if args.workload == "config4" else 2, frames)
+    depth, gt, k = orc.workload({"config4": 4, "config1": 1}.get(args.workload, 2), frames)
     second = args.workload == "config3"
     for _ in range(args.warmup):
         cpu_sample(depth, gt, k, frames, units, args.workload)
@@ -357,8 +366,9 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded procedural room, BASELINE {args.workload} shapes)",
-        "config": {"workload": f"{args.workload} VGA hashed, bounded CPU sample: first {frames} frames x {units} "
-                               f"{what}s per step", "frames": frames, "directions": units},
+        "config": {"workload": f"{args.workload} {'160x120 dense' if args.workload == 'config1' else 'VGA hashed'}, "
+                               f"bounded CPU sample: first {frames} frames x {units} {what}s per step",
+                   "frames": frames, "directions": units},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"first {frames} VGA frames x {units} {what}s per step, one oracle pass per {what} "
                                    "(oracle/ restatement; the reference needs Eigen/libpng/doctest, absent); the same "
@@ -561,8 +571,9 @@ def main():
         return
     second = args.workload == "config3"
     four = args.workload == "config4"
+    one = args.workload == "config1"
     if args.frames <= 0:
-        args.frames = 30 if second else (500 if four else 100)
+        args.frames = 30 if second else (500 if four else (10 if one else 100))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -582,8 +593,12 @@ def main():
     from paper_2405_02187_b200 import capi
     ctx = csf.Context(local)
     n = args.frames
-    depth, gt, k = csf.synth_workload(4 if four else 2, n, ctx=ctx)
-    if four:
+    depth, gt, k = csf.synth_workload(4 if four else (1 if one else 2), n, ctx=ctx)
+    if one:
+        units_all = DIRS1
+        off, mine = shard_directions(units_all, world, rank)
+        cfg = pipeline_cfg1(csf, capi, k, mine, n)
+    elif four:
         # weak scaling: every rank runs one 8-direction share of the 8-GPU job
         off, mine = shard_directions(DIRS4, 8, rank % 8)
         units_all = [d for r in range(world) for d in shard_directions(DIRS4, 8, r % 8)[1]]
@@ -705,7 +720,10 @@ def main():
                           "peak_source": peak_src, "fp64": fp64_roofline(cat, args.workload)}
     roofline = max(rooflines.values(), key=lambda r: r["share_of_step"]) if rooflines else None
 
-    if four:
+    if one:
+        workload = (f"config1: {n} frames 160x120, dense 128^3 TSDF at 2 cm (mu 6 cm), h = 1e-20, "
+                    f"{len(units_all)} first-frame twist directions")
+    elif four:
         workload = (f"config4: {n} VGA frames, 60x60 m terrain + 200 boxes, hashed 8^3 blocks 2 cm, 64 directions "
                     f"(6 first-frame + 4 intrinsics + 54 keyframe twists), 8 directions per GPU")
     elif second:
@@ -718,11 +736,14 @@ def main():
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak" if four else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": ("synthetic (seeded procedural terrain rendered on device; BASELINE config 4 shapes)" if four else
+                 "synthetic (seeded toy room rendered on device; BASELINE config 1 shapes)" if one else
                  "synthetic (seeded procedural room rendered on device; BASELINE config 2 shapes)"),
         "config": {"workload": workload, "frames": n, "directions": len(units_all),
                    "directions_per_rank": len(mine), "order": 2 if second else 1,
                    "parallelism": f"{'pairs' if second else 'directions'} sharded x{world}",
-                   "l2": "working set (hashed volume, ~GBs) >> L2"},
+                   "l2": ("working set: dense 128^3 x (16 + 6x8) B = 134 MB volume + maps > L2 (126 MB), "
+                          "no flush" if one else
+                          "working set (hashed volume, ~GBs) >> L2")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "launch_mode": {"used": "cuda_graph" if use_graph else "stream", "stream_ms_per_step": ms_stream / args.steps,
