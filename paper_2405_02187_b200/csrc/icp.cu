@@ -1354,9 +1354,14 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
   const int C = 1 + Dp;
   const int g0 = blockIdx.y * G;
   extern __shared__ double sm[];
-  S* rows = reinterpret_cast<S*>(sm);                 // [kR2Threads][7]
-  double* streams = sm + sizeof(S) / 8 * kR2Threads * 7;  // [NA][33]: the canonical 32 streams
+  S* rows = reinterpret_cast<S*>(sm);  // [kR2Threads][7]
   __shared__ int s_wsum[kR2Warps];
+  // the canonical order (§3.3): lane l of every warp is stream l; warp w owns
+  // the accumulators q = w, w + 8, w + 16, w + 24 (< 27), all components of S
+  constexpr int kQ = (27 + kR2Warps - 1) / kR2Warps;
+  S acc[kQ];
+#pragma unroll
+  for (int i = 0; i < kQ; ++i) acc[i] = lit<S>(0.0);
   Pose<double> c2w, w2p;
   load_pose_real(pose, C, &c2w);
 #pragma unroll
@@ -1368,7 +1373,6 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
   const int n_slots = nxs * nys;
   const int t0 = blockIdx.x * tile_slots, t1 = min(n_slots, t0 + tile_slots);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < NA * 33; i += blockDim.x) streams[i] = 0.0;
   int ebase = 0;
   for (int c0 = t0; c0 < t1; c0 += kR2Threads) {
     const int slot = c0 + threadIdx.x;
@@ -1424,37 +1428,40 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
       row[6] = r;
     }
     __syncthreads();
-    // accumulate_row (orc_icp.hpp): one thread per (accumulator, slot) adds
-    // the S product of the two row entries into the correspondence's stream
-    // (global entry index mod 32), streams in entry order
-    const int acc = threadIdx.x;
-    if (acc < NA) {
-      const int q = acc / CG, c = acc % CG;
-      const int ja = acc_row_a(q), jb = acc_row_b(q);
-      double* str = streams + acc * 33;
-      for (int e = 0; e < total; ++e) {
-        const S prod = rows[7 * e + ja] * rows[7 * e + jb];
-        const int k = (ebase + e) & 31;
-        str[k] = str[k] + (c == 0 ? prod.re : prod.im[c - 1]);
+    // accumulate_row (orc_icp.hpp): lane l adds, in entry order, the S
+    // product of the two row entries of every correspondence whose global
+    // entry index is l mod 32
+    const int first = (lane - (ebase & 31) + 32) & 31;
+    for (int e = first; e < total; e += 32) {
+#pragma unroll
+      for (int i = 0; i < kQ; ++i) {
+        const int q = warp + kR2Warps * i;
+        if (q < 27) acc[i] = acc[i] + rows[7 * e + acc_row_a(q)] * rows[7 * e + acc_row_b(q)];
       }
     }
     ebase += total;
   }
   if (threadIdx.x == 0 && blockIdx.y == 0) counts[blockIdx.x] = ebase;
-  const int acc = threadIdx.x;
-  if (acc < NA) {
-    // the fixed butterfly of the first-order kernel, lane 0's value
-    double* str = streams + acc * 33;
+  // the fixed butterfly of the first-order kernel, lane 0's value
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-      for (int l = 0; l < off; ++l) str[l] = str[l] + str[l + off];
-    const int q = acc / CG, c = acc % CG;
-    if (c == 0) {
-      if (blockIdx.y == 0) partials[static_cast<long long>(blockIdx.x) * 27 * C + q * C] = str[0];
-    } else {
-      partials[static_cast<long long>(blockIdx.x) * 27 * C + q * C + g0 + c] = str[0];
+  for (int i = 0; i < kQ; ++i) {
+    const int q = warp + kR2Warps * i;
+    double v[CG];
+    v[0] = acc[i].re;
+#pragma unroll
+    for (int g = 0; g < G; ++g) v[1 + g] = acc[i].im[g];
+#pragma unroll
+    for (int c = 0; c < CG; ++c)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v[c] = v[c] + __shfl_xor_sync(0xffffffffu, v[c], off);
+    if (lane == 0 && q < 27) {
+      double* dst = partials + static_cast<long long>(blockIdx.x) * 27 * C + q * C;
+      if (blockIdx.y == 0) dst[0] = v[0];
+#pragma unroll
+      for (int g = 0; g < G; ++g) dst[g0 + 1 + g] = v[1 + g];
     }
   }
+  (void)NA;
 }
 
 // stage: [0..11] new real pose, [12] |delta.re|, [13] correspondence count,
@@ -1803,7 +1810,7 @@ void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double
   using S = B<1>;
   const int tiles = icp_tiles(w, h, stride);
   const int pairs = Dp / 3;
-  const size_t smem = sizeof(S) * kR2Threads * 7 + sizeof(double) * 27 * (1 + Traits<S>::G) * 33;
+  const size_t smem = sizeof(S) * kR2Threads * 7;
   const long long n_slots = static_cast<long long>((w + stride - 1) / stride) * ((h + stride - 1) / stride);
   const int tile_slots = icp_tile_slots(n_slots);
   launch_pdl(k_icp_reduce2<S>, dim3(tiles, pairs), dim3(kR2Threads), smem, L.stream, st, depth, w, h, stride, intr,

@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     if constexpr (kAdj)
       fused += fuse_voxel_adjoint<NDP>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
     else
-      count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm, dch));
+      count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm,
+                                       LD ? dch : nullptr));
   }
   flush_updates(upd, fused);
 }
@@ -379,7 +380,8 @@ __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView
       if constexpr (kAdj)
         fused += fuse_voxel_adjoint<NDP>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
       else
-        count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm, dch));
+        count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm,
+                                         LD ? dch : nullptr));
     }
   }
   flush_updates(upd, fused);
@@ -630,6 +632,20 @@ __global__ void k_alloc_finalize(int* n_blocks, int max_blocks, const int* first
 //     the two samples at the recorded alphas (bit-identical real parts), the
 //     interpolated vertex and the gradient normal in L<G>.
 // ----------------------------------------------------------------------------
+// Pixel order of the raycast kernels: 8x4-pixel warp tiles in row-major
+// tile order (lin = 32 * tile + lane).  The rays of a warp are a compact
+// patch, so their march trip counts and their lift gathers (shared voxels)
+// are more alike than along a 32-pixel row.  lin < tiled_count(w, h).
+CSF_HD long long tiled_count(int w, int h) { return 32LL * ((w + 7) / 8) * ((h + 3) / 4); }
+CSF_DEV bool tile_pixel(long long lin, int w, int h, int* x, int* y) {
+  const int tiles_x = (w + 7) >> 3;
+  const long long t = lin >> 5;
+  const int l = static_cast<int>(lin & 31);
+  *x = 8 * static_cast<int>(t % tiles_x) + (l & 7);
+  *y = 4 * static_cast<int>(t / tiles_x) + (l >> 3);
+  return *x < w && *y < h;
+}
+
 struct Box {
   bool use;
   double lo[3], hi[3];
@@ -714,9 +730,9 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
   if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
   else if (threadIdx.x < 16) s_pose[threadIdx.x] = intr[(threadIdx.x - 12) * C];
   __syncthreads();
-  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pix >= w * h) return;
-  const int x = pix % w, y = pix / w;
+  int x, y;
+  if (!tile_pixel(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, w, h, &x, &y)) return;
+  const int pix = y * w + x;
   Pose<double> c2w;
 #pragma unroll
   for (int e = 0; e < 9; ++e) c2w.R.m[e] = s_pose[e];
@@ -931,12 +947,15 @@ __global__ void __launch_bounds__(128) k_raycast_march_seg(HashView vol, const d
   if (threadIdx.x < 12) s_pose[threadIdx.x] = pose[threadIdx.x * C];
   else if (threadIdx.x < 16) s_pose[threadIdx.x] = intr[(threadIdx.x - 12) * C];
   __syncthreads();
-  const int P = w * h;
+  const long long T = tiled_count(w, h);
   const long long item = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (item >= static_cast<long long>(P) * S) return;
-  const int seg = static_cast<int>(item / P), pix = static_cast<int>(item % P);
+  if (item >= T * S) return;
+  const int seg = static_cast<int>(item / T);
+  int px_, py_;
+  if (!tile_pixel(item % T, w, h, &px_, &py_)) return;
+  const int pix = py_ * w + px_;
   V3<double> o, dir;
-  ray_of(s_pose, pix % w, pix / w, &o, &dir);
+  ray_of(s_pose, px_, py_, &o, &dir);
   V3<double> invd;
 #pragma unroll
   for (int a = 0; a < 3; ++a) invd.v[a] = dir.v[a] != 0.0 ? 1.0 / dir.v[a] : 0.0;
@@ -1128,6 +1147,20 @@ constexpr int kLiftPix = 32;  // max pixels per block (8 lanes each in the real 
 // pixels per block: as many as keep the channel pass to one round of items
 // (items = channel-pass items per pixel)
 inline int lift_pixels(int items) { return items <= 8 ? kLiftPix : (items >= 256 ? 1 : 256 / items); }
+// Pixel p of a lift CTA: one 8x4 warp tile (tile_pixel) when the CTA takes
+// 32 pixels, else npix consecutive pixels.  -1: outside the image.
+CSF_DEV int lift_pixel(int npix, int p, int w, int h) {
+  if (npix == kLiftPix) {
+    int x, y;
+    return tile_pixel(static_cast<long long>(blockIdx.x) * kLiftPix + p, w, h, &x, &y) ? y * w + x : -1;
+  }
+  const long long pix = static_cast<long long>(blockIdx.x) * npix + p;
+  return pix < static_cast<long long>(w) * h ? static_cast<int>(pix) : -1;
+}
+inline unsigned lift_grid(int npix, int w, int h) {
+  return static_cast<unsigned>(npix == kLiftPix ? tiled_count(w, h) / kLiftPix
+                                                : (static_cast<long long>(w) * h + npix - 1) / npix);
+}
 
 #ifndef CSF_LIFT_MINB
 #define CSF_LIFT_MINB 2
@@ -1152,12 +1185,12 @@ __global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol,
   // ---- real pass: lane s of pixel p
   {
     const int p = threadIdx.x >> 3, s = threadIdx.x & 7;
-    const int pix = blockIdx.x * npix + p;
+    const int pix = p < npix ? lift_pixel(npix, p, w, h) : -1;
     LiftRec& r = recs[p < npix ? p : 0];
     double2 hit = make_double2(0.0, -1.0);
-    if (p < npix && pix < P) hit = hits[pix];
+    if (pix >= 0) hit = hits[pix];
     const bool active = hit.y >= 0.0;
-    const int x = pix % w, y = pix / w;
+    const int x = pix >= 0 ? pix % w : 0, y = pix >= 0 ? pix / w : 0;
     double R[9], T[3];
 #pragma unroll
     for (int e = 0; e < 9; ++e) R[e] = sm[e * C];
@@ -1252,8 +1285,8 @@ __global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol,
   for (int it = threadIdx.x; it < npix * Dh; it += blockDim.x) {
     const int p = it / Dh, d = (it - p * Dh) * CH;
     const LiftRec& r = recs[p];
-    const int pix = blockIdx.x * npix + p;
-    if (pix >= P) continue;
+    const int pix = lift_pixel(npix, p, w, h);
+    if (pix < 0) continue;
     if (!r.ok) {  // no surface: zero channels (no separate memset of the maps)
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -1784,7 +1817,7 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
     if (S > 1) {
       if constexpr (V::kHashed) {
         cudaMemsetAsync(seg_first, 0xFF, sizeof(unsigned) * P, L.stream);
-        const long long items = static_cast<long long>(P) * S;
+        const long long items = tiled_count(w, h) * S;
         launch_pdl(k_raycast_march_seg, dim3(static_cast<unsigned>((items + 127) / 128)), dim3(128), 0, L.stream, view,
                    pose, intr, w, h, Dp, S, atab, n_tab, step, seg_first);
         launch_pdl(k_raycast_march_fin, dim3((P + 127) / 128), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp, atab,
@@ -1792,7 +1825,8 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
         *L.launches += 1;
       }
     } else {
-      launch_pdl(k_raycast_march<V>, dim3((P + 127) / 128), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp,
+      const unsigned march_grid = static_cast<unsigned>((tiled_count(w, h) + 127) / 128);
+      launch_pdl(k_raycast_march<V>, dim3(march_grid), dim3(128), 0, L.stream, view, pose, intr, w, h, Dp,
                  near_clip, far_clip, step, box, hits, vre, nre, atab, n_tab);
     }
     if (Dp > 0 && vim && order == 2) {  // the first-order lift writes every pixel
@@ -1821,10 +1855,10 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
   const int npix = lift_pixels(pair ? Dp / 2 : Dp);
   const size_t smem_c = smem + sizeof(LiftRec) * npix;
   if (pair)
-    launch_pdl(k_raycast_lift_coop<V, 2>, dim3((P + npix - 1) / npix), dim3(8 * kLiftPix), smem_c, L.stream, view,
+    launch_pdl(k_raycast_lift_coop<V, 2>, dim3(lift_grid(npix, w, h)), dim3(8 * kLiftPix), smem_c, L.stream, view,
                pose, intr, w, h, Dp, hits, vre, nre, vim, nim, npix);
   else
-    launch_pdl(k_raycast_lift_coop<V, 1>, dim3((P + npix - 1) / npix), dim3(8 * kLiftPix), smem_c, L.stream, view,
+    launch_pdl(k_raycast_lift_coop<V, 1>, dim3(lift_grid(npix, w, h)), dim3(8 * kLiftPix), smem_c, L.stream, view,
                pose, intr, w, h, Dp, hits, vre, nre, vim, nim, npix);
   *L.launches += 1;
 }
