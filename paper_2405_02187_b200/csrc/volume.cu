@@ -1187,8 +1187,12 @@ __global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol,
     const int p = threadIdx.x >> 3, s = threadIdx.x & 7;
     const int pix = p < npix ? lift_pixel(npix, p, w, h) : -1;
     LiftRec& r = recs[p < npix ? p : 0];
-    double2 hit = make_double2(0.0, -1.0);
-    if (pix >= 0) hit = hits[pix];
+    // the crossing alphas and the march's two samples, loaded together
+    double2 hit = make_double2(0.0, -1.0), fpair = make_double2(0.0, 0.0);
+    if (pix >= 0) {
+      hit = hits[pix];
+      fpair = hits[P + pix];
+    }
     const bool active = hit.y >= 0.0;
     const int x = pix >= 0 ? pix % w : 0, y = pix >= 0 ? pix / w : 0;
     double R[9], T[3];
@@ -1206,8 +1210,7 @@ __global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol,
     for (int q = 0; q < 3; ++q) dir[q] = R[3 * q] * dn[0] + (R[3 * q + 1] * dn[1] + R[3 * q + 2] * dn[2]);
     const double a0 = hit.x, a1 = hit.y;
     // f0, f1: the march's samples at a0, a1 (same arithmetic as sample_real_ex)
-    const double2 fpair = active ? hits[P + pix] : make_double2(0.0, 0.0);
-    const double f0 = fpair.x, f1 = fpair.y;
+    const double f0 = active ? fpair.x : 0.0, f1 = active ? fpair.y : 0.0;
     const double span = a1 - a0;
     const double num = span * f0, den = f1 - f0;
     const double astar = a0 - num / den;
