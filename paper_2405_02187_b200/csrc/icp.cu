@@ -44,8 +44,9 @@ using csfi::IcpLevelArgs;
 //      term re(J_a) im(J_b) + im(J_a) re(J_b) (csfd.hpp:50-53);
 //   C  reduces the 32 streams with a fixed xor butterfly and writes its tile
 //      partial; the last CTA of each group of kLvGroup tiles sums the group
-//      in tile order, the last group sums the groups in order and releases
-//      the grid barrier;
+//      in tile order and releases the group's generation flag; every CTA
+//      waits for all group flags (the grid barrier) and sums the group
+//      totals in group order itself;
 //   D  every CTA solves the same 6x6 system redundantly from the totals (the
 //      real LDLT in the oracle's Ldlt6 order, channels in tangent form
 //      against the real factors), applies exp(delta) T per channel and takes
@@ -68,9 +69,10 @@ constexpr int kLvMaxTiles = csfi::kIcpMaxTiles;
 constexpr int kLvGroup = csfi::kIcpGroup;
 constexpr int kLvMaxGroups = (kLvMaxTiles + kLvGroup - 1) / kLvGroup;
 constexpr int kMaxC = 1 + 64;  // CSF_MAX_DIRECTIONS
-// Barrier words: group counters and the total counter share one line; the
-// release generation that every CTA polls sits 256 bytes away, so the polls
-// never queue in front of the counters' atomics in the same L2 line.
+// Barrier words: the group arrival counters share one line; the groups'
+// release generations (one word per group, what every CTA polls) sit 256
+// bytes away, so the polls never queue in front of the counters' atomics in
+// the same L2 line.
 constexpr int kFlagWord = 64;
 
 // shared-memory record fields of one correspondence (structure of arrays)
@@ -367,8 +369,8 @@ CSF_DEV void level_accumulate(const IcpLevelArgs& a, int c, int ebase, int e0, i
   }
 }
 
-// Grid barrier of the level kernel: the CTA that completes the last group
-// publishes generation `gen`; everyone waits for it.
+// Grid barrier of the level kernel: the CTA that completes a group publishes
+// generation `gen` on the group's flag; everyone waits for every group.
 CSF_DEV void release_gen(unsigned* flag, unsigned gen) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(gen) : "memory");
 }
@@ -1043,22 +1045,14 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_icp_level(IcpLevelArgs a) {
       }
       __syncthreads();
       lv_mark(seq, it, 6);
-      if (tid == 0) s_last = atom_add_acq_rel(a.sync + kLvMaxGroups, 1u) == static_cast<unsigned>(n_groups - 1);
-      __syncthreads();
-      if (s_last) {
-        // every group total is published: release the grid (each CTA sums
-        // the group totals itself, in group order)
-        lv_mark(seq, it, 7);
-        if (tid == 0) {
-          a.sync[kLvMaxGroups] = 0u;
-          release_gen(a.sync + kFlagWord, gen + it + 1);
-        }
-        lv_mark(seq, it, 3);
-      }
+      // publish this group's total: its own generation flag
+      if (tid == 0) release_gen(a.sync + kFlagWord + grp, gen + it + 1);
+      lv_mark(seq, it, 3);
     }
-    // ---- grid barrier
-    if (tid == 0) {
-      while (static_cast<int>(poll_gen(a.sync + kFlagWord) - (gen + it + 1)) < 0) __nanosleep(32);
+    // ---- grid barrier: thread g waits for group g's flag (every CTA then
+    // sums the group totals itself, in group order)
+    if (tid < n_groups) {
+      while (static_cast<int>(poll_gen(a.sync + kFlagWord + tid) - (gen + it + 1)) < 0) __nanosleep(32);
       fence_acquire();
     }
     __syncthreads();
