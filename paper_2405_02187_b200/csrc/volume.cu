@@ -489,27 +489,33 @@ __global__ void k_touch(const unsigned long long* __restrict__ cand, int n, unsi
                         int* set_first, int* set_slot, int bits, int* err, int* counters) {
   pdl_wait();
   pdl_trigger();
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const unsigned long long key = cand[s];
-  if (key == kEmptyKey) {
-    set_slot[s] = -1;
-    return;
-  }
-  const unsigned mask = (1u << bits) - 1u;
-  unsigned hsh = set_hash(key, bits);
-  for (unsigned probe = 0; probe <= mask; ++probe) {
-    const unsigned long long prev = atomicCAS(set_keys + hsh, kEmptyKey, key);
-    if (prev == kEmptyKey || prev == key) {
-      atomicMin(set_first + hsh, s);
-      set_slot[s] = static_cast<int>(hsh);
-      return;
+  // grid-stride (a few waves of resident CTAs instead of one CTA per 256
+  // slots: the kernel is CTA-launch-bound otherwise)
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const unsigned long long key = cand[s];
+    if (key == kEmptyKey) {
+      set_slot[s] = -1;
+      continue;
     }
-    hsh = (hsh + 1u) & mask;
+    const unsigned mask = (1u << bits) - 1u;
+    unsigned hsh = set_hash(key, bits);
+    bool placed = false;
+    for (unsigned probe = 0; probe <= mask; ++probe) {
+      const unsigned long long prev = atomicCAS(set_keys + hsh, kEmptyKey, key);
+      if (prev == kEmptyKey || prev == key) {
+        atomicMin(set_first + hsh, s);
+        set_slot[s] = static_cast<int>(hsh);
+        placed = true;
+        break;
+      }
+      hsh = (hsh + 1u) & mask;
+    }
+    if (!placed) {
+      set_slot[s] = -1;
+      atomicExch(counters + 2, 1);
+      raise(err, kErrNoMem);
+    }
   }
-  set_slot[s] = -1;
-  atomicExch(counters + 2, 1);
-  raise(err, kErrNoMem);
 }
 
 __global__ void k_flags(HashView vol, const unsigned long long* __restrict__ cand, int n,
@@ -517,22 +523,22 @@ __global__ void k_flags(HashView vol, const unsigned long long* __restrict__ can
                         int* new_flag, int* cand_block) {
   pdl_wait();
   pdl_trigger();
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const int hs = set_slot[s];
-  const bool first = hs >= 0 && set_first[hs] == s;
-  int nf = 0;
-  if (first) {
-    const unsigned long long key = cand[s];
-    const int bx = static_cast<int>((key >> 42) & 0x1FFFFF) - kCoordBias;
-    const int by = static_cast<int>((key >> 21) & 0x1FFFFF) - kCoordBias;
-    const int bz = static_cast<int>(key & 0x1FFFFF) - kCoordBias;
-    const int id = vol.find(bx, by, bz);
-    cand_block[s] = id;
-    nf = id < 0;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const int hs = set_slot[s];
+    const bool first = hs >= 0 && set_first[hs] == s;
+    int nf = 0;
+    if (first) {
+      const unsigned long long key = cand[s];
+      const int bx = static_cast<int>((key >> 42) & 0x1FFFFF) - kCoordBias;
+      const int by = static_cast<int>((key >> 21) & 0x1FFFFF) - kCoordBias;
+      const int bz = static_cast<int>(key & 0x1FFFFF) - kCoordBias;
+      const int id = vol.find(bx, by, bz);
+      cand_block[s] = id;
+      nf = id < 0;
+    }
+    first_flag[s] = first;
+    new_flag[s] = nf;
   }
-  first_flag[s] = first;
-  new_flag[s] = nf;
 }
 
 // Lock-free insertion into a chain kept sorted by key: the resulting chains
@@ -565,6 +571,11 @@ CSF_DEV void occ_mark(unsigned* occ, int gbits, unsigned ux, unsigned uy, unsign
   atomicOr(occ2 + (b2 >> 5), 1u << (b2 & 31));
 }
 
+CSF_DEV void insert_slot(HashView vol, int* heads, unsigned long long* keys, int* next, int* coords,
+                         const int* n_blocks, int max_blocks, const unsigned long long* __restrict__ cand,
+                         const int* __restrict__ first_flag, const int* __restrict__ new_flag,
+                         const int* __restrict__ first_rank, const int* __restrict__ new_rank,
+                         const int* __restrict__ cand_block, int* visible, int* err, int s);
 __global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int* next, int* coords, const int* n_blocks,
                          int max_blocks, const unsigned long long* __restrict__ cand, int n,
                          const int* __restrict__ first_flag, const int* __restrict__ new_flag,
@@ -572,8 +583,17 @@ __global__ void k_insert(HashView vol, int* heads, unsigned long long* keys, int
                          const int* __restrict__ cand_block, int* visible, int* err) {
   pdl_wait();
   pdl_trigger();
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n || !first_flag[s]) return;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x)
+    insert_slot(vol, heads, keys, next, coords, n_blocks, max_blocks, cand, first_flag, new_flag, first_rank,
+                new_rank, cand_block, visible, err, s);
+}
+
+CSF_DEV void insert_slot(HashView vol, int* heads, unsigned long long* keys, int* next, int* coords,
+                         const int* n_blocks, int max_blocks, const unsigned long long* __restrict__ cand,
+                         const int* __restrict__ first_flag, const int* __restrict__ new_flag,
+                         const int* __restrict__ first_rank, const int* __restrict__ new_rank,
+                         const int* __restrict__ cand_block, int* visible, int* err, int s) {
+  if (!first_flag[s]) return;
   int id = cand_block[s];
   if (new_flag[s]) {
     id = *n_blocks + new_rank[s];
@@ -1773,7 +1793,7 @@ void launch_allocate(const Launch& L, const HashDev& v, int Dp, AllocScratch& a,
   cudaMemsetAsync(a.set_first, 0x7F, sizeof(int) << a.set_bits, L.stream);
   const dim3 b2(32, 8), g2((w + 31) / 32, (h + 7) / 8);
   launch_pdl(k_band, dim3(g2), dim3(b2), 0, L.stream, depth, w, h, pose, intr, C, v.mu, v.vs, v.ox, v.oy, v.oz, K, a.cand);
-  const int tb = 256, gb = (n + tb - 1) / tb;
+  const int tb = 256, gb = std::min((n + tb - 1) / tb, 8 * csfi::sm_count());  // grid-stride kernels
   launch_pdl(k_touch, dim3(gb), dim3(tb), 0, L.stream, a.cand, n, a.set_keys, a.set_first, a.set_slot, a.set_bits, L.err, a.counters);
   launch_pdl(k_flags, dim3(gb), dim3(tb), 0, L.stream, view, a.cand, n, a.set_first, a.set_slot, a.first_flag, a.new_flag, a.cand_block);
   size_t bytes = a.cub_tmp_bytes;
