@@ -161,6 +161,47 @@ struct HashView {
     *es = !((w4 >> (b4 & 31)) & 1u) ? 4 : (!((w2 >> (b2 & 31)) & 1u) ? 2 : 0);
     *blk = id;
   }
+  // probe() of the block of cell (i0, j0, k0) and the voxel ids of the cell's
+  // 8 corners (-1: unallocated), every load issued in one round trip (the
+  // march's in-band trips otherwise chain distance -> block id -> corner ids
+  // -> voxels).  sd, es, blk: as probe().
+  CSF_DEV void probe_cell(int i0, int j0, int k0, int* sd, int* es, int* blk, long long* v) const {
+    const int half = 1 << (gbits - 1);
+    const unsigned side = 1u << gbits;
+    const unsigned ux = static_cast<unsigned>((i0 >> 3) + half), uy = static_cast<unsigned>((j0 >> 3) + half),
+                   uz = static_cast<unsigned>((k0 >> 3) + half);
+    const unsigned ux1 = static_cast<unsigned>(((i0 + 1) >> 3) + half), uy1 = static_cast<unsigned>(((j0 + 1) >> 3) + half),
+                   uz1 = static_cast<unsigned>(((k0 + 1) >> 3) + half);
+    if (!(ux < side && uy < side && uz < side && ux1 < side && uy1 < side && uz1 < side)) {
+      probe(i0 >> 3, j0 >> 3, k0 >> 3, sd, es, blk);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = voxel(i0 + (c & 1), j0 + ((c >> 1) & 1), k0 + (c >> 2));
+      return;
+    }
+    const int sb = gbits - 3, s4 = gbits - 2, s2 = gbits - 1;
+    const unsigned* occ4 = occ + ((1u << (3 * sb)) >> 5);
+    const unsigned* occ2 = occ4 + ((1u << (3 * s4)) >> 5);
+    const unsigned bsb = ((uz >> 3) << sb | (uy >> 3)) << sb | (ux >> 3);
+    const unsigned b4 = ((uz >> 2) << s4 | (uy >> 2)) << s4 | (ux >> 2);
+    const unsigned b2 = ((uz >> 1) << s2 | (uy >> 1)) << s2 | (ux >> 1);
+    const int d = __ldg(sdist + bsb);
+    const unsigned w4 = __ldg(occ4 + (b4 >> 5));
+    const unsigned w2 = __ldg(occ2 + (b2 >> 5));
+    int g[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const unsigned cx = (c & 1) ? ux1 : ux, cy = ((c >> 1) & 1) ? uy1 : uy, cz = (c >> 2) ? uz1 : uz;
+      g[c] = __ldg(grid + ((static_cast<size_t>(cz) << gbits | cy) << gbits | cx));
+    }
+    *sd = d;
+    *es = d > 0 ? 0 : (!((w4 >> (b4 & 31)) & 1u) ? 4 : (!((w2 >> (b2 & 31)) & 1u) ? 2 : 0));
+    *blk = d > 0 ? -1 : g[0];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = i0 + (c & 1), j = j0 + ((c >> 1) & 1), k = k0 + (c >> 2);
+      v[c] = g[c] < 0 ? -1 : static_cast<long long>(g[c]) * kBlockVoxels + (((k & 7) * 8 + (j & 7)) * 8 + (i & 7));
+    }
+  }
   // d > 0: every super-block within Chebyshev distance d - 1 of this one is
   // inside the window and empty; 0: occupied or outside the window.
   CSF_DEV int super_dist(int bx, int by, int bz) const {

@@ -708,6 +708,39 @@ CSF_DEV bool sample_real(const V& vol, double px, double py, double pz, typename
   return true;
 }
 
+// sample_real with the corner voxel ids already known (HashView::probe_cell):
+// the same arithmetic, the corner loads in one round trip.
+template <typename V>
+CSF_DEV bool sample_real_at(const V& vol, double px, double py, double pz, const long long* v, double* out) {
+  const double gx = (px - vol.ox) / vol.vs;
+  const double gy = (py - vol.oy) / vol.vs;
+  const double gz = (pz - vol.oz) / vol.vs;
+  const int i0 = ifloor(gx), j0 = ifloor(gy), k0 = ifloor(gz);
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) ok = ok && v[c] >= 0;
+  if (!ok) return false;
+  double2 rw[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) rw[c] = vol.vox.rw[v[c]];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) ok = ok && rw[c].y > 0.0;
+  if (!ok) return false;
+  const double fx = gx - static_cast<double>(i0);
+  const double fy = gy - static_cast<double>(j0);
+  const double fz = gz - static_cast<double>(k0);
+  double accum = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double wx = (c & 1) ? fx : 1.0 - fx;
+    const double wy = ((c >> 1) & 1) ? fy : 1.0 - fy;
+    const double wz = (c >> 2) ? fz : 1.0 - fz;
+    accum = accum + ((wx * wy) * wz) * rw[c].x;
+  }
+  *out = accum;
+  return true;
+}
+
 // Exit distance of the ray from the axis-aligned box of `span` blocks whose
 // lowest block is (bx, by, bz) (inverse direction precomputed; used only to
 // bound skipped alphas, with a margin, so ~1 ulp error is immaterial).
@@ -834,7 +867,8 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
         // empty space: the cube of (2d - 1)^3 empty super-blocks around this
         // one (distance field), else this unallocated block
         int sd, es, blk;
-        vol.probe(bx, by, bz, &sd, &es, &blk);
+        long long cv[8];
+        vol.probe_cell(i0, j0, k0, &sd, &es, &blk, cv);
         int span = 0, lx = bx, ly = by, lz = bz;
         if (sd > 0) {
           span = 8 * (2 * sd - 1);
@@ -864,7 +898,7 @@ __global__ void __launch_bounds__(128) k_raycast_march(V vol, const double* __re
         }
         double f;
         CSF_MSTAT(++nsamp);
-        if (!sample_real(vol, px, py, pz, cache, &f)) {
+        if (!sample_real_at(vol, px, py, pz, cv, &f)) {
           have_prev = false;
           ++n;
           continue;
@@ -993,7 +1027,8 @@ __global__ void __launch_bounds__(128) k_raycast_march_seg(HashView vol, const d
               k0 = ifloor((pz - vol.oz) / vol.vs);
     const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
     int sd, es, blk;
-    vol.probe(bx, by, bz, &sd, &es, &blk);
+    long long cv[8];
+    vol.probe_cell(i0, j0, k0, &sd, &es, &blk, cv);
     int span = 0, lx = bx, ly = by, lz = bz;
     if (sd > 0) {
       span = 8 * (2 * sd - 1);
@@ -1020,8 +1055,7 @@ __global__ void __launch_bounds__(128) k_raycast_march_seg(HashView vol, const d
       continue;
     }
     double f;
-    NoCache c;
-    if (!sample_real(vol, px, py, pz, c, &f)) {
+    if (!sample_real_at(vol, px, py, pz, cv, &f)) {
       have_prev = false;
       ++n;
       continue;
