@@ -532,7 +532,7 @@ __global__ void k_flags(HashView vol, const unsigned long long* __restrict__ can
       const int bx = static_cast<int>((key >> 42) & 0x1FFFFF) - kCoordBias;
       const int by = static_cast<int>((key >> 21) & 0x1FFFFF) - kCoordBias;
       const int bz = static_cast<int>(key & 0x1FFFFF) - kCoordBias;
-      const int id = vol.find(bx, by, bz);
+      const int id = vol.block(bx, by, bz);  // the dense index (one load) or the chain
       cand_block[s] = id;
       nf = id < 0;
     }
@@ -971,10 +971,12 @@ CSF_DEV bool table_sample(const HashView& vol, const V3<double>& o, const V3<dou
   const double px = o.v[0] + alpha * dir.v[0], py = o.v[1] + alpha * dir.v[1], pz = o.v[2] + alpha * dir.v[2];
   const int i0 = ifloor((px - vol.ox) / vol.vs), j0 = ifloor((py - vol.oy) / vol.vs),
             k0 = ifloor((pz - vol.oz) / vol.vs);
-  const int bx = i0 >> 3, by = j0 >> 3, bz = k0 >> 3;
-  if (vol.super_occupied(bx, by, bz) == 0 || vol.block(bx, by, bz) < 0) return false;
-  NoCache c;
-  return sample_real(vol, px, py, pz, c, f);
+  // one round trip for the occupancy test and the corner ids (probe_cell)
+  int sd, es, blk;
+  long long cv[8];
+  vol.probe_cell(i0, j0, k0, &sd, &es, &blk, cv);
+  if (sd > 0 || blk < 0) return false;
+  return sample_real_at(vol, px, py, pz, cv, f);
 }
 
 CSF_DEV void ray_of(const double* s_pose, int x, int y, V3<double>* o, V3<double>* dir) {
