@@ -1862,14 +1862,9 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
     // the small levels, where the longest ray sets the kernel time.
     int S = 1;
     if constexpr (V::kHashed) {
-#ifndef CSF_SEG_MAX
-#define CSF_SEG_MAX 16
-#endif
-#ifndef CSF_SEG_TARGET
-#define CSF_SEG_TARGET 320000
-#endif
-      constexpr int kSegMax = CSF_SEG_MAX;
-      constexpr long long kTargetThreads = CSF_SEG_TARGET;
+      // (measured: 640k / 1.3M / 160k targets and S = 2 at level 0 are slower)
+      constexpr int kSegMax = 16;
+      constexpr long long kTargetThreads = 320000;
       while (S < kSegMax && static_cast<long long>(P) * S * 2 <= kTargetThreads) S *= 2;
       if (!atab || !seg_first) S = 1;
     }
@@ -1906,11 +1901,7 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
   }
   // first order: the cooperative lift (8 lanes per pixel for the real chain,
   // then one thread per (pixel, channel))
-#ifdef CSF_LIFT_SCALAR
-  const bool pair = false;
-#else
   const bool pair = Dp % 2 == 0;
-#endif
   const int npix = lift_pixels(pair ? Dp / 2 : Dp);
   const size_t smem_c = smem + sizeof(LiftRec) * npix;
   if (pair)
