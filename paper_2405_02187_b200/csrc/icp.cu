@@ -319,72 +319,53 @@ CSF_DEV void level_accumulate(const IcpLevelArgs& a, int c, int ebase, int e0, i
   (void)ifx;
   (void)ify;
   const int Dp = a.Dp;
-  // one correspondence's channel row, accumulated (the model-map channels
-  // MVi / MNi loaded by the caller)
-  auto row_acc = [&](int e, const double (&MVi)[3], const double (&MNi)[3]) {
-      const double d = s_rec[kRD * kSegSlots + e];
-      const double vv[3] = {s_rec[kRV0 * kSegSlots + e], s_rec[kRV1 * kSegSlots + e], d};
-      const double tnx = d * -cxc, tny = d * -cyc;
-      const double vi[3] = {CSF_CH_DIV(__fma_rn(tnx, kfx, -s_rec[kRNX * kSegSlots + e] * fxc), kfx * kfx, ifx),
-                            CSF_CH_DIV(__fma_rn(tny, kfy, -s_rec[kRNY * kSegSlots + e] * fyc), kfy * kfy, ify), 0.0};
-      double P[3], DF[3], MN[3], Pi[3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        P[r] = s_rec[(kRP0 + r) * kSegSlots + e];
-        DF[r] = s_rec[(kRDF0 + r) * kSegSlots + e];
-        MN[r] = s_rec[(kRMN0 + r) * kSegSlots + e];
-        double qi[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) qi[k] = __fma_rn(s_pose[(3 * r + k) * C], vi[k], s_pose[(3 * r + k) * C + c] * vv[k]);
-        Pi[r] = (qi[0] + (qi[1] + qi[2])) + s_pose[(9 + r) * C + c];
-      }
-      const double DFi[3] = {Pi[0] - MVi[0], Pi[1] - MVi[1], Pi[2] - MVi[2]};
-      double ti[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) ti[k] = __fma_rn(DF[k], MNi[k], DFi[k] * MN[k]);
-      double ch[7], row[7];
-      ch[0] = MNi[0];
-      ch[1] = MNi[1];
-      ch[2] = MNi[2];
-      ch[3] = __fma_rn(P[1], MNi[2], Pi[1] * MN[2]) - __fma_rn(P[2], MNi[1], Pi[2] * MN[1]);
-      ch[4] = __fma_rn(P[2], MNi[0], Pi[2] * MN[0]) - __fma_rn(P[0], MNi[2], Pi[0] * MN[2]);
-      ch[5] = __fma_rn(P[0], MNi[1], Pi[0] * MN[1]) - __fma_rn(P[1], MNi[0], Pi[1] * MN[0]);
-      ch[6] = ti[0] + (ti[1] + ti[2]);
-      row[0] = MN[0];
-      row[1] = MN[1];
-      row[2] = MN[2];
-      row[3] = s_rec[kRPN0 * kSegSlots + e];
-      row[4] = s_rec[kRPN1 * kSegSlots + e];
-      row[5] = s_rec[kRPN2 * kSegSlots + e];
-      row[6] = s_rec[kRRR * kSegSlots + e];
-#pragma unroll
-    for (int q = 0; q < 27; ++q)
-      acc[q] = __fma_rn(row[acc_row_a(q)], ch[acc_row_b(q)], __fma_rn(ch[acc_row_a(q)], row[acc_row_b(q)], acc[q]));
-  };
-  auto load_maps = [&](int e, double (&MVi)[3], double (&MNi)[3]) {
+  for (int e = e0 + first; e < e0 + n; e += 32) {
     // the model-map channels of the correspondence (prefetched into L1 by phase A)
     const long long m = s_m[e];
+    double MVi[3], MNi[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       MVi[k] = __ldg(a.vim + (3 * m + k) * Dp + c - 1);
       MNi[k] = __ldg(a.nim + (3 * m + k) * Dp + c - 1);
     }
-  };
-  int e = e0 + first;
-#ifdef CSF_ACC_U2
-  // two of the lane's entries per trip: both entries' gathers in flight
-  for (; e + 32 < e0 + n; e += 64) {
-    double MVa[3], MNa[3], MVb[3], MNb[3];
-    load_maps(e, MVa, MNa);
-    load_maps(e + 32, MVb, MNb);
-    row_acc(e, MVa, MNa);
-    row_acc(e + 32, MVb, MNb);
-  }
-#endif
-  for (; e < e0 + n; e += 32) {
-    double MVi[3], MNi[3];
-    load_maps(e, MVi, MNi);
-    row_acc(e, MVi, MNi);
+    const double d = s_rec[kRD * kSegSlots + e];
+    const double vv[3] = {s_rec[kRV0 * kSegSlots + e], s_rec[kRV1 * kSegSlots + e], d};
+    const double tnx = d * -cxc, tny = d * -cyc;
+    const double vi[3] = {CSF_CH_DIV(__fma_rn(tnx, kfx, -s_rec[kRNX * kSegSlots + e] * fxc), kfx * kfx, ifx),
+                          CSF_CH_DIV(__fma_rn(tny, kfy, -s_rec[kRNY * kSegSlots + e] * fyc), kfy * kfy, ify), 0.0};
+    double P[3], DF[3], MN[3], Pi[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      P[r] = s_rec[(kRP0 + r) * kSegSlots + e];
+      DF[r] = s_rec[(kRDF0 + r) * kSegSlots + e];
+      MN[r] = s_rec[(kRMN0 + r) * kSegSlots + e];
+      double qi[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) qi[k] = __fma_rn(s_pose[(3 * r + k) * C], vi[k], s_pose[(3 * r + k) * C + c] * vv[k]);
+      Pi[r] = (qi[0] + (qi[1] + qi[2])) + s_pose[(9 + r) * C + c];
+    }
+    const double DFi[3] = {Pi[0] - MVi[0], Pi[1] - MVi[1], Pi[2] - MVi[2]};
+    double ti[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ti[k] = __fma_rn(DF[k], MNi[k], DFi[k] * MN[k]);
+    double ch[7], row[7];
+    ch[0] = MNi[0];
+    ch[1] = MNi[1];
+    ch[2] = MNi[2];
+    ch[3] = __fma_rn(P[1], MNi[2], Pi[1] * MN[2]) - __fma_rn(P[2], MNi[1], Pi[2] * MN[1]);
+    ch[4] = __fma_rn(P[2], MNi[0], Pi[2] * MN[0]) - __fma_rn(P[0], MNi[2], Pi[0] * MN[2]);
+    ch[5] = __fma_rn(P[0], MNi[1], Pi[0] * MN[1]) - __fma_rn(P[1], MNi[0], Pi[1] * MN[0]);
+    ch[6] = ti[0] + (ti[1] + ti[2]);
+    row[0] = MN[0];
+    row[1] = MN[1];
+    row[2] = MN[2];
+    row[3] = s_rec[kRPN0 * kSegSlots + e];
+    row[4] = s_rec[kRPN1 * kSegSlots + e];
+    row[5] = s_rec[kRPN2 * kSegSlots + e];
+    row[6] = s_rec[kRRR * kSegSlots + e];
+#pragma unroll
+    for (int q = 0; q < 27; ++q)
+      acc[q] = __fma_rn(row[acc_row_a(q)], ch[acc_row_b(q)], __fma_rn(ch[acc_row_a(q)], row[acc_row_b(q)], acc[q]));
   }
 }
 
