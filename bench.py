@@ -684,16 +684,23 @@ def main():
     prof = ctx.profile_read()
     ctx.profile(False)
 
-    # ---------------- e2e through the public API from pinned host memory
+    # ---------------- e2e through the public API from pinned host memory, in
+    # the launch mode `value` chose (graph: the per-frame upload waits are
+    # external event-wait nodes of the replayed run); two untimed calls set
+    # up the capture
     pinned = torch.empty(depth.shape, dtype=torch.float32, pin_memory=True)
     pinned.numpy()[:] = depth
     host_frames = pinned.numpy()
+    pipe.set_graph(use_graph)
+    for _ in range(2):
+        pipe.run_host(host_frames, gt)
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         r = pipe.run_host(host_frames, gt)
     t_e2e = time.perf_counter() - t0
+    pipe.set_graph(False)
     if dist is not None:
         t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

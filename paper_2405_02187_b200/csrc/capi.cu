@@ -999,15 +999,19 @@ struct csf_pipeline_s {
   std::vector<cudaEvent_t> frame_ev;
   bool wait_frames = false;
   // CUDA graph of a whole run (csf_pipeline_set_graph): captured on the
-  // first graph-mode run after a stream run of the same frame count
+  // first graph-mode run after a stream run of the same frame count.  Two
+  // graphs: [0] device-resident frames (csf_pipeline_run), [1] run_host's
+  // per-frame upload waits (captured as external event-wait nodes).
   bool use_graph = false;
-  cudaGraphExec_t graph_exec = nullptr;
-  int exec_frames = 0;   // frame count of graph_exec
-  int graph_frames = 0;  // frame count of the last stream run
-  unsigned long long graph_launches = 0;
-  int stream_runs = 0;
+  bool capturing = false;
+  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};
+  int exec_frames[2] = {0, 0};   // frame count of graph_exec
+  int graph_frames[2] = {0, 0};  // frame count of the last stream run
+  unsigned long long graph_launches[2] = {0, 0};
+  int stream_runs[2] = {0, 0};
   ~csf_pipeline_s() {
-    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    for (cudaGraphExec_t g : graph_exec)
+      if (g) cudaGraphExecDestroy(g);
     for (cudaEvent_t e : frame_ev) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     hits.release();
@@ -1163,11 +1167,13 @@ static int pipeline_run_body(csf_pipeline p, int n_frames);
 extern "C" int csf_pipeline_set_graph(csf_pipeline p, int enable) {
   if (!p) return CSF_EINVAL;
   p->use_graph = enable != 0;
-  if (!p->use_graph && p->graph_exec) {
+  if (!p->use_graph) {
     cudaSetDevice(p->ctx->device);
     cudaStreamSynchronize(p->ctx->stream);
-    cudaGraphExecDestroy(p->graph_exec);
-    p->graph_exec = nullptr;
+    for (cudaGraphExec_t& g : p->graph_exec) {
+      if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
   }
   return CSF_OK;
 }
@@ -1178,49 +1184,53 @@ extern "C" int csf_pipeline_run(csf_pipeline p, int n_frames) {
   if (n_frames <= 0 || n_frames > p->n_uploaded) return fail(ctx, CSF_EINVAL, "csf_pipeline_run: frames not uploaded");
   cudaSetDevice(ctx->device);
   // Graph mode replays the captured run: no host work per kernel.  A run is
-  // captured only after a stream run of the same frame count has set up every
-  // lazily allocated scratch; profiling and per-frame upload waits (run_host)
-  // take the stream path.
-  const bool graph = p->use_graph && !ctx->prof.on && !p->wait_frames;
-  if (graph && p->graph_exec && p->exec_frames == n_frames) {
-    CUDA_TRY(ctx, cudaGraphLaunch(p->graph_exec, ctx->stream));
-    ctx->launches += p->graph_launches;
+  // captured only after a stream run of the same frame count (and mode) has
+  // set up every lazily allocated scratch; profiling takes the stream path.
+  // run_host's per-frame upload waits become external event-wait nodes: a
+  // replay waits for the events' latest records (this call's uploads).
+  const int m = p->wait_frames ? 1 : 0;
+  const bool graph = p->use_graph && !ctx->prof.on;
+  if (graph && p->graph_exec[m] && p->exec_frames[m] == n_frames) {
+    CUDA_TRY(ctx, cudaGraphLaunch(p->graph_exec[m], ctx->stream));
+    ctx->launches += p->graph_launches[m];
     p->n_run = n_frames;
     return CSF_OK;
   }
-  if (graph && p->stream_runs > 0 && p->graph_frames == n_frames) {
-    if (p->graph_exec) {
-      cudaGraphExecDestroy(p->graph_exec);
-      p->graph_exec = nullptr;
+  if (graph && p->stream_runs[m] > 0 && p->graph_frames[m] == n_frames) {
+    if (p->graph_exec[m]) {
+      cudaGraphExecDestroy(p->graph_exec[m]);
+      p->graph_exec[m] = nullptr;
     }
     cudaGraph_t g = nullptr;
     CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     const unsigned long long l0 = ctx->launches;
+    p->capturing = true;
     const int rc = pipeline_run_body(p, n_frames);
+    p->capturing = false;
     const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
     if (rc) {
       if (g) cudaGraphDestroy(g);
       return rc;
     }
     if (ce != cudaSuccess) return fail(ctx, CSF_ECUDA, std::string("csf_pipeline_run: capture: ") + cudaGetErrorString(ce));
-    const cudaError_t ie = cudaGraphInstantiate(&p->graph_exec, g, 0);
+    const cudaError_t ie = cudaGraphInstantiate(&p->graph_exec[m], g, 0);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) {
-      p->graph_exec = nullptr;
+      p->graph_exec[m] = nullptr;
       return fail(ctx, CSF_ECUDA, std::string("csf_pipeline_run: graph instantiate: ") + cudaGetErrorString(ie));
     }
-    p->graph_launches = ctx->launches - l0;
-    p->exec_frames = n_frames;
+    p->graph_launches[m] = ctx->launches - l0;
+    p->exec_frames[m] = n_frames;
     ctx->launches = l0;
-    CUDA_TRY(ctx, cudaGraphLaunch(p->graph_exec, ctx->stream));
-    ctx->launches += p->graph_launches;
+    CUDA_TRY(ctx, cudaGraphLaunch(p->graph_exec[m], ctx->stream));
+    ctx->launches += p->graph_launches[m];
     p->n_run = n_frames;
     return CSF_OK;
   }
   const int rc = pipeline_run_body(p, n_frames);
   if (rc == CSF_OK) {
-    ++p->stream_runs;
-    p->graph_frames = n_frames;
+    ++p->stream_runs[m];
+    p->graph_frames[m] = n_frames;
   }
   return rc;
 }
@@ -1246,7 +1256,8 @@ static int pipeline_run_body(csf_pipeline p, int n_frames) {
   else
     launch_seed(L, p->G, p->Dp, p->dirs.p, p->D, cfg.h, p->gt.p, p->kbase.p, p->pose.p, p->intr_levels.p, p->levels);
   launch_frame_begin(L, st, 0);
-  if (p->wait_frames) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, p->frame_ev[0], 0));
+  if (p->wait_frames)
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, p->frame_ev[0], p->capturing ? cudaEventWaitExternal : 0));
   launch_bilateral(L, p->frames.p, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
   int* upd = &st->pad[1];
   rc = volume_fuse(v, p->raw.p, W, H, p->pose.p, p->intr_levels.p, upd);
@@ -1255,7 +1266,8 @@ static int pipeline_run_body(csf_pipeline p, int n_frames) {
 
   for (int f = 1; f < n_frames; ++f) {
     launch_frame_begin(L, st, f);
-    if (p->wait_frames) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, p->frame_ev[f], 0));
+    if (p->wait_frames)
+      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, p->frame_ev[f], p->capturing ? cudaEventWaitExternal : 0));
     {
       PROF(ctx, kPBilateral);
       launch_bilateral(L, p->frames.p + P * f, nullptr, p->raw.p, p->pyr0.p, W, H, 4.5, 0.03, 3);
