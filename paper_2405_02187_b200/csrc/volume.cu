@@ -648,9 +648,11 @@ __global__ void k_alloc_finalize(int* n_blocks, int max_blocks, const int* first
 //     skip stops 1e-6 m before the block's analytic exit so the exact
 //     per-sample test decides every boundary case.  Output: the crossing's
 //     (alpha_prev, alpha) or a miss.
-//   k_raycast_lift — one thread per (hit pixel, channel group): re-evaluates
-//     the two samples at the recorded alphas (bit-identical real parts), the
-//     interpolated vertex and the gradient normal in L<G>.
+//   k_raycast_lift_coop / k_raycast_lift2_coop — the lifted epilogue: a
+//     real pass per hit pixel (8 lanes: the two samples at the recorded
+//     alphas, bit-identical, and the 6 central differences), then the
+//     channels per (pixel, channel pair) in tangent form (first order) or per
+//     (pixel, parameter pair) in Bicomplex arithmetic (second order).
 // ----------------------------------------------------------------------------
 // Pixel order of the raycast kernels: 8x4-pixel warp tiles in row-major
 // tile order (lin = 32 * tile + lane).  The rays of a warp are a compact
@@ -1109,7 +1111,7 @@ __global__ void __launch_bounds__(128) k_raycast_march_fin(HashView vol, const d
 // respect to the cell fractions (real parts of sample_tsdf<S>, bit-identical).
 template <typename V>
 CSF_DEV bool sample_real_ex(const V& vol, double px, double py, double pz, double* out, int* vid, double* wgt,
-                            double* ds) {
+                            double* ds, double* Fout = nullptr) {
   const double gx = (px - vol.ox) / vol.vs;
   const double gy = (py - vol.oy) / vol.vs;
   const double gz = (pz - vol.oz) / vol.vs;
@@ -1145,6 +1147,7 @@ CSF_DEV bool sample_real_ex(const V& vol, double px, double py, double pz, doubl
     dsy += (((c >> 1) & 1) ? 1.0 : -1.0) * (wx * wz) * F;
     dsz += ((c >> 2) ? 1.0 : -1.0) * (wx * wy) * F;
     vid[c] = static_cast<int>(v[c]);
+    if (Fout) Fout[c] = rw[c].x;
   }
   ds[0] = dsx;
   ds[1] = dsy;
@@ -1428,67 +1431,173 @@ __global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol,
   }
 }
 
+// ---- second order, cooperative: the per-pixel real pass of the first-order
+// lift (8 lanes per pixel: the crossing pair and the 6 central differences)
+// records each sample's corner voxels and their real fields; then one thread
+// per (pixel, pair) evaluates the lifted epilogue of raycast<S> (tsdf.hpp:
+// 255-284) in Bicomplex arithmetic with those corners (no block lookups, no
+// (F, W) loads): sample_tsdf<S> / sample_gradient<S>'s operations.
+struct LiftRec2 {
+  double F[8][8];  // corner real fields per sample
+  int vid[8][8];   // corner voxel ids per sample
+  int ok;
+  int pad_;
+};
+
+// sample_tsdf<S> (order-2 branch) with the corners known and valid.
 template <typename S, typename V>
-__global__ void __launch_bounds__(128) k_raycast_lift(V vol, const double* __restrict__ pose,
-                                                      const double* __restrict__ intr, int w, int h, int Dp,
-                                                      const double2* __restrict__ hits, double* __restrict__ vre,
-                                                      double* __restrict__ nre, double* __restrict__ vim,
-                                                      double* __restrict__ nim) {
+CSF_DEV S sample_tsdf_at(const V& vol, const V3<S>& p, const int* vid, const double* F, int g0) {
+  const S gx = (p.v[0] - vol.ox) / vol.vs;
+  const S gy = (p.v[1] - vol.oy) / vol.vs;
+  const S gz = (p.v[2] - vol.oz) / vol.vs;
+  const int i0 = ifloor(re(gx)), j0 = ifloor(re(gy)), k0 = ifloor(re(gz));
+  const S fx = gx - static_cast<double>(i0);
+  const S fy = gy - static_cast<double>(j0);
+  const S fz = gz - static_cast<double>(k0);
+  S accum = lit<S>(0.0);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const S wx = (c & 1) ? fx : 1.0 - fx;
+    const S wy = ((c >> 1) & 1) ? fy : 1.0 - fy;
+    const S wz = (c >> 2) ? fz : 1.0 - fz;
+    accum = accum + ((wx * wy) * wz) * field_at<S>(vol.vox, vid[c], F[c], g0);
+  }
+  return accum;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) k_raycast_lift2_coop(V vol, const double* __restrict__ pose,
+                                                            const double* __restrict__ intr, int w, int h, int Dp,
+                                                            const double2* __restrict__ hits, double* __restrict__ vre,
+                                                            double* __restrict__ nre, double* __restrict__ vim,
+                                                            double* __restrict__ nim) {
   pdl_wait();
   pdl_trigger();
+  using S = B<1>;
+  constexpr int G = Traits<S>::G;
   extern __shared__ double sm[];
   const int C = 1 + Dp;
+  LiftRec2* recs = reinterpret_cast<LiftRec2*>(sm + 16 * C);
   for (int i = threadIdx.x; i < 12 * C; i += blockDim.x) sm[i] = pose[i];
   for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) sm[12 * C + i] = intr[i];
   __syncthreads();
-  constexpr int G = Traits<S>::G;
-  const int passes = G == 0 ? 1 : Dp / G;
-  const long long item = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (item >= static_cast<long long>(w) * h * passes) return;
-  const int pix = static_cast<int>(item / passes);
-  const int gi = static_cast<int>(item % passes);
-  const double2 hit = hits[pix];
-  if (hit.y < 0.0) return;
-  const double alpha_prev = hit.x, alpha_hit = hit.y;
-  const int x = pix % w, y = pix / w;
   const double* kk = sm + 12 * C;
-  const int g0 = gi * G;
-  typename V::Cache cache;
-  cache.reset();
-  Pose<S> P;
-#pragma unroll
-  for (int e = 0; e < 9; ++e) P.R.m[e] = load_ch<S>(sm + e * C, g0, G);
-#pragma unroll
-  for (int e = 0; e < 3; ++e) P.t.v[e] = load_ch<S>(sm + (9 + e) * C, g0, G);
-  const S fx = load_ch<S>(kk, g0, G), fy = load_ch<S>(kk + C, g0, G);
-  const S cx = load_ch<S>(kk + 2 * C, g0, G), cy = load_ch<S>(kk + 3 * C, g0, G);
-  const S one = lit<S>(1.0);
-  const V3<S> dcs = mk3<S>((static_cast<double>(x) - cx) / fx, (static_cast<double>(y) - cy) / fy, one);
-  const S rns = sqrt_s(dot3(dcs, dcs));
-  const V3<S> dirs = matvec(P.R, mk3<S>(dcs.v[0] / rns, dcs.v[1] / rns, dcs.v[2] / rns));
-  const V3<S>& os = P.t;
-  auto at = [&](double a) {
-    return mk3<S>(os.v[0] + a * dirs.v[0], os.v[1] + a * dirs.v[1], os.v[2] + a * dirs.v[2]);
-  };
-  S fl_prev, fl;
-  sample_tsdf<S>(vol, at(alpha_prev), g0, &fl_prev, cache);
-  sample_tsdf<S>(vol, at(alpha_hit), g0, &fl, cache);
-  const double span = alpha_hit - alpha_prev;
-  const S astar = alpha_prev - (span * fl_prev) / (fl - fl_prev);
-  const V3<S> v = mk3<S>(os.v[0] + astar * dirs.v[0], os.v[1] + astar * dirs.v[1], os.v[2] + astar * dirs.v[2]);
-  V3<S> grad;
-  if (!sample_gradient<S>(vol, v, g0, &grad, cache)) return;
-  const S len2 = dot3(grad, grad);
-  if (!(re(len2) > 0.0)) return;
-  const S ln = sqrt_s(len2);
-  const V3<S> n = mk3<S>(grad.v[0] / ln, grad.v[1] / ln, grad.v[2] / ln);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    if (gi == 0) {
-      vre[3LL * pix + c] = re(v.v[c]);
-      nre[3LL * pix + c] = re(n.v[c]);
+  const int P = w * h;
+  const double hv = vol.vs;
+  // ---- real pass: lane s of pixel p (k_raycast_lift_coop's arithmetic)
+  {
+    const int p = threadIdx.x >> 3, s = threadIdx.x & 7;
+    const int pix = lift_pixel(kLiftPix, p, w, h);
+    LiftRec2& r = recs[p];
+    double2 hit = make_double2(0.0, -1.0), fpair = make_double2(0.0, 0.0);
+    if (pix >= 0) {
+      hit = hits[pix];
+      fpair = hits[P + pix];
     }
-    if constexpr (G > 0) {
+    const bool active = hit.y >= 0.0;
+    const int x = pix >= 0 ? pix % w : 0, y = pix >= 0 ? pix / w : 0;
+    double R[9], T[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) R[e] = sm[e * C];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) T[e] = sm[(9 + e) * C];
+    const double fxk = kk[0], fyk = kk[C], cxk = kk[2 * C], cyk = kk[3 * C];
+    const double tx = static_cast<double>(x) - cxk, ty = static_cast<double>(y) - cyk;
+    const double dc[3] = {tx / fxk, ty / fyk, 1.0};
+    const double rn = sqrt(dc[0] * dc[0] + (dc[1] * dc[1] + 1.0 * 1.0));
+    const double dn[3] = {dc[0] / rn, dc[1] / rn, dc[2] / rn};
+    double dir[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) dir[q] = R[3 * q] * dn[0] + (R[3 * q + 1] * dn[1] + R[3 * q + 2] * dn[2]);
+    const double a0 = hit.x, a1 = hit.y;
+    const double f0 = active ? fpair.x : 0.0, f1 = active ? fpair.y : 0.0;
+    const double astar = a0 - ((a1 - a0) * f0) / (f1 - f0);
+    const double vv[3] = {T[0] + astar * dir[0], T[1] + astar * dir[1], T[2] + astar * dir[2]};
+    bool ok = true;
+    double g = 0.0;
+    if (active) {
+      double q[3];
+      if (s < 2) {
+        const double a = s == 0 ? a0 : a1;
+        q[0] = T[0] + a * dir[0];
+        q[1] = T[1] + a * dir[1];
+        q[2] = T[2] + a * dir[2];
+      } else {
+        const int axis = (s - 2) >> 1;
+        q[0] = vv[0];
+        q[1] = vv[1];
+        q[2] = vv[2];
+        q[axis] = (s & 1) ? q[axis] + hv : q[axis] - hv;
+      }
+      double wgt[8], ds[3];
+      ok = sample_real_ex(vol, q[0], q[1], q[2], &g, r.vid[s], wgt, ds, r.F[s]);
+    }
+    const unsigned lane0 = (threadIdx.x & 31) & ~7u;
+    const unsigned all_ok = __ballot_sync(0xffffffffu, ok);
+    const bool group_ok = ((all_ok >> lane0) & 0xffu) == 0xffu;
+    double fs[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) fs[k] = __shfl_sync(0xffffffffu, g, lane0 + 2 + k);
+    if (s == 0) {
+      bool good = active && group_ok;
+      double grad[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) grad[a] = (fs[2 * a + 1] - fs[2 * a]) / (2.0 * hv);
+      good = good && grad[0] * grad[0] + (grad[1] * grad[1] + grad[2] * grad[2]) > 0.0;
+      r.ok = good ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  // ---- one thread per (pixel, pair): the Bicomplex chain
+  const int passes = Dp / G;
+  for (int it = threadIdx.x; it < kLiftPix * passes; it += blockDim.x) {
+    const int p = it / passes, gi = it - p * passes;
+    const LiftRec2& r = recs[p];
+    const int pix = lift_pixel(kLiftPix, p, w, h);
+    if (pix < 0 || !r.ok) continue;
+    const double2 hit = hits[pix];
+    const double alpha_prev = hit.x, alpha_hit = hit.y;
+    const int x = pix % w, y = pix / w;
+    const int g0 = gi * G;
+    Pose<S> Ps;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Ps.R.m[e] = load_ch<S>(sm + e * C, g0, G);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) Ps.t.v[e] = load_ch<S>(sm + (9 + e) * C, g0, G);
+    const S fx = load_ch<S>(kk, g0, G), fy = load_ch<S>(kk + C, g0, G);
+    const S cx = load_ch<S>(kk + 2 * C, g0, G), cy = load_ch<S>(kk + 3 * C, g0, G);
+    const S one = lit<S>(1.0);
+    const V3<S> dcs = mk3<S>((static_cast<double>(x) - cx) / fx, (static_cast<double>(y) - cy) / fy, one);
+    const S rns = sqrt_s(dot3(dcs, dcs));
+    const V3<S> dirs = matvec(Ps.R, mk3<S>(dcs.v[0] / rns, dcs.v[1] / rns, dcs.v[2] / rns));
+    const V3<S>& os = Ps.t;
+    auto at = [&](double a) {
+      return mk3<S>(os.v[0] + a * dirs.v[0], os.v[1] + a * dirs.v[1], os.v[2] + a * dirs.v[2]);
+    };
+    const S fl_prev = sample_tsdf_at<S>(vol, at(alpha_prev), r.vid[0], r.F[0], g0);
+    const S fl = sample_tsdf_at<S>(vol, at(alpha_hit), r.vid[1], r.F[1], g0);
+    const double span = alpha_hit - alpha_prev;
+    const S astar = alpha_prev - (span * fl_prev) / (fl - fl_prev);
+    const V3<S> v = mk3<S>(os.v[0] + astar * dirs.v[0], os.v[1] + astar * dirs.v[1], os.v[2] + astar * dirs.v[2]);
+    V3<S> grad;
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {  // sample_gradient<S> (tsdf.hpp:181-196)
+      V3<S> lo = v, hi = v;
+      lo.v[axis] = lo.v[axis] - hv;
+      hi.v[axis] = hi.v[axis] + hv;
+      const S flo = sample_tsdf_at<S>(vol, lo, r.vid[2 + 2 * axis], r.F[2 + 2 * axis], g0);
+      const S fhi = sample_tsdf_at<S>(vol, hi, r.vid[3 + 2 * axis], r.F[3 + 2 * axis], g0);
+      grad.v[axis] = (fhi - flo) / (2.0 * hv);
+    }
+    const S len2 = dot3(grad, grad);
+    const S ln = sqrt_s(len2);
+    const V3<S> n = mk3<S>(grad.v[0] / ln, grad.v[1] / ln, grad.v[2] / ln);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (gi == 0) {
+        vre[3LL * pix + c] = re(v.v[c]);
+        nre[3LL * pix + c] = re(n.v[c]);
+      }
       double* vi = vim + (3LL * pix + c) * Dp + g0;
       double* ni = nim + (3LL * pix + c) * Dp + g0;
 #pragma unroll
@@ -1892,10 +2001,10 @@ static void raycast_impl(const Launch& L, const V& view, Box box, int order, int
   if (L.phase == 1) return;
   const size_t smem = sizeof(double) * 16 * (1 + Dp);
   if (order == 2) {
-    // second order: one thread per (hit pixel, pair) in Bicomplex arithmetic
-    const long long items = static_cast<long long>(P) * (Dp / 3);
-    launch_pdl(k_raycast_lift<B<1>, V>, dim3(static_cast<int>((items + 127) / 128)), dim3(128), smem, L.stream, view,
-               pose, intr, w, h, Dp, hits, vre, nre, vim, nim);
+    // second order: the cooperative real pass, then one thread per (hit
+    // pixel, pair) in Bicomplex arithmetic over the recorded corners
+    launch_pdl(k_raycast_lift2_coop<V>, dim3(lift_grid(kLiftPix, w, h)), dim3(8 * kLiftPix),
+               smem + sizeof(LiftRec2) * kLiftPix, L.stream, view, pose, intr, w, h, Dp, hits, vre, nre, vim, nim);
     *L.launches += 1;
     return;
   }
