@@ -21,6 +21,9 @@
 #include <cstdlib>
 
 #include "csf_internal.h"
+// Bicomplex quotients with the separate 1/b.re^2 division in this unit (the
+// order-2 reduce/solve measured faster with it; lifted.cuh)
+#define CSF_B_DEN_DIV
 #include "geometry.cuh"
 
 namespace csfd {
