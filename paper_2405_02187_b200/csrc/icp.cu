@@ -1331,6 +1331,7 @@ __global__ void k_objective(const double* __restrict__ traj, const double* __res
 // ============================================================================
 constexpr int kR2Warps = 8;
 constexpr int kR2Threads = 32 * kR2Warps;
+constexpr int kR2Pairs = 5;  // pairs per CTA: one association serves them
 
 template <typename S>
 __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st, const double* __restrict__ depth,
@@ -1349,16 +1350,11 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
   constexpr int CG = 1 + G;
   constexpr int NA = 27 * CG;  // accumulator threads
   const int C = 1 + Dp;
-  const int g0 = blockIdx.y * G;
+  const int n_pairs = Dp / G;
   extern __shared__ double sm[];
-  S* rows = reinterpret_cast<S*>(sm);  // [kR2Threads][7]
+  S* rows = reinterpret_cast<S*>(sm);                                  // [kR2Threads][7]
+  int* s_corr = reinterpret_cast<int*>(rows + kR2Threads * 7);         // [tile_slots][4]: x, y, u, v
   __shared__ int s_wsum[kR2Warps];
-  // the canonical order (§3.3): lane l of every warp is stream l; warp w owns
-  // the accumulators q = w, w + 8, w + 16, w + 24 (< 27), all components of S
-  constexpr int kQ = (27 + kR2Warps - 1) / kR2Warps;
-  S acc[kQ];
-#pragma unroll
-  for (int i = 0; i < kQ; ++i) acc[i] = lit<S>(0.0);
   Pose<double> c2w, w2p;
   load_pose_real(pose, C, &c2w);
 #pragma unroll
@@ -1370,7 +1366,9 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
   const int n_slots = nxs * nys;
   const int t0 = blockIdx.x * tile_slots, t1 = min(n_slots, t0 + tile_slots);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int ebase = 0;
+  // ---- the tile's association once for the CTA's kR2Pairs pairs: the
+  // correspondences (pixel, model pixel) compacted in slot order
+  int n_corr = 0;
   for (int c0 = t0; c0 < t1; c0 += kR2Threads) {
     const int slot = c0 + threadIdx.x;
     int x = 0, y = 0, u = 0, v = 0;
@@ -1381,7 +1379,7 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
       corr = associate_slot(depth, w, h, x, y, fx, fy, cx, cy, c2w, w2p, vre, nre, d_max, cos_max, &u, &v);
     }
     const unsigned ballot = __ballot_sync(0xffffffffu, corr);
-    __syncthreads();  // the previous chunk's rows are consumed
+    __syncthreads();
     if (lane == 0) s_wsum[warp] = __popc(ballot);
     __syncthreads();
     int before = 0, total = 0;
@@ -1391,71 +1389,94 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
       total += s_wsum[k];
     }
     if (corr) {
-      const int pos = before + __popc(ballot & ((1u << lane) - 1u));
-      // jacobian_row (icp.cpp:20-24): vertex = backproject(K, x, y, d) in S
-      // (frames.hpp:38-41), p = base * vertex, r = (p - mv) . mn, J = [mn; p x mn]
-      const double d = depth[y * w + x];
-      const S kfx = load_ch<S>(intr, g0, G), kfy = load_ch<S>(intr + C, g0, G);
-      const S kcx = load_ch<S>(intr + 2 * C, g0, G), kcy = load_ch<S>(intr + 3 * C, g0, G);
-      const V3<S> vert = mk3<S>((d * (static_cast<double>(x) - kcx)) / kfx,
-                                (d * (static_cast<double>(y) - kcy)) / kfy, lit<S>(d));
-      Pose<S> base;
+      int* e4 = s_corr + 4 * (n_corr + before + __popc(ballot & ((1u << lane) - 1u)));
+      e4[0] = x;
+      e4[1] = y;
+      e4[2] = u;
+      e4[3] = v;
+    }
+    n_corr += total;
+  }
+  if (threadIdx.x == 0 && blockIdx.y == 0) counts[blockIdx.x] = n_corr;
+  // ---- per pair: the rows in S and the canonical-order sums (§3.3): lane l
+  // of every warp is stream l; warp w owns the accumulators q = w, w + 8,
+  // w + 16, w + 24 (< 27), all components of S
+  constexpr int kQ = (27 + kR2Warps - 1) / kR2Warps;
+  const int pa = blockIdx.y * kR2Pairs, pb = min(n_pairs, pa + kR2Pairs);
+  for (int pair = pa; pair < pb; ++pair) {
+    const int g0 = pair * G;
+    S acc[kQ];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) base.R.m[e] = load_ch<S>(pose + e * C, g0, G);
+    for (int i = 0; i < kQ; ++i) acc[i] = lit<S>(0.0);
+    for (int e0 = 0; e0 < n_corr; e0 += kR2Threads) {
+      const int e = e0 + threadIdx.x;
+      __syncthreads();  // the previous chunk's rows are consumed (and s_corr is complete)
+      if (e < n_corr) {
+        const int* e4 = s_corr + 4 * e;
+        const int x = e4[0], y = e4[1], u = e4[2], v = e4[3];
+        // jacobian_row (icp.cpp:20-24): vertex = backproject(K, x, y, d) in S
+        // (frames.hpp:38-41), p = base * vertex, r = (p - mv) . mn, J = [mn; p x mn]
+        const double d = depth[y * w + x];
+        const S kfx = load_ch<S>(intr, g0, G), kfy = load_ch<S>(intr + C, g0, G);
+        const S kcx = load_ch<S>(intr + 2 * C, g0, G), kcy = load_ch<S>(intr + 3 * C, g0, G);
+        const V3<S> vert = mk3<S>((d * (static_cast<double>(x) - kcx)) / kfx,
+                                  (d * (static_cast<double>(y) - kcy)) / kfy, lit<S>(d));
+        Pose<S> base;
 #pragma unroll
-      for (int e = 0; e < 3; ++e) base.t.v[e] = load_ch<S>(pose + (9 + e) * C, g0, G);
-      const long long m = static_cast<long long>(v) * w + u;
-      V3<S> mv, mn;
+        for (int q = 0; q < 9; ++q) base.R.m[q] = load_ch<S>(pose + q * C, g0, G);
 #pragma unroll
-      for (int c3 = 0; c3 < 3; ++c3) {
-        mv.v[c3].re = vre[3 * m + c3];
-        mn.v[c3].re = nre[3 * m + c3];
+        for (int q = 0; q < 3; ++q) base.t.v[q] = load_ch<S>(pose + (9 + q) * C, g0, G);
+        const long long m = static_cast<long long>(v) * w + u;
+        V3<S> mv, mn;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          mv.v[c3].im[g] = vim[(3 * m + c3) * Dp + g0 + g];
-          mn.v[c3].im[g] = nim[(3 * m + c3) * Dp + g0 + g];
+        for (int c3 = 0; c3 < 3; ++c3) {
+          mv.v[c3].re = vre[3 * m + c3];
+          mn.v[c3].re = nre[3 * m + c3];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            mv.v[c3].im[g] = vim[(3 * m + c3) * Dp + g0 + g];
+            mn.v[c3].im[g] = nim[(3 * m + c3) * Dp + g0 + g];
+          }
+        }
+        const V3<S> pw = apply(base, vert);
+        const S r = dot3(sub3(pw, mv), mn);
+        const V3<S> pn = cross3(pw, mn);
+        S* row = rows + 7 * threadIdx.x;
+        row[0] = mn.v[0]; row[1] = mn.v[1]; row[2] = mn.v[2];
+        row[3] = pn.v[0]; row[4] = pn.v[1]; row[5] = pn.v[2];
+        row[6] = r;
+      }
+      __syncthreads();
+      // accumulate_row (orc_icp.hpp): lane l adds, in entry order, the S
+      // product of the two row entries of every correspondence whose entry
+      // index is l mod 32 (e0 is a multiple of 32)
+      const int cnt = min(kR2Threads, n_corr - e0);
+      for (int k = lane; k < cnt; k += 32) {
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) {
+          const int q = warp + kR2Warps * i;
+          if (q < 27) acc[i] = acc[i] + rows[7 * k + acc_row_a(q)] * rows[7 * k + acc_row_b(q)];
         }
       }
-      const V3<S> pw = apply(base, vert);
-      const S r = dot3(sub3(pw, mv), mn);
-      const V3<S> pn = cross3(pw, mn);
-      S* row = rows + 7 * pos;
-      row[0] = mn.v[0]; row[1] = mn.v[1]; row[2] = mn.v[2];
-      row[3] = pn.v[0]; row[4] = pn.v[1]; row[5] = pn.v[2];
-      row[6] = r;
     }
-    __syncthreads();
-    // accumulate_row (orc_icp.hpp): lane l adds, in entry order, the S
-    // product of the two row entries of every correspondence whose global
-    // entry index is l mod 32
-    const int first = (lane - (ebase & 31) + 32) & 31;
-    for (int e = first; e < total; e += 32) {
+    // the fixed butterfly of the first-order kernel, lane 0's value
 #pragma unroll
-      for (int i = 0; i < kQ; ++i) {
-        const int q = warp + kR2Warps * i;
-        if (q < 27) acc[i] = acc[i] + rows[7 * e + acc_row_a(q)] * rows[7 * e + acc_row_b(q)];
+    for (int i = 0; i < kQ; ++i) {
+      const int q = warp + kR2Warps * i;
+      double vv[CG];
+      vv[0] = acc[i].re;
+#pragma unroll
+      for (int g = 0; g < G; ++g) vv[1 + g] = acc[i].im[g];
+#pragma unroll
+      for (int c = 0; c < CG; ++c)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) vv[c] = vv[c] + __shfl_xor_sync(0xffffffffu, vv[c], off);
+      if (lane == 0 && q < 27) {
+        double* dst = partials + static_cast<long long>(blockIdx.x) * 27 * C + q * C;
+        if (pair == 0) dst[0] = vv[0];
+#pragma unroll
+        for (int g = 0; g < G; ++g) dst[g0 + 1 + g] = vv[1 + g];
       }
-    }
-    ebase += total;
-  }
-  if (threadIdx.x == 0 && blockIdx.y == 0) counts[blockIdx.x] = ebase;
-  // the fixed butterfly of the first-order kernel, lane 0's value
-#pragma unroll
-  for (int i = 0; i < kQ; ++i) {
-    const int q = warp + kR2Warps * i;
-    double v[CG];
-    v[0] = acc[i].re;
-#pragma unroll
-    for (int g = 0; g < G; ++g) v[1 + g] = acc[i].im[g];
-#pragma unroll
-    for (int c = 0; c < CG; ++c)
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v[c] = v[c] + __shfl_xor_sync(0xffffffffu, v[c], off);
-    if (lane == 0 && q < 27) {
-      double* dst = partials + static_cast<long long>(blockIdx.x) * 27 * C + q * C;
-      if (blockIdx.y == 0) dst[0] = v[0];
-#pragma unroll
-      for (int g = 0; g < G; ++g) dst[g0 + 1 + g] = v[1 + g];
     }
   }
   (void)NA;
@@ -1807,10 +1828,11 @@ void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double
   using S = B<1>;
   const int tiles = icp_tiles(w, h, stride);
   const int pairs = Dp / 3;
-  const size_t smem = sizeof(S) * kR2Threads * 7;
   const long long n_slots = static_cast<long long>((w + stride - 1) / stride) * ((h + stride - 1) / stride);
   const int tile_slots = icp_tile_slots(n_slots);
-  launch_pdl(k_icp_reduce2<S>, dim3(tiles, pairs), dim3(kR2Threads), smem, L.stream, st, depth, w, h, stride, intr,
+  const size_t smem = sizeof(S) * kR2Threads * 7 + sizeof(int) * 4 * static_cast<size_t>(tile_slots);
+  launch_pdl(k_icp_reduce2<S>, dim3(tiles, (pairs + kR2Pairs - 1) / kR2Pairs), dim3(kR2Threads), smem, L.stream, st,
+             depth, w, h, stride, intr,
              pose, vre, nre, vim, nim, d_max, cos_max, Dp, tile_slots, partials, counts);
   launch_pdl(k_icp_solve2<S>, dim3(pairs), dim3(128), 0, L.stream, st, partials, counts, tiles, pose, Dp, stage);
   launch_pdl(k_icp_commit, dim3(1), dim3(1), 0, L.stream, st, pose, Dp, stage, level, tol);
