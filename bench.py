@@ -183,6 +183,16 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def synth_rgb(depth):
+    """uint8 colour frames [n][h][w][3] for the RGB-D ingest (configs 2-3):
+    a seeded albedo texture (seed 1, the scene's seed) shaded by the rendered
+    depth; invalid pixels black."""
+    rng = np.random.default_rng(1)
+    albedo = rng.integers(64, 256, size=(1,) + depth.shape[1:] + (3,), dtype=np.int32)
+    shade = np.clip(255.0 / (1.0 + depth), 0, 255).astype(np.int32)[..., None]
+    return np.where(depth[..., None] > 0, (albedo * shade) >> 8, 0).astype(np.uint8)
+
+
 def measured_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -691,14 +701,21 @@ def main():
     pinned = torch.empty(depth.shape, dtype=torch.float32, pin_memory=True)
     pinned.numpy()[:] = depth
     host_frames = pinned.numpy()
+    # configs 2 and 3 ingest uint8 RGB beside the depth (BASELINE configs[1]);
+    # the path never reads colour (the reference has none), it is uploaded only
+    host_rgb = None
+    if not one and not four:
+        rgb_pinned = torch.empty(depth.shape + (3,), dtype=torch.uint8, pin_memory=True)
+        rgb_pinned.numpy()[:] = synth_rgb(depth)
+        host_rgb = rgb_pinned.numpy()
     pipe.set_graph(use_graph)
     for _ in range(2):
-        pipe.run_host(host_frames, gt)
+        pipe.run_host(host_frames, gt, rgb=host_rgb)
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r = pipe.run_host(host_frames, gt)
+        r = pipe.run_host(host_frames, gt, rgb=host_rgb)
     t_e2e = time.perf_counter() - t0
     pipe.set_graph(False)
     if dist is not None:
@@ -706,7 +723,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_e2e = float(t.item())
     e2e_value = units_per_step * args.steps / t_e2e
-    h2d = int(depth.nbytes + gt.nbytes)
+    h2d = int(depth.nbytes + gt.nbytes + (host_rgb.nbytes if host_rgb is not None else 0))
     d2h = int(8 * (len(mine) + 1))
 
     # ---------------- roofline: every category with a bytes model; the dominant one is `roofline`
@@ -751,7 +768,9 @@ def main():
                    "l2": ("working set: dense 128^3 x (16 + 6x8) B = 134 MB volume + maps > L2 (126 MB), "
                           "no flush" if one else
                           "working set (hashed volume, ~GBs) >> L2")},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ingest": "float32 depth + uint8 RGB (colour unused by the path)" if host_rgb is not None
+                else "float32 depth"},
         "gpu_launches": int(launches),
         "launch_mode": {"used": "cuda_graph" if use_graph else "stream", "stream_ms_per_step": ms_stream / args.steps,
                         "graph_ms_per_step": ms_graph / args.steps},

@@ -798,6 +798,19 @@ class Pipeline {
     if (objective) *objective = obj;
     return g;
   }
+  // RGB-D ingest (BASELINE config 2): rgb [n][h][w][3] uint8 beside the depth;
+  // colour is uploaded, unused (the reference has no colour term)
+  std::vector<double> csfd_pipeline_gradient_rgbd(const std::vector<float>& depth,
+                                                  const std::vector<unsigned char>& rgb,
+                                                  const std::vector<double>& gt, int n, double* objective = nullptr) {
+    if (cfg_.order == 2) throw std::invalid_argument("csfd_pipeline_gradient_rgbd: pipeline has order 2");
+    if (rgb.size() != depth.size() * 3) throw std::invalid_argument("csfd_pipeline_gradient_rgbd: rgb size");
+    std::vector<double> g(static_cast<size_t>(cfg_.n_dirs));
+    double obj = 0.0;
+    check(ctx_, csf_pipeline_run_host_rgbd(p_, depth.data(), rgb.data(), gt.data(), n, g.data(), &obj));
+    if (objective) *objective = obj;
+    return g;
+  }
   // H_{pair_i[p], pair_j[p]} per pair
   std::vector<double> csfd_pipeline_hessian(const std::vector<float>& depth, const std::vector<double>& gt, int n,
                                             double* objective = nullptr) {

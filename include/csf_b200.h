@@ -454,6 +454,16 @@ int csf_pipeline_volume(csf_pipeline p, csf_volume* out);
 /* One end-to-end call from host buffers: upload, run, read back. */
 int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames, double* gradient,
                           double* objective);
+/* BASELINE config 2's RGB-D ingest: as csf_pipeline_run_host, plus uint8 colour
+ * frames rgb [n][h][w][3] (NULL: none) uploaded behind each frame's depth on
+ * the copy stream into the pipeline's colour buffer.  Colour is ingested and
+ * unused — the reference pipeline has no colour term (frames.hpp
+ * reads depth only) — so no kernel waits on it; the call returns after the
+ * colour uploads have landed (the host buffer is borrowed for the call). */
+int csf_pipeline_run_host_rgbd(csf_pipeline p, const float* depth, const unsigned char* rgb, const double* gt,
+                               int n_frames, double* gradient, double* objective);
+/* Colour frame `frame` as ingested by the last run_host_rgbd call, out [h][w][3]. */
+int csf_pipeline_download_rgb(csf_pipeline p, int frame, unsigned char* out);
 
 /* ---- direction-sharded runs (collective C2) ------------------
  * Rank r of N packs a contiguous block of the directions (or pairs) as its

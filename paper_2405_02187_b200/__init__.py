@@ -812,16 +812,32 @@ class Pipeline:
         v.close = lambda: None  # the pipeline owns the handle
         return v
 
-    def run_host(self, depth: np.ndarray, gt: np.ndarray) -> PipelineResult:
-        """End-to-end call from host buffers (upload + run + read back)."""
+    def run_host(self, depth: np.ndarray, gt: np.ndarray, rgb: np.ndarray | None = None) -> PipelineResult:
+        """End-to-end call from host buffers (upload + run + read back).
+        rgb: optional uint8 colour frames [n][h][w][3] (csf_pipeline_run_host_rgbd:
+        ingested beside the depth, unused by the path, as the reference)."""
         d = np.ascontiguousarray(depth, dtype=np.float32)
         g = _f64(gt).reshape(-1, 12)
         self.n_frames = self.n_run = d.shape[0]
         grad = np.zeros(max(self.D, 1))
         obj = C.c_double()
-        self.ctx.check(self.ctx.lib.csf_pipeline_run_host(self.h, _fp(d), _dp(g), self.n_frames, _dp(grad),
-                                                          C.byref(obj)))
+        if rgb is None:
+            self.ctx.check(self.ctx.lib.csf_pipeline_run_host(self.h, _fp(d), _dp(g), self.n_frames, _dp(grad),
+                                                              C.byref(obj)))
+        else:
+            c = np.ascontiguousarray(rgb, dtype=np.uint8)
+            if c.shape != d.shape + (3,):
+                raise ValueError(f"rgb must be {d.shape + (3,)} uint8, got {c.shape}")
+            self.ctx.check(self.ctx.lib.csf_pipeline_run_host_rgbd(
+                self.h, _fp(d), c.ctypes.data_as(C.POINTER(C.c_ubyte)), _dp(g), self.n_frames, _dp(grad),
+                C.byref(obj)))
         return PipelineResult(grad[: self.D].copy(), obj.value)
+
+    def rgb_frame(self, frame: int) -> np.ndarray:
+        """Colour frame `frame` as ingested by the last run_host(rgb=...)."""
+        out = np.empty((self.cfg.k.height, self.cfg.k.width, 3), np.uint8)
+        self.ctx.check(self.ctx.lib.csf_pipeline_download_rgb(self.h, frame, out.ctypes.data_as(C.POINTER(C.c_ubyte))))
+        return out
 
     def hessian(self, poses: bool = False, stats: bool = False) -> "HessianResult":
         """Order-2 result: H_{i_p j_p} per pair and the pair's first-order

@@ -30,7 +30,7 @@ EXPORTS = (
     "csf_comm_unique_id", "csf_ctx_attach_comm", "csf_gather_columns",
     "csf_raycast", "csf_track_frame", "csf_track_frame_traced", "csf_icp_energy_derivs", "csf_view_scores", "csf_associate",
     "csf_linearized_step", "csf_pairwise_sum", "csf_pipeline_create", "csf_pipeline_destroy", "csf_pipeline_upload",
-    "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_hessian", "csf_pipeline_run_host", "csf_pipeline_volume", "csf_pipeline_set_graph",
+    "csf_pipeline_run", "csf_pipeline_result", "csf_pipeline_hessian", "csf_pipeline_run_host", "csf_pipeline_run_host_rgbd", "csf_pipeline_download_rgb", "csf_pipeline_volume", "csf_pipeline_set_graph",
     "csf_synth_workload", "csf_default_reloc_cfg", "csf_reloc_create", "csf_reloc_destroy", "csf_reloc_info",
     "csf_reloc_energy", "csf_relocalize", "csf_depth_cloud", "csf_eval_nn_error", "csf_io_last_error",
     "csf_write_depth_png16", "csf_read_depth_png16", "csf_read_intrinsics", "csf_write_intrinsics",
@@ -154,6 +154,8 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
         "csf_pipeline_result": (ip, [vp, dp, dp, dp, i32p]),
         "csf_pipeline_hessian": (ip, [vp, dp, dp, dp, dp, dp, i32p]),
         "csf_pipeline_run_host": (ip, [vp, fp, dp, ip, dp, dp]),
+        "csf_pipeline_run_host_rgbd": (ip, [vp, fp, C.POINTER(C.c_ubyte), dp, ip, dp, dp]),
+        "csf_pipeline_download_rgb": (ip, [vp, ip, C.POINTER(C.c_ubyte)]),
         "csf_pipeline_volume": (ip, [vp, C.POINTER(vp)]),
         "csf_pipeline_set_graph": (ip, [vp, ip]),
         "csf_synth_workload": (ip, [vp, ip, ip, ip, ip, fp, dp, C.POINTER(Intrinsics)]),

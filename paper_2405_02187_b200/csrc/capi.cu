@@ -989,6 +989,7 @@ struct csf_pipeline_s {
   int W = 0, H = 0, levels = 3;
   int n_uploaded = 0, n_run = 0;
   DevBuf<float> frames;
+  DevBuf<unsigned char> rgb;  // run_host_rgbd: colour frames [max_frames][H][W][3], ingested, unused
   DevBuf<double> gt, raw, pyr0, pyr1, pyr2, vre, nre, vim, nim, partials, pose, pred_pose, intr_levels, traj, kbase,
       out, stage;
   DevBuf<int> counts, stats, dirs, pair_i, pair_j;
@@ -1015,6 +1016,7 @@ struct csf_pipeline_s {
     for (cudaEvent_t e : frame_ev) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     hits.release();
+    rgb.release();
     frames.release(); gt.release(); raw.release(); pyr0.release(); pyr1.release(); pyr2.release(); vre.release();
     nre.release(); vim.release(); nim.release(); partials.release(); pose.release(); pred_pose.release();
     intr_levels.release(); traj.release(); kbase.release(); out.release(); counts.release(); stats.release();
@@ -1398,12 +1400,28 @@ extern "C" int csf_pipeline_volume(csf_pipeline p, csf_volume* out) {
   return CSF_OK;
 }
 
+extern "C" int csf_pipeline_download_rgb(csf_pipeline p, int frame, unsigned char* out) {
+  if (!p || !out || frame < 0 || frame >= p->cfg.max_frames) return CSF_EINVAL;
+  csf_ctx ctx = p->ctx;
+  if (!p->rgb.p) return fail(ctx, CSF_EINVAL, "csf_pipeline_download_rgb: no colour frames were ingested");
+  cudaSetDevice(ctx->device);
+  const size_t P = static_cast<size_t>(p->W) * p->H;
+  if (p->copy_stream) CUDA_TRY(ctx, cudaStreamSynchronize(p->copy_stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(out, p->rgb.p + 3 * P * frame, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+  return sync_check(ctx, "csf_pipeline_download_rgb");
+}
+
 // One end-to-end call.  The frames go up on a copy stream, one event per
 // frame, and frame f's kernels wait only for frame f's upload, so (from
 // pinned host memory) the H2D of later frames overlaps the device work of
 // earlier ones.
 extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const double* gt, int n_frames,
                                      double* gradient, double* objective) {
+  return csf_pipeline_run_host_rgbd(p, depth, nullptr, gt, n_frames, gradient, objective);
+}
+
+extern "C" int csf_pipeline_run_host_rgbd(csf_pipeline p, const float* depth, const unsigned char* rgb,
+                                          const double* gt, int n_frames, double* gradient, double* objective) {
   if (!p || !depth || !gt || n_frames <= 0) return CSF_EINVAL;
   csf_ctx ctx = p->ctx;
   if (n_frames > p->cfg.max_frames) return fail(ctx, CSF_EINVAL, "csf_pipeline_run_host: more frames than max_frames");
@@ -1419,10 +1437,15 @@ extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const d
   CUDA_TRY(ctx, cudaEventRecord(p->frame_ev[0], ctx->stream));
   CUDA_TRY(ctx, cudaStreamWaitEvent(p->copy_stream, p->frame_ev[0], 0));
   CUDA_TRY(ctx, cudaMemcpyAsync(p->gt.p, gt, sizeof(double) * 12 * n_frames, cudaMemcpyHostToDevice, ctx->stream));
+  if (rgb && !p->rgb.p) CUDA_TRY(ctx, p->rgb.alloc(P * 3 * static_cast<size_t>(p->cfg.max_frames)));
   for (int f = 0; f < n_frames; ++f) {
     CUDA_TRY(ctx, cudaMemcpyAsync(p->frames.p + P * f, depth + P * f, sizeof(float) * P, cudaMemcpyHostToDevice,
                                   p->copy_stream));
     CUDA_TRY(ctx, cudaEventRecord(p->frame_ev[f], p->copy_stream));
+    // colour after the frame's depth event: the frame's kernels never wait on it
+    if (rgb)
+      CUDA_TRY(ctx, cudaMemcpyAsync(p->rgb.p + 3 * P * f, rgb + 3 * P * f, 3 * P, cudaMemcpyHostToDevice,
+                                    p->copy_stream));
   }
   p->n_uploaded = n_frames;
   p->wait_frames = true;
@@ -1433,7 +1456,13 @@ extern "C" int csf_pipeline_run_host(csf_pipeline p, const float* depth, const d
     cudaStreamSynchronize(p->copy_stream);
     return rc;
   }
-  return csf_pipeline_result(p, gradient, objective, nullptr, nullptr);
+  rc = csf_pipeline_result(p, gradient, objective, nullptr, nullptr);
+  // the colour uploads borrow the caller's buffer until they land
+  if (rgb) {
+    const cudaError_t e = cudaStreamSynchronize(p->copy_stream);
+    if (!rc && e != cudaSuccess) return fail(ctx, CSF_ECUDA, cudaGetErrorString(e));
+  }
+  return rc;
 }
 
 // ---------------------------------------------------------------------------

@@ -254,3 +254,28 @@ def test_run_host_matches_staged_run(gpu_ctx, orc, pinned):
         assert np.array_equal(r.gradient, ref.gradient)
     full = pipe.result()
     assert np.array_equal(full.poses, ref.poses) and np.array_equal(full.stats, ref.stats)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_run_host_rgbd_ingests_colour(gpu_ctx, orc, graph):
+    """BASELINE config 2's RGB-D ingest (csf_pipeline_run_host_rgbd): the
+    uint8 colour frames land on the device byte for byte beside the depth,
+    and the derivative is bit-identical to the depth-only call (colour is
+    ingested, unused — the reference has no colour term)."""
+    import torch
+    n = 4
+    d, gt, k = orc.workload(2, n, 160, 120)
+    cfg = _pipeline_cfg(2, k, [0, 1, 6, 7], n, True)
+    pipe = csf.Pipeline(cfg, ctx=gpu_ctx)
+    pipe.set_graph(graph)
+    host = torch.from_numpy(np.ascontiguousarray(d, dtype=np.float32)).pin_memory().numpy()
+    ref = pipe.run_host(host, gt)
+    rgb = np.random.default_rng(7).integers(0, 256, size=d.shape + (3,), dtype=np.uint8)
+    rgb_pinned = torch.from_numpy(rgb).pin_memory().numpy()
+    for _ in range(2):
+        r = pipe.run_host(host, gt, rgb=rgb_pinned)
+        assert r.objective == ref.objective and np.array_equal(r.gradient, ref.gradient)
+    for f in range(n):
+        assert np.array_equal(pipe.rgb_frame(f), rgb[f])
+    with pytest.raises(ValueError):
+        pipe.run_host(host, gt, rgb=rgb[:, :, :, :2])
