@@ -314,6 +314,145 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
   return true;
 }
 
+// Second-order fusion in tangent form.  Every Bicomplex operation of
+// measured_tsdf<B<1>> (csfd.hpp:103-140 rules, the truncated product: im12 =
+// a.re b12 + a12 b.re + a1 b2 + a2 b1) is evaluated on the channel slots only,
+// with the real intermediates of the one real chain (bit-identical to the
+// reference's double chain) shared by all pairs: the generic path re-runs the
+// real chain, its IEEE divisions and square roots once per pair.  Quotients
+// and square roots use the real pass's reciprocals (a few ulp per channel, as
+// the first-order adjoint form).  Per pair: the 19 inputs' (im1, im2, im12)
+// from shared memory, the voxel's three field slots read and written.
+struct Ch3 {
+  double a, b, ab;  // im1, im2, im12
+};
+// x * y (both lifted), real parts xr, yr
+CSF_DEV Ch3 ch_mul(double xr, const Ch3& x, double yr, const Ch3& y) {
+  return {xr * y.a + x.a * yr, xr * y.b + x.b * yr, ((xr * y.ab + x.ab * yr) + x.a * y.b) + x.b * y.a};
+}
+// x / y with real parts xr, yr; inv = 1 / yr, inv2 = inv * inv
+CSF_DEV Ch3 ch_div(double xr, const Ch3& x, double yr, const Ch3& y, double inv, double inv2) {
+  return {(x.a * yr - xr * y.a) * inv2, (x.b * yr - xr * y.b) * inv2,
+          ((x.ab * inv - (x.a * y.b + x.b * y.a) * inv2) - (xr * y.ab) * inv2) + ((((2.0 * xr) * y.a) * y.b) * inv2) * inv};
+}
+// lift2 (csfd.hpp:212-263): d1 = f'(x), d2 = f''(x)
+CSF_DEV Ch3 ch_lift(const Ch3& z, double d1, double d2) {
+  return {d1 * z.a, d1 * z.b, d1 * z.ab + (d2 * z.a) * z.b};
+}
+CSF_DEV Ch3 ch_add(const Ch3& x, const Ch3& y) { return {x.a + y.a, x.b + y.b, x.ab + y.ab}; }
+CSF_DEV Ch3 ch_sub(const Ch3& x, const Ch3& y) { return {x.a - y.a, x.b - y.b, x.ab - y.ab}; }
+CSF_DEV Ch3 ch_scale(const Ch3& x, double c) { return {x.a * c, x.b * c, x.ab * c}; }
+CSF_DEV Ch3 ch_at(const double* row, int o) { return {row[o], row[o + 1], row[o + 2]}; }
+
+CSF_DEV bool fuse_voxel_pairs(const VoxelStore& vox, long long v, double px, double py, double pz,
+                              const double* __restrict__ depth, int w, int h, double mu, double cap, int Dp,
+                              const double* sm) {
+  const int C = 1 + Dp;
+  double R[9], t[3], c[3];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) R[e] = sm[e * C];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    t[e] = sm[(9 + e) * C];
+    c[e] = sm[(12 + e) * C];
+  }
+  const double kfx = sm[15 * C], kfy = sm[16 * C], kcx = sm[17 * C], kcy = sm[18 * C];
+  // ---- the real chain (fuse_voxel_adjoint's, measured_tsdf<double>)
+  double pc[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) pc[r] = (R[3 * r] * px + (R[3 * r + 1] * py + R[3 * r + 2] * pz)) + t[r];
+  if (!(pc[2] > 0.0)) return false;
+  const double ax = kfx * pc[0], ay = kfy * pc[1];
+  const double lx = ax / pc[2] + kcx;
+  const double ly = ay / pc[2] + kcy;
+  const int x0 = ifloor(lx), y0 = ifloor(ly);
+  if (x0 < 0 || y0 < 0 || x0 + 1 >= w || y0 + 1 >= h) return false;
+  const double d00 = depth[y0 * w + x0];
+  const double d10 = depth[y0 * w + x0 + 1];
+  const double d01 = depth[(y0 + 1) * w + x0];
+  const double d11 = depth[(y0 + 1) * w + x0 + 1];
+  if (!(d00 > 0.0) || !(d10 > 0.0) || !(d01 > 0.0) || !(d11 > 0.0)) return false;
+  const double nearv = fmin(fmin(d00, d10), fmin(d01, d11));
+  const double farv = fmax(fmax(d00, d10), fmax(d01, d11));
+  if (farv - nearv > 0.1) return false;
+  const double fxf = lx - static_cast<double>(x0);
+  const double fyf = ly - static_cast<double>(y0);
+  const double top = d00 + fxf * (d10 - d00);
+  const double bot = d01 + fxf * (d11 - d01);
+  const double sampled = top + fyf * (bot - top);
+  const double nx = lx - kcx, ny = ly - kcy;
+  const double rx = nx / kfx;
+  const double ry = ny / kfy;
+  const double lam2 = rx * rx + (ry * ry + 1.0 * 1.0);
+  const double lam = sqrt(lam2);
+  const double dx = c[0] - px, dy = c[1] - py, dz = c[2] - pz;
+  const double dist2 = dx * dx + (dy * dy + dz * dz);
+  const double dist = sqrt(dist2);
+  const double eta = sampled - dist / lam;
+  if (eta < -mu) return false;
+  const double q = eta / mu;
+  double psi = 1.0 < q ? 1.0 : q;
+  psi = -1.0 > psi ? -1.0 : psi;
+  const bool sat = 1.0 < q || -1.0 > q;
+  const double2 rw = vox.rw[v];
+  const double wt = rw.y;
+  const double fre = (wt * rw.x + psi) / (wt + 1.0);
+  const double inv_w1 = 1.0 / (wt + 1.0);
+  double* fim = vox.fim + v * vox.Dp;
+  const int NP = Dp / 3;
+  if (sat) {
+    // psi is the literal +-1 (clamp_s): its channels are zero
+    for (int pr = 0; pr < NP; ++pr) {
+      double* f3 = fim + 3 * pr;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) f3[k] = (wt * f3[k]) * inv_w1;
+    }
+  } else {
+    // reciprocals of the chain's divisors and the sqrt derivatives
+    const double iz = 1.0 / pc[2], iz2 = iz * iz;
+    const double ifx = 1.0 / kfx, ifx2 = ifx * ifx, ify = 1.0 / kfy, ify2 = ify * ify;
+    const double ilam = 1.0 / lam, ilam2 = ilam * ilam;
+    const double l1 = 0.5 / lam, l2 = (-0.5 * l1) / lam2;
+    const double s1 = 0.5 / dist, s2 = (-0.5 * s1) / dist2;
+    const double dd0 = d10 - d00, dd1 = d11 - d01, bt = bot - top;
+    const double imu = 1.0 / mu;
+    for (int pr = 0; pr < NP; ++pr) {
+      const int o = 1 + 3 * pr;
+      Ch3 pcc[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const Ch3 r0 = ch_at(sm + (3 * r) * C, o), r1 = ch_at(sm + (3 * r + 1) * C, o);
+        const Ch3 r2 = ch_at(sm + (3 * r + 2) * C, o), tr = ch_at(sm + (9 + r) * C, o);
+        pcc[r] = ch_add(ch_add(ch_scale(r0, px), ch_add(ch_scale(r1, py), ch_scale(r2, pz))), tr);
+      }
+      const Ch3 cfx = ch_at(sm + 15 * C, o), cfy = ch_at(sm + 16 * C, o);
+      const Ch3 ccx = ch_at(sm + 17 * C, o), ccy = ch_at(sm + 18 * C, o);
+      // lx = (fx pc0) / pc2 + cx, ly likewise
+      const Ch3 lxc = ch_add(ch_div(ax, ch_mul(kfx, cfx, pc[0], pcc[0]), pc[2], pcc[2], iz, iz2), ccx);
+      const Ch3 lyc = ch_add(ch_div(ay, ch_mul(kfy, cfy, pc[1], pcc[1]), pc[2], pcc[2], iz, iz2), ccy);
+      // bilinear depth: top + fy (bot - top), top/bot linear in fx
+      const Ch3 btc = ch_sub(ch_scale(lxc, dd1), ch_scale(lxc, dd0));
+      const Ch3 smp = ch_add(ch_scale(lxc, dd0), ch_mul(fyf, lyc, bt, btc));
+      // lambda = sqrt(rx^2 + ry^2 + 1)
+      const Ch3 rxc = ch_div(nx, ch_sub(lxc, ccx), kfx, cfx, ifx, ifx2);
+      const Ch3 ryc = ch_div(ny, ch_sub(lyc, ccy), kfy, cfy, ify, ify2);
+      const Ch3 lamc = ch_lift(ch_add(ch_mul(rx, rxc, rx, rxc), ch_mul(ry, ryc, ry, ryc)), l1, l2);
+      // dist = |center - p|
+      const Ch3 c0 = ch_at(sm + 12 * C, o), c1 = ch_at(sm + 13 * C, o), c2 = ch_at(sm + 14 * C, o);
+      const Ch3 distc =
+          ch_lift(ch_add(ch_mul(dx, c0, dx, c0), ch_add(ch_mul(dy, c1, dy, c1), ch_mul(dz, c2, dz, c2))), s1, s2);
+      const Ch3 psic = ch_scale(ch_sub(smp, ch_div(dist, distc, lam, lamc, ilam, ilam2)), imu);
+      double* f3 = fim + 3 * pr;
+      f3[0] = (wt * f3[0] + psic.a) * inv_w1;
+      f3[1] = (wt * f3[1] + psic.b) * inv_w1;
+      f3[2] = (wt * f3[2] + psic.ab) * inv_w1;
+    }
+  }
+  const double wn = wt + 1.0;
+  vox.rw[v] = make_double2(fre, cap < wn ? cap : wn);
+  return true;
+}
+
 // LD: the depth image carries perturbation channels (dch [P][Dp]): the
 // generic lifted evaluation (the adjoint form's 19 partials omit the depth
 // corners' channels).
@@ -326,6 +465,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
   pdl_trigger();
   extern __shared__ double sm[];
   constexpr bool kAdj = kAdjointFusion && Traits<S>::kOrder == 1 && !LD;
+  constexpr bool kPairs = kAdjointFusion && Traits<S>::kOrder == 2 && !LD;
   stage_pose_w2c<S>(pose, intr, Dp, sm);
   if constexpr (kAdj) stage_jacobian<NDP>(sm);
   const long long n = static_cast<long long>(vol.nx) * vol.ny * vol.nz;
@@ -340,6 +480,8 @@ __global__ void __launch_bounds__(256, 2) k_integrate_dense(DenseView vol, const
     const double pz = vol.oz + vol.vs * static_cast<double>(k);
     if constexpr (kAdj)
       fused += fuse_voxel_adjoint<NDP>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
+    else if constexpr (kPairs)
+      count_updates(upd, fuse_voxel_pairs(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
     else
       count_updates(upd, fuse_voxel<S>(vol.vox, v, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm,
                                        LD ? dch : nullptr));
@@ -363,6 +505,7 @@ __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView
   pdl_trigger();
   extern __shared__ double sm[];
   constexpr bool kAdj = kAdjointFusion && Traits<S>::kOrder == 1 && !LD;
+  constexpr bool kPairs = kAdjointFusion && Traits<S>::kOrder == 2 && !LD;
   stage_pose_w2c<S>(pose, intr, Dp, sm);
   if constexpr (kAdj) stage_jacobian<NDP>(sm);
   const int n_vis = counters[0];
@@ -379,6 +522,8 @@ __global__ void __launch_bounds__(256, CSF_INT_MINB) k_integrate_hashed(HashView
       const long long vv = static_cast<long long>(b) * kBlockVoxels + l;
       if constexpr (kAdj)
         fused += fuse_voxel_adjoint<NDP>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm);
+      else if constexpr (kPairs)
+        count_updates(upd, fuse_voxel_pairs(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm));
       else
         count_updates(upd, fuse_voxel<S>(vol.vox, vv, px, py, pz, depth, w, h, vol.mu, vol.cap, Dp, sm,
                                          LD ? dch : nullptr));
@@ -1118,7 +1263,7 @@ __global__ void __launch_bounds__(128) k_raycast_march_fin(HashView vol, const d
 // respect to the cell fractions (real parts of sample_tsdf<S>, bit-identical).
 template <typename V>
 CSF_DEV bool sample_real_ex(const V& vol, double px, double py, double pz, double* out, int* vid, double* wgt,
-                            double* ds, double* Fout = nullptr) {
+                            double* ds, double* Fout = nullptr, double* frac = nullptr) {
   const double gx = (px - vol.ox) / vol.vs;
   const double gy = (py - vol.oy) / vol.vs;
   const double gz = (pz - vol.oz) / vol.vs;
@@ -1159,6 +1304,11 @@ CSF_DEV bool sample_real_ex(const V& vol, double px, double py, double pz, doubl
   ds[0] = dsx;
   ds[1] = dsy;
   ds[2] = dsz;
+  if (frac) {
+    frac[0] = fx;
+    frac[1] = fy;
+    frac[2] = fz;
+  }
   *out = acc;
   return true;
 }
@@ -1449,6 +1599,18 @@ struct LiftRec2 {
   int vid[8][8];   // corner voxel ids per sample
   int ok;
   int pad_;
+#ifndef CSF_EXACT_CHANNELS
+  // tangent form: per sample the trilinear weights, dS/df (ds), the mixed
+  // second derivatives d2S/df_a df_b (E: xy, xz, yz) and the weight products
+  // of the edge differences (wp: 4 x wy wz, 4 x wx wz, 4 x wx wy); per pixel
+  // the real intermediates of the epilogue
+  double wgt[8][8];
+  double ds[8][3];
+  double E[8][3];
+  double wp[8][12];
+  double dc[2], rn, a0, a1, f0, f1, num, den, astar, ln;
+  double dn[3], dir[3], grad[3];
+#endif
 };
 
 // sample_tsdf<S> (order-2 branch) with the corners known and valid.
@@ -1536,8 +1698,34 @@ __global__ void __launch_bounds__(256) k_raycast_lift2_coop(V vol, const double*
         q[2] = vv[2];
         q[axis] = (s & 1) ? q[axis] + hv : q[axis] - hv;
       }
+#ifndef CSF_EXACT_CHANNELS
+      double fr[3];
+      ok = sample_real_ex(vol, q[0], q[1], q[2], &g, r.vid[s], r.wgt[s], r.ds[s], r.F[s], fr);
+      if (ok) {
+        const double wx[2] = {1.0 - fr[0], fr[0]}, wy[2] = {1.0 - fr[1], fr[1]}, wz[2] = {1.0 - fr[2], fr[2]};
+        double exy = 0.0, exz = 0.0, eyz = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+          const double sgx = cx ? 1.0 : -1.0, sgy = cy ? 1.0 : -1.0, sgz = cz ? 1.0 : -1.0;
+          exy += (sgx * sgy) * wz[cz] * r.F[s][c];
+          exz += (sgx * sgz) * wy[cy] * r.F[s][c];
+          eyz += (sgy * sgz) * wx[cx] * r.F[s][c];
+        }
+        r.E[s][0] = exy;
+        r.E[s][1] = exz;
+        r.E[s][2] = eyz;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          r.wp[s][m] = wy[m & 1] * wz[m >> 1];
+          r.wp[s][4 + m] = wx[m & 1] * wz[m >> 1];
+          r.wp[s][8 + m] = wx[m & 1] * wy[m >> 1];
+        }
+      }
+#else
       double wgt[8], ds[3];
       ok = sample_real_ex(vol, q[0], q[1], q[2], &g, r.vid[s], wgt, ds, r.F[s]);
+#endif
     }
     const unsigned lane0 = (threadIdx.x & 31) & ~7u;
     const unsigned all_ok = __ballot_sync(0xffffffffu, ok);
@@ -1550,11 +1738,159 @@ __global__ void __launch_bounds__(256) k_raycast_lift2_coop(V vol, const double*
       double grad[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) grad[a] = (fs[2 * a + 1] - fs[2 * a]) / (2.0 * hv);
-      good = good && grad[0] * grad[0] + (grad[1] * grad[1] + grad[2] * grad[2]) > 0.0;
+      const double len2 = grad[0] * grad[0] + (grad[1] * grad[1] + grad[2] * grad[2]);
+      good = good && len2 > 0.0;
       r.ok = good ? 1 : 0;
+#ifndef CSF_EXACT_CHANNELS
+      if (good) {
+        // the real outputs (bit-identical to the Bicomplex chain's real parts)
+        const double ln = sqrt(len2);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          vre[3LL * pix + c] = vv[c];
+          nre[3LL * pix + c] = grad[c] / ln;
+          r.dn[c] = dn[c];
+          r.dir[c] = dir[c];
+          r.grad[c] = grad[c];
+        }
+        r.dc[0] = dc[0];
+        r.dc[1] = dc[1];
+        r.rn = rn;
+        r.a0 = a0;
+        r.a1 = a1;
+        r.f0 = f0;
+        r.f1 = f1;
+        r.num = (a1 - a0) * f0;
+        r.den = f1 - f0;
+        r.astar = astar;
+        r.ln = ln;
+      }
+#endif
     }
   }
   __syncthreads();
+#ifndef CSF_EXACT_CHANNELS
+  // ---- one thread per (pixel, pair): the Bicomplex epilogue in tangent form
+  // (Ch3 slots over the recorded reals; the trilinear samples through their
+  // weights, first and mixed second derivatives in the cell fractions)
+  {
+    const int passes = Dp / G;
+    const double ivs = 1.0 / hv, i2h = 1.0 / (2.0 * hv);
+    for (int it = threadIdx.x; it < kLiftPix * passes; it += blockDim.x) {
+      const int p = it / passes, gi = it - p * passes;
+      const LiftRec2& r = recs[p];
+      const int pix = lift_pixel(kLiftPix, p, w, h);
+      if (pix < 0 || !r.ok) continue;
+      const int x = pix % w, y = pix / w;
+      const int o = 1 + gi * G;
+      const double fxk = kk[0], fyk = kk[C], cxk = kk[2 * C], cyk = kk[3 * C];
+      const Ch3 cfx = ch_at(kk, o), cfy = ch_at(kk + C, o), ccx = ch_at(kk + 2 * C, o), ccy = ch_at(kk + 3 * C, o);
+      // dcs = ((x - cx) / fx, (y - cy) / fy, 1)
+      const double ifx = 1.0 / fxk, ify = 1.0 / fyk;
+      const Ch3 zero = {0.0, 0.0, 0.0};
+      const Ch3 dc0 = ch_div(static_cast<double>(x) - cxk, ch_scale(ccx, -1.0), fxk, cfx, ifx, ifx * ifx);
+      const Ch3 dc1 = ch_div(static_cast<double>(y) - cyk, ch_scale(ccy, -1.0), fyk, cfy, ify, ify * ify);
+      // rns = sqrt(dot(dcs, dcs)); dn = dcs / rns
+      const double rn2 = r.dc[0] * r.dc[0] + (r.dc[1] * r.dc[1] + 1.0 * 1.0);
+      const double l1 = 0.5 / r.rn, l2 = (-0.5 * l1) / rn2;
+      const Ch3 rnc = ch_lift(ch_add(ch_mul(r.dc[0], dc0, r.dc[0], dc0), ch_mul(r.dc[1], dc1, r.dc[1], dc1)), l1, l2);
+      const double irn = 1.0 / r.rn, irn2 = irn * irn;
+      const Ch3 dnc[3] = {ch_div(r.dc[0], dc0, r.rn, rnc, irn, irn2), ch_div(r.dc[1], dc1, r.rn, rnc, irn, irn2),
+                          ch_div(1.0, zero, r.rn, rnc, irn, irn2)};
+      // dirs = R dn; T = t
+      Ch3 dirc[3], Tc[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const Ch3 m0 = ch_mul(sm[(3 * q) * C], ch_at(sm + (3 * q) * C, o), r.dn[0], dnc[0]);
+        const Ch3 m1 = ch_mul(sm[(3 * q + 1) * C], ch_at(sm + (3 * q + 1) * C, o), r.dn[1], dnc[1]);
+        const Ch3 m2 = ch_mul(sm[(3 * q + 2) * C], ch_at(sm + (3 * q + 2) * C, o), r.dn[2], dnc[2]);
+        dirc[q] = ch_add(m0, ch_add(m1, m2));
+        Tc[q] = ch_at(sm + (9 + q) * C, o);
+      }
+      // a trilinear sample of recorded sample s at a position with channels pc
+      auto sample = [&](int sidx, const Ch3* pc) {
+        const int* vid = r.vid[sidx];
+        Ch3 Gc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double* src = vol.vox.fim + static_cast<long long>(vid[c]) * vol.vox.Dp + (o - 1);
+          Gc[c] = {__ldg(src), __ldg(src + 1), __ldg(src + 2)};
+        }
+        Ch3 fr[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) fr[a] = ch_scale(pc[a], ivs);
+        Ch3 acc = zero;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc = ch_add(acc, ch_scale(Gc[c], r.wgt[sidx][c]));
+        // dS/df of the im1 and im2 fields (edge differences)
+        double d1[3], d2[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const int st = 1 << a;
+          double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            // the four edges along axis a: low corner index with bit a clear
+            const int lo = a == 0 ? 2 * m : a == 1 ? (m & 1) + 4 * (m >> 1) : m;
+            s1 += r.wp[sidx][4 * a + m] * (Gc[lo + st].a - Gc[lo].a);
+            s2 += r.wp[sidx][4 * a + m] * (Gc[lo + st].b - Gc[lo].b);
+          }
+          d1[a] = s1;
+          d2[a] = s2;
+        }
+        const double* D = r.ds[sidx];
+        const double* E = r.E[sidx];
+        Ch3 out;
+        out.a = acc.a + ((D[0] * fr[0].a + D[1] * fr[1].a) + D[2] * fr[2].a);
+        out.b = acc.b + ((D[0] * fr[0].b + D[1] * fr[1].b) + D[2] * fr[2].b);
+        out.ab = acc.ab + ((D[0] * fr[0].ab + D[1] * fr[1].ab) + D[2] * fr[2].ab) +
+                 (((d1[0] * fr[0].b + d1[1] * fr[1].b) + d1[2] * fr[2].b) +
+                  ((d2[0] * fr[0].a + d2[1] * fr[1].a) + d2[2] * fr[2].a)) +
+                 ((E[0] * (fr[0].a * fr[1].b + fr[1].a * fr[0].b) + E[1] * (fr[0].a * fr[2].b + fr[2].a * fr[0].b)) +
+                  E[2] * (fr[1].a * fr[2].b + fr[2].a * fr[1].b));
+        return out;
+      };
+      Ch3 q0[3], q1[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        q0[a] = ch_add(Tc[a], ch_scale(dirc[a], r.a0));
+        q1[a] = ch_add(Tc[a], ch_scale(dirc[a], r.a1));
+      }
+      const Ch3 flp = sample(0, q0), flh = sample(1, q1);
+      // astar = a0 - (span f0) / (f1 - f0)
+      const double iden = 1.0 / r.den;
+      const Ch3 qa = ch_div(r.num, ch_scale(flp, r.a1 - r.a0), r.den, ch_sub(flh, flp), iden, iden * iden);
+      const Ch3 ast = ch_scale(qa, -1.0);
+      Ch3 vc[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) vc[a] = ch_add(Tc[a], ch_mul(r.astar, ast, r.dir[a], dirc[a]));
+      Ch3 gc[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) gc[a] = ch_scale(ch_sub(sample(3 + 2 * a, vc), sample(2 + 2 * a, vc)), i2h);
+      // n = grad / |grad|
+      const double len2 = r.grad[0] * r.grad[0] + (r.grad[1] * r.grad[1] + r.grad[2] * r.grad[2]);
+      const double n1 = 0.5 / r.ln, n2 = (-0.5 * n1) / len2;
+      const Ch3 lnc = ch_lift(ch_add(ch_mul(r.grad[0], gc[0], r.grad[0], gc[0]),
+                                     ch_add(ch_mul(r.grad[1], gc[1], r.grad[1], gc[1]),
+                                            ch_mul(r.grad[2], gc[2], r.grad[2], gc[2]))),
+                              n1, n2);
+      const double iln = 1.0 / r.ln, iln2 = iln * iln;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const Ch3 nc = ch_div(r.grad[c], gc[c], r.ln, lnc, iln, iln2);
+        double* vi = vim + (3LL * pix + c) * Dp + (o - 1);
+        double* ni = nim + (3LL * pix + c) * Dp + (o - 1);
+        vi[0] = vc[c].a;
+        vi[1] = vc[c].b;
+        vi[2] = vc[c].ab;
+        ni[0] = nc.a;
+        ni[1] = nc.b;
+        ni[2] = nc.ab;
+      }
+    }
+    return;
+  }
+#endif
   // ---- one thread per (pixel, pair): the Bicomplex chain
   const int passes = Dp / G;
   for (int it = threadIdx.x; it < kLiftPix * passes; it += blockDim.x) {
