@@ -326,19 +326,38 @@ CSF_DEV bool fuse_voxel_adjoint(const VoxelStore& vox, long long v, double px, d
 struct Ch3 {
   double a, b, ab;  // im1, im2, im12
 };
+// kF: contract the slot arithmetic with explicit fused multiply-adds (the
+// library builds with -fmad=false so that real chains stay bit-identical;
+// slots are held to the 1e-9 tolerance, not to the per-operation rounding).
+// The fusion measured faster with them (order-2 fusion 274 -> 257 ms per
+// config-3 step), the lift slower (138 -> 142 ms), so each picks its form.
 // x * y (both lifted), real parts xr, yr
+template <bool kF = false>
 CSF_DEV Ch3 ch_mul(double xr, const Ch3& x, double yr, const Ch3& y) {
+  if constexpr (kF)
+    return {fma(xr, y.a, x.a * yr), fma(xr, y.b, x.b * yr), fma(x.b, y.a, fma(x.a, y.b, fma(xr, y.ab, x.ab * yr)))};
   return {xr * y.a + x.a * yr, xr * y.b + x.b * yr, ((xr * y.ab + x.ab * yr) + x.a * y.b) + x.b * y.a};
 }
 // x / y with real parts xr, yr; inv = 1 / yr, inv2 = inv * inv
+template <bool kF = false>
 CSF_DEV Ch3 ch_div(double xr, const Ch3& x, double yr, const Ch3& y, double inv, double inv2) {
+  if constexpr (kF) {
+    const double k = ((2.0 * xr) * inv2) * inv;
+    double ab = fma(-fma(x.a, y.b, x.b * y.a), inv2, x.ab * inv);
+    ab = fma(-(xr * y.ab), inv2, ab);
+    return {fma(x.a, yr, -(xr * y.a)) * inv2, fma(x.b, yr, -(xr * y.b)) * inv2, fma(k * y.a, y.b, ab)};
+  }
   return {(x.a * yr - xr * y.a) * inv2, (x.b * yr - xr * y.b) * inv2,
           ((x.ab * inv - (x.a * y.b + x.b * y.a) * inv2) - (xr * y.ab) * inv2) + ((((2.0 * xr) * y.a) * y.b) * inv2) * inv};
 }
 // lift2 (csfd.hpp:212-263): d1 = f'(x), d2 = f''(x)
+template <bool kF = false>
 CSF_DEV Ch3 ch_lift(const Ch3& z, double d1, double d2) {
+  if constexpr (kF) return {d1 * z.a, d1 * z.b, fma(d2 * z.a, z.b, d1 * z.ab)};
   return {d1 * z.a, d1 * z.b, d1 * z.ab + (d2 * z.a) * z.b};
 }
+// x * c + y
+CSF_DEV Ch3 ch_fma(const Ch3& x, double c, const Ch3& y) { return {fma(x.a, c, y.a), fma(x.b, c, y.b), fma(x.ab, c, y.ab)}; }
 CSF_DEV Ch3 ch_add(const Ch3& x, const Ch3& y) { return {x.a + y.a, x.b + y.b, x.ab + y.ab}; }
 CSF_DEV Ch3 ch_sub(const Ch3& x, const Ch3& y) { return {x.a - y.a, x.b - y.b, x.ab - y.ab}; }
 CSF_DEV Ch3 ch_scale(const Ch3& x, double c) { return {x.a * c, x.b * c, x.ab * c}; }
@@ -423,29 +442,29 @@ CSF_DEV bool fuse_voxel_pairs(const VoxelStore& vox, long long v, double px, dou
       for (int r = 0; r < 3; ++r) {
         const Ch3 r0 = ch_at(sm + (3 * r) * C, o), r1 = ch_at(sm + (3 * r + 1) * C, o);
         const Ch3 r2 = ch_at(sm + (3 * r + 2) * C, o), tr = ch_at(sm + (9 + r) * C, o);
-        pcc[r] = ch_add(ch_add(ch_scale(r0, px), ch_add(ch_scale(r1, py), ch_scale(r2, pz))), tr);
+        pcc[r] = ch_fma(r0, px, ch_fma(r1, py, ch_fma(r2, pz, tr)));
       }
       const Ch3 cfx = ch_at(sm + 15 * C, o), cfy = ch_at(sm + 16 * C, o);
       const Ch3 ccx = ch_at(sm + 17 * C, o), ccy = ch_at(sm + 18 * C, o);
       // lx = (fx pc0) / pc2 + cx, ly likewise
-      const Ch3 lxc = ch_add(ch_div(ax, ch_mul(kfx, cfx, pc[0], pcc[0]), pc[2], pcc[2], iz, iz2), ccx);
-      const Ch3 lyc = ch_add(ch_div(ay, ch_mul(kfy, cfy, pc[1], pcc[1]), pc[2], pcc[2], iz, iz2), ccy);
+      const Ch3 lxc = ch_add(ch_div<true>(ax, ch_mul<true>(kfx, cfx, pc[0], pcc[0]), pc[2], pcc[2], iz, iz2), ccx);
+      const Ch3 lyc = ch_add(ch_div<true>(ay, ch_mul<true>(kfy, cfy, pc[1], pcc[1]), pc[2], pcc[2], iz, iz2), ccy);
       // bilinear depth: top + fy (bot - top), top/bot linear in fx
       const Ch3 btc = ch_sub(ch_scale(lxc, dd1), ch_scale(lxc, dd0));
-      const Ch3 smp = ch_add(ch_scale(lxc, dd0), ch_mul(fyf, lyc, bt, btc));
+      const Ch3 smp = ch_add(ch_scale(lxc, dd0), ch_mul<true>(fyf, lyc, bt, btc));
       // lambda = sqrt(rx^2 + ry^2 + 1)
-      const Ch3 rxc = ch_div(nx, ch_sub(lxc, ccx), kfx, cfx, ifx, ifx2);
-      const Ch3 ryc = ch_div(ny, ch_sub(lyc, ccy), kfy, cfy, ify, ify2);
-      const Ch3 lamc = ch_lift(ch_add(ch_mul(rx, rxc, rx, rxc), ch_mul(ry, ryc, ry, ryc)), l1, l2);
+      const Ch3 rxc = ch_div<true>(nx, ch_sub(lxc, ccx), kfx, cfx, ifx, ifx2);
+      const Ch3 ryc = ch_div<true>(ny, ch_sub(lyc, ccy), kfy, cfy, ify, ify2);
+      const Ch3 lamc = ch_lift<true>(ch_add(ch_mul<true>(rx, rxc, rx, rxc), ch_mul<true>(ry, ryc, ry, ryc)), l1, l2);
       // dist = |center - p|
       const Ch3 c0 = ch_at(sm + 12 * C, o), c1 = ch_at(sm + 13 * C, o), c2 = ch_at(sm + 14 * C, o);
       const Ch3 distc =
-          ch_lift(ch_add(ch_mul(dx, c0, dx, c0), ch_add(ch_mul(dy, c1, dy, c1), ch_mul(dz, c2, dz, c2))), s1, s2);
-      const Ch3 psic = ch_scale(ch_sub(smp, ch_div(dist, distc, lam, lamc, ilam, ilam2)), imu);
+          ch_lift<true>(ch_add(ch_mul<true>(dx, c0, dx, c0), ch_add(ch_mul<true>(dy, c1, dy, c1), ch_mul<true>(dz, c2, dz, c2))), s1, s2);
+      const Ch3 psic = ch_scale(ch_sub(smp, ch_div<true>(dist, distc, lam, lamc, ilam, ilam2)), imu);
       double* f3 = fim + 3 * pr;
-      f3[0] = (wt * f3[0] + psic.a) * inv_w1;
-      f3[1] = (wt * f3[1] + psic.b) * inv_w1;
-      f3[2] = (wt * f3[2] + psic.ab) * inv_w1;
+      f3[0] = fma(wt, f3[0], psic.a) * inv_w1;
+      f3[1] = fma(wt, f3[1], psic.b) * inv_w1;
+      f3[2] = fma(wt, f3[2], psic.ab) * inv_w1;
     }
   }
   const double wn = wt + 1.0;
