@@ -14,3 +14,5 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/fp64_peak.cu -o tools/_bu
   tools/_build/fp64_peak > gpurun_out/final/fp64_peak.json; echo fp64=$?
 bash tools/ncu_capture.sh
 python tools/ncu_traffic.py config2 r02 > gpurun_out/final/traffic.log 2>&1; echo traffic=$?
+bash tools/ncu_c3_o2.sh
+python tools/ncu_traffic.py config3 r02 > gpurun_out/final/traffic_c3.log 2>&1; echo traffic_c3=$?

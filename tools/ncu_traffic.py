@@ -23,9 +23,12 @@ def to_bytes(v, unit):
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
 
 
+CATS_C3 = {"c3_integrate": "integrate", "c3_lift2": "raycast_lift"}  # tools/ncu_c3_o2.sh
+
+
 def main(workload="config2", rnd="r01"):
     out = {}
-    for kern, cat in CATS.items():
+    for kern, cat in (CATS_C3 if workload == "config3" else CATS).items():
         rep = ROOT / "gpurun_out" / f"prof_{kern}.ncu-rep"
         if not rep.exists():
             continue
