@@ -1331,6 +1331,19 @@ __global__ void k_objective(const double* __restrict__ traj, const double* __res
 // ============================================================================
 constexpr int kR2Warps = 8;
 constexpr int kR2Threads = 32 * kR2Warps;
+constexpr int kR2RowStride = 7 * 4 + 1;  // doubles per correspondence row record (odd: conflict-free)
+template <typename S> CSF_DEV void put_row(double* row, int i, const S& v) {
+  row[4 * i] = v.re;
+#pragma unroll
+  for (int g = 0; g < 3; ++g) row[4 * i + 1 + g] = v.im[g];
+}
+template <typename S> CSF_DEV S get_row(const double* row, int i) {
+  S v;
+  v.re = row[4 * i];
+#pragma unroll
+  for (int g = 0; g < 3; ++g) v.im[g] = row[4 * i + 1 + g];
+  return v;
+}
 constexpr int kR2Pairs = 5;  // pairs per CTA: one association serves them
 
 template <typename S>
@@ -1352,8 +1365,11 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
   const int C = 1 + Dp;
   const int n_pairs = Dp / G;
   extern __shared__ double sm[];
-  S* rows = reinterpret_cast<S*>(sm);                                  // [kR2Threads][7]
-  int* s_corr = reinterpret_cast<int*>(rows + kR2Threads * 7);         // [tile_slots][4]: x, y, u, v
+  // rows [kR2Threads][kR2RowStride] doubles: a correspondence's 7 row entries
+  // (S = 4 doubles each) plus one pad double, so the odd stride puts the 32
+  // lanes' 8-byte accesses on distinct bank pairs (stride 28: 4-way conflicts)
+  double* rows = sm;
+  int* s_corr = reinterpret_cast<int*>(rows + kR2Threads * kR2RowStride);  // [tile_slots][4]: x, y, u, v
   __shared__ int s_wsum[kR2Warps];
   Pose<double> c2w, w2p;
   load_pose_real(pose, C, &c2w);
@@ -1441,10 +1457,10 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
         const V3<S> pw = apply(base, vert);
         const S r = dot3(sub3(pw, mv), mn);
         const V3<S> pn = cross3(pw, mn);
-        S* row = rows + 7 * threadIdx.x;
-        row[0] = mn.v[0]; row[1] = mn.v[1]; row[2] = mn.v[2];
-        row[3] = pn.v[0]; row[4] = pn.v[1]; row[5] = pn.v[2];
-        row[6] = r;
+        double* row = rows + kR2RowStride * threadIdx.x;
+        put_row(row, 0, mn.v[0]); put_row(row, 1, mn.v[1]); put_row(row, 2, mn.v[2]);
+        put_row(row, 3, pn.v[0]); put_row(row, 4, pn.v[1]); put_row(row, 5, pn.v[2]);
+        put_row(row, 6, r);
       }
       __syncthreads();
       // accumulate_row (orc_icp.hpp): lane l adds, in entry order, the S
@@ -1455,7 +1471,9 @@ __global__ void __launch_bounds__(kR2Threads) k_icp_reduce2(const TrackState* st
 #pragma unroll
         for (int i = 0; i < kQ; ++i) {
           const int q = warp + kR2Warps * i;
-          if (q < 27) acc[i] = acc[i] + rows[7 * k + acc_row_a(q)] * rows[7 * k + acc_row_b(q)];
+          if (q < 27)
+            acc[i] = acc[i] + get_row<S>(rows + kR2RowStride * k, acc_row_a(q)) *
+                                  get_row<S>(rows + kR2RowStride * k, acc_row_b(q));
         }
       }
     }
@@ -1830,7 +1848,7 @@ void launch_icp_iteration2(const Launch& L, int Dp, TrackState* st, const double
   const int pairs = Dp / 3;
   const long long n_slots = static_cast<long long>((w + stride - 1) / stride) * ((h + stride - 1) / stride);
   const int tile_slots = icp_tile_slots(n_slots);
-  const size_t smem = sizeof(S) * kR2Threads * 7 + sizeof(int) * 4 * static_cast<size_t>(tile_slots);
+  const size_t smem = sizeof(double) * kR2Threads * kR2RowStride + sizeof(int) * 4 * static_cast<size_t>(tile_slots);
   launch_pdl(k_icp_reduce2<S>, dim3(tiles, (pairs + kR2Pairs - 1) / kR2Pairs), dim3(kR2Threads), smem, L.stream, st,
              depth, w, h, stride, intr,
              pose, vre, nre, vim, nim, d_max, cos_max, Dp, tile_slots, partials, counts);
