@@ -1376,8 +1376,11 @@ struct LiftRec {
   double rn, a0, a1, astar, num, den, ln;
   int vid[8][8];
   int ok;
-  int pad_;
+  int pad_[3];  // odd record size in doubles (149): the channel pass's lanes
+                // read ~6 pixels' records at one field offset; the even size
+                // 148 put pixels p and p + 4 on one bank pair
 };
+static_assert(sizeof(LiftRec) % 16 == 8, "LiftRec: odd size in doubles");
 constexpr int kLiftPix = 32;  // max pixels per block (8 lanes each in the real pass)
 // pixels per block: as many as keep the channel pass to one round of items
 // (items = channel-pass items per pixel)
