@@ -1616,9 +1616,13 @@ __global__ void __launch_bounds__(256, CSF_LIFT_MINB) k_raycast_lift_coop(V vol,
 // per (pixel, pair) evaluates the lifted epilogue of raycast<S> (tsdf.hpp:
 // 255-284) in Bicomplex arithmetic with those corners (no block lookups, no
 // (F, W) loads): sample_tsdf<S> / sample_gradient<S>'s operations.
+// Per-sample rows at odd strides (9, 3, 13) and a record size of 8 mod 16
+// doubles: the real pass's 32 lanes (4 pixels x 8 samples) store one field
+// offset together, and these strides put each half-warp on distinct bank
+// pairs (the 8-double rows gave 8-way conflicts).
 struct LiftRec2 {
-  double F[8][8];  // corner real fields per sample
-  int vid[8][8];   // corner voxel ids per sample
+  double F[8][9];  // corner real fields per sample
+  int vid[8][9];   // corner voxel ids per sample
   int ok;
   int pad_;
 #ifndef CSF_EXACT_CHANNELS
@@ -1626,14 +1630,18 @@ struct LiftRec2 {
   // second derivatives d2S/df_a df_b (E: xy, xz, yz) and the weight products
   // of the edge differences (wp: 4 x wy wz, 4 x wx wz, 4 x wx wy); per pixel
   // the real intermediates of the epilogue
-  double wgt[8][8];
+  double wgt[8][9];
   double ds[8][3];
   double E[8][3];
-  double wp[8][12];
+  double wp[8][13];
   double dc[2], rn, a0, a1, f0, f1, num, den, astar, ln;
   double dn[3], dir[3], grad[3];
+  double pad2_[7];
 #endif
 };
+#ifndef CSF_EXACT_CHANNELS
+static_assert(sizeof(LiftRec2) % 128 == 64, "LiftRec2: 8 mod 16 doubles");
+#endif
 
 // sample_tsdf<S> (order-2 branch) with the corners known and valid.
 template <typename S, typename V>
