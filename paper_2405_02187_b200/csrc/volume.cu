@@ -1368,17 +1368,19 @@ CSF_DEV void sample_channels(const VoxelStore& vox, const int* vid, const double
 // truncated-Complex rule of every operation (csfd.hpp:44-58) applied to the
 // saved real intermediates.  Many light threads keep far more voxel-channel gathers
 // in flight than one heavy thread per (pixel, group).
+// Per-sample rows of 9 (the real pass's 4 pixels x 8 samples per warp store
+// one field offset together: rows of 8 gave 4-way bank conflicts) and an odd
+// record size in doubles (161: the channel pass's lanes read ~6 pixels'
+// records at one field offset; an even size put pixels p, p + 4 on one bank pair).
 struct LiftRec {
-  double wgt[8][8];
+  double wgt[8][9];
   double ds[8][3];
   double f[8];
   double dc[3], dn[3], dir[3], grad[3];
   double rn, a0, a1, astar, num, den, ln;
-  int vid[8][8];
+  int vid[8][9];
   int ok;
-  int pad_[3];  // odd record size in doubles (149): the channel pass's lanes
-                // read ~6 pixels' records at one field offset; the even size
-                // 148 put pixels p and p + 4 on one bank pair
+  int pad_[3];
 };
 static_assert(sizeof(LiftRec) % 16 == 8, "LiftRec: odd size in doubles");
 constexpr int kLiftPix = 32;  // max pixels per block (8 lanes each in the real pass)
